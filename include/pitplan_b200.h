@@ -1,0 +1,181 @@
+/*
+ * pitplan_b200.h -- C ABI of the B200-native move-evaluation engine.
+ *
+ * The reference (`pitplan`, pure Python) has no FFI: its plug-in point for this
+ * path is the Python function
+ *     pitplan.evaluate.evaluate_candidates_parallel   (pkg/src/pitplan/evaluate.py:306-318)
+ * plus the feasibility / repair helpers it and its callers use:
+ *     pitplan.evaluate.check_feasible                 (evaluate.py:82-105)
+ *     pitplan.hybrid._precedence_repair_pass          (hybrid.py:493-510)
+ *     pitplan.hybrid.lns_repair (unmine fixpoint)     (hybrid.py:199-211)
+ * The Python shim `paper_2511_18296_b200.evaluate` keeps those signatures and
+ * binds this library with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every entry point returns an int status: 0 ok, PP_ERR_* otherwise; the
+ *     message of the last failure on the calling thread is pp_last_error().
+ *   - no C++ exception, abort or silent CPU fallback crosses this boundary.
+ *   - `mem` selects the address space of the caller's array arguments:
+ *       PP_MEM_HOST   host pointers (pageable or pp_host_alloc'd); the call copies
+ *                     in, runs, copies out and returns after the stream drains.
+ *       PP_MEM_DEVICE device pointers (e.g. torch tensor data_ptr()); the call only
+ *                     enqueues work on `stream` (NULL = the context's own stream).
+ *     Instance / scenario uploads (pp_set_instance ...) always take host pointers.
+ *   - UNMINED = -1 is the "not scheduled" period, as blockmodel.py:18.
+ *   - all floating point is IEEE binary64 with the reference's operation order; the
+ *     kernels are compiled without FMA contraction so results are bit-identical to
+ *     the reference CPU evaluator.
+ *   - a context is not thread-safe; use one context per host thread.
+ */
+#ifndef PITPLAN_B200_H
+#define PITPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_ABI_VERSION 1
+
+/* status codes (mapped to pitplan.errors classes by the Python shim) */
+#define PP_OK 0
+#define PP_ERR_INVALID_ARGS 1   /* -> InvalidArgs   (errors.py:16)  */
+#define PP_ERR_SHAPE 2          /* -> ShapeMismatch (errors.py:24)  */
+#define PP_ERR_CUDA 3           /* -> DeviceError                   */
+#define PP_ERR_VALIDATION 4     /* -> ValidationError (errors.py:12) e.g. a cycle */
+#define PP_ERR_STATE 5          /* call order: instance/scenarios/schedule missing */
+
+#define PP_MEM_HOST 0
+#define PP_MEM_DEVICE 1
+
+/* evaluation flags (evaluate_candidates_parallel keyword arguments, evaluate.py:306-318) */
+#define PP_NET_MINING_COST 1u   /* net_mining_cost=True: value -= disc[t] * cost[b][t] */
+#define PP_LITERAL_VALUE 2u     /* literal_kernel_value=True: unit = mass * 100 */
+#define PP_USE_SIGMA 4u         /* sigma is not None: sig_row from the uploaded sigma[S][T] */
+
+#define PP_SCENARIO_EXPECTED (-1) /* s=None: scenario-mean unit values and sigma row */
+
+#define PP_MOVE_REASSIGN 0      /* move (b, t_new): t_new in [-1, T) */
+#define PP_MOVE_SWAP 1          /* move (b1, b2): exchange their periods */
+
+#define PP_REPAIR_PUSH_FORWARD 0 /* _precedence_repair_pass (hybrid.py:493-510) */
+#define PP_REPAIR_UNMINE 1       /* lns_repair unmine fixpoint (hybrid.py:199-211) */
+
+#if defined(__GNUC__)
+#define PP_API __attribute__((visibility("default")))
+#else
+#define PP_API
+#endif
+
+typedef struct pp_ctx pp_ctx;
+
+/* Selected move.  For candidate evaluation: value = improvement, block / period of the
+ * move, block = -1 when no candidate is feasible (best is None, evaluate.py:411-421).
+ * For explicit moves: value = delta, block = move index (-1 if none), period = -1. */
+typedef struct pp_best {
+    double value;
+    int32_t block;
+    int32_t period;
+} pp_best;
+
+/* Outputs of pp_eval_candidates; NULL members are not computed / written.
+ * best_t, best_val, feasible and global are required. */
+typedef struct pp_cand_out {
+    int32_t *best_t;     /* [C] best period or -1                    (CandidateMove.period)      */
+    double *best_val;    /* [C] improvement or -inf                  (CandidateMove.improvement) */
+    uint8_t *feasible;   /* [C]                                      (CandidateMove.feasible)    */
+    double *trace_val;   /* [C*T] per-(candidate, period) value, -inf if infeasible (trace CSV)  */
+    uint8_t *trace_feas; /* [C*T] per-(candidate, period) feasibility                             */
+    double *exp_delta;   /* [C*T] expected delta over scenarios (np.mean of per-scenario deltas)  */
+    double *cvar;        /* [C*T] CVaR10 of the per-scenario deltas (saa.py:150-166 semantics)    */
+    float *scen_delta;   /* [C*S*T] per-scenario delta, layout [candidate][scenario][period]      */
+    pp_best *global;     /* [1] overall best move (evaluate.py:404-421 order)                     */
+} pp_cand_out;
+
+/* Outputs of pp_eval_moves; NULL members are not computed / written.
+ * feasible, delta and global are required. */
+typedef struct pp_move_out {
+    uint8_t *feasible;  /* [M] */
+    double *delta;      /* [M] kernel-value delta (parity key), -inf if infeasible */
+    double *exp_delta;  /* [M] */
+    double *cvar;       /* [M] */
+    float *scen_delta;  /* [M*S] layout [move][scenario] */
+    pp_best *global;    /* [1] value = best delta, block = move index (lowest on ties) */
+} pp_move_out;
+
+/* ---- library / context --------------------------------------------------------- */
+PP_API int pp_abi_version(void);
+PP_API const char *pp_last_error(void);
+PP_API int pp_device_count(int *count);
+PP_API int pp_ctx_create(int device, pp_ctx **out);
+PP_API int pp_ctx_destroy(pp_ctx *ctx);
+PP_API int pp_ctx_stream(pp_ctx *ctx, void **stream);          /* the context's cudaStream_t */
+PP_API int pp_synchronize(pp_ctx *ctx, void *stream);
+PP_API int pp_host_alloc(size_t bytes, void **ptr);             /* pinned host memory */
+PP_API int pp_host_free(void *ptr);
+
+/* ---- static tables (host pointers) ------------------------------------------------
+ * Instance: precedence edge list in reference order (blockmodel.py:94, 180-184),
+ * masses (blockmodel.py:128), undiscounted mining cost [B][T] (blockmodel.py:137),
+ * capacity [T], discount table disc[t] = (1+r)^-t computed by the host (evaluate.py:341).
+ * Builds CSR adjacency and topological levels on the device side; PP_ERR_VALIDATION
+ * on a cycle (blockmodel.py:228-245). */
+PP_API int pp_set_instance(pp_ctx *ctx, int32_t n_blocks, int32_t n_periods, int64_t n_edges,
+                    const int32_t *edge_i, const int32_t *edge_j, const double *mass,
+                    const double *cost, const double *capacity, const double *discount);
+/* spatial[b] = geological_consistency(features_b, params, diameter) (uncertainty.py:185-191,
+ * evaluate.py:342-347), computed on the device. */
+PP_API int pp_set_geology(pp_ctx *ctx, const double *alteration, const double *structural,
+                   const double *dist_intrusion, double w1, double w2, double w3,
+                   double diameter);
+/* Scenario tables: vmax[S][B] = max over modes of v[s][b][o] (evaluate.py:108-124) in the
+ * reference layout (transposed to block-major on the device), sigma[S][T] or NULL
+ * (uncertainty.py:276-321).  Derives unit_mean[b] (evaluate.py:302) and the scenario-mean
+ * sigma row (evaluate.py:351) on the device. */
+PP_API int pp_set_scenarios(pp_ctx *ctx, int32_t n_scenarios, const double *vmax_sb,
+                     const double *sigma_st);
+
+/* ---- schedule -------------------------------------------------------------------- */
+/* Upload assign[B] and recompute period_mass[t] = masses[assign == t].sum() bit-exactly
+ * (numpy pairwise summation, evaluate.py:334-337). */
+PP_API int pp_set_schedule(pp_ctx *ctx, const int32_t *assign, int32_t mem, void *stream);
+/* Apply accepted deltas assign[blocks[k]] = periods[k] and recompute period_mass. */
+PP_API int pp_apply_moves(pp_ctx *ctx, const int32_t *blocks, const int32_t *periods, int32_t n,
+                   int32_t mem, void *stream);
+PP_API int pp_get_schedule(pp_ctx *ctx, int32_t *assign_out, double *period_mass_out, int32_t mem,
+                    void *stream);
+
+/* ---- hot path ---------------------------------------------------------------------- */
+/* evaluate_candidates_parallel (evaluate.py:306-430) against the current schedule.
+ * scenario: PP_SCENARIO_EXPECTED (s=None) or k in [0, S) (s=k).  Candidates may repeat;
+ * results are in input order and independent of any launch geometry. */
+PP_API int pp_eval_candidates(pp_ctx *ctx, const int32_t *cand, int32_t n_cand, int32_t scenario,
+                       uint32_t flags, const pp_cand_out *out, int32_t mem, void *stream);
+/* Explicit moves against the current schedule: kind PP_MOVE_REASSIGN with (a=block,
+ * b=t_new) or PP_MOVE_SWAP with (a=b1, b=b2); feasibility rules of hybrid.py:348-403. */
+PP_API int pp_eval_moves(pp_ctx *ctx, int32_t kind, const int32_t *a, const int32_t *b, int32_t n_moves,
+                  int32_t scenario, uint32_t flags, const pp_move_out *out, int32_t mem,
+                  void *stream);
+/* check_feasible (evaluate.py:82-105) for P schedules assign[P][B]. */
+PP_API int pp_check_feasible(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, int64_t *pred_count,
+                      double *excess, double *violation, double *period_mass, int32_t mem,
+                      void *stream);
+/* Batched repair of P schedules in place, in topological waves:
+ * PP_REPAIR_PUSH_FORWARD = _precedence_repair_pass, PP_REPAIR_UNMINE = the unmine fixpoint
+ * (unmined_out[P][B] = 1 where the fixpoint unmined a block; may be NULL). */
+PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode, uint8_t *unmined_out,
+              int32_t mem, void *stream);
+/* Ordered reduction of n pp_best records (e.g. one per GPU after an all-gather) with the
+ * selection order of evaluate.py:404-409; records with block < 0 are "none".  This is the
+ * deterministic "allreduce-argmax" step of multi-GPU evaluation. */
+PP_API int pp_reduce_best(pp_ctx *ctx, const pp_best *records, int32_t n, pp_best *out, int32_t mem,
+                          void *stream);
+/* Topological level of every block (longest predecessor chain), host output. */
+PP_API int pp_get_levels(pp_ctx *ctx, int32_t *n_levels, int32_t *level_of_block);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PITPLAN_B200_H */

@@ -1,0 +1,142 @@
+"""ctypes binding of the C ABI in include/pitplan_b200.h.
+
+The compiled library lives next to this file (built in-tree by
+`__graft_entry__.build()`); there is no CPU fallback: if it cannot be loaded every
+entry point raises `ExtensionMissing`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ExtensionMissing, raise_for_status
+
+LIB_NAME = "libpitplan_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+PP_MEM_HOST = 0
+PP_MEM_DEVICE = 1
+PP_NET_MINING_COST = 1
+PP_LITERAL_VALUE = 2
+PP_USE_SIGMA = 4
+PP_SCENARIO_EXPECTED = -1
+PP_MOVE_REASSIGN = 0
+PP_MOVE_SWAP = 1
+PP_REPAIR_PUSH_FORWARD = 0
+PP_REPAIR_UNMINE = 1
+
+c_void_p = ctypes.c_void_p
+c_int32 = ctypes.c_int32
+c_int64 = ctypes.c_int64
+c_uint32 = ctypes.c_uint32
+c_double = ctypes.c_double
+c_size_t = ctypes.c_size_t
+
+
+class PPBest(ctypes.Structure):
+    _fields_ = [("value", c_double), ("block", c_int32), ("period", c_int32)]
+
+
+class PPCandOut(ctypes.Structure):
+    _fields_ = [
+        ("best_t", c_void_p),
+        ("best_val", c_void_p),
+        ("feasible", c_void_p),
+        ("trace_val", c_void_p),
+        ("trace_feas", c_void_p),
+        ("exp_delta", c_void_p),
+        ("cvar", c_void_p),
+        ("scen_delta", c_void_p),
+        ("global_", c_void_p),
+    ]
+
+
+class PPMoveOut(ctypes.Structure):
+    _fields_ = [
+        ("feasible", c_void_p),
+        ("delta", c_void_p),
+        ("exp_delta", c_void_p),
+        ("cvar", c_void_p),
+        ("scen_delta", c_void_p),
+        ("global_", c_void_p),
+    ]
+
+
+# name -> (restype, argtypes); every entry point of include/pitplan_b200.h
+SIGNATURES = {
+    "pp_abi_version": (c_int32, []),
+    "pp_last_error": (ctypes.c_char_p, []),
+    "pp_device_count": (c_int32, [ctypes.POINTER(ctypes.c_int)]),
+    "pp_ctx_create": (c_int32, [ctypes.c_int, ctypes.POINTER(c_void_p)]),
+    "pp_ctx_destroy": (c_int32, [c_void_p]),
+    "pp_ctx_stream": (c_int32, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "pp_synchronize": (c_int32, [c_void_p, c_void_p]),
+    "pp_host_alloc": (c_int32, [c_size_t, ctypes.POINTER(c_void_p)]),
+    "pp_host_free": (c_int32, [c_void_p]),
+    "pp_set_instance": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "pp_set_geology": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
+                                 c_double]),
+    "pp_set_scenarios": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    "pp_set_schedule": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    "pp_apply_moves": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
+    "pp_get_schedule": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+    "pp_eval_candidates": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_uint32,
+                                     ctypes.POINTER(PPCandOut), c_int32, c_void_p]),
+    "pp_eval_moves": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32, c_uint32,
+                                ctypes.POINTER(PPMoveOut), c_int32, c_void_p]),
+    "pp_check_feasible": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_int32, c_void_p]),
+    "pp_repair": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
+    "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
+    "pp_get_levels": (c_int32, [c_void_p, ctypes.POINTER(c_int32), c_void_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and return the ctypes handle; raises ExtensionMissing."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise ExtensionMissing(
+                f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback for the sm_100a engine)"
+            )
+        try:
+            handle = ctypes.CDLL(p)
+        except OSError as exc:  # pragma: no cover
+            raise ExtensionMissing(f"cannot load {p}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = handle
+        return handle
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().pp_last_error()
+        raise_for_status(rc, msg.decode() if msg else "")
+
+
+def ptr(a) -> int | None:
+    """Raw address of a numpy array / torch tensor / int / None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if hasattr(a, "ctypes"):
+        return a.ctypes.data
+    raise TypeError(f"cannot take the address of {type(a)!r}")

@@ -1,0 +1,312 @@
+"""`Engine`: one device context holding an instance, a scenario set and the current
+schedule, exposing the hot path with host (numpy) or device (torch) buffers.
+
+Host-buffer calls are synchronous and are what the drop-in `evaluate_candidates_parallel`
+uses; device-buffer calls (`*_device`) only enqueue work on a CUDA stream and are what
+the benchmark times with inputs resident in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import PPBest, PPCandOut, PPMoveOut, check, ptr
+from .errors import InvalidArgs, ShapeMismatch
+from .model import BlockModel, ScenarioTables, cvar_k
+
+DEFAULT_PSI_WEIGHTS = (0.4, 0.35, 0.25)  # UncertaintyParams.psi_weights (uncertainty.py:147)
+
+
+class PinnedPool:
+    """Page-locked host arrays (pp_host_alloc) for host<->device copies that DMA directly."""
+
+    def __init__(self):
+        self.lib = _lib.load()
+        self._ptrs = []
+
+    def empty(self, shape, dtype) -> np.ndarray:
+        dt = np.dtype(dtype)
+        n = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+        p = ctypes.c_void_p()
+        check(self.lib.pp_host_alloc(max(n * dt.itemsize, 1), ctypes.byref(p)))
+        self._ptrs.append(p.value)
+        buf = (ctypes.c_char * max(n * dt.itemsize, 1)).from_address(p.value)
+        return np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
+
+    def close(self):
+        while self._ptrs:
+            self.lib.pp_host_free(self._ptrs.pop())
+
+
+def _i32(a, n=None, name="array") -> np.ndarray:
+    out = np.ascontiguousarray(np.asarray(a), dtype=np.int32)
+    if n is not None and out.size != n:
+        raise ShapeMismatch(f"{name} has {out.size} entries, expected {n}")
+    return out
+
+
+class Engine:
+    """A pitplan_b200 context on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = ctypes.c_void_p()
+        check(self.lib.pp_ctx_create(int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = int(device)
+        self.bm: BlockModel | None = None
+        self.n_scenarios = 0
+        self.has_sigma = False
+        self._keep = []
+
+    # -- lifecycle -----------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.pp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(self.lib.pp_ctx_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def synchronize(self, stream=None):
+        check(self.lib.pp_synchronize(self._h, stream))
+
+    # -- static tables ---------------------------------------------------------------
+    def set_instance(self, bm: BlockModel):
+        B, T = bm.n_blocks, bm.n_periods
+        disc = np.ascontiguousarray(bm.discount())
+        check(self.lib.pp_set_instance(
+            self._h, B, T, bm.n_edges, ptr(bm.edges_i), ptr(bm.edges_j), ptr(bm.mass),
+            ptr(np.ascontiguousarray(bm.cost)), ptr(bm.capacity), ptr(disc)))
+        self.bm = bm
+        self.n_scenarios = 0
+
+    def set_geology(self, psi_weights=DEFAULT_PSI_WEIGHTS, diameter: float | None = None):
+        bm = self._need_bm()
+        w1, w2, w3 = (float(w) for w in psi_weights)
+        diam = bm.diameter() if diameter is None else float(diameter)
+        check(self.lib.pp_set_geology(self._h, ptr(bm.alteration), ptr(bm.structural),
+                                      ptr(bm.dist_intrusion), w1, w2, w3, diam))
+
+    def set_scenarios(self, tables: ScenarioTables):
+        bm = self._need_bm()
+        vmax = np.ascontiguousarray(tables.vmax, dtype=np.float64)
+        if vmax.ndim != 2 or vmax.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("scenario value table does not match the instance")
+        sig = None
+        if tables.sigma is not None:
+            sig = np.ascontiguousarray(tables.sigma, dtype=np.float64)
+            if sig.shape != (vmax.shape[0], bm.n_periods):
+                raise ShapeMismatch("sigma must be [S][T]")
+        check(self.lib.pp_set_scenarios(self._h, vmax.shape[0], ptr(vmax), ptr(sig)))
+        self.n_scenarios = int(vmax.shape[0])
+        self.has_sigma = sig is not None
+
+    def _need_bm(self) -> BlockModel:
+        if self.bm is None:
+            raise InvalidArgs("set_instance first")
+        return self.bm
+
+    # -- schedule --------------------------------------------------------------------
+    def set_schedule(self, assign):
+        """Host numpy array or a device int32 torch tensor."""
+        bm = self._need_bm()
+        if hasattr(assign, "data_ptr"):
+            check(self.lib.pp_set_schedule(self._h, assign.data_ptr(), _lib.PP_MEM_DEVICE, None))
+            return
+        a = _i32(assign, bm.n_blocks, "assignment")
+        if a.size and (a.min() < -1 or a.max() >= bm.n_periods):
+            raise InvalidArgs("schedule has period indices out of range")
+        check(self.lib.pp_set_schedule(self._h, ptr(a), _lib.PP_MEM_HOST, None))
+
+    def set_schedule_device(self, assign_tensor, stream=None):
+        check(self.lib.pp_set_schedule(self._h, assign_tensor.data_ptr(), _lib.PP_MEM_DEVICE, stream))
+
+    def apply_moves(self, blocks, periods):
+        b = _i32(blocks)
+        t = _i32(periods, b.size, "periods")
+        check(self.lib.pp_apply_moves(self._h, ptr(b), ptr(t), b.size, _lib.PP_MEM_HOST, None))
+
+    def get_schedule(self):
+        bm = self._need_bm()
+        a = np.empty(bm.n_blocks, dtype=np.int32)
+        pm = np.empty(bm.n_periods, dtype=np.float64)
+        check(self.lib.pp_get_schedule(self._h, ptr(a), ptr(pm), _lib.PP_MEM_HOST, None))
+        return a, pm
+
+    # -- evaluation --------------------------------------------------------------------
+    @staticmethod
+    def flags(net=False, literal=False, use_sigma=True) -> int:
+        f = 0
+        if net:
+            f |= _lib.PP_NET_MINING_COST
+        if literal:
+            f |= _lib.PP_LITERAL_VALUE
+        if use_sigma:
+            f |= _lib.PP_USE_SIGMA
+        return f
+
+    def eval_candidates(self, cand, scenario=None, *, net=False, literal=False, use_sigma=True,
+                        trace=False, stats=False, scen=False, out: dict | None = None,
+                        validate: bool = True) -> dict:
+        """Host-buffer evaluation; returns numpy arrays (and `best` as a tuple or None).
+        `out` may supply preallocated (e.g. pinned) host arrays for any output."""
+        bm = self._need_bm()
+        c = cand if (not validate and isinstance(cand, np.ndarray) and cand.dtype == np.int32) else _i32(cand)
+        C, T, S = c.size, bm.n_periods, self.n_scenarios
+        if validate and C and (c.min() < 0 or c.max() >= bm.n_blocks):
+            raise InvalidArgs("candidate block out of range")
+        out = out or {}
+        res = {
+            "best_t": out.get("best_t", None) if "best_t" in out else np.empty(C, np.int32),
+            "best_val": out["best_val"] if "best_val" in out else np.empty(C, np.float64),
+            "feasible": out["feasible"] if "feasible" in out else np.empty(C, np.uint8),
+        }
+        if trace:
+            res["trace_val"] = out.get("trace_val", None) if "trace_val" in out else np.empty((C, T), np.float64)
+            res["trace_feas"] = out["trace_feas"] if "trace_feas" in out else np.empty((C, T), np.uint8)
+        if stats:
+            res["exp_delta"] = out["exp_delta"] if "exp_delta" in out else np.empty((C, T), np.float64)
+            res["cvar"] = out["cvar"] if "cvar" in out else np.empty((C, T), np.float64)
+        if scen:
+            res["scen_delta"] = out["scen_delta"] if "scen_delta" in out else np.empty((C, S, T), np.float32)
+        g = PPBest()
+        out = PPCandOut(
+            ptr(res["best_t"]), ptr(res["best_val"]), ptr(res["feasible"]),
+            ptr(res.get("trace_val")), ptr(res.get("trace_feas")), ptr(res.get("exp_delta")),
+            ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g))
+        sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
+        check(self.lib.pp_eval_candidates(self._h, ptr(c), C, sc, self.flags(net, literal, use_sigma),
+                                          ctypes.byref(out), _lib.PP_MEM_HOST, None))
+        res["best"] = None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
+        return res
+
+    def eval_candidates_device(self, cand, out: dict, scenario=None, *, net=False, literal=False,
+                               use_sigma=True, stream=None):
+        """Device-buffer evaluation: `cand` an int32 CUDA tensor, `out` a dict of CUDA
+        tensors (best_t, best_val, feasible, global [16-byte], optional trace_val,
+        trace_feas, exp_delta, cvar, scen_delta).  Enqueues on `stream`."""
+        o = PPCandOut(
+            ptr(out["best_t"]), ptr(out["best_val"]), ptr(out["feasible"]),
+            ptr(out.get("trace_val")), ptr(out.get("trace_feas")), ptr(out.get("exp_delta")),
+            ptr(out.get("cvar")), ptr(out.get("scen_delta")), ptr(out["global"]))
+        sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
+        check(self.lib.pp_eval_candidates(self._h, ptr(cand), int(cand.numel()), sc,
+                                          self.flags(net, literal, use_sigma), ctypes.byref(o),
+                                          _lib.PP_MEM_DEVICE, stream))
+
+    def eval_moves(self, a, b, kind="reassign", scenario=None, *, net=False, literal=False,
+                   use_sigma=True, stats=False, scen=False) -> dict:
+        bm = self._need_bm()
+        av = _i32(a)
+        bv = _i32(b, av.size, "move arrays")
+        M, S = av.size, self.n_scenarios
+        k = _lib.PP_MOVE_SWAP if kind == "swap" else _lib.PP_MOVE_REASSIGN
+        res = {"feasible": np.empty(M, np.uint8), "delta": np.empty(M, np.float64)}
+        if stats:
+            res["exp_delta"] = np.empty(M, np.float64)
+            res["cvar"] = np.empty(M, np.float64)
+        if scen:
+            res["scen_delta"] = np.empty((M, S), np.float32)
+        g = PPBest()
+        out = PPMoveOut(ptr(res["feasible"]), ptr(res["delta"]), ptr(res.get("exp_delta")),
+                        ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g))
+        sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
+        check(self.lib.pp_eval_moves(self._h, k, ptr(av), ptr(bv), M, sc,
+                                     self.flags(net, literal, use_sigma), ctypes.byref(out),
+                                     _lib.PP_MEM_HOST, None))
+        del bm
+        res["best"] = None if g.block < 0 else (int(g.block), float(g.value))
+        return res
+
+    def eval_moves_device(self, a, b, out: dict, kind="reassign", scenario=None, *, net=False,
+                          literal=False, use_sigma=True, stream=None):
+        k = _lib.PP_MOVE_SWAP if kind == "swap" else _lib.PP_MOVE_REASSIGN
+        o = PPMoveOut(ptr(out["feasible"]), ptr(out["delta"]), ptr(out.get("exp_delta")),
+                      ptr(out.get("cvar")), ptr(out.get("scen_delta")), ptr(out["global"]))
+        sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
+        check(self.lib.pp_eval_moves(self._h, k, ptr(a), ptr(b), int(a.numel()), sc,
+                                     self.flags(net, literal, use_sigma), ctypes.byref(o),
+                                     _lib.PP_MEM_DEVICE, stream))
+
+    def check_feasible(self, assign_batch) -> dict:
+        bm = self._need_bm()
+        a = np.ascontiguousarray(np.atleast_2d(np.asarray(assign_batch)), dtype=np.int32)
+        if a.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("schedule length does not match the instance")
+        P = a.shape[0]
+        res = {
+            "pred_count": np.empty(P, np.int64),
+            "excess": np.empty(P, np.float64),
+            "violation": np.empty(P, np.float64),
+            "period_mass": np.empty((P, bm.n_periods), np.float64),
+        }
+        check(self.lib.pp_check_feasible(self._h, ptr(a), P, ptr(res["pred_count"]), ptr(res["excess"]),
+                                         ptr(res["violation"]), ptr(res["period_mass"]),
+                                         _lib.PP_MEM_HOST, None))
+        return res
+
+    def repair(self, assign_batch, mode="push", unmined=False):
+        """Returns (repaired int32 [P][B], unmined flags [P][B] or None)."""
+        bm = self._need_bm()
+        a = np.array(np.atleast_2d(np.asarray(assign_batch)), dtype=np.int32, order="C")
+        if a.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("schedule length does not match the instance")
+        m = _lib.PP_REPAIR_UNMINE if mode == "unmine" else _lib.PP_REPAIR_PUSH_FORWARD
+        u = np.empty(a.shape, np.uint8) if unmined else None
+        check(self.lib.pp_repair(self._h, ptr(a), a.shape[0], m, ptr(u), _lib.PP_MEM_HOST, None))
+        return a, u
+
+    def reduce_best_device(self, records, out, stream=None):
+        """Ordered argmax over n 16-byte pp_best records (device tensors)."""
+        n = records.numel() * records.element_size() // 16
+        check(self.lib.pp_reduce_best(self._h, ptr(records), int(n), ptr(out), _lib.PP_MEM_DEVICE, stream))
+
+    def reduce_best(self, recs):
+        """Host version: recs = list of (value, block, period) with block < 0 meaning none."""
+        arr = (PPBest * max(len(recs), 1))()
+        for i, (v, b, t) in enumerate(recs):
+            arr[i].value, arr[i].block, arr[i].period = float(v), int(b), int(t)
+        g = PPBest()
+        check(self.lib.pp_reduce_best(self._h, ctypes.addressof(arr), len(recs), ctypes.addressof(g),
+                                      _lib.PP_MEM_HOST, None))
+        return None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
+
+    def levels(self):
+        bm = self._need_bm()
+        n = ctypes.c_int32()
+        lv = np.empty(bm.n_blocks, np.int32)
+        check(self.lib.pp_get_levels(self._h, ctypes.byref(n), ptr(lv)))
+        return int(n.value), lv
+
+    # -- convenience -------------------------------------------------------------------
+    @classmethod
+    def from_tables(cls, bm: BlockModel, tables: ScenarioTables | None, assign=None, device=0,
+                    psi_weights=DEFAULT_PSI_WEIGHTS) -> "Engine":
+        eng = cls(device)
+        eng.set_instance(bm)
+        eng.set_geology(psi_weights)
+        if tables is not None:
+            eng.set_scenarios(tables)
+        if assign is not None:
+            eng.set_schedule(assign)
+        return eng
+
+    @property
+    def cvar_k(self) -> int:
+        return cvar_k(self.n_scenarios) if self.n_scenarios else 1

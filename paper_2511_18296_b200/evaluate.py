@@ -1,0 +1,224 @@
+"""Drop-in replacements for the reference evaluator entry points.
+
+    evaluate_candidates_parallel   pitplan/evaluate.py:306-430
+    check_feasible                 pitplan/evaluate.py:82-105
+    precedence_repair_pass         pitplan/hybrid.py:493-510  (`_precedence_repair_pass`)
+    unmine_fixpoint                pitplan/hybrid.py:199-211  (first step of `lns_repair`)
+
+Same signatures, argument meaning, return types and error behaviour as the
+reference; the work runs in the sm_100a kernels of csrc/pitplan_b200.cu through the
+C ABI.  Objects are duck-typed: a `pitplan` Instance / ScenarioSet /
+UncertaintyFactors / Schedule, or this package's own `BlockModel` with a
+`ScenarioTables` (then `scenarios` carries both vmax and sigma and `sigma` is only
+a switch).  When `pitplan` is importable the reference's own `CandidateMove` and
+`ViolationReport` classes are returned.
+"""
+
+from __future__ import annotations
+
+import csv
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+from .engine import DEFAULT_PSI_WEIGHTS, Engine
+from .errors import InvalidArgs
+from .model import BlockModel, CandidateMove, ScenarioTables, ViolationReport
+
+_MAX_CACHED = 4
+_tls = threading.local()  # one engine cache per host thread (contexts are not thread-safe)
+
+
+def _types():
+    try:
+        from pitplan.evaluate import CandidateMove as RefMove
+        from pitplan.evaluate import ViolationReport as RefReport
+
+        return RefMove, RefReport
+    except Exception:  # noqa: BLE001
+        return CandidateMove, ViolationReport
+
+
+def _cache() -> OrderedDict:
+    c = getattr(_tls, "engines", None)
+    if c is None:
+        c = _tls.engines = OrderedDict()
+    return c
+
+
+class _Entry:
+    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params")
+
+    def __init__(self, instance, bm, engine):
+        self.instance = instance  # strong ref: keeps id(instance) from being reused
+        self.bm = bm
+        self.engine = engine
+        self.scen_key = None
+        self.scen_refs = None
+        self.params = None
+
+
+def _device() -> int:
+    return int(getattr(_tls, "device", 0))
+
+
+def set_device(device: int) -> None:
+    """CUDA device used by the drop-in functions on this thread."""
+    _tls.device = int(device)
+
+
+def _entry(instance) -> _Entry:
+    cache = _cache()
+    key = id(instance)
+    e = cache.get(key)
+    if e is not None and e.instance is instance:
+        cache.move_to_end(key)
+        return e
+    bm = instance if isinstance(instance, BlockModel) else BlockModel.from_instance(instance)
+    eng = Engine(_device())
+    eng.set_instance(bm)
+    e = _Entry(instance, bm, eng)
+    cache[key] = e
+    while len(cache) > _MAX_CACHED:
+        _, old = cache.popitem(last=False)
+        old.engine.close()
+    return e
+
+
+def _psi_weights(params):
+    if params is None:
+        return DEFAULT_PSI_WEIGHTS
+    return tuple(float(w) for w in params.psi_weights)
+
+
+def _bind_scenarios(e: _Entry, scenarios, sigma, params):
+    weights = _psi_weights(params)
+    if e.params != weights:
+        e.engine.set_geology(weights)
+        e.params = weights
+    if scenarios is None:
+        return
+    key = (id(scenarios), id(sigma))
+    if e.scen_key == key and e.scen_refs is not None and e.scen_refs[0] is scenarios and e.scen_refs[1] is sigma:
+        return
+    if isinstance(scenarios, ScenarioTables):
+        tables = scenarios
+    else:
+        tables = ScenarioTables.from_reference(e.bm, scenarios, sigma)
+    e.engine.set_scenarios(tables)
+    e.scen_key = key
+    e.scen_refs = (scenarios, sigma)
+
+
+def _assignment(schedule) -> np.ndarray:
+    return np.asarray(getattr(schedule, "assignment", schedule))
+
+
+def evaluate_candidates_parallel(
+    instance,
+    schedule,
+    candidates,
+    scenarios,
+    s,
+    sigma,
+    worker_count: int = 1,
+    literal_kernel_value: bool = False,
+    net_mining_cost: bool = False,
+    params=None,
+    trace_path=None,
+):
+    """Best insertion period per candidate plus the overall best move.
+
+    Reference: pitplan/evaluate.py:306-430.  Output is bit-identical to the reference
+    for every candidate order; `worker_count` is validated and otherwise ignored (the
+    result never depended on it).  Infeasible candidates come back with improvement -inf.
+    """
+    if worker_count < 1:
+        raise InvalidArgs("worker_count must be >= 1")
+    cand = np.fromiter((int(b) for b in candidates), dtype=np.int64)
+    e = _entry(instance)
+    B = e.bm.n_blocks
+    if cand.size and (cand.min() < -B or cand.max() >= B):
+        raise InvalidArgs("candidate block id out of range")
+    cand = np.where(cand < 0, cand + B, cand)  # Python negative indexing, as assign[b] would
+    _bind_scenarios(e, None if literal_kernel_value and scenarios is None else scenarios, sigma, params)
+    eng = e.engine
+    if s is not None and not (0 <= int(s) < max(eng.n_scenarios, 1)):
+        raise InvalidArgs(f"scenario index {s} out of range")
+    eng.set_schedule(_assignment(schedule))
+    res = eng.eval_candidates(
+        cand, None if s is None else int(s), net=net_mining_cost, literal=literal_kernel_value,
+        use_sigma=sigma is not None, trace=trace_path is not None,
+    )
+    Move, _ = _types()
+    bt = res["best_t"].tolist()
+    bv = res["best_val"].tolist()
+    fe = res["feasible"].tolist()
+    moves = [Move(block=b, period=t, improvement=v, feasible=bool(f))
+             for b, t, v, f in zip(cand.tolist(), bt, bv, fe)]
+    best = None
+    if res["best"] is not None:
+        gb, gt, gv = res["best"]
+        best = Move(block=gb, period=gt, improvement=gv, feasible=True)
+    if trace_path:
+        _write_trace(trace_path, cand, res["trace_feas"], res["trace_val"])
+    return moves, best
+
+
+def _write_trace(path, cand, feas, val):
+    """Per-(candidate, period) CSV, rows sorted like `sorted(trace_rows)` (evaluate.py:423-428)."""
+    C, T = val.shape if val.ndim == 2 else (0, 0)
+    b = np.repeat(cand, T)
+    t = np.tile(np.arange(T), C)
+    f = feas.reshape(-1).astype(np.int64)
+    v = val.reshape(-1)
+    # tuples (b, t, feasible, value): duplicates of a candidate give identical rows
+    order = np.lexsort((v, f, t, b))
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["candidate", "period", "feasible", "value"])
+        for k in order.tolist():
+            w.writerow([int(b[k]), int(t[k]), int(f[k]), repr(float(v[k]))])
+
+
+def check_feasible(instance, schedule):
+    """Precedence-pair count, capacity excess and violation (evaluate.py:82-105)."""
+    e = _entry(instance)
+    r = e.engine.check_feasible(_assignment(schedule)[None, :])
+    _, Report = _types()
+    return Report(precedence_violations=int(r["pred_count"][0]), capacity_excess=float(r["excess"][0]),
+                  violation=float(r["violation"][0]))
+
+
+def check_feasible_batch(instance, assignments):
+    """check_feasible for a population [P][B]; returns the dict of arrays."""
+    return _entry(instance).engine.check_feasible(assignments)
+
+
+def precedence_repair_pass(instance, assign: np.ndarray) -> None:
+    """In-place `_precedence_repair_pass` (hybrid.py:493-510) in topological waves."""
+    e = _entry(instance)
+    out, _ = e.engine.repair(np.asarray(assign)[None, :], mode="push")
+    assign[...] = out[0]
+
+
+def precedence_repair_batch(instance, assignments: np.ndarray) -> np.ndarray:
+    out, _ = _entry(instance).engine.repair(assignments, mode="push")
+    return out
+
+
+def unmine_fixpoint(instance, assign: np.ndarray):
+    """The unmine fixpoint opening `lns_repair` (hybrid.py:199-211), in place; returns the
+    block ids it unmined (the additions to the repair pool)."""
+    e = _entry(instance)
+    out, u = e.engine.repair(np.asarray(assign)[None, :], mode="unmine", unmined=True)
+    assign[...] = out[0]
+    return np.nonzero(u[0])[0]
+
+
+def clear_cache() -> None:
+    cache = _cache()
+    while cache:
+        _, e = cache.popitem()
+        e.engine.close()

@@ -1,0 +1,55 @@
+"""Install the B200 engine behind the reference's own plug-in points.
+
+The reference has no operator registry: the GA/LNS/SA and column-generation loops
+reach the evaluator through module-level names, and `pitplan.hybrid` binds
+`evaluate_candidates_parallel` / `check_feasible` by value at import
+(hybrid.py:22-28), as does `pitplan.colgen` for `check_feasible` (colgen.py:23).
+`install()` therefore rebinds the names in every module that holds them, so the
+unchanged loops (`lns_repair` hybrid.py:252, `HybridSearch._measure` hybrid.py:600,
+`_crossover` hybrid.py:721, DW integerisation colgen.py:573) run on the GPU.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import evaluate as _ev
+
+_PATCHES = {
+    "pitplan.evaluate": {
+        "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
+        "check_feasible": _ev.check_feasible,
+    },
+    "pitplan.hybrid": {
+        "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
+        "check_feasible": _ev.check_feasible,
+        "_precedence_repair_pass": _ev.precedence_repair_pass,
+    },
+    "pitplan.colgen": {"check_feasible": _ev.check_feasible},
+    "pitplan.saa": {},
+    "pitplan": {"check_feasible": _ev.check_feasible},
+}
+
+_saved: list[tuple[object, str, object]] = []
+
+
+def install() -> list[str]:
+    """Rebind the reference entry points; returns the patched 'module.name' list."""
+    done = []
+    for modname, names in _PATCHES.items():
+        try:
+            mod = importlib.import_module(modname)
+        except ImportError:
+            continue
+        for name, fn in names.items():
+            if hasattr(mod, name):
+                _saved.append((mod, name, getattr(mod, name)))
+                setattr(mod, name, fn)
+                done.append(f"{modname}.{name}")
+    return done
+
+
+def uninstall() -> None:
+    while _saved:
+        mod, name, orig = _saved.pop()
+        setattr(mod, name, orig)

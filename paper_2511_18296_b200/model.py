@@ -1,0 +1,256 @@
+"""Host-side data model: the reference's result records and the flat tables the
+device holds.
+
+`Schedule`, `CandidateMove` and `ViolationReport` mirror the reference dataclasses
+(evaluate.py:28-79) field for field; when the engine is installed into `pitplan`
+the drop-in functions return the reference's own classes instead (install.py).
+
+`BlockModel` is the flattened, device-ready view of a `pitplan.blockmodel.Instance`
+(blockmodel.py:91-185): precedence as an edge list plus CSR adjacency, per-block
+masses / costs / geology features, per-period capacity.  `ScenarioTables` is the
+per-scenario-set value table `vmax[s][b] = max_o v[s][b][o]` (evaluate.py:108-124)
+plus the sigma[s][t] matrix (uncertainty.py:276-321).
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import InvalidArgs, ShapeMismatch, ValidationError
+
+UNMINED = -1  # blockmodel.py:18
+
+
+@dataclass
+class Schedule:
+    """Stage-1 decision: period index per block, UNMINED (-1) for unmined (evaluate.py:28-60)."""
+
+    assignment: np.ndarray
+
+    def __post_init__(self):
+        self.assignment = np.asarray(self.assignment, dtype=int)
+
+    @classmethod
+    def empty(cls, n_blocks: int) -> "Schedule":
+        return cls(np.full(n_blocks, UNMINED, dtype=int))
+
+    @property
+    def n_blocks(self) -> int:
+        return self.assignment.size
+
+    def copy(self) -> "Schedule":
+        return Schedule(self.assignment.copy())
+
+    def digest(self) -> str:
+        return hashlib.sha256(self.assignment.astype("<i8").tobytes()).hexdigest()
+
+
+@dataclass
+class ViolationReport:
+    """evaluate.py:63-71."""
+
+    precedence_violations: int
+    capacity_excess: float
+    violation: float
+
+    @property
+    def feasible(self) -> bool:
+        return self.violation == 0.0
+
+
+@dataclass
+class CandidateMove:
+    """evaluate.py:74-79."""
+
+    block: int
+    period: int
+    improvement: float
+    feasible: bool
+
+
+@dataclass
+class BlockModel:
+    """Flat tables of one block-model instance (all numpy, host side)."""
+
+    n_blocks: int
+    n_periods: int
+    edges_i: np.ndarray  # int32[E]  (i, j): i mined no later than j, reference list order
+    edges_j: np.ndarray  # int32[E]
+    mass: np.ndarray  # f64[B]
+    cost: np.ndarray  # f64[B, T] undiscounted mining cost
+    capacity: np.ndarray  # f64[T]
+    discount_rate: float
+    coords: np.ndarray  # f64[B, 3]
+    alteration: np.ndarray  # f64[B]
+    structural: np.ndarray  # f64[B]
+    dist_intrusion: np.ndarray  # f64[B]
+    base_grade: np.ndarray  # f64[B]
+    price: float = 5.0
+    recovery_by_mode: tuple = (0.85,)
+    processing_cost_by_mode: tuple = (1.0,)
+    n_modes: int = 1
+    stored_values: np.ndarray | None = None  # f64[S_builtin, B, O] (blockmodel.py:141-147)
+    _csr: tuple | None = field(default=None, repr=False)
+
+    def __post_init__(self):
+        B, T = self.n_blocks, self.n_periods
+        self.edges_i = np.ascontiguousarray(self.edges_i, dtype=np.int32)
+        self.edges_j = np.ascontiguousarray(self.edges_j, dtype=np.int32)
+        self.mass = np.ascontiguousarray(self.mass, dtype=np.float64)
+        self.cost = np.ascontiguousarray(self.cost, dtype=np.float64).reshape(B, T)
+        self.capacity = np.ascontiguousarray(self.capacity, dtype=np.float64)
+        self.coords = np.ascontiguousarray(self.coords, dtype=np.float64).reshape(B, 3)
+        for name in ("alteration", "structural", "dist_intrusion", "base_grade"):
+            setattr(self, name, np.ascontiguousarray(getattr(self, name), dtype=np.float64))
+        if T < 1:
+            raise ValidationError("n_periods must be >= 1")
+        if self.mass.shape != (B,) or self.capacity.shape != (T,):
+            raise ShapeMismatch("mass / capacity arrays do not match n_blocks / n_periods")
+        if self.edges_i.shape != self.edges_j.shape:
+            raise ShapeMismatch("edge arrays differ in length")
+        if self.edges_i.size and (
+            self.edges_i.min() < 0 or self.edges_j.min() < 0
+            or self.edges_i.max() >= B or self.edges_j.max() >= B
+        ):
+            raise ValidationError("precedence edge references unknown block")
+
+    # -- derived -------------------------------------------------------------
+    @property
+    def n_edges(self) -> int:
+        return int(self.edges_i.size)
+
+    def csr(self):
+        """(pred_ptr, pred_idx, succ_ptr, succ_idx): predecessors of j and successors
+        of i in reference list order (blockmodel.py:180-184)."""
+        if self._csr is None:
+            B = self.n_blocks
+            oj = np.argsort(self.edges_j, kind="stable")
+            oi = np.argsort(self.edges_i, kind="stable")
+            pred_ptr = np.zeros(B + 1, dtype=np.int32)
+            succ_ptr = np.zeros(B + 1, dtype=np.int32)
+            pred_ptr[1:] = np.cumsum(np.bincount(self.edges_j, minlength=B))
+            succ_ptr[1:] = np.cumsum(np.bincount(self.edges_i, minlength=B))
+            self._csr = (
+                pred_ptr,
+                np.ascontiguousarray(self.edges_i[oj], dtype=np.int32),
+                succ_ptr,
+                np.ascontiguousarray(self.edges_j[oi], dtype=np.int32),
+            )
+        return self._csr
+
+    def discount(self) -> np.ndarray:
+        """(1 + r) ** (-t) with Python float pow (evaluate.py:341)."""
+        r = self.discount_rate
+        return np.array([(1.0 + r) ** (-t) for t in range(self.n_periods)], dtype=np.float64)
+
+    def diameter(self) -> float:
+        """Instance diameter (evaluate.py:342-344)."""
+        spans = self.coords.max(axis=0) - self.coords.min(axis=0)
+        return float(np.sqrt((spans**2).sum()))
+
+    def mean_capacity(self) -> float:
+        """float(np.mean(mining_capacity)) (evaluate.py:103)."""
+        return float(np.mean(self.capacity))
+
+    def fingerprint(self) -> str:
+        h = hashlib.sha256()
+        for a in (self.edges_i, self.edges_j, self.mass, self.cost, self.capacity,
+                  self.alteration, self.structural, self.dist_intrusion, self.coords):
+            h.update(np.ascontiguousarray(a).tobytes())
+        h.update(repr((self.n_blocks, self.n_periods, self.discount_rate)).encode())
+        return h.hexdigest()
+
+    # -- construction from the reference data model ----------------------------
+    @classmethod
+    def from_instance(cls, inst) -> "BlockModel":
+        """Flatten a `pitplan.blockmodel.Instance` (duck-typed)."""
+        blocks = inst.blocks
+        B, T = len(blocks), int(inst.n_periods)
+        prec = np.asarray(inst.precedence, dtype=np.int64).reshape(-1, 2)
+        econ = inst.economics
+        feats = np.array(
+            [(b.features.alteration_intensity, b.features.structural_density,
+              b.features.distance_to_intrusion) for b in blocks], dtype=np.float64,
+        ).reshape(B, 3)
+        stored = None
+        if inst.modes and len(inst.modes[0].value) == B:
+            stored = np.asarray(inst.builtin_values(), dtype=np.float64)
+        return cls(
+            n_blocks=B,
+            n_periods=T,
+            edges_i=prec[:, 0],
+            edges_j=prec[:, 1],
+            mass=inst.masses(),
+            cost=inst.mining_costs().reshape(B, T),
+            capacity=np.asarray(inst.mining_capacity, dtype=np.float64),
+            discount_rate=float(inst.discount_rate),
+            coords=inst.coords_array().reshape(B, 3),
+            alteration=feats[:, 0],
+            structural=feats[:, 1],
+            dist_intrusion=feats[:, 2],
+            base_grade=inst.base_grades(),
+            price=float(econ.price),
+            recovery_by_mode=tuple(econ.recovery_by_mode),
+            processing_cost_by_mode=tuple(econ.processing_cost_by_mode),
+            n_modes=len(inst.modes),
+            stored_values=stored,
+        )
+
+
+def scenario_values(bm: BlockModel, grades: np.ndarray | None, use_stored: bool = False) -> np.ndarray:
+    """vmax[s][b] = max over modes of v[s][b][o] (evaluate.py:108-124, 300-303).
+
+    v = ((grades * m) * price) * recovery_o - m * processing_cost_o, or the stored
+    per-mode matrices when the scenario set is the instance's builtin one."""
+    if use_stored:
+        if bm.stored_values is None:
+            raise InvalidArgs("scenario set uses stored values but the instance has none")
+        return np.ascontiguousarray(bm.stored_values.max(axis=2))
+    g = np.asarray(grades, dtype=np.float64)
+    if g.ndim != 2 or g.shape[1] != bm.n_blocks:
+        raise ShapeMismatch("scenario set does not match instance block count")
+    m = bm.mass[None, :]
+    best = None
+    for o in range(bm.n_modes):
+        rec = bm.recovery_by_mode[o % len(bm.recovery_by_mode)]
+        cost = bm.processing_cost_by_mode[o % len(bm.processing_cost_by_mode)]
+        v = g * m * bm.price * rec - m * cost
+        best = v if best is None else np.maximum(best, v)
+    return np.ascontiguousarray(best)
+
+
+@dataclass
+class ScenarioTables:
+    """Per-scenario-set tables: vmax[S][B] (reference layout) and sigma[S][T] or None."""
+
+    vmax: np.ndarray
+    sigma: np.ndarray | None
+
+    def __post_init__(self):
+        self.vmax = np.ascontiguousarray(self.vmax, dtype=np.float64)
+        if self.sigma is not None:
+            self.sigma = np.ascontiguousarray(self.sigma, dtype=np.float64)
+            if self.sigma.shape[0] != self.vmax.shape[0]:
+                raise ShapeMismatch("sigma scenario count differs from the value table")
+
+    @property
+    def n_scenarios(self) -> int:
+        return int(self.vmax.shape[0])
+
+    @classmethod
+    def from_reference(cls, bm: BlockModel, scenarios, sigma) -> "ScenarioTables":
+        """From a `pitplan.scenarios.ScenarioSet` and `UncertaintyFactors | None`."""
+        use_stored = bool(getattr(scenarios, "meta", {}).get("use_stored_values"))
+        vmax = scenario_values(bm, None if use_stored else scenarios.grades, use_stored)
+        sig = None if sigma is None else np.asarray(sigma.sigma, dtype=np.float64)
+        return cls(vmax=vmax, sigma=sig)
+
+
+def cvar_k(n_scenarios: int) -> int:
+    """ceil(0.1 n) lowest samples enter CVaR10 (saa.py:157)."""
+    import math
+
+    return max(1, math.ceil(0.1 * n_scenarios))

@@ -1,0 +1,85 @@
+"""Helpers that turn tests/golden/*.npz entries into inputs (test-only)."""
+
+from __future__ import annotations
+
+import functools
+import hashlib
+import os
+
+import numpy as np
+
+from paper_2511_18296_b200.model import BlockModel, ScenarioTables
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@functools.lru_cache(maxsize=None)
+def load(name: str):
+    with np.load(os.path.join(GOLDEN, f"{name}.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def bm_from(store: dict, p: str) -> BlockModel:
+    B, T = int(store[p + "n_blocks"]), int(store[p + "n_periods"])
+    e = store[p + "edges"].reshape(-1, 2)
+    f = store[p + "features"].reshape(B, 3)
+    return BlockModel(
+        n_blocks=B, n_periods=T, edges_i=e[:, 0], edges_j=e[:, 1], mass=store[p + "mass"],
+        cost=store[p + "cost"], capacity=store[p + "capacity"],
+        discount_rate=float(store[p + "discount_rate"]), coords=store[p + "coords"],
+        alteration=f[:, 0], structural=f[:, 1], dist_intrusion=f[:, 2],
+        base_grade=np.zeros(B),
+    )
+
+
+def tables_from(store: dict, p: str) -> ScenarioTables:
+    return ScenarioTables(vmax=store[p + "vmax"], sigma=store.get(p + "sigma"))
+
+
+def digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def instance_digest(bm: BlockModel) -> str:
+    edges = np.stack([bm.edges_i, bm.edges_j], axis=1).astype(np.int32)
+    feats = np.stack([bm.alteration, bm.structural, bm.dist_intrusion], axis=1)
+    return digest(edges, bm.mass, bm.cost, bm.capacity, bm.coords, feats)
+
+
+@functools.lru_cache(maxsize=None)
+def config(name: str):
+    """The synthetic configuration, rebuilt with the package's reference-identical builders.
+
+    sigma is taken from the golden fixture when one exists (its Moran's I term goes
+    through a BLAS dot product whose last ulp depends on the host's thread count);
+    c["golden_ok"] says whether every input is bit-identical to the reference run's."""
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.model import scenario_values
+
+    c = synth.build_config(name)
+    c["vmax"] = scenario_values(c["bm"], c["grades"])
+    c["sigma_synth"] = c["sigma"]
+    try:
+        st = load(name.lower())
+    except FileNotFoundError:
+        st = None
+    c["golden_ok"] = False
+    if st is not None and f"{name}_sigma" in st:
+        c["sigma"] = st[f"{name}_sigma"]
+        c["golden_ok"] = (instance_digest(c["bm"]) == st[f"{name}_digest_instance"].item().decode()
+                          and digest(c["vmax"]) == st[f"{name}_digest_vmax"].item().decode())
+    c["greedy"] = synth.greedy_initialize(c["bm"], c["grades"], c["sigma"])
+    return c
+
+
+def same(a, b) -> bool:
+    """Bit-level equality for float arrays (NaN == NaN, -inf == -inf; -0.0 == 0.0)."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    if a.dtype.kind == "f":
+        return bool(np.all((a == b) | (np.isnan(a) & np.isnan(b))))
+    return bool(np.array_equal(a, b))

@@ -1,0 +1,313 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation (pitplan) in the
+build container.  Run:  python tests/golden/make_golden.py
+
+The reference checkout (/root/reference) is not available on the GPU box, so its
+outputs are frozen here together with the inputs (small cases) or sha256 digests of
+the inputs (large cases, rebuilt bit-identically by paper_2511_18296_b200.synth).
+Every array below is produced by calling the reference's own functions:
+
+  evaluate_candidates_parallel  evaluate.py:306-430   (moves, best, trace CSV)
+  check_feasible                evaluate.py:82-105
+  _precedence_repair_pass       hybrid.py:493-510
+  lns_repair (max_iters=0)      hybrid.py:199-211 unmine fixpoint
+  risk_metrics                  saa.py:150-166 (CVaR10 of per-scenario deltas)
+"""
+
+from __future__ import annotations
+
+import csv
+import hashlib
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+REF = os.environ.get("PITPLAN_REF", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+from pitplan.blockmodel import UNMINED, Block, Economics, GeoFeatures, Instance, OperatingMode, generate_synthetic  # noqa: E402
+from pitplan.evaluate import Schedule, check_feasible, evaluate_candidates_parallel  # noqa: E402
+from pitplan.hybrid import _precedence_repair_pass, greedy_initialize, lns_repair  # noqa: E402
+from pitplan.rng import substream  # noqa: E402
+from pitplan.saa import risk_metrics  # noqa: E402
+from pitplan.scenarios import builtin_scenarios, sample_lognormal  # noqa: E402
+from pitplan.uncertainty import uncertainty_factors  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def flat(inst: Instance, prefix: str) -> dict:
+    """Raw tables of a reference Instance (no product code involved)."""
+    prec = np.asarray(inst.precedence, dtype=np.int64).reshape(-1, 2)
+    return {
+        f"{prefix}n_blocks": np.int64(inst.n_blocks),
+        f"{prefix}n_periods": np.int64(inst.n_periods),
+        f"{prefix}edges": prec,
+        f"{prefix}mass": inst.masses(),
+        f"{prefix}cost": inst.mining_costs().reshape(inst.n_blocks, inst.n_periods),
+        f"{prefix}capacity": np.asarray(inst.mining_capacity, dtype=np.float64),
+        f"{prefix}discount_rate": np.float64(inst.discount_rate),
+        f"{prefix}coords": inst.coords_array().reshape(inst.n_blocks, 3),
+        f"{prefix}features": np.array([(b.features.alteration_intensity, b.features.structural_density,
+                                        b.features.distance_to_intrusion) for b in inst.blocks]).reshape(-1, 3),
+    }
+
+
+def vmax_of(inst, scen) -> np.ndarray:
+    from pitplan.evaluate import scenario_mode_values
+
+    return scenario_mode_values(inst, scen).max(axis=2)
+
+
+def full_greedy(inst) -> np.ndarray:
+    """HybridSearch._full_greedy (hybrid.py:643-667) without building a HybridSearch."""
+    masses = inst.masses()
+    assign = np.full(inst.n_blocks, UNMINED, dtype=int)
+    load = np.zeros(inst.n_periods)
+    for b in inst.topological_order():
+        t_min, ok = 0, True
+        for p in inst.predecessors(b):
+            if assign[p] == UNMINED:
+                ok = False
+                break
+            t_min = max(t_min, assign[p])
+        if not ok:
+            continue
+        for t in range(t_min, inst.n_periods):
+            if load[t] + masses[b] <= inst.mining_capacity[t]:
+                assign[b] = t
+                load[t] += masses[b]
+                break
+    return assign
+
+
+def run_kernel(inst, sched, cand, scen, s, sigma, **kw):
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "trace.csv")
+        moves, best = evaluate_candidates_parallel(inst, sched, cand, scen, s, sigma, trace_path=path, **kw)
+        rows = list(csv.reader(open(path)))[1:]
+    T = inst.n_periods
+    # trace rows are sorted by (candidate, period); re-key to input order [C][T]
+    by_key = {(int(r[0]), int(r[1])): (int(r[2]), float(r[3])) for r in rows}
+    tv = np.array([[by_key[(int(b), t)][1] for t in range(T)] for b in cand], dtype=np.float64).reshape(-1, T)
+    tf = np.array([[by_key[(int(b), t)][0] for t in range(T)] for b in cand], dtype=np.uint8).reshape(-1, T)
+    out = {
+        "best_t": np.array([m.period for m in moves], dtype=np.int32),
+        "best_val": np.array([m.improvement for m in moves], dtype=np.float64),
+        "feasible": np.array([m.feasible for m in moves], dtype=np.uint8),
+        "best": np.array([best.block, best.period, best.improvement] if best else [-1, -1, -np.inf]),
+        "trace_val": tv,
+        "trace_feas": tf,
+    }
+    return out
+
+
+def put(store: dict, prefix: str, res: dict, keys=("best_t", "best_val", "feasible", "best", "trace_val", "trace_feas")):
+    for k in keys:
+        store[f"{prefix}{k}"] = res[k]
+
+
+def scenario_stats(inst, sched, cand, scen, sigma, net=False):
+    """Per-scenario deltas d_k(b,t) = kernel value with s=k at t minus at the current period,
+    from the reference kernel's own trace; expected = np.mean over k, CVaR10 via risk_metrics."""
+    S, T, C = scen.n_s, inst.n_periods, len(cand)
+    vals = np.empty((S, C, T))
+    for k in range(S):
+        vals[k] = run_kernel(inst, sched, cand, scen, k, sigma, net_mining_cost=net)["trace_val"]
+    a = sched.assignment
+    d = np.empty((S, C, T))
+    feas = np.isfinite(vals[0])
+    for i, b in enumerate(cand):
+        ab = a[b]
+        for k in range(S):
+            d[k, i] = vals[k, i] - vals[k, i, ab] if ab != UNMINED else vals[k, i]
+    exp = np.full((C, T), -np.inf)
+    cvar = np.full((C, T), -np.inf)
+    for i in range(C):
+        for t in range(T):
+            if feas[i, t]:
+                exp[i, t] = float(np.mean(d[:, i, t]))
+                cvar[i, t] = risk_metrics(d[:, i, t]).cvar10
+    d = np.where(feas[None], d, -np.inf)
+    return np.transpose(d, (1, 0, 2)).astype(np.float32), exp, cvar
+
+
+# ------------------------------------------------------------------------------------------
+def small_cases(store):
+    """The 20 TestKernelDeterminism cases (test_acceptance.py:140-165) plus variants."""
+    for case in range(20):
+        p = f"kd{case}_"
+        inst = generate_synthetic(27, (3, 3, 3), 3, 1, seed=300 + case, n_rock_types=1)
+        scen = sample_lognormal(inst, 2, 0.3, seed=400 + case)
+        sigma = uncertainty_factors(inst, scen.grades)
+        sched = greedy_initialize(inst, scen, sigma)
+        drop = substream(500 + case, "kern").choice(27, size=6, replace=False)
+        for b in drop:
+            sched.assignment[b] = -1
+        cand = [int(b) for b in drop]
+        store.update(flat(inst, p))
+        store[p + "vmax"] = vmax_of(inst, scen)
+        store[p + "sigma"] = sigma.sigma
+        store[p + "assign"] = sched.assignment.astype(np.int32)
+        store[p + "cand"] = np.array(cand, dtype=np.int32)
+        put(store, p + "s0_", run_kernel(inst, sched, cand, scen, 0, sigma))
+        put(store, p + "sN_", run_kernel(inst, sched, cand, scen, None, sigma))
+        put(store, p + "net_", run_kernel(inst, sched, cand, scen, None, sigma, net_mining_cost=True))
+        put(store, p + "nosig_", run_kernel(inst, sched, cand, scen, 1, None))
+        put(store, p + "lit_", run_kernel(inst, sched, cand, scen, 0, sigma, literal_kernel_value=True))
+        # all-blocks candidates on the undamaged greedy schedule (mined candidates too)
+        sched2 = greedy_initialize(inst, scen, sigma)
+        allc = list(range(27))
+        store[p + "assign2"] = sched2.assignment.astype(np.int32)
+        put(store, p + "all_", run_kernel(inst, sched2, allc, scen, None, sigma, net_mining_cost=True))
+        sd, ex, cv = scenario_stats(inst, sched2, allc, scen, sigma, net=True)
+        store[p + "all_scen_delta"], store[p + "all_exp"], store[p + "all_cvar"] = sd, ex, cv
+        # check_feasible / repair / unmine fixpoint on random assignments
+        rng = np.random.default_rng(1000 + case)
+        rand = rng.integers(-1, 3, size=(4, 27))
+        store[p + "rand"] = rand.astype(np.int32)
+        cf = [check_feasible(inst, Schedule(r)) for r in rand]
+        store[p + "rand_pred"] = np.array([c.precedence_violations for c in cf], dtype=np.int64)
+        store[p + "rand_excess"] = np.array([c.capacity_excess for c in cf])
+        store[p + "rand_viol"] = np.array([c.violation for c in cf])
+        rep = []
+        for r in rand:
+            a = r.copy()
+            _precedence_repair_pass(inst, a)
+            rep.append(a)
+        store[p + "rand_repair"] = np.array(rep, dtype=np.int32)
+        big = Instance(blocks=inst.blocks, precedence=inst.precedence, n_periods=inst.n_periods,
+                       mining_capacity=tuple([1e12] * inst.n_periods), plant_hours=inst.plant_hours,
+                       modes=inst.modes, rock_types=inst.rock_types, discount_rate=inst.discount_rate,
+                       economics=inst.economics)
+        fix = [lns_repair(big, Schedule(r), [], scen, None, max_iters=0).assignment for r in rand]
+        store[p + "rand_unmine"] = np.array(fix, dtype=np.int32)
+
+
+def _feat(alt=0.5, struct=0.5, dist=1.0):
+    return GeoFeatures(alteration_intensity=alt, structural_density=struct, distance_to_intrusion=dist)
+
+
+def _block(bid, mass, coords, grade, n_periods, cost=0.0):
+    return Block(id=bid, mass=float(mass), coords=tuple(float(c) for c in coords), base_grade=float(grade),
+                 rock_type_by_scenario=(0,), features=_feat(),
+                 mining_cost_by_period=tuple([float(cost)] * n_periods))
+
+
+def _instance(blocks, precedence=(), n_periods=1, capacity=1e9):
+    modes = [OperatingMode(id=0, rate=100.0, blend_fraction={"ore": 1.0},
+                           value=tuple((100.0,) for _ in blocks))]
+    return Instance(blocks=list(blocks), precedence=[tuple(e) for e in precedence], n_periods=n_periods,
+                    mining_capacity=tuple([capacity] * n_periods), plant_hours=tuple([1e9] * n_periods),
+                    modes=modes, rock_types=["ore"], discount_rate=0.08, economics=Economics())
+
+
+def hand_cases(store):
+    """Worked examples of test_evaluate.py:20-50 and 204-258."""
+    cases = {
+        # forced choice: block 1 fits only period 1 (test_evaluate.py:204-211)
+        "forced": (_instance([_block(0, 100, (0, 0, 0), 1, 2), _block(1, 100, (0, 0, 1), 1, 2)], [(0, 1)], 2, 150.0),
+                   [0, UNMINED], [1], 0, False),
+        # earlier period wins under discounting (213-220)
+        "early": (_instance([_block(0, 100, (0, 0, 0), 1, 2)], (), 2, 500.0), [UNMINED], [0], 0, False),
+        # infeasible sentinel (238-245)
+        "infeas": (_instance([_block(0, 100, (0, 0, 0), 1, 1), _block(1, 100, (0, 0, 1), 1, 1)], [(0, 1)], 1),
+                   [UNMINED, UNMINED], [1], 0, False),
+        # literal kernel value 100*100*factor = 11250 (247-258)
+        "literal": (_instance([_block(0, 100, (0, 0, 0), 1, 1)], (), 1, 500.0), [UNMINED], [0], 0, True),
+    }
+    for name, (inst, assign, cand, s, lit) in cases.items():
+        p = f"hand_{name}_"
+        scen = builtin_scenarios(inst)
+        sched = Schedule(np.array(assign))
+        store.update(flat(inst, p))
+        store[p + "vmax"] = vmax_of(inst, scen)
+        store[p + "assign"] = np.array(assign, dtype=np.int32)
+        store[p + "cand"] = np.array(cand, dtype=np.int32)
+        store[p + "literal"] = np.int64(lit)
+        put(store, p, run_kernel(inst, sched, cand, scen, s, None, literal_kernel_value=lit))
+    feas = {
+        "prec": (_instance([_block(0, 100, (0, 0, 0), 1, 2), _block(1, 100, (0, 0, 1), 1, 2)], [(0, 1)], 2), [1, 0]),
+        "unmined_parent": (_instance([_block(0, 100, (0, 0, 0), 1, 2), _block(1, 100, (0, 0, 1), 1, 2)], [(0, 1)], 2),
+                           [UNMINED, 0]),
+        "same": (_instance([_block(0, 100, (0, 0, 0), 1, 2), _block(1, 100, (0, 0, 1), 1, 2)], [(0, 1)], 2), [0, 0]),
+        "capacity": (_instance([_block(0, 600, (0, 0, 0), 1, 1), _block(1, 600, (1, 0, 0), 1, 1)], (), 1, 1000.0), [0, 0]),
+        "empty": (generate_synthetic(8, (2, 2, 2), 3, 1, seed=11, n_rock_types=1), [UNMINED] * 8),
+    }
+    for name, (inst, assign) in feas.items():
+        p = f"feas_{name}_"
+        store.update(flat(inst, p))
+        store[p + "assign"] = np.array(assign, dtype=np.int32)
+        r = check_feasible(inst, Schedule(np.array(assign)))
+        store[p + "out"] = np.array([r.precedence_violations, r.capacity_excess, r.violation])
+
+
+def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
+    inst = generate_synthetic(n, dims, T, 1, seed=1, n_rock_types=1, capacity_factor=cf)
+    scen = sample_lognormal(inst, S, 0.3, seed=2)
+    sigma = uncertainty_factors(inst, scen.grades)
+    cand = substream(3, "cand").integers(0, n, size=C).astype(np.int32)
+    p = f"{name}_"
+    f = flat(inst, "")
+    store[p + "digest_instance"] = np.bytes_(digest(f["edges"].astype(np.int32), f["mass"], f["cost"], f["capacity"],
+                                                    f["coords"], f["features"]))
+    store[p + "digest_scen"] = np.bytes_(digest(vmax_of(inst, scen), sigma.sigma))
+    store[p + "digest_vmax"] = np.bytes_(digest(vmax_of(inst, scen)))
+    # sigma[S][T] depends on a BLAS dot product (Moran's I), whose rounding varies with the
+    # host's thread count: freeze the small matrix itself
+    store[p + "sigma"] = sigma.sigma
+    store[p + "cand"] = cand
+    for sname, assign in (("full", full_greedy(inst)), ("greedy", greedy_initialize(inst, scen, sigma).assignment)):
+        q = f"{p}{sname}_"
+        sched = Schedule(assign)
+        store[q + "digest_assign"] = np.bytes_(digest(assign.astype(np.int32)))
+        keys = ("best_t", "best_val", "feasible", "best") + (("trace_val", "trace_feas") if n <= 4000 else ())
+        put(store, q + "sN_", run_kernel(inst, sched, cand.tolist(), scen, None, sigma), keys)
+        put(store, q + "net_", run_kernel(inst, sched, cand.tolist(), scen, None, sigma, net_mining_cost=True), keys)
+        put(store, q + "s0_", run_kernel(inst, sched, cand.tolist(), scen, 0, sigma), keys)
+        r = check_feasible(inst, sched)
+        store[q + "feas"] = np.array([r.precedence_violations, r.capacity_excess, r.violation])
+        if scen_subset and sname == "full":
+            sub = cand[:scen_subset].tolist()
+            sd, ex, cv = scenario_stats(inst, sched, sub, scen, sigma, net=True)
+            store[q + "sub_scen_delta"], store[q + "sub_exp"], store[q + "sub_cvar"] = sd, ex, cv
+    # repair pass on crossover-like damaged schedules (hybrid.py:716-722 shape)
+    rng = np.random.default_rng(7)
+    full = full_greedy(inst)
+    emp = np.full(n, UNMINED)
+    reps, srcs = [], []
+    for k in range(3):
+        cut = int(rng.integers(1, n))
+        child = full.copy()
+        child[cut:] = rng.integers(-1, T, size=n - cut) if k == 2 else emp[cut:]
+        srcs.append(child.astype(np.int32))
+        a = child.copy()
+        _precedence_repair_pass(inst, a)
+        reps.append(a.astype(np.int32))
+    store[p + "repair_in"] = np.array(srcs)
+    store[p + "repair_out"] = np.array(reps)
+
+
+def main():
+    store: dict = {}
+    small_cases(store)
+    hand_cases(store)
+    np.savez_compressed(os.path.join(OUT, "small.npz"), **store)
+    store = {"numpy_version": np.bytes_(np.__version__)}
+    config_case(store, "C1", 4000, (20, 20, 10), 10, 10, 1000, scen_subset=200)
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **store)
+    store = {"numpy_version": np.bytes_(np.__version__)}
+    config_case(store, "C2", 50000, (50, 50, 20), 15, 20, 16667)
+    np.savez_compressed(os.path.join(OUT, "c2.npz"), **store)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,65 @@
+"""The C-ABI library loads and exports every entry point include/pitplan_b200.h declares
+(CPU test: no compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2511_18296_b200 import _lib
+from paper_2511_18296_b200.errors import DeviceError, InvalidArgs, PitplanError, raise_for_status
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "pitplan_b200.h")
+
+
+def _declared():
+    src = open(HDR).read()
+    return sorted(set(re.findall(r"^PP_API\s+[\w\s\*]*?\b(pp_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_lists_entry_points():
+    names = _declared()
+    assert "pp_eval_candidates" in names and "pp_check_feasible" in names and len(names) >= 20
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(_declared()) == set(_lib.SIGNATURES), "ctypes signatures out of sync with the header"
+
+
+def test_abi_version_and_error_channel():
+    lib = _lib.load()
+    assert lib.pp_abi_version() == 1
+    assert isinstance(lib.pp_last_error(), bytes)
+
+
+def test_null_arguments_are_errors_not_crashes():
+    lib = _lib.load()
+    assert lib.pp_ctx_create(0, None) == 1
+    assert b"NULL" in lib.pp_last_error()
+    assert lib.pp_set_instance(None, 1, 1, 0, None, None, None, None, None, None) == 1
+
+
+def test_status_mapping():
+    with pytest.raises(InvalidArgs):
+        raise_for_status(1, "x")
+    with pytest.raises(DeviceError):
+        raise_for_status(3, "x")
+    with pytest.raises(PitplanError):
+        raise_for_status(5, "x")
+
+
+def test_no_gpu_context_creation_fails_loudly():
+    lib = _lib.load()
+    n = ctypes.c_int()
+    rc = lib.pp_device_count(ctypes.byref(n))
+    if rc == 0 and n.value > 0:
+        pytest.skip("a GPU is present")
+    from paper_2511_18296_b200.engine import Engine
+
+    with pytest.raises(PitplanError):
+        Engine(0)

@@ -1,0 +1,148 @@
+"""Pin the CPU oracle (oracle/oracle.c) to outputs of the reference itself.
+
+tests/golden/*.npz were produced by tests/golden/make_golden.py calling the reference
+pitplan functions; these CPU tests run everywhere and require bit-identical results.
+"""
+
+import numpy as np
+import pytest
+
+from tests._fixtures import bm_from, config, instance_digest, load, same, tables_from
+
+KD = range(20)
+
+
+def _oracle(oracle_lib, store, p, sigma=True):
+    t = tables_from(store, p)
+    return oracle_lib.Oracle(bm_from(store, p), t.vmax, t.sigma if sigma else None)
+
+
+def _check(res, store, q, trace=True):
+    assert same(res["best_t"], store[q + "best_t"]), q
+    assert same(res["best_val"], store[q + "best_val"]), q
+    assert same(res["feasible"], store[q + "feasible"]), q
+    g = store[q + "best"]
+    if g[0] < 0:
+        assert res["best"] is None, q
+    else:
+        assert res["best"] == (int(g[0]), int(g[1]), float(g[2])), q
+    if trace:
+        assert same(res["trace_val"], store[q + "trace_val"]), q
+        assert same(res["trace_feas"], store[q + "trace_feas"]), q
+
+
+def test_pairwise_sum_matches_numpy(oracle_lib):
+    rng = np.random.default_rng(0)
+    for n in list(range(0, 300)) + [511, 512, 513, 1000, 4097, 8191, 8193, 20000, 65537]:
+        x = rng.uniform(-1e3, 1e6, n)
+        assert oracle_lib.np_sum(x) == float(np.sum(x)), n
+
+
+@pytest.mark.parametrize("case", KD)
+def test_kernel_determinism_cases(oracle_lib, case):
+    """test_acceptance.py:140-165 cases, every kernel flag combination."""
+    st = load("small")
+    p = f"kd{case}_"
+    o = _oracle(oracle_lib, st, p)
+    a, c = st[p + "assign"], st[p + "cand"]
+    _check(o.eval_candidates(a, c, 0, trace=True), st, p + "s0_")
+    _check(o.eval_candidates(a, c, None, trace=True), st, p + "sN_")
+    _check(o.eval_candidates(a, c, None, net=True, trace=True), st, p + "net_")
+    _check(o.eval_candidates(a, c, 1, use_sigma=False, trace=True), st, p + "nosig_")
+    _check(o.eval_candidates(a, c, 0, literal=True, trace=True), st, p + "lit_")
+    a2 = st[p + "assign2"]
+    allc = np.arange(27, dtype=np.int32)
+    r = o.eval_candidates(a2, allc, None, net=True, trace=True, stats=True, scen=True)
+    _check(r, st, p + "all_")
+    # per-scenario deltas from the reference kernel run with s=k, CVaR via risk_metrics
+    assert same(r["scen_delta"], st[p + "all_scen_delta"])
+    assert same(r["exp_delta"], st[p + "all_exp"])
+    assert same(r["cvar"], st[p + "all_cvar"])
+
+
+@pytest.mark.parametrize("case", KD)
+def test_feasibility_and_repair(oracle_lib, case):
+    st = load("small")
+    p = f"kd{case}_"
+    o = _oracle(oracle_lib, st, p)
+    for k, a in enumerate(st[p + "rand"]):
+        pc, ex, vi = o.check_feasible(a)
+        assert pc == st[p + "rand_pred"][k]
+        assert ex == st[p + "rand_excess"][k]
+        assert vi == st[p + "rand_viol"][k]
+        assert np.array_equal(o.precedence_repair(a), st[p + "rand_repair"][k])
+        fixed, _ = o.unmine_fixpoint(a)
+        assert np.array_equal(fixed, st[p + "rand_unmine"][k])
+
+
+def test_hand_cases(oracle_lib):
+    st = load("small")
+    for name in ("forced", "early", "infeas", "literal"):
+        p = f"hand_{name}_"
+        o = _oracle(oracle_lib, st, p, sigma=False)
+        r = o.eval_candidates(st[p + "assign"], st[p + "cand"], 0, literal=bool(st[p + "literal"]),
+                              use_sigma=False, trace=True)
+        _check(r, st, p)
+    # worked values of test_evaluate.py
+    assert int(st["hand_forced_best"][1]) == 1
+    assert int(st["hand_early_best"][1]) == 0
+    assert st["hand_infeas_best"][0] == -1 and st["hand_infeas_best_val"][0] == -np.inf
+    assert st["hand_literal_best"][2] == 11250.0
+    for name in ("prec", "unmined_parent", "same", "capacity", "empty"):
+        p = f"feas_{name}_"
+        o = oracle_lib.Oracle(bm_from(st, p))
+        pc, ex, vi = o.check_feasible(st[p + "assign"])
+        exp = st[p + "out"]
+        assert (pc, ex, vi) == (int(exp[0]), float(exp[1]), float(exp[2])), name
+    assert tuple(st["feas_capacity_out"]) == (0.0, 200.0, 0.2)
+
+
+@pytest.mark.parametrize("name", ["C1", pytest.param("C2", marks=pytest.mark.slow)])
+def test_synth_rebuilds_reference_inputs(name):
+    """paper_2511_18296_b200.synth reproduces the reference builders bit for bit."""
+    st = load(name.lower())
+    c = config(name)
+    from tests._fixtures import digest
+
+    assert instance_digest(c["bm"]) == st[f"{name}_digest_instance"].item().decode()
+    assert digest(c["vmax"], c["sigma_synth"]) == st[f"{name}_digest_scen"].item().decode()
+    assert c["golden_ok"]
+    assert np.array_equal(c["cand"], st[f"{name}_cand"])
+    assert digest(c["assign"].astype(np.int32)) == st[f"{name}_full_digest_assign"].item().decode()
+    assert digest(c["greedy"].astype(np.int32)) == st[f"{name}_greedy_digest_assign"].item().decode()
+
+
+@pytest.mark.parametrize("name", ["C1", pytest.param("C2", marks=pytest.mark.slow)])
+def test_config_batches(oracle_lib, name):
+    st = load(name.lower())
+    c = config(name)
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    trace = name == "C1"
+    for sname in ("full", "greedy"):
+        a = c["assign"] if sname == "full" else c["greedy"]
+        q = f"{name}_{sname}_"
+        _check(o.eval_candidates(a, c["cand"], None, trace=trace, nthreads=4), st, q + "sN_", trace)
+        _check(o.eval_candidates(a, c["cand"], None, net=True, trace=trace, nthreads=4), st, q + "net_", trace)
+        _check(o.eval_candidates(a, c["cand"], 0, trace=trace), st, q + "s0_", trace)
+        pc, ex, vi = o.check_feasible(a)
+        f = st[q + "feas"]
+        assert (pc, ex, vi) == (int(f[0]), float(f[1]), float(f[2]))
+    if name == "C1":
+        sub = c["cand"][:200]
+        r = o.eval_candidates(c["assign"], sub, None, net=True, stats=True, scen=True)
+        assert same(r["scen_delta"], st["C1_full_sub_scen_delta"])
+        assert same(r["exp_delta"], st["C1_full_sub_exp"])
+        assert same(r["cvar"], st["C1_full_sub_cvar"])
+    for k, a in enumerate(st[f"{name}_repair_in"]):
+        assert np.array_equal(o.precedence_repair(a), st[f"{name}_repair_out"][k])
+
+
+def test_oracle_thread_count_invariance(oracle_lib):
+    """worker_count bit-identity (test_evaluate.py:222-229) for the OpenMP oracle."""
+    c = config("C1")
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    r1 = o.eval_candidates(c["assign"], c["cand"], None, stats=True, nthreads=1)
+    r8 = o.eval_candidates(c["assign"], c["cand"], None, stats=True, nthreads=8)
+    for k in ("best_t", "best_val", "feasible", "exp_delta", "cvar"):
+        assert same(r1[k], r8[k])
+    assert r1["best"] == r8["best"]
