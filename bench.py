@@ -1,0 +1,422 @@
+"""Benchmark of the B200 move-evaluation engine (BASELINE.json metric).
+
+One step = one evaluator batch of the headline configuration C2:
+50,000-block model, 15 periods, 20 scenarios, 16,667 candidate blocks x 15 periods =
+250,005 candidate moves, each evaluated under all 20 scenarios:
+
+  k_period_mass: period masses of the current schedule (bit-exact numpy pairwise tree)
+  + k_eval_candidates (launched with programmatic dependent launch so its gathers
+    overlap k_period_mass): precedence window, capacity test, kernel value (ref parity key),
+    per-scenario deltas -> expected delta and CVaR10 per move, per-candidate argmax,
+    grid argmax (1 kernel)
+  [+ N>1: NCCL all-gather of the 16-byte per-GPU best and an ordered reduce kernel]
+
+`value` is device-timed (CUDA events, inputs resident in HBM, L2 flushed by a 256 MiB
+write between timed steps); `e2e` is the same batch through the C ABI with host
+buffers (pinned), host<->device copies inside the timed region.
+`--impl reference` times the CPU restatement of the reference (oracle/, the reference
+itself is pure Python and cannot run on the GPU box) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "move×scenario evals/sec and ms per 250k-move batch (50k blocks); % HBM roofline"
+UNIT = "move-scenario evals/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_inputs(config: str, rank: int = 0):
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.model import ScenarioTables, scenario_values
+
+    c = synth.build_config(config)
+    if rank:
+        c["cand"] = synth.candidate_blocks(c["bm"].n_blocks, c["C"], seed=3 + rank)
+    c["tables"] = ScenarioTables(scenario_values(c["bm"], c["grades"]), c["sigma"])
+    return c
+
+
+def algorithmic_bytes(c, deg_mean: float) -> dict:
+    """Compulsory bytes of one k_eval_candidates launch."""
+    C, T, S = c["C"], c["T"], c["S"]
+    per_cand = (4 + 32 + 4 + 8 + 8 * deg_mean   # cand id, BlockRow, assign[b], unit_mean[b], adjacency ids+assign
+                + 8 * T + 8 * ((S + 3) & ~3)      # mining-cost row, vmax row (fp64, padded to 4)
+                + 13 + 16 * T)                    # best (t, value, flag) + per-move exp_delta & cvar
+    M = C * T
+    survey = M * (80 + 8 * deg_mean) + 8 * M * S  # SURVEY §8(d) per-move figure, fp64 vmax, no reuse
+    return {"per_candidate": per_cand, "per_launch": per_cand * C, "survey_uncached": survey}
+
+
+def cpu_reference(c, seconds: float = 3.0, nthreads: int | None = None, max_batches: int | None = None):
+    """Time the oracle port on the same batch (period mass + evaluation + scenario stats)."""
+    from oracle import oracle
+
+    oracle.build()
+    o = oracle.Oracle(c["bm"], c["tables"].vmax, c["tables"].sigma)
+    nthreads = nthreads or os.cpu_count() or 1
+    o.eval_candidates(c["assign"], c["cand"], None, net=True, stats=True, nthreads=nthreads)  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or not times:
+        t0 = time.perf_counter()
+        o.eval_candidates(c["assign"], c["cand"], None, net=True, stats=True, nthreads=nthreads)
+        times.append(time.perf_counter() - t0)
+        if max_batches and len(times) >= max_batches:
+            break
+    return times, nthreads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = build_inputs(args.config)
+    M, S = c["C"] * c["T"], c["S"]
+    from oracle import oracle
+
+    oracle.build()
+    o = oracle.Oracle(c["bm"], c["tables"].vmax, c["tables"].sigma)
+    nth = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    o.eval_candidates(c["assign"], c["cand"], None, net=True, stats=True, nthreads=nth)
+    one = time.perf_counter() - t0
+    budget = 150.0
+    frac = 1.0
+    if (args.steps + args.warmup) * one > budget:
+        frac = max(budget / ((args.steps + args.warmup) * one), 0.02)
+    n_c = max(1, int(round(c["C"] * frac)))
+    cand = c["cand"][:n_c]
+    for _ in range(args.warmup):
+        o.eval_candidates(c["assign"], cand, None, net=True, stats=True, nthreads=nth)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.eval_candidates(c["assign"], cand, None, net=True, stats=True, nthreads=nth)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    value = n_c * c["T"] * S / t
+    sample = (f"{n_c} of {c['C']} candidates x {c['T']} periods x {S} scenarios per step "
+              f"({'full batch' if n_c == c['C'] else 'bounded sample'}), incl. period masses")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "ms_per_250k_batch": t * 1e3 * (M / (n_c * c["T"])), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: 50k-block model, 15 periods, 20 scenarios, 16,667 candidates x 15 periods"
+                   if args.config == "C2" else args.config, "blocks": c["bm"].n_blocks, "periods": c["T"],
+                   "scenarios": S, "moves_per_batch": M, "net_mining_cost": True},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_gpu(args):
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_18296_b200.engine import Engine, PinnedPool
+
+    c = build_inputs(args.config, rank)
+    bm, T, S, C = c["bm"], c["T"], c["S"], c["C"]
+    M = C * T
+    dev = torch.device("cuda", local)
+    eng = Engine.from_tables(bm, c["tables"], c["assign"], device=local)
+    deg_mean = 2.0 * bm.n_edges / bm.n_blocks
+    # a dedicated stream: handle 0 (torch's legacy default stream) would mean "the engine
+    # context's own stream" to the C ABI, and events recorded on it would not order the kernels
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    assert sptr != 0
+
+    assign_d = torch.from_numpy(c["assign"].astype(np.int32)).to(dev)
+    cand_d = torch.from_numpy(c["cand"]).to(dev)
+    out = {
+        "best_t": torch.empty(C, dtype=torch.int32, device=dev),
+        "best_val": torch.empty(C, dtype=torch.float64, device=dev),
+        "feasible": torch.empty(C, dtype=torch.uint8, device=dev),
+        "exp_delta": torch.empty(C, T, dtype=torch.float64, device=dev),
+        "cvar": torch.empty(C, T, dtype=torch.float64, device=dev),
+        "global": torch.empty(2, dtype=torch.float64, device=dev),
+    }
+    gathered = torch.empty(2 * world, dtype=torch.float64, device=dev)
+    final = torch.empty(2, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    pm_copy = torch.empty(T, dtype=torch.float64, device=dev)
+
+    def step():
+        # the schedule is read in place; the call enqueues k_period_mass + k_eval_candidates (PDL)
+        eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
+        eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out["global"])
+            eng.reduce_best_device(gathered, final, stream=sptr)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+
+    graph = None
+    if world == 1 and not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cs = torch.cuda.current_stream().cuda_stream
+                eng.set_schedule_device(assign_d, stream=cs, borrow=True)
+                eng.eval_candidates_device(cand_d, out, None, net=True, stream=cs)
+            g.replay()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] graph capture failed, eager launches: {exc}", file=sys.stderr)
+            graph = None
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        time.sleep(0.05)
+        for i in range(args.steps):
+            flush.fill_(i)  # 256 MiB write: nothing of the previous step stays in the 126 MB L2
+            starts[i].record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.05)
+    if dist is not None:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_local = float(np.mean(step_ms))
+    t_max = t_local
+    if dist is not None:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+
+    # dominant kernel alone: k_eval_candidates timed with events on its stream, L2 flushed,
+    # period masses refreshed beforehand so the call launches only the evaluation kernel
+    kms = []
+    for i in range(min(args.steps, 200)):
+        flush.fill_(i)
+        eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
+        eng.period_mass_device(pm_copy, stream=sptr)
+        kstarts[i].record(stream)
+        eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
+        kends[i].record(stream)
+    torch.cuda.synchronize()
+    kms = [s.elapsed_time(e) for s, e in zip(kstarts[:min(args.steps, 200)], kends[:min(args.steps, 200)])]
+    k_ms = float(np.mean(kms))
+
+    result = None
+    if rank == 0:
+        hbm, peak_kind = _peaks()
+        ab = algorithmic_bytes(c, deg_mean)
+        achieved = ab["per_launch"] / (k_ms * 1e-3) / 1e9
+        value = world * M * S / (t_max * 1e-3)
+
+        # e2e through the C ABI with host (pinned) buffers: H2D schedule + candidates, D2H results
+        pool = PinnedPool()
+        h_assign = pool.empty(bm.n_blocks, np.int32)
+        h_assign[:] = c["assign"]
+        h_cand = pool.empty(C, np.int32)
+        h_cand[:] = c["cand"]
+        h_out = {"best_t": pool.empty(C, np.int32), "best_val": pool.empty(C, np.float64),
+                 "feasible": pool.empty(C, np.uint8), "exp_delta": pool.empty((C, T), np.float64),
+                 "cvar": pool.empty((C, T), np.float64)}
+        e2e = []
+        for i in range(args.warmup + min(args.steps, 300)):
+            flush.fill_(i)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.set_schedule(h_assign)
+            r = eng.eval_candidates(h_cand, None, net=True, stats=True, out=h_out, validate=False)
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                e2e.append(t1 - t0)
+        e2e_t = float(np.median(e2e))
+        h2d = h_assign.nbytes + h_cand.nbytes
+        d2h = sum(a.nbytes for a in h_out.values()) + 16
+        # parity spot check of the timed configuration against the device run
+        assert r["best"] is not None
+        g = out["global"].cpu().numpy()
+        gi = g.view(np.int32)
+        assert (int(gi[2]), int(gi[3]), float(g[0])) == r["best"], "device/host paths disagree"
+        pool.close()
+
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            ts, nth = cpu_reference(c, seconds=args.cpu_seconds)
+            t_cpu = float(np.median(ts))
+            cpu = {"value": M * S / t_cpu, "unit": UNIT, "cores": nth, "kind": "port",
+                   "sample": f"{len(ts)} full batches ({M} moves x {S} scenarios each, incl. period masses), "
+                             f"oracle/oracle.c with OpenMP, median"}
+        launches_per_step = 2 + (1 if world > 1 else 0)  # k_period_mass + k_eval_candidates [+ k_reduce_best]
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_max,
+            "ms_per_250k_batch": t_max * (250000.0 / M),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": ("C2: 50k-block model (50x50x20), 15 periods, 20 lognormal scenarios with sigma, "
+                             "16,667 candidate blocks x 15 periods = 250,005 moves per GPU per step, "
+                             "net mining cost, per-move expected delta + CVaR10, argmax")
+                if args.config == "C2" else args.config,
+                "blocks": bm.n_blocks, "periods": T, "scenarios": S, "candidates": C, "moves_per_batch": M,
+                "l2": "256 MiB flush write between timed steps",
+                "cuda_graph": graph is not None,
+            },
+            "roofline": {
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": hbm,
+                "unit": "GB/s",
+                "frac": achieved / hbm,
+                "traffic": args.ncu_traffic,
+                "kernel": "k_eval_candidates",
+                "kernel_ms": k_ms,
+                "algorithmic_bytes_per_launch": ab["per_launch"],
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "survey_uncached_bytes_per_launch": ab["survey_uncached"],
+            },
+            "e2e": {"value": M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_t * 1e3,
+                    "api": "Engine.set_schedule + Engine.eval_candidates (pp_set_schedule/pp_eval_candidates, PP_MEM_HOST, pinned)"},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "best_move": {"block": r["best"][0], "period": r["best"][1], "value": r["best"][2]},
+        }
+        print(json.dumps(result))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    ap.add_argument("--ncu-traffic", type=float, default=None,
+                    help="dram bytes per k_eval_candidates launch from the committed ncu capture")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

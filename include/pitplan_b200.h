@@ -49,6 +49,7 @@ extern "C" {
 
 #define PP_MEM_HOST 0
 #define PP_MEM_DEVICE 1
+#define PP_MEM_DEVICE_BORROW 2  /* pp_set_schedule only: read the caller's device buffer in place */
 
 /* evaluation flags (evaluate_candidates_parallel keyword arguments, evaluate.py:306-318) */
 #define PP_NET_MINING_COST 1u   /* net_mining_cost=True: value -= disc[t] * cost[b][t] */
@@ -138,8 +139,10 @@ PP_API int pp_set_scenarios(pp_ctx *ctx, int32_t n_scenarios, const double *vmax
                      const double *sigma_st);
 
 /* ---- schedule -------------------------------------------------------------------- */
-/* Upload assign[B] and recompute period_mass[t] = masses[assign == t].sum() bit-exactly
- * (numpy pairwise summation, evaluate.py:334-337). */
+/* Install assign[B] as the current schedule (copied, or borrowed in place with
+ * PP_MEM_DEVICE_BORROW until the next call).  period_mass[t] = masses[assign == t].sum()
+ * is recomputed bit-exactly (numpy pairwise summation, evaluate.py:334-337) by the next
+ * evaluation launch, overlapped with it through programmatic dependent launch. */
 PP_API int pp_set_schedule(pp_ctx *ctx, const int32_t *assign, int32_t mem, void *stream);
 /* Apply accepted deltas assign[blocks[k]] = periods[k] and recompute period_mass. */
 PP_API int pp_apply_moves(pp_ctx *ctx, const int32_t *blocks, const int32_t *periods, int32_t n,
@@ -172,6 +175,12 @@ PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode
  * deterministic "allreduce-argmax" step of multi-GPU evaluation. */
 PP_API int pp_reduce_best(pp_ctx *ctx, const pp_best *records, int32_t n, pp_best *out, int32_t mem,
                           void *stream);
+/* Linear expected-NPV table enpv[B][T] of the current scenario set:
+ * factored = 0: disc[t]*mean_s(sig[s][t]*vmax[s][b]) - disc[t]*cost[b][t]  (colgen.py:187-204)
+ * factored = 1: disc[t]*(mean_s(sig[s][t]*vmax[s][b]) - cost[b][t])        (hybrid.py:673-678,
+ *               saa.py:65-69); sig = ones unless PP_USE_SIGMA. */
+PP_API int pp_enpv_table(pp_ctx *ctx, uint32_t flags, int32_t factored, double *out, int32_t mem,
+                         void *stream);
 /* Topological level of every block (longest predecessor chain), host output. */
 PP_API int pp_get_levels(pp_ctx *ctx, int32_t *n_levels, int32_t *level_of_block);
 

@@ -548,3 +548,23 @@ void or_eval_moves(int32_t B, int32_t T, int32_t S, const int32_t *pp, const int
     *g_val = gv;
     *g_index = gi;
 }
+
+/* Linear ENPV table, [B][T]:
+ *   factored = 0: disc[t] * mean_s(sig[s][t] * v[s][b]) - disc[t] * cost[b][t]   (colgen.py:187-204)
+ *   factored = 1: disc[t] * (mean_s(sig[s][t] * v[s][b]) - cost[b][t])           (hybrid.py:673-678)
+ * mean_s = numpy .mean(axis=0) of the [S][B] product array: sequential in s, then / S. */
+void or_enpv_table(int32_t B, int32_t T, int32_t S, const double *vmax, const double *sigma,
+                   const double *disc, const double *cost, int32_t factored, double *out) {
+    for (int32_t b = 0; b < B; b++) {
+        for (int32_t t = 0; t < T; t++) {
+            double acc = 0.0;
+            for (int32_t s = 0; s < S; s++) {
+                double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
+                acc += sg * vmax[(size_t)s * B + b];
+            }
+            double mean = acc / (double)S;
+            double c = cost[(size_t)b * T + t];
+            out[(size_t)b * T + t] = factored ? disc[t] * (mean - c) : disc[t] * mean - disc[t] * c;
+        }
+    }
+}

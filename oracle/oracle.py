@@ -45,6 +45,7 @@ _SIGS = {
     "or_topological_order": (ctypes.c_int, [_i32, _P, _P, _P, _P]),
     "or_precedence_repair": (None, [_i32, _P, _P, _P, _P]),
     "or_unmine_fixpoint": (None, [_i32, _i64, _P, _P, _P, _P]),
+    "or_enpv_table": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _i32, _P]),
     "or_eval_moves": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                              _P, _P, _P, _P, _i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _i32]),
 }
@@ -211,6 +212,14 @@ class Oracle:
         if scen:
             res["scen_delta"] = sd
         return res
+
+    # -- linear ENPV table (colgen.py:187-204; hybrid.py:673-678) -------------------------
+    def enpv_table(self, use_sigma=True, factored=False) -> np.ndarray:
+        out = np.empty((self.B, self.T), np.float64)
+        sig = self.sigma if use_sigma else None
+        lib().or_enpv_table(self.B, self.T, self.S, _p(self.vmax), _p(sig), _p(self.disc), _p(self.cost),
+                            int(bool(factored)), _p(out))
+        return out
 
     # -- check_feasible (evaluate.py:82-105) ------------------------------------------
     def check_feasible(self, assign):

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 PP_MEM_HOST = 0
 PP_MEM_DEVICE = 1
+PP_MEM_DEVICE_BORROW = 2
 PP_NET_MINING_COST = 1
 PP_LITERAL_VALUE = 2
 PP_USE_SIGMA = 4
@@ -91,6 +92,7 @@ SIGNATURES = {
                                     c_int32, c_void_p]),
     "pp_repair": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
+    "pp_enpv_table": (c_int32, [c_void_p, c_uint32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_get_levels": (c_int32, [c_void_p, ctypes.POINTER(c_int32), c_void_p]),
 }
 

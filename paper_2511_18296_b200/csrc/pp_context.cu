@@ -1,0 +1,133 @@
+// pp_context.cu -- error channel, device context and library entry points of the C ABI.
+//
+// Translation units of libpitplan_b200.so (C ABI: include/pitplan_b200.h):
+//   pp_context.cu   error channel, device context, shared host helpers
+//   pp_schedule.cu  period masses (numpy pairwise tree, bit-exact), check_feasible,
+//                   topological-wave repair, table preparation (geology, scenario tables,
+//                   linear ENPV), accepted-move application, ordered argmax reduce
+//   pp_eval.cu      evaluate_candidates_parallel: staged fast path + general kernel
+//   pp_moves.cu     explicit reassign / unmine / swap moves
+//
+// All float arithmetic on the value path uses explicit round-to-nearest intrinsics and the
+// library is compiled with -fmad=false: no multiply-add is ever contracted, so every double
+// matches the reference's numpy/Python scalar evaluation bit for bit.
+
+#include "pp_internal.cuh"
+
+// ------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+
+int ensure_grid_scratch(pp_ctx *c, int grid) {
+    TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
+    if (c->counter.bytes == 0) {
+        TRY(c->counter.ensure(sizeof(unsigned int) * 4));
+        CUDA_TRY(cudaMemset(c->counter.ptr, 0, c->counter.bytes));
+    }
+    return PP_OK;
+}
+
+
+int pick_kc(int k) {
+    if (k <= 2) return 2;
+    if (k <= 8) return 8;
+    if (k <= 128) return 128;
+    return -1;
+}
+
+int check_ready(pp_ctx *c, uint32_t flags, int scenario) {
+    if (!c) return fail(PP_ERR_INVALID_ARGS, "NULL context");
+    if (!c->have_instance || !c->have_spatial) return fail(PP_ERR_STATE, "pp_set_instance and pp_set_geology first");
+    if (!c->have_sched) return fail(PP_ERR_STATE, "pp_set_schedule first");
+    if (!c->have_scen && !(flags & PP_LITERAL_VALUE)) return fail(PP_ERR_STATE, "pp_set_scenarios first");
+    if ((flags & PP_USE_SIGMA) && !c->have_sigma) return fail(PP_ERR_STATE, "PP_USE_SIGMA without an uploaded sigma");
+    if (scenario < -1 || (c->have_scen && scenario >= c->S) || (!c->have_scen && scenario >= 0))
+        return fail(PP_ERR_INVALID_ARGS, "scenario %d out of range", scenario);
+    return PP_OK;
+}
+
+
+extern "C" {
+
+int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+const char *pp_last_error(void) { return g_last_error.c_str(); }
+
+int pp_device_count(int *count) {
+    if (!count) return fail(PP_ERR_INVALID_ARGS, "count is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(PP_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    }
+    *count = n;
+    return PP_OK;
+}
+
+int pp_ctx_create(int device, pp_ctx **out) {
+    if (!out) return fail(PP_ERR_INVALID_ARGS, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    TRY(pp_device_count(&n));
+    if (device < 0 || device >= n) return fail(PP_ERR_INVALID_ARGS, "device %d out of range (%d devices)", device, n);
+    pp_ctx *c = new (std::nothrow) pp_ctx();
+    if (!c) return fail(PP_ERR_CUDA, "out of host memory");
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(PP_ERR_CUDA, "context init: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return PP_OK;
+}
+
+int pp_ctx_destroy(pp_ctx *c) {
+    if (!c) return PP_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf *b : c->all()) b->release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return PP_OK;
+}
+
+int pp_ctx_stream(pp_ctx *c, void **stream) {
+    if (!c || !stream) return fail(PP_ERR_INVALID_ARGS, "NULL argument");
+    *stream = (void *)c->stream;
+    return PP_OK;
+}
+
+int pp_synchronize(pp_ctx *c, void *stream) {
+    if (!c) return fail(PP_ERR_INVALID_ARGS, "NULL context");
+    TRY(use_device(c));
+    CUDA_TRY(cudaStreamSynchronize(pick(c, stream)));
+    return PP_OK;
+}
+
+int pp_host_alloc(size_t bytes, void **ptr) {
+    if (!ptr) return fail(PP_ERR_INVALID_ARGS, "ptr is NULL");
+    CUDA_TRY(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+    return PP_OK;
+}
+
+int pp_host_free(void *ptr) {
+    if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+    return PP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,458 @@
+// pp_internal.cuh -- shared device helpers, parameter blocks and the host context of the
+// pitplan_b200 engine (included by every translation unit of the library).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "pitplan_b200.h"
+
+// last-error channel of the C ABI (pp_context.cu)
+int fail(int code, const char *fmt, ...);
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(PP_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+#define TRY(expr)                    \
+    do {                             \
+        int rc_ = (expr);            \
+        if (rc_ != PP_OK) return rc_; \
+    } while (0)
+
+
+// ------------------------------------------------------------------------------------
+// device helpers: IEEE binary64, round-to-nearest, never contracted
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double f64_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double f64_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double f64_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double f64_div(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ double tree8(const double r[8]) {
+    // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))   (numpy pairwise block combine)
+    return f64_add(f64_add(f64_add(r[0], r[1]), f64_add(r[2], r[3])), f64_add(f64_add(r[4], r[5]), f64_add(r[6], r[7])));
+}
+
+constexpr double kInf = __builtin_huge_val();
+
+// Per-block static record: one 32-byte load gives mass, spatial factor and adjacency.
+struct __align__(16) BlockRow {
+    double mass;
+    double spatial;
+    int32_t adj;  // offset into adj[]: predecessors then successors, reference order
+    int32_t cnt;  // npred | nsucc << 16
+    int32_t level;
+    int32_t pad;
+};
+
+// numpy pairwise-sum plan for a fixed length n: leaves in order, plus the number of
+// post-order additions that follow each leaf.
+constexpr int kMaxLeaves = 32;
+struct PwPlan {
+    int n;
+    int nleaf;
+    int start[kMaxLeaves];
+    int len[kMaxLeaves];
+    int adds[kMaxLeaves];
+};
+
+// Device copy of a PwPlan: int words [n, nleaf, start[kMaxLeaves], len[kMaxLeaves], adds[kMaxLeaves]].
+constexpr int kPlanWords = 2 + 3 * kMaxLeaves;
+
+// Streaming numpy pairwise sum over x[0..n), fed 8 values at a time in order.  Every leaf
+// of numpy's recursion starts at a multiple of 8 and all but the last end on one, and the
+// 8-accumulator part of a leaf covers whole 8-blocks, so each 8-block is either entirely
+// "main" (accumulator j gets element j of the block) or entirely remainder.
+struct PwStream {
+    double r[8];
+    double res;
+    double stk[8];
+    int sp, leaf, nleaf, ls, le, lmain;
+
+    __device__ __forceinline__ void set_leaf(const int *P) {
+        ls = __ldg(P + 2 + leaf);
+        int L = __ldg(P + 2 + kMaxLeaves + leaf);
+        le = ls + L;
+        lmain = (L >= 8) ? ls + L - (L & 7) : ls;
+        res = -0.0;
+    }
+    __device__ __forceinline__ void begin(const int *P) {
+        sp = 0;
+        leaf = 0;
+        nleaf = __ldg(P + 1);
+        set_leaf(P);
+    }
+    // x[0..nvalid) are elements s8 .. s8+nvalid-1 (s8 a multiple of 8)
+    __device__ __forceinline__ void block(int s8, const double x[8], int nvalid, const int *P) {
+        if (s8 < lmain) {
+            if (s8 == ls) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = x[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = f64_add(r[j], x[j]);
+            }
+            if (s8 + 8 == lmain) res = tree8(r);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < nvalid) res = f64_add(res, x[j]);
+        }
+        if (s8 + 8 >= le) finish(P);
+    }
+    __device__ __forceinline__ void finish(const int *P) {
+        stk[sp++] = res;
+        const int nadd = __ldg(P + 2 + 2 * kMaxLeaves + leaf);
+        for (int a = 0; a < nadd; a++) {
+            double rhs = stk[--sp];
+            double lhs = stk[--sp];
+            stk[sp++] = f64_add(lhs, rhs);
+        }
+        leaf++;
+        if (leaf < nleaf) set_leaf(P);
+    }
+    // float(np.mean(x)) = (0.0 + pairwise(x)) / n
+    __device__ __forceinline__ double mean(const int *P) const { return f64_div(f64_add(0.0, stk[0]), (double)__ldg(P)); }
+};
+
+// k smallest values seen (ascending), for CVaR10 (saa.py:157-164).
+template <int KC>
+struct TopK {
+    double a[KC];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int j = 0; j < KC; j++) a[j] = kInf;
+    }
+    __device__ __forceinline__ void push(double x) {
+        if (x < a[KC - 1]) {
+            if constexpr (KC <= 8) {
+#pragma unroll
+                for (int j = KC - 1; j > 0; j--) a[j] = (x < a[j - 1]) ? a[j - 1] : ((x < a[j]) ? x : a[j]);
+                a[0] = (x < a[0]) ? x : a[0];
+            } else {  // insertion sort step in local memory
+                int j = KC - 1;
+                while (j > 0 && x < a[j - 1]) {
+                    a[j] = a[j - 1];
+                    j--;
+                }
+                a[j] = x;
+            }
+        }
+    }
+    // float(srt[:k].mean()) = (0.0 + pairwise(a[0..k))) / k,  k <= 128
+    __device__ __forceinline__ double mean(int k) const {
+        double s;
+        if (k < 8) {
+            s = -0.0;
+#pragma unroll
+            for (int j = 0; j < KC; j++)
+                if (j < k) s = f64_add(s, a[j]);
+        } else {
+            double r[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = a[j < KC ? j : 0];
+            int main_ = k - (k & 7);
+            for (int i = 8; i < main_; i += 8)
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = f64_add(r[j], a[(i + j) < KC ? (i + j) : 0]);
+            s = tree8(r);
+            for (int i = main_; i < k; i++) s = f64_add(s, a[i < KC ? i : 0]);
+        }
+        return f64_div(f64_add(0.0, s), (double)k);
+    }
+};
+template <>
+struct TopK<2> {  // k <= 2 (S <= 20): two registers, insertion rarely taken
+    double a0, a1;
+    __device__ __forceinline__ void init() { a0 = a1 = kInf; }
+    __device__ __forceinline__ void push(double x) {
+        if (x < a1) {
+            if (x < a0) {
+                a1 = a0;
+                a0 = x;
+            } else {
+                a1 = x;
+            }
+        }
+    }
+    __device__ __forceinline__ double mean(int k) const {
+        double s = f64_add(-0.0, a0);
+        if (k > 1) s = f64_add(s, a1);
+        return f64_div(f64_add(0.0, s), (double)k);
+    }
+};
+template <>
+struct TopK<0> {
+    __device__ __forceinline__ void init() {}
+    __device__ __forceinline__ void push(double) {}
+    __device__ __forceinline__ double mean(int) const { return 0.0; }
+};
+
+// selection order of evaluate.py:404-409: value desc, then block asc, then period asc
+struct Best {
+    double v;
+    int b;
+    int t;
+};
+__device__ __forceinline__ bool better(const Best &x, const Best &y) {
+    return x.v > y.v || (x.v == y.v && (x.b < y.b || (x.b == y.b && x.t < y.t)));
+}
+__device__ __forceinline__ Best shfl_best(const Best &x, int off) {
+    Best y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, off);
+    y.b = __shfl_xor_sync(0xffffffffu, x.b, off);
+    y.t = __shfl_xor_sync(0xffffffffu, x.t, off);
+    return y;
+}
+
+// CTA argmax of per-thread candidates in smem, then the last CTA to finish reduces the
+// per-CTA partials in index order.  Deterministic: `better` is a total order.
+static __device__ void grid_argmax(Best mine, Best *s_red, pp_best *partial, unsigned int *counter,
+                            pp_best *global) {
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Best o = shfl_best(mine, off);
+        if (better(o, mine)) mine = o;
+    }
+    if (lane == 0) s_red[warp] = mine;
+    __syncthreads();
+    if (warp == 0) {
+        Best x = (lane < nw) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Best o = shfl_best(x, off);
+            if (better(o, x)) x = o;
+        }
+        if (lane == 0) {
+            pp_best pb;
+            pb.value = x.v;
+            pb.block = x.b;
+            pb.period = x.t;
+            partial[blockIdx.x] = pb;
+            __threadfence();
+            unsigned int prev = atomicAdd(counter, 1u);
+            s_last = (prev == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    Best x{-kInf, INT_MAX, INT_MAX};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const pp_best *q = partial + i;
+        Best o{__ldcg(&q->value), __ldcg(&q->block), __ldcg(&q->period)};
+        if (better(o, x)) x = o;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Best o = shfl_best(x, off);
+        if (better(o, x)) x = o;
+    }
+    if (lane == 0) s_red[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Best y = s_red[0];
+        for (int w = 1; w < nw; w++)
+            if (better(s_red[w], y)) y = s_red[w];
+        pp_best g;
+        bool none = (y.b == INT_MAX);
+        g.value = none ? -kInf : y.v;
+        g.block = none ? -1 : y.b;
+        g.period = none ? -1 : y.t;
+        *global = g;
+        *counter = 0u;  // re-arm for the next launch (graph replay safe)
+    }
+}
+
+
+// ------------------------------------------------------------------------------------
+// kernel parameter blocks
+// ------------------------------------------------------------------------------------
+struct EvalParams {
+    const BlockRow *rows;
+    const int32_t *adj;
+    const int32_t *assign;
+    const double *pm;
+    const double *cap;
+    const double *disc;
+    const double *cost;      // [B][T]
+    const double *vmax;      // [B][Sp]
+    const double *unit_mean; // [B]
+    const double *sig_row;   // [T] (ones / scenario mean / sigma[k])
+    const double *sigma;     // [S][T] (ones if no sigma)
+    const int32_t *cand;
+    int C, B, T, S, Sp, scen, cvar_k;
+    unsigned flags;
+    const int *plan;
+    int32_t *best_t;
+    double *best_val;
+    uint8_t *feas;
+    double *trace_val;
+    uint8_t *trace_feas;
+    double *exp_delta;
+    double *cvar;
+    float *scen_delta;
+    pp_best *partial;
+    unsigned int *counter;
+    pp_best *global;
+};
+
+constexpr int EV_THREADS = 256;
+
+struct MoveParams {
+    const BlockRow *rows;
+    const int32_t *adj;
+    const int32_t *assign;
+    const double *pm;
+    const double *cap;
+    const double *disc;
+    const double *cost;
+    const double *vmax;
+    const double *unit_mean;
+    const double *sig_row;
+    const double *sigma;
+    const int32_t *ma;
+    const int32_t *mb;
+    int M, B, T, S, Sp, scen, cvar_k, kind;
+    unsigned flags;
+    const int *plan;
+    uint8_t *feas;
+    double *delta;
+    double *exp_delta;
+    double *cvar;
+    float *scen_delta;
+    pp_best *partial;
+    unsigned int *counter;
+    pp_best *global;
+};
+
+// ------------------------------------------------------------------------------------
+// host side: context
+// ------------------------------------------------------------------------------------
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t need) {
+        if (need <= bytes) return PP_OK;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        size_t n = std::max<size_t>(need, 256);
+        CUDA_TRY(cudaMalloc(&ptr, n));
+        bytes = n;
+        return PP_OK;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T *as() const {
+        return reinterpret_cast<T *>(ptr);
+    }
+};
+
+struct pp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int B = 0, T = 0, S = 0, Sp = 0, n_levels = 0, deg_max = 0;
+    long long E = 0;
+    bool have_instance = false, have_spatial = false, have_scen = false, have_sigma = false, have_sched = false;
+    double mean_cap = 0.0;
+    std::vector<int> level_ptr;  // host, n_levels + 1
+    std::vector<int> level_of;   // host, B
+    PwPlan plan{};
+    int cvar_k = 1;
+    // static tables
+    DevBuf rows, adj, cost, cap, disc, level_blocks, ones_t, mass;
+    const int32_t *assign_ptr = nullptr;  // current schedule (own buffer or a borrowed device buffer)
+    bool borrowed = false;
+    bool pm_dirty = true;
+    DevBuf vmax, unit_mean, sigma, sig_mean, ones_st, plan_dev;
+    // schedule
+    DevBuf assign, pm;
+    // scratch
+    DevBuf cnt, compact, pm_batch, predcnt, partial, counter, pm_flags;
+    size_t pm_flags_n = 0;
+    DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
+        h_pm;
+    std::vector<DevBuf *> all() {
+        return {&rows, &adj, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
+                &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
+                &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
+                &h_d2, &h_pm};
+    }
+};
+
+inline int use_device(pp_ctx *c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    return PP_OK;
+}
+
+inline cudaStream_t pick(pp_ctx *c, void *stream) { return stream ? (cudaStream_t)stream : c->stream; }
+
+// host copy of numpy's pairwise sum (for np.mean(capacity), evaluate.py:103)
+inline double host_pairwise(const double *a, long n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (long i = 0; i < n; i++) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        long i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    }
+    long n2 = n / 2;
+    n2 -= n2 % 8;
+    return host_pairwise(a, n2) + host_pairwise(a + n2, n - n2);
+}
+
+// launch with programmatic stream serialization (PDL) when a period-mass kernel precedes
+template <typename... KArgs, typename... Args>
+inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(EV_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return PP_OK;
+}
+
+
+// ---- shared host helpers (pp_context.cu, pp_schedule.cu) ----
+int ensure_grid_scratch(pp_ctx *c, int grid);
+int check_ready(pp_ctx *c, uint32_t flags, int scenario);
+int pick_kc(int k);
+int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st);
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched);

@@ -1,0 +1,265 @@
+// pp_moves.cu -- explicit reassign / unmine / swap move evaluation and pp_eval_moves.
+#include "pp_internal.cuh"
+
+// ------------------------------------------------------------------------------------
+// explicit moves (reassign / unmine / swap), one thread per move
+// ------------------------------------------------------------------------------------
+
+__device__ __forceinline__ double kernel_value(const MoveParams &p, const BlockRow &r, int b, int t) {
+    double unit;
+    if (p.flags & PP_LITERAL_VALUE) unit = f64_mul(r.mass, 100.0);
+    else if (p.scen < 0) unit = __ldg(p.unit_mean + b);
+    else unit = __ldg(p.vmax + (size_t)b * p.Sp + p.scen);
+    double d = __ldg(p.disc + t);
+    double v = f64_mul(f64_mul(f64_mul(unit, d), __ldg(p.sig_row + t)), r.spatial);
+    if (p.flags & PP_NET_MINING_COST) v = f64_sub(v, f64_mul(d, __ldg(p.cost + (size_t)b * p.T + t)));
+    return v;
+}
+
+__device__ __forceinline__ double scen_value(const MoveParams &p, const BlockRow &r, int b, int t, int s) {
+    double d = __ldg(p.disc + t);
+    double v = f64_mul(f64_mul(f64_mul(__ldg(p.vmax + (size_t)b * p.Sp + s), d), __ldg(p.sigma + (size_t)s * p.T + t)),
+                    r.spatial);
+    if (p.flags & PP_NET_MINING_COST) v = f64_sub(v, f64_mul(d, __ldg(p.cost + (size_t)b * p.T + t)));
+    return v;
+}
+
+// window(b) of hybrid.py:348-355 with block `ob` seen at period `ot`; lo = -2 encodes None
+__device__ __forceinline__ void move_window(const MoveParams &p, const BlockRow &r, int ob, int ot, int &lo,
+                                            int &hi) {
+    const int npred = r.cnt & 0xffff, nnb = npred + (r.cnt >> 16);
+    int l = 0, h = p.T - 1;
+    bool none = false;
+    for (int k = 0; k < nnb; k++) {
+        int nb = __ldg(p.adj + r.adj + k);
+        int tn = (nb == ob) ? ot : p.assign[nb];
+        if (k < npred) {
+            if (tn < 0) none = true;
+            else l = max(l, tn);
+        } else if (tn >= 0) {
+            h = min(h, tn);
+        }
+    }
+    lo = none ? -2 : l;
+    hi = h;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(EV_THREADS) k_eval_moves(const MoveParams p) {
+    __shared__ Best s_red[EV_THREADS / 32];
+    const int i = blockIdx.x * EV_THREADS + threadIdx.x;
+    const bool active = i < p.M;
+    bool ok = false;
+    double dl = -kInf;
+    int b1 = 0, b2 = 0, t1 = -1, t2 = -1;
+    BlockRow r1, r2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (active) {
+        const int x = p.ma[i], y = p.mb[i];
+        if (p.kind == PP_MOVE_REASSIGN) {
+            if (x >= 0 && x < p.B && y >= -1 && y < p.T) {
+                b1 = x;
+                r1 = p.rows[b1];
+                t1 = p.assign[b1];  // old period
+                t2 = y;             // new period
+                const int npred = r1.cnt & 0xffff, nnb = npred + (r1.cnt >> 16);
+                if (t2 == t1) {
+                    ok = false;
+                } else if (t2 < 0) {  // unmine: allowed iff mined and no mined successor
+                    ok = true;
+                    for (int k = npred; k < nnb; k++)
+                        if (p.assign[__ldg(p.adj + r1.adj + k)] >= 0) ok = false;
+                } else {
+                    ok = true;
+                    for (int k = 0; k < nnb; k++) {
+                        int tn = p.assign[__ldg(p.adj + r1.adj + k)];
+                        if (k < npred) {
+                            if (tn < 0 || tn > t2) ok = false;
+                        } else if (tn >= 0 && tn < t2) {
+                            ok = false;
+                        }
+                    }
+                    if (ok) {
+                        double load = f64_add(__ldcg(p.pm + t2), r1.mass);
+                        if (load > __ldg(p.cap + t2)) ok = false;
+                    }
+                }
+                if (ok) {
+                    double vn = (t2 >= 0) ? kernel_value(p, r1, b1, t2) : 0.0;
+                    double vo = (t1 >= 0) ? kernel_value(p, r1, b1, t1) : 0.0;
+                    dl = f64_sub(vn, vo);
+                }
+            }
+        } else {
+            if (x >= 0 && x < p.B && y >= 0 && y < p.B && x != y) {
+                b1 = x;
+                b2 = y;
+                r1 = p.rows[b1];
+                r2 = p.rows[b2];
+                t1 = p.assign[b1];
+                t2 = p.assign[b2];
+                if (t1 >= 0 && t2 >= 0 && t1 != t2) {
+                    double l1 = f64_add(f64_sub(__ldcg(p.pm + t1), r1.mass), r2.mass);
+                    double l2 = f64_add(f64_sub(__ldcg(p.pm + t2), r2.mass), r1.mass);
+                    if (!(l1 > __ldg(p.cap + t1)) && !(l2 > __ldg(p.cap + t2))) {
+                        int lo1, hi1, lo2, hi2;
+                        move_window(p, r1, b2, t1, lo1, hi1);
+                        move_window(p, r2, b1, t2, lo2, hi2);
+                        ok = lo1 != -2 && lo1 <= t2 && t2 <= hi1 && lo2 != -2 && lo2 <= t1 && t1 <= hi2;
+                    }
+                }
+                if (ok) {
+                    double v12 = kernel_value(p, r1, b1, t2), v11 = kernel_value(p, r1, b1, t1);
+                    double v21 = kernel_value(p, r2, b2, t1), v22 = kernel_value(p, r2, b2, t2);
+                    dl = f64_add(f64_sub(v12, v11), f64_sub(v21, v22));
+                }
+            }
+        }
+        p.feas[i] = ok ? 1 : 0;
+        p.delta[i] = dl;
+    }
+    if constexpr (KC > 0) {
+        if (active && (p.exp_delta || p.cvar || p.scen_delta)) {
+            const int S = p.S;
+            if (ok) {
+                PwStream acc;
+                acc.begin(p.plan);
+                TopK<KC> tk;
+                tk.init();
+                for (int s8 = 0; s8 < S; s8 += 8) {
+                    double x[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const int s = s8 + j;
+                        double ds = 0.0;
+                        if (s < S) {
+                            if (p.kind == PP_MOVE_REASSIGN) {
+                                ds = (t2 >= 0) ? scen_value(p, r1, b1, t2, s) : 0.0;
+                                if (t1 >= 0) ds = f64_sub(ds, scen_value(p, r1, b1, t1, s));
+                            } else {
+                                ds = f64_add(f64_sub(scen_value(p, r1, b1, t2, s), scen_value(p, r1, b1, t1, s)),
+                                             f64_sub(scen_value(p, r2, b2, t1, s), scen_value(p, r2, b2, t2, s)));
+                            }
+                            tk.push(ds);
+                            if (p.scen_delta) p.scen_delta[(size_t)i * S + s] = (float)ds;
+                        }
+                        x[j] = ds;
+                    }
+                    acc.block(s8, x, min(8, S - s8), p.plan);
+                }
+                if (p.exp_delta) p.exp_delta[i] = acc.mean(p.plan);
+                if (p.cvar) p.cvar[i] = tk.mean(p.cvar_k);
+            } else {
+                if (p.exp_delta) p.exp_delta[i] = -kInf;
+                if (p.cvar) p.cvar[i] = -kInf;
+                if (p.scen_delta)
+                    for (int s = 0; s < S; s++) p.scen_delta[(size_t)i * S + s] = -__int_as_float(0x7f800000);
+            }
+        }
+    }
+    Best mine{-kInf, INT_MAX, INT_MAX};
+    if (active && ok) mine = Best{dl, i, -1};
+    grid_argmax(mine, s_red, p.partial, p.counter, p.global);
+}
+
+
+extern "C" {
+
+int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, int32_t M, int32_t scenario,
+                  uint32_t flags, const pp_move_out *out, int32_t mem, void *stream) {
+    TRY(check_ready(c, flags, scenario));
+    if (kind != PP_MOVE_REASSIGN && kind != PP_MOVE_SWAP) return fail(PP_ERR_INVALID_ARGS, "unknown move kind %d", kind);
+    if (M < 0 || (M > 0 && (!a || !b))) return fail(PP_ERR_INVALID_ARGS, "bad move arrays");
+    if (!out || !out->feasible || !out->delta || !out->global)
+        return fail(PP_ERR_INVALID_ARGS, "feasible, delta and global outputs are required");
+    const bool stats = out->exp_delta || out->cvar || out->scen_delta;
+    if (stats && !c->have_scen) return fail(PP_ERR_STATE, "scenario statistics need pp_set_scenarios");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int T = c->T, S = c->S;
+    const int grid = std::max(1, (M + EV_THREADS - 1) / EV_THREADS);
+    TRY(ensure_grid_scratch(c, grid));
+    const int kc = stats ? pick_kc(c->cvar_k) : 0;
+    if (kc < 0) return fail(PP_ERR_INVALID_ARGS, "CVaR sample count %d too large", c->cvar_k);
+    pp_move_out o = *out;
+    const int32_t *da = a, *db = b;
+    if (mem == PP_MEM_HOST) {
+        const size_t Ms = (size_t)std::max(M, 1);
+        TRY(c->h_a.ensure(sizeof(int32_t) * Ms));
+        TRY(c->h_b.ensure(sizeof(int32_t) * Ms));
+        TRY(c->h_o3.ensure(Ms));
+        TRY(c->h_o2.ensure(sizeof(double) * Ms));
+        TRY(c->h_glob.ensure(sizeof(pp_best)));
+        o.feasible = c->h_o3.as<uint8_t>();
+        o.delta = c->h_o2.as<double>();
+        o.global = c->h_glob.as<pp_best>();
+        if (out->exp_delta) { TRY(c->h_o6.ensure(sizeof(double) * Ms)); o.exp_delta = c->h_o6.as<double>(); }
+        if (out->cvar) { TRY(c->h_o7.ensure(sizeof(double) * Ms)); o.cvar = c->h_o7.as<double>(); }
+        if (out->scen_delta) { TRY(c->h_o8.ensure(sizeof(float) * Ms * std::max(S, 1))); o.scen_delta = c->h_o8.as<float>(); }
+        if (M > 0) {
+            CUDA_TRY(cudaMemcpyAsync(c->h_a.ptr, a, sizeof(int32_t) * M, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(c->h_b.ptr, b, sizeof(int32_t) * M, cudaMemcpyHostToDevice, st));
+        }
+        da = c->h_a.as<int32_t>();
+        db = c->h_b.as<int32_t>();
+    }
+    MoveParams mp;
+    memset(&mp, 0, sizeof(mp));
+    mp.rows = c->rows.as<BlockRow>();
+    mp.adj = c->adj.as<int32_t>();
+    mp.assign = c->assign_ptr;
+    mp.pm = c->pm.as<double>();
+    mp.cap = c->cap.as<double>();
+    mp.disc = c->disc.as<double>();
+    mp.cost = c->cost.as<double>();
+    mp.vmax = c->have_scen ? c->vmax.as<double>() : nullptr;
+    mp.unit_mean = c->have_scen ? c->unit_mean.as<double>() : nullptr;
+    if (!(flags & PP_USE_SIGMA)) mp.sig_row = c->ones_t.as<double>();
+    else if (scenario < 0) mp.sig_row = c->sig_mean.as<double>();
+    else mp.sig_row = c->sigma.as<double>() + (size_t)scenario * T;
+    mp.sigma = (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : c->ones_st.as<double>();
+    mp.ma = da;
+    mp.mb = db;
+    mp.M = M;
+    mp.B = c->B;
+    mp.T = T;
+    mp.S = S;
+    mp.Sp = c->Sp;
+    mp.scen = scenario;
+    mp.cvar_k = c->cvar_k;
+    mp.kind = kind;
+    mp.flags = flags;
+    mp.plan = c->plan_dev.as<int>();
+    mp.feas = o.feasible;
+    mp.delta = o.delta;
+    mp.exp_delta = o.exp_delta;
+    mp.cvar = o.cvar;
+    mp.scen_delta = o.scen_delta;
+    mp.partial = c->partial.as<pp_best>();
+    mp.counter = c->counter.as<unsigned int>();
+    mp.global = o.global;
+    bool pdl;
+    TRY(refresh_pm(c, st, &pdl));
+    switch (kc) {
+        case 0: TRY(launch_eval(k_eval_moves<0>, grid, 0, st, pdl, mp)); break;
+        case 2: TRY(launch_eval(k_eval_moves<2>, grid, 0, st, pdl, mp)); break;
+        case 8: TRY(launch_eval(k_eval_moves<8>, grid, 0, st, pdl, mp)); break;
+        default: TRY(launch_eval(k_eval_moves<128>, grid, 0, st, pdl, mp)); break;
+    }
+    if (mem == PP_MEM_HOST) {
+        const size_t Ms = (size_t)M;
+        CUDA_TRY(cudaMemcpyAsync(out->global, o.global, sizeof(pp_best), cudaMemcpyDeviceToHost, st));
+        if (M > 0) {
+            CUDA_TRY(cudaMemcpyAsync(out->feasible, o.feasible, Ms, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(out->delta, o.delta, sizeof(double) * Ms, cudaMemcpyDeviceToHost, st));
+            if (out->exp_delta) CUDA_TRY(cudaMemcpyAsync(out->exp_delta, o.exp_delta, sizeof(double) * Ms, cudaMemcpyDeviceToHost, st));
+            if (out->cvar) CUDA_TRY(cudaMemcpyAsync(out->cvar, o.cvar, sizeof(double) * Ms, cudaMemcpyDeviceToHost, st));
+            if (out->scen_delta)
+                CUDA_TRY(cudaMemcpyAsync(out->scen_delta, o.scen_delta, sizeof(float) * Ms * S, cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,946 @@
+// pp_schedule.cu -- schedule-side kernels: bit-exact period masses (numpy pairwise tree),
+// check_feasible, topological-wave repair, table preparation, and their C-ABI entry points.
+#include "pp_internal.cuh"
+
+// ------------------------------------------------------------------------------------
+// period mass, bit-exact numpy pairwise summation per period (evaluate.py:334-337)
+//
+// k_pm_chunks (P1): CTA c of schedule p owns blocks [c*512, (c+1)*512): one coalesced load
+//   of assign and mass per thread; the rank of a block among same-period blocks is
+//   (lower warps' count) + popc(match_any & lanemask_lt) -- stable, block order.  The CTA
+//   publishes its per-period counts, looks back over the published counts of lower chunks
+//   (all P1 CTAs are resident once they have triggered their PDL dependents), and
+//   scatters masses into per-period compacted arrays compact[p][t][.].
+// k_pm_tree (P2): one CTA per (period, schedule): numpy's recursion laid out as a heap
+//   (node id, children 2id+1 | 2id+2); in units of 8-blocks a node of m blocks splits
+//   floor(m/2) | ceil(m/2), leaves hold <= 128 elements.  Built level-parallel top-down,
+//   leaf sums with 8 lanes per leaf (lane j = accumulator j, a butterfly reproduces
+//   ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), then folded level-parallel bottom-up:
+//   pm = 0.0 + root.
+// ------------------------------------------------------------------------------------
+constexpr int PM_THREADS = 512;
+constexpr int PM_MAXT = 128;
+constexpr int PM_CH = 512;             // blocks per P1 chunk (one per thread)
+constexpr int PM_MAX_DEPTH = 11;       // heap levels 0..11: n <= 128 * 2^11 = 262144 per period
+constexpr int PM_HEAP = (1 << (PM_MAX_DEPTH + 1)) - 1;
+
+// serial pairwise sum (pathological sizes only)
+__device__ double pairwise_serial(const double *a, int n) {
+    double vst[64];
+    int stk_o[64], stk_n[64], sp = 0, vp = 0;
+    stk_o[sp] = 0;
+    stk_n[sp] = n;
+    sp++;
+    while (sp > 0) {
+        sp--;
+        int o = stk_o[sp], m = stk_n[sp];
+        if (m < 0) {
+            double rhs = vst[--vp];
+            double lhs = vst[--vp];
+            vst[vp++] = f64_add(lhs, rhs);
+            continue;
+        }
+        if (m <= 128) {
+            double res;
+            if (m < 8) {
+                res = -0.0;
+                for (int i = 0; i < m; i++) res = f64_add(res, a[o + i]);
+            } else {
+                double r[8];
+                for (int j = 0; j < 8; j++) r[j] = a[o + j];
+                int i = 8;
+                for (; i < m - (m % 8); i += 8)
+                    for (int j = 0; j < 8; j++) r[j] = f64_add(r[j], a[o + i + j]);
+                res = tree8(r);
+                for (; i < m; i++) res = f64_add(res, a[o + i]);
+            }
+            vst[vp++] = res;
+            continue;
+        }
+        int n2 = m / 2;
+        n2 -= n2 % 8;
+        stk_o[sp] = 0;
+        stk_n[sp] = -1;
+        sp++;
+        stk_o[sp] = o + n2;
+        stk_n[sp] = m - n2;
+        sp++;
+        stk_o[sp] = o;
+        stk_n[sp] = n2;
+        sp++;
+    }
+    return vp ? vst[0] : -0.0;
+}
+
+
+__global__ void __launch_bounds__(PM_THREADS) k_pm_chunks(const int32_t *__restrict__ assign,
+                                                           const double *__restrict__ mass, int B, int T, int nchunk,
+                                                           int32_t *__restrict__ agg, int32_t *__restrict__ flags,
+                                                           double *__restrict__ compact) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ int s_cnt[PM_THREADS / 32][PM_MAXT];
+    __shared__ int s_base[PM_MAXT];
+    const int c = blockIdx.x, p = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = c * PM_CH + tid;
+    int t = (b < B) ? __ldg(assign + (size_t)p * B + b) : -1;
+    if (t < 0 || t >= T) t = -1;
+    const double m = (b < B) ? __ldg(mass + b) : 0.0;
+    for (int i = tid; i < (PM_THREADS / 32) * PM_MAXT; i += PM_THREADS) (&s_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const unsigned mt = __match_any_sync(0xffffffffu, t);
+    const int rank_w = __popc(mt & ((1u << lane) - 1u));
+    if (t >= 0 && rank_w == 0) s_cnt[warp][t] = __popc(mt);
+    __syncthreads();
+    int32_t *my_agg = agg + ((size_t)p * nchunk + c) * T;
+    for (int j = tid; j < T; j += PM_THREADS) {
+        int run = 0;
+        for (int w = 0; w < PM_THREADS / 32; w++) {
+            const int x = s_cnt[w][j];
+            s_cnt[w][j] = run;
+            run += x;
+        }
+        my_agg[j] = run;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(flags + (size_t)p * nchunk + c), "r"(1) : "memory");
+    }
+    // look-back: warp 0 waits until every lower chunk has published (flags polled with
+    // independent acquire loads), then base[j] = sum of lower chunks' counts of period j
+    if (warp == 0) {
+        const int32_t *fl = flags + (size_t)p * nchunk;
+        for (;;) {
+            bool ok = true;
+            for (int k0 = 0; k0 < c; k0 += 128) {
+                int f[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int k = k0 + u * 32 + lane;
+                    f[u] = 1;
+                    if (k < c) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f[u]) : "l"(fl + k) : "memory");
+                }
+                ok &= (f[0] != 0) & (f[1] != 0) & (f[2] != 0) & (f[3] != 0);
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    for (int j = warp; j < T; j += PM_THREADS / 32) {
+        int sum = 0;
+        for (int k0 = 0; k0 < c; k0 += 128) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = k0 + u * 32 + lane;
+                v[u] = (k < c) ? __ldcg(agg + ((size_t)p * nchunk + k) * T + j) : 0;
+            }
+            sum += v[0] + v[1] + v[2] + v[3];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) s_base[j] = sum;
+    }
+    __syncthreads();
+    if (t >= 0) compact[((size_t)p * T + t) * B + s_base[t] + s_cnt[warp][t] + rank_w] = m;
+}
+
+struct PmTreeSmem {
+    int start[PM_HEAP];
+    int len[PM_HEAP];  // -1: dead (below a leaf)
+    double val[PM_HEAP];
+    int leaves[1 << PM_MAX_DEPTH];
+    int nleaf;
+    int depth;
+    int total;
+};
+
+__global__ void __launch_bounds__(PM_THREADS) k_pm_tree(const int32_t *__restrict__ agg, int32_t *__restrict__ flags,
+                                                         const double *__restrict__ compact, int B, int T, int nchunk,
+                                                         double *__restrict__ pm_out) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // P1 complete and visible
+    extern __shared__ __align__(16) unsigned char tree_dyn[];
+    PmTreeSmem &sm = *reinterpret_cast<PmTreeSmem *>(tree_dyn);
+    const int t = blockIdx.x, p = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {
+        int sum = 0;
+        for (int k0 = 0; k0 < nchunk; k0 += 128) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = k0 + u * 32 + lane;
+                v[u] = (k < nchunk) ? __ldcg(agg + ((size_t)p * nchunk + k) * T + t) : 0;
+            }
+            sum += v[0] + v[1] + v[2] + v[3];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) {
+            sm.total = sum;
+            sm.nleaf = 0;
+        }
+    }
+    // re-arm the look-back flags of this schedule for the next P1 launch (P1 has finished)
+    if (t == 0)
+        for (int k = tid; k < nchunk; k += PM_THREADS) flags[(size_t)p * nchunk + k] = 0;
+    __syncthreads();
+    const int n = sm.total;
+    const double *a = compact + ((size_t)p * T + t) * B;
+    // top-down heap build
+    if (tid == 0) {
+        sm.start[0] = 0;
+        sm.len[0] = n;
+    }
+    __syncthreads();
+    int depth = 0;
+    bool overflow = false;
+    for (int d = 0;; d++) {
+        const int first = (1 << d) - 1, cnt = 1 << d;
+        bool any_internal = false;
+        for (int j = tid; j < cnt; j += PM_THREADS) {
+            const int id = first + j;
+            const int ln = sm.len[id];
+            if (ln < 0) continue;
+            if (ln <= 128) {
+                const int k = atomicAdd(&sm.nleaf, 1);
+                sm.leaves[k] = id;
+            } else {
+                any_internal = true;
+                if (d < PM_MAX_DEPTH) {
+                    const int n2 = ((ln >> 3) >> 1) << 3;  // floor(m/2) whole 8-blocks left
+                    sm.start[2 * id + 1] = sm.start[id];
+                    sm.len[2 * id + 1] = n2;
+                    sm.start[2 * id + 2] = sm.start[id] + n2;
+                    sm.len[2 * id + 2] = ln - n2;
+                }
+            }
+        }
+        // children of leaves / dead nodes are dead
+        if (d < PM_MAX_DEPTH)
+            for (int j = tid; j < cnt; j += PM_THREADS) {
+                const int id = first + j;
+                const int ln = sm.len[id];
+                if (ln <= 128) {
+                    sm.len[2 * id + 1] = -1;
+                    sm.len[2 * id + 2] = -1;
+                }
+            }
+        const int more = __syncthreads_or(any_internal);
+        if (!more) {
+            depth = d;
+            break;
+        }
+        if (d == PM_MAX_DEPTH) {
+            overflow = true;
+            break;
+        }
+    }
+    if (overflow) {  // > 262144 blocks in one period: serial evaluation (correct, slow)
+        if (tid == 0) pm_out[(size_t)p * T + t] = f64_add(0.0, pairwise_serial(a, n));
+        return;
+    }
+    // leaf sums
+    const int nleaf = sm.nleaf;
+    const int sub = tid & 7, grp = tid >> 3, ngrp = PM_THREADS >> 3;
+    for (int l0 = 0; l0 < nleaf; l0 += ngrp) {
+        const int l = l0 + grp;
+        const bool act = l < nleaf;
+        const int id = act ? sm.leaves[l] : 0;
+        const int o = act ? sm.start[id] : 0;
+        const int len = act ? sm.len[id] : 0;
+        double r = 0.0;
+        if (act && len >= 8) {
+            // all (<= 16) loads of this accumulator issued before the sequential adds
+            const int nm = len >> 3;
+            double x[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = (u < nm) ? __ldcg(a + o + 8 * u + sub) : 0.0;
+            r = x[0];
+#pragma unroll
+            for (int u = 1; u < 16; u++)
+                if (u < nm) r = f64_add(r, x[u]);
+        }
+        r = f64_add(r, __shfl_xor_sync(0xffffffffu, r, 1));
+        r = f64_add(r, __shfl_xor_sync(0xffffffffu, r, 2));
+        r = f64_add(r, __shfl_xor_sync(0xffffffffu, r, 4));
+        if (act && sub == 0) {
+            double res;
+            int i;
+            if (len < 8) {
+                res = -0.0;
+                i = 0;
+            } else {
+                res = r;
+                i = len - (len & 7);
+            }
+            for (; i < len; i++) res = f64_add(res, __ldcg(a + o + i));
+            sm.val[id] = res;
+        }
+    }
+    __syncthreads();
+    // bottom-up fold: internal node = left + right
+    for (int d = depth - 1; d >= 0; d--) {
+        const int first = (1 << d) - 1, cnt = 1 << d;
+        for (int j = tid; j < cnt; j += PM_THREADS) {
+            const int id = first + j;
+            if (sm.len[id] > 128) sm.val[id] = f64_add(sm.val[2 * id + 1], sm.val[2 * id + 2]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) pm_out[(size_t)p * T + t] = f64_add(0.0, n ? sm.val[0] : -0.0);
+}
+
+
+// ------------------------------------------------------------------------------------
+// check_feasible pieces
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_pred_count(const int32_t *__restrict__ assign, const BlockRow *__restrict__ rows,
+                                                    const int32_t *__restrict__ adj, int B,
+                                                    unsigned long long *__restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    const int32_t *a = assign + (size_t)p * B;
+    unsigned c = 0;
+    if (j < B) {
+        int tj = a[j];
+        if (tj >= 0) {
+            BlockRow r = rows[j];
+            int npred = r.cnt & 0xffff;
+            for (int k = 0; k < npred; k++) {
+                int ti = a[__ldg(adj + r.adj + k)];
+                if (ti < 0 || ti > tj) c++;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out + p, (unsigned long long)c);
+}
+
+__global__ void k_feas_final(const double *__restrict__ pm, const double *__restrict__ cap, int T, int P,
+                             double mean_cap, const unsigned long long *__restrict__ cnt,
+                             int64_t *__restrict__ pred_out, double *__restrict__ excess_out,
+                             double *__restrict__ viol_out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    double ex = 0.0;
+    for (int t = 0; t < T; t++) {
+        double d = f64_sub(pm[(size_t)p * T + t], cap[t]);
+        ex = f64_add(ex, (d > 0.0) ? d : 0.0);  // excess += max(0.0, load - cap)
+    }
+    unsigned long long c = cnt[p];
+    pred_out[p] = (int64_t)c;
+    excess_out[p] = ex;
+    viol_out[p] = f64_add((double)c, f64_div(ex, mean_cap));
+}
+
+// ------------------------------------------------------------------------------------
+// repair waves over topological levels
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_repair_level(int32_t *__restrict__ assign, int B,
+                                                      const BlockRow *__restrict__ rows,
+                                                      const int32_t *__restrict__ adj,
+                                                      const int32_t *__restrict__ level_blocks, int lstart,
+                                                      int lcount, int mode, uint8_t *__restrict__ unmined) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= lcount) return;
+    const int p = blockIdx.y;
+    int32_t *a = assign + (size_t)p * B;
+    const int b = __ldg(level_blocks + lstart + k);
+    const int t = a[b];
+    if (t < 0) return;
+    const BlockRow r = rows[b];
+    const int npred = r.cnt & 0xffff;
+    if (mode == PP_REPAIR_PUSH_FORWARD) {
+        int t_min = 0;
+        bool ok = true;
+        for (int e = 0; e < npred; e++) {
+            int tp = a[__ldg(adj + r.adj + e)];
+            if (tp < 0) {
+                ok = false;
+                break;
+            }
+            t_min = max(t_min, tp);
+        }
+        if (!ok) a[b] = -1;
+        else if (t < t_min) a[b] = t_min;
+    } else {
+        bool bad = false;
+        for (int e = 0; e < npred; e++) {
+            int tp = a[__ldg(adj + r.adj + e)];
+            if (tp < 0 || tp > t) bad = true;
+        }
+        if (bad) {
+            a[b] = -1;
+            if (unmined) unmined[(size_t)p * B + b] = 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// table preparation kernels
+// ------------------------------------------------------------------------------------
+__global__ void k_spatial(BlockRow *rows, int B, const double *alt, const double *strc, const double *dist,
+                          double w1, double w2, double w3, double diameter) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    // geological_consistency (uncertainty.py:185-191)
+    double dn = 0.0;
+    if (diameter > 0) {
+        dn = f64_div(dist[b], diameter);
+        if (1.0 < dn) dn = 1.0;
+    }
+    double raw = f64_add(f64_add(f64_mul(w1, alt[b]), f64_mul(w2, strc[b])), f64_mul(w3, f64_sub(1.0, dn)));
+    double v = f64_add(0.5, raw);
+    if (v < 0.5) v = 0.5;
+    if (v > 1.5) v = 1.5;
+    rows[b].spatial = v;
+}
+
+// vmax [S][B] -> [B][Sp] and unit_mean[b] = (sum_s vmax[s][b]) / S sequentially (evaluate.py:302)
+__global__ void k_scen_tables(const double *__restrict__ vsb, int S, int B, int Sp, double *__restrict__ vbs,
+                              double *__restrict__ unit_mean) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double acc = 0.0;
+    for (int s = 0; s < S; s++) {
+        double v = vsb[(size_t)s * B + b];
+        vbs[(size_t)b * Sp + s] = v;
+        acc = f64_add(acc, v);
+    }
+    for (int s = S; s < Sp; s++) vbs[(size_t)b * Sp + s] = 0.0;
+    unit_mean[b] = f64_div(acc, (double)S);
+}
+
+// sigma.mean(axis=0) sequentially over s (evaluate.py:351)
+__global__ void k_sig_mean(const double *sigma, int S, int T, double *out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    double acc = 0.0;
+    for (int s = 0; s < S; s++) acc = f64_add(acc, sigma[(size_t)s * T + t]);
+    out[t] = f64_div(acc, (double)S);
+}
+
+// Linear ENPV table enpv[b][t]: colgen.py:187-204 form
+//   disc[t] * mean_s(sig[s][t] * vmax[s][b]) - disc[t] * cost[b][t]
+// or, with `factored`, the hybrid.py:673-678 / saa.py:65-69 form
+//   disc[t] * (mean_s(sig[s][t] * vmax[s][b]) - cost[b][t]);
+// mean_s is numpy's .mean(axis=0) over an [S][B] array: sequential in s, then / S.
+__global__ void k_enpv_table(const double *__restrict__ vmax, int Sp, int S, int B, int T,
+                             const double *__restrict__ sigma, const double *__restrict__ disc,
+                             const double *__restrict__ cost, int factored, double *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * T) return;
+    const int b = i / T, t = i - b * T;
+    const double *row = vmax + (size_t)b * Sp;
+    double acc = 0.0;
+    for (int s = 0; s < S; s++) acc = f64_add(acc, f64_mul(__ldg(sigma + (size_t)s * T + t), __ldg(row + s)));
+    const double mean = f64_div(acc, (double)S);
+    const double d = __ldg(disc + t), c = __ldg(cost + (size_t)b * T + t);
+    out[i] = factored ? f64_mul(d, f64_sub(mean, c)) : f64_sub(f64_mul(d, mean), f64_mul(d, c));
+}
+
+// deterministic reduce of per-shard bests (block < 0 = none), evaluate.py:404-409 order
+__global__ void k_reduce_best(const pp_best *__restrict__ recs, int n, pp_best *__restrict__ out) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    Best x{-kInf, INT_MAX, INT_MAX};
+    for (int i = 0; i < n; i++) {
+        pp_best r = recs[i];
+        if (r.block < 0) continue;
+        Best o{r.value, r.block, r.period};
+        if (better(o, x)) x = o;
+    }
+    pp_best g;
+    bool none = (x.b == INT_MAX);
+    g.value = none ? -kInf : x.v;
+    g.block = none ? -1 : x.b;
+    g.period = none ? -1 : x.t;
+    *out = g;
+}
+
+__global__ void k_apply_moves(int32_t *assign, int B, int T, const int32_t *blocks, const int32_t *periods, int n) {
+    // sequential in input order so a block moved twice ends at its last period
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int k = 0; k < n; k++) {
+        int b = blocks[k], t = periods[k];
+        if (b >= 0 && b < B && t >= -1 && t < T) assign[b] = t;
+    }
+}
+
+
+// period masses of P schedules (device pointers) into pm_out[P][T]: P1 (chunks) then
+// P2 (trees), P2 launched as a programmatic dependent of P1
+int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st) {
+    const int B = c->B, T = c->T;
+    const int nchunk = (B + PM_CH - 1) / PM_CH;
+    // compacted masses: B doubles per (period, schedule); batches bounded to ~512 MiB
+    const size_t per = (size_t)T * B * sizeof(double);
+    const int pchunk = std::max(1, std::min(P, (int)std::max<size_t>(1, ((size_t)512 << 20) / per)));
+    TRY(c->compact.ensure(per * pchunk));
+    TRY(c->cnt.ensure(sizeof(int32_t) * (size_t)pchunk * nchunk * (T + 1)));
+    if (c->pm_flags_n < (size_t)pchunk * nchunk) {
+        TRY(c->pm_flags.ensure(sizeof(int32_t) * (size_t)pchunk * nchunk));
+        CUDA_TRY(cudaMemset(c->pm_flags.ptr, 0, sizeof(int32_t) * (size_t)pchunk * nchunk));
+        c->pm_flags_n = (size_t)pchunk * nchunk;
+    }
+    static bool attr_done = false;
+    if (!attr_done) {
+        CUDA_TRY(cudaFuncSetAttribute(k_pm_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PmTreeSmem)));
+        attr_done = true;
+    }
+    for (int p0 = 0; p0 < P; p0 += pchunk) {
+        const int np = std::min(pchunk, P - p0);
+        k_pm_chunks<<<dim3(nchunk, np), PM_THREADS, 0, st>>>(d_assign + (size_t)p0 * B, c->mass.as<double>(), B, T,
+                                                             nchunk, c->cnt.as<int32_t>(), c->pm_flags.as<int32_t>(),
+                                                             c->compact.as<double>());
+        CUDA_TRY(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(T, np);
+        cfg.blockDim = dim3(PM_THREADS);
+        cfg.dynamicSmemBytes = sizeof(PmTreeSmem);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pm_tree, (const int32_t *)c->cnt.as<int32_t>(), c->pm_flags.as<int32_t>(),
+                                    (const double *)c->compact.as<double>(), B, T, nchunk, d_pm + (size_t)p0 * T));
+    }
+    return PP_OK;
+}
+
+// recompute the current schedule's period masses if the schedule changed
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched) {
+    *launched = false;
+    if (!c->pm_dirty) return PP_OK;
+    TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st));
+    c->pm_dirty = false;
+    *launched = true;
+    return PP_OK;
+}
+
+
+static void plan_rec(PwPlan &p, int o, int n) {
+    if (n <= 128) {
+        p.start[p.nleaf] = o;
+        p.len[p.nleaf] = n;
+        p.adds[p.nleaf] = 0;
+        p.nleaf++;
+        return;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    plan_rec(p, o, n2);
+    plan_rec(p, o + n2, n - n2);
+    p.adds[p.nleaf - 1]++;
+}
+
+static int make_plan(int n, PwPlan *p) {
+    // leaves hold 56..128 elements once n > 128
+    if (n > 128 * (kMaxLeaves / 2)) return fail(PP_ERR_INVALID_ARGS, "too many scenarios (%d) for the pairwise plan", n);
+    memset(p, 0, sizeof(*p));
+    p->n = n;
+    if (n > 0) plan_rec(*p, 0, n);
+    return PP_OK;
+}
+
+
+static void plan_words(const PwPlan &p, int *w) {
+    w[0] = p.n;
+    w[1] = p.nleaf;
+    for (int i = 0; i < kMaxLeaves; i++) {
+        w[2 + i] = p.start[i];
+        w[2 + kMaxLeaves + i] = p.len[i];
+        w[2 + 2 * kMaxLeaves + i] = p.adds[i];
+    }
+}
+
+extern "C" {
+
+int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *ei, const int32_t *ej,
+                    const double *mass, const double *cost, const double *capacity, const double *discount) {
+    if (!c) return fail(PP_ERR_INVALID_ARGS, "NULL context");
+    if (B < 1 || T < 1) return fail(PP_ERR_INVALID_ARGS, "need n_blocks >= 1 and n_periods >= 1");
+    if (T > PM_MAXT) return fail(PP_ERR_INVALID_ARGS, "n_periods %d exceeds the supported %d", T, PM_MAXT);
+    if (E < 0 || (E > 0 && (!ei || !ej))) return fail(PP_ERR_INVALID_ARGS, "bad edge arrays");
+    if (!mass || !cost || !capacity || !discount) return fail(PP_ERR_INVALID_ARGS, "NULL table");
+    for (int64_t e = 0; e < E; e++)
+        if (ei[e] < 0 || ei[e] >= B || ej[e] < 0 || ej[e] >= B)
+            return fail(PP_ERR_VALIDATION, "precedence edge (%d, %d) references unknown block", ei[e], ej[e]);
+    for (int t = 0; t < T; t++)
+        if (!(capacity[t] > 0)) return fail(PP_ERR_VALIDATION, "mining capacity must be > 0 in every period");
+    TRY(use_device(c));
+    // adjacency: predecessors of b (edges (i, b) in list order) then successors (edges (b, j))
+    std::vector<int> npred(B, 0), nsucc(B, 0);
+    for (int64_t e = 0; e < E; e++) {
+        npred[ej[e]]++;
+        nsucc[ei[e]]++;
+    }
+    for (int b = 0; b < B; b++)
+        if (npred[b] > 0xffff || nsucc[b] > 0x7fff)
+            return fail(PP_ERR_INVALID_ARGS, "block %d has too many neighbours", b);
+    std::vector<int> start(B + 1, 0);
+    for (int b = 0; b < B; b++) start[b + 1] = start[b] + npred[b] + nsucc[b];
+    std::vector<int> adj((size_t)std::max<long long>(start[B], 1));
+    std::vector<int> fp(B), fs(B);
+    for (int b = 0; b < B; b++) {
+        fp[b] = start[b];
+        fs[b] = start[b] + npred[b];
+    }
+    for (int64_t e = 0; e < E; e++) {
+        adj[fp[ej[e]]++] = ei[e];
+        adj[fs[ei[e]]++] = ej[e];
+    }
+    // topological levels (longest predecessor chain) by Kahn's algorithm; cycle check
+    std::vector<int> indeg(npred), level(B, 0), queue;
+    queue.reserve(B);
+    for (int b = 0; b < B; b++)
+        if (indeg[b] == 0) queue.push_back(b);
+    for (size_t q = 0; q < queue.size(); q++) {
+        int b = queue[q];
+        for (int k = start[b] + npred[b]; k < start[b + 1]; k++) {
+            int j = adj[k];
+            level[j] = std::max(level[j], level[b] + 1);
+            if (--indeg[j] == 0) queue.push_back(j);
+        }
+    }
+    if ((int)queue.size() != B) return fail(PP_ERR_VALIDATION, "cycle in precedence graph");
+    int nlev = 0;
+    for (int b = 0; b < B; b++) nlev = std::max(nlev, level[b] + 1);
+    std::vector<int> lptr(nlev + 1, 0), lblocks(B);
+    for (int b = 0; b < B; b++) lptr[level[b] + 1]++;
+    for (int l = 0; l < nlev; l++) lptr[l + 1] += lptr[l];
+    {
+        std::vector<int> fill(lptr.begin(), lptr.end() - 1);
+        for (int b = 0; b < B; b++) lblocks[fill[level[b]]++] = b;
+    }
+    std::vector<BlockRow> rows(B);
+    for (int b = 0; b < B; b++) {
+        rows[b].mass = mass[b];
+        rows[b].spatial = 0.0;
+        rows[b].adj = start[b];
+        rows[b].cnt = npred[b] | (nsucc[b] << 16);
+        rows[b].level = level[b];
+        rows[b].pad = 0;
+    }
+    TRY(c->rows.ensure(sizeof(BlockRow) * B));
+    TRY(c->adj.ensure(sizeof(int) * adj.size()));
+    TRY(c->cost.ensure(sizeof(double) * (size_t)B * T));
+    TRY(c->cap.ensure(sizeof(double) * T));
+    TRY(c->disc.ensure(sizeof(double) * T));
+    TRY(c->ones_t.ensure(sizeof(double) * T));
+    TRY(c->level_blocks.ensure(sizeof(int) * B));
+    TRY(c->assign.ensure(sizeof(int) * B));
+    TRY(c->mass.ensure(sizeof(double) * B));
+    TRY(c->pm.ensure(sizeof(double) * T));
+    std::vector<double> ones(T, 1.0);
+    CUDA_TRY(cudaMemcpy(c->rows.ptr, rows.data(), sizeof(BlockRow) * B, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->adj.ptr, adj.data(), sizeof(int) * adj.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->cost.ptr, cost, sizeof(double) * (size_t)B * T, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->mass.ptr, mass, sizeof(double) * B, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->cap.ptr, capacity, sizeof(double) * T, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->disc.ptr, discount, sizeof(double) * T, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->ones_t.ptr, ones.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->level_blocks.ptr, lblocks.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+    c->B = B;
+    c->T = T;
+    c->E = E;
+    c->n_levels = nlev;
+    c->deg_max = 0;
+    for (int b = 0; b < B; b++) c->deg_max = std::max(c->deg_max, npred[b] + nsucc[b]);
+    c->level_ptr = lptr;
+    c->level_of = level;
+    c->mean_cap = (0.0 + host_pairwise(capacity, T)) / (double)T;
+    c->have_instance = true;
+    c->assign_ptr = c->assign.as<int32_t>();
+    c->borrowed = false;
+    c->pm_dirty = true;
+    c->have_spatial = false;
+    c->have_scen = false;
+    c->have_sched = false;
+    return PP_OK;
+}
+
+int pp_set_geology(pp_ctx *c, const double *alt, const double *strc, const double *dist, double w1, double w2,
+                   double w3, double diameter) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (!alt || !strc || !dist) return fail(PP_ERR_INVALID_ARGS, "NULL feature array");
+    TRY(use_device(c));
+    const int B = c->B;
+    DevBuf tmp;
+    int rc = tmp.ensure(sizeof(double) * 3 * (size_t)B);
+    if (rc) return rc;
+    double *d = tmp.as<double>();
+    cudaError_t e = cudaMemcpy(d, alt, sizeof(double) * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + B, strc, sizeof(double) * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + 2 * (size_t)B, dist, sizeof(double) * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        k_spatial<<<(B + 255) / 256, 256, 0, c->stream>>>(c->rows.as<BlockRow>(), B, d, d + B, d + 2 * (size_t)B, w1,
+                                                          w2, w3, diameter);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    tmp.release();
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "pp_set_geology: %s", cudaGetErrorString(e));
+    c->have_spatial = true;
+    return PP_OK;
+}
+
+int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *sigma_st) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (S < 1 || !vmax_sb) return fail(PP_ERR_INVALID_ARGS, "need n_scenarios >= 1 and a value table");
+    TRY(use_device(c));
+    PwPlan plan;
+    TRY(make_plan(S, &plan));
+    const int B = c->B, T = c->T;
+    const int Sp = (S + 3) & ~3;
+    TRY(c->vmax.ensure(sizeof(double) * (size_t)B * Sp));
+    TRY(c->unit_mean.ensure(sizeof(double) * B));
+    TRY(c->sigma.ensure(sizeof(double) * (size_t)S * T));
+    TRY(c->ones_st.ensure(sizeof(double) * (size_t)S * T));
+    TRY(c->sig_mean.ensure(sizeof(double) * T));
+    TRY(c->plan_dev.ensure(sizeof(int) * kPlanWords));
+    DevBuf tmp;
+    TRY(tmp.ensure(sizeof(double) * (size_t)S * B));
+    cudaError_t e = cudaMemcpy(tmp.ptr, vmax_sb, sizeof(double) * (size_t)S * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        k_scen_tables<<<(B + 255) / 256, 256, 0, c->stream>>>(tmp.as<double>(), S, B, Sp, c->vmax.as<double>(),
+                                                              c->unit_mean.as<double>());
+        e = cudaGetLastError();
+    }
+    std::vector<double> ones((size_t)S * T, 1.0);
+    int words[kPlanWords];
+    plan_words(plan, words);
+    if (e == cudaSuccess) e = cudaMemcpy(c->plan_dev.ptr, words, sizeof(words), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->ones_st.ptr, ones.data(), sizeof(double) * ones.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && sigma_st) {
+        e = cudaMemcpy(c->sigma.ptr, sigma_st, sizeof(double) * (size_t)S * T, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) {
+            k_sig_mean<<<(T + 127) / 128, 128, 0, c->stream>>>(c->sigma.as<double>(), S, T, c->sig_mean.as<double>());
+            e = cudaGetLastError();
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    tmp.release();
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "pp_set_scenarios: %s", cudaGetErrorString(e));
+    c->S = S;
+    c->Sp = Sp;
+    c->plan = plan;
+    c->cvar_k = std::max(1, (int)std::ceil(0.1 * S));
+    c->have_sigma = sigma_st != nullptr;
+    c->have_scen = true;
+    return PP_OK;
+}
+
+int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (!assign) return fail(PP_ERR_INVALID_ARGS, "assign is NULL");
+    if (mem != PP_MEM_HOST && mem != PP_MEM_DEVICE && mem != PP_MEM_DEVICE_BORROW)
+        return fail(PP_ERR_INVALID_ARGS, "unknown memory kind %d", mem);
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    if (mem == PP_MEM_HOST) {
+        for (int b = 0; b < c->B; b++)
+            if (assign[b] < -1 || assign[b] >= c->T)
+                return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
+    }
+    if (mem == PP_MEM_DEVICE_BORROW) {
+        c->assign_ptr = assign;  // read in place until the next pp_set_schedule
+        c->borrowed = true;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(c->assign.ptr, assign, sizeof(int32_t) * c->B,
+                                 mem == PP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        c->assign_ptr = c->assign.as<int32_t>();
+        c->borrowed = false;
+    }
+    c->pm_dirty = true;  // period masses are recomputed by the next evaluation launch (PDL-overlapped)
+    if (mem == PP_MEM_HOST) CUDA_TRY(cudaStreamSynchronize(st));
+    c->have_sched = true;
+    return PP_OK;
+}
+
+int pp_apply_moves(pp_ctx *c, const int32_t *blocks, const int32_t *periods, int32_t n, int32_t mem, void *stream) {
+    if (!c || !c->have_sched) return fail(PP_ERR_STATE, "pp_set_schedule first");
+    if (n < 0 || (n > 0 && (!blocks || !periods))) return fail(PP_ERR_INVALID_ARGS, "bad move arrays");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    if (n == 0) return PP_OK;
+    if (c->borrowed) {  // take a private copy before writing
+        CUDA_TRY(cudaMemcpyAsync(c->assign.ptr, c->assign_ptr, sizeof(int32_t) * c->B, cudaMemcpyDeviceToDevice, st));
+        c->assign_ptr = c->assign.as<int32_t>();
+        c->borrowed = false;
+    }
+    const int32_t *db = blocks, *dp = periods;
+    if (mem == PP_MEM_HOST) {
+        for (int k = 0; k < n; k++)
+            if (blocks[k] < 0 || blocks[k] >= c->B || periods[k] < -1 || periods[k] >= c->T)
+                return fail(PP_ERR_INVALID_ARGS, "move (%d, %d) out of range", blocks[k], periods[k]);
+        TRY(c->h_a.ensure(sizeof(int32_t) * n));
+        TRY(c->h_b.ensure(sizeof(int32_t) * n));
+        CUDA_TRY(cudaMemcpyAsync(c->h_a.ptr, blocks, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(c->h_b.ptr, periods, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        db = c->h_a.as<int32_t>();
+        dp = c->h_b.as<int32_t>();
+    }
+    k_apply_moves<<<1, 32, 0, st>>>(c->assign.as<int32_t>(), c->B, c->T, db, dp, n);
+    CUDA_TRY(cudaGetLastError());
+    c->pm_dirty = true;
+    if (mem == PP_MEM_HOST) CUDA_TRY(cudaStreamSynchronize(st));
+    return PP_OK;
+}
+
+int pp_get_schedule(pp_ctx *c, int32_t *assign_out, double *pm_out, int32_t mem, void *stream) {
+    if (!c || !c->have_sched) return fail(PP_ERR_STATE, "pp_set_schedule first");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    bool launched;
+    if (pm_out) TRY(refresh_pm(c, st, &launched));
+    cudaMemcpyKind k = (mem == PP_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (assign_out) CUDA_TRY(cudaMemcpyAsync(assign_out, c->assign_ptr, sizeof(int32_t) * c->B, k, st));
+    if (pm_out) CUDA_TRY(cudaMemcpyAsync(pm_out, c->pm.ptr, sizeof(double) * c->T, k, st));
+    if (mem == PP_MEM_HOST) CUDA_TRY(cudaStreamSynchronize(st));
+    return PP_OK;
+}
+
+int pp_check_feasible(pp_ctx *c, const int32_t *assign, int32_t P, int64_t *pred_count, double *excess,
+                      double *violation, double *period_mass, int32_t mem, void *stream) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (P < 0 || (P > 0 && !assign) || !pred_count || !excess || !violation)
+        return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if (P == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B, T = c->T;
+    const int32_t *da = assign;
+    int64_t *dcnt = pred_count;
+    double *dex = excess, *dvi = violation, *dpm = period_mass;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_assign.ensure(sizeof(int32_t) * (size_t)P * B));
+        TRY(c->h_i64.ensure(sizeof(int64_t) * P));
+        TRY(c->h_d1.ensure(sizeof(double) * P));
+        TRY(c->h_d2.ensure(sizeof(double) * P));
+        TRY(c->h_pm.ensure(sizeof(double) * (size_t)P * T));
+        CUDA_TRY(cudaMemcpyAsync(c->h_assign.ptr, assign, sizeof(int32_t) * (size_t)P * B, cudaMemcpyHostToDevice, st));
+        da = c->h_assign.as<int32_t>();
+        dcnt = c->h_i64.as<int64_t>();
+        dex = c->h_d1.as<double>();
+        dvi = c->h_d2.as<double>();
+        dpm = c->h_pm.as<double>();
+    } else if (!dpm) {
+        TRY(c->pm_batch.ensure(sizeof(double) * (size_t)P * T));
+        dpm = c->pm_batch.as<double>();
+    }
+    TRY(c->predcnt.ensure(sizeof(unsigned long long) * P));
+    CUDA_TRY(cudaMemsetAsync(c->predcnt.ptr, 0, sizeof(unsigned long long) * P, st));
+    TRY(run_period_mass(c, da, P, dpm, st));
+    k_pred_count<<<dim3((B + 255) / 256, P), 256, 0, st>>>(da, c->rows.as<BlockRow>(), c->adj.as<int32_t>(), B,
+                                                           c->predcnt.as<unsigned long long>());
+    k_feas_final<<<(P + 127) / 128, 128, 0, st>>>(dpm, c->cap.as<double>(), T, P, c->mean_cap,
+                                                  c->predcnt.as<unsigned long long>(), dcnt, dex, dvi);
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaMemcpyAsync(pred_count, dcnt, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(excess, dex, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(violation, dvi, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+        if (period_mass)
+            CUDA_TRY(cudaMemcpyAsync(period_mass, dpm, sizeof(double) * (size_t)P * T, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+int pp_repair(pp_ctx *c, int32_t *assign, int32_t P, int32_t mode, uint8_t *unmined_out, int32_t mem, void *stream) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (P < 0 || (P > 0 && !assign)) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if (mode != PP_REPAIR_PUSH_FORWARD && mode != PP_REPAIR_UNMINE) return fail(PP_ERR_INVALID_ARGS, "unknown repair mode %d", mode);
+    if (P == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B;
+    int32_t *da = assign;
+    uint8_t *du = unmined_out;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_assign.ensure(sizeof(int32_t) * (size_t)P * B));
+        CUDA_TRY(cudaMemcpyAsync(c->h_assign.ptr, assign, sizeof(int32_t) * (size_t)P * B, cudaMemcpyHostToDevice, st));
+        da = c->h_assign.as<int32_t>();
+        if (unmined_out) {
+            TRY(c->h_o5.ensure((size_t)P * B));
+            du = c->h_o5.as<uint8_t>();
+        }
+    }
+    if (du) CUDA_TRY(cudaMemsetAsync(du, 0, (size_t)P * B, st));
+    for (int l = 1; l < c->n_levels; l++) {
+        int ls = c->level_ptr[l], lc = c->level_ptr[l + 1] - ls;
+        if (lc <= 0) continue;
+        k_repair_level<<<dim3((lc + 255) / 256, P), 256, 0, st>>>(da, B, c->rows.as<BlockRow>(), c->adj.as<int32_t>(),
+                                                                  c->level_blocks.as<int32_t>(), ls, lc, mode, du);
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaMemcpyAsync(assign, da, sizeof(int32_t) * (size_t)P * B, cudaMemcpyDeviceToHost, st));
+        if (unmined_out) CUDA_TRY(cudaMemcpyAsync(unmined_out, du, (size_t)P * B, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+int pp_reduce_best(pp_ctx *c, const pp_best *recs, int32_t n, pp_best *out, int32_t mem, void *stream) {
+    if (!c || n < 0 || (n > 0 && !recs) || !out) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const pp_best *dr = recs;
+    pp_best *dout = out;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_d1.ensure(sizeof(pp_best) * (size_t)std::max(n, 1)));
+        TRY(c->h_glob.ensure(sizeof(pp_best)));
+        if (n > 0) CUDA_TRY(cudaMemcpyAsync(c->h_d1.ptr, recs, sizeof(pp_best) * n, cudaMemcpyHostToDevice, st));
+        dr = c->h_d1.as<pp_best>();
+        dout = c->h_glob.as<pp_best>();
+    }
+    k_reduce_best<<<1, 32, 0, st>>>(dr, n, dout);
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(pp_best), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+int pp_enpv_table(pp_ctx *c, uint32_t flags, int32_t factored, double *out, int32_t mem, void *stream) {
+    if (!c || !c->have_instance || !c->have_scen) return fail(PP_ERR_STATE, "pp_set_instance and pp_set_scenarios first");
+    if (!out) return fail(PP_ERR_INVALID_ARGS, "out is NULL");
+    if ((flags & PP_USE_SIGMA) && !c->have_sigma) return fail(PP_ERR_STATE, "PP_USE_SIGMA without an uploaded sigma");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const size_t n = (size_t)c->B * c->T;
+    double *dout = out;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_o4.ensure(sizeof(double) * n));
+        dout = c->h_o4.as<double>();
+    }
+    const double *sig = (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : c->ones_st.as<double>();
+    k_enpv_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->vmax.as<double>(), c->Sp, c->S, c->B, c->T, sig,
+                                                              c->disc.as<double>(), c->cost.as<double>(),
+                                                              factored ? 1 : 0, dout);
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+
+int pp_get_levels(pp_ctx *c, int32_t *n_levels, int32_t *level_of_block) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (n_levels) *n_levels = c->n_levels;
+    if (level_of_block) memcpy(level_of_block, c->level_of.data(), sizeof(int32_t) * c->B);
+    return PP_OK;
+}
+
+}  // extern "C"

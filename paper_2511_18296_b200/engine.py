@@ -134,13 +134,19 @@ class Engine:
             raise InvalidArgs("schedule has period indices out of range")
         check(self.lib.pp_set_schedule(self._h, ptr(a), _lib.PP_MEM_HOST, None))
 
-    def set_schedule_device(self, assign_tensor, stream=None):
-        check(self.lib.pp_set_schedule(self._h, assign_tensor.data_ptr(), _lib.PP_MEM_DEVICE, stream))
+    def set_schedule_device(self, assign_tensor, stream=None, borrow: bool = False):
+        # borrow: read the device tensor in place (no copy) until the next set_schedule
+        mem = _lib.PP_MEM_DEVICE_BORROW if borrow else _lib.PP_MEM_DEVICE
+        check(self.lib.pp_set_schedule(self._h, assign_tensor.data_ptr(), mem, stream))
 
     def apply_moves(self, blocks, periods):
         b = _i32(blocks)
         t = _i32(periods, b.size, "periods")
         check(self.lib.pp_apply_moves(self._h, ptr(b), ptr(t), b.size, _lib.PP_MEM_HOST, None))
+
+    def period_mass_device(self, out_tensor, stream=None):
+        """Refresh (if stale) and copy the current period masses into a device f64[T] tensor."""
+        check(self.lib.pp_get_schedule(self._h, None, ptr(out_tensor), _lib.PP_MEM_DEVICE, stream))
 
     def get_schedule(self):
         bm = self._need_bm()
@@ -286,6 +292,14 @@ class Engine:
         check(self.lib.pp_reduce_best(self._h, ctypes.addressof(arr), len(recs), ctypes.addressof(g),
                                       _lib.PP_MEM_HOST, None))
         return None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
+
+    def enpv_table(self, use_sigma=True, factored=False) -> np.ndarray:
+        """enpv[B][T]: colgen.py:187-204 form, or hybrid.py:673-678 / saa.py:65-69 when factored."""
+        bm = self._need_bm()
+        out = np.empty((bm.n_blocks, bm.n_periods), np.float64)
+        check(self.lib.pp_enpv_table(self._h, self.flags(use_sigma=use_sigma), int(bool(factored)), ptr(out),
+                                     _lib.PP_MEM_HOST, None))
+        return out
 
     def levels(self):
         bm = self._need_bm()

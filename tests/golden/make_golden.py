@@ -26,6 +26,7 @@ import numpy as np
 REF = os.environ.get("PITPLAN_REF", "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 
+from pitplan.colgen import _enpv_adjusted  # noqa: E402
 from pitplan.blockmodel import UNMINED, Block, Economics, GeoFeatures, Instance, OperatingMode, generate_synthetic  # noqa: E402
 from pitplan.evaluate import Schedule, check_feasible, evaluate_candidates_parallel  # noqa: E402
 from pitplan.hybrid import _precedence_repair_pass, greedy_initialize, lns_repair  # noqa: E402
@@ -158,6 +159,8 @@ def small_cases(store):
         store[p + "sigma"] = sigma.sigma
         store[p + "assign"] = sched.assignment.astype(np.int32)
         store[p + "cand"] = np.array(cand, dtype=np.int32)
+        store[p + "enpv"] = _enpv_adjusted(inst, scen, sigma)
+        store[p + "enpv_nosig"] = _enpv_adjusted(inst, scen, None)
         put(store, p + "s0_", run_kernel(inst, sched, cand, scen, 0, sigma))
         put(store, p + "sN_", run_kernel(inst, sched, cand, scen, None, sigma))
         put(store, p + "net_", run_kernel(inst, sched, cand, scen, None, sigma, net_mining_cost=True))
@@ -265,6 +268,8 @@ def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
     # host's thread count: freeze the small matrix itself
     store[p + "sigma"] = sigma.sigma
     store[p + "cand"] = cand
+    if n <= 4000:
+        store[p + "enpv"] = _enpv_adjusted(inst, scen, sigma)
     for sname, assign in (("full", full_greedy(inst)), ("greedy", greedy_initialize(inst, scen, sigma).assignment)):
         q = f"{p}{sname}_"
         sched = Schedule(assign)

@@ -261,7 +261,7 @@ def test_device_buffers_match_host_path():
         "scen_delta": torch.empty(C, S, T, dtype=torch.float32, device=dev),
         "global": torch.empty(2, dtype=torch.float64, device=dev),
     }
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = torch.cuda.Stream(dev).cuda_stream  # explicit stream (0 = the context's own)
     eng.set_schedule_device(torch.from_numpy(c["assign"].astype(np.int32)).to(dev), stream=stream)
     eng.eval_candidates_device(cand, out, None, net=True, stream=stream)
     torch.cuda.synchronize()
@@ -302,4 +302,19 @@ def test_errors_are_raised_not_fallen_back():
     with pytest.raises(PitplanError):
         fresh.eval_candidates(np.array([0]), None)
     fresh.close()
+    eng.close()
+
+
+def test_enpv_table_matches_reference(oracle_lib, small):
+    for case in range(0, 20, 4):
+        p = f"kd{case}_"
+        eng = Engine.from_tables(bm_from(small, p), tables_from(small, p))
+        assert same(eng.enpv_table(True), small[p + "enpv"])
+        assert same(eng.enpv_table(False), small[p + "enpv_nosig"])
+        eng.close()
+    c = config("C1")
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], c["sigma"]))
+    assert same(eng.enpv_table(True), load("c1")["C1_enpv"])
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    assert same(eng.enpv_table(True, factored=True), o.enpv_table(True, factored=True))
     eng.close()

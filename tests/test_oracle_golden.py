@@ -146,3 +146,16 @@ def test_oracle_thread_count_invariance(oracle_lib):
     for k in ("best_t", "best_val", "feasible", "exp_delta", "cvar"):
         assert same(r1[k], r8[k])
     assert r1["best"] == r8["best"]
+
+
+def test_enpv_table(oracle_lib):
+    """Linear ENPV table (colgen.py:187-204) against the reference's _enpv_adjusted."""
+    st = load("small")
+    for case in KD:
+        p = f"kd{case}_"
+        o = _oracle(oracle_lib, st, p)
+        assert same(o.enpv_table(True), st[p + "enpv"])
+        assert same(o.enpv_table(False), st[p + "enpv_nosig"])
+    c = config("C1")
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    assert same(o.enpv_table(True), load("c1")["C1_enpv"])
