@@ -1,274 +1,6 @@
-// pp_eval.cu -- candidate evaluation kernels (evaluate_candidates_parallel, evaluate.py:306-430)
-// and pp_eval_candidates.
+// pp_eval.cu -- evaluate_candidates_parallel (evaluate.py:306-430): the staged fast-path kernel
+// and pp_eval_candidates (which dispatches to pp_eval_general.cu otherwise).
 #include "pp_internal.cuh"
-
-// ------------------------------------------------------------------------------------
-// candidate evaluation: K1 value, K2 precedence window, K3 capacity, K4 argmax
-// ------------------------------------------------------------------------------------
-
-// Persistent grid: each lane group of G = pow2 >= T lanes (4..32) walks candidates
-// grp, grp + total_groups, ...; lane tl owns periods tl, tl+G, ... (PER slots, PER > 1
-// only when T > 32).  Per candidate:
-//   A  loads + precedence window (K2), no dependency on the period masses
-//   B  per-scenario deltas for every precedence-feasible period (K1 statistics), still
-//      independent of the period masses -- this overlaps k_period_mass under PDL
-//   C  griddepcontrol.wait, capacity (K3), parity value, lowest-t argmax, outputs; K4
-//      grid argmax after the loop.
-// Shared memory (stats only): sigma staged once per CTA as [T][SS] (SS = S | 1, odd
-// stride: conflict-free for lanes = periods), then per group the candidate's vmax row and
-// its current-period values.
-template <int PER, int KC, bool BIGS, bool SCEN>
-__global__ void __launch_bounds__(EV_THREADS) k_eval_candidates(const EvalParams p, const int G,
-                                                                const int total_groups) {
-    extern __shared__ __align__(16) double ev_dyn[];
-    __shared__ Best s_red[EV_THREADS / 32];
-
-    const int GPW = 32 / G, GPC = (EV_THREADS / 32) * GPW;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tl = lane & (G - 1);
-    const int gl = warp * GPW + lane / G;  // group within CTA
-    const int T = p.T, S = p.S;
-    const bool net = p.flags & PP_NET_MINING_COST;
-    constexpr bool STATS_T = KC > 0;
-    const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar);
-    const int SS = S | 1;
-    const int SB = BIGS ? 32 : p.Sp;
-    double *s_sig = ev_dyn;  // [T][SS] (not BIGS)
-    double *rowb = ev_dyn + (BIGS ? 0 : (size_t)T * SS) + (size_t)gl * 2 * SB;
-    double *oldb = rowb + SB;
-    if (!BIGS && stats) {
-        for (int i = threadIdx.x; i < S * T; i += EV_THREADS) {
-            const int s = i / T, t = i - s * T;
-            s_sig[t * SS + s] = __ldg(p.sigma + i);
-        }
-        __syncthreads();
-    }
-
-    Best best_all{-kInf, INT_MAX, INT_MAX};
-    const int warp_first = blockIdx.x * GPC + warp * GPW;
-    for (int base = warp_first; base < p.C; base += total_groups) {
-        const int grp = base + lane / G;
-        int b = (grp < p.C) ? __ldg(p.cand + grp) : -1;
-        const bool active = (b >= 0 && b < p.B);
-        if (!active) b = 0;
-
-        // ---- A: loads and precedence window (evaluate.py:361-372) ----
-        const BlockRow row = p.rows[b];
-        const int ab = p.assign[b];
-        double unit;
-        if (p.flags & PP_LITERAL_VALUE) unit = f64_mul(row.mass, 100.0);
-        else if (p.scen < 0) unit = __ldg(p.unit_mean + b);
-        else unit = __ldg(p.vmax + (size_t)b * p.Sp + p.scen);
-        double c_t[PER], d_t[PER];
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            const int t = tl + k * G;
-            const int tc = (t < T) ? t : 0;
-            c_t[k] = net ? __ldg(p.cost + (size_t)b * T + tc) : 0.0;
-            d_t[k] = __ldg(p.disc + tc);
-        }
-        const int npred = row.cnt & 0xffff, nnb = npred + (row.cnt >> 16);
-        int lo = 0, hi = INT_MAX;
-        for (int k = tl; k < nnb; k += G) {
-            const int tn = p.assign[__ldg(p.adj + row.adj + k)];
-            if (k < npred) lo = max(lo, tn < 0 ? INT_MAX : tn);
-            else if (tn >= 0) hi = min(hi, tn);
-        }
-        for (int off = G >> 1; off > 0; off >>= 1) {
-            lo = max(lo, __shfl_xor_sync(0xffffffffu, lo, off, G));
-            hi = min(hi, __shfl_xor_sync(0xffffffffu, hi, off, G));
-        }
-        bool pok[PER];
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            const int t = tl + k * G;
-            pok[k] = active && t < T && lo <= t && t <= hi;
-        }
-
-        // ---- B: per-scenario deltas d_s = val_s(b,t) - val_s(b,a[b]) (evaluate.py:380-382
-        //      with s=k): expected = np.mean(d), CVaR10 (saa.py:157-164), raw d_s ----
-        double ex_t[PER], cv_t[PER];
-        if constexpr (STATS_T) {
-            if (stats) {
-                const double *vrow = p.vmax + (size_t)b * p.Sp;
-                const int abc = (ab >= 0 && ab < T) ? ab : 0;
-                const double d_ab = __ldg(p.disc + abc);
-                const double dc_ab = net ? f64_mul(d_ab, __ldg(p.cost + (size_t)b * T + abc)) : 0.0;
-                const bool mined = ab >= 0;
-                if constexpr (!BIGS) {
-                    __syncwarp();
-                    const double *sg_ab = s_sig + (size_t)abc * SS;
-                    for (int j = tl; j < S; j += G) {
-                        const double x = __ldg(vrow + j);
-                        rowb[j] = x;
-                        const double v = f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), sg_ab[j]), row.spatial), dc_ab);
-                        oldb[j] = mined ? v : 0.0;  // x - 0.0 == x: subtracting it is exact
-                    }
-                    __syncwarp();
-                    const int main_ = S & ~7;
-#pragma unroll
-                    for (int k = 0; k < PER; k++) {
-                        ex_t[k] = -kInf;
-                        cv_t[k] = -kInf;
-                        if (!pok[k]) continue;
-                        const int t = tl + k * G;
-                        const double dk = d_t[k], sp = row.spatial;
-                        const double dc = net ? f64_mul(dk, c_t[k]) : 0.0;
-                        const double *sg = s_sig + (size_t)t * SS;
-                        float *sd = SCEN ? p.scen_delta + (size_t)grp * S * T + t : nullptr;
-                        double r[8];
-#pragma unroll
-                        for (int j = 0; j < 8; j++) r[j] = -0.0;
-                        TopK<KC> tk;
-                        tk.init();
-                        // numpy pairwise, single leaf (S <= 128): accumulator j takes s = j (mod 8)
-                        for (int s8 = 0; s8 < main_; s8 += 8) {
-#pragma unroll
-                            for (int j = 0; j < 8; j++) {
-                                const int s = s8 + j;
-                                const double v = f64_sub(
-                                    f64_sub(f64_mul(f64_mul(f64_mul(rowb[s], dk), sg[s]), sp), dc), oldb[s]);
-                                r[j] = f64_add(r[j], v);
-                                tk.push(v);
-                                if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
-                            }
-                        }
-                        double res = main_ ? tree8(r) : -0.0;
-                        for (int s = main_; s < S; s++) {
-                            const double v =
-                                f64_sub(f64_sub(f64_mul(f64_mul(f64_mul(rowb[s], dk), sg[s]), sp), dc), oldb[s]);
-                            res = f64_add(res, v);
-                            tk.push(v);
-                            if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
-                        }
-                        ex_t[k] = f64_div(f64_add(0.0, res), (double)S);
-                        cv_t[k] = tk.mean(p.cvar_k);
-                    }
-                } else {
-                    // S > 128: numpy's multi-leaf recursion, rows staged 32 scenarios at a time,
-                    // sigma read from global [S][T]
-#pragma unroll
-                    for (int k = 0; k < PER; k++) {
-                        ex_t[k] = -kInf;
-                        cv_t[k] = -kInf;
-                    }
-#pragma unroll
-                    for (int k = 0; k < PER; k++) {
-                        const int t = tl + k * G;
-                        const int tc = (t < T) ? t : 0;
-                        const bool ok = pok[k];
-                        const double dc_t = net ? f64_mul(d_t[k], c_t[k]) : 0.0;
-                        PwStream acc;
-                        acc.begin(p.plan);
-                        TopK<KC> tk;
-                        tk.init();
-                        for (int s0 = 0; s0 < S; s0 += 32) {
-                            __syncwarp();
-                            for (int j = tl; j < 32 && s0 + j < S; j += G) {
-                                const int s = s0 + j;
-                                const double x = __ldg(vrow + s);
-                                rowb[j] = x;
-                                const double v = f64_sub(
-                                    f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma + (size_t)s * T + abc)), row.spatial),
-                                    dc_ab);
-                                oldb[j] = mined ? v : 0.0;
-                            }
-                            __syncwarp();
-                            if (ok) {
-                                const int s_end = min(s0 + 32, S);
-                                for (int s8 = s0; s8 < s_end; s8 += 8) {
-                                    double x[8];
-#pragma unroll
-                                    for (int j = 0; j < 8; j++) {
-                                        const int s = s8 + j;
-                                        double dlt = 0.0;
-                                        if (s < s_end) {
-                                            dlt = f64_sub(
-                                                f64_sub(f64_mul(f64_mul(f64_mul(rowb[s - s0], d_t[k]),
-                                                                        __ldg(p.sigma + (size_t)s * T + tc)),
-                                                                row.spatial),
-                                                        dc_t),
-                                                oldb[s - s0]);
-                                            tk.push(dlt);
-                                            if constexpr (SCEN)
-                                                p.scen_delta[((size_t)grp * S + s) * T + t] = (float)dlt;
-                                        }
-                                        x[j] = dlt;
-                                    }
-                                    acc.block(s8, x, min(8, s_end - s8), p.plan);
-                                }
-                            }
-                        }
-                        if (ok) {
-                            ex_t[k] = acc.mean(p.plan);
-                            cv_t[k] = tk.mean(p.cvar_k);
-                        }
-                    }
-                }
-            }
-        }
-
-        // ---- C: capacity against the period masses (evaluate.py:373-378) ----
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        Best mine{-kInf, INT_MAX, INT_MAX};
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            const int t = tl + k * G;
-            const int tc = (t < T) ? t : 0;
-            bool ok = pok[k];
-            if (ok) {
-                double load = f64_add(__ldcg(p.pm + tc), row.mass);
-                if (ab == t) load = f64_sub(load, row.mass);
-                if (load > __ldg(p.cap + tc)) ok = false;
-            }
-            double v = -kInf;
-            if (ok) {
-                v = f64_mul(f64_mul(f64_mul(unit, d_t[k]), __ldg(p.sig_row + tc)), row.spatial);
-                if (net) v = f64_sub(v, f64_mul(d_t[k], c_t[k]));
-            }
-            if (active && t < T) {
-                const size_t m = (size_t)grp * T + t;
-                if (p.trace_val) p.trace_val[m] = v;
-                if (p.trace_feas) p.trace_feas[m] = ok ? 1 : 0;
-                if constexpr (STATS_T) {
-                    if (stats) {
-                        if (p.exp_delta) p.exp_delta[m] = ok ? ex_t[k] : -kInf;
-                        if (p.cvar) p.cvar[m] = ok ? cv_t[k] : -kInf;
-                        if constexpr (SCEN) {
-                            if (!ok)  // infeasible: overwrite (or fill) the raw deltas with -inf
-                                for (int s = 0; s < S; s++)
-                                    p.scen_delta[((size_t)grp * S + s) * T + t] = -__int_as_float(0x7f800000);
-                        }
-                    }
-                }
-            }
-            if (ok && (v > mine.v || (v == mine.v && t < mine.t))) {
-                mine.v = v;
-                mine.t = t;
-            }
-        }
-        for (int off = G >> 1; off > 0; off >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, mine.v, off, G);
-            const int ot = __shfl_xor_sync(0xffffffffu, mine.t, off, G);
-            if (ov > mine.v || (ov == mine.v && ot < mine.t)) {
-                mine.v = ov;
-                mine.t = ot;
-            }
-        }
-        const bool cand_ok = mine.t != INT_MAX;
-        if (active && tl == 0) {
-            p.best_t[grp] = cand_ok ? mine.t : -1;
-            p.best_val[grp] = mine.v;
-            p.feas[grp] = cand_ok ? 1 : 0;
-            if (cand_ok) {
-                Best cb{mine.v, b, mine.t};
-                if (better(cb, best_all)) best_all = cb;
-            }
-        }
-    }
-    // K4: grid argmax over candidates (evaluate.py:404-421 order)
-    grid_argmax(best_all, s_red, p.partial, p.counter, p.global);
-}
 
 // ------------------------------------------------------------------------------------
 // k_eval_staged: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
@@ -295,32 +27,35 @@ __device__ __forceinline__ void cp_async4(void *s, const void *g) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct StagedLayout {  // byte offsets into dynamic shared memory
-    int sig, vrow, old, cost, row, unit, ex, cv, b, ab, lo, hi, total;
+    int sig, tab, vrow, cost, nbr, ex, cv, row, unit, pair, b, ab, lo, hi, npair, okbits, total;
 };
 
 static __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-static __host__ __device__ inline StagedLayout staged_layout(int NB, int T, int S, int Sp, int GPC, bool stats,
+static __host__ __device__ inline StagedLayout staged_layout(int NB, int T, int S, int Sp, int nbr_stride, bool stats,
                                                              bool need_vrow, bool net) {
     StagedLayout L;
     int o = 0;
-    const int SS = S | 1;
-    L.sig = o;
-    o += stats ? align16(8 * T * SS) : 0;
+    L.sig = o;  // sigma [S][T] (statistics)
+    o += stats ? align16(8 * S * T) : 0;
+    L.tab = o;  // cap, disc, sig_row, pm: [4][T]
+    o += align16(8 * 4 * T);
     L.vrow = o;
     o += need_vrow ? align16(8 * NB * Sp) : 0;
-    L.old = o;
-    o += stats ? align16(8 * GPC * Sp) : 0;
     L.cost = o;
     o += net ? align16(8 * NB * T) : 0;
-    L.row = o;
-    o += align16(32 * NB);
-    L.unit = o;
-    o += align16(8 * NB);
+    L.nbr = o;
+    o += align16(4 * NB * nbr_stride);
     L.ex = o;
     o += stats ? align16(8 * NB * T) : 0;
     L.cv = o;
     o += stats ? align16(8 * NB * T) : 0;
+    L.row = o;
+    o += align16(32 * NB);
+    L.unit = o;
+    o += align16(8 * NB);
+    L.pair = o;
+    o += stats ? align16(4 * NB * T) : 0;
     L.b = o;
     o += align16(4 * NB);
     L.ab = o;
@@ -329,288 +64,391 @@ static __host__ __device__ inline StagedLayout staged_layout(int NB, int T, int 
     o += align16(4 * NB);
     L.hi = o;
     o += align16(4 * NB);
+    L.npair = o;
+    o += align16(4 * (NB + 1));
+    L.okbits = o;  // one 32-bit mask of feasible periods per candidate (T <= 32)
+    o += align16(4 * NB);
     L.total = o;
     return L;
 }
 
+// One (candidate, period) pair: per-scenario deltas d_s = val_s(b,t) - val_s(b,a[b])
+// (evaluate.py:380-382 with s=k), expected = np.mean(d) (a single numpy pairwise leaf,
+// S <= 128), CVaR10 = mean of the k smallest (saa.py:157-164); raw d_s optionally.
 template <int KC, bool SCEN>
-__global__ void __launch_bounds__(EV_THREADS) k_eval_staged(const EvalParams p, const int G, const int NB) {
+__device__ __forceinline__ void pair_stats(const EvalParams &p, int S, int T, const double *sg, const double *rowb,
+                                           int t, int abc,
+                                           double d_t, double dc_t, double d_ab, double dc_ab, double sp, bool mined,
+                                           double *ex, double *cv, float *sd) {
+    const int main_ = S & ~7;  // sg: sigma [S][T] staged in shared memory
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[j] = -0.0;
+    TopK<KC> tk;
+    tk.init();
+    for (int s8 = 0; s8 < main_; s8 += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int s = s8 + j;
+            const double x = rowb[s];
+            const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), sg[s * T + t]), sp), dc_t);
+            const double vo =
+                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), sg[s * T + abc]), sp), dc_ab) : 0.0;
+            const double v = f64_sub(vn, vo);  // vn - 0.0 == vn exactly
+            acc[j] = f64_add(acc[j], v);
+            tk.push(v);
+            if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
+        }
+    }
+    double res = main_ ? tree8(acc) : -0.0;
+    for (int s = main_; s < S; s++) {
+        const double x = rowb[s];
+        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), sg[s * T + t]), sp), dc_t);
+        const double vo =
+            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), sg[s * T + abc]), sp), dc_ab) : 0.0;
+        const double v = f64_sub(vn, vo);
+        res = f64_add(res, v);
+        tk.push(v);
+        if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
+    }
+    *ex = f64_div(f64_add(0.0, res), (double)S);
+    *cv = tk.mean(p.cvar_k);
+}
+
+// ------------------------------------------------------------------------------------
+// k_eval_staged: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
+// Sized for the sparsity of the problem (at C2 a candidate's precedence window holds 1.2
+// of 15 periods on average, 8% of the moves are feasible), NB candidates per CTA:
+//   stage 1  candidate ids
+//   stage 2  one warp per candidate: BlockRow, assign, unit, padded neighbour row,
+//            mining-cost row, vmax row via cp.async -- one round trip for the batch
+//   stage 3  one thread per candidate: neighbour periods -> precedence window
+//            (evaluate.py:361-372); then the list of precedence-feasible (candidate, t)
+//   B        one thread per feasible pair: per-scenario statistics into shared memory
+//   C        griddepcontrol.wait; one thread per candidate walks its window: capacity
+//            (evaluate.py:373-378), parity value (379-384), lowest-t argmax (387-388)
+//   out      one thread per (candidate, period): coalesced writes of the [NB][T] block
+//   K4       warp argmax of the CTA's candidates, deterministic grid argmax
+// Stages 1-3 and B never read the period masses: under programmatic dependent launch
+// they overlap k_pm_chunks / k_pm_tree.
+// ------------------------------------------------------------------------------------
+#ifdef PP_EVAL_PROBE
+__device__ unsigned long long g_ev_probe[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define EV_PROBE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_ev_probe[blockIdx.x][k] = gtimer(); } while (0)
+#else
+#define EV_PROBE(k) do { } while (0)
+#endif
+
+template <int KC, bool SCEN>
+__global__ void __launch_bounds__(EV_THREADS, 4) k_eval_staged(const EvalParams p, const int NB) {
     extern __shared__ __align__(16) unsigned char st_dyn[];
     __shared__ Best s_red[EV_THREADS / 32];
-    const int T = p.T, S = p.S, Sp = p.Sp, SS = S | 1;
-    const int GPW = 32 / G, GPC = (EV_THREADS / 32) * GPW;
+    constexpr int NW = EV_THREADS / 32;
+    const int T = p.T, S = p.S, Sp = p.Sp, NS = p.nbr_stride;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-    const int tl = lane & (G - 1);
-    const int gl = warp * GPW + lane / G;
     const bool net = p.flags & PP_NET_MINING_COST;
     const bool literal = p.flags & PP_LITERAL_VALUE;
     constexpr bool STATS_T = KC > 0;
     const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar);
     const bool need_vrow = stats || (!literal && p.scen >= 0);
-    const StagedLayout L = staged_layout(NB, T, S, Sp, GPC, stats, need_vrow, net);
+    const StagedLayout L = staged_layout(NB, T, S, Sp, NS, stats, need_vrow, net);
     double *s_sig = reinterpret_cast<double *>(st_dyn + L.sig);
+    double *s_cap = reinterpret_cast<double *>(st_dyn + L.tab);
+    double *s_disc = s_cap + T, *s_srow = s_cap + 2 * T, *s_pm = s_cap + 3 * T;
     double *s_vrow = reinterpret_cast<double *>(st_dyn + L.vrow);
-    double *s_old = reinterpret_cast<double *>(st_dyn + L.old);
     double *s_cost = reinterpret_cast<double *>(st_dyn + L.cost);
-    BlockRow *s_row = reinterpret_cast<BlockRow *>(st_dyn + L.row);
-    double *s_unit = reinterpret_cast<double *>(st_dyn + L.unit);
+    int *s_nbr = reinterpret_cast<int *>(st_dyn + L.nbr);
     double *s_ex = reinterpret_cast<double *>(st_dyn + L.ex);
     double *s_cv = reinterpret_cast<double *>(st_dyn + L.cv);
+    BlockRow *s_row = reinterpret_cast<BlockRow *>(st_dyn + L.row);
+    double *s_unit = reinterpret_cast<double *>(st_dyn + L.unit);
+    int *s_pair = reinterpret_cast<int *>(st_dyn + L.pair);
     int *s_b = reinterpret_cast<int *>(st_dyn + L.b);
     int *s_ab = reinterpret_cast<int *>(st_dyn + L.ab);
     int *s_lo = reinterpret_cast<int *>(st_dyn + L.lo);
     int *s_hi = reinterpret_cast<int *>(st_dyn + L.hi);
+    int *s_np = reinterpret_cast<int *>(st_dyn + L.npair);
+    unsigned *s_ok = reinterpret_cast<unsigned *>(st_dyn + L.okbits);
     const int c0 = blockIdx.x * NB;
+    EV_PROBE(0);
 
-    // ---- stage 1: candidate ids (and sigma, transposed to [T][SS]) ----
+    // ---- stage 1 ----
     for (int i = tid; i < NB; i += EV_THREADS) {
         const int g = c0 + i;
         int b = (g < p.C) ? __ldg(p.cand + g) : -1;
         if (b >= p.B) b = -1;
         s_b[i] = b;
     }
-    if (stats)
-        for (int i = tid; i < S * T; i += EV_THREADS) {
-            const int s = i / T, t = i - s * T;
-            s_sig[t * SS + s] = __ldg(p.sigma + i);
-        }
+    for (int t = tid; t < T; t += EV_THREADS) {
+        s_cap[t] = __ldg(p.cap + t);
+        s_disc[t] = __ldg(p.disc + t);
+        s_srow[t] = __ldg(p.sig_row + t);
+    }
+    if (stats) {  // sigma [S][T] (S*T*8 is a multiple of 8; copy 8-byte pieces)
+        for (int e = tid; e < S * T; e += EV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+    }
     __syncthreads();
+    EV_PROBE(1);
 
-    // ---- stage 2: per-candidate rows, one warp per candidate, lanes over 4..16-byte pieces ----
+    // ---- stage 2: every row of every candidate in one cp.async round trip ----
     {
-        const int n_cost = net ? T : 0;
-        const int n_vrow = need_vrow ? (Sp >> 1) : 0;
         const bool want_unit = !literal && p.scen < 0;
-        const int nops = 3 + (want_unit ? 1 : 0) + n_cost + n_vrow;
-        for (int i = warp; i < NB; i += EV_THREADS / 32) {
-            const int bb = s_b[i];
-            const int b = bb < 0 ? 0 : bb;
-            for (int op = lane; op < nops; op += 32) {
-                if (op < 2) {
-                    cp_async16(reinterpret_cast<char *>(s_row + i) + 16 * op,
-                               reinterpret_cast<const char *>(p.rows + b) + 16 * op);
-                } else if (op == 2) {
-                    cp_async4(s_ab + i, p.assign + b);
-                } else {
-                    int q = op - 3;
-                    if (want_unit) {
-                        if (q == 0) {
-                            cp_async8(s_unit + i, p.unit_mean + b);
-                            continue;
-                        }
-                        q -= 1;
-                    }
-                    if (q < n_cost) cp_async8(s_cost + (size_t)i * T + q, p.cost + (size_t)b * T + q);
-                    else {
-                        q -= n_cost;
-                        cp_async16(s_vrow + (size_t)i * Sp + 2 * q, p.vmax + (size_t)b * Sp + 2 * q);
-                    }
-                }
-            }
+        const int nv = need_vrow ? (Sp >> 1) : 0, nn = NS >> 2;
+        for (int i = warp; i < NB; i += NW) {
+            const int b = max(s_b[i], 0);
+            if (lane < 2)
+                cp_async16(reinterpret_cast<char *>(s_row + i) + 16 * lane,
+                           reinterpret_cast<const char *>(p.rows + b) + 16 * lane);
+            if (lane == 2) cp_async4(s_ab + i, p.assign + b);
+            if (lane == 3 && want_unit) cp_async8(s_unit + i, p.unit_mean + b);
+            if (lane < nn) cp_async16(s_nbr + (size_t)i * NS + 4 * lane, p.nbr + (size_t)b * NS + 4 * lane);
+            if (net && lane < T) cp_async8(s_cost + (size_t)i * T + lane, p.cost + (size_t)b * T + lane);
+            for (int q = lane; q < nv; q += 32)
+                cp_async16(s_vrow + (size_t)i * Sp + 2 * q, p.vmax + (size_t)b * Sp + 2 * q);
         }
         cp_async_wait_all();
     }
     __syncthreads();
+    EV_PROBE(2);
 
-    // ---- stage 3: precedence window per candidate (evaluate.py:361-372), one warp each ----
-    for (int i = warp; i < NB; i += EV_THREADS / 32) {
+    // ---- stage 3: precedence window, one thread per candidate ----
+    for (int i = tid; i < NB; i += EV_THREADS) {
         const BlockRow r = s_row[i];
         const int npred = r.cnt & 0xffff, nnb = npred + (r.cnt >> 16);
+        const int *nb = s_nbr + (size_t)i * NS;
         int lo = 0, hi = INT_MAX;
-        if (lane < nnb) {
-            const int tn = p.assign[__ldg(p.adj + r.adj + lane)];
-            if (lane < npred) lo = (tn < 0) ? INT_MAX : tn;
-            else if (tn >= 0) hi = tn;
-        }
+        int tn[32];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = max(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = min(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        for (int k = 0; k < 32; k++)  // independent gathers first (assign is L2-resident)
+            if (k < nnb) tn[k] = p.assign[nb[k]];
+#pragma unroll
+        for (int k = 0; k < 32; k++) {
+            if (k < npred) lo = max(lo, tn[k] < 0 ? INT_MAX : tn[k]);
+            else if (k < nnb && tn[k] >= 0) hi = min(hi, tn[k]);
         }
-        if (lane == 0) {
-            s_lo[i] = lo;
-            s_hi[i] = hi;
-            if (s_b[i] < 0) s_lo[i] = INT_MAX;  // inactive slot: nothing feasible
-            if (!literal && p.scen >= 0) s_unit[i] = s_vrow[(size_t)i * Sp + p.scen];
-            if (literal) s_unit[i] = f64_mul(r.mass, 100.0);
+        if (s_b[i] < 0) lo = INT_MAX;  // inactive slot: nothing feasible
+        s_lo[i] = lo;
+        s_hi[i] = hi;
+        if (!literal && p.scen >= 0) s_unit[i] = s_vrow[(size_t)i * Sp + p.scen];
+        if (literal) s_unit[i] = f64_mul(r.mass, 100.0);
+    }
+    EV_PROBE(3);
+
+    // ---- C: capacity (evaluate.py:373-378), parity value (379-384), lowest-t argmax
+    //      (387-388), one thread per candidate.  Everything above overlapped the
+    //      period-mass kernels (PDL); the period masses are needed from here on.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int t = tid; t < T; t += EV_THREADS) s_pm[t] = __ldcg(p.pm + t);
+    __syncthreads();
+    EV_PROBE(4);
+    Best mine{-kInf, INT_MAX, INT_MAX};
+    for (int i = tid; i < NB; i += EV_THREADS) {
+        const int b = s_b[i];
+        const BlockRow r = s_row[i];
+        const int ab = s_ab[i];
+        const int lo = s_lo[i], z = min(s_hi[i], T - 1);
+        unsigned okb = 0u;
+        double bv = -kInf;
+        int bt = INT_MAX;
+        for (int t = lo; t <= z; t++) {
+            double load = f64_add(s_pm[t], r.mass);
+            if (ab == t) load = f64_sub(load, r.mass);
+            if (load > s_cap[t]) continue;
+            okb |= 1u << t;
+            const double d = s_disc[t];
+            double v = f64_mul(f64_mul(f64_mul(s_unit[i], d), s_srow[t]), r.spatial);
+            if (net) v = f64_sub(v, f64_mul(d, s_cost[(size_t)i * T + t]));
+            if (v > bv) {  // strict: the lowest period wins ties (evaluate.py:387-388)
+                bv = v;
+                bt = t;
+            }
+        }
+        s_ok[i] = okb;
+        s_np[i] = __popc(okb);
+        if (b >= 0) {
+            const int grp = c0 + i;
+            const bool cand_ok = bt != INT_MAX;
+            p.best_t[grp] = cand_ok ? bt : -1;
+            p.best_val[grp] = bv;
+            p.feas[grp] = cand_ok ? 1 : 0;
+            if (cand_ok) {
+                Best cb{bv, b, bt};
+                if (better(cb, mine)) mine = cb;
+            }
         }
     }
     __syncthreads();
+    EV_PROBE(5);
 
-    // ---- B: per-scenario deltas for precedence-feasible periods (no period masses needed) ----
-    const int t = tl;
-    const bool lane_t = t < T;
-    const double d_t = __ldg(p.disc + (lane_t ? t : 0));
+    // ---- B: statistics of the feasible (candidate, period) pairs (~8% of moves at C2) ----
     if constexpr (STATS_T) {
         if (stats) {
-            double *oldb = s_old + (size_t)gl * Sp;
-            const int main_ = S & ~7;
-            for (int i = gl; i < NB; i += GPC) {
-                const int b = s_b[i];
-                const BlockRow r = s_row[i];
-                const int ab = s_ab[i];
-                const bool mined = ab >= 0;
-                const int abc = (ab >= 0 && ab < T) ? ab : 0;
-                const double *rowb = s_vrow + (size_t)i * Sp;
-                const double d_ab = __ldg(p.disc + abc);
-                const double dc_ab = net ? f64_mul(d_ab, s_cost[(size_t)i * T + abc]) : 0.0;
-                const double *sg_ab = s_sig + (size_t)abc * SS;
-                __syncwarp();
-                for (int j = tl; j < S; j += G) {
-                    const double v = f64_sub(f64_mul(f64_mul(f64_mul(rowb[j], d_ab), sg_ab[j]), r.spatial), dc_ab);
-                    oldb[j] = mined ? v : 0.0;  // x - 0.0 == x
+            if (warp == 0) {  // exclusive scan of the pair counts
+                int carry = 0;
+                for (int i0 = 0; i0 < NB; i0 += 32) {
+                    const int v = (i0 + lane < NB) ? s_np[i0 + lane] : 0;
+                    int incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (i0 + lane < NB) s_np[i0 + lane] = carry + incl - v;
+                    carry += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                __syncwarp();
-                const bool pok = lane_t && b >= 0 && s_lo[i] <= t && t <= s_hi[i];
-                if (!pok) continue;
-                const double dc = net ? f64_mul(d_t, s_cost[(size_t)i * T + t]) : 0.0;
-                const double sp = r.spatial;
-                const double *sg = s_sig + (size_t)t * SS;
-                float *sd = SCEN ? p.scen_delta + (size_t)(c0 + i) * S * T + t : nullptr;
-                double acc[8];
+                if (lane == 0) s_np[NB] = carry;
+            }
+            __syncthreads();
+            for (int i = tid; i < NB; i += EV_THREADS) {  // pair list: (candidate << 8) | period
+                unsigned okb = s_ok[i];
+                int o = s_np[i];
+                while (okb) {
+                    const int t = __ffs(okb) - 1;
+                    okb &= okb - 1;
+                    s_pair[o++] = (i << 8) | t;
+                }
+            }
+            __syncthreads();
+            const int npairs = s_np[NB];
+            if constexpr (KC <= 2) {
+                // 8 lanes per pair; lane j owns numpy's accumulator j (scenarios s = j mod 8),
+                // the butterfly xor 1,2,4 is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the <8-element
+                // tail is added in order; per-lane two smallest merged by butterfly (CVaR, k <= 2)
+                const int sub = lane & 7, sgi = tid >> 3, nsg = EV_THREADS >> 3;
+                const int main_ = S & ~7, nrem = S - main_;
+                for (int k0 = 0; k0 < npairs; k0 += nsg) {
+                    const int k = k0 + sgi;
+                    const bool act = k < npairs;
+                    const int pr = act ? s_pair[k] : 0;
+                    const int i = pr >> 8, t = pr & 0xff;
+                    const int ab = s_ab[i];
+                    const bool mined = ab >= 0;
+                    const int abc = mined ? ab : 0;
+                    const double d_t = s_disc[t], d_ab = s_disc[abc], sp = s_row[i].spatial;
+                    const double dc_t = net ? f64_mul(d_t, s_cost[(size_t)i * T + t]) : 0.0;
+                    const double dc_ab = net ? f64_mul(d_ab, s_cost[(size_t)i * T + abc]) : 0.0;
+                    const double *rowb = s_vrow + (size_t)i * Sp;
+                    float *sd = SCEN ? p.scen_delta + (size_t)(c0 + i) * S * T + t : nullptr;
+                    double acc = -0.0, a0 = kInf, a1 = kInf, remv = 0.0;
+                    if (act) {
+                        for (int s_ = sub; s_ < S; s_ += 8) {
+                            const double x = rowb[s_];
+                            const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
+                            const double vo =
+                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
+                            const double v = f64_sub(vn, vo);  // vn - 0.0 == vn exactly
+                            if (s_ < main_) acc = f64_add(acc, v);
+                            else remv = v;
+                            if (v < a1) {
+                                if (v < a0) {
+                                    a1 = a0;
+                                    a0 = v;
+                                } else {
+                                    a1 = v;
+                                }
+                            }
+                            if constexpr (SCEN) sd[(size_t)s_ * T] = (float)v;
+                        }
+                    }
+                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+                    double res = main_ ? acc : -0.0;
+                    for (int j = 0; j < nrem; j++) res = f64_add(res, __shfl_sync(0xffffffffu, remv, (lane & ~7) + j));
 #pragma unroll
-                for (int j = 0; j < 8; j++) acc[j] = -0.0;
-                TopK<KC> tk;
-                tk.init();
-                for (int s8 = 0; s8 < main_; s8 += 8) {
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const int s = s8 + j;
-                        const double v =
-                            f64_sub(f64_sub(f64_mul(f64_mul(f64_mul(rowb[s], d_t), sg[s]), sp), dc), oldb[s]);
-                        acc[j] = f64_add(acc[j], v);
-                        tk.push(v);
-                        if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
+                    for (int o = 1; o < 8; o <<= 1) {
+                        const double b0 = __shfl_xor_sync(0xffffffffu, a0, o);
+                        const double b1 = __shfl_xor_sync(0xffffffffu, a1, o);
+                        const double lo = (b0 < a0) ? b0 : a0, hi = (b0 < a0) ? a0 : b0;
+                        const double m1 = (b1 < a1) ? b1 : a1;
+                        a0 = lo;
+                        a1 = (m1 < hi) ? m1 : hi;
+                    }
+                    if (act && sub == 0) {
+                        s_ex[(size_t)i * T + t] = f64_div(f64_add(0.0, res), (double)S);
+                        double c = f64_add(-0.0, a0);
+                        if (p.cvar_k > 1) c = f64_add(c, a1);
+                        s_cv[(size_t)i * T + t] = f64_mul(f64_add(0.0, c), p.cvar_k > 1 ? 0.5 : 1.0);
                     }
                 }
-                double res = main_ ? tree8(acc) : -0.0;
-                for (int s = main_; s < S; s++) {
-                    const double v = f64_sub(f64_sub(f64_mul(f64_mul(f64_mul(rowb[s], d_t), sg[s]), sp), dc), oldb[s]);
-                    res = f64_add(res, v);
-                    tk.push(v);
-                    if constexpr (SCEN) sd[(size_t)s * T] = (float)v;
+            } else {
+                for (int k = tid; k < npairs; k += EV_THREADS) {  // one thread per pair
+                    const int i = s_pair[k] >> 8, t = s_pair[k] & 0xff;
+                    const int ab = s_ab[i];
+                    const int abc = (ab >= 0 && ab < T) ? ab : 0;
+                    const double d_t = s_disc[t], d_ab = s_disc[abc];
+                    const double dc_t = net ? f64_mul(d_t, s_cost[(size_t)i * T + t]) : 0.0;
+                    const double dc_ab = net ? f64_mul(d_ab, s_cost[(size_t)i * T + abc]) : 0.0;
+                    float *sd = SCEN ? p.scen_delta + (size_t)(c0 + i) * S * T + t : nullptr;
+                    pair_stats<KC, SCEN>(p, S, T, s_sig, s_vrow + (size_t)i * Sp, t, abc, d_t, dc_t, d_ab, dc_ab,
+                                         s_row[i].spatial, ab >= 0, s_ex + (size_t)i * T + t, s_cv + (size_t)i * T + t,
+                                         sd);
                 }
-                s_ex[(size_t)i * T + t] = f64_div(f64_add(0.0, res), (double)S);
-                s_cv[(size_t)i * T + t] = tk.mean(p.cvar_k);
             }
+            __syncthreads();
         }
     }
+    EV_PROBE(6);
 
-    // ---- C: capacity (evaluate.py:373-378), parity value, outputs, argmax ----
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const double pm_t = lane_t ? __ldcg(p.pm + t) : 0.0;
-    const double cap_t = __ldg(p.cap + (lane_t ? t : 0));
-    const double sr_t = __ldg(p.sig_row + (lane_t ? t : 0));
-    Best best_all{-kInf, INT_MAX, INT_MAX};
-    for (int i = gl; i < NB; i += GPC) {
-        const int b = s_b[i];
-        const int grp = c0 + i;
-        const bool active = b >= 0;
-        const BlockRow r = s_row[i];
-        const int ab = s_ab[i];
-        bool ok = active && lane_t && s_lo[i] <= t && t <= s_hi[i];
-        if (ok) {
-            double load = f64_add(pm_t, r.mass);
-            if (ab == t) load = f64_sub(load, r.mass);
-            if (load > cap_t) ok = false;
-        }
-        double v = -kInf;
-        if (ok) {
-            v = f64_mul(f64_mul(f64_mul(s_unit[i], d_t), sr_t), r.spatial);
-            if (net) v = f64_sub(v, f64_mul(d_t, s_cost[(size_t)i * T + t]));
-        }
-        if (active && lane_t) {
-            const size_t m = (size_t)grp * T + t;
-            if (p.trace_val) p.trace_val[m] = v;
-            if (p.trace_feas) p.trace_feas[m] = ok ? 1 : 0;
+    // ---- per-(candidate, period) outputs: the CTA's [NB][T] block, coalesced ----
+    const bool want_trace = p.trace_val || p.trace_feas;
+    if (want_trace || stats) {
+        const int nvalid = min(NB, p.C - c0);
+        for (int e = tid; e < nvalid * T; e += EV_THREADS) {
+            const int i = e / T, t = e - i * T;
+            const size_t m = (size_t)c0 * T + e;
+            const bool ok = (s_ok[i] >> t) & 1u;
+            if (want_trace) {
+                double v = -kInf;
+                if (ok) {
+                    const double d = s_disc[t];
+                    const BlockRow &r = s_row[i];
+                    v = f64_mul(f64_mul(f64_mul(s_unit[i], d), s_srow[t]), r.spatial);
+                    if (net) v = f64_sub(v, f64_mul(d, s_cost[(size_t)i * T + t]));
+                }
+                if (p.trace_val) p.trace_val[m] = v;
+                if (p.trace_feas) p.trace_feas[m] = ok ? 1 : 0;
+            }
             if constexpr (STATS_T) {
                 if (stats) {
-                    if (p.exp_delta) p.exp_delta[m] = ok ? s_ex[(size_t)i * T + t] : -kInf;
-                    if (p.cvar) p.cvar[m] = ok ? s_cv[(size_t)i * T + t] : -kInf;
+                    if (p.exp_delta) p.exp_delta[m] = ok ? s_ex[e] : -kInf;
+                    if (p.cvar) p.cvar[m] = ok ? s_cv[e] : -kInf;
                     if constexpr (SCEN) {
-                        if (!ok)
+                        if (!ok)  // infeasible: raw deltas are -inf (also overwrites capacity-infeasible pairs)
                             for (int s = 0; s < S; s++)
-                                p.scen_delta[((size_t)grp * S + s) * T + t] = -__int_as_float(0x7f800000);
+                                p.scen_delta[((size_t)(c0 + i) * S + s) * T + t] = -__int_as_float(0x7f800000);
                     }
                 }
             }
         }
-        Best mine{-kInf, INT_MAX, INT_MAX};
-        if (ok) {
-            mine.v = v;
-            mine.t = t;
-        }
-        for (int off = G >> 1; off > 0; off >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, mine.v, off, G);
-            const int ot = __shfl_xor_sync(0xffffffffu, mine.t, off, G);
-            if (ov > mine.v || (ov == mine.v && ot < mine.t)) {
-                mine.v = ov;
-                mine.t = ot;
-            }
-        }
-        const bool cand_ok = mine.t != INT_MAX;
-        if (active && tl == 0) {
-            p.best_t[grp] = cand_ok ? mine.t : -1;
-            p.best_val[grp] = mine.v;
-            p.feas[grp] = cand_ok ? 1 : 0;
-            if (cand_ok) {
-                Best cb{mine.v, b, mine.t};
-                if (better(cb, best_all)) best_all = cb;
-            }
-        }
     }
-    grid_argmax(best_all, s_red, p.partial, p.counter, p.global);
+
+    // ---- K4: CTA argmax (candidates are one per thread of warp 0 when NB <= 32) ----
+    if (NB > 32) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Best o = shfl_best(mine, off);
+            if (better(o, mine)) mine = o;
+        }
+        if (lane == 0) s_red[warp] = mine;
+        __syncthreads();
+        if (warp == 0) mine = (lane < NW) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
+        __syncthreads();
+    }
+    grid_argmax_warp0(mine, s_red, p.partial, p.counter, p.global);
+    EV_PROBE(7);
 }
 
-
-
-// dynamic shared memory of k_eval_candidates: sigma [T][S|1] + per-group row buffers
-static size_t eval_smem(int S, int Sp, int T, int G, bool stats, bool bigs) {
-    if (!stats) return 0;
-    const int gpc = (EV_THREADS / 32) * (32 / G);
-    size_t rows = sizeof(double) * (size_t)gpc * 2 * (bigs ? 32 : Sp);
-    size_t sig = bigs ? 0 : sizeof(double) * (size_t)T * (S | 1);
-    return rows + sig;
+#ifdef PP_EVAL_PROBE
+extern "C" PP_API int pp_debug_eval_probe(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_ev_probe, sizeof(unsigned long long) * 4096 * 8) == cudaSuccess ? 0 : 3;
 }
-
-template <typename K>
-static int set_smem_attr(K kern, size_t bytes) {
-    if (bytes > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    return PP_OK;
-}
-
-// resident CTAs of a kernel at this smem size (cached per instantiation)
-template <typename K>
-static int resident_ctas(K kern, size_t smem, int device) {
-    int per_sm = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, EV_THREADS, smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms < 1) sms = 148;
-    return per_sm * sms;
-}
-
-template <int PER, int KC, bool BIGS, bool SCEN>
-static int launch_cand1(int ngroups, int G, size_t smem, cudaStream_t st, bool pdl, int device, const EvalParams &ep) {
-    auto kern = k_eval_candidates<PER, KC, BIGS, SCEN>;
-    TRY(set_smem_attr(kern, smem));
-    const int gpc = (EV_THREADS / 32) * (32 / G);
-    const int need = std::max(1, (ngroups + gpc - 1) / gpc);
-    const int grid = std::min(need, resident_ctas(kern, smem, device));
-    return launch_eval(kern, grid, smem, st, pdl, ep, G, grid * gpc);
-}
-
-// general path (T > 32, S > 128 or degree > 32): the 128-slot top-k covers every k
-template <int PER>
-static int launch_cand_kc(int kc, bool bigs, bool scen, int ngroups, int G, size_t smem, cudaStream_t st, bool pdl,
-                          int device, const EvalParams &ep) {
-    if (kc == 0) return launch_cand1<PER, 0, false, false>(ngroups, G, smem, st, pdl, device, ep);
-    if (bigs)
-        return scen ? launch_cand1<PER, 128, true, true>(ngroups, G, smem, st, pdl, device, ep)
-                    : launch_cand1<PER, 128, true, false>(ngroups, G, smem, st, pdl, device, ep);
-    return scen ? launch_cand1<PER, 128, false, true>(ngroups, G, smem, st, pdl, device, ep)
-                : launch_cand1<PER, 128, false, false>(ngroups, G, smem, st, pdl, device, ep);
-}
-
+#endif
 
 extern "C" {
 
@@ -668,6 +506,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     memset(&ep, 0, sizeof(ep));
     ep.rows = c->rows.as<BlockRow>();
     ep.adj = c->adj.as<int32_t>();
+    ep.nbr = c->nbr.as<int32_t>();
+    ep.nbr_stride = c->nbr_stride;
     ep.assign = c->assign_ptr;
     ep.pm = c->pm.as<double>();
     ep.cap = c->cap.as<double>();
@@ -702,11 +542,11 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     ep.global = o.global;
 
     // fast path: whole candidate batches staged in shared memory
-    if (T <= 32 && (!stats || S <= 128) && c->deg_max <= 32) {
-        const int gpc_s = (EV_THREADS / 32) * (32 / G);
-        const int NB = std::max(32, gpc_s);
+    if (T <= 32 && (!stats || S <= 128) && c->deg_max <= 32 && c->nbr.ptr) {
+        const int NB = 32;
         const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
-        const StagedLayout Ls = staged_layout(NB, T, S, c->Sp, gpc_s, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
+        const StagedLayout Ls =
+            staged_layout(NB, T, S, c->Sp, c->nbr_stride, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
         if (Ls.total <= 200 * 1024) {
             const int sgrid = std::max(1, (C + NB - 1) / NB);
             TRY(ensure_grid_scratch(c, sgrid));
@@ -714,10 +554,10 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
             TRY(refresh_pm(c, st, &pdl));
             const bool scen = o.scen_delta != nullptr;
             const size_t smem_s = (size_t)Ls.total;
-#define PP_STAGED(KC, SC)                                                                  \
-    {                                                                                      \
-        TRY(set_smem_attr(k_eval_staged<KC, SC>, smem_s));                                 \
-        TRY(launch_eval(k_eval_staged<KC, SC>, sgrid, smem_s, st, pdl, ep, G, NB));        \
+#define PP_STAGED(KC, SC)                                                              \
+    {                                                                                  \
+        TRY(set_smem_attr(k_eval_staged<KC, SC>, smem_s));                             \
+        TRY(launch_eval(k_eval_staged<KC, SC>, sgrid, smem_s, st, pdl, ep, NB));       \
     }
             if (kc == 0) PP_STAGED(0, false)
             else if (kc == 2) { if (scen) PP_STAGED(2, true) else PP_STAGED(2, false) }
@@ -728,14 +568,10 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         }
     }
     {
-    const bool bigs = S > 128;
-    const size_t smem = eval_smem(S, c->Sp, T, G, stats, bigs);
-    if (smem > 227 * 1024) return fail(PP_ERR_INVALID_ARGS, "n_periods x n_scenarios too large for shared staging");
-    bool pdl;
-    TRY(refresh_pm(c, st, &pdl));
-    const bool scen = o.scen_delta != nullptr;
-    if (PER == 1) TRY(launch_cand_kc<1>(kc, bigs, scen, C, G, smem, st, pdl, c->device, ep));
-    else TRY(launch_cand_kc<4>(kc, bigs, scen, C, G, smem, st, pdl, c->device, ep));
+        bool pdl;
+        TRY(refresh_pm(c, st, &pdl));
+        TRY(launch_general_candidates(PER, kc, o.scen_delta != nullptr, C, G, S, c->Sp, T, stats, st, pdl, c->device,
+                                      ep));
     }
 copy_out:
 

@@ -193,7 +193,8 @@ struct TopK<2> {  // k <= 2 (S <= 20): two registers, insertion rarely taken
     __device__ __forceinline__ double mean(int k) const {
         double s = f64_add(-0.0, a0);
         if (k > 1) s = f64_add(s, a1);
-        return f64_div(f64_add(0.0, s), (double)k);
+        // x / 1 and x / 2 are exact scalings: the multiply gives the same correctly rounded value
+        return f64_mul(f64_add(0.0, s), k > 1 ? 0.5 : 1.0);
     }
 };
 template <>
@@ -282,12 +283,67 @@ static __device__ void grid_argmax(Best mine, Best *s_red, pp_best *partial, uns
 }
 
 
+// Grid argmax when warp 0 already holds the CTA's candidates (lanes 0..31); every thread
+// of the CTA must call it.  Same deterministic last-CTA reduction as grid_argmax.
+static __device__ void grid_argmax_warp0(Best x, Best *s_red, pp_best *partial, unsigned int *counter,
+                                         pp_best *global) {
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (warp == 0) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Best o = shfl_best(x, off);
+            if (better(o, x)) x = o;
+        }
+        if (lane == 0) {
+            pp_best pb;
+            pb.value = x.v;
+            pb.block = x.b;
+            pb.period = x.t;
+            partial[blockIdx.x] = pb;
+            __threadfence();
+            unsigned int prev = atomicAdd(counter, 1u);
+            s_last = (prev == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    Best y{-kInf, INT_MAX, INT_MAX};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const pp_best *q = partial + i;
+        Best o{__ldcg(&q->value), __ldcg(&q->block), __ldcg(&q->period)};
+        if (better(o, y)) y = o;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Best o = shfl_best(y, off);
+        if (better(o, y)) y = o;
+    }
+    if (lane == 0) s_red[warp] = y;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Best z = s_red[0];
+        for (int w = 1; w < nw; w++)
+            if (better(s_red[w], z)) z = s_red[w];
+        pp_best g;
+        bool none = (z.b == INT_MAX);
+        g.value = none ? -kInf : z.v;
+        g.block = none ? -1 : z.b;
+        g.period = none ? -1 : z.t;
+        *global = g;
+        *counter = 0u;
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // kernel parameter blocks
 // ------------------------------------------------------------------------------------
 struct EvalParams {
     const BlockRow *rows;
     const int32_t *adj;
+    const int32_t *nbr;  // [B][nbr_stride]: predecessors then successors, padded to 16 bytes
+    int nbr_stride;
     const int32_t *assign;
     const double *pm;
     const double *cap;
@@ -383,6 +439,8 @@ struct pp_ctx {
     int cvar_k = 1;
     // static tables
     DevBuf rows, adj, cost, cap, disc, level_blocks, ones_t, mass;
+    DevBuf nbr;        // padded neighbour table [B][nbr_stride] (staged kernel)
+    int nbr_stride = 0;
     const int32_t *assign_ptr = nullptr;  // current schedule (own buffer or a borrowed device buffer)
     bool borrowed = false;
     bool pm_dirty = true;
@@ -395,7 +453,7 @@ struct pp_ctx {
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm;
     std::vector<DevBuf *> all() {
-        return {&rows, &adj, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
+        return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm};
@@ -456,3 +514,22 @@ int check_ready(pp_ctx *c, uint32_t flags, int scenario);
 int pick_kc(int k);
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st);
 int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched);
+int launch_general_candidates(int PER, int kc, bool scen, int C, int G, int S, int Sp, int T, bool stats,
+                              cudaStream_t st, bool pdl, int device, const EvalParams &ep);
+
+template <typename K>
+inline int set_smem_attr(K kern, size_t bytes) {
+    if (bytes > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return PP_OK;
+}
+
+// resident CTAs of a kernel at this smem size (cached per instantiation)
+template <typename K>
+inline int resident_ctas(K kern, size_t smem, int device) {
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, EV_THREADS, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms < 1) sms = 148;
+    return per_sm * sms;
+}
+

@@ -21,7 +21,7 @@
 constexpr int PM_THREADS = 512;
 constexpr int PM_MAXT = 128;
 constexpr int PM_CH = 512;             // blocks per P1 chunk (one per thread)
-constexpr int PM_MAX_DEPTH = 11;       // heap levels 0..11: n <= 128 * 2^11 = 262144 per period
+constexpr int PM_MAX_DEPTH = 10;       // heap levels 0..10: n <= 128 * 2^10 = 131072 per period
 constexpr int PM_HEAP = (1 << (PM_MAX_DEPTH + 1)) - 1;
 
 // serial pairwise sum (pathological sizes only)
@@ -73,14 +73,30 @@ __device__ double pairwise_serial(const double *a, int n) {
 }
 
 
-__global__ void __launch_bounds__(PM_THREADS) k_pm_chunks(const int32_t *__restrict__ assign,
-                                                           const double *__restrict__ mass, int B, int T, int nchunk,
-                                                           int32_t *__restrict__ agg, int32_t *__restrict__ flags,
-                                                           double *__restrict__ compact) {
-    asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ int s_cnt[PM_THREADS / 32][PM_MAXT];
-    __shared__ int s_base[PM_MAXT];
-    const int c = blockIdx.x, p = blockIdx.y;
+#ifdef PP_EVAL_PROBE
+__device__ unsigned long long g_pm_probe[2][512][2];
+__device__ __forceinline__ unsigned long long pm_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PMP(k, j) do { const int i_ = (k) ? (int)blockIdx.x - nchunk : (int)blockIdx.x; if (threadIdx.x == 0 && blockIdx.y == 0 && i_ < 512) g_pm_probe[k][i_][j] = pm_gtimer(); } while (0)
+extern "C" PP_API int pp_debug_pm_probe(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_pm_probe, sizeof(g_pm_probe)) == cudaSuccess ? 0 : 3;
+}
+#else
+#define PMP(k, j) do { } while (0)
+#endif
+#ifdef PP_EVAL_PROBE
+#define PMCP(k, j) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[k][blockIdx.x][j] = pm_gtimer(); } while (0)
+#else
+#define PMCP(k, j) do { } while (0)
+#endif
+
+__device__ void pm_chunk_cta(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
+                             int nchunk, int c, int p, int32_t *__restrict__ agg, int32_t *__restrict__ flags,
+                             double *__restrict__ compact, int (*s_cnt)[PM_MAXT], int *s_base) {
+    PMP(0, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b = c * PM_CH + tid;
     int t = (b < B) ? __ldg(assign + (size_t)p * B + b) : -1;
@@ -145,6 +161,7 @@ __global__ void __launch_bounds__(PM_THREADS) k_pm_chunks(const int32_t *__restr
     }
     __syncthreads();
     if (t >= 0) compact[((size_t)p * T + t) * B + s_base[t] + s_cnt[warp][t] + rank_w] = m;
+    PMP(0, 1);
 }
 
 struct PmTreeSmem {
@@ -157,14 +174,10 @@ struct PmTreeSmem {
     int total;
 };
 
-__global__ void __launch_bounds__(PM_THREADS) k_pm_tree(const int32_t *__restrict__ agg, int32_t *__restrict__ flags,
-                                                         const double *__restrict__ compact, int B, int T, int nchunk,
-                                                         double *__restrict__ pm_out) {
-    asm volatile("griddepcontrol.launch_dependents;");
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // P1 complete and visible
-    extern __shared__ __align__(16) unsigned char tree_dyn[];
-    PmTreeSmem &sm = *reinterpret_cast<PmTreeSmem *>(tree_dyn);
-    const int t = blockIdx.x, p = blockIdx.y;
+__device__ void pm_tree_cta(const int32_t *__restrict__ agg, int32_t *__restrict__ flags,
+                            const double *__restrict__ compact, int B, int T, int nchunk, int t, int p,
+                            double *__restrict__ pm_out, PmTreeSmem &sm) {
+    PMP(1, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) {
         int sum = 0;
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(PM_THREADS) k_pm_tree(const int32_t *__restric
             break;
         }
     }
-    if (overflow) {  // > 262144 blocks in one period: serial evaluation (correct, slow)
+    if (overflow) {  // > 131072 blocks in one period: serial evaluation (correct, slow)
         if (tid == 0) pm_out[(size_t)p * T + t] = f64_add(0.0, pairwise_serial(a, n));
         return;
     }
@@ -292,6 +305,54 @@ __global__ void __launch_bounds__(PM_THREADS) k_pm_tree(const int32_t *__restric
         __syncthreads();
     }
     if (tid == 0) pm_out[(size_t)p * T + t] = f64_add(0.0, n ? sm.val[0] : -0.0);
+    PMP(1, 1);
+}
+
+// One launch computes the period masses of P schedules: CTAs x < nchunk compact a chunk
+// (pm_chunk_cta, decoupled look-back across chunks); the last T CTAs of each schedule wait
+// until every chunk has scattered, then build one period's pairwise tree (pm_tree_cta).
+// Tree CTAs have higher block indices than the chunks they wait for, so they are
+// dispatched after them.  done[2p] counts finished chunks, done[2p+1] finished trees; the
+// last tree CTA re-arms both (graph-replay safe).
+__global__ void __launch_bounds__(PM_THREADS) k_period_mass(const int32_t *__restrict__ assign,
+                                                             const double *__restrict__ mass, int B, int T, int nchunk,
+                                                             int32_t *__restrict__ agg, int32_t *__restrict__ flags,
+                                                             unsigned int *__restrict__ done,
+                                                             double *__restrict__ compact, double *__restrict__ pm_out) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ __align__(16) unsigned char pm_dyn[];
+    const int p = blockIdx.y;
+    if ((int)blockIdx.x < nchunk) {
+        int(*s_cnt)[PM_MAXT] = reinterpret_cast<int(*)[PM_MAXT]>(pm_dyn);
+        int *s_base = reinterpret_cast<int *>(pm_dyn + sizeof(int) * (PM_THREADS / 32) * PM_MAXT);
+        pm_chunk_cta(assign, mass, B, T, nchunk, blockIdx.x, p, agg, flags, compact, s_cnt, s_base);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(done + 2 * p, 1u);
+        }
+        return;
+    }
+    const int t = blockIdx.x - nchunk;
+    if (threadIdx.x == 0) {
+        unsigned int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + 2 * p) : "memory");
+            if ((int)v >= nchunk) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    pm_tree_cta(agg, flags, compact, B, T, nchunk, t, p, pm_out, *reinterpret_cast<PmTreeSmem *>(pm_dyn));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(done + 2 * p + 1, 1u);
+        if ((int)prev == T - 1) {
+            done[2 * p] = 0u;
+            done[2 * p + 1] = 0u;
+        }
+    }
 }
 
 
@@ -474,6 +535,239 @@ __global__ void k_apply_moves(int32_t *assign, int B, int T, const int32_t *bloc
 
 // period masses of P schedules (device pointers) into pm_out[P][T]: P1 (chunks) then
 // P2 (trees), P2 launched as a programmatic dependent of P1
+// ---------------------------------------------------------------------------------------------
+// Cluster fast path (B <= 65536, T <= 16): one 8-CTA cluster per schedule, 1024 threads per CTA.
+// Warp w of CTA r owns the contiguous blocks [(32 r + w) * 32K, +32K) and ranks them inside
+// their periods with match_any (phase 1, loads kept in registers).  Per-warp counts are
+// scanned in shared memory, the CTA totals are scanned across the cluster through
+// distributed shared memory, and every block's mass lands at its numpy position in
+// compact[p][t][.] (phase 2).  After a cluster barrier CTA r builds the pairwise trees of
+// periods r and r + 8 side by side.  No global counters or flags: graph-replay safe, and
+// only 8 SMs per schedule are touched, so the evaluation CTAs launched behind it (PDL)
+// keep their residency.
+constexpr int PMC_R = 8;
+constexpr int PMC_THREADS = 1024;
+constexpr int PMC_WARPS = PMC_THREADS / 32;
+constexpr int PMC_MAXT = 16;
+constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;
+constexpr int PMC_MAXB = PMC_R * PMC_THREADS * 8;
+
+struct PmcTree {
+    int start[PM_HEAP];
+    int len[PM_HEAP];
+    double val[PM_HEAP];
+    int leaves[1 << PM_MAX_DEPTH];
+};
+struct PmcSmem {
+    int cnt[PMC_WARPS][PMC_MAXT];
+    int tot[PMC_MAXT];
+    int off[PMC_MAXT];
+    int n[PMC_MAXT];
+    int nleaf[PMC_MAXQ];
+    PmcTree tree[PMC_MAXQ];
+};
+
+__device__ __forceinline__ void cluster_sync_acqrel() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int ld_dsmem_i32(const int *p, int rank) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    uint32_t ra;
+    int v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <int K>
+__global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
+    k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
+                 double *__restrict__ compact, double *__restrict__ pm_out) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ __align__(16) unsigned char pmc_dyn[];
+    PmcSmem &sm = *reinterpret_cast<PmcSmem *>(pmc_dyn);
+    PMCP(0, 0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = blockIdx.x, p = blockIdx.y;
+    const int32_t *as = assign + (size_t)p * B;
+    const int base = (r * PMC_WARPS + warp) * (32 * K);
+    int tk[K];
+    double mk[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int b = base + k * 32 + lane;
+        int t = -1;
+        double m = 0.0;
+        if (b < B) {
+            t = __ldg(as + b);
+            m = __ldg(mass + b);
+        }
+        tk[k] = ((unsigned)t < (unsigned)T) ? t : -1;
+        mk[k] = m;
+    }
+    for (int i = tid; i < PMC_WARPS * PMC_MAXT; i += PMC_THREADS) (&sm.cnt[0][0])[i] = 0;
+    __syncthreads();
+    // phase 1: rank inside (warp, period)
+    int pos[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const unsigned mt = __match_any_sync(0xffffffffu, tk[k]);
+        const int lr = __popc(mt & ((1u << lane) - 1u));
+        const int b0 = tk[k] >= 0 ? sm.cnt[warp][tk[k]] : 0;
+        pos[k] = b0 + lr;
+        __syncwarp();
+        if (tk[k] >= 0 && lr == 0) sm.cnt[warp][tk[k]] = b0 + __popc(mt);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per-period exclusive scan over the warps (warp j scans period j)
+    if (warp < T) {
+        const int v = sm.cnt[lane][warp];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        sm.cnt[lane][warp] = inc - v;
+        if (lane == 31) sm.tot[warp] = inc;
+    }
+    cluster_sync_acqrel();
+    // cross-CTA scan of the period totals through distributed shared memory
+    if (warp < T) {
+        const int v = lane < PMC_R ? ld_dsmem_i32(&sm.tot[warp], lane) : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < PMC_R; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int off = __shfl_sync(0xffffffffu, inc - v, r);
+        const int n = __shfl_sync(0xffffffffu, inc, PMC_R - 1);
+        if (lane == 0) {
+            sm.off[warp] = off;
+            sm.n[warp] = n;
+        }
+    }
+    __syncthreads();
+    // phase 2: scatter to the numpy order
+#pragma unroll
+    for (int k = 0; k < K; k++)
+        if (tk[k] >= 0) {
+            const int t = tk[k];
+            compact[((size_t)p * T + t) * B + sm.off[t] + sm.cnt[warp][t] + pos[k]] = mk[k];
+        }
+    __threadfence();
+    cluster_sync_acqrel();  // every block of the schedule is in place; remote smem no longer read
+    PMCP(0, 1);
+    // trees of periods r, r + 8 (slot g)
+    const int q = (T - r + PMC_R - 1) / PMC_R;
+    if (q <= 0) return;
+    if (tid < q) {
+        sm.tree[tid].start[0] = 0;
+        sm.tree[tid].len[0] = sm.n[r + PMC_R * tid];
+        sm.nleaf[tid] = 0;
+    }
+    __syncthreads();
+    int depth = 0;
+    for (int d = 0;; d++) {
+        const int first = (1 << d) - 1, cnt = 1 << d;
+        bool any_internal = false;
+        for (int x = tid; x < q * cnt; x += PMC_THREADS) {
+            const int g = x >> d, id = first + (x & (cnt - 1));
+            PmcTree &tr = sm.tree[g];
+            const int ln = tr.len[id];
+            if (ln <= 128) {  // leaf, or dead (below a leaf): its children are dead
+                if (ln >= 0) tr.leaves[atomicAdd(&sm.nleaf[g], 1)] = id;
+                if (d < PM_MAX_DEPTH) {
+                    tr.len[2 * id + 1] = -1;
+                    tr.len[2 * id + 2] = -1;
+                }
+            } else {
+                any_internal = true;  // cannot exceed PM_MAX_DEPTH: n <= 65536
+                const int n2 = ((ln >> 3) >> 1) << 3;
+                tr.start[2 * id + 1] = tr.start[id];
+                tr.len[2 * id + 1] = n2;
+                tr.start[2 * id + 2] = tr.start[id] + n2;
+                tr.len[2 * id + 2] = ln - n2;
+            }
+        }
+        if (!__syncthreads_or(any_internal)) {
+            depth = d;
+            break;
+        }
+    }
+    // leaf sums: 8 lanes per leaf, lane j owns numpy accumulator j
+    const int nl0 = sm.nleaf[0], nl = nl0 + (q > 1 ? sm.nleaf[1] : 0);
+    const int sub = tid & 7, grp = tid >> 3;
+    for (int l0 = 0; l0 < nl; l0 += PMC_THREADS / 8) {
+        const int l = l0 + grp;
+        const bool act = l < nl;
+        const int g = (l >= nl0) ? 1 : 0;
+        PmcTree &tr = sm.tree[g];
+        const double *a = compact + ((size_t)p * T + r + PMC_R * g) * B;
+        const int id = act ? tr.leaves[l - (g ? nl0 : 0)] : 0;
+        const int o = act ? tr.start[id] : 0;
+        const int len = act ? tr.len[id] : 0;
+        double rr = 0.0;
+        if (act && len >= 8) {
+            const int nm = len >> 3;
+            double x[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = (u < nm) ? __ldcg(a + o + 8 * u + sub) : 0.0;
+            rr = x[0];
+#pragma unroll
+            for (int u = 1; u < 16; u++)
+                if (u < nm) rr = f64_add(rr, x[u]);
+        }
+        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 1));
+        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 2));
+        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 4));
+        if (act && sub == 0) {
+            double res;
+            int i;
+            if (len < 8) {
+                res = -0.0;
+                i = 0;
+            } else {
+                res = rr;
+                i = len - (len & 7);
+            }
+            for (; i < len; i++) res = f64_add(res, __ldcg(a + o + i));
+            tr.val[id] = res;
+        }
+    }
+    __syncthreads();
+    for (int d = depth - 1; d >= 0; d--) {
+        const int first = (1 << d) - 1, cnt = 1 << d;
+        for (int x = tid; x < q * cnt; x += PMC_THREADS) {
+            PmcTree &tr = sm.tree[x >> d];
+            const int id = first + (x & (cnt - 1));
+            if (tr.len[id] > 128) tr.val[id] = f64_add(tr.val[2 * id + 1], tr.val[2 * id + 2]);
+        }
+        __syncthreads();
+    }
+    if (tid < q) {
+        const int t = r + PMC_R * tid;
+        pm_out[(size_t)p * T + t] = f64_add(0.0, sm.n[t] ? sm.tree[tid].val[0] : -0.0);
+    }
+    PMCP(1, 1);
+}
+
+template <int K>
+static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_pm_cluster<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(PmcSmem)));
+        attr = true;
+    }
+    k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, sizeof(PmcSmem), st>>>(d_assign, c->mass.as<double>(), c->B,
+                                                                             c->T, c->compact.as<double>(), d_pm);
+    CUDA_TRY(cudaGetLastError());
+    return PP_OK;
+}
+
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st) {
     const int B = c->B, T = c->T;
     const int nchunk = (B + PM_CH - 1) / PM_CH;
@@ -482,34 +776,39 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
     const int pchunk = std::max(1, std::min(P, (int)std::max<size_t>(1, ((size_t)512 << 20) / per)));
     TRY(c->compact.ensure(per * pchunk));
     TRY(c->cnt.ensure(sizeof(int32_t) * (size_t)pchunk * nchunk * (T + 1)));
-    if (c->pm_flags_n < (size_t)pchunk * nchunk) {
-        TRY(c->pm_flags.ensure(sizeof(int32_t) * (size_t)pchunk * nchunk));
-        CUDA_TRY(cudaMemset(c->pm_flags.ptr, 0, sizeof(int32_t) * (size_t)pchunk * nchunk));
-        c->pm_flags_n = (size_t)pchunk * nchunk;
+    const size_t nflags = (size_t)pchunk * nchunk + 2 * (size_t)pchunk;
+    if (c->pm_flags_n < nflags) {
+        TRY(c->pm_flags.ensure(sizeof(int32_t) * nflags));
+        CUDA_TRY(cudaMemset(c->pm_flags.ptr, 0, sizeof(int32_t) * nflags));
+        c->pm_flags_n = nflags;
     }
+    if (T <= PMC_MAXT && B <= PMC_MAXB) {
+        const int K = B <= PMC_MAXB / 8 ? 1 : B <= PMC_MAXB / 4 ? 2 : B <= PMC_MAXB / 2 ? 4 : 8;
+        for (int p0 = 0; p0 < P; p0 += pchunk) {
+            const int np = std::min(pchunk, P - p0);
+            const int32_t *a = d_assign + (size_t)p0 * B;
+            double *o = d_pm + (size_t)p0 * T;
+            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st));
+            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st));
+            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st));
+            else TRY(launch_pm_cluster<8>(c, a, np, o, st));
+        }
+        return PP_OK;
+    }
+    const size_t smem = std::max(sizeof(PmTreeSmem), sizeof(int) * ((PM_THREADS / 32) * PM_MAXT + PM_MAXT));
     static bool attr_done = false;
     if (!attr_done) {
-        CUDA_TRY(cudaFuncSetAttribute(k_pm_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PmTreeSmem)));
+        CUDA_TRY(cudaFuncSetAttribute(k_period_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done = true;
     }
+    int32_t *flags = c->pm_flags.as<int32_t>();
+    unsigned int *done = reinterpret_cast<unsigned int *>(flags + (size_t)pchunk * nchunk);
     for (int p0 = 0; p0 < P; p0 += pchunk) {
         const int np = std::min(pchunk, P - p0);
-        k_pm_chunks<<<dim3(nchunk, np), PM_THREADS, 0, st>>>(d_assign + (size_t)p0 * B, c->mass.as<double>(), B, T,
-                                                             nchunk, c->cnt.as<int32_t>(), c->pm_flags.as<int32_t>(),
-                                                             c->compact.as<double>());
+        k_period_mass<<<dim3(nchunk + T, np), PM_THREADS, smem, st>>>(d_assign + (size_t)p0 * B, c->mass.as<double>(), B,
+                                                                       T, nchunk, c->cnt.as<int32_t>(), flags, done,
+                                                                       c->compact.as<double>(), d_pm + (size_t)p0 * T);
         CUDA_TRY(cudaGetLastError());
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(T, np);
-        cfg.blockDim = dim3(PM_THREADS);
-        cfg.dynamicSmemBytes = sizeof(PmTreeSmem);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pm_tree, (const int32_t *)c->cnt.as<int32_t>(), c->pm_flags.as<int32_t>(),
-                                    (const double *)c->compact.as<double>(), B, T, nchunk, d_pm + (size_t)p0 * T));
     }
     return PP_OK;
 }
@@ -653,6 +952,15 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
     c->n_levels = nlev;
     c->deg_max = 0;
     for (int b = 0; b < B; b++) c->deg_max = std::max(c->deg_max, npred[b] + nsucc[b]);
+    // padded neighbour table for the staged evaluation kernel (one 16-byte-granular row per block)
+    c->nbr_stride = std::max(4, (c->deg_max + 3) & ~3);
+    if (c->deg_max <= 32) {
+        std::vector<int> nbr((size_t)B * c->nbr_stride, 0);
+        for (int b = 0; b < B; b++)
+            for (int k = 0; k < npred[b] + nsucc[b]; k++) nbr[(size_t)b * c->nbr_stride + k] = adj[start[b] + k];
+        TRY(c->nbr.ensure(sizeof(int) * nbr.size()));
+        CUDA_TRY(cudaMemcpy(c->nbr.ptr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice));
+    }
     c->level_ptr = lptr;
     c->level_of = level;
     c->mean_cap = (0.0 + host_pairwise(capacity, T)) / (double)T;

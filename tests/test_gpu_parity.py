@@ -318,3 +318,37 @@ def test_enpv_table_matches_reference(oracle_lib, small):
     o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
     assert same(eng.enpv_table(True, factored=True), o.enpv_table(True, factored=True))
     eng.close()
+
+
+def _flat_bm(B, T, seed):
+    from paper_2511_18296_b200.model import BlockModel
+
+    rng = np.random.default_rng(seed)
+    z = np.zeros(B)
+    return BlockModel(n_blocks=B, n_periods=T, edges_i=np.zeros(0, np.int32), edges_j=np.zeros(0, np.int32),
+                      mass=rng.lognormal(8.0, 1.5, B), cost=np.zeros((B, T)), capacity=np.full(T, 1e30),
+                      discount_rate=0.08, coords=np.zeros((B, 3)), alteration=z, structural=z,
+                      dist_intrusion=z, base_grade=z)
+
+
+@pytest.mark.parametrize("B,T", [(1, 1), (100, 3), (8192, 15), (8193, 16), (16385, 9), (50000, 15),
+                                 (65536, 8), (65536, 16), (65537, 15), (70000, 17), (5000, 40)])
+def test_period_mass_paths(oracle_lib, B, T):
+    """numpy-pairwise period masses on both device paths (the 8-CTA cluster path for
+    B <= 65536 and T <= 16, the look-back path otherwise): uniform, skewed (one period
+    holding almost every block, the deepest pairwise tree), all unmined, ragged tails."""
+    bm = _flat_bm(B, T, B + T)
+    rng = np.random.default_rng(B * 7 + T)
+    pop = [rng.integers(-1, T, B), np.where(rng.random(B) < 0.97, T - 1, rng.integers(-1, T, B)),
+           np.full(B, -1), np.full(B, 0), (np.arange(B) * 7919) % (T + 1) - 1]
+    pop = np.stack(pop).astype(np.int32)
+    eng = Engine.from_tables(bm, None)
+    o = oracle_lib.Oracle(bm)
+    r = eng.check_feasible(pop)
+    for k in range(pop.shape[0]):
+        assert same(r["period_mass"][k], o.period_mass(pop[k])), k
+    for k in range(pop.shape[0]):  # single-schedule path (pm refresh behind set_schedule)
+        eng.set_schedule(pop[k])
+        _, pm = eng.get_schedule()
+        assert same(pm, o.period_mass(pop[k])), k
+    eng.close()

@@ -1,0 +1,47 @@
+"""Timeline of one evaluation step (P1, P2, eval CTAs) from globaltimer probes."""
+import ctypes, sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2511_18296_b200 import _lib
+lib = _lib.load(sys.argv[1]); _lib._lib = lib
+lib.pp_debug_eval_probe.argtypes = [ctypes.c_void_p]; lib.pp_debug_pm_probe.argtypes = [ctypes.c_void_p]
+from bench import build_inputs
+from paper_2511_18296_b200.engine import Engine
+c = build_inputs("C2")
+dev = torch.device("cuda", 0)
+st = torch.cuda.Stream(dev); torch.cuda.set_stream(st); sp = st.cuda_stream
+eng = Engine.from_tables(c["bm"], c["tables"], c["assign"])
+C, T = c["C"], c["T"]
+assign_d = torch.from_numpy(c["assign"].astype(np.int32)).to(dev)
+cand_d = torch.from_numpy(c["cand"]).to(dev)
+out = {"best_t": torch.empty(C, dtype=torch.int32, device=dev), "best_val": torch.empty(C, dtype=torch.float64, device=dev),
+       "feasible": torch.empty(C, dtype=torch.uint8, device=dev), "exp_delta": torch.empty(C, T, dtype=torch.float64, device=dev),
+       "cvar": torch.empty(C, T, dtype=torch.float64, device=dev), "global": torch.empty(2, dtype=torch.float64, device=dev)}
+flush = torch.empty(256 << 18, dtype=torch.int32, device=dev)
+grid = (C + 31) // 32
+g = torch.cuda.CUDAGraph()
+for _ in range(3):
+    eng.set_schedule_device(assign_d, stream=sp, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=sp)
+st.synchronize()
+with torch.cuda.graph(g):
+    cs = torch.cuda.current_stream().cuda_stream
+    eng.set_schedule_device(assign_d, stream=cs, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=cs)
+for rep in range(4):
+    flush.fill_(rep); st.synchronize()
+    g.replay(); st.synchronize()
+ev = np.zeros((4096, 8), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
+pm = np.zeros((2, 512, 2), np.uint64); lib.pp_debug_pm_probe(pm.ctypes.data); pm = pm.astype(np.int64)
+cl = pm[0, :8, 0].min() > 0
+if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
+    t0 = min(pm[0, :8, 0].min(), ev[:, 0].min())
+    f = lambda x: (x - t0) / 1000
+    print(f"PM cluster (8 CTAs): start {f(pm[0,:8,0].min()):.2f}..{f(pm[0,:8,0].max()):.2f}  scattered {f(pm[0,:8,1].min()):.2f}..{f(pm[0,:8,1].max()):.2f}  trees done {f(pm[1,:8,1].min()):.2f}..{f(pm[1,:8,1].max()):.2f} us")
+else:
+    nch = (c["bm"].n_blocks + 511) // 512
+    p1, p2 = pm[0, :nch], pm[1, :T]
+    t0 = min(p1[:, 0].min(), ev[:, 0].min())
+    f = lambda x: (x - t0) / 1000
+    print(f"P1 ({nch} CTAs): start {f(p1[:,0].min()):.2f}..{f(p1[:,0].max()):.2f}  end {f(p1[:,1].min()):.2f}..{f(p1[:,1].max()):.2f} us")
+    print(f"P2 ({T} CTAs): after-wait {f(p2[:,0].min()):.2f}..{f(p2[:,0].max()):.2f}  end {f(p2[:,1].min()):.2f}..{f(p2[:,1].max()):.2f} us")
+names = ["start", "ids", "rows", "window", "pm-wait", "capacity", "stats", "end"]
+for k in range(8):
+    print(f"eval {names[k]:9s} min {f(ev[:,k].min()):6.2f}  median {f(np.median(ev[:,k])):6.2f}  max {f(ev[:,k].max()):6.2f} us")

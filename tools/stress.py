@@ -40,9 +40,11 @@ for it in range(iters):
                         bad_total += 1
                         idx = np.argwhere(badm)
                         _, pm = eng.get_schedule()
+                        again = eng.eval_candidates(cand, s, net=net, trace=True, stats=True, scen=True)[k]
+                        rep = bool(np.all((again == y) | (np.isnan(again) & np.isnan(y))))
                         print(f"it{it} T={T} S={S} s={s} net={net} {k}: {badm.sum()} bad; first {idx[:3].tolist()}"
-                              f" got {x[tuple(idx[0])]} ref {y[tuple(idx[0])]}; pm ok {np.array_equal(pm, o.period_mass(assign))}",
-                              flush=True)
+                              f" got {x[tuple(idx[0])]!r} ref {y[tuple(idx[0])]!r}; pm ok {np.array_equal(pm, o.period_mass(assign))};"
+                              f" immediate rerun correct={rep}", flush=True)
                         break
         eng.close()
 print(f"done {iters} iters, {bad_total} mismatching calls, {time.time()-t0:.1f}s")
