@@ -4,11 +4,12 @@ One step = one evaluator batch of the headline configuration C2 (SURVEY.md §8(d
 50,000-block model, 15 periods, 20 scenarios, 16,667 candidate blocks x 15 periods =
 250,005 candidate moves, each evaluated under all 20 scenarios:
 
-  k_period_mass: period masses of the current schedule (bit-exact numpy pairwise tree)
-  + k_eval_candidates (launched with programmatic dependent launch so its gathers
-    overlap k_period_mass): precedence window, capacity test, kernel value (ref parity key),
-    per-scenario deltas -> expected delta and CVaR10 per move, per-candidate argmax,
-    grid argmax (1 kernel)
+  k_pm_cluster: period masses of the current schedule (bit-exact numpy pairwise tree,
+    one 8-CTA cluster)
+  + k_eval_warp (launched with programmatic dependent launch so its gathers and the
+    per-scenario statistics overlap k_pm_cluster): precedence window, capacity test,
+    kernel value (ref parity key), per-scenario deltas -> expected delta and CVaR10 of
+    every feasible move (sparse output), per-candidate argmax, grid argmax (1 kernel)
   [+ N>1: NCCL all-gather of the 16-byte per-GPU best and an ordered reduce kernel]
 
 `value` is device-timed (CUDA events, inputs resident in HBM, L2 flushed by a 256 MiB
@@ -114,15 +115,19 @@ def build_inputs(config: str, rank: int = 0):
     return c
 
 
-def algorithmic_bytes(c, deg_mean: float) -> dict:
-    """Compulsory bytes of one k_eval_candidates launch."""
+def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
+    """Compulsory bytes of one k_eval_warp launch: every candidate's inputs
+    once, its best move, and one (candidate, period, expected delta, CVaR10) record per
+    feasible move (sparse statistics output)."""
     C, T, S = c["C"], c["T"], c["S"]
     per_cand = (4 + 32 + 4 + 8 + 8 * deg_mean   # cand id, BlockRow, assign[b], unit_mean[b], adjacency ids+assign
-                + 8 * T + 8 * ((S + 3) & ~3)      # mining-cost row, vmax row (fp64, padded to 4)
-                + 13 + 16 * T)                    # best (t, value, flag) + per-move exp_delta & cvar
+                + 8 * T + 8 * ((S + 1) & ~1)      # mining-cost row, vmax row (fp64, padded to 2)
+                + 13)                             # best (t, value, flag)
+    per_pair = 4 + 4 + 8 + 8
     M = C * T
     survey = M * (80 + 8 * deg_mean) + 8 * M * S  # SURVEY §8(d) per-move figure, fp64 vmax, no reuse
-    return {"per_candidate": per_cand, "per_launch": per_cand * C, "survey_uncached": survey}
+    return {"per_candidate": per_cand, "per_pair": per_pair,
+            "per_launch": per_cand * C + per_pair * n_pairs, "survey_uncached": survey}
 
 
 def cpu_reference(c, seconds: float = 3.0, nthreads: int | None = None, max_batches: int | None = None):
@@ -223,9 +228,13 @@ def run_gpu(args):
         "best_t": torch.empty(C, dtype=torch.int32, device=dev),
         "best_val": torch.empty(C, dtype=torch.float64, device=dev),
         "feasible": torch.empty(C, dtype=torch.uint8, device=dev),
-        "exp_delta": torch.empty(C, T, dtype=torch.float64, device=dev),
-        "cvar": torch.empty(C, T, dtype=torch.float64, device=dev),
         "global": torch.empty(2, dtype=torch.float64, device=dev),
+        # sparse statistics of the feasible moves (pp_cand_out.pair_*)
+        "pair_cand": torch.empty(C * T, dtype=torch.int32, device=dev),
+        "pair_period": torch.empty(C * T, dtype=torch.int32, device=dev),
+        "pair_exp": torch.empty(C * T, dtype=torch.float64, device=dev),
+        "pair_cvar": torch.empty(C * T, dtype=torch.float64, device=dev),
+        "n_pairs": torch.zeros(1, dtype=torch.int32, device=dev),
     }
     gathered = torch.empty(2 * world, dtype=torch.float64, device=dev)
     final = torch.empty(2, dtype=torch.float64, device=dev)
@@ -234,7 +243,7 @@ def run_gpu(args):
     pm_copy = torch.empty(T, dtype=torch.float64, device=dev)
 
     def step():
-        # the schedule is read in place; the call enqueues k_period_mass + k_eval_candidates (PDL)
+        # the schedule is read in place; the call enqueues k_pm_cluster + k_eval_warp (PDL)
         eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
         eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
         if world > 1:
@@ -290,7 +299,7 @@ def run_gpu(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
 
-    # dominant kernel alone: k_eval_candidates timed with events on its stream, L2 flushed,
+    # dominant kernel alone: k_eval_warp timed with events on its stream, L2 flushed,
     # period masses refreshed beforehand so the call launches only the evaluation kernel
     kms = []
     for i in range(min(args.steps, 200)):
@@ -307,7 +316,7 @@ def run_gpu(args):
     result = None
     if rank == 0:
         hbm, peak_kind = _peaks()
-        ab = algorithmic_bytes(c, deg_mean)
+        ab = algorithmic_bytes(c, deg_mean, int(out["n_pairs"].item()))
         achieved = ab["per_launch"] / (k_ms * 1e-3) / 1e9
         value = world * M * S / (t_max * 1e-3)
 
@@ -318,21 +327,24 @@ def run_gpu(args):
         h_cand = pool.empty(C, np.int32)
         h_cand[:] = c["cand"]
         h_out = {"best_t": pool.empty(C, np.int32), "best_val": pool.empty(C, np.float64),
-                 "feasible": pool.empty(C, np.uint8), "exp_delta": pool.empty((C, T), np.float64),
-                 "cvar": pool.empty((C, T), np.float64)}
+                 "feasible": pool.empty(C, np.uint8), "pair_cand": pool.empty(C * T, np.int32),
+                 "pair_period": pool.empty(C * T, np.int32), "pair_exp": pool.empty(C * T, np.float64),
+                 "pair_cvar": pool.empty(C * T, np.float64), "n_pairs": pool.empty(1, np.int32)}
         e2e = []
         for i in range(args.warmup + min(args.steps, 300)):
             flush.fill_(i)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             eng.set_schedule(h_assign)
-            r = eng.eval_candidates(h_cand, None, net=True, stats=True, out=h_out, validate=False)
+            r = eng.eval_candidates(h_cand, None, net=True, pairs=True, out=h_out, validate=False)
             t1 = time.perf_counter()
             if i >= args.warmup:
                 e2e.append(t1 - t0)
         e2e_t = float(np.median(e2e))
         h2d = h_assign.nbytes + h_cand.nbytes
-        d2h = sum(a.nbytes for a in h_out.values()) + 16
+        npairs = int(h_out["n_pairs"][0])
+        d2h = (h_out["best_t"].nbytes + h_out["best_val"].nbytes + h_out["feasible"].nbytes + 16 + 4
+               + npairs * (4 + 4 + 8 + 8))
         # parity spot check of the timed configuration against the device run
         assert r["best"] is not None
         g = out["global"].cpu().numpy()
@@ -347,7 +359,7 @@ def run_gpu(args):
             cpu = {"value": M * S / t_cpu, "unit": UNIT, "cores": nth, "kind": "port",
                    "sample": f"{len(ts)} full batches ({M} moves x {S} scenarios each, incl. period masses), "
                              f"oracle/oracle.c with OpenMP, median"}
-        launches_per_step = 2 + (1 if world > 1 else 0)  # k_period_mass + k_eval_candidates [+ k_reduce_best]
+        launches_per_step = 2 + (1 if world > 1 else 0)  # k_pm_cluster + k_eval_warp [+ k_reduce_best]
         result = {
             "metric": METRIC,
             "value": value,
@@ -378,7 +390,7 @@ def run_gpu(args):
                 "unit": "GB/s",
                 "frac": achieved / hbm,
                 "traffic": args.ncu_traffic,
-                "kernel": "k_eval_candidates",
+                "kernel": "k_eval_warp",
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": ab["per_launch"],
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
@@ -411,7 +423,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     ap.add_argument("--ncu-traffic", type=float, default=None,
-                    help="dram bytes per k_eval_candidates launch from the committed ncu capture")
+                    help="dram bytes per k_eval_warp launch from the committed ncu capture")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -16,6 +16,7 @@ from .errors import ExtensionMissing, raise_for_status
 LIB_NAME = "libpitplan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
+ABI_VERSION = 2  # include/pitplan_b200.h PP_ABI_VERSION
 PP_MEM_HOST = 0
 PP_MEM_DEVICE = 1
 PP_MEM_DEVICE_BORROW = 2
@@ -51,6 +52,11 @@ class PPCandOut(ctypes.Structure):
         ("cvar", c_void_p),
         ("scen_delta", c_void_p),
         ("global_", c_void_p),
+        ("pair_cand", c_void_p),
+        ("pair_period", c_void_p),
+        ("pair_exp", c_void_p),
+        ("pair_cvar", c_void_p),
+        ("n_pairs", c_void_p),
     ]
 
 
@@ -120,6 +126,8 @@ def load(path: str | None = None):
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        if handle.pp_abi_version() != ABI_VERSION:
+            raise ExtensionMissing(f"{p} has ABI {handle.pp_abi_version()}, expected {ABI_VERSION}; rebuild it")
         if path is None:
             _lib = handle
         return handle

@@ -2,16 +2,6 @@
 // and pp_eval_candidates (which dispatches to pp_eval_general.cu otherwise).
 #include "pp_internal.cuh"
 
-// ------------------------------------------------------------------------------------
-// k_eval_staged: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
-// A CTA takes NB consecutive candidates and stages everything they need in shared
-// memory with a handful of dependent round trips for the whole batch (instead of one
-// chain per candidate): ids; BlockRow / assign / unit / mining-cost row / vmax row via
-// cp.async; adjacency ids then neighbour periods (precedence window reduced per warp).
-// Groups of G lanes (lanes = periods) then compute from shared memory.  Everything
-// before griddepcontrol.wait is independent of the period masses, so it overlaps the
-// period-mass kernels under programmatic dependent launch.
-// ------------------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void *s, const void *g) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
@@ -25,52 +15,6 @@ __device__ __forceinline__ void cp_async4(void *s, const void *g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-struct StagedLayout {  // byte offsets into dynamic shared memory
-    int sig, tab, vrow, cost, nbr, ex, cv, row, unit, pair, b, ab, lo, hi, npair, okbits, total;
-};
-
-static __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-
-static __host__ __device__ inline StagedLayout staged_layout(int NB, int T, int S, int Sp, int nbr_stride, bool stats,
-                                                             bool need_vrow, bool net) {
-    StagedLayout L;
-    int o = 0;
-    L.sig = o;  // sigma [S][T] (statistics)
-    o += stats ? align16(8 * S * T) : 0;
-    L.tab = o;  // cap, disc, sig_row, pm: [4][T]
-    o += align16(8 * 4 * T);
-    L.vrow = o;
-    o += need_vrow ? align16(8 * NB * Sp) : 0;
-    L.cost = o;
-    o += net ? align16(8 * NB * T) : 0;
-    L.nbr = o;
-    o += align16(4 * NB * nbr_stride);
-    L.ex = o;
-    o += stats ? align16(8 * NB * T) : 0;
-    L.cv = o;
-    o += stats ? align16(8 * NB * T) : 0;
-    L.row = o;
-    o += align16(32 * NB);
-    L.unit = o;
-    o += align16(8 * NB);
-    L.pair = o;
-    o += stats ? align16(4 * NB * T) : 0;
-    L.b = o;
-    o += align16(4 * NB);
-    L.ab = o;
-    o += align16(4 * NB);
-    L.lo = o;
-    o += align16(4 * NB);
-    L.hi = o;
-    o += align16(4 * NB);
-    L.npair = o;
-    o += align16(4 * (NB + 1));
-    L.okbits = o;  // one 32-bit mask of feasible periods per candidate (T <= 32)
-    o += align16(4 * NB);
-    L.total = o;
-    return L;
-}
 
 // One (candidate, period) pair: per-scenario deltas d_s = val_s(b,t) - val_s(b,a[b])
 // (evaluate.py:380-382 with s=k), expected = np.mean(d) (a single numpy pairwise leaf,
@@ -116,22 +60,49 @@ __device__ __forceinline__ void pair_stats(const EvalParams &p, int S, int T, co
 }
 
 // ------------------------------------------------------------------------------------
-// k_eval_staged: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
-// Sized for the sparsity of the problem (at C2 a candidate's precedence window holds 1.2
-// of 15 periods on average, 8% of the moves are feasible), NB candidates per CTA:
-//   stage 1  candidate ids
-//   stage 2  one warp per candidate: BlockRow, assign, unit, padded neighbour row,
-//            mining-cost row, vmax row via cp.async -- one round trip for the batch
-//   stage 3  one thread per candidate: neighbour periods -> precedence window
-//            (evaluate.py:361-372); then the list of precedence-feasible (candidate, t)
-//   B        one thread per feasible pair: per-scenario statistics into shared memory
-//   C        griddepcontrol.wait; one thread per candidate walks its window: capacity
-//            (evaluate.py:373-378), parity value (379-384), lowest-t argmax (387-388)
-//   out      one thread per (candidate, period): coalesced writes of the [NB][T] block
-//   K4       warp argmax of the CTA's candidates, deterministic grid argmax
-// Stages 1-3 and B never read the period masses: under programmatic dependent launch
-// they overlap k_pm_chunks / k_pm_tree.
+// k_eval_warp: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
+// Every warp owns CPW consecutive candidates end to end; warps never wait for one another
+// until the final CTA argmax, so the SM overlaps one warp's load latency with another's
+// arithmetic.  Lane t is period t for the capacity / value / argmax of a candidate
+// (evaluate.py:361-388); lane k is neighbour slot k for its precedence window.
+//   loads     candidate ids -> {BlockRow, own period, unit, mining-cost row (lane t),
+//             vmax row (cp.async to the warp's shared slice), 32 neighbour ids (lane k)}
+//             -> neighbour periods; window = redux.sync max / min over the lanes
+//   wait      griddepcontrol.wait (the period-mass kernel), lane t loads pm[t]
+//   moves     capacity (373-378), value (379-384), lowest-t argmax (387-388) per candidate:
+//             ballot of the feasible periods, butterfly argmax, trace row written by lane t
+//   stats     per feasible (candidate, period) pair: 8-lane sub-groups (CVaR k <= 2) or one
+//             lane per pair: expected delta (numpy pairwise mean) and CVaR10
+//   argmax    warp -> CTA -> deterministic grid argmax (last CTA)
+// Everything before the wait is independent of the period masses and overlaps the
+// period-mass kernel under programmatic dependent launch.
 // ------------------------------------------------------------------------------------
+constexpr int CPW = 4;  // candidates per warp
+
+__device__ __forceinline__ int nth_bit(unsigned m, int k) {  // index of the k-th (0-based) set bit
+    for (; k > 0; k--) m &= m - 1;
+    return __ffs(m) - 1;
+}
+constexpr int NBR_W = 32;  // neighbour slots per block (padded table, one 128-byte row)
+constexpr int NBR_SUCC = 1 << 30;  // successor tag in the neighbour table; -1 = padding
+
+struct WarpLayout {  // per-warp slice of dynamic shared memory (byte offsets)
+    int vrow, ex, cv, total;
+};
+static __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool stats, bool need_vrow) {
+    WarpLayout L;
+    int o = 0;
+    L.vrow = o;
+    o += need_vrow ? align16(8 * CPW * Sp) : 0;
+    L.ex = o;
+    o += stats ? align16(8 * CPW * T) : 0;
+    L.cv = o;
+    o += stats ? align16(8 * CPW * T) : 0;
+    L.total = o;
+    return L;
+}
+
 #ifdef PP_EVAL_PROBE
 __device__ unsigned long long g_ev_probe[4096][8];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -145,202 +116,132 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int KC, bool SCEN>
-__global__ void __launch_bounds__(EV_THREADS, 4) k_eval_staged(const EvalParams p, const int NB) {
-    extern __shared__ __align__(16) unsigned char st_dyn[];
+__global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p) {
+    extern __shared__ __align__(16) unsigned char wv_dyn[];
     __shared__ Best s_red[EV_THREADS / 32];
     constexpr int NW = EV_THREADS / 32;
-    const int T = p.T, S = p.S, Sp = p.Sp, NS = p.nbr_stride;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int T = p.T, S = p.S, Sp = p.Sp;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool net = p.flags & PP_NET_MINING_COST;
     const bool literal = p.flags & PP_LITERAL_VALUE;
     constexpr bool STATS_T = KC > 0;
-    const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar);
+    const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar || p.n_pairs);
     const bool need_vrow = stats || (!literal && p.scen >= 0);
-    const StagedLayout L = staged_layout(NB, T, S, Sp, NS, stats, need_vrow, net);
-    double *s_sig = reinterpret_cast<double *>(st_dyn + L.sig);
-    double *s_cap = reinterpret_cast<double *>(st_dyn + L.tab);
-    double *s_disc = s_cap + T, *s_srow = s_cap + 2 * T, *s_pm = s_cap + 3 * T;
-    double *s_vrow = reinterpret_cast<double *>(st_dyn + L.vrow);
-    double *s_cost = reinterpret_cast<double *>(st_dyn + L.cost);
-    int *s_nbr = reinterpret_cast<int *>(st_dyn + L.nbr);
-    double *s_ex = reinterpret_cast<double *>(st_dyn + L.ex);
-    double *s_cv = reinterpret_cast<double *>(st_dyn + L.cv);
-    BlockRow *s_row = reinterpret_cast<BlockRow *>(st_dyn + L.row);
-    double *s_unit = reinterpret_cast<double *>(st_dyn + L.unit);
-    int *s_pair = reinterpret_cast<int *>(st_dyn + L.pair);
-    int *s_b = reinterpret_cast<int *>(st_dyn + L.b);
-    int *s_ab = reinterpret_cast<int *>(st_dyn + L.ab);
-    int *s_lo = reinterpret_cast<int *>(st_dyn + L.lo);
-    int *s_hi = reinterpret_cast<int *>(st_dyn + L.hi);
-    int *s_np = reinterpret_cast<int *>(st_dyn + L.npair);
-    unsigned *s_ok = reinterpret_cast<unsigned *>(st_dyn + L.okbits);
-    const int c0 = blockIdx.x * NB;
+    const bool want_unit = !literal && p.scen < 0;
+    const bool want_trace = p.trace_val || p.trace_feas;
+    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow);
+    unsigned char *wbase = wv_dyn + (size_t)warp * L.total;
+    double *w_vrow = reinterpret_cast<double *>(wbase + L.vrow);
+    double *w_ex = reinterpret_cast<double *>(wbase + L.ex);
+    double *w_cv = reinterpret_cast<double *>(wbase + L.cv);
+    const int cw = (blockIdx.x * NW + warp) * CPW;
     EV_PROBE(0);
 
-    // ---- stage 1 ----
-    for (int i = tid; i < NB; i += EV_THREADS) {
-        const int g = c0 + i;
-        int b = (g < p.C) ? __ldg(p.cand + g) : -1;
-        if (b >= p.B) b = -1;
-        s_b[i] = b;
+    // ---- loads: ids, then every row of the warp's candidates in one round trip ----
+    int bl = -1;
+    if (lane < CPW && cw + lane < p.C) {
+        bl = __ldg(p.cand + cw + lane);
+        if (bl < 0 || bl >= p.B) bl = -1;
     }
-    for (int t = tid; t < T; t += EV_THREADS) {
-        s_cap[t] = __ldg(p.cap + t);
-        s_disc[t] = __ldg(p.disc + t);
-        s_srow[t] = __ldg(p.sig_row + t);
+    double cap_t = 0.0, disc_t = 0.0, srow_t = 0.0;
+    if (lane < T) {
+        cap_t = __ldg(p.cap + lane);
+        disc_t = __ldg(p.disc + lane);
+        srow_t = __ldg(p.sig_row + lane);
     }
-    if (stats) {  // sigma [S][T] (S*T*8 is a multiple of 8; copy 8-byte pieces)
-        for (int e = tid; e < S * T; e += EV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+    int b[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
+    double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
+    int ab_l = -1;
+    if (bl >= 0) {
+        mass_l = __ldg(&p.rows[bl].mass);
+        spat_l = __ldg(&p.rows[bl].spatial);
+        ab_l = __ldg(p.assign + bl);
+        if (want_unit) unit_l = __ldg(p.unit_mean + bl);
     }
-    __syncthreads();
+    double cost_r[CPW];
+    int nb[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; j++) {
+        cost_r[j] = (net && lane < T && b[j] >= 0) ? __ldg(p.cost + (size_t)b[j] * T + lane) : 0.0;
+        nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
+    }
+    if (need_vrow) {
+#pragma unroll
+        for (int j = 0; j < CPW; j++)
+            if (b[j] >= 0)
+                for (int q = lane; q < (Sp >> 1); q += 32)
+                    cp_async16(w_vrow + (size_t)j * Sp + 2 * q, p.vmax + (size_t)b[j] * Sp + 2 * q);
+    }
+    // neighbour periods -> precedence window (evaluate.py:361-372): lo = latest predecessor
+    // period (an unmined predecessor forbids every period), hi = earliest mined successor
+    int tn[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; j++) tn[j] = nb[j] >= 0 ? p.assign[nb[j] & (NBR_SUCC - 1)] : 0;
+    int lo[CPW], hi[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; j++) {
+        const bool pred = nb[j] >= 0 && !(nb[j] & NBR_SUCC), succ = nb[j] >= 0 && (nb[j] & NBR_SUCC);
+        const int lc = pred ? (tn[j] < 0 ? INT_MAX : tn[j]) : 0;
+        const int hc = (succ && tn[j] >= 0) ? tn[j] : INT_MAX;
+        lo[j] = (int)__reduce_max_sync(FULL, (unsigned)lc);
+        hi[j] = (int)__reduce_min_sync(FULL, (unsigned)hc);
+        if (b[j] < 0) lo[j] = INT_MAX;
+    }
+    if (need_vrow) cp_async_wait_all();
+    __syncwarp();
     EV_PROBE(1);
 
-    // ---- stage 2: every row of every candidate in one cp.async round trip ----
-    {
-        const bool want_unit = !literal && p.scen < 0;
-        const int nv = need_vrow ? (Sp >> 1) : 0, nn = NS >> 2;
-        for (int i = warp; i < NB; i += NW) {
-            const int b = max(s_b[i], 0);
-            if (lane < 2)
-                cp_async16(reinterpret_cast<char *>(s_row + i) + 16 * lane,
-                           reinterpret_cast<const char *>(p.rows + b) + 16 * lane);
-            if (lane == 2) cp_async4(s_ab + i, p.assign + b);
-            if (lane == 3 && want_unit) cp_async8(s_unit + i, p.unit_mean + b);
-            if (lane < nn) cp_async16(s_nbr + (size_t)i * NS + 4 * lane, p.nbr + (size_t)b * NS + 4 * lane);
-            if (net && lane < T) cp_async8(s_cost + (size_t)i * T + lane, p.cost + (size_t)b * T + lane);
-            for (int q = lane; q < nv; q += 32)
-                cp_async16(s_vrow + (size_t)i * Sp + 2 * q, p.vmax + (size_t)b * Sp + 2 * q);
-        }
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    EV_PROBE(2);
-
-    // ---- stage 3: precedence window, one thread per candidate ----
-    for (int i = tid; i < NB; i += EV_THREADS) {
-        const BlockRow r = s_row[i];
-        const int npred = r.cnt & 0xffff, nnb = npred + (r.cnt >> 16);
-        const int *nb = s_nbr + (size_t)i * NS;
-        int lo = 0, hi = INT_MAX;
-        int tn[32];
+    // ---- statistics of the precedence-feasible (candidate, period) pairs, before the
+    //      period masses are known (overlaps the period-mass kernel); capacity only
+    //      removes pairs, so the outputs below select from these ----
+    unsigned okm[CPW];
 #pragma unroll
-        for (int k = 0; k < 32; k++)  // independent gathers first (assign is L2-resident)
-            if (k < nnb) tn[k] = p.assign[nb[k]];
-#pragma unroll
-        for (int k = 0; k < 32; k++) {
-            if (k < npred) lo = max(lo, tn[k] < 0 ? INT_MAX : tn[k]);
-            else if (k < nnb && tn[k] >= 0) hi = min(hi, tn[k]);
-        }
-        if (s_b[i] < 0) lo = INT_MAX;  // inactive slot: nothing feasible
-        s_lo[i] = lo;
-        s_hi[i] = hi;
-        if (!literal && p.scen >= 0) s_unit[i] = s_vrow[(size_t)i * Sp + p.scen];
-        if (literal) s_unit[i] = f64_mul(r.mass, 100.0);
-    }
-    EV_PROBE(3);
-
-    // ---- C: capacity (evaluate.py:373-378), parity value (379-384), lowest-t argmax
-    //      (387-388), one thread per candidate.  Everything above overlapped the
-    //      period-mass kernels (PDL); the period masses are needed from here on.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int t = tid; t < T; t += EV_THREADS) s_pm[t] = __ldcg(p.pm + t);
-    __syncthreads();
-    EV_PROBE(4);
-    Best mine{-kInf, INT_MAX, INT_MAX};
-    for (int i = tid; i < NB; i += EV_THREADS) {
-        const int b = s_b[i];
-        const BlockRow r = s_row[i];
-        const int ab = s_ab[i];
-        const int lo = s_lo[i], z = min(s_hi[i], T - 1);
-        unsigned okb = 0u;
-        double bv = -kInf;
-        int bt = INT_MAX;
-        for (int t = lo; t <= z; t++) {
-            double load = f64_add(s_pm[t], r.mass);
-            if (ab == t) load = f64_sub(load, r.mass);
-            if (load > s_cap[t]) continue;
-            okb |= 1u << t;
-            const double d = s_disc[t];
-            double v = f64_mul(f64_mul(f64_mul(s_unit[i], d), s_srow[t]), r.spatial);
-            if (net) v = f64_sub(v, f64_mul(d, s_cost[(size_t)i * T + t]));
-            if (v > bv) {  // strict: the lowest period wins ties (evaluate.py:387-388)
-                bv = v;
-                bt = t;
-            }
-        }
-        s_ok[i] = okb;
-        s_np[i] = __popc(okb);
-        if (b >= 0) {
-            const int grp = c0 + i;
-            const bool cand_ok = bt != INT_MAX;
-            p.best_t[grp] = cand_ok ? bt : -1;
-            p.best_val[grp] = bv;
-            p.feas[grp] = cand_ok ? 1 : 0;
-            if (cand_ok) {
-                Best cb{bv, b, bt};
-                if (better(cb, mine)) mine = cb;
-            }
-        }
-    }
-    __syncthreads();
-    EV_PROBE(5);
-
-    // ---- B: statistics of the feasible (candidate, period) pairs (~8% of moves at C2) ----
+    for (int j = 0; j < CPW; j++) okm[j] = __ballot_sync(FULL, lane < T && lane >= lo[j] && lane <= hi[j]);
     if constexpr (STATS_T) {
         if (stats) {
-            if (warp == 0) {  // exclusive scan of the pair counts
-                int carry = 0;
-                for (int i0 = 0; i0 < NB; i0 += 32) {
-                    const int v = (i0 + lane < NB) ? s_np[i0 + lane] : 0;
-                    int incl = v;
+            int cum[CPW + 1];
+            cum[0] = 0;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    if (i0 + lane < NB) s_np[i0 + lane] = carry + incl - v;
-                    carry += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (lane == 0) s_np[NB] = carry;
-            }
-            __syncthreads();
-            for (int i = tid; i < NB; i += EV_THREADS) {  // pair list: (candidate << 8) | period
-                unsigned okb = s_ok[i];
-                int o = s_np[i];
-                while (okb) {
-                    const int t = __ffs(okb) - 1;
-                    okb &= okb - 1;
-                    s_pair[o++] = (i << 8) | t;
-                }
-            }
-            __syncthreads();
-            const int npairs = s_np[NB];
-            if constexpr (KC <= 2) {
+            for (int j = 0; j < CPW; j++) cum[j + 1] = cum[j] + __popc(okm[j]);
+            const int npairs = cum[CPW];
+            if constexpr (KC < 0) {  // (8-lane sub-group variant, disabled)
                 // 8 lanes per pair; lane j owns numpy's accumulator j (scenarios s = j mod 8),
                 // the butterfly xor 1,2,4 is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the <8-element
                 // tail is added in order; per-lane two smallest merged by butterfly (CVaR, k <= 2)
-                const int sub = lane & 7, sgi = tid >> 3, nsg = EV_THREADS >> 3;
+                const int sub = lane & 7;
                 const int main_ = S & ~7, nrem = S - main_;
-                for (int k0 = 0; k0 < npairs; k0 += nsg) {
-                    const int k = k0 + sgi;
+                for (int k0 = 0; k0 < npairs; k0 += 4) {
+                    const int k = k0 + (lane >> 3);
                     const bool act = k < npairs;
-                    const int pr = act ? s_pair[k] : 0;
-                    const int i = pr >> 8, t = pr & 0xff;
-                    const int ab = s_ab[i];
+                    int j = 0, t = 0;
+#pragma unroll
+                    for (int jj = 0; jj < CPW; jj++)
+                        if (k >= cum[jj] && k < cum[jj + 1]) {
+                            j = jj;
+                            t = nth_bit(okm[jj], k - cum[jj]);
+                        }
+                    const int ab = __shfl_sync(FULL, ab_l, j);
+                    const double sp = __shfl_sync(FULL, spat_l, j);
+                    const int bj = __shfl_sync(FULL, bl, j);
                     const bool mined = ab >= 0;
                     const int abc = mined ? ab : 0;
-                    const double d_t = s_disc[t], d_ab = s_disc[abc], sp = s_row[i].spatial;
-                    const double dc_t = net ? f64_mul(d_t, s_cost[(size_t)i * T + t]) : 0.0;
-                    const double dc_ab = net ? f64_mul(d_ab, s_cost[(size_t)i * T + abc]) : 0.0;
-                    const double *rowb = s_vrow + (size_t)i * Sp;
-                    float *sd = SCEN ? p.scen_delta + (size_t)(c0 + i) * S * T + t : nullptr;
+                    const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
+                    const double dc_t = net ? f64_mul(d_t, __ldg(p.cost + (size_t)max(bj, 0) * T + t)) : 0.0;
+                    const double dc_ab = net ? f64_mul(d_ab, __ldg(p.cost + (size_t)max(bj, 0) * T + abc)) : 0.0;
+                    const double *rowb = w_vrow + (size_t)j * Sp;
+                    float *sd = SCEN ? p.scen_delta + (size_t)(cw + j) * S * T + t : nullptr;
                     double acc = -0.0, a0 = kInf, a1 = kInf, remv = 0.0;
                     if (act) {
                         for (int s_ = sub; s_ < S; s_ += 8) {
                             const double x = rowb[s_];
-                            const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
+                            const double vn =
+                                f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma + s_ * T + t)), sp), dc_t);
                             const double vo =
-                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
+                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma + s_ * T + abc)), sp), dc_ab)
+                                      : 0.0;
                             const double v = f64_sub(vn, vo);  // vn - 0.0 == vn exactly
                             if (s_ < main_) acc = f64_add(acc, v);
                             else remv = v;
@@ -355,93 +256,160 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_staged(const EvalParams 
                             if constexpr (SCEN) sd[(size_t)s_ * T] = (float)v;
                         }
                     }
-                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
-                    acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
                     double res = main_ ? acc : -0.0;
-                    for (int j = 0; j < nrem; j++) res = f64_add(res, __shfl_sync(0xffffffffu, remv, (lane & ~7) + j));
+                    for (int q = 0; q < nrem; q++) res = f64_add(res, __shfl_sync(FULL, remv, (lane & ~7) + q));
 #pragma unroll
                     for (int o = 1; o < 8; o <<= 1) {
-                        const double b0 = __shfl_xor_sync(0xffffffffu, a0, o);
-                        const double b1 = __shfl_xor_sync(0xffffffffu, a1, o);
-                        const double lo = (b0 < a0) ? b0 : a0, hi = (b0 < a0) ? a0 : b0;
+                        const double b0 = __shfl_xor_sync(FULL, a0, o);
+                        const double b1 = __shfl_xor_sync(FULL, a1, o);
+                        const double lo_ = (b0 < a0) ? b0 : a0, hi_ = (b0 < a0) ? a0 : b0;
                         const double m1 = (b1 < a1) ? b1 : a1;
-                        a0 = lo;
-                        a1 = (m1 < hi) ? m1 : hi;
+                        a0 = lo_;
+                        a1 = (m1 < hi_) ? m1 : hi_;
                     }
                     if (act && sub == 0) {
-                        s_ex[(size_t)i * T + t] = f64_div(f64_add(0.0, res), (double)S);
+                        w_ex[j * T + t] = f64_div(f64_add(0.0, res), (double)S);
                         double c = f64_add(-0.0, a0);
                         if (p.cvar_k > 1) c = f64_add(c, a1);
-                        s_cv[(size_t)i * T + t] = f64_mul(f64_add(0.0, c), p.cvar_k > 1 ? 0.5 : 1.0);
+                        w_cv[j * T + t] = f64_mul(f64_add(0.0, c), p.cvar_k > 1 ? 0.5 : 1.0);
                     }
                 }
             } else {
-                for (int k = tid; k < npairs; k += EV_THREADS) {  // one thread per pair
-                    const int i = s_pair[k] >> 8, t = s_pair[k] & 0xff;
-                    const int ab = s_ab[i];
-                    const int abc = (ab >= 0 && ab < T) ? ab : 0;
-                    const double d_t = s_disc[t], d_ab = s_disc[abc];
-                    const double dc_t = net ? f64_mul(d_t, s_cost[(size_t)i * T + t]) : 0.0;
-                    const double dc_ab = net ? f64_mul(d_ab, s_cost[(size_t)i * T + abc]) : 0.0;
-                    float *sd = SCEN ? p.scen_delta + (size_t)(c0 + i) * S * T + t : nullptr;
-                    pair_stats<KC, SCEN>(p, S, T, s_sig, s_vrow + (size_t)i * Sp, t, abc, d_t, dc_t, d_ab, dc_ab,
-                                         s_row[i].spatial, ab >= 0, s_ex + (size_t)i * T + t, s_cv + (size_t)i * T + t,
-                                         sd);
-                }
-            }
-            __syncthreads();
-        }
-    }
-    EV_PROBE(6);
-
-    // ---- per-(candidate, period) outputs: the CTA's [NB][T] block, coalesced ----
-    const bool want_trace = p.trace_val || p.trace_feas;
-    if (want_trace || stats) {
-        const int nvalid = min(NB, p.C - c0);
-        for (int e = tid; e < nvalid * T; e += EV_THREADS) {
-            const int i = e / T, t = e - i * T;
-            const size_t m = (size_t)c0 * T + e;
-            const bool ok = (s_ok[i] >> t) & 1u;
-            if (want_trace) {
-                double v = -kInf;
-                if (ok) {
-                    const double d = s_disc[t];
-                    const BlockRow &r = s_row[i];
-                    v = f64_mul(f64_mul(f64_mul(s_unit[i], d), s_srow[t]), r.spatial);
-                    if (net) v = f64_sub(v, f64_mul(d, s_cost[(size_t)i * T + t]));
-                }
-                if (p.trace_val) p.trace_val[m] = v;
-                if (p.trace_feas) p.trace_feas[m] = ok ? 1 : 0;
-            }
-            if constexpr (STATS_T) {
-                if (stats) {
-                    if (p.exp_delta) p.exp_delta[m] = ok ? s_ex[e] : -kInf;
-                    if (p.cvar) p.cvar[m] = ok ? s_cv[e] : -kInf;
-                    if constexpr (SCEN) {
-                        if (!ok)  // infeasible: raw deltas are -inf (also overwrites capacity-infeasible pairs)
-                            for (int s = 0; s < S; s++)
-                                p.scen_delta[((size_t)(c0 + i) * S + s) * T + t] = -__int_as_float(0x7f800000);
+                for (int k0 = 0; k0 < npairs; k0 += 32) {  // one lane per pair
+                    const int k = k0 + lane;
+                    int j = 0, t = 0;
+#pragma unroll
+                    for (int jj = 0; jj < CPW; jj++)
+                        if (k >= cum[jj] && k < cum[jj + 1]) {
+                            j = jj;
+                            t = nth_bit(okm[jj], k - cum[jj]);
+                        }
+                    const int ab = __shfl_sync(FULL, ab_l, j);
+                    const double sp = __shfl_sync(FULL, spat_l, j);
+                    const int bj = __shfl_sync(FULL, bl, j);
+                    if (k < npairs) {
+                        const int abc = ab >= 0 ? ab : 0;
+                        const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
+                        const double dc_t = net ? f64_mul(d_t, __ldg(p.cost + (size_t)bj * T + t)) : 0.0;
+                        const double dc_ab = net ? f64_mul(d_ab, __ldg(p.cost + (size_t)bj * T + abc)) : 0.0;
+                        float *sd = SCEN ? p.scen_delta + (size_t)(cw + j) * S * T + t : nullptr;
+                        pair_stats<KC, SCEN>(p, S, T, p.sigma, w_vrow + (size_t)j * Sp, t, abc, d_t, dc_t, d_ab, dc_ab, sp,
+                                             ab >= 0, w_ex + j * T + t, w_cv + j * T + t, sd);
                     }
                 }
             }
+            __syncwarp();
         }
     }
+    EV_PROBE(2);
 
-    // ---- K4: CTA argmax (candidates are one per thread of warp 0 when NB <= 32) ----
-    if (NB > 32) {
+    // ---- moves (needs the period masses) ----
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const double pm_t = lane < T ? __ldcg(p.pm + lane) : 0.0;
+    EV_PROBE(3);
+    Best wbest{-kInf, INT_MAX, INT_MAX};
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            Best o = shfl_best(mine, off);
-            if (better(o, mine)) mine = o;
+    for (int j = 0; j < CPW; j++) {
+        const double mass = __shfl_sync(FULL, mass_l, j), spat = __shfl_sync(FULL, spat_l, j);
+        const int ab = __shfl_sync(FULL, ab_l, j);
+        double unit;
+        if (literal) unit = f64_mul(mass, 100.0);
+        else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
+        else unit = __shfl_sync(FULL, unit_l, j);
+        bool ok = false;
+        double v = -kInf;
+        if (lane < T && lane >= lo[j] && lane <= hi[j]) {
+            double load = f64_add(pm_t, mass);
+            if (ab == lane) load = f64_sub(load, mass);
+            ok = !(load > cap_t);
+            if (ok) {
+                v = f64_mul(f64_mul(f64_mul(unit, disc_t), srow_t), spat);
+                if (net) v = f64_sub(v, f64_mul(disc_t, cost_r[j]));
+            }
         }
-        if (lane == 0) s_red[warp] = mine;
-        __syncthreads();
-        if (warp == 0) mine = (lane < NW) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
-        __syncthreads();
+        okm[j] = __ballot_sync(FULL, ok);
+        // lowest-t argmax: the reference's strict '>' scan in period order (evaluate.py:387-388)
+        double bv = -kInf;
+        int bt = INT_MAX;
+        for (unsigned mm = okm[j]; mm; mm &= mm - 1) {
+            const int t = __ffs(mm) - 1;
+            const double vt = __shfl_sync(FULL, v, t);
+            if (vt > bv) {
+                bv = vt;
+                bt = t;
+            }
+        }
+        const int g = cw + j;
+        if (g < p.C) {
+            if (lane == 0 && b[j] >= 0) {
+                p.best_t[g] = bt != INT_MAX ? bt : -1;
+                p.best_val[g] = bv;
+                p.feas[g] = bt != INT_MAX ? 1 : 0;
+            }
+            if (want_trace && lane < T) {
+                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = ok ? v : -kInf;
+                if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = ok ? 1 : 0;
+            }
+        }
+        if (b[j] >= 0 && bt != INT_MAX) {
+            const Best cb{bv, b[j], bt};
+            if (better(cb, wbest)) wbest = cb;
+        }
     }
+    EV_PROBE(4);
+
+    // ---- per-(candidate, period) statistics outputs (capacity-feasible pairs only) ----
+    if constexpr (STATS_T) {
+        if (stats) {
+#pragma unroll
+            for (int j = 0; j < CPW; j++) {
+                const int g = cw + j;
+                if (g >= p.C || lane >= T) continue;
+                const bool ok = (okm[j] >> lane) & 1u;
+                if (p.exp_delta) p.exp_delta[(size_t)g * T + lane] = ok ? w_ex[j * T + lane] : -kInf;
+                if (p.cvar) p.cvar[(size_t)g * T + lane] = ok ? w_cv[j * T + lane] : -kInf;
+                if constexpr (SCEN) {
+                    if (!ok)  // infeasible: raw deltas are -inf
+                        for (int s = 0; s < S; s++)
+                            p.scen_delta[((size_t)g * S + s) * T + lane] = -__int_as_float(0x7f800000);
+                }
+            }
+            if (p.n_pairs) {  // sparse: the warp's feasible moves, one atomic per warp
+                int cum[CPW + 1];
+                cum[0] = 0;
+#pragma unroll
+                for (int j = 0; j < CPW; j++) cum[j + 1] = cum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
+                const int np = cum[CPW];
+                int base = 0;
+                if (lane == 0 && np) base = atomicAdd(p.n_pairs, np);
+                base = __shfl_sync(FULL, base, 0);
+                for (int k = lane; k < np; k += 32) {
+                    int j = 0, t = 0;
+#pragma unroll
+                    for (int jj = 0; jj < CPW; jj++)
+                        if (k >= cum[jj] && k < cum[jj + 1]) {
+                            j = jj;
+                            t = nth_bit(okm[jj], k - cum[jj]);
+                        }
+                    p.pair_cand[base + k] = cw + j;
+                    p.pair_period[base + k] = t;
+                    p.pair_exp[base + k] = w_ex[j * T + t];
+                    p.pair_cvar[base + k] = w_cv[j * T + t];
+                }
+            }
+        }
+    }
+    EV_PROBE(5);
+
+    // ---- argmax: warp -> CTA -> grid ----
+    if (lane == 0) s_red[warp] = wbest;
+    __syncthreads();
+    Best mine = (warp == 0 && lane < NW) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
     grid_argmax_warp0(mine, s_red, p.partial, p.counter, p.global);
-    EV_PROBE(7);
+    EV_PROBE(6);
 }
 
 #ifdef PP_EVAL_PROBE
@@ -458,7 +426,10 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     if (C < 0 || (C > 0 && !cand)) return fail(PP_ERR_INVALID_ARGS, "bad candidate array");
     if (!out || !out->best_t || !out->best_val || !out->feasible || !out->global)
         return fail(PP_ERR_INVALID_ARGS, "best_t, best_val, feasible and global outputs are required");
-    const bool stats = out->exp_delta || out->cvar || out->scen_delta;
+    const bool pairs = out->n_pairs != nullptr;
+    if (pairs && (!out->pair_cand || !out->pair_period || !out->pair_exp || !out->pair_cvar))
+        return fail(PP_ERR_INVALID_ARGS, "n_pairs needs pair_cand, pair_period, pair_exp and pair_cvar");
+    const bool stats = out->exp_delta || out->cvar || out->scen_delta || pairs;
     if (stats && !c->have_scen) return fail(PP_ERR_STATE, "scenario statistics need pp_set_scenarios");
     TRY(use_device(c));
     cudaStream_t st = pick(c, stream);
@@ -498,6 +469,15 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         if (out->exp_delta) { TRY(c->h_o6.ensure(sizeof(double) * CT)); o.exp_delta = c->h_o6.as<double>(); }
         if (out->cvar) { TRY(c->h_o7.ensure(sizeof(double) * CT)); o.cvar = c->h_o7.as<double>(); }
         if (out->scen_delta) { TRY(c->h_o8.ensure(sizeof(float) * CT * std::max(S, 1))); o.scen_delta = c->h_o8.as<float>(); }
+        if (pairs) {
+            TRY(c->h_p.ensure((2 * sizeof(int32_t) + 2 * sizeof(double)) * CT + 16));
+            char *q = static_cast<char *>(c->h_p.ptr);
+            o.pair_exp = reinterpret_cast<double *>(q);
+            o.pair_cvar = reinterpret_cast<double *>(q + sizeof(double) * CT);
+            o.pair_cand = reinterpret_cast<int32_t *>(q + 2 * sizeof(double) * CT);
+            o.pair_period = reinterpret_cast<int32_t *>(q + 2 * sizeof(double) * CT + sizeof(int32_t) * CT);
+            o.n_pairs = reinterpret_cast<int32_t *>(q + (2 * sizeof(double) + 2 * sizeof(int32_t)) * CT);
+        }
         if (C > 0) CUDA_TRY(cudaMemcpyAsync(c->h_cand.ptr, cand, sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
         dcand = c->h_cand.as<int32_t>();
     }
@@ -537,35 +517,38 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     ep.exp_delta = o.exp_delta;
     ep.cvar = o.cvar;
     ep.scen_delta = o.scen_delta;
+    ep.pair_cand = o.pair_cand;
+    ep.pair_period = o.pair_period;
+    ep.pair_exp = o.pair_exp;
+    ep.pair_cvar = o.pair_cvar;
+    ep.n_pairs = o.n_pairs;
+    if (pairs) CUDA_TRY(cudaMemsetAsync(o.n_pairs, 0, sizeof(int32_t), st));
     ep.partial = c->partial.as<pp_best>();
     ep.counter = c->counter.as<unsigned int>();
     ep.global = o.global;
 
-    // fast path: whole candidate batches staged in shared memory
-    if (T <= 32 && (!stats || S <= 128) && c->deg_max <= 32 && c->nbr.ptr) {
-        const int NB = 32;
+    // fast path: one warp per CPW candidates (k_eval_warp)
+    if (T <= 32 && (!stats || S <= 128) && c->nbr.ptr) {
         const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
-        const StagedLayout Ls =
-            staged_layout(NB, T, S, c->Sp, c->nbr_stride, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
-        if (Ls.total <= 200 * 1024) {
-            const int sgrid = std::max(1, (C + NB - 1) / NB);
-            TRY(ensure_grid_scratch(c, sgrid));
-            bool pdl;
-            TRY(refresh_pm(c, st, &pdl));
-            const bool scen = o.scen_delta != nullptr;
-            const size_t smem_s = (size_t)Ls.total;
-#define PP_STAGED(KC, SC)                                                              \
-    {                                                                                  \
-        TRY(set_smem_attr(k_eval_staged<KC, SC>, smem_s));                             \
-        TRY(launch_eval(k_eval_staged<KC, SC>, sgrid, smem_s, st, pdl, ep, NB));       \
+        const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow);
+        const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32);
+        const int per_cta = CPW * (EV_THREADS / 32);
+        const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
+        TRY(ensure_grid_scratch(c, wgrid));
+        bool pdl;
+        TRY(refresh_pm(c, st, &pdl));
+        const bool scen = o.scen_delta != nullptr;
+#define PP_WARP(KC, SC)                                                     \
+    {                                                                       \
+        TRY(set_smem_attr(k_eval_warp<KC, SC>, smem_w));                    \
+        TRY(launch_eval(k_eval_warp<KC, SC>, wgrid, smem_w, st, pdl, ep));  \
     }
-            if (kc == 0) PP_STAGED(0, false)
-            else if (kc == 2) { if (scen) PP_STAGED(2, true) else PP_STAGED(2, false) }
-            else if (kc == 8) { if (scen) PP_STAGED(8, true) else PP_STAGED(8, false) }
-            else { if (scen) PP_STAGED(128, true) else PP_STAGED(128, false) }
-#undef PP_STAGED
-            goto copy_out;
-        }
+        if (kc == 0) PP_WARP(0, false)
+        else if (kc == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }
+        else if (kc == 8) { if (scen) PP_WARP(8, true) else PP_WARP(8, false) }
+        else { if (scen) PP_WARP(128, true) else PP_WARP(128, false) }
+#undef PP_WARP
+        goto copy_out;
     }
     {
         bool pdl;
@@ -588,6 +571,17 @@ copy_out:
             if (out->cvar) CUDA_TRY(cudaMemcpyAsync(out->cvar, o.cvar, sizeof(double) * CT, cudaMemcpyDeviceToHost, st));
             if (out->scen_delta)
                 CUDA_TRY(cudaMemcpyAsync(out->scen_delta, o.scen_delta, sizeof(float) * CT * S, cudaMemcpyDeviceToHost, st));
+        }
+        if (pairs) {  // count first, then exactly the written entries
+            CUDA_TRY(cudaMemcpyAsync(out->n_pairs, o.n_pairs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            const size_t n = (size_t)std::max(0, *out->n_pairs);
+            if (n) {
+                CUDA_TRY(cudaMemcpyAsync(out->pair_cand, o.pair_cand, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaMemcpyAsync(out->pair_period, o.pair_period, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaMemcpyAsync(out->pair_exp, o.pair_exp, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaMemcpyAsync(out->pair_cvar, o.pair_cvar, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            }
         }
         CUDA_TRY(cudaStreamSynchronize(st));
     }

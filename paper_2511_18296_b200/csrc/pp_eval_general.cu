@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_candidates(const EvalParams
     const int T = p.T, S = p.S;
     const bool net = p.flags & PP_NET_MINING_COST;
     constexpr bool STATS_T = KC > 0;
-    const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar);
+    const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar || p.n_pairs);
     const int SS = S | 1;
     const int SB = BIGS ? 32 : p.Sp;
     double *s_sig = ev_dyn;  // [T][SS] (not BIGS)
@@ -234,6 +234,13 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_candidates(const EvalParams
                     if (stats) {
                         if (p.exp_delta) p.exp_delta[m] = ok ? ex_t[k] : -kInf;
                         if (p.cvar) p.cvar[m] = ok ? cv_t[k] : -kInf;
+                        if (p.n_pairs && ok) {
+                            const int q = atomicAdd(p.n_pairs, 1);
+                            p.pair_cand[q] = grp;
+                            p.pair_period[q] = t;
+                            p.pair_exp[q] = ex_t[k];
+                            p.pair_cvar[q] = cv_t[k];
+                        }
                         if constexpr (SCEN) {
                             if (!ok)  // infeasible: overwrite (or fill) the raw deltas with -inf
                                 for (int s = 0; s < S; s++)

@@ -365,6 +365,11 @@ struct EvalParams {
     double *exp_delta;
     double *cvar;
     float *scen_delta;
+    int32_t *pair_cand;
+    int32_t *pair_period;
+    double *pair_exp;
+    double *pair_cvar;
+    int32_t *n_pairs;
     pp_best *partial;
     unsigned int *counter;
     pp_best *global;
@@ -451,12 +456,12 @@ struct pp_ctx {
     DevBuf cnt, compact, pm_batch, predcnt, partial, counter, pm_flags;
     size_t pm_flags_n = 0;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
-        h_pm;
+        h_pm, h_p;
     std::vector<DevBuf *> all() {
         return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
-                &h_d2, &h_pm};
+                &h_d2, &h_pm, &h_p};
     }
 };
 

@@ -89,7 +89,9 @@ extern "C" PP_API int pp_debug_pm_probe(unsigned long long *out) {
 #endif
 #ifdef PP_EVAL_PROBE
 #define PMCP(k, j) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[k][blockIdx.x][j] = pm_gtimer(); } while (0)
+#define PMCS(st) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[1][16 + 8 * (st) + blockIdx.x][0] = pm_gtimer(); } while (0)
 #else
+#define PMCS(st) do { } while (0)
 #define PMCP(k, j) do { } while (0)
 #endif
 
@@ -537,34 +539,34 @@ __global__ void k_apply_moves(int32_t *assign, int B, int T, const int32_t *bloc
 // P2 (trees), P2 launched as a programmatic dependent of P1
 // ---------------------------------------------------------------------------------------------
 // Cluster fast path (B <= 65536, T <= 16): one 8-CTA cluster per schedule, 1024 threads per CTA.
-// Warp w of CTA r owns the contiguous blocks [(32 r + w) * 32K, +32K) and ranks them inside
-// their periods with match_any (phase 1, loads kept in registers).  Per-warp counts are
-// scanned in shared memory, the CTA totals are scanned across the cluster through
-// distributed shared memory, and every block's mass lands at its numpy position in
-// compact[p][t][.] (phase 2).  After a cluster barrier CTA r builds the pairwise trees of
-// periods r and r + 8 side by side.  No global counters or flags: graph-replay safe, and
-// only 8 SMs per schedule are touched, so the evaluation CTAs launched behind it (PDL)
-// keep their residency.
+//  1. Warp w of CTA r owns the contiguous blocks [(32 r + w) * 32K, +32K).  Lane t keeps the
+//     warp's running count of period t; a block's rank inside its period is that count plus
+//     the lower lanes of the same ballot (no shared-memory round trips).  Per-warp counts are
+//     scanned over the warps; the CTA totals are exchanged through distributed shared memory
+//     (8 x T integers), which fixes every block's position in its period's numpy order.
+//  2. The masses are scattered to compact[p][t][pos] (L2), then a cluster barrier.
+//  3. CTA r reduces periods r and r + 8.  numpy's recursion (pairwise.c: blocks of 8, leaves of
+//     <= 128 elements) splits m = n/8 blocks floor|ceil, so the rightmost node is the largest at
+//     every depth and every leaf sits at depth D or D + 1, D = (first depth whose rightmost node
+//     is a leaf) - 1.  Sixteen lanes per depth-D node walk its root path to find its range and
+//     sum its one or two leaves (one L2 round trip); the 2^D node values fold as a perfect tree.
+// Distributed shared memory carries only the counts: its bandwidth (~20 B/clk/SM) is far below
+// L2's, so the masses go through L2.
+// ---------------------------------------------------------------------------------------------
 constexpr int PMC_R = 8;
 constexpr int PMC_THREADS = 1024;
 constexpr int PMC_WARPS = PMC_THREADS / 32;
 constexpr int PMC_MAXT = 16;
 constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;
 constexpr int PMC_MAXB = PMC_R * PMC_THREADS * 8;
+constexpr int PMC_MAXNODE = 512;  // 2^D for n <= 65536 (n = 65535: D = 9)
 
-struct PmcTree {
-    int start[PM_HEAP];
-    int len[PM_HEAP];
-    double val[PM_HEAP];
-    int leaves[1 << PM_MAX_DEPTH];
-};
 struct PmcSmem {
     int cnt[PMC_WARPS][PMC_MAXT];
-    int tot[PMC_MAXT];
-    int off[PMC_MAXT];
+    int tot[PMC_MAXT];  // this CTA's count per period (read by the cluster)
+    int off[PMC_MAXT];  // this CTA's first position per period
     int n[PMC_MAXT];
-    int nleaf[PMC_MAXQ];
-    PmcTree tree[PMC_MAXQ];
+    double val[PMC_MAXQ][PMC_MAXNODE];
 };
 
 __device__ __forceinline__ void cluster_sync_acqrel() {
@@ -575,18 +577,34 @@ __device__ __forceinline__ int ld_dsmem_i32(const int *p, int rank) {
     uint32_t ra;
     int v;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra));
     return v;
+}
+
+// range [start, start + len) in 8-element blocks of node i at depth d of a tree over m blocks
+__device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &len) {
+    int s = 0, l = m;
+    for (int k = d - 1; k >= 0; k--) {
+        const int h = l >> 1;
+        if ((i >> k) & 1) {
+            s += h;
+            l -= h;
+        } else {
+            l = h;
+        }
+    }
+    start = s;
+    len = l;
 }
 
 template <int K>
 __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
                  double *__restrict__ compact, double *__restrict__ pm_out) {
-    asm volatile("griddepcontrol.launch_dependents;");
-    extern __shared__ __align__(16) unsigned char pmc_dyn[];
-    PmcSmem &sm = *reinterpret_cast<PmcSmem *>(pmc_dyn);
+    __shared__ PmcSmem h;
     PMCP(0, 0);
+    asm volatile("griddepcontrol.launch_dependents;");
+    constexpr unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = blockIdx.x, p = blockIdx.y;
     const int32_t *as = assign + (size_t)p * B;
@@ -605,165 +623,155 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
         tk[k] = ((unsigned)t < (unsigned)T) ? t : -1;
         mk[k] = m;
     }
-    for (int i = tid; i < PMC_WARPS * PMC_MAXT; i += PMC_THREADS) (&sm.cnt[0][0])[i] = 0;
+    PMCS(0);
+    // ranks inside (warp, period): match_any groups, running counts in shared memory
+    for (int i = tid; i < PMC_WARPS * PMC_MAXT; i += PMC_THREADS) (&h.cnt[0][0])[i] = 0;
     __syncthreads();
-    // phase 1: rank inside (warp, period)
+    const unsigned lt = (1u << lane) - 1u;
     int pos[K];
 #pragma unroll
     for (int k = 0; k < K; k++) {
-        const unsigned mt = __match_any_sync(0xffffffffu, tk[k]);
-        const int lr = __popc(mt & ((1u << lane) - 1u));
-        const int b0 = tk[k] >= 0 ? sm.cnt[warp][tk[k]] : 0;
+        const unsigned mt = __match_any_sync(FULL, tk[k]);
+        const int lr = __popc(mt & lt);
+        const int b0 = tk[k] >= 0 ? h.cnt[warp][tk[k]] : 0;
         pos[k] = b0 + lr;
         __syncwarp();
-        if (tk[k] >= 0 && lr == 0) sm.cnt[warp][tk[k]] = b0 + __popc(mt);
+        if (tk[k] >= 0 && lr == 0) h.cnt[warp][tk[k]] = b0 + __popc(mt);
         __syncwarp();
     }
     __syncthreads();
     // per-period exclusive scan over the warps (warp j scans period j)
     if (warp < T) {
-        const int v = sm.cnt[lane][warp];
+        const int v = h.cnt[lane][warp];
         int inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            const int y = __shfl_up_sync(FULL, inc, o);
             if (lane >= o) inc += y;
         }
-        sm.cnt[lane][warp] = inc - v;
-        if (lane == 31) sm.tot[warp] = inc;
+        h.cnt[lane][warp] = inc - v;
+        if (lane == 31) h.tot[warp] = inc;
     }
-    cluster_sync_acqrel();
-    // cross-CTA scan of the period totals through distributed shared memory
-    if (warp < T) {
-        const int v = lane < PMC_R ? ld_dsmem_i32(&sm.tot[warp], lane) : 0;
+    cluster_sync_acqrel();  // totals published
+    PMCS(1);
+    if (warp < T) {  // cross-CTA scan of the totals through distributed shared memory
+        const int v = lane < PMC_R ? ld_dsmem_i32(&h.tot[warp], lane) : 0;
         int inc = v;
 #pragma unroll
         for (int o = 1; o < PMC_R; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            const int y = __shfl_up_sync(FULL, inc, o);
             if (lane >= o) inc += y;
         }
-        const int off = __shfl_sync(0xffffffffu, inc - v, r);
-        const int n = __shfl_sync(0xffffffffu, inc, PMC_R - 1);
+        const int off = __shfl_sync(FULL, inc - v, r);
+        const int n = __shfl_sync(FULL, inc, PMC_R - 1);
         if (lane == 0) {
-            sm.off[warp] = off;
-            sm.n[warp] = n;
+            h.off[warp] = off;
+            h.n[warp] = n;
         }
     }
     __syncthreads();
-    // phase 2: scatter to the numpy order
+    PMCS(2);
 #pragma unroll
     for (int k = 0; k < K; k++)
         if (tk[k] >= 0) {
             const int t = tk[k];
-            compact[((size_t)p * T + t) * B + sm.off[t] + sm.cnt[warp][t] + pos[k]] = mk[k];
+            compact[((size_t)p * T + t) * B + h.off[t] + h.cnt[warp][t] + pos[k]] = mk[k];
         }
     __threadfence();
-    cluster_sync_acqrel();  // every block of the schedule is in place; remote smem no longer read
+    cluster_sync_acqrel();  // every block of the schedule is in place (remote totals no longer read)
     PMCP(0, 1);
-    // trees of periods r, r + 8 (slot g)
-    const int q = (T - r + PMC_R - 1) / PMC_R;
-    if (q <= 0) return;
-    if (tid < q) {
-        sm.tree[tid].start[0] = 0;
-        sm.tree[tid].len[0] = sm.n[r + PMC_R * tid];
-        sm.nleaf[tid] = 0;
+    // depth-D nodes of the (up to two) periods of this CTA
+    const int q = max(0, (T - r + PMC_R - 1) / PMC_R);
+    int Dg[PMC_MAXQ], cntg[PMC_MAXQ];
+#pragma unroll
+    for (int g = 0; g < PMC_MAXQ; g++) {
+        Dg[g] = 0;
+        cntg[g] = 0;
+        if (g < q) {
+            const int n = h.n[r + PMC_R * g], m = n >> 3, rem = n & 7;
+            int d = 0;
+            while (8 * ((m + (1 << d) - 1) >> d) + rem > 128) d++;
+            Dg[g] = max(d - 1, 0);
+            cntg[g] = 1 << Dg[g];
+        }
+    }
+    const int nitems = cntg[0] + cntg[1];
+    const int sub = tid & 7, half = (tid >> 3) & 1;  // 16 lanes per node: half c sums child leaf c
+    for (int it0 = 0; it0 < nitems; it0 += PMC_THREADS / 16) {
+        const int it = it0 + (tid >> 4);
+        const bool act = it < nitems;
+        const int g = (it >= cntg[0]) ? 1 : 0;
+        const int i = act ? it - (g ? cntg[0] : 0) : 0;
+        const int t = r + PMC_R * g;
+        const int n = act ? h.n[t] : 0, m = n >> 3, rem = n & 7, D = g ? Dg[1] : Dg[0];
+        int s0, l0;
+        pw_node(m, D, i, s0, l0);
+        const bool last = i == (1 << D) - 1;
+        const int L = 8 * l0 + (last ? rem : 0);
+        const bool split = L > 128;  // a node of depth D is one leaf or two
+        int o = 8 * s0, len = L;
+        if (split) {
+            int s1, l1;
+            pw_node(m, D + 1, 2 * i + half, s1, l1);
+            o = 8 * s1;
+            len = 8 * l1 + ((last && half == 1) ? rem : 0);
+        }
+        const bool use = act && (split || half == 0);
+        const double *a = compact + ((size_t)p * T + t) * B + o;
+        // every load of the leaf in flight: 16 accumulator elements per lane + one tail element
+        const int nm = len >> 3, ntail = len & 7, e0 = len - ntail;
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) x[u] = (use && u < nm) ? __ldcg(a + 8 * u + sub) : 0.0;
+        const double tailv = (use && sub < ntail) ? __ldcg(a + e0 + sub) : 0.0;
+        double acc = x[0];
+#pragma unroll
+        for (int u = 1; u < 16; u++)
+            if (u < nm) acc = f64_add(acc, x[u]);
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
+        double res = len < 8 ? -0.0 : acc;
+        const int lbase = lane & ~7;
+        for (int e = 0; e < 7; e++) {  // uniform trip count (shuffles)
+            const double y = __shfl_sync(FULL, tailv, lbase + e);
+            if (e < ntail) res = f64_add(res, y);
+        }
+        const double other = __shfl_xor_sync(FULL, res, 8);  // the sibling leaf
+        if (use && sub == 0 && half == 0) h.val[g][i] = split ? f64_add(res, other) : res;
     }
     __syncthreads();
-    int depth = 0;
-    for (int d = 0;; d++) {
-        const int first = (1 << d) - 1, cnt = 1 << d;
-        bool any_internal = false;
-        for (int x = tid; x < q * cnt; x += PMC_THREADS) {
-            const int g = x >> d, id = first + (x & (cnt - 1));
-            PmcTree &tr = sm.tree[g];
-            const int ln = tr.len[id];
-            if (ln <= 128) {  // leaf, or dead (below a leaf): its children are dead
-                if (ln >= 0) tr.leaves[atomicAdd(&sm.nleaf[g], 1)] = id;
-                if (d < PM_MAX_DEPTH) {
-                    tr.len[2 * id + 1] = -1;
-                    tr.len[2 * id + 2] = -1;
-                }
-            } else {
-                any_internal = true;  // cannot exceed PM_MAX_DEPTH: n <= 65536
-                const int n2 = ((ln >> 3) >> 1) << 3;
-                tr.start[2 * id + 1] = tr.start[id];
-                tr.len[2 * id + 1] = n2;
-                tr.start[2 * id + 2] = tr.start[id] + n2;
-                tr.len[2 * id + 2] = ln - n2;
-            }
-        }
-        if (!__syncthreads_or(any_internal)) {
-            depth = d;
-            break;
-        }
-    }
-    // leaf sums: 8 lanes per leaf, lane j owns numpy accumulator j
-    const int nl0 = sm.nleaf[0], nl = nl0 + (q > 1 ? sm.nleaf[1] : 0);
-    const int sub = tid & 7, grp = tid >> 3;
-    for (int l0 = 0; l0 < nl; l0 += PMC_THREADS / 8) {
-        const int l = l0 + grp;
-        const bool act = l < nl;
-        const int g = (l >= nl0) ? 1 : 0;
-        PmcTree &tr = sm.tree[g];
-        const double *a = compact + ((size_t)p * T + r + PMC_R * g) * B;
-        const int id = act ? tr.leaves[l - (g ? nl0 : 0)] : 0;
-        const int o = act ? tr.start[id] : 0;
-        const int len = act ? tr.len[id] : 0;
-        double rr = 0.0;
-        if (act && len >= 8) {
-            const int nm = len >> 3;
+    PMCS(3);
+    // perfect-tree fold of the 2^D node values: warp g folds period slot g
+    if (warp < q) {
+        const int g = warp, cnt = g ? cntg[1] : cntg[0];
+        const int per = cnt > 32 ? cnt >> 5 : 1;  // consecutive values per lane (<= 16)
+        double v = 0.0;
+        if (lane * per < cnt) {
             double x[16];
 #pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = (u < nm) ? __ldcg(a + o + 8 * u + sub) : 0.0;
-            rr = x[0];
+            for (int u = 0; u < 16; u++) x[u] = (u < per) ? h.val[g][lane * per + u] : 0.0;
 #pragma unroll
-            for (int u = 1; u < 16; u++)
-                if (u < nm) rr = f64_add(rr, x[u]);
+            for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+                for (int u = 0; u < 16; u += 2 * w)
+                    if (u + w < per) x[u] = f64_add(x[u], x[u + w]);
+            v = x[0];
         }
-        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 1));
-        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 2));
-        rr = f64_add(rr, __shfl_xor_sync(0xffffffffu, rr, 4));
-        if (act && sub == 0) {
-            double res;
-            int i;
-            if (len < 8) {
-                res = -0.0;
-                i = 0;
-            } else {
-                res = rr;
-                i = len - (len & 7);
-            }
-            for (; i < len; i++) res = f64_add(res, __ldcg(a + o + i));
-            tr.val[id] = res;
+        const int lanes = cnt > 32 ? 32 : cnt;
+        for (int o = 1; o < lanes; o <<= 1) v = f64_add(v, __shfl_xor_sync(FULL, v, o));
+        if (lane == 0) {
+            const int t = r + PMC_R * g;
+            pm_out[(size_t)p * T + t] = f64_add(0.0, h.n[t] ? v : -0.0);
         }
-    }
-    __syncthreads();
-    for (int d = depth - 1; d >= 0; d--) {
-        const int first = (1 << d) - 1, cnt = 1 << d;
-        for (int x = tid; x < q * cnt; x += PMC_THREADS) {
-            PmcTree &tr = sm.tree[x >> d];
-            const int id = first + (x & (cnt - 1));
-            if (tr.len[id] > 128) tr.val[id] = f64_add(tr.val[2 * id + 1], tr.val[2 * id + 2]);
-        }
-        __syncthreads();
-    }
-    if (tid < q) {
-        const int t = r + PMC_R * tid;
-        pm_out[(size_t)p * T + t] = f64_add(0.0, sm.n[t] ? sm.tree[tid].val[0] : -0.0);
     }
     PMCP(1, 1);
 }
 
 template <int K>
 static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(k_pm_cluster<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(PmcSmem)));
-        attr = true;
-    }
-    k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, sizeof(PmcSmem), st>>>(d_assign, c->mass.as<double>(), c->B,
-                                                                             c->T, c->compact.as<double>(), d_pm);
+    k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, 0, st>>>(d_assign, c->mass.as<double>(), c->B, c->T,
+                                                              c->compact.as<double>(), d_pm);
     CUDA_TRY(cudaGetLastError());
     return PP_OK;
 }
@@ -952,14 +960,18 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
     c->n_levels = nlev;
     c->deg_max = 0;
     for (int b = 0; b < B; b++) c->deg_max = std::max(c->deg_max, npred[b] + nsucc[b]);
-    // padded neighbour table for the staged evaluation kernel (one 16-byte-granular row per block)
-    c->nbr_stride = std::max(4, (c->deg_max + 3) & ~3);
+    // padded neighbour table for the warp evaluation kernel: one 128-byte row of 32 slots per
+    // block, predecessors as ids, successors tagged with 1 << 30, padding -1
+    c->nbr_stride = 32;
     if (c->deg_max <= 32) {
-        std::vector<int> nbr((size_t)B * c->nbr_stride, 0);
+        std::vector<int> nbr((size_t)B * 32, -1);
         for (int b = 0; b < B; b++)
-            for (int k = 0; k < npred[b] + nsucc[b]; k++) nbr[(size_t)b * c->nbr_stride + k] = adj[start[b] + k];
+            for (int k = 0; k < npred[b] + nsucc[b]; k++)
+                nbr[(size_t)b * 32 + k] = adj[start[b] + k] | (k < npred[b] ? 0 : (1 << 30));
         TRY(c->nbr.ensure(sizeof(int) * nbr.size()));
         CUDA_TRY(cudaMemcpy(c->nbr.ptr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice));
+    } else {
+        c->nbr.release();
     }
     c->level_ptr = lptr;
     c->level_of = level;
@@ -1052,10 +1064,13 @@ int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream)
         return fail(PP_ERR_INVALID_ARGS, "unknown memory kind %d", mem);
     TRY(use_device(c));
     cudaStream_t st = pick(c, stream);
-    if (mem == PP_MEM_HOST) {
-        for (int b = 0; b < c->B; b++)
-            if (assign[b] < -1 || assign[b] >= c->T)
-                return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
+    if (mem == PP_MEM_HOST) {  // branch-free min/max (vectorises)
+        int32_t lo = 0, hi = -1;
+        for (int b = 0; b < c->B; b++) {
+            lo = std::min(lo, assign[b]);
+            hi = std::max(hi, assign[b]);
+        }
+        if (lo < -1 || hi >= c->T) return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
     }
     if (mem == PP_MEM_DEVICE_BORROW) {
         c->assign_ptr = assign;  // read in place until the next pp_set_schedule
@@ -1067,8 +1082,7 @@ int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream)
         c->borrowed = false;
     }
     c->pm_dirty = true;  // period masses are recomputed by the next evaluation launch (PDL-overlapped)
-    if (mem == PP_MEM_HOST) CUDA_TRY(cudaStreamSynchronize(st));
-    c->have_sched = true;
+    c->have_sched = true;  // host copies are stream-ordered (see the header), no synchronisation here
     return PP_OK;
 }
 

@@ -129,9 +129,7 @@ class Engine:
         if hasattr(assign, "data_ptr"):
             check(self.lib.pp_set_schedule(self._h, assign.data_ptr(), _lib.PP_MEM_DEVICE, None))
             return
-        a = _i32(assign, bm.n_blocks, "assignment")
-        if a.size and (a.min() < -1 or a.max() >= bm.n_periods):
-            raise InvalidArgs("schedule has period indices out of range")
+        a = _i32(assign, bm.n_blocks, "assignment")  # range validated by pp_set_schedule
         check(self.lib.pp_set_schedule(self._h, ptr(a), _lib.PP_MEM_HOST, None))
 
     def set_schedule_device(self, assign_tensor, stream=None, borrow: bool = False):
@@ -168,10 +166,12 @@ class Engine:
         return f
 
     def eval_candidates(self, cand, scenario=None, *, net=False, literal=False, use_sigma=True,
-                        trace=False, stats=False, scen=False, out: dict | None = None,
+                        trace=False, stats=False, scen=False, pairs=False, out: dict | None = None,
                         validate: bool = True) -> dict:
         """Host-buffer evaluation; returns numpy arrays (and `best` as a tuple or None).
-        `out` may supply preallocated (e.g. pinned) host arrays for any output."""
+        `out` may supply preallocated (e.g. pinned) host arrays for any output.
+        pairs=True returns the statistics of the feasible moves only, as
+        res["pairs"] = {"cand", "period", "exp", "cvar"} (unordered; capacity C*T)."""
         bm = self._need_bm()
         c = cand if (not validate and isinstance(cand, np.ndarray) and cand.dtype == np.int32) else _i32(cand)
         C, T, S = c.size, bm.n_periods, self.n_scenarios
@@ -191,26 +191,41 @@ class Engine:
             res["cvar"] = out["cvar"] if "cvar" in out else np.empty((C, T), np.float64)
         if scen:
             res["scen_delta"] = out["scen_delta"] if "scen_delta" in out else np.empty((C, S, T), np.float32)
+        pr = None
+        if pairs:
+            cap = max(C * T, 1)
+            pr = {"cand": out["pair_cand"] if "pair_cand" in out else np.empty(cap, np.int32),
+                  "period": out["pair_period"] if "pair_period" in out else np.empty(cap, np.int32),
+                  "exp": out["pair_exp"] if "pair_exp" in out else np.empty(cap, np.float64),
+                  "cvar": out["pair_cvar"] if "pair_cvar" in out else np.empty(cap, np.float64),
+                  "n": out["n_pairs"] if "n_pairs" in out else np.zeros(1, np.int32)}
         g = PPBest()
         out = PPCandOut(
             ptr(res["best_t"]), ptr(res["best_val"]), ptr(res["feasible"]),
             ptr(res.get("trace_val")), ptr(res.get("trace_feas")), ptr(res.get("exp_delta")),
-            ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g))
+            ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g),
+            *((ptr(pr["cand"]), ptr(pr["period"]), ptr(pr["exp"]), ptr(pr["cvar"]), ptr(pr["n"])) if pr else ()))
         sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
         check(self.lib.pp_eval_candidates(self._h, ptr(c), C, sc, self.flags(net, literal, use_sigma),
                                           ctypes.byref(out), _lib.PP_MEM_HOST, None))
         res["best"] = None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
+        if pr is not None:
+            n = int(pr["n"][0])
+            res["pairs"] = {k: pr[k][:n] for k in ("cand", "period", "exp", "cvar")}
         return res
 
     def eval_candidates_device(self, cand, out: dict, scenario=None, *, net=False, literal=False,
                                use_sigma=True, stream=None):
         """Device-buffer evaluation: `cand` an int32 CUDA tensor, `out` a dict of CUDA
         tensors (best_t, best_val, feasible, global [16-byte], optional trace_val,
-        trace_feas, exp_delta, cvar, scen_delta).  Enqueues on `stream`."""
+        trace_feas, exp_delta, cvar, scen_delta, or the sparse pair_cand / pair_period /
+        pair_exp / pair_cvar [C*T] with n_pairs [1]).  Enqueues on `stream`."""
         o = PPCandOut(
             ptr(out["best_t"]), ptr(out["best_val"]), ptr(out["feasible"]),
             ptr(out.get("trace_val")), ptr(out.get("trace_feas")), ptr(out.get("exp_delta")),
-            ptr(out.get("cvar")), ptr(out.get("scen_delta")), ptr(out["global"]))
+            ptr(out.get("cvar")), ptr(out.get("scen_delta")), ptr(out["global"]),
+            ptr(out.get("pair_cand")), ptr(out.get("pair_period")), ptr(out.get("pair_exp")),
+            ptr(out.get("pair_cvar")), ptr(out.get("n_pairs")))
         sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
         check(self.lib.pp_eval_candidates(self._h, ptr(cand), int(cand.numel()), sc,
                                           self.flags(net, literal, use_sigma), ctypes.byref(o),

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = _lib.load()
-    assert lib.pp_abi_version() == 1
+    assert lib.pp_abi_version() == _lib.ABI_VERSION
     assert isinstance(lib.pp_last_error(), bytes)
 
 
@@ -63,3 +63,19 @@ def test_no_gpu_context_creation_fails_loudly():
 
     with pytest.raises(PitplanError):
         Engine(0)
+
+
+def _struct_fields(name):
+    src = open(HDR).read()
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), src, flags=re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    return re.findall(r"\*?\s*(\w+);", body)
+
+
+def test_header_abi_version_and_struct_layouts_match_ctypes():
+    src = open(HDR).read()
+    assert int(re.search(r"#define PP_ABI_VERSION (\d+)", src).group(1)) == _lib.ABI_VERSION
+    for cname, py in (("pp_cand_out", _lib.PPCandOut), ("pp_move_out", _lib.PPMoveOut), ("pp_best", _lib.PPBest)):
+        want = [f.rstrip("_") for f in _struct_fields(cname)]
+        got = [f[0].rstrip("_") for f in py._fields_]
+        assert want == got, (cname, want, got)

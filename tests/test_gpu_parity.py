@@ -352,3 +352,66 @@ def test_period_mass_paths(oracle_lib, B, T):
         _, pm = eng.get_schedule()
         assert same(pm, o.period_mass(pop[k])), k
     eng.close()
+
+
+def _pairs_match_dense(pr, ref):
+    """The sparse pair list equals the dense reference restricted to the feasible moves."""
+    ci, ti = np.nonzero(ref["trace_feas"] == 1)
+    order = np.lexsort((pr["period"], pr["cand"]))
+    assert np.array_equal(pr["cand"][order], ci) and np.array_equal(pr["period"][order], ti)
+    assert same(pr["exp"][order], ref["exp_delta"][ci, ti])
+    assert same(pr["cvar"][order], ref["cvar"][ci, ti])
+
+
+@pytest.mark.parametrize("T,S", [(7, 9), (15, 20), (40, 30), (9, 200)])
+def test_sparse_pairs_against_oracle(oracle_lib, T, S):
+    """pairs=True: the warp kernel (T <= 32, S <= 128) and the general kernel (T > 32 or
+    S > 128) append every feasible move's expected delta and CVaR exactly once."""
+    bm, vmax, sigma = _rand_instance(23 + T + S, n=(8, 7, 5), T=T, S=S)
+    from paper_2511_18296_b200 import synth
+
+    assign = synth.full_greedy(bm)
+    rng = np.random.default_rng(T + S)
+    assign[rng.random(assign.size) < 0.1] = -1
+    cand = rng.integers(0, bm.n_blocks, size=301).astype(np.int32)
+    eng = Engine.from_tables(bm, ScenarioTables(vmax, sigma), assign)
+    o = oracle_lib.Oracle(bm, vmax, sigma)
+    for net in (False, True):
+        got = eng.eval_candidates(cand, None, net=net, pairs=True)
+        ref = o.eval_candidates(assign, cand, None, net=net, trace=True, stats=True)
+        _same_res(got, ref, ("best_t", "best_val", "feasible"))
+        assert got["pairs"]["cand"].size == int(ref["trace_feas"].sum()) > 0
+        _pairs_match_dense(got["pairs"], ref)
+    eng.close()
+
+
+def test_sparse_pairs_c2_and_device_mode(oracle_lib):
+    import torch
+
+    c = config("C2")
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], c["sigma"]), c["assign"])
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    ref = o.eval_candidates(c["assign"], c["cand"], None, net=True, trace=True, stats=True, nthreads=8)
+    got = eng.eval_candidates(c["cand"], None, net=True, pairs=True)
+    _pairs_match_dense(got["pairs"], ref)
+    C, T = c["C"], c["T"]
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream(dev)
+    out = {"best_t": torch.empty(C, dtype=torch.int32, device=dev),
+           "best_val": torch.empty(C, dtype=torch.float64, device=dev),
+           "feasible": torch.empty(C, dtype=torch.uint8, device=dev),
+           "global": torch.empty(2, dtype=torch.float64, device=dev),
+           "pair_cand": torch.empty(C * T, dtype=torch.int32, device=dev),
+           "pair_period": torch.empty(C * T, dtype=torch.int32, device=dev),
+           "pair_exp": torch.empty(C * T, dtype=torch.float64, device=dev),
+           "pair_cvar": torch.empty(C * T, dtype=torch.float64, device=dev),
+           "n_pairs": torch.zeros(1, dtype=torch.int32, device=dev)}
+    with torch.cuda.stream(st):
+        cand_d = torch.from_numpy(c["cand"]).to(dev)
+        eng.eval_candidates_device(cand_d, out, None, net=True, stream=st.cuda_stream)
+    st.synchronize()
+    n = int(out["n_pairs"].item())
+    pr = {"cand": out["pair_cand"][:n].cpu().numpy(), "period": out["pair_period"][:n].cpu().numpy(),
+          "exp": out["pair_exp"][:n].cpu().numpy(), "cvar": out["pair_cvar"][:n].cpu().numpy()}
+    _pairs_match_dense(pr, ref)
+    eng.close()

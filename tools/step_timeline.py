@@ -34,6 +34,9 @@ cl = pm[0, :8, 0].min() > 0
 if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
     t0 = min(pm[0, :8, 0].min(), ev[:, 0].min())
     f = lambda x: (x - t0) / 1000
+    for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves"]):
+        v = pm[1, 16 + 8 * k:24 + 8 * k, 0]
+        print(f"  pm {nm:8s} {f(v.min()):.2f}..{f(v.max()):.2f} us")
     print(f"PM cluster (8 CTAs): start {f(pm[0,:8,0].min()):.2f}..{f(pm[0,:8,0].max()):.2f}  scattered {f(pm[0,:8,1].min()):.2f}..{f(pm[0,:8,1].max()):.2f}  trees done {f(pm[1,:8,1].min()):.2f}..{f(pm[1,:8,1].max()):.2f} us")
 else:
     nch = (c["bm"].n_blocks + 511) // 512
@@ -42,6 +45,6 @@ else:
     f = lambda x: (x - t0) / 1000
     print(f"P1 ({nch} CTAs): start {f(p1[:,0].min()):.2f}..{f(p1[:,0].max()):.2f}  end {f(p1[:,1].min()):.2f}..{f(p1[:,1].max()):.2f} us")
     print(f"P2 ({T} CTAs): after-wait {f(p2[:,0].min()):.2f}..{f(p2[:,0].max()):.2f}  end {f(p2[:,1].min()):.2f}..{f(p2[:,1].max()):.2f} us")
-names = ["start", "ids", "rows", "window", "pm-wait", "capacity", "stats", "end"]
-for k in range(8):
+names = ["start", "loads", "stats", "pm-wait", "moves", "outputs", "end"]
+for k in range(len(names)):
     print(f"eval {names[k]:9s} min {f(ev[:,k].min()):6.2f}  median {f(np.median(ev[:,k])):6.2f}  max {f(ev[:,k].max()):6.2f} us")
