@@ -87,14 +87,20 @@ constexpr int NBR_W = 32;  // neighbour slots per block (padded table, one 128-b
 constexpr int NBR_SUCC = 1 << 30;  // successor tag in the neighbour table; -1 = padding
 
 struct WarpLayout {  // per-warp slice of dynamic shared memory (byte offsets)
-    int vrow, ex, cv, total;
+    int vrow, cost, val, ex, cv, total;
 };
+// dynamic shared memory: [sigma S x T (statistics)] [NW warp slices]
+static __host__ __device__ inline int sig_bytes(int S, int T, bool stats) { return stats ? ((8 * S * T + 15) & ~15) : 0; }
 static __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool stats, bool need_vrow) {
+static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool stats, bool need_vrow, bool net) {
     WarpLayout L;
     int o = 0;
     L.vrow = o;
     o += need_vrow ? align16(8 * CPW * Sp) : 0;
+    L.cost = o;
+    o += net ? align16(8 * CPW * T) : 0;
+    L.val = o;  // per-(candidate, lane) kernel value
+    o += 8 * CPW * 32;
     L.ex = o;
     o += stats ? align16(8 * CPW * T) : 0;
     L.cv = o;
@@ -119,6 +125,9 @@ template <int KC, bool SCEN>
 __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p) {
     extern __shared__ __align__(16) unsigned char wv_dyn[];
     __shared__ Best s_red[EV_THREADS / 32];
+    __shared__ int s_cab[EV_THREADS / 32 * CPW], s_cb[EV_THREADS / 32 * CPW], s_wcnt[EV_THREADS / 32];
+    __shared__ double s_csp[EV_THREADS / 32 * CPW], s_cm[EV_THREADS / 32 * CPW], s_cu[EV_THREADS / 32 * CPW];
+    __shared__ int s_pair[EV_THREADS / 32 * CPW * 32];
     constexpr int NW = EV_THREADS / 32;
     constexpr unsigned FULL = 0xffffffffu;
     const int T = p.T, S = p.S, Sp = p.Sp;
@@ -130,9 +139,13 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     const bool need_vrow = stats || (!literal && p.scen >= 0);
     const bool want_unit = !literal && p.scen < 0;
     const bool want_trace = p.trace_val || p.trace_feas;
-    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow);
-    unsigned char *wbase = wv_dyn + (size_t)warp * L.total;
+    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow, net);
+    const int sigb = sig_bytes(S, T, stats);
+    double *s_sig = reinterpret_cast<double *>(wv_dyn);
+    unsigned char *wslices = wv_dyn + sigb;
+    unsigned char *wbase = wslices + (size_t)warp * L.total;
     double *w_vrow = reinterpret_cast<double *>(wbase + L.vrow);
+    double *w_cost = reinterpret_cast<double *>(wbase + L.cost);
     double *w_ex = reinterpret_cast<double *>(wbase + L.ex);
     double *w_cv = reinterpret_cast<double *>(wbase + L.cv);
     const int cw = (blockIdx.x * NW + warp) * CPW;
@@ -144,28 +157,32 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
         bl = __ldg(p.cand + cw + lane);
         if (bl < 0 || bl >= p.B) bl = -1;
     }
-    double cap_t = 0.0, disc_t = 0.0, srow_t = 0.0;
-    if (lane < T) {
-        cap_t = __ldg(p.cap + lane);
-        disc_t = __ldg(p.disc + lane);
-        srow_t = __ldg(p.sig_row + lane);
-    }
     int b[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
-    double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
-    int ab_l = -1;
-    if (bl >= 0) {
-        mass_l = __ldg(&p.rows[bl].mass);
-        spat_l = __ldg(&p.rows[bl].spatial);
-        ab_l = __ldg(p.assign + bl);
-        if (want_unit) unit_l = __ldg(p.unit_mean + bl);
+    if (stats)  // sigma [S][T] for the pair statistics, staged once per CTA
+        for (int e = threadIdx.x; e < S * T; e += EV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+    // per-candidate scalars to shared memory (read by the pair pool and the moves)
+    if (lane < CPW) {
+        double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
+        int ab_l = -1;
+        if (bl >= 0) {
+            mass_l = __ldg(&p.rows[bl].mass);
+            spat_l = __ldg(&p.rows[bl].spatial);
+            ab_l = __ldg(p.assign + bl);
+            if (want_unit) unit_l = __ldg(p.unit_mean + bl);
+        }
+        const int i = warp * CPW + lane;
+        s_cm[i] = mass_l;
+        s_csp[i] = spat_l;
+        s_cu[i] = unit_l;
+        s_cab[i] = ab_l;
+        s_cb[i] = bl;
     }
-    double cost_r[CPW];
     int nb[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
-        cost_r[j] = (net && lane < T && b[j] >= 0) ? __ldg(p.cost + (size_t)b[j] * T + lane) : 0.0;
+        if (net && lane < T && b[j] >= 0) cp_async8(w_cost + j * T + lane, p.cost + (size_t)b[j] * T + lane);
         nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
     }
     if (need_vrow) {
@@ -180,168 +197,134 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     int tn[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) tn[j] = nb[j] >= 0 ? p.assign[nb[j] & (NBR_SUCC - 1)] : 0;
-    int lo[CPW], hi[CPW];
+    unsigned win[CPW];  // precedence window of candidate j as a period mask (lane t = period t)
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
         const bool pred = nb[j] >= 0 && !(nb[j] & NBR_SUCC), succ = nb[j] >= 0 && (nb[j] & NBR_SUCC);
         const int lc = pred ? (tn[j] < 0 ? INT_MAX : tn[j]) : 0;
         const int hc = (succ && tn[j] >= 0) ? tn[j] : INT_MAX;
-        lo[j] = (int)__reduce_max_sync(FULL, (unsigned)lc);
-        hi[j] = (int)__reduce_min_sync(FULL, (unsigned)hc);
-        if (b[j] < 0) lo[j] = INT_MAX;
+        const int lo = (int)__reduce_max_sync(FULL, (unsigned)lc);
+        const int hi = (int)__reduce_min_sync(FULL, (unsigned)hc);
+        win[j] = __ballot_sync(FULL, b[j] >= 0 && lane < T && lane >= lo && lane <= hi);
     }
-    if (need_vrow) cp_async_wait_all();
+    if (need_vrow || net || stats) cp_async_wait_all();
     __syncwarp();
     EV_PROBE(1);
 
     // ---- statistics of the precedence-feasible (candidate, period) pairs, before the
     //      period masses are known (overlaps the period-mass kernel); capacity only
     //      removes pairs, so the outputs below select from these ----
-    unsigned okm[CPW];
-#pragma unroll
-    for (int j = 0; j < CPW; j++) okm[j] = __ballot_sync(FULL, lane < T && lane >= lo[j] && lane <= hi[j]);
     if constexpr (STATS_T) {
         if (stats) {
+            // CTA-wide pool of the pairs, one thread per pair: a warp holds ~9 pairs at C2, a CTA
+            // ~70, so pooling keeps ~3x more of each warp's lanes busy than per-warp lists
             int cum[CPW + 1];
             cum[0] = 0;
 #pragma unroll
-            for (int j = 0; j < CPW; j++) cum[j + 1] = cum[j] + __popc(okm[j]);
-            const int npairs = cum[CPW];
-            if constexpr (KC < 0) {  // (8-lane sub-group variant, disabled)
-                // 8 lanes per pair; lane j owns numpy's accumulator j (scenarios s = j mod 8),
-                // the butterfly xor 1,2,4 is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the <8-element
-                // tail is added in order; per-lane two smallest merged by butterfly (CVaR, k <= 2)
-                const int sub = lane & 7;
-                const int main_ = S & ~7, nrem = S - main_;
-                for (int k0 = 0; k0 < npairs; k0 += 4) {
-                    const int k = k0 + (lane >> 3);
-                    const bool act = k < npairs;
-                    int j = 0, t = 0;
+            for (int j = 0; j < CPW; j++) cum[j + 1] = cum[j] + __popc(win[j]);
+            const int np = cum[CPW];
+            if (lane == 0) s_wcnt[warp] = np;
+            __syncthreads();
+            int base = 0, total = 0;
 #pragma unroll
-                    for (int jj = 0; jj < CPW; jj++)
-                        if (k >= cum[jj] && k < cum[jj + 1]) {
-                            j = jj;
-                            t = nth_bit(okm[jj], k - cum[jj]);
-                        }
-                    const int ab = __shfl_sync(FULL, ab_l, j);
-                    const double sp = __shfl_sync(FULL, spat_l, j);
-                    const int bj = __shfl_sync(FULL, bl, j);
-                    const bool mined = ab >= 0;
-                    const int abc = mined ? ab : 0;
-                    const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
-                    const double dc_t = net ? f64_mul(d_t, __ldg(p.cost + (size_t)max(bj, 0) * T + t)) : 0.0;
-                    const double dc_ab = net ? f64_mul(d_ab, __ldg(p.cost + (size_t)max(bj, 0) * T + abc)) : 0.0;
-                    const double *rowb = w_vrow + (size_t)j * Sp;
-                    float *sd = SCEN ? p.scen_delta + (size_t)(cw + j) * S * T + t : nullptr;
-                    double acc = -0.0, a0 = kInf, a1 = kInf, remv = 0.0;
-                    if (act) {
-                        for (int s_ = sub; s_ < S; s_ += 8) {
-                            const double x = rowb[s_];
-                            const double vn =
-                                f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma + s_ * T + t)), sp), dc_t);
-                            const double vo =
-                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma + s_ * T + abc)), sp), dc_ab)
-                                      : 0.0;
-                            const double v = f64_sub(vn, vo);  // vn - 0.0 == vn exactly
-                            if (s_ < main_) acc = f64_add(acc, v);
-                            else remv = v;
-                            if (v < a1) {
-                                if (v < a0) {
-                                    a1 = a0;
-                                    a0 = v;
-                                } else {
-                                    a1 = v;
-                                }
-                            }
-                            if constexpr (SCEN) sd[(size_t)s_ * T] = (float)v;
-                        }
-                    }
-                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
-                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
-                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
-                    double res = main_ ? acc : -0.0;
-                    for (int q = 0; q < nrem; q++) res = f64_add(res, __shfl_sync(FULL, remv, (lane & ~7) + q));
-#pragma unroll
-                    for (int o = 1; o < 8; o <<= 1) {
-                        const double b0 = __shfl_xor_sync(FULL, a0, o);
-                        const double b1 = __shfl_xor_sync(FULL, a1, o);
-                        const double lo_ = (b0 < a0) ? b0 : a0, hi_ = (b0 < a0) ? a0 : b0;
-                        const double m1 = (b1 < a1) ? b1 : a1;
-                        a0 = lo_;
-                        a1 = (m1 < hi_) ? m1 : hi_;
-                    }
-                    if (act && sub == 0) {
-                        w_ex[j * T + t] = f64_div(f64_add(0.0, res), (double)S);
-                        double c = f64_add(-0.0, a0);
-                        if (p.cvar_k > 1) c = f64_add(c, a1);
-                        w_cv[j * T + t] = f64_mul(f64_add(0.0, c), p.cvar_k > 1 ? 0.5 : 1.0);
-                    }
-                }
-            } else {
-                for (int k0 = 0; k0 < npairs; k0 += 32) {  // one lane per pair
-                    const int k = k0 + lane;
-                    int j = 0, t = 0;
-#pragma unroll
-                    for (int jj = 0; jj < CPW; jj++)
-                        if (k >= cum[jj] && k < cum[jj + 1]) {
-                            j = jj;
-                            t = nth_bit(okm[jj], k - cum[jj]);
-                        }
-                    const int ab = __shfl_sync(FULL, ab_l, j);
-                    const double sp = __shfl_sync(FULL, spat_l, j);
-                    const int bj = __shfl_sync(FULL, bl, j);
-                    if (k < npairs) {
-                        const int abc = ab >= 0 ? ab : 0;
-                        const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
-                        const double dc_t = net ? f64_mul(d_t, __ldg(p.cost + (size_t)bj * T + t)) : 0.0;
-                        const double dc_ab = net ? f64_mul(d_ab, __ldg(p.cost + (size_t)bj * T + abc)) : 0.0;
-                        float *sd = SCEN ? p.scen_delta + (size_t)(cw + j) * S * T + t : nullptr;
-                        pair_stats<KC, SCEN>(p, S, T, p.sigma, w_vrow + (size_t)j * Sp, t, abc, d_t, dc_t, d_ab, dc_ab, sp,
-                                             ab >= 0, w_ex + j * T + t, w_cv + j * T + t, sd);
-                    }
-                }
+            for (int w = 0; w < NW; w++) {
+                const int x = s_wcnt[w];
+                base += w < warp ? x : 0;
+                total += x;
             }
-            __syncwarp();
+            for (int k = lane; k < np; k += 32) {
+                int j = 0, t = 0;
+#pragma unroll
+                for (int jj = 0; jj < CPW; jj++)
+                    if (k >= cum[jj] && k < cum[jj + 1]) {
+                        j = jj;
+                        t = nth_bit(win[jj], k - cum[jj]);
+                    }
+                s_pair[base + k] = ((warp * CPW + j) << 8) | t;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < total; k += EV_THREADS) {
+                const int e = s_pair[k], i = e >> 8, t = e & 0xff;
+                const int wq = i / CPW, jq = i - wq * CPW;
+                unsigned char *wb = wslices + (size_t)wq * L.total;
+                const int ab = s_cab[i], bj = s_cb[i];
+                const double sp = s_csp[i];
+                const int abc = ab >= 0 ? ab : 0;
+                const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
+                const double *wc = reinterpret_cast<const double *>(wb + L.cost) + jq * T;
+                const double dc_t = net ? f64_mul(d_t, wc[t]) : 0.0;
+                const double dc_ab = net ? f64_mul(d_ab, wc[abc]) : 0.0;
+                float *sd = SCEN ? p.scen_delta + (size_t)(blockIdx.x * NW * CPW + i) * S * T + t : nullptr;
+                pair_stats<KC, SCEN>(p, S, T, s_sig, reinterpret_cast<double *>(wb + L.vrow) + (size_t)jq * Sp, t, abc,
+                                     d_t, dc_t, d_ab, dc_ab, sp, ab >= 0,
+                                     reinterpret_cast<double *>(wb + L.ex) + jq * T + t,
+                                     reinterpret_cast<double *>(wb + L.cv) + jq * T + t, sd);
+            }
+            __syncthreads();
         }
+    }
+
+
+    // ---- moves, pm-independent half: value of every window period (evaluate.py:379-384) and
+    //      its rank in the reference's selection order (value desc, then period asc: the
+    //      strict '>' scan of 387-388 keeps the first maximum; -inf / NaN never selected) ----
+    double cap_t = 0.0, disc_t = 0.0, srow_t = 0.0;
+    if (lane < T) {
+        cap_t = __ldg(p.cap + lane);
+        disc_t = __ldg(p.disc + lane);
+        srow_t = __ldg(p.sig_row + lane);
+    }
+    double *w_val = reinterpret_cast<double *>(wbase + L.val);
+    unsigned key[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; j++) {
+        const int ci = warp * CPW + j;
+        const bool in = (win[j] >> lane) & 1u;
+        double v = -kInf;
+        if (in) {
+            double unit;
+            if (literal) unit = f64_mul(s_cm[ci], 100.0);
+            else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
+            else unit = s_cu[ci];
+            v = f64_mul(f64_mul(f64_mul(unit, disc_t), srow_t), s_csp[ci]);
+            if (net) v = f64_sub(v, f64_mul(disc_t, w_cost[j * T + lane]));
+        }
+        w_val[j * 32 + lane] = v;
+        const bool valid = in && v > -kInf;
+        const unsigned vm = __ballot_sync(FULL, valid);
+        __syncwarp();
+        int rank = 0;
+        for (unsigned mm = vm; mm; mm &= mm - 1) {
+            const int u = __ffs(mm) - 1;
+            const double vu = w_val[j * 32 + u];
+            rank += (vu > v || (vu == v && u < lane)) ? 1 : 0;
+        }
+        key[j] = valid ? (unsigned)((rank << 5) | lane) : 0xffffffffu;
     }
     EV_PROBE(2);
 
-    // ---- moves (needs the period masses) ----
+    // ---- moves, pm half: capacity (evaluate.py:373-378) and the selection ----
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const double pm_t = lane < T ? __ldcg(p.pm + lane) : 0.0;
     EV_PROBE(3);
     Best wbest{-kInf, INT_MAX, INT_MAX};
+    unsigned okm[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
-        const double mass = __shfl_sync(FULL, mass_l, j), spat = __shfl_sync(FULL, spat_l, j);
-        const int ab = __shfl_sync(FULL, ab_l, j);
-        double unit;
-        if (literal) unit = f64_mul(mass, 100.0);
-        else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
-        else unit = __shfl_sync(FULL, unit_l, j);
+        const int ci = warp * CPW + j;
+        const double mass = s_cm[ci];
+        const int ab = s_cab[ci];
+        b[j] = s_cb[ci];
         bool ok = false;
-        double v = -kInf;
-        if (lane < T && lane >= lo[j] && lane <= hi[j]) {
+        if ((win[j] >> lane) & 1u) {
             double load = f64_add(pm_t, mass);
             if (ab == lane) load = f64_sub(load, mass);
             ok = !(load > cap_t);
-            if (ok) {
-                v = f64_mul(f64_mul(f64_mul(unit, disc_t), srow_t), spat);
-                if (net) v = f64_sub(v, f64_mul(disc_t, cost_r[j]));
-            }
         }
         okm[j] = __ballot_sync(FULL, ok);
-        // lowest-t argmax: the reference's strict '>' scan in period order (evaluate.py:387-388)
-        double bv = -kInf;
-        int bt = INT_MAX;
-        for (unsigned mm = okm[j]; mm; mm &= mm - 1) {
-            const int t = __ffs(mm) - 1;
-            const double vt = __shfl_sync(FULL, v, t);
-            if (vt > bv) {
-                bv = vt;
-                bt = t;
-            }
-        }
+        const unsigned kmin = __reduce_min_sync(FULL, ok ? key[j] : 0xffffffffu);
+        const int bt = kmin == 0xffffffffu ? INT_MAX : (int)(kmin & 31u);
+        const double bv = bt != INT_MAX ? w_val[j * 32 + bt] : -kInf;
         const int g = cw + j;
         if (g < p.C) {
             if (lane == 0 && b[j] >= 0) {
@@ -350,7 +333,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                 p.feas[g] = bt != INT_MAX ? 1 : 0;
             }
             if (want_trace && lane < T) {
-                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = ok ? v : -kInf;
+                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = ok ? w_val[j * 32 + lane] : -kInf;
                 if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = ok ? 1 : 0;
             }
         }
@@ -377,36 +360,41 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                             p.scen_delta[((size_t)g * S + s) * T + lane] = -__int_as_float(0x7f800000);
                 }
             }
-            if (p.n_pairs) {  // sparse: the warp's feasible moves, one atomic per warp
-                int cum[CPW + 1];
-                cum[0] = 0;
-#pragma unroll
-                for (int j = 0; j < CPW; j++) cum[j + 1] = cum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
-                const int np = cum[CPW];
-                int base = 0;
-                if (lane == 0 && np) base = atomicAdd(p.n_pairs, np);
-                base = __shfl_sync(FULL, base, 0);
-                for (int k = lane; k < np; k += 32) {
-                    int j = 0, t = 0;
-#pragma unroll
-                    for (int jj = 0; jj < CPW; jj++)
-                        if (k >= cum[jj] && k < cum[jj + 1]) {
-                            j = jj;
-                            t = nth_bit(okm[jj], k - cum[jj]);
-                        }
-                    p.pair_cand[base + k] = cw + j;
-                    p.pair_period[base + k] = t;
-                    p.pair_exp[base + k] = w_ex[j * T + t];
-                    p.pair_cvar[base + k] = w_cv[j * T + t];
-                }
-            }
         }
     }
     EV_PROBE(5);
 
+    // ---- sparse pairs: the warp's slot range is reserved before the CTA barrier below, so
+    //      the atomic's round trip overlaps it; the entries are written after it ----
+    int pcum[CPW + 1], pbase = 0;
+    if constexpr (STATS_T) {
+        pcum[0] = 0;
+#pragma unroll
+        for (int j = 0; j < CPW; j++) pcum[j + 1] = pcum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
+        if (stats && p.n_pairs && lane == 0 && pcum[CPW]) pbase = atomicAdd(p.n_pairs, pcum[CPW]);
+    }
     // ---- argmax: warp -> CTA -> grid ----
     if (lane == 0) s_red[warp] = wbest;
     __syncthreads();
+    if constexpr (STATS_T) {
+        if (stats && p.n_pairs) {
+            const int np = pcum[CPW];
+            pbase = __shfl_sync(FULL, pbase, 0);
+            for (int k = lane; k < np; k += 32) {
+                int j = 0, t = 0;
+#pragma unroll
+                for (int jj = 0; jj < CPW; jj++)
+                    if (k >= pcum[jj] && k < pcum[jj + 1]) {
+                        j = jj;
+                        t = nth_bit(okm[jj], k - pcum[jj]);
+                    }
+                p.pair_cand[pbase + k] = cw + j;
+                p.pair_period[pbase + k] = t;
+                p.pair_exp[pbase + k] = w_ex[j * T + t];
+                p.pair_cvar[pbase + k] = w_cv[j * T + t];
+            }
+        }
+    }
     Best mine = (warp == 0 && lane < NW) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
     grid_argmax_warp0(mine, s_red, p.partial, p.counter, p.global);
     EV_PROBE(6);
@@ -452,8 +440,12 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     pp_cand_out o = *out;
     const int32_t *dcand = cand;
     if (mem == PP_MEM_HOST) {
-        for (int i = 0; i < C; i++)
-            if (cand[i] < 0 || cand[i] >= c->B) return fail(PP_ERR_INVALID_ARGS, "candidate block %d out of range", cand[i]);
+        int32_t lo = 0, hi = 0;  // branch-free min/max (vectorises)
+        for (int i = 0; i < C; i++) {
+            lo = std::min(lo, cand[i]);
+            hi = std::max(hi, cand[i]);
+        }
+        if (lo < 0 || hi >= c->B) return fail(PP_ERR_INVALID_ARGS, "candidate block out of range [0, %d)", c->B);
         const size_t Cs = (size_t)std::max(C, 1), CT = Cs * T;
         TRY(c->h_cand.ensure(sizeof(int32_t) * Cs));
         TRY(c->h_o1.ensure(sizeof(int32_t) * Cs));
@@ -522,7 +514,6 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     ep.pair_exp = o.pair_exp;
     ep.pair_cvar = o.pair_cvar;
     ep.n_pairs = o.n_pairs;
-    if (pairs) CUDA_TRY(cudaMemsetAsync(o.n_pairs, 0, sizeof(int32_t), st));
     ep.partial = c->partial.as<pp_best>();
     ep.counter = c->counter.as<unsigned int>();
     ep.global = o.global;
@@ -530,13 +521,13 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     // fast path: one warp per CPW candidates (k_eval_warp)
     if (T <= 32 && (!stats || S <= 128) && c->nbr.ptr) {
         const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
-        const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow);
-        const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32);
+        const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
+        const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32) + sig_bytes(S, T, stats);
         const int per_cta = CPW * (EV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));
         bool pdl;
-        TRY(refresh_pm(c, st, &pdl));
+        TRY(refresh_pm(c, st, &pdl, o.n_pairs));  // zeroes n_pairs ahead of the evaluation
         const bool scen = o.scen_delta != nullptr;
 #define PP_WARP(KC, SC)                                                     \
     {                                                                       \
@@ -552,7 +543,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     }
     {
         bool pdl;
-        TRY(refresh_pm(c, st, &pdl));
+        TRY(refresh_pm(c, st, &pdl, o.n_pairs));  // zeroes n_pairs ahead of the evaluation
         TRY(launch_general_candidates(PER, kc, o.scen_delta != nullptr, C, G, S, c->Sp, T, stats, st, pdl, c->device,
                                       ep));
     }
@@ -572,18 +563,32 @@ copy_out:
             if (out->scen_delta)
                 CUDA_TRY(cudaMemcpyAsync(out->scen_delta, o.scen_delta, sizeof(float) * CT * S, cudaMemcpyDeviceToHost, st));
         }
-        if (pairs) {  // count first, then exactly the written entries
+        // sparse pairs: the count and a speculative prefix (sized from the previous call) in
+        // the same round trip; the rest, if any, after the count is known
+        size_t spec = 0;
+        auto copy_pairs = [&](size_t lo, size_t hi) -> int {
+            if (hi <= lo) return PP_OK;
+            const size_t n = hi - lo;
+            CUDA_TRY(cudaMemcpyAsync(out->pair_cand + lo, o.pair_cand + lo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(out->pair_period + lo, o.pair_period + lo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(out->pair_exp + lo, o.pair_exp + lo, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(out->pair_cvar + lo, o.pair_cvar + lo, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            return PP_OK;
+        };
+        if (pairs) {
             CUDA_TRY(cudaMemcpyAsync(out->n_pairs, o.n_pairs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            const size_t n = (size_t)std::max(0, *out->n_pairs);
-            if (n) {
-                CUDA_TRY(cudaMemcpyAsync(out->pair_cand, o.pair_cand, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-                CUDA_TRY(cudaMemcpyAsync(out->pair_period, o.pair_period, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-                CUDA_TRY(cudaMemcpyAsync(out->pair_exp, o.pair_exp, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-                CUDA_TRY(cudaMemcpyAsync(out->pair_cvar, o.pair_cvar, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-            }
+            spec = std::min((size_t)C * T, c->last_pairs + c->last_pairs / 4 + 1024);
+            TRY(copy_pairs(0, spec));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
+        if (pairs) {
+            const size_t n = (size_t)std::max(0, *out->n_pairs);
+            c->last_pairs = n;
+            if (n > spec) {
+                TRY(copy_pairs(spec, n));
+                CUDA_TRY(cudaStreamSynchronize(st));
+            }
+        }
     }
     return PP_OK;
 }

@@ -455,6 +455,7 @@ struct pp_ctx {
     // scratch
     DevBuf cnt, compact, pm_batch, predcnt, partial, counter, pm_flags;
     size_t pm_flags_n = 0;
+    size_t last_pairs = 0;  // sparse pair count of the previous host-mode evaluation
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
     std::vector<DevBuf *> all() {
@@ -517,14 +518,17 @@ inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream
 int ensure_grid_scratch(pp_ctx *c, int grid);
 int check_ready(pp_ctx *c, uint32_t flags, int scenario);
 int pick_kc(int k);
-int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st);
-int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched);
+// zero (optional): a device word the period-mass launch sets to 0 before anything that follows it
+int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st,
+                    int32_t *zero = nullptr);
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, int32_t *zero = nullptr);
 int launch_general_candidates(int PER, int kc, bool scen, int C, int G, int S, int Sp, int T, bool stats,
                               cudaStream_t st, bool pdl, int device, const EvalParams &ep);
 
 template <typename K>
 inline int set_smem_attr(K kern, size_t bytes) {
-    if (bytes > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // the 48 KB default covers static + dynamic; opt in with room for the kernels' static arrays
+    if (bytes > 32 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     return PP_OK;
 }
 

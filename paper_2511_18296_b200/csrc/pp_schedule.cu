@@ -600,9 +600,10 @@ __device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &le
 template <int K>
 __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
-                 double *__restrict__ compact, double *__restrict__ pm_out) {
+                 double *__restrict__ compact, double *__restrict__ pm_out, int32_t *__restrict__ zero) {
     __shared__ PmcSmem h;
     PMCP(0, 0);
+    if (zero && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *zero = 0;  // complete before dependents' wait
     asm volatile("griddepcontrol.launch_dependents;");
     constexpr unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -769,14 +770,15 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
 }
 
 template <int K>
-static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st) {
+static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
+                             int32_t *zero) {
     k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, 0, st>>>(d_assign, c->mass.as<double>(), c->B, c->T,
-                                                              c->compact.as<double>(), d_pm);
+                                                              c->compact.as<double>(), d_pm, zero);
     CUDA_TRY(cudaGetLastError());
     return PP_OK;
 }
 
-int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st) {
+int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st, int32_t *zero) {
     const int B = c->B, T = c->T;
     const int nchunk = (B + PM_CH - 1) / PM_CH;
     // compacted masses: B doubles per (period, schedule); batches bounded to ~512 MiB
@@ -796,13 +798,15 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
             const int np = std::min(pchunk, P - p0);
             const int32_t *a = d_assign + (size_t)p0 * B;
             double *o = d_pm + (size_t)p0 * T;
-            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st));
-            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st));
-            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st));
-            else TRY(launch_pm_cluster<8>(c, a, np, o, st));
+            int32_t *z = p0 == 0 ? zero : nullptr;
+            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st, z));
+            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st, z));
+            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st, z));
+            else TRY(launch_pm_cluster<8>(c, a, np, o, st, z));
         }
         return PP_OK;
     }
+    if (zero) CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(int32_t), st));
     const size_t smem = std::max(sizeof(PmTreeSmem), sizeof(int) * ((PM_THREADS / 32) * PM_MAXT + PM_MAXT));
     static bool attr_done = false;
     if (!attr_done) {
@@ -822,10 +826,13 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
 }
 
 // recompute the current schedule's period masses if the schedule changed
-int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched) {
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, int32_t *zero) {
     *launched = false;
-    if (!c->pm_dirty) return PP_OK;
-    TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st));
+    if (!c->pm_dirty) {
+        if (zero) CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(int32_t), st));
+        return PP_OK;
+    }
+    TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st, zero));
     c->pm_dirty = false;
     *launched = true;
     return PP_OK;
