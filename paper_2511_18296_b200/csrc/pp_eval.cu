@@ -109,6 +109,33 @@ static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool sta
     return L;
 }
 
+
+// 128-bit compare-and-swap of a pp_best record {value, block, period} in the selection order of
+// evaluate.py:404-409; the initial record {-inf, -1, -1} loses to every selectable move.
+__device__ __forceinline__ void best_cas(pp_best *g, const Best &x) {
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(g);
+    unsigned long long lo = __ldcg(a), hi = __ldcg(a + 1);
+    const unsigned long long nlo = (unsigned long long)__double_as_longlong(x.v);
+    const unsigned long long nhi = (unsigned long long)(unsigned)x.b | ((unsigned long long)(unsigned)x.t << 32);
+    for (;;) {
+        const Best cur{__longlong_as_double((long long)lo), (int)(unsigned)(hi & 0xffffffffull), (int)(unsigned)(hi >> 32)};
+        if (cur.b >= 0 && !better(x, cur)) return;
+        unsigned long long olo, ohi;
+        asm volatile(
+            "{\n\t.reg .b128 d, c, n;\n\t"
+            "mov.b128 c, {%2, %3};\n\t"
+            "mov.b128 n, {%4, %5};\n\t"
+            "atom.global.cas.b128 d, [%6], c, n;\n\t"
+            "mov.b128 {%0, %1}, d;\n\t}"
+            : "=l"(olo), "=l"(ohi)
+            : "l"(lo), "l"(hi), "l"(nlo), "l"(nhi), "l"(a)
+            : "memory");
+        if (olo == lo && ohi == hi) return;
+        lo = olo;
+        hi = ohi;
+    }
+}
+
 #ifdef PP_EVAL_PROBE
 __device__ unsigned long long g_ev_probe[4096][8];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -232,15 +259,11 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                 base += w < warp ? x : 0;
                 total += x;
             }
-            for (int k = lane; k < np; k += 32) {
-                int j = 0, t = 0;
+            {
+                const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-                for (int jj = 0; jj < CPW; jj++)
-                    if (k >= cum[jj] && k < cum[jj + 1]) {
-                        j = jj;
-                        t = nth_bit(win[jj], k - cum[jj]);
-                    }
-                s_pair[base + k] = ((warp * CPW + j) << 8) | t;
+                for (int j = 0; j < CPW; j++)
+                    if ((win[j] >> lane) & 1u) s_pair[base + cum[j] + __popc(win[j] & lt)] = ((warp * CPW + j) << 8) | lane;
             }
             __syncthreads();
             for (int k = threadIdx.x; k < total; k += EV_THREADS) {
@@ -364,39 +387,41 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     }
     EV_PROBE(5);
 
-    // ---- sparse pairs: the warp's slot range is reserved before the CTA barrier below, so
-    //      the atomic's round trip overlaps it; the entries are written after it ----
-    int pcum[CPW + 1], pbase = 0;
-    if constexpr (STATS_T) {
-        pcum[0] = 0;
-#pragma unroll
-        for (int j = 0; j < CPW; j++) pcum[j + 1] = pcum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
-        if (stats && p.n_pairs && lane == 0 && pcum[CPW]) pbase = atomicAdd(p.n_pairs, pcum[CPW]);
-    }
-    // ---- argmax: warp -> CTA -> grid ----
-    if (lane == 0) s_red[warp] = wbest;
-    __syncthreads();
+    // ---- sparse pairs: one reservation per warp, lane t writes candidate j's period-t entry ----
     if constexpr (STATS_T) {
         if (stats && p.n_pairs) {
-            const int np = pcum[CPW];
-            pbase = __shfl_sync(FULL, pbase, 0);
-            for (int k = lane; k < np; k += 32) {
-                int j = 0, t = 0;
+            int pcum[CPW + 1];
+            pcum[0] = 0;
 #pragma unroll
-                for (int jj = 0; jj < CPW; jj++)
-                    if (k >= pcum[jj] && k < pcum[jj + 1]) {
-                        j = jj;
-                        t = nth_bit(okm[jj], k - pcum[jj]);
-                    }
-                p.pair_cand[pbase + k] = cw + j;
-                p.pair_period[pbase + k] = t;
-                p.pair_exp[pbase + k] = w_ex[j * T + t];
-                p.pair_cvar[pbase + k] = w_cv[j * T + t];
-            }
+            for (int j = 0; j < CPW; j++) pcum[j + 1] = pcum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
+            int pbase = 0;
+            if (lane == 0 && pcum[CPW]) pbase = atomicAdd(p.n_pairs, pcum[CPW]);
+            pbase = __shfl_sync(FULL, pbase, 0);
+            const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int j = 0; j < CPW; j++)
+                if (cw + j < p.C && ((okm[j] >> lane) & 1u)) {
+                    const int q = pbase + pcum[j] + __popc(okm[j] & lt);
+                    p.pair_cand[q] = cw + j;
+                    p.pair_period[q] = lane;
+                    p.pair_exp[q] = w_ex[j * T + lane];
+                    p.pair_cvar[q] = w_cv[j * T + lane];
+                }
         }
     }
-    Best mine = (warp == 0 && lane < NW) ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
-    grid_argmax_warp0(mine, s_red, p.partial, p.counter, p.global);
+    // ---- argmax: warp -> CTA (shared memory) -> the global record by one 128-bit
+    //      compare-and-swap per CTA (no last-CTA pass; initialised ahead of the launch) ----
+    if (lane == 0) s_red[warp] = wbest;
+    __syncthreads();
+    if (warp == 0) {
+        Best x = lane < NW ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const Best o = shfl_best(x, off);
+            if (better(o, x)) x = o;
+        }
+        if (lane == 0 && x.b != INT_MAX) best_cas(p.global, x);
+    }
     EV_PROBE(6);
 }
 
@@ -526,8 +551,11 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         const int per_cta = CPW * (EV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));
+        if (reinterpret_cast<uintptr_t>(o.global) & 15u)
+            return fail(PP_ERR_INVALID_ARGS, "global (pp_best) must be 16-byte aligned");
         bool pdl;
-        TRY(refresh_pm(c, st, &pdl, o.n_pairs));  // zeroes n_pairs ahead of the evaluation
+        const EvalInit init{o.n_pairs, o.global};
+        TRY(refresh_pm(c, st, &pdl, &init));  // initialises n_pairs and the best record ahead of the evaluation
         const bool scen = o.scen_delta != nullptr;
 #define PP_WARP(KC, SC)                                                     \
     {                                                                       \
@@ -543,7 +571,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     }
     {
         bool pdl;
-        TRY(refresh_pm(c, st, &pdl, o.n_pairs));  // zeroes n_pairs ahead of the evaluation
+        const EvalInit init{o.n_pairs, nullptr};  // the general kernel's last CTA writes the best record
+        TRY(refresh_pm(c, st, &pdl, &init));
         TRY(launch_general_candidates(PER, kc, o.scen_delta != nullptr, C, G, S, c->Sp, T, stats, st, pdl, c->device,
                                       ep));
     }

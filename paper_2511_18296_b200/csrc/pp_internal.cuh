@@ -456,13 +456,14 @@ struct pp_ctx {
     DevBuf cnt, compact, pm_batch, predcnt, partial, counter, pm_flags;
     size_t pm_flags_n = 0;
     size_t last_pairs = 0;  // sparse pair count of the previous host-mode evaluation
+    DevBuf best_none;       // one pp_best {-inf, -1, -1}
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
     std::vector<DevBuf *> all() {
         return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
-                &h_d2, &h_pm, &h_p};
+                &h_d2, &h_pm, &h_p, &best_none};
     }
 };
 
@@ -518,10 +519,16 @@ inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream
 int ensure_grid_scratch(pp_ctx *c, int grid);
 int check_ready(pp_ctx *c, uint32_t flags, int scenario);
 int pick_kc(int k);
-// zero (optional): a device word the period-mass launch sets to 0 before anything that follows it
+// Per-launch output state the evaluation kernel accumulates into with atomics: the period-mass
+// launch ahead of it initialises it (n_pairs = 0, best = none), otherwise a copy node does.
+struct EvalInit {
+    int32_t *n_pairs;
+    pp_best *best;
+};
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st,
-                    int32_t *zero = nullptr);
-int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, int32_t *zero = nullptr);
+                    const EvalInit *init = nullptr);
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init = nullptr);
+int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st);
 int launch_general_candidates(int PER, int kc, bool scen, int C, int G, int S, int Sp, int T, bool stats,
                               cudaStream_t st, bool pdl, int device, const EvalParams &ep);
 

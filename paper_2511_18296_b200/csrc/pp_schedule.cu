@@ -1,6 +1,7 @@
 // pp_schedule.cu -- schedule-side kernels: bit-exact period masses (numpy pairwise tree),
 // check_feasible, topological-wave repair, table preparation, and their C-ABI entry points.
 #include "pp_internal.cuh"
+#include <limits>
 
 // ------------------------------------------------------------------------------------
 // period mass, bit-exact numpy pairwise summation per period (evaluate.py:334-337)
@@ -600,10 +601,13 @@ __device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &le
 template <int K>
 __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
-                 double *__restrict__ compact, double *__restrict__ pm_out, int32_t *__restrict__ zero) {
+                 double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init) {
     __shared__ PmcSmem h;
     PMCP(0, 0);
-    if (zero && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *zero = 0;  // complete before dependents' wait
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {  // complete before the dependents' wait
+        if (init.n_pairs) *init.n_pairs = 0;
+        if (init.best) *init.best = pp_best{-kInf, -1, -1};
+    }
     asm volatile("griddepcontrol.launch_dependents;");
     constexpr unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -771,14 +775,15 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
 
 template <int K>
 static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
-                             int32_t *zero) {
+                             const EvalInit *init) {
+    const EvalInit in = init ? *init : EvalInit{nullptr, nullptr};
     k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, 0, st>>>(d_assign, c->mass.as<double>(), c->B, c->T,
-                                                              c->compact.as<double>(), d_pm, zero);
+                                                              c->compact.as<double>(), d_pm, in);
     CUDA_TRY(cudaGetLastError());
     return PP_OK;
 }
 
-int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st, int32_t *zero) {
+int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st, const EvalInit *init) {
     const int B = c->B, T = c->T;
     const int nchunk = (B + PM_CH - 1) / PM_CH;
     // compacted masses: B doubles per (period, schedule); batches bounded to ~512 MiB
@@ -798,7 +803,7 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
             const int np = std::min(pchunk, P - p0);
             const int32_t *a = d_assign + (size_t)p0 * B;
             double *o = d_pm + (size_t)p0 * T;
-            int32_t *z = p0 == 0 ? zero : nullptr;
+            const EvalInit *z = p0 == 0 ? init : nullptr;
             if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st, z));
             else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st, z));
             else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st, z));
@@ -806,7 +811,7 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
         }
         return PP_OK;
     }
-    if (zero) CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(int32_t), st));
+    if (init) TRY(init_eval_outputs(c, *init, st));
     const size_t smem = std::max(sizeof(PmTreeSmem), sizeof(int) * ((PM_THREADS / 32) * PM_MAXT + PM_MAXT));
     static bool attr_done = false;
     if (!attr_done) {
@@ -826,13 +831,26 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
 }
 
 // recompute the current schedule's period masses if the schedule changed
-int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, int32_t *zero) {
+int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st) {
+    if (init.n_pairs) CUDA_TRY(cudaMemsetAsync(init.n_pairs, 0, sizeof(int32_t), st));
+    if (init.best) {
+        if (!c->best_none.ptr) {
+            TRY(c->best_none.ensure(sizeof(pp_best)));
+            const pp_best none{-std::numeric_limits<double>::infinity(), -1, -1};
+            CUDA_TRY(cudaMemcpy(c->best_none.ptr, &none, sizeof(pp_best), cudaMemcpyHostToDevice));
+        }
+        CUDA_TRY(cudaMemcpyAsync(init.best, c->best_none.ptr, sizeof(pp_best), cudaMemcpyDeviceToDevice, st));
+    }
+    return PP_OK;
+}
+
+int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init) {
     *launched = false;
     if (!c->pm_dirty) {
-        if (zero) CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(int32_t), st));
+        if (init) TRY(init_eval_outputs(c, *init, st));
         return PP_OK;
     }
-    TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st, zero));
+    TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st, init));
     c->pm_dirty = false;
     *launched = true;
     return PP_OK;
