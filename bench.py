@@ -115,6 +115,22 @@ def build_inputs(config: str, rank: int = 0):
     return c
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_eval_warp launch from the committed
+    `ncu --set full` capture (profiles/r01_ncu_full.json), or None."""
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full.json")
+    try:
+        m = json.load(open(f))["k_eval_warp"]
+    except (OSError, KeyError, ValueError):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v, u = m[k]
+        tot += float(v) * scale.get(u, 1)
+    return tot
+
+
 def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
     """Compulsory bytes of one k_eval_warp launch: every candidate's inputs
     once, its best move, and one (candidate, period, expected delta, CVaR10) record per
@@ -389,7 +405,7 @@ def run_gpu(args):
                 "peak": hbm,
                 "unit": "GB/s",
                 "frac": achieved / hbm,
-                "traffic": args.ncu_traffic,
+                "traffic": args.ncu_traffic if args.ncu_traffic is not None else _ncu_traffic(),
                 "kernel": "k_eval_warp",
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": ab["per_launch"],
