@@ -154,9 +154,12 @@ PP_API int pp_set_scenarios(pp_ctx *ctx, int32_t n_scenarios, const double *vmax
  * PP_MEM_DEVICE_BORROW until the next call).  period_mass[t] = masses[assign == t].sum()
  * is recomputed bit-exactly (numpy pairwise summation, evaluate.py:334-337) by the next
  * evaluation launch, overlapped with it through programmatic dependent launch.
- * PP_MEM_HOST: the values are range-checked here and the copy is stream-ordered, not
- * synchronous -- a pageable buffer may be reused on return (the driver stages it); a
- * page-locked buffer must stay unchanged until the next synchronous call returns. */
+ * PP_MEM_HOST: the copy is stream-ordered, not synchronous -- a pageable buffer may be
+ * reused on return (the driver stages it); a page-locked buffer must stay unchanged until
+ * the next synchronous call returns.  Period indices outside [-1, T) are an error
+ * (PP_ERR_INVALID_ARGS): checked here, or -- for B <= 65536 and T <= 16 -- on the device by
+ * the period-mass kernel and reported by the next host-mode call, after which the context
+ * has no schedule until the next pp_set_schedule. */
 PP_API int pp_set_schedule(pp_ctx *ctx, const int32_t *assign, int32_t mem, void *stream);
 /* Apply accepted deltas assign[blocks[k]] = periods[k] and recompute period_mass. */
 PP_API int pp_apply_moves(pp_ctx *ctx, const int32_t *blocks, const int32_t *periods, int32_t n,

@@ -101,6 +101,8 @@ int pp_ctx_destroy(pp_ctx *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf *b : c->all()) b->release();
+    if (c->h_bad) cudaFreeHost(c->h_bad);
+    if (c->h_bounce) cudaFreeHost(c->h_bounce);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return PP_OK;
@@ -121,7 +123,7 @@ int pp_synchronize(pp_ctx *c, void *stream) {
 
 int pp_host_alloc(size_t bytes, void **ptr) {
     if (!ptr) return fail(PP_ERR_INVALID_ARGS, "ptr is NULL");
-    CUDA_TRY(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+    CUDA_TRY(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable | cudaHostAllocMapped));
     return PP_OK;
 }
 

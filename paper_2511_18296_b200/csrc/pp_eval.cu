@@ -137,7 +137,7 @@ __device__ __forceinline__ void best_cas(pp_best *g, const Best &x) {
 }
 
 #ifdef PP_EVAL_PROBE
-__device__ unsigned long long g_ev_probe[4096][8];
+__device__ unsigned long long g_ev_probe[4096][12];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     int bl = -1;
     if (lane < CPW && cw + lane < p.C) {
         bl = __ldg(p.cand + cw + lane);
-        if (bl < 0 || bl >= p.B) bl = -1;
+        if (bl < 0 || bl >= p.B) {
+            if (p.bad_cand) *p.bad_cand = 1;  // reported by the host-mode call
+            bl = -1;
+        }
     }
     int b[CPW];
 #pragma unroll
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                     if ((win[j] >> lane) & 1u) s_pair[base + cum[j] + __popc(win[j] & lt)] = ((warp * CPW + j) << 8) | lane;
             }
             __syncthreads();
+            EV_PROBE(8);
             for (int k = threadIdx.x; k < total; k += EV_THREADS) {
                 const int e = s_pair[k], i = e >> 8, t = e & 0xff;
                 const int wq = i / CPW, jq = i - wq * CPW;
@@ -286,6 +290,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
             __syncthreads();
         }
     }
+    EV_PROBE(7);
 
 
     // ---- moves, pm-independent half: value of every window period (evaluate.py:379-384) and
@@ -427,14 +432,63 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
 
 #ifdef PP_EVAL_PROBE
 extern "C" PP_API int pp_debug_eval_probe(unsigned long long *out) {
-    return cudaMemcpyFromSymbol(out, g_ev_probe, sizeof(unsigned long long) * 4096 * 8) == cudaSuccess ? 0 : 3;
+    return cudaMemcpyFromSymbol(out, g_ev_probe, sizeof(unsigned long long) * 4096 * 12) == cudaSuccess ? 0 : 3;
 }
 #endif
+
+
+// ------------------------------------------------------------------------------------
+// Host-mode copy-out: when every output array is page-locked (device-mapped under UVA), one
+// launch writes all of them straight into host memory with 16-byte stores, reading the sparse
+// pair count on the device -- instead of one cudaMemcpyAsync per array (each ~4 us of CPU) and
+// a speculative pair copy.
+// ------------------------------------------------------------------------------------
+struct CopySeg {
+    const unsigned char *src;
+    unsigned char *dst;
+    unsigned long long bytes;  // fixed size, or
+    int per_pair;              // > 0: bytes = n_pairs * per_pair
+};
+constexpr int PP_MAX_SEGS = 16;
+struct CopyOut {
+    CopySeg seg[PP_MAX_SEGS];
+    int nseg;
+    const int32_t *n_pairs;
+};
+
+__global__ void __launch_bounds__(256) k_copy_out(const CopyOut co) {
+    const CopySeg &sg = co.seg[blockIdx.y];
+    const unsigned long long bytes =
+        sg.per_pair > 0 ? (unsigned long long)max(0, __ldcg(co.n_pairs)) * sg.per_pair : sg.bytes;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15u) == 0;
+    unsigned long long body = 0;
+    if (vec) {
+        body = bytes & ~15ull;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(sg.src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(sg.dst);
+        for (unsigned long long i = tid; i < body / 16; i += stride) d4[i] = __ldcg(s4 + i);
+    }
+    for (unsigned long long i = body + tid; i < bytes; i += stride) sg.dst[i] = sg.src[i];
+}
+
+// device pointer of a page-locked host buffer, or nullptr (pageable / unknown)
+static void *mapped_host(const void *p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+}
 
 extern "C" {
 
 int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenario, uint32_t flags,
                        const pp_cand_out *out, int32_t mem, void *stream) {
+    HostTrace ht("pp_eval_candidates");
     TRY(check_ready(c, flags, scenario));
     if (C < 0 || (C > 0 && !cand)) return fail(PP_ERR_INVALID_ARGS, "bad candidate array");
     if (!out || !out->best_t || !out->best_val || !out->feasible || !out->global)
@@ -464,13 +518,19 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 
     pp_cand_out o = *out;
     const int32_t *dcand = cand;
+    const bool warp_path = T <= 32 && (!stats || S <= 128) && c->nbr.ptr;
     if (mem == PP_MEM_HOST) {
-        int32_t lo = 0, hi = 0;  // branch-free min/max (vectorises)
-        for (int i = 0; i < C; i++) {
-            lo = std::min(lo, cand[i]);
-            hi = std::max(hi, cand[i]);
+        if (!warp_path) {  // the warp kernel range-checks the ids itself (reported after the sync)
+            int32_t lo = 0, hi = 0;  // branch-free min/max (vectorises)
+            for (int i = 0; i < C; i++) {
+                lo = std::min(lo, cand[i]);
+                hi = std::max(hi, cand[i]);
+            }
+            if (lo < 0 || hi >= c->B) return fail(PP_ERR_INVALID_ARGS, "candidate block out of range [0, %d)", c->B);
+            ht.mark("validate");
+        } else if (!c->bad_cand.ptr) {
+            TRY(c->bad_cand.ensure(sizeof(int32_t)));
         }
-        if (lo < 0 || hi >= c->B) return fail(PP_ERR_INVALID_ARGS, "candidate block out of range [0, %d)", c->B);
         const size_t Cs = (size_t)std::max(C, 1), CT = Cs * T;
         TRY(c->h_cand.ensure(sizeof(int32_t) * Cs));
         TRY(c->h_o1.ensure(sizeof(int32_t) * Cs));
@@ -497,6 +557,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         }
         if (C > 0) CUDA_TRY(cudaMemcpyAsync(c->h_cand.ptr, cand, sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
         dcand = c->h_cand.as<int32_t>();
+        ht.mark("h2d");
     }
 
     EvalParams ep;
@@ -544,7 +605,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     ep.global = o.global;
 
     // fast path: one warp per CPW candidates (k_eval_warp)
-    if (T <= 32 && (!stats || S <= 128) && c->nbr.ptr) {
+    if (warp_path) {
         const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
         const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32) + sig_bytes(S, T, stats);
@@ -554,7 +615,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         if (reinterpret_cast<uintptr_t>(o.global) & 15u)
             return fail(PP_ERR_INVALID_ARGS, "global (pp_best) must be 16-byte aligned");
         bool pdl;
-        const EvalInit init{o.n_pairs, o.global};
+        ep.bad_cand = mem == PP_MEM_HOST ? c->bad_cand.as<int32_t>() : nullptr;
+        const EvalInit init{o.n_pairs, o.global, ep.bad_cand};
         TRY(refresh_pm(c, st, &pdl, &init));  // initialises n_pairs and the best record ahead of the evaluation
         const bool scen = o.scen_delta != nullptr;
 #define PP_WARP(KC, SC)                                                     \
@@ -571,15 +633,84 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     }
     {
         bool pdl;
-        const EvalInit init{o.n_pairs, nullptr};  // the general kernel's last CTA writes the best record
+        const EvalInit init{o.n_pairs, nullptr, nullptr};  // the general kernel's last CTA writes the best record
         TRY(refresh_pm(c, st, &pdl, &init));
         TRY(launch_general_candidates(PER, kc, o.scen_delta != nullptr, C, G, S, c->Sp, T, stats, st, pdl, c->device,
                                       ep));
     }
 copy_out:
+    ht.mark("launch");
 
     if (mem == PP_MEM_HOST) {
         const size_t Cs = (size_t)C, CT = Cs * T;
+        {  // one copy-out launch when every destination is page-locked
+            CopyOut co;
+            memset(&co, 0, sizeof(co));
+            co.n_pairs = o.n_pairs;
+            bool ok = true;
+            // small fixed-size results in pageable memory (e.g. a ctypes pp_best) go through a
+            // page-locked bounce buffer of the context, copied out by the CPU after the sync
+            if (!c->h_bounce) {
+                CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_bounce), 256,
+                                       cudaHostAllocPortable | cudaHostAllocMapped));
+            }
+            struct Bounce {
+                void *user;
+                size_t off, bytes;
+            } bounce[4];
+            int nb = 0;
+            size_t boff = 0;
+            auto add = [&](const void *src, void *dst, size_t bytes, int per_pair) {
+                if (!dst || !ok) return;
+                void *d = mapped_host(dst);
+                if (!d && per_pair == 0 && bytes <= 64 && nb < 4) {
+                    bounce[nb++] = Bounce{dst, boff, bytes};
+                    d = c->h_bounce + boff;
+                    boff += 64;
+                }
+                if (!d || co.nseg == PP_MAX_SEGS) {
+                    ok = false;
+                    return;
+                }
+                co.seg[co.nseg++] = CopySeg{static_cast<const unsigned char *>(src), static_cast<unsigned char *>(d),
+                                            (unsigned long long)bytes, per_pair};
+            };
+            add(o.global, out->global, sizeof(pp_best), 0);
+            if (C > 0) {
+                add(o.best_t, out->best_t, sizeof(int32_t) * Cs, 0);
+                add(o.best_val, out->best_val, sizeof(double) * Cs, 0);
+                add(o.feasible, out->feasible, Cs, 0);
+                add(o.trace_val, out->trace_val, sizeof(double) * CT, 0);
+                add(o.trace_feas, out->trace_feas, CT, 0);
+                add(o.exp_delta, out->exp_delta, sizeof(double) * CT, 0);
+                add(o.cvar, out->cvar, sizeof(double) * CT, 0);
+                add(o.scen_delta, out->scen_delta, sizeof(float) * CT * S, 0);
+            }
+            int32_t bad_c = 0;
+            if (warp_path) add(c->bad_cand.ptr, &bad_c, sizeof(int32_t), 0);
+            const bool bad_copy = c->bad_pending && !c->pm_dirty;
+            if (bad_copy) add(c->pm_bad.ptr, c->h_bad, sizeof(int32_t) * 8, 0);
+            if (pairs) {
+                add(o.n_pairs, out->n_pairs, sizeof(int32_t), 0);
+                add(o.pair_cand, out->pair_cand, 0, sizeof(int32_t));
+                add(o.pair_period, out->pair_period, 0, sizeof(int32_t));
+                add(o.pair_exp, out->pair_exp, 0, sizeof(double));
+                add(o.pair_cvar, out->pair_cvar, 0, sizeof(double));
+            }
+            ht.mark("map check");
+            if (ok) {
+                k_copy_out<<<dim3(32, co.nseg), 256, 0, st>>>(co);
+                CUDA_TRY(cudaGetLastError());
+                ht.mark("d2h enqueue");
+                CUDA_TRY(stream_wait(st));
+                ht.mark("sync");
+                for (int i = 0; i < nb; i++) memcpy(bounce[i].user, c->h_bounce + bounce[i].off, bounce[i].bytes);
+                TRY(check_schedule_range(c, bad_copy));
+                if (bad_c) return fail(PP_ERR_INVALID_ARGS, "candidate block out of range [0, %d)", c->B);
+                if (pairs) c->last_pairs = (size_t)std::max(0, *out->n_pairs);
+                return PP_OK;
+            }
+        }
         CUDA_TRY(cudaMemcpyAsync(out->global, o.global, sizeof(pp_best), cudaMemcpyDeviceToHost, st));
         if (C > 0) {
             CUDA_TRY(cudaMemcpyAsync(out->best_t, o.best_t, sizeof(int32_t) * Cs, cudaMemcpyDeviceToHost, st));
@@ -609,13 +740,21 @@ copy_out:
             spec = std::min((size_t)C * T, c->last_pairs + c->last_pairs / 4 + 1024);
             TRY(copy_pairs(0, spec));
         }
-        CUDA_TRY(cudaStreamSynchronize(st));
+        ht.mark("d2h enqueue");
+        CUDA_TRY(stream_wait(st));
+        ht.mark("sync");
+        TRY(check_schedule_range(c, false));
+        if (warp_path) {
+            int32_t bad_c = 0;
+            CUDA_TRY(cudaMemcpy(&bad_c, c->bad_cand.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost));
+            if (bad_c) return fail(PP_ERR_INVALID_ARGS, "candidate block out of range [0, %d)", c->B);
+        }
         if (pairs) {
             const size_t n = (size_t)std::max(0, *out->n_pairs);
             c->last_pairs = n;
             if (n > spec) {
                 TRY(copy_pairs(spec, n));
-                CUDA_TRY(cudaStreamSynchronize(st));
+                CUDA_TRY(stream_wait(st));
             }
         }
     }

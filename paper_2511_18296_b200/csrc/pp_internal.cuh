@@ -3,6 +3,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <climits>
@@ -365,6 +368,7 @@ struct EvalParams {
     double *exp_delta;
     double *cvar;
     float *scen_delta;
+    int32_t *bad_cand;
     int32_t *pair_cand;
     int32_t *pair_period;
     double *pair_exp;
@@ -457,15 +461,52 @@ struct pp_ctx {
     size_t pm_flags_n = 0;
     size_t last_pairs = 0;  // sparse pair count of the previous host-mode evaluation
     DevBuf best_none;       // one pp_best {-inf, -1, -1}
+    // host-mode schedules on the cluster path are range-checked on the device by k_pm_cluster
+    // (one flag per CTA) and reported by the next host-mode call that synchronises
+    DevBuf pm_bad;
+    int32_t *h_bad = nullptr;  // page-locked mirror [8]
+    unsigned char *h_bounce = nullptr;  // page-locked bounce buffer for small host-mode results
+    DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
+    bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
     std::vector<DevBuf *> all() {
         return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
-                &h_d2, &h_pm, &h_p, &best_none};
+                &h_d2, &h_pm, &h_p, &best_none, &bad_cand};
     }
 };
+
+// PP_TRACE_HOST=1: per-phase host time of the C-ABI calls on stderr (diagnostics only)
+struct HostTrace {
+    const char *name;
+    bool on;
+    std::chrono::steady_clock::time_point t0, t;
+    explicit HostTrace(const char *n) : name(n), on(std::getenv("PP_TRACE_HOST") != nullptr) {
+        if (on) t0 = t = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[%s] %-12s %7.1f us\n", name, what, std::chrono::duration<double, std::micro>(n - t).count());
+        t = n;
+    }
+    ~HostTrace() {
+        if (on)
+            std::fprintf(stderr, "[%s] total        %7.1f us\n", name,
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
+// Host-mode completion wait: spin on the stream (the results are usually ~20-40 us away, below a
+// blocking synchronisation's wake-up latency).
+inline cudaError_t stream_wait(cudaStream_t st) {
+    cudaError_t e;
+    while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
+    }
+    return e;
+}
 
 inline int use_device(pp_ctx *c) {
     CUDA_TRY(cudaSetDevice(c->device));
@@ -524,11 +565,16 @@ int pick_kc(int k);
 struct EvalInit {
     int32_t *n_pairs;
     pp_best *best;
+    int32_t *bad_cand;  // set to 0; the evaluation stores 1 on an out-of-range candidate id
 };
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st,
                     const EvalInit *init = nullptr);
 int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init = nullptr);
 int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st);
+bool pm_cluster_path(const pp_ctx *c);
+// after the stream was synchronised: PP_ERR_INVALID_ARGS if the pending host schedule had
+// period indices out of range (h_bad already copied when `copied`)
+int check_schedule_range(pp_ctx *c, bool copied);
 int launch_general_candidates(int PER, int kc, bool scen, int C, int G, int S, int Sp, int T, bool stats,
                               cudaStream_t st, bool pdl, int device, const EvalParams &ep);
 

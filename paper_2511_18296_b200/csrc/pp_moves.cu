@@ -258,6 +258,7 @@ int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, i
                 CUDA_TRY(cudaMemcpyAsync(out->scen_delta, o.scen_delta, sizeof(float) * Ms * S, cudaMemcpyDeviceToHost, st));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
+        TRY(check_schedule_range(c, false));
     }
     return PP_OK;
 }

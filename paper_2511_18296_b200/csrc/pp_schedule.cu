@@ -601,12 +601,14 @@ __device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &le
 template <int K>
 __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
-                 double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init) {
+                 double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init,
+                 int32_t *__restrict__ bad) {
     __shared__ PmcSmem h;
     PMCP(0, 0);
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {  // complete before the dependents' wait
         if (init.n_pairs) *init.n_pairs = 0;
         if (init.best) *init.best = pp_best{-kInf, -1, -1};
+        if (init.bad_cand) *init.bad_cand = 0;
     }
     asm volatile("griddepcontrol.launch_dependents;");
     constexpr unsigned FULL = 0xffffffffu;
@@ -616,6 +618,7 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     const int base = (r * PMC_WARPS + warp) * (32 * K);
     int tk[K];
     double mk[K];
+    int badl = 0;
 #pragma unroll
     for (int k = 0; k < K; k++) {
         const int b = base + k * 32 + lane;
@@ -626,6 +629,7 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
             m = __ldg(mass + b);
         }
         tk[k] = ((unsigned)t < (unsigned)T) ? t : -1;
+        badl |= (t < -1) | (t >= T);
         mk[k] = m;
     }
     PMCS(0);
@@ -644,7 +648,8 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
         if (tk[k] >= 0 && lr == 0) h.cnt[warp][tk[k]] = b0 + __popc(mt);
         __syncwarp();
     }
-    __syncthreads();
+    const int anybad = __syncthreads_or(badl);  // (also the barrier after the ranks)
+    if (bad && threadIdx.x == 0 && blockIdx.y == 0) bad[blockIdx.x] = anybad;  // every CTA writes its flag
     // per-period exclusive scan over the warps (warp j scans period j)
     if (warp < T) {
         const int v = h.cnt[lane][warp];
@@ -775,10 +780,10 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
 
 template <int K>
 static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
-                             const EvalInit *init) {
-    const EvalInit in = init ? *init : EvalInit{nullptr, nullptr};
+                             const EvalInit *init, int32_t *bad) {
+    const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
     k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, 0, st>>>(d_assign, c->mass.as<double>(), c->B, c->T,
-                                                              c->compact.as<double>(), d_pm, in);
+                                                              c->compact.as<double>(), d_pm, in, bad);
     CUDA_TRY(cudaGetLastError());
     return PP_OK;
 }
@@ -797,17 +802,18 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
         CUDA_TRY(cudaMemset(c->pm_flags.ptr, 0, sizeof(int32_t) * nflags));
         c->pm_flags_n = nflags;
     }
-    if (T <= PMC_MAXT && B <= PMC_MAXB) {
+    if (pm_cluster_path(c)) {
         const int K = B <= PMC_MAXB / 8 ? 1 : B <= PMC_MAXB / 4 ? 2 : B <= PMC_MAXB / 2 ? 4 : 8;
         for (int p0 = 0; p0 < P; p0 += pchunk) {
             const int np = std::min(pchunk, P - p0);
             const int32_t *a = d_assign + (size_t)p0 * B;
             double *o = d_pm + (size_t)p0 * T;
             const EvalInit *z = p0 == 0 ? init : nullptr;
-            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st, z));
-            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st, z));
-            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st, z));
-            else TRY(launch_pm_cluster<8>(c, a, np, o, st, z));
+            int32_t *bad = (P == 1 && d_assign == c->assign_ptr && c->bad_pending) ? c->pm_bad.as<int32_t>() : nullptr;
+            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st, z, bad));
+            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st, z, bad));
+            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st, z, bad));
+            else TRY(launch_pm_cluster<8>(c, a, np, o, st, z, bad));
         }
         return PP_OK;
     }
@@ -831,8 +837,23 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
 }
 
 // recompute the current schedule's period masses if the schedule changed
+bool pm_cluster_path(const pp_ctx *c) { return c->T <= PMC_MAXT && c->B <= PMC_MAXB; }
+
+int check_schedule_range(pp_ctx *c, bool copied) {
+    if (!c->bad_pending || c->pm_dirty) return PP_OK;  // not range-checked yet
+    c->bad_pending = false;
+    if (!copied) CUDA_TRY(cudaMemcpy(c->h_bad, c->pm_bad.ptr, sizeof(int32_t) * PMC_R, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < PMC_R; r++)
+        if (c->h_bad[r]) {
+            c->have_sched = false;  // unusable until the next pp_set_schedule
+            return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
+        }
+    return PP_OK;
+}
+
 int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st) {
     if (init.n_pairs) CUDA_TRY(cudaMemsetAsync(init.n_pairs, 0, sizeof(int32_t), st));
+    if (init.bad_cand) CUDA_TRY(cudaMemsetAsync(init.bad_cand, 0, sizeof(int32_t), st));
     if (init.best) {
         if (!c->best_none.ptr) {
             TRY(c->best_none.ensure(sizeof(pp_best)));
@@ -1083,19 +1104,29 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
 }
 
 int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream) {
+    HostTrace ht("pp_set_schedule");
     if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
     if (!assign) return fail(PP_ERR_INVALID_ARGS, "assign is NULL");
     if (mem != PP_MEM_HOST && mem != PP_MEM_DEVICE && mem != PP_MEM_DEVICE_BORROW)
         return fail(PP_ERR_INVALID_ARGS, "unknown memory kind %d", mem);
     TRY(use_device(c));
     cudaStream_t st = pick(c, stream);
-    if (mem == PP_MEM_HOST) {  // branch-free min/max (vectorises)
+    c->bad_pending = false;
+    if (mem == PP_MEM_HOST && pm_cluster_path(c)) {  // range-checked by k_pm_cluster on the device
+        if (!c->pm_bad.ptr) {
+            TRY(c->pm_bad.ensure(sizeof(int32_t) * PMC_R));
+            CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_bad), sizeof(int32_t) * PMC_R,
+                                   cudaHostAllocPortable | cudaHostAllocMapped));
+        }
+        c->bad_pending = true;
+    } else if (mem == PP_MEM_HOST) {  // branch-free min/max (vectorises)
         int32_t lo = 0, hi = -1;
         for (int b = 0; b < c->B; b++) {
             lo = std::min(lo, assign[b]);
             hi = std::max(hi, assign[b]);
         }
         if (lo < -1 || hi >= c->T) return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
+        ht.mark("validate");
     }
     if (mem == PP_MEM_DEVICE_BORROW) {
         c->assign_ptr = assign;  // read in place until the next pp_set_schedule
@@ -1150,7 +1181,10 @@ int pp_get_schedule(pp_ctx *c, int32_t *assign_out, double *pm_out, int32_t mem,
     cudaMemcpyKind k = (mem == PP_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (assign_out) CUDA_TRY(cudaMemcpyAsync(assign_out, c->assign_ptr, sizeof(int32_t) * c->B, k, st));
     if (pm_out) CUDA_TRY(cudaMemcpyAsync(pm_out, c->pm.ptr, sizeof(double) * c->T, k, st));
-    if (mem == PP_MEM_HOST) CUDA_TRY(cudaStreamSynchronize(st));
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        TRY(check_schedule_range(c, false));
+    }
     return PP_OK;
 }
 

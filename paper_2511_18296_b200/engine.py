@@ -61,6 +61,7 @@ class Engine:
         self.n_scenarios = 0
         self.has_sigma = False
         self._keep = []
+        self._eval_cache = None
 
     # -- lifecycle -----------------------------------------------------------------
     def close(self):
@@ -169,22 +170,33 @@ class Engine:
                         trace=False, stats=False, scen=False, pairs=False, out: dict | None = None,
                         validate: bool = True) -> dict:
         """Host-buffer evaluation; returns numpy arrays (and `best` as a tuple or None).
-        `out` may supply preallocated (e.g. pinned) host arrays for any output.
+        `out` may supply preallocated (e.g. pinned) host arrays for any output; page-locked
+        arrays (PinnedPool) are written in place by one copy-out launch, and a repeated call
+        with the same `out` arrays reuses the argument block (no per-call marshalling).
         pairs=True returns the statistics of the feasible moves only, as
-        res["pairs"] = {"cand", "period", "exp", "cvar"} (unordered; capacity C*T)."""
+        res["pairs"] = {"cand", "period", "exp", "cvar"} (unordered; capacity C*T).
+        Candidate ids are range-checked by pp_eval_candidates (`validate` is kept for
+        compatibility)."""
         bm = self._need_bm()
-        c = cand if (not validate and isinstance(cand, np.ndarray) and cand.dtype == np.int32) else _i32(cand)
+        c = cand if (isinstance(cand, np.ndarray) and cand.dtype == np.int32 and cand.flags.c_contiguous) \
+            else _i32(cand)
         C, T, S = c.size, bm.n_periods, self.n_scenarios
-        if validate and C and (c.min() < 0 or c.max() >= bm.n_blocks):
-            raise InvalidArgs("candidate block out of range")
+        key = None
+        if out:
+            key = (C, trace, stats, scen, pairs) + tuple(id(v) for v in out.values())
+            hit = self._eval_cache
+            if hit is not None and hit[0] == key:
+                _, _keep, res, pr, g, argblock = hit
+                self._eval_call(c, C, scenario, net, literal, use_sigma, argblock)
+                return self._eval_result(res, pr, g)
         out = out or {}
         res = {
-            "best_t": out.get("best_t", None) if "best_t" in out else np.empty(C, np.int32),
+            "best_t": out["best_t"] if "best_t" in out else np.empty(C, np.int32),
             "best_val": out["best_val"] if "best_val" in out else np.empty(C, np.float64),
             "feasible": out["feasible"] if "feasible" in out else np.empty(C, np.uint8),
         }
         if trace:
-            res["trace_val"] = out.get("trace_val", None) if "trace_val" in out else np.empty((C, T), np.float64)
+            res["trace_val"] = out["trace_val"] if "trace_val" in out else np.empty((C, T), np.float64)
             res["trace_feas"] = out["trace_feas"] if "trace_feas" in out else np.empty((C, T), np.uint8)
         if stats:
             res["exp_delta"] = out["exp_delta"] if "exp_delta" in out else np.empty((C, T), np.float64)
@@ -200,14 +212,24 @@ class Engine:
                   "cvar": out["pair_cvar"] if "pair_cvar" in out else np.empty(cap, np.float64),
                   "n": out["n_pairs"] if "n_pairs" in out else np.zeros(1, np.int32)}
         g = PPBest()
-        out = PPCandOut(
+        argblock = PPCandOut(
             ptr(res["best_t"]), ptr(res["best_val"]), ptr(res["feasible"]),
             ptr(res.get("trace_val")), ptr(res.get("trace_feas")), ptr(res.get("exp_delta")),
             ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g),
             *((ptr(pr["cand"]), ptr(pr["period"]), ptr(pr["exp"]), ptr(pr["cvar"]), ptr(pr["n"])) if pr else ()))
+        if key is not None:  # the arrays are kept alive by the cache entry, so their ids stay valid
+            self._eval_cache = (key, tuple(out.values()), res, pr, g, argblock)
+        self._eval_call(c, C, scenario, net, literal, use_sigma, argblock)
+        return self._eval_result(res, pr, g)
+
+    def _eval_call(self, c, C, scenario, net, literal, use_sigma, argblock):
         sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
-        check(self.lib.pp_eval_candidates(self._h, ptr(c), C, sc, self.flags(net, literal, use_sigma),
-                                          ctypes.byref(out), _lib.PP_MEM_HOST, None))
+        check(self.lib.pp_eval_candidates(self._h, c.ctypes.data, C, sc, self.flags(net, literal, use_sigma),
+                                          ctypes.byref(argblock), _lib.PP_MEM_HOST, None))
+
+    @staticmethod
+    def _eval_result(res, pr, g):
+        res = dict(res)
         res["best"] = None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
         if pr is not None:
             n = int(pr["n"][0])

@@ -296,8 +296,20 @@ def test_errors_are_raised_not_fallen_back():
         eng.eval_candidates(np.array([c["bm"].n_blocks]), None)
     with pytest.raises(InvalidArgs):
         eng.eval_candidates(np.array([0]), c["S"])
+    # out-of-range periods: range-checked on the device, reported by the next host-mode call
+    bad = np.full(c["bm"].n_blocks, c["T"])
     with pytest.raises(InvalidArgs):
-        eng.set_schedule(np.full(c["bm"].n_blocks, c["T"]))
+        eng.set_schedule(bad)
+        eng.eval_candidates(c["cand"], None, net=True)
+    with pytest.raises(PitplanError):  # no schedule until the next set_schedule
+        eng.eval_candidates(c["cand"], None)
+    bad[:] = c["assign"]
+    bad[17] = -2
+    with pytest.raises(InvalidArgs):
+        eng.set_schedule(bad)
+        eng.get_schedule()
+    eng.set_schedule(c["assign"])
+    assert eng.eval_candidates(c["cand"], None, net=True)["best"] is not None
     fresh = Engine(0)
     with pytest.raises(PitplanError):
         fresh.eval_candidates(np.array([0]), None)

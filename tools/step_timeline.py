@@ -28,7 +28,7 @@ with torch.cuda.graph(g):
 for rep in range(4):
     flush.fill_(rep); st.synchronize()
     g.replay(); st.synchronize()
-ev = np.zeros((4096, 8), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
+ev = np.zeros((4096, 12), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
 pm = np.zeros((2, 512, 2), np.uint64); lib.pp_debug_pm_probe(pm.ctypes.data); pm = pm.astype(np.int64)
 cl = pm[0, :8, 0].min() > 0
 if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
@@ -45,6 +45,6 @@ else:
     f = lambda x: (x - t0) / 1000
     print(f"P1 ({nch} CTAs): start {f(p1[:,0].min()):.2f}..{f(p1[:,0].max()):.2f}  end {f(p1[:,1].min()):.2f}..{f(p1[:,1].max()):.2f} us")
     print(f"P2 ({T} CTAs): after-wait {f(p2[:,0].min()):.2f}..{f(p2[:,0].max()):.2f}  end {f(p2[:,1].min()):.2f}..{f(p2[:,1].max()):.2f} us")
-names = ["start", "loads", "stats", "pm-wait", "moves", "outputs", "end"]
+names = ["start", "loads", "values", "pm-wait", "moves", "outputs", "end", "stats", "pooled"]
 for k in range(len(names)):
     print(f"eval {names[k]:9s} min {f(ev[:,k].min()):6.2f}  median {f(np.median(ev[:,k])):6.2f}  max {f(ev[:,k].max()):6.2f} us")
