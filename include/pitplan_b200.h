@@ -187,6 +187,15 @@ PP_API int pp_check_feasible(pp_ctx *ctx, const int32_t *assign, int32_t n_sched
  * (unmined_out[P][B] = 1 where the fixpoint unmined a block; may be NULL). */
 PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode, uint8_t *unmined_out,
               int32_t mem, void *stream);
+/* lns_repair's over-capacity ejection (hybrid.py:213-235) for P schedules assign[P][B] in place,
+ * applied after the unmine fixpoint (pp_repair PP_REPAIR_UNMINE): in every period whose mass
+ * (numpy pairwise) exceeds its target -- capacity, or capacity * (1 - destroy_fraction) when
+ * destroy_fraction > 0 -- the blocks with no mined successor are unmined in ascending
+ * (mean_grade[b] * mass[b], b) order until the mass is within the target (sequential f64
+ * subtraction).  mean_grade[B] = scenarios.grades.mean(axis=0).  ejected_out[P][B] (may be
+ * NULL) marks the ejected blocks. */
+PP_API int pp_eject(pp_ctx *ctx, int32_t *assign, int32_t n_sched, const double *mean_grade, double destroy_fraction,
+             uint8_t *ejected_out, int32_t mem, void *stream);
 /* Ordered reduction of n pp_best records (e.g. one per GPU after an all-gather) with the
  * selection order of evaluate.py:404-409; records with block < 0 are "none".  This is the
  * deterministic "allreduce-argmax" step of multi-GPU evaluation. */

@@ -401,6 +401,64 @@ void or_unmine_fixpoint(int32_t B, int64_t E, const int32_t *ei, const int32_t *
     }
 }
 
+/* ---- over-capacity ejection: lns_repair's destroy step (hybrid.py:213-235) -------
+ * mean_grade = scenarios.grades.mean(axis=0) (hybrid.py:214).  For each period t in order:
+ * load = masses[mined_in(t)].sum() (numpy pairwise, hybrid.py:217); target = cap[t], or
+ * cap[t] * (1 - destroy_fraction) when destroy_fraction > 0 and load > cap[t] (218-221);
+ * nothing happens when load <= target (222-223).  Otherwise the blocks of t whose successors
+ * are all UNMINED (224-228; evaluated before any ejection in t) are sorted by
+ * (mean_grade[b] * masses[b], b) (229) and unmined in that order, load -= masses[b] after
+ * each, while load > target (230-235).  Ejections in t never change the candidate list of a
+ * later period after the unmine fixpoint (successors are mined no earlier than their
+ * predecessors), but this restatement simply follows the reference order.  ejected_out[b] = 1
+ * for every ejected block (the additions to the repair pool). */
+typedef struct {
+    double key;
+    int32_t b;
+} or_ekey;
+static int or_ekey_cmp(const void *x, const void *y) {
+    const or_ekey *a = (const or_ekey *)x, *b = (const or_ekey *)y;
+    if (a->key < b->key) return -1;
+    if (a->key > b->key) return 1;
+    return (a->b > b->b) - (a->b < b->b);
+}
+void or_eject(int32_t B, int32_t T, const int32_t *succ_ptr, const int32_t *succ_idx, const double *mass,
+              const double *cap, const double *mean_grade, double destroy_fraction, int32_t *assign,
+              uint8_t *ejected_out) {
+    if (ejected_out) memset(ejected_out, 0, (size_t)B);
+    double *buf = (double *)malloc(sizeof(double) * (size_t)(B > 0 ? B : 1));
+    or_ekey *ej = (or_ekey *)malloc(sizeof(or_ekey) * (size_t)(B > 0 ? B : 1));
+    for (int32_t t = 0; t < T; t++) {
+        int64_t n = 0;
+        for (int32_t b = 0; b < B; b++)
+            if (assign[b] == t) buf[n++] = mass[b];
+        double load = or_np_sum(buf, n);
+        double target = cap[t];
+        if (destroy_fraction > 0 && load > cap[t]) target = cap[t] * (1.0 - destroy_fraction);
+        if (load <= target) continue;
+        int64_t ne = 0;
+        for (int32_t b = 0; b < B; b++) {
+            if (assign[b] != t) continue;
+            int ok = 1;
+            for (int32_t k = succ_ptr[b]; k < succ_ptr[b + 1] && ok; k++) ok = assign[succ_idx[k]] == UNMINED;
+            if (ok) {
+                ej[ne].key = mean_grade[b] * mass[b];
+                ej[ne].b = b;
+                ne++;
+            }
+        }
+        qsort(ej, (size_t)ne, sizeof(or_ekey), or_ekey_cmp);
+        for (int64_t k = 0; k < ne; k++) {
+            if (load <= target) break;
+            assign[ej[k].b] = UNMINED;
+            if (ejected_out) ejected_out[ej[k].b] = 1;
+            load -= mass[ej[k].b];
+        }
+    }
+    free(buf);
+    free(ej);
+}
+
 /* ---- explicit moves (reassign / unmine / swap) ---------------------------------
  * Reassign move (b, t_new), t_old = assign[b]:
  *   t_new == t_old                 -> not a move (infeasible), as polish skips t == orig

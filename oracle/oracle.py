@@ -46,6 +46,7 @@ _SIGS = {
     "or_precedence_repair": (None, [_i32, _P, _P, _P, _P]),
     "or_unmine_fixpoint": (None, [_i32, _i64, _P, _P, _P, _P]),
     "or_enpv_table": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _i32, _P]),
+    "or_eject": (None, [_i32, _i32, _P, _P, _P, _P, _P, _f64, _P, _P]),
     "or_eval_moves": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                              _P, _P, _P, _P, _i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _i32]),
 }
@@ -234,6 +235,15 @@ class Oracle:
         a = np.array(assign, dtype=np.int32, order="C")
         lib().or_precedence_repair(self.B, _p(self.pp), _p(self.pi), _p(self.order), _p(a))
         return a
+
+    def eject(self, assign, mean_grade, destroy_fraction=0.0):
+        """lns_repair's over-capacity ejection (hybrid.py:213-235) -> (assign, ejected mask)."""
+        a = np.array(assign, dtype=np.int32, order="C")
+        g = np.ascontiguousarray(mean_grade, dtype=np.float64)
+        e = np.empty(self.B, np.uint8)
+        lib().or_eject(self.B, self.T, _p(self.sp), _p(self.si), _p(self.mass), _p(self.cap), _p(g),
+                       float(destroy_fraction), _p(a), _p(e))
+        return a, e
 
     def unmine_fixpoint(self, assign):
         a = np.array(assign, dtype=np.int32, order="C")

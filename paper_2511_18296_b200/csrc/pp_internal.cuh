@@ -467,6 +467,7 @@ struct pp_ctx {
     int32_t *h_bad = nullptr;  // page-locked mirror [8]
     unsigned char *h_bounce = nullptr;  // page-locked bounce buffer for small host-mode results
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
+    DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
@@ -474,7 +475,7 @@ struct pp_ctx {
         return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
-                &h_d2, &h_pm, &h_p, &best_none, &bad_cand};
+                &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk};
     }
 };
 

@@ -403,6 +403,112 @@ __global__ void k_feas_final(const double *__restrict__ pm, const double *__rest
 }
 
 // ------------------------------------------------------------------------------------
+// lns_repair's over-capacity ejection (hybrid.py:213-235), after the unmine fixpoint.
+// Pass 1 (k_eject_list, one thread per block): every mined block of an over-target period
+// whose successors are all UNMINED joins its period's list with key mean_grade[b] * mass[b].
+// All lists are built from the same state before anything is ejected, which is what the
+// reference's ascending-t loop sees: after the fixpoint a block's successors are mined no
+// earlier than it, so ejecting in period t never changes the list of a later period.
+// Pass 2 (k_eject_apply, one CTA per period): repeatedly the smallest (key, b) is ejected
+// while load > target, load -= mass[b] in that order (the reference's sequential loop).
+// load = the bit-exact period mass (k_pm_cluster / k_period_mass).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double eject_target(double load, double cap, double df) {
+    return (df > 0 && load > cap) ? f64_mul(cap, f64_sub(1.0, df)) : cap;
+}
+
+__global__ void __launch_bounds__(256) k_eject_list(const int32_t *__restrict__ assign, int B, int T,
+                                                    const BlockRow *__restrict__ rows,
+                                                    const int32_t *__restrict__ adj, const double *__restrict__ pm,
+                                                    const double *__restrict__ cap, const double *__restrict__ grade,
+                                                    double df, int32_t *__restrict__ count,
+                                                    double *__restrict__ lkey, int32_t *__restrict__ lblk) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int t = assign[b];
+    if (t < 0 || t >= T) return;
+    const double load = pm[t];
+    if (load <= eject_target(load, cap[t], df)) return;
+    const BlockRow r = rows[b];
+    const int npred = r.cnt & 0xffff, nsucc = r.cnt >> 16;
+    for (int e = 0; e < nsucc; e++)
+        if (assign[__ldg(adj + r.adj + npred + e)] != -1) return;
+    const int k = atomicAdd(count + t, 1);
+    lkey[(size_t)t * B + k] = f64_mul(__ldg(grade + b), r.mass);
+    lblk[(size_t)t * B + k] = b;
+}
+
+__global__ void __launch_bounds__(512) k_eject_apply(int32_t *__restrict__ assign, int B,
+                                                     const double *__restrict__ mass, const double *__restrict__ pm,
+                                                     const double *__restrict__ cap, double df,
+                                                     const int32_t *__restrict__ count,
+                                                     const double *__restrict__ lkey, int32_t *__restrict__ lblk,
+                                                     uint8_t *__restrict__ ejected) {
+    const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = count[t];
+    if (n == 0) return;
+    const double *key = lkey + (size_t)t * B;
+    int32_t *blk = lblk + (size_t)t * B;
+    const double target = eject_target(pm[t], cap[t], df);
+    __shared__ double s_load;
+    __shared__ double s_k[16];
+    __shared__ int s_b[16], s_i[16];
+    if (tid == 0) s_load = pm[t];
+    for (;;) {
+        __syncthreads();
+        const double load = s_load;
+        if (load <= target) break;
+        // smallest remaining (key, b): a total order, so the choice is deterministic
+        double bk = kInf;
+        int bb = INT_MAX, bi = -1;
+        for (int i = tid; i < n; i += blockDim.x) {
+            const int b = blk[i];
+            if (b < 0) continue;
+            const double k = key[i];
+            if (k < bk || (k == bk && b < bb)) {
+                bk = k;
+                bb = b;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int ob = __shfl_xor_sync(0xffffffffu, bb, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ok < bk || (ok == bk && ob < bb)) {
+                bk = ok;
+                bb = ob;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_k[warp] = bk;
+            s_b[warp] = bb;
+            s_i[warp] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double k = s_k[0];
+            int b = s_b[0], i = s_i[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+                if (s_k[w] < k || (s_k[w] == k && s_b[w] < b)) {
+                    k = s_k[w];
+                    b = s_b[w];
+                    i = s_i[w];
+                }
+            if (i < 0) {
+                s_load = -kInf;  // list exhausted: the reference's for-loop ends
+            } else {
+                assign[b] = -1;
+                if (ejected) ejected[b] = 1;
+                blk[i] = -1;
+                s_load = f64_sub(load, mass[b]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // repair waves over topological levels
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_repair_level(int32_t *__restrict__ assign, int B,
@@ -1266,6 +1372,57 @@ int pp_repair(pp_ctx *c, int32_t *assign, int32_t P, int32_t mode, uint8_t *unmi
         CUDA_TRY(cudaMemcpyAsync(assign, da, sizeof(int32_t) * (size_t)P * B, cudaMemcpyDeviceToHost, st));
         if (unmined_out) CUDA_TRY(cudaMemcpyAsync(unmined_out, du, (size_t)P * B, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return PP_OK;
+}
+
+int pp_eject(pp_ctx *c, int32_t *assign, int32_t P, const double *mean_grade, double destroy_fraction,
+             uint8_t *ejected_out, int32_t mem, void *stream) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (P < 0 || (P > 0 && (!assign || !mean_grade))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if (!(destroy_fraction >= 0.0)) return fail(PP_ERR_INVALID_ARGS, "destroy_fraction must be >= 0");
+    if (P == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B, T = c->T;
+    int32_t *da = assign;
+    uint8_t *du = ejected_out;
+    const double *dg = mean_grade;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_assign.ensure(sizeof(int32_t) * (size_t)P * B));
+        TRY(c->h_d2.ensure(sizeof(double) * (size_t)B));
+        CUDA_TRY(cudaMemcpyAsync(c->h_assign.ptr, assign, sizeof(int32_t) * (size_t)P * B, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(c->h_d2.ptr, mean_grade, sizeof(double) * B, cudaMemcpyHostToDevice, st));
+        da = c->h_assign.as<int32_t>();
+        dg = c->h_d2.as<double>();
+        if (ejected_out) {
+            TRY(c->h_o5.ensure((size_t)P * B));
+            du = c->h_o5.as<uint8_t>();
+        }
+    }
+    if (du) CUDA_TRY(cudaMemsetAsync(du, 0, (size_t)P * B, st));
+    TRY(c->pm_batch.ensure(sizeof(double) * (size_t)P * T));
+    TRY(c->ej_count.ensure(sizeof(int32_t) * T));
+    TRY(c->ej_key.ensure(sizeof(double) * (size_t)T * B));
+    TRY(c->ej_blk.ensure(sizeof(int32_t) * (size_t)T * B));
+    TRY(run_period_mass(c, da, P, c->pm_batch.as<double>(), st));
+    for (int p = 0; p < P; p++) {  // one schedule at a time: the lists use [T][B] scratch
+        int32_t *ap = da + (size_t)p * B;
+        const double *pmp = c->pm_batch.as<double>() + (size_t)p * T;
+        CUDA_TRY(cudaMemsetAsync(c->ej_count.ptr, 0, sizeof(int32_t) * T, st));
+        k_eject_list<<<(B + 255) / 256, 256, 0, st>>>(ap, B, T, c->rows.as<BlockRow>(), c->adj.as<int32_t>(), pmp,
+                                                      c->cap.as<double>(), dg, destroy_fraction,
+                                                      c->ej_count.as<int32_t>(), c->ej_key.as<double>(),
+                                                      c->ej_blk.as<int32_t>());
+        k_eject_apply<<<T, 512, 0, st>>>(ap, B, c->mass.as<double>(), pmp, c->cap.as<double>(), destroy_fraction,
+                                         c->ej_count.as<int32_t>(), c->ej_key.as<double>(), c->ej_blk.as<int32_t>(),
+                                         du ? du + (size_t)p * B : nullptr);
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        CUDA_TRY(cudaMemcpyAsync(assign, da, sizeof(int32_t) * (size_t)P * B, cudaMemcpyDeviceToHost, st));
+        if (ejected_out) CUDA_TRY(cudaMemcpyAsync(ejected_out, du, (size_t)P * B, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(stream_wait(st));
     }
     return PP_OK;
 }

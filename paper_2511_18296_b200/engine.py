@@ -315,6 +315,28 @@ class Engine:
         check(self.lib.pp_repair(self._h, ptr(a), a.shape[0], m, ptr(u), _lib.PP_MEM_HOST, None))
         return a, u
 
+    def eject(self, assign_batch, mean_grade, destroy_fraction=0.0):
+        """lns_repair's over-capacity ejection (hybrid.py:213-235), after the unmine fixpoint.
+        Returns (assign int32 [P][B], ejected flags uint8 [P][B])."""
+        bm = self._need_bm()
+        a = np.array(np.atleast_2d(np.asarray(assign_batch)), dtype=np.int32, order="C")
+        if a.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("schedule length does not match the instance")
+        g = np.ascontiguousarray(mean_grade, dtype=np.float64)
+        if g.size != bm.n_blocks:
+            raise ShapeMismatch("mean_grade length does not match the instance")
+        e = np.empty(a.shape, np.uint8)
+        check(self.lib.pp_eject(self._h, ptr(a), a.shape[0], ptr(g), float(destroy_fraction), ptr(e),
+                                _lib.PP_MEM_HOST, None))
+        return a, e
+
+    def lns_destroy(self, assign_batch, mean_grade, destroy_fraction=0.0):
+        """The destroy step of lns_repair (hybrid.py:199-235): unmine fixpoint, then ejection.
+        Returns (assign [P][B], pool additions [P][B] (fixpoint-unmined or ejected))."""
+        a, u = self.repair(assign_batch, mode="unmine", unmined=True)
+        a, e = self.eject(a, mean_grade, destroy_fraction)
+        return a, (u | e)
+
     def reduce_best_device(self, records, out, stream=None):
         """Ordered argmax over n 16-byte pp_best records (device tensors)."""
         n = records.numel() * records.element_size() // 16

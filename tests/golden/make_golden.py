@@ -193,6 +193,19 @@ def small_cases(store):
                        economics=inst.economics)
         fix = [lns_repair(big, Schedule(r), [], scen, None, max_iters=0).assignment for r in rand]
         store[p + "rand_unmine"] = np.array(fix, dtype=np.int32)
+        # lns_repair's destroy step with the real capacities: unmine fixpoint + over-capacity
+        # ejection (hybrid.py:199-235), destroy_fraction 0 and 0.3; a result equal to the input
+        # while the fixpoint changed something would be the violation guard's revert (skipped)
+        store[p + "mean_grade"] = scen.grades.mean(axis=0)
+        for tag, df in (("d0", 0.0), ("d3", 0.3)):
+            outs = []
+            for r in rand:
+                out = lns_repair(inst, Schedule(r), [], scen, None, max_iters=0, destroy_fraction=df).assignment
+                before = check_feasible(inst, Schedule(r)).violation
+                after = check_feasible(inst, Schedule(out)).violation
+                assert after <= before, "violation guard reverted a destroy step"
+                outs.append(out)
+            store[p + f"rand_destroy_{tag}"] = np.array(outs, dtype=np.int32)
 
 
 def _feat(alt=0.5, struct=0.5, dist=1.0):
@@ -299,6 +312,25 @@ def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
         reps.append(a.astype(np.int32))
     store[p + "repair_in"] = np.array(srcs)
     store[p + "repair_out"] = np.array(reps)
+    if n <= 4000:  # lns_repair's destroy step (hybrid.py:199-235) on overloaded schedules
+        store[p + "mean_grade"] = scen.grades.mean(axis=0)
+        ins = []
+        tm = int(full.max())  # the last period the full schedule uses
+        for merge in (((tm, tm - 1),), ((tm - 1, tm - 2), (tm, tm - 2)), ((1, 0),)):
+            a = full.copy()  # merging a period into an earlier one keeps precedence, overloads it
+            for src, dst in merge:
+                a[a == src] = dst
+            ins.append(a.astype(np.int32))
+        a = full.copy()  # plus a precedence-damaged one (the fixpoint runs first)
+        mined = np.nonzero(a >= 0)[0]
+        pick = rng.choice(mined, size=len(mined) // 10, replace=False)
+        a[pick] = rng.integers(0, max(1, T // 3), size=pick.size)
+        ins.append(a.astype(np.int32))
+        store[p + "destroy_in"] = np.array(ins)
+        for tag, df in (("d0", 0.0), ("d25", 0.25)):
+            outs = [lns_repair(inst, Schedule(a.astype(int)), [], scen, None, max_iters=0,
+                               destroy_fraction=df).assignment.astype(np.int32) for a in ins]
+            store[p + f"destroy_{tag}"] = np.array(outs)
 
 
 def main():

@@ -427,3 +427,31 @@ def test_sparse_pairs_c2_and_device_mode(oracle_lib):
           "exp": out["pair_exp"][:n].cpu().numpy(), "cvar": out["pair_cvar"][:n].cpu().numpy()}
     _pairs_match_dense(pr, ref)
     eng.close()
+
+
+@pytest.mark.parametrize("case", [0, 5, 11, 19])
+def test_destroy_step_small(small, case):
+    """lns_repair's unmine fixpoint + over-capacity ejection (hybrid.py:199-235) against the
+    reference's lns_repair(max_iters=0) on random schedules, destroy_fraction 0 and 0.3."""
+    p = f"kd{case}_"
+    eng = Engine.from_tables(bm_from(small, p), None)
+    for tag, df in (("d0", 0.0), ("d3", 0.3)):
+        out, _ = eng.lns_destroy(small[p + "rand"], small[p + "mean_grade"], df)
+        assert np.array_equal(out, small[p + f"rand_destroy_{tag}"]), tag
+    eng.close()
+
+
+def test_destroy_step_c1(oracle_lib):
+    st = load("c1")
+    c = config("C1")
+    eng = Engine.from_tables(c["bm"], None)
+    o = oracle_lib.Oracle(c["bm"])
+    ins = st["C1_destroy_in"]
+    for tag, df in (("d0", 0.0), ("d25", 0.25)):
+        out, pool = eng.lns_destroy(ins, st["C1_mean_grade"], df)  # all schedules in one batch
+        assert np.array_equal(out, st[f"C1_destroy_{tag}"]), tag
+        for k in range(ins.shape[0]):
+            f, u = o.unmine_fixpoint(ins[k])
+            ref, e = o.eject(f, st["C1_mean_grade"], df)
+            assert np.array_equal(pool[k], (u | e)), (tag, k)
+    eng.close()

@@ -73,6 +73,28 @@ def test_feasibility_and_repair(oracle_lib, case):
         assert np.array_equal(o.precedence_repair(a), st[p + "rand_repair"][k])
         fixed, _ = o.unmine_fixpoint(a)
         assert np.array_equal(fixed, st[p + "rand_unmine"][k])
+        # lns_repair's destroy step with the real capacities (hybrid.py:199-235)
+        for tag, df in (("d0", 0.0), ("d3", 0.3)):
+            f2, _ = o.unmine_fixpoint(a)
+            out, _ = o.eject(f2, st[p + "mean_grade"], df)
+            assert np.array_equal(out, st[p + f"rand_destroy_{tag}"][k]), (tag, k)
+
+
+def test_destroy_step_c1(oracle_lib):
+    """Unmine fixpoint + over-capacity ejection on overloaded 4k-block schedules, against the
+    reference's lns_repair(max_iters=0) (hybrid.py:199-235)."""
+    st = load("c1")
+    c = config("C1")
+    o = oracle_lib.Oracle(c["bm"])
+    ejected_any = False
+    for k in range(st["C1_destroy_in"].shape[0]):
+        a = st["C1_destroy_in"][k]
+        for tag, df in (("d0", 0.0), ("d25", 0.25)):
+            f, _ = o.unmine_fixpoint(a)
+            out, ej = o.eject(f, st["C1_mean_grade"], df)
+            assert np.array_equal(out, st[f"C1_destroy_{tag}"][k]), (k, tag)
+            ejected_any |= bool(ej.any())
+    assert ejected_any
 
 
 def test_hand_cases(oracle_lib):
