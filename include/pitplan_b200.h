@@ -196,6 +196,10 @@ PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode
  * NULL) marks the ejected blocks. */
 PP_API int pp_eject(pp_ctx *ctx, int32_t *assign, int32_t n_sched, const double *mean_grade, double destroy_fraction,
              uint8_t *ejected_out, int32_t mem, void *stream);
+/* spatial[B] = geological_consistency of every block (uncertainty.py:185-191, the factor
+ * pp_set_geology computed on the device), e.g. for lns_repair's realism fallback
+ * (hybrid.py:238-244, 256-260). */
+PP_API int pp_get_spatial(pp_ctx *ctx, double *spatial_out, int32_t mem, void *stream);
 /* Ordered reduction of n pp_best records (e.g. one per GPU after an all-gather) with the
  * selection order of evaluate.py:404-409; records with block < 0 are "none".  This is the
  * deterministic "allreduce-argmax" step of multi-GPU evaluation. */

@@ -1427,6 +1427,19 @@ int pp_eject(pp_ctx *c, int32_t *assign, int32_t P, const double *mean_grade, do
     return PP_OK;
 }
 
+int pp_get_spatial(pp_ctx *c, double *out, int32_t mem, void *stream) {
+    if (!c || !c->have_instance || !c->have_spatial) return fail(PP_ERR_STATE, "pp_set_instance and pp_set_geology first");
+    if (!out) return fail(PP_ERR_INVALID_ARGS, "out is NULL");
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    // BlockRow.spatial: one strided 2-D copy (pitch 32 bytes -> 8 bytes)
+    const char *src = reinterpret_cast<const char *>(c->rows.ptr) + offsetof(BlockRow, spatial);
+    CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(double), src, sizeof(BlockRow), sizeof(double), c->B,
+                               mem == PP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
+    if (mem == PP_MEM_HOST) CUDA_TRY(stream_wait(st));
+    return PP_OK;
+}
+
 int pp_reduce_best(pp_ctx *c, const pp_best *recs, int32_t n, pp_best *out, int32_t mem, void *stream) {
     if (!c || n < 0 || (n > 0 && !recs) || !out) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
     TRY(use_device(c));

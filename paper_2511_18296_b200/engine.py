@@ -315,6 +315,13 @@ class Engine:
         check(self.lib.pp_repair(self._h, ptr(a), a.shape[0], m, ptr(u), _lib.PP_MEM_HOST, None))
         return a, u
 
+    def spatial(self) -> np.ndarray:
+        """geological_consistency of every block (uncertainty.py:185-191), as computed on the device."""
+        bm = self._need_bm()
+        out = np.empty(bm.n_blocks, np.float64)
+        check(self.lib.pp_get_spatial(self._h, ptr(out), _lib.PP_MEM_HOST, None))
+        return out
+
     def eject(self, assign_batch, mean_grade, destroy_fraction=0.0):
         """lns_repair's over-capacity ejection (hybrid.py:213-235), after the unmine fixpoint.
         Returns (assign int32 [P][B], ejected flags uint8 [P][B])."""

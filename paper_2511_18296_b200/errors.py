@@ -36,6 +36,14 @@ class ShapeMismatch(PitplanError, _base("ShapeMismatch", Exception)):
     """Array dimensions disagree with the instance (errors.py:24)."""
 
 
+class RepairStalled(PitplanError, _base("RepairStalled", Exception)):
+    """No feasible insertion exists; carries the best-effort schedule (errors.py:52-57)."""
+
+    def __init__(self, message, schedule=None):
+        super().__init__(message)
+        self.schedule = schedule
+
+
 class DeviceError(PitplanError):
     """The sm_100a extension reported a CUDA failure (no CPU fallback exists)."""
 

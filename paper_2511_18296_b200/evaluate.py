@@ -4,6 +4,9 @@
     check_feasible                 pitplan/evaluate.py:82-105
     precedence_repair_pass         pitplan/hybrid.py:493-510  (`_precedence_repair_pass`)
     unmine_fixpoint                pitplan/hybrid.py:199-211  (first step of `lns_repair`)
+    lns_repair                     pitplan/hybrid.py:169-274  (destroy step and every insertion
+                                   evaluation on the device; candidate ranking by the
+                                   reference's own neighbour-similarity helper)
 
 Same signatures, argument meaning, return types and error behaviour as the
 reference; the work runs in the sm_100a kernels of csrc/pitplan_b200.cu through the
@@ -48,7 +51,7 @@ def _cache() -> OrderedDict:
 
 
 class _Entry:
-    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params")
+    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params", "rook")
 
     def __init__(self, instance, bm, engine):
         self.instance = instance  # strong ref: keeps id(instance) from being reused
@@ -57,6 +60,7 @@ class _Entry:
         self.scen_key = None
         self.scen_refs = None
         self.params = None
+        self.rook = None
 
 
 def _device() -> int:
@@ -215,6 +219,80 @@ def unmine_fixpoint(instance, assign: np.ndarray):
     out, u = e.engine.repair(np.asarray(assign)[None, :], mode="unmine", unmined=True)
     assign[...] = out[0]
     return np.nonzero(u[0])[0]
+
+
+def lns_repair(
+    instance,
+    schedule,
+    unassigned,
+    scenarios,
+    sigma,
+    max_iters: int = 100,
+    seed: int = 0,
+    realism_threshold: float = 0.5,
+    destroy_fraction: float = 0.0,
+    candidate_width: int = 16,
+    strict: bool = False,
+    only_positive: bool = False,
+    net_mining_cost: bool = False,
+    params=None,
+):
+    """Destroy-and-reinsert repair (hybrid.py:169-274), same signature and result.
+
+    Destroy (hybrid.py:199-235): the unmine fixpoint and the over-capacity ejection run on the
+    device (pp_repair + pp_eject, bit-exact period masses).  Repair (238-263): the geological
+    consistency of every block comes from the device (pp_get_spatial) instead of 50k Python
+    calls; each insertion round evaluates its candidates with the device kernel; the ranking
+    by scheduled-neighbour similarity and the realism fallback are the reference's own code.
+    The reference's helpers are restated in model.py (rook_neighbor_map,
+    scheduled_neighbor_similarity), so pitplan is not required."""
+    from .errors import RepairStalled
+    from .model import rook_neighbor_map, scheduled_neighbor_similarity
+
+    e = _entry(instance)
+    _bind_scenarios(e, scenarios, sigma, params)
+    sched = schedule.copy()
+    before = check_feasible(instance, sched)
+    pool: set[int] = {int(b) for b in unassigned}
+    grades = getattr(scenarios, "grades", None)
+    if grades is None:
+        raise InvalidArgs("lns_repair needs scenarios with grades[S][B] (mean grade ranking, hybrid.py:214)")
+    mean_grade = np.asarray(grades).mean(axis=0)
+    a, added = e.engine.lns_destroy(np.asarray(sched.assignment)[None, :], mean_grade, destroy_fraction)
+    sched.assignment[...] = a[0]
+    pool.update(int(b) for b in np.nonzero(added[0])[0])
+
+    spatial = e.engine.spatial()
+    rook = e.rook if e.rook is not None else rook_neighbor_map(e.bm)
+    e.rook = rook
+    iters = 0
+    stalled = False
+    while pool and iters < max_iters:
+        sims = scheduled_neighbor_similarity(sched.assignment, pool, mean_grade, rook)
+        ranked = sorted(pool, key=lambda b: (-sims[b], b))
+        cand = ranked[:candidate_width]
+        moves, best = evaluate_candidates_parallel(
+            instance, sched, cand, scenarios, None, sigma,
+            net_mining_cost=net_mining_cost, params=params,
+        )
+        if best is None or (only_positive and best.improvement <= 0.0):
+            stalled = best is None
+            break
+        chosen = best
+        if spatial[best.block] < realism_threshold:
+            feasible = [m for m in moves if m.feasible]
+            feasible.sort(key=lambda m: (-spatial[m.block], m.block))
+            chosen = feasible[0]
+        sched.assignment[chosen.block] = chosen.period
+        pool.discard(chosen.block)
+        iters += 1
+
+    after = check_feasible(instance, sched)
+    if after.violation > before.violation:
+        return schedule.copy()
+    if stalled and strict:
+        raise RepairStalled("no feasible insertion for remaining blocks", schedule=sched)
+    return sched
 
 
 def clear_cache() -> None:

@@ -24,8 +24,9 @@ _PATCHES = {
         "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
         "check_feasible": _ev.check_feasible,
         "_precedence_repair_pass": _ev.precedence_repair_pass,
+        "lns_repair": _ev.lns_repair,
     },
-    "pitplan.colgen": {"check_feasible": _ev.check_feasible},
+    "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair},
     "pitplan.saa": {},
     "pitplan": {"check_feasible": _ev.check_feasible},
 }

@@ -228,6 +228,7 @@ class ScenarioTables:
 
     vmax: np.ndarray
     sigma: np.ndarray | None
+    grades: np.ndarray | None = None  # [S][B], optional (lns_repair's mean grade, hybrid.py:214)
 
     def __post_init__(self):
         self.vmax = np.ascontiguousarray(self.vmax, dtype=np.float64)
@@ -246,7 +247,7 @@ class ScenarioTables:
         use_stored = bool(getattr(scenarios, "meta", {}).get("use_stored_values"))
         vmax = scenario_values(bm, None if use_stored else scenarios.grades, use_stored)
         sig = None if sigma is None else np.asarray(sigma.sigma, dtype=np.float64)
-        return cls(vmax=vmax, sigma=sig)
+        return cls(vmax=vmax, sigma=sig, grades=getattr(scenarios, "grades", None))
 
 
 def cvar_k(n_scenarios: int) -> int:
@@ -254,3 +255,25 @@ def cvar_k(n_scenarios: int) -> int:
     import math
 
     return max(1, math.ceil(0.1 * n_scenarios))
+
+
+def rook_neighbor_map(bm: BlockModel) -> dict:
+    """`_rook_neighbor_map` (hybrid.py:159-166): rook neighbours of every block, in the order
+    of `rook_weights` (uncertainty.py)."""
+    from .synth import rook_pairs
+
+    ii, jj = rook_pairs(bm.coords)
+    out: dict[int, list[int]] = {}
+    for i, j in zip(ii.tolist(), jj.tolist()):
+        out.setdefault(int(i), []).append(int(j))
+    return out
+
+
+def scheduled_neighbor_similarity(assign: np.ndarray, blocks, mean_grade: np.ndarray, rook: dict) -> dict:
+    """`_scheduled_neighbor_similarity` (hybrid.py:142-156): minus the mean absolute grade
+    difference to the already-scheduled rook neighbours; -inf without one."""
+    sims = {}
+    for b in blocks:
+        vals = [abs(mean_grade[b] - mean_grade[j]) for j in rook.get(b, ()) if assign[j] != UNMINED]
+        sims[b] = -float(np.mean(vals)) if vals else -np.inf
+    return sims

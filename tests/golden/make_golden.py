@@ -197,6 +197,14 @@ def small_cases(store):
         # ejection (hybrid.py:199-235), destroy_fraction 0 and 0.3; a result equal to the input
         # while the fixpoint changed something would be the violation guard's revert (skipped)
         store[p + "mean_grade"] = scen.grades.mean(axis=0)
+        store[p + "grades"] = scen.grades
+        # whole lns_repair runs (destroy + similarity-ranked insertions, hybrid.py:169-274)
+        for tag, kw in (("a", dict(max_iters=50)),
+                        ("b", dict(max_iters=50, destroy_fraction=0.3, net_mining_cost=True)),
+                        ("c", dict(max_iters=50, realism_threshold=0.95, candidate_width=4))):
+            outs = [lns_repair(inst, Schedule(r), [0, 5], scen, sigma, **kw).assignment.astype(np.int32)
+                    for r in rand[:2]]
+            store[p + f"lns_{tag}"] = np.array(outs)
         for tag, df in (("d0", 0.0), ("d3", 0.3)):
             outs = []
             for r in rand:
@@ -331,6 +339,10 @@ def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
             outs = [lns_repair(inst, Schedule(a.astype(int)), [], scen, None, max_iters=0,
                                destroy_fraction=df).assignment.astype(np.int32) for a in ins]
             store[p + f"destroy_{tag}"] = np.array(outs)
+        # a whole lns_repair run at 4k blocks (40 insertion rounds after the destroy step)
+        store[p + "grades"] = scen.grades
+        store[p + "lns"] = lns_repair(inst, Schedule(ins[0].astype(int)), [], scen, sigma, max_iters=40,
+                                      destroy_fraction=0.1).assignment.astype(np.int32)
 
 
 def main():

@@ -455,3 +455,36 @@ def test_destroy_step_c1(oracle_lib):
             ref, e = o.eject(f, st["C1_mean_grade"], df)
             assert np.array_equal(pool[k], (u | e)), (tag, k)
     eng.close()
+
+
+@pytest.mark.parametrize("case", [0, 3, 8, 14, 19])
+def test_lns_repair_dropin_small(small, case):
+    """The whole lns_repair (hybrid.py:169-274) through the drop-in: device destroy step and
+    insertion evaluations, restated similarity ranking; equal to the reference's runs."""
+    from paper_2511_18296_b200 import evaluate as dropin
+    from paper_2511_18296_b200.model import Schedule
+
+    p = f"kd{case}_"
+    bm = bm_from(small, p)
+    tables = ScenarioTables(small[p + "vmax"], small[p + "sigma"], grades=small[p + "grades"])
+    variants = {"a": dict(max_iters=50),
+                "b": dict(max_iters=50, destroy_fraction=0.3, net_mining_cost=True),
+                "c": dict(max_iters=50, realism_threshold=0.95, candidate_width=4)}
+    for tag, kw in variants.items():
+        for k in range(2):
+            out = dropin.lns_repair(bm, Schedule(small[p + "rand"][k]), [0, 5], tables, True, **kw)
+            assert np.array_equal(out.assignment, small[p + f"lns_{tag}"][k]), (tag, k)
+    dropin.clear_cache()
+
+
+def test_lns_repair_dropin_c1():
+    from paper_2511_18296_b200 import evaluate as dropin
+    from paper_2511_18296_b200.model import Schedule
+
+    st = load("c1")
+    c = config("C1")
+    tables = ScenarioTables(c["vmax"], c["sigma"], grades=st["C1_grades"])
+    out = dropin.lns_repair(c["bm"], Schedule(st["C1_destroy_in"][0]), [], tables, True, max_iters=40,
+                            destroy_fraction=0.1)
+    assert np.array_equal(out.assignment, st["C1_lns"])
+    dropin.clear_cache()

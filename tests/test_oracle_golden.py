@@ -181,3 +181,40 @@ def test_enpv_table(oracle_lib):
     c = config("C1")
     o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
     assert same(o.enpv_table(True), load("c1")["C1_enpv"])
+
+
+def test_restated_lns_helpers_match_reference():
+    """model.rook_neighbor_map / scheduled_neighbor_similarity against hybrid.py:142-166
+    (skipped where the reference package is not importable, e.g. on the GPU box)."""
+    import os
+    import sys
+
+    ref_src = "/root/reference/pkg/src"  # present in the build container only
+    added = os.path.isdir(ref_src) and ref_src not in sys.path
+    if added:
+        sys.path.insert(0, ref_src)
+    try:
+        _restated_helpers_check()
+    finally:
+        if added:
+            sys.path.remove(ref_src)
+
+
+def _restated_helpers_check():
+    hybrid = pytest.importorskip("pitplan.hybrid")
+    from pitplan.blockmodel import generate_synthetic
+    from pitplan.evaluate import Schedule as RefSchedule
+
+    from paper_2511_18296_b200.model import BlockModel, rook_neighbor_map, scheduled_neighbor_similarity
+
+    inst = generate_synthetic(60, (5, 4, 3), 4, 1, seed=5, n_rock_types=1)
+    bm = BlockModel.from_instance(inst)
+    ref = hybrid._rook_neighbor_map(inst)
+    mine = rook_neighbor_map(bm)
+    assert {k: v for k, v in ref.items()} == mine
+    rng = np.random.default_rng(3)
+    a = rng.integers(-1, 4, size=60)
+    g = rng.random(60)
+    pool = list(range(0, 60, 3))
+    assert hybrid._scheduled_neighbor_similarity(inst, RefSchedule(a), pool, g, ref) == \
+        scheduled_neighbor_similarity(a, pool, g, mine)
