@@ -87,12 +87,19 @@ constexpr int NBR_W = 32;  // neighbour slots per block (padded table, one 128-b
 constexpr int NBR_SUCC = 1 << 30;  // successor tag in the neighbour table; -1 = padding
 
 struct WarpLayout {  // per-warp slice of dynamic shared memory (byte offsets)
-    int vrow, cost, val, ex, cv, total;
+    int vrow, cost, val, ex, cv, big, total;
 };
 // dynamic shared memory: [sigma S x T (statistics)] [NW warp slices]
 static __host__ __device__ inline int sig_bytes(int S, int T, bool stats) { return stats ? ((8 * S * T + 15) & ~15) : 0; }
 static __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool stats, bool need_vrow, bool net) {
+// bign: warp-per-move statistics (KC < 0): per-scenario deltas padded to a power of two + leaf sums
+static __host__ __device__ inline int big_pow2(int S) {
+    int n = 32;
+    while (n < S) n <<= 1;
+    return n;
+}
+static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool stats, bool need_vrow, bool net,
+                                                         int bign = 0) {
     WarpLayout L;
     int o = 0;
     L.vrow = o;
@@ -105,6 +112,8 @@ static __host__ __device__ inline WarpLayout warp_layout(int T, int Sp, bool sta
     o += stats ? align16(8 * CPW * T) : 0;
     L.cv = o;
     o += stats ? align16(8 * CPW * T) : 0;
+    L.big = o;
+    o += bign ? align16(8 * (bign + kMaxLeaves)) : 0;
     L.total = o;
     return L;
 }
@@ -161,12 +170,13 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool net = p.flags & PP_NET_MINING_COST;
     const bool literal = p.flags & PP_LITERAL_VALUE;
-    constexpr bool STATS_T = KC > 0;
+    constexpr bool STATS_T = KC != 0;  // KC > 0: pooled thread per move, top-KC in registers;
+                                       // KC < 0: warp per move, bitonic sort (k > 8 or S > 128)
     const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar || p.n_pairs);
     const bool need_vrow = stats || (!literal && p.scen >= 0);
     const bool want_unit = !literal && p.scen < 0;
     const bool want_trace = p.trace_val || p.trace_feas;
-    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow, net);
+    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow, net, (KC < 0 && stats) ? big_pow2(S) : 0);
     const int sigb = sig_bytes(S, T, stats);
     double *s_sig = reinterpret_cast<double *>(wv_dyn);
     unsigned char *wslices = wv_dyn + sigb;
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     // ---- statistics of the precedence-feasible (candidate, period) pairs, before the
     //      period masses are known (overlaps the period-mass kernel); capacity only
     //      removes pairs, so the outputs below select from these ----
-    if constexpr (STATS_T) {
+    if constexpr (KC > 0) {
         if (stats) {
             // CTA-wide pool of the pairs, one thread per pair: a warp holds ~9 pairs at C2, a CTA
             // ~70, so pooling keeps ~3x more of each warp's lanes busy than per-warp lists
@@ -368,6 +378,109 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
         if (b[j] >= 0 && bt != INT_MAX) {
             const Best cb{bv, b[j], bt};
             if (better(cb, wbest)) wbest = cb;
+        }
+    }
+    // ---- KC < 0: statistics of the feasible moves, one warp per move (after the capacity
+    //      test: with many scenarios the statistics dominate, so only feasible moves pay) ----
+    if constexpr (KC < 0) {
+        if (stats) {
+            const int P2 = big_pow2(S);
+            double *vb = reinterpret_cast<double *>(wbase + L.big);
+            double *lv = vb + P2;
+            const int *P = p.plan;
+            const int nleaf = __ldg(P + 1);
+            const int kq = p.cvar_k;
+            for (int j = 0; j < CPW; j++) {
+                const int ci = warp * CPW + j;
+                const int ab = s_cab[ci];
+                const double sp = s_csp[ci];
+                const bool mined = ab >= 0;
+                const int abc = mined ? ab : 0;
+                const double d_ab = __ldg(p.disc + abc);
+                const double dc_ab = net ? f64_mul(d_ab, w_cost[j * T + abc]) : 0.0;
+                const double *rowb = w_vrow + (size_t)j * Sp;
+                for (unsigned mm = okm[j]; mm; mm &= mm - 1) {  // warp-uniform
+                    const int t = __ffs(mm) - 1;
+                    const double d_t = __ldg(p.disc + t);
+                    const double dc_t = net ? f64_mul(d_t, w_cost[j * T + t]) : 0.0;
+                    for (int s_ = lane; s_ < P2; s_ += 32) {
+                        double v = kInf;  // padding sorts last
+                        if (s_ < S) {
+                            const double x = rowb[s_];
+                            const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
+                            const double vo =
+                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
+                            v = f64_sub(vn, vo);
+                            if constexpr (SCEN) p.scen_delta[((size_t)(cw + j) * S + s_) * T + t] = (float)v;
+                        }
+                        vb[s_] = v;
+                    }
+                    __syncwarp();
+                    // expected delta: numpy pairwise over d[0..S) (the plan's leaves, 8 lanes each)
+                    for (int l0 = 0; l0 < nleaf; l0 += 4) {
+                        const int l = l0 + (lane >> 3), sub = lane & 7;
+                        const bool act = l < nleaf;
+                        const int ls = act ? __ldg(P + 2 + l) : 0, len = act ? __ldg(P + 2 + kMaxLeaves + l) : 0;
+                        const int nm = len >> 3;
+                        double acc = 0.0;
+                        if (nm > 0) {
+                            acc = vb[ls + sub];
+                            for (int u = 1; u < nm; u++) acc = f64_add(acc, vb[ls + 8 * u + sub]);
+                        }
+                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
+                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
+                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
+                        if (act && sub == 0) {
+                            double r = len >= 8 ? acc : -0.0;
+                            for (int i = len - (len & 7); i < len; i++) r = f64_add(r, vb[ls + i]);
+                            lv[l] = r;
+                        }
+                    }
+                    __syncwarp();
+                    // CVaR10: bitonic sort ascending, then the mean of the k smallest (saa.py:157-164)
+                    for (int k2 = 2; k2 <= P2; k2 <<= 1)
+                        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+                            for (int i = lane; i < P2; i += 32) {
+                                const int q = i ^ jj;
+                                if (q > i) {
+                                    const double a = vb[i], b2 = vb[q];
+                                    if ((a > b2) == ((i & k2) == 0)) {
+                                        vb[i] = b2;
+                                        vb[q] = a;
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    const int kn = kq >> 3;
+                    double cacc = 0.0;
+                    if (lane < 8 && kn > 0) {
+                        cacc = vb[lane];
+                        for (int u = 1; u < kn; u++) cacc = f64_add(cacc, vb[8 * u + lane]);
+                    }
+                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 1));
+                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 2));
+                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 4));
+                    if (lane == 0) {
+                        double r = kq >= 8 ? cacc : -0.0;
+                        for (int i = kq - (kq & 7); i < kq; i++) r = f64_add(r, vb[i]);
+                        w_cv[j * T + t] = f64_div(f64_add(0.0, r), (double)kq);
+                        double stk[8];
+                        int sp_ = 0;
+                        for (int l = 0; l < nleaf; l++) {  // numpy's recursion, post-order
+                            stk[sp_++] = lv[l];
+                            const int nadd = __ldg(P + 2 + 2 * kMaxLeaves + l);
+                            for (int a = 0; a < nadd; a++) {
+                                const double rhs = stk[--sp_];
+                                const double lhs = stk[--sp_];
+                                stk[sp_++] = f64_add(lhs, rhs);
+                            }
+                        }
+                        w_ex[j * T + t] = f64_div(f64_add(0.0, stk[0]), (double)S);
+                    }
+                    __syncwarp();
+                }
+            }
         }
     }
     EV_PROBE(4);
@@ -518,7 +631,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 
     pp_cand_out o = *out;
     const int32_t *dcand = cand;
-    const bool warp_path = T <= 32 && (!stats || S <= 128) && c->nbr.ptr;
+    const bool warp_path = T <= 32 && (!stats || S <= 256) && c->nbr.ptr;
     if (mem == PP_MEM_HOST) {
         if (!warp_path) {  // the warp kernel range-checks the ids itself (reported after the sync)
             int32_t lo = 0, hi = 0;  // branch-free min/max (vectorises)
@@ -607,7 +720,9 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     // fast path: one warp per CPW candidates (k_eval_warp)
     if (warp_path) {
         const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
-        const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0);
+        const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 8 ? 8 : -1;  // -1: warp per move
+        const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
+                                          kcw < 0 ? big_pow2(S) : 0);
         const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32) + sig_bytes(S, T, stats);
         const int per_cta = CPW * (EV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
@@ -624,10 +739,10 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         TRY(set_smem_attr(k_eval_warp<KC, SC>, smem_w));                    \
         TRY(launch_eval(k_eval_warp<KC, SC>, wgrid, smem_w, st, pdl, ep));  \
     }
-        if (kc == 0) PP_WARP(0, false)
-        else if (kc == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }
-        else if (kc == 8) { if (scen) PP_WARP(8, true) else PP_WARP(8, false) }
-        else { if (scen) PP_WARP(128, true) else PP_WARP(128, false) }
+        if (kcw == 0) PP_WARP(0, false)
+        else if (kcw == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }
+        else if (kcw == 8) { if (scen) PP_WARP(8, true) else PP_WARP(8, false) }
+        else { if (scen) PP_WARP(-1, true) else PP_WARP(-1, false) }
 #undef PP_WARP
         goto copy_out;
     }
