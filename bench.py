@@ -329,44 +329,62 @@ def run_gpu(args):
     kms = [s.elapsed_time(e) for s, e in zip(kstarts[:min(args.steps, 200)], kends[:min(args.steps, 200)])]
     k_ms = float(np.mean(kms))
 
+    # e2e through the C ABI with host (pinned) buffers on every rank: H2D schedule + candidates,
+    # both kernels, D2H of the best moves and the sparse statistics; for N > 1 also the 16-byte
+    # per-rank best through NCCL (all-gather + ordered reduce) and back to the host
+    pool = PinnedPool()
+    h_assign = pool.empty(bm.n_blocks, np.int32)
+    h_assign[:] = c["assign"]
+    h_cand = pool.empty(C, np.int32)
+    h_cand[:] = c["cand"]
+    h_out = {"best_t": pool.empty(C, np.int32), "best_val": pool.empty(C, np.float64),
+             "feasible": pool.empty(C, np.uint8), "pair_cand": pool.empty(C * T, np.int32),
+             "pair_period": pool.empty(C * T, np.int32), "pair_exp": pool.empty(C * T, np.float64),
+             "pair_cvar": pool.empty(C * T, np.float64), "n_pairs": pool.empty(1, np.int32)}
+    h_best = pool.empty(2, np.float64)
+    h_best_t = torch.from_numpy(h_best)
+    d_best = torch.empty(2, dtype=torch.float64, device=dev)
+    e2e = []
+    r = None
+    for i in range(args.warmup + min(args.steps, 300)):
+        flush.fill_(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.set_schedule(h_assign)
+        r = eng.eval_candidates(h_cand, None, net=True, pairs=True, out=h_out, validate=False)
+        if world > 1:
+            bv, bb, bt = r["best"] if r["best"] is not None else (-np.inf, -1, -1)
+            h_best[0] = bv
+            h_best.view(np.int32)[2:4] = (bb, bt)
+            d_best.copy_(h_best_t, non_blocking=True)
+            dist.all_gather_into_tensor(gathered, d_best)
+            eng.reduce_best_device(gathered, final, stream=sptr)
+            h_best_t.copy_(final)  # synchronising D2H of the global best
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append(t1 - t0)
+    e2e_t = float(np.median(e2e))
+    if dist is not None:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    h2d = h_assign.nbytes + h_cand.nbytes
+    npairs = int(h_out["n_pairs"][0])
+    d2h = (h_out["best_t"].nbytes + h_out["best_val"].nbytes + h_out["feasible"].nbytes + 16 + 4
+           + npairs * (4 + 4 + 8 + 8))
+    # parity spot check of the timed configuration against the device run
+    assert r["best"] is not None
+    g = out["global"].cpu().numpy()
+    gi = g.view(np.int32)
+    assert (int(gi[2]), int(gi[3]), float(g[0])) == r["best"], "device/host paths disagree"
+    pool.close()
+
     result = None
     if rank == 0:
         hbm, peak_kind = _peaks()
         ab = algorithmic_bytes(c, deg_mean, int(out["n_pairs"].item()))
         achieved = ab["per_launch"] / (k_ms * 1e-3) / 1e9
         value = world * M * S / (t_max * 1e-3)
-
-        # e2e through the C ABI with host (pinned) buffers: H2D schedule + candidates, D2H results
-        pool = PinnedPool()
-        h_assign = pool.empty(bm.n_blocks, np.int32)
-        h_assign[:] = c["assign"]
-        h_cand = pool.empty(C, np.int32)
-        h_cand[:] = c["cand"]
-        h_out = {"best_t": pool.empty(C, np.int32), "best_val": pool.empty(C, np.float64),
-                 "feasible": pool.empty(C, np.uint8), "pair_cand": pool.empty(C * T, np.int32),
-                 "pair_period": pool.empty(C * T, np.int32), "pair_exp": pool.empty(C * T, np.float64),
-                 "pair_cvar": pool.empty(C * T, np.float64), "n_pairs": pool.empty(1, np.int32)}
-        e2e = []
-        for i in range(args.warmup + min(args.steps, 300)):
-            flush.fill_(i)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            eng.set_schedule(h_assign)
-            r = eng.eval_candidates(h_cand, None, net=True, pairs=True, out=h_out, validate=False)
-            t1 = time.perf_counter()
-            if i >= args.warmup:
-                e2e.append(t1 - t0)
-        e2e_t = float(np.median(e2e))
-        h2d = h_assign.nbytes + h_cand.nbytes
-        npairs = int(h_out["n_pairs"][0])
-        d2h = (h_out["best_t"].nbytes + h_out["best_val"].nbytes + h_out["feasible"].nbytes + 16 + 4
-               + npairs * (4 + 4 + 8 + 8))
-        # parity spot check of the timed configuration against the device run
-        assert r["best"] is not None
-        g = out["global"].cpu().numpy()
-        gi = g.view(np.int32)
-        assert (int(gi[2]), int(gi[3]), float(g[0])) == r["best"], "device/host paths disagree"
-        pool.close()
 
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -412,9 +430,11 @@ def run_gpu(args):
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "survey_uncached_bytes_per_launch": ab["survey_uncached"],
             },
-            "e2e": {"value": M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": world * M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_t * 1e3,
-                    "api": "Engine.set_schedule + Engine.eval_candidates (pp_set_schedule/pp_eval_candidates, PP_MEM_HOST, pinned)"},
+                    "api": "Engine.set_schedule + Engine.eval_candidates (pp_set_schedule/pp_eval_candidates, "
+                           "PP_MEM_HOST, pinned)" + (" + NCCL all-gather/reduce of the per-rank best" if world > 1 else ""),
+                    "note": "per rank; max over ranks" if world > 1 else None},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
