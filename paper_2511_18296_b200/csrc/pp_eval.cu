@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     __shared__ int s_cab[EV_THREADS / 32 * CPW], s_cb[EV_THREADS / 32 * CPW], s_wcnt[EV_THREADS / 32];
     __shared__ double s_csp[EV_THREADS / 32 * CPW], s_cm[EV_THREADS / 32 * CPW], s_cu[EV_THREADS / 32 * CPW];
     __shared__ int s_pair[EV_THREADS / 32 * CPW * 32];
+    __shared__ double s_tab[3][32];  // cap, disc, sig_row per period (cp.async at entry)
     constexpr int NW = EV_THREADS / 32;
     constexpr unsigned FULL = 0xffffffffu;
     const int T = p.T, S = p.S, Sp = p.Sp;
@@ -202,6 +203,11 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
     if (stats)  // sigma [S][T] for the pair statistics, staged once per CTA
         for (int e = threadIdx.x; e < S * T; e += EV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+    if (threadIdx.x < T) {
+        cp_async8(&s_tab[0][threadIdx.x], p.cap + threadIdx.x);
+        cp_async8(&s_tab[1][threadIdx.x], p.disc + threadIdx.x);
+        cp_async8(&s_tab[2][threadIdx.x], p.sig_row + threadIdx.x);
+    }
     // per-candidate scalars to shared memory (read by the pair pool and the moves)
     if (lane < CPW) {
         double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
         const int hi = (int)__reduce_min_sync(FULL, (unsigned)hc);
         win[j] = __ballot_sync(FULL, b[j] >= 0 && lane < T && lane >= lo && lane <= hi);
     }
-    if (need_vrow || net || stats) cp_async_wait_all();
+    cp_async_wait_all();
     __syncwarp();
     EV_PROBE(1);
 
@@ -287,10 +293,19 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                 const int ab = s_cab[i], bj = s_cb[i];
                 const double sp = s_csp[i];
                 const int abc = ab >= 0 ? ab : 0;
-                const double d_t = __ldg(p.disc + t), d_ab = __ldg(p.disc + abc);
+                const double d_t = s_tab[1][t], d_ab = s_tab[1][abc];
                 const double *wc = reinterpret_cast<const double *>(wb + L.cost) + jq * T;
                 const double dc_t = net ? f64_mul(d_t, wc[t]) : 0.0;
                 const double dc_ab = net ? f64_mul(d_ab, wc[abc]) : 0.0;
+                {  // the move's kernel value (evaluate.py:379-384), used by the selection below
+                    double unit;
+                    if (literal) unit = f64_mul(s_cm[i], 100.0);
+                    else if (p.scen >= 0) unit = reinterpret_cast<const double *>(wb + L.vrow)[(size_t)jq * Sp + p.scen];
+                    else unit = s_cu[i];
+                    double v = f64_mul(f64_mul(f64_mul(unit, d_t), s_tab[2][t]), sp);
+                    if (net) v = f64_sub(v, dc_t);
+                    reinterpret_cast<double *>(wb + L.val)[jq * 32 + t] = v;
+                }
                 float *sd = SCEN ? p.scen_delta + (size_t)(blockIdx.x * NW * CPW + i) * S * T + t : nullptr;
                 pair_stats<KC, SCEN>(p, S, T, s_sig, reinterpret_cast<double *>(wb + L.vrow) + (size_t)jq * Sp, t, abc,
                                      d_t, dc_t, d_ab, dc_ab, sp, ab >= 0,
@@ -306,12 +321,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     // ---- moves, pm-independent half: value of every window period (evaluate.py:379-384) and
     //      its rank in the reference's selection order (value desc, then period asc: the
     //      strict '>' scan of 387-388 keeps the first maximum; -inf / NaN never selected) ----
-    double cap_t = 0.0, disc_t = 0.0, srow_t = 0.0;
-    if (lane < T) {
-        cap_t = __ldg(p.cap + lane);
-        disc_t = __ldg(p.disc + lane);
-        srow_t = __ldg(p.sig_row + lane);
-    }
+    if (!(KC > 0 && stats)) __syncthreads();  // s_tab (the pooled path passed a CTA barrier already)
     double *w_val = reinterpret_cast<double *>(wbase + L.val);
     unsigned key[CPW];
 #pragma unroll
@@ -319,15 +329,20 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
         const int ci = warp * CPW + j;
         const bool in = (win[j] >> lane) & 1u;
         double v = -kInf;
-        if (in) {
-            double unit;
-            if (literal) unit = f64_mul(s_cm[ci], 100.0);
-            else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
-            else unit = s_cu[ci];
-            v = f64_mul(f64_mul(f64_mul(unit, disc_t), srow_t), s_csp[ci]);
-            if (net) v = f64_sub(v, f64_mul(disc_t, w_cost[j * T + lane]));
+        if (KC > 0 && stats) {
+            if (in) v = w_val[j * 32 + lane];  // computed with the statistics of the move
+        } else {
+            if (in) {
+                const double disc_t = s_tab[1][lane];
+                double unit;
+                if (literal) unit = f64_mul(s_cm[ci], 100.0);
+                else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
+                else unit = s_cu[ci];
+                v = f64_mul(f64_mul(f64_mul(unit, disc_t), s_tab[2][lane]), s_csp[ci]);
+                if (net) v = f64_sub(v, f64_mul(disc_t, w_cost[j * T + lane]));
+            }
+            w_val[j * 32 + lane] = v;
         }
-        w_val[j * 32 + lane] = v;
         const bool valid = in && v > -kInf;
         const unsigned vm = __ballot_sync(FULL, valid);
         __syncwarp();
@@ -357,7 +372,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
         if ((win[j] >> lane) & 1u) {
             double load = f64_add(pm_t, mass);
             if (ab == lane) load = f64_sub(load, mass);
-            ok = !(load > cap_t);
+            ok = !(load > s_tab[0][lane]);
         }
         okm[j] = __ballot_sync(FULL, ok);
         const unsigned kmin = __reduce_min_sync(FULL, ok ? key[j] : 0xffffffffu);
@@ -804,7 +819,7 @@ copy_out:
             int32_t bad_c = 0;
             if (warp_path) add(c->bad_cand.ptr, &bad_c, sizeof(int32_t), 0);
             const bool bad_copy = c->bad_pending && !c->pm_dirty;
-            if (bad_copy) add(c->pm_bad.ptr, c->h_bad, sizeof(int32_t) * 8, 0);
+            if (bad_copy) add(c->pm_bad.ptr, c->h_bad, sizeof(int32_t) * 16, 0);
             if (pairs) {
                 add(o.n_pairs, out->n_pairs, sizeof(int32_t), 0);
                 add(o.pair_cand, out->pair_cand, 0, sizeof(int32_t));

@@ -90,7 +90,7 @@ extern "C" PP_API int pp_debug_pm_probe(unsigned long long *out) {
 #endif
 #ifdef PP_EVAL_PROBE
 #define PMCP(k, j) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[k][blockIdx.x][j] = pm_gtimer(); } while (0)
-#define PMCS(st) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[1][16 + 8 * (st) + blockIdx.x][0] = pm_gtimer(); } while (0)
+#define PMCS(st) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_pm_probe[1][16 + 16 * (st) + blockIdx.x][0] = pm_gtimer(); } while (0)
 #else
 #define PMCS(st) do { } while (0)
 #define PMCP(k, j) do { } while (0)
@@ -660,7 +660,8 @@ __global__ void k_apply_moves(int32_t *assign, int B, int T, const int32_t *bloc
 // Distributed shared memory carries only the counts: its bandwidth (~20 B/clk/SM) is far below
 // L2's, so the masses go through L2.
 // ---------------------------------------------------------------------------------------------
-constexpr int PMC_R = 8;
+constexpr int PMC_R = 8;    // portable cluster size (fallback)
+constexpr int PMC_R16 = 16;  // non-portable: used when the GPU can place a 16-CTA cluster
 constexpr int PMC_THREADS = 1024;
 constexpr int PMC_WARPS = PMC_THREADS / 32;
 constexpr int PMC_MAXT = 16;
@@ -704,8 +705,8 @@ __device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &le
     len = l;
 }
 
-template <int K>
-__global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
+template <int K, int R>  // R CTAs per schedule, one cluster (launch attribute)
+__global__ void __launch_bounds__(PMC_THREADS, 1)
     k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
                  double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init,
                  int32_t *__restrict__ bad) {
@@ -771,15 +772,15 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     cluster_sync_acqrel();  // totals published
     PMCS(1);
     if (warp < T) {  // cross-CTA scan of the totals through distributed shared memory
-        const int v = lane < PMC_R ? ld_dsmem_i32(&h.tot[warp], lane) : 0;
+        const int v = lane < R ? ld_dsmem_i32(&h.tot[warp], lane) : 0;
         int inc = v;
 #pragma unroll
-        for (int o = 1; o < PMC_R; o <<= 1) {
+        for (int o = 1; o < R; o <<= 1) {
             const int y = __shfl_up_sync(FULL, inc, o);
             if (lane >= o) inc += y;
         }
         const int off = __shfl_sync(FULL, inc - v, r);
-        const int n = __shfl_sync(FULL, inc, PMC_R - 1);
+        const int n = __shfl_sync(FULL, inc, R - 1);
         if (lane == 0) {
             h.off[warp] = off;
             h.n[warp] = n;
@@ -797,14 +798,14 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
     cluster_sync_acqrel();  // every block of the schedule is in place (remote totals no longer read)
     PMCP(0, 1);
     // depth-D nodes of the (up to two) periods of this CTA
-    const int q = max(0, (T - r + PMC_R - 1) / PMC_R);
+    const int q = max(0, (T - r + R - 1) / R);
     int Dg[PMC_MAXQ], cntg[PMC_MAXQ];
 #pragma unroll
     for (int g = 0; g < PMC_MAXQ; g++) {
         Dg[g] = 0;
         cntg[g] = 0;
         if (g < q) {
-            const int n = h.n[r + PMC_R * g], m = n >> 3, rem = n & 7;
+            const int n = h.n[r + R * g], m = n >> 3, rem = n & 7;
             int d = 0;
             while (8 * ((m + (1 << d) - 1) >> d) + rem > 128) d++;
             Dg[g] = max(d - 1, 0);
@@ -818,7 +819,7 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
         const bool act = it < nitems;
         const int g = (it >= cntg[0]) ? 1 : 0;
         const int i = act ? it - (g ? cntg[0] : 0) : 0;
-        const int t = r + PMC_R * g;
+        const int t = r + R * g;
         const int n = act ? h.n[t] : 0, m = n >> 3, rem = n & 7, D = g ? Dg[1] : Dg[0];
         int s0, l0;
         pw_node(m, D, i, s0, l0);
@@ -877,21 +878,73 @@ __global__ void __cluster_dims__(PMC_R, 1, 1) __launch_bounds__(PMC_THREADS, 1)
         const int lanes = cnt > 32 ? 32 : cnt;
         for (int o = 1; o < lanes; o <<= 1) v = f64_add(v, __shfl_xor_sync(FULL, v, o));
         if (lane == 0) {
-            const int t = r + PMC_R * g;
+            const int t = r + R * g;
             pm_out[(size_t)p * T + t] = f64_add(0.0, h.n[t] ? v : -0.0);
         }
     }
     PMCP(1, 1);
 }
 
+template <int K, int R>
+static int launch_pm_cluster_r(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
+                               const EvalInit *init, int32_t *bad) {
+    const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(R, np);
+    cfg.blockDim = dim3(PMC_THREADS);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = R;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_pm_cluster<K, R>, d_assign, (const double *)c->mass.as<double>(),
+                                             c->B, c->T, c->compact.as<double>(), d_pm, in, bad);
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "k_pm_cluster launch: %s", cudaGetErrorString(e));
+    return PP_OK;
+}
+
+// 16-CTA clusters halve each CTA's share of the blocks (the kernel is latency-bound on 8 SMs);
+// they need the non-portable opt-in and a GPC with 16 free SMs, probed once per device
+static bool pm_use_r16(int device) {
+    static int cached[64];  // 0 unknown, 1 yes, 2 no
+    if (device < 0 || device >= 64) return false;
+    if (!cached[device]) {
+        bool ok = cudaFuncSetAttribute(k_pm_cluster<4, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                      cudaSuccess &&
+                  cudaFuncSetAttribute(k_pm_cluster<2, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                      cudaSuccess &&
+                  cudaFuncSetAttribute(k_pm_cluster<1, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                      cudaSuccess;
+        if (ok) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(PMC_R16);
+            cfg.blockDim = dim3(PMC_THREADS);
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = PMC_R16;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            ok = cudaOccupancyMaxActiveClusters(&n, k_pm_cluster<4, PMC_R16>, &cfg) == cudaSuccess && n >= 1;
+        }
+        cudaGetLastError();
+        cached[device] = ok ? 1 : 2;
+    }
+    return cached[device] == 1;
+}
+
 template <int K>
 static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
                              const EvalInit *init, int32_t *bad) {
-    const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
-    k_pm_cluster<K><<<dim3(PMC_R, np), PMC_THREADS, 0, st>>>(d_assign, c->mass.as<double>(), c->B, c->T,
-                                                              c->compact.as<double>(), d_pm, in, bad);
-    CUDA_TRY(cudaGetLastError());
-    return PP_OK;
+    // same K per thread with twice the CTAs covers twice the blocks: use K/2 at 16 CTAs
+    if (K > 1 && pm_use_r16(c->device))
+        return launch_pm_cluster_r<(K > 1 ? K / 2 : 1), PMC_R16>(c, d_assign, np, d_pm, st, init, bad);
+    return launch_pm_cluster_r<K, PMC_R>(c, d_assign, np, d_pm, st, init, bad);
 }
 
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st, const EvalInit *init) {
@@ -948,8 +1001,8 @@ bool pm_cluster_path(const pp_ctx *c) { return c->T <= PMC_MAXT && c->B <= PMC_M
 int check_schedule_range(pp_ctx *c, bool copied) {
     if (!c->bad_pending || c->pm_dirty) return PP_OK;  // not range-checked yet
     c->bad_pending = false;
-    if (!copied) CUDA_TRY(cudaMemcpy(c->h_bad, c->pm_bad.ptr, sizeof(int32_t) * PMC_R, cudaMemcpyDeviceToHost));
-    for (int r = 0; r < PMC_R; r++)
+    if (!copied) CUDA_TRY(cudaMemcpy(c->h_bad, c->pm_bad.ptr, sizeof(int32_t) * PMC_R16, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < PMC_R16; r++)
         if (c->h_bad[r]) {
             c->have_sched = false;  // unusable until the next pp_set_schedule
             return fail(PP_ERR_INVALID_ARGS, "schedule has period indices out of range");
@@ -1220,8 +1273,9 @@ int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream)
     c->bad_pending = false;
     if (mem == PP_MEM_HOST && pm_cluster_path(c)) {  // range-checked by k_pm_cluster on the device
         if (!c->pm_bad.ptr) {
-            TRY(c->pm_bad.ensure(sizeof(int32_t) * PMC_R));
-            CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_bad), sizeof(int32_t) * PMC_R,
+            TRY(c->pm_bad.ensure(sizeof(int32_t) * PMC_R16));
+            CUDA_TRY(cudaMemset(c->pm_bad.ptr, 0, sizeof(int32_t) * PMC_R16));
+            CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_bad), sizeof(int32_t) * PMC_R16,
                                    cudaHostAllocPortable | cudaHostAllocMapped));
         }
         c->bad_pending = true;

@@ -30,14 +30,16 @@ for rep in range(4):
     g.replay(); st.synchronize()
 ev = np.zeros((4096, 12), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
 pm = np.zeros((2, 512, 2), np.uint64); lib.pp_debug_pm_probe(pm.ctypes.data); pm = pm.astype(np.int64)
-cl = pm[0, :8, 0].min() > 0
+nr = int((pm[0, :16, 0] > 0).sum())
+cl = nr >= 8
 if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
-    t0 = min(pm[0, :8, 0].min(), ev[:, 0].min())
+    t0 = min(pm[0, :nr, 0].min(), ev[:, 0].min())
     f = lambda x: (x - t0) / 1000
     for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves"]):
-        v = pm[1, 16 + 8 * k:24 + 8 * k, 0]
+        v = pm[1, 16 + 16 * k:32 + 16 * k, 0]
+        v = v[v > 0]
         print(f"  pm {nm:8s} {f(v.min()):.2f}..{f(v.max()):.2f} us")
-    print(f"PM cluster (8 CTAs): start {f(pm[0,:8,0].min()):.2f}..{f(pm[0,:8,0].max()):.2f}  scattered {f(pm[0,:8,1].min()):.2f}..{f(pm[0,:8,1].max()):.2f}  trees done {f(pm[1,:8,1].min()):.2f}..{f(pm[1,:8,1].max()):.2f} us")
+    print(f"PM cluster ({nr} CTAs): start {f(pm[0,:nr,0].min()):.2f}..{f(pm[0,:nr,0].max()):.2f}  scattered {f(pm[0,:nr,1].min()):.2f}..{f(pm[0,:nr,1].max()):.2f}  trees done {f(pm[1,:nr,1].min()):.2f}..{f(pm[1,:nr,1].max()):.2f} us")
 else:
     nch = (c["bm"].n_blocks + 511) // 512
     p1, p2 = pm[0, :nch], pm[1, :T]
