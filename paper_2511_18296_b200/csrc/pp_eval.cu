@@ -559,6 +559,15 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
 }
 
 #ifdef PP_EVAL_PROBE
+__device__ unsigned long long g_stamp[8];
+__global__ void k_stamp(int slot) { g_stamp[slot] = gtimer(); }
+extern "C" PP_API int pp_debug_stamp(void *stream, int slot) {
+    k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(slot);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+extern "C" PP_API int pp_debug_stamps(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_stamp, sizeof(g_stamp)) == cudaSuccess ? 0 : 3;
+}
 extern "C" PP_API int pp_debug_eval_probe(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_ev_probe, sizeof(unsigned long long) * 4096 * 12) == cudaSuccess ? 0 : 3;
 }

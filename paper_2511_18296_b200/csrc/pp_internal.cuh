@@ -550,7 +550,8 @@ inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    static const bool no_pdl = std::getenv("PP_NO_PDL") != nullptr;  // diagnostics: serialise the launches
+    cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
     if (e != cudaSuccess) return fail(PP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return PP_OK;

@@ -794,7 +794,8 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             const int t = tk[k];
             compact[((size_t)p * T + t) * B + h.off[t] + h.cnt[warp][t] + pos[k]] = mk[k];
         }
-    __threadfence();
+    // the cluster barrier's release/acquire orders these global stores for every thread of the
+    // cluster (no separate sequentially consistent fence)
     cluster_sync_acqrel();  // every block of the schedule is in place (remote totals no longer read)
     PMCP(0, 1);
     // depth-D nodes of the (up to two) periods of this CTA

@@ -25,9 +25,21 @@ st.synchronize()
 with torch.cuda.graph(g):
     cs = torch.cuda.current_stream().cuda_stream
     eng.set_schedule_device(assign_d, stream=cs, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=cs)
+lib.pp_debug_stamp.argtypes = [ctypes.c_void_p, ctypes.c_int]; lib.pp_debug_stamps.argtypes = [ctypes.c_void_p]
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 for rep in range(4):
-    flush.fill_(rep); st.synchronize()
-    g.replay(); st.synchronize()
+    flush.fill_(rep)
+    lib.pp_debug_stamp(sp, 0)
+    if "noevents" not in sys.argv: e0.record(st)
+    if "eager" in sys.argv:
+        eng.set_schedule_device(assign_d, stream=sp, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=sp)
+    else:
+        g.replay()
+    if "noevents" not in sys.argv: e1.record(st)
+    lib.pp_debug_stamp(sp, 1)
+    st.synchronize()
+stamps = np.zeros(8, np.uint64); lib.pp_debug_stamps(stamps.ctypes.data); stamps = stamps.astype(np.int64)
+print(f"event elapsed {e0.elapsed_time(e1) * 1000 if 'noevents' not in sys.argv else 0:.2f} us; stamp-to-stamp {(stamps[1] - stamps[0]) / 1000:.2f} us")
 ev = np.zeros((4096, 12), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
 pm = np.zeros((2, 512, 2), np.uint64); lib.pp_debug_pm_probe(pm.ctypes.data); pm = pm.astype(np.int64)
 nr = int((pm[0, :16, 0] > 0).sum())
@@ -50,3 +62,4 @@ else:
 names = ["start", "loads", "values", "pm-wait", "moves", "outputs", "end", "stats", "pooled"]
 for k in range(len(names)):
     print(f"eval {names[k]:9s} min {f(ev[:,k].min()):6.2f}  median {f(np.median(ev[:,k])):6.2f}  max {f(ev[:,k].max()):6.2f} us")
+print(f"stamp before the step {f(stamps[0]):.2f} us, after {f(stamps[1]):.2f} us (relative to the first kernel start)")
