@@ -459,6 +459,76 @@ void or_eject(int32_t B, int32_t T, const int32_t *succ_ptr, const int32_t *succ
     free(ej);
 }
 
+/* ---- relaxed NPV: ScheduleEvaluator.npv_relaxed / per_scenario_npv, single-mode fast path ----
+ * stage-2 (evaluate.py:166-183): blocks of period t sorted by density = v[s,b,0] / m[b] with
+ * np.argsort(-density, kind="stable") (ties keep block order); greedy: while density > 0 and
+ * hours_left > 0: take = min(m, hours_left * rate); total += density * take;
+ * hours_left -= take / rate.  _npv (evaluate.py:222-234): total -= disc[t] * costs[mined, t].sum()
+ * (numpy pairwise), then total += disc[t] * sigma[s,t] * raw / n_s for s in order;
+ * per_scenario_npv (248-258): out[s] += disc[t] * sigma[s,t] * raw - disc[t] * costsum. */
+typedef struct {
+    double d;
+    int32_t k;
+} or_dens;
+static int or_dens_cmp(const void *x, const void *y) {
+    const or_dens *a = (const or_dens *)x, *b = (const or_dens *)y;
+    const double na = -a->d, nb = -b->d;
+    if (na < nb) return -1;
+    if (na > nb) return 1;
+    return (a->k > b->k) - (a->k < b->k);
+}
+static double or_stage2_fast(int64_t n, const int32_t *ids, const double *vrow_s, const double *mass, double hours,
+                             double rate, or_dens *buf) {
+    for (int64_t k = 0; k < n; k++) {
+        buf[k].d = vrow_s[ids[k]] / mass[ids[k]];
+        buf[k].k = (int32_t)k;
+    }
+    qsort(buf, (size_t)n, sizeof(or_dens), or_dens_cmp);
+    double hours_left = hours, total = 0.0;
+    for (int64_t k = 0; k < n; k++) {
+        const double d = buf[k].d;
+        if (d <= 0 || hours_left <= 0) break;
+        const double m = mass[ids[buf[k].k]];
+        const double hr = hours_left * rate;
+        const double take = (hr < m) ? hr : m;
+        total += d * take;
+        hours_left -= take / rate;
+    }
+    return total;
+}
+void or_npv_relaxed(int32_t B, int32_t T, int32_t S, const int32_t *assign, const double *mass, const double *cost,
+                    const double *vmax_sb, const double *sigma_st, const double *disc, const double *plant_hours,
+                    double rate, double *npv_out, double *per_scen_out) {
+    int32_t *ids = (int32_t *)malloc(sizeof(int32_t) * (size_t)(B > 0 ? B : 1));
+    double *buf = (double *)malloc(sizeof(double) * (size_t)(B > 0 ? B : 1));
+    or_dens *db = (or_dens *)malloc(sizeof(or_dens) * (size_t)(B > 0 ? B : 1));
+    double total = 0.0;
+    if (per_scen_out)
+        for (int32_t s = 0; s < S; s++) per_scen_out[s] = 0.0;
+    for (int32_t t = 0; t < T; t++) {
+        int64_t n = 0;
+        for (int32_t b = 0; b < B; b++)
+            if (assign[b] == t) ids[n++] = b;
+        double costv = 0.0;
+        if (n) {
+            for (int64_t k = 0; k < n; k++) buf[k] = cost[(size_t)ids[k] * T + t];
+            const double csum = or_np_sum(buf, n);
+            total -= disc[t] * csum;
+            costv = disc[t] * csum;
+        }
+        for (int32_t s = 0; s < S; s++) {
+            const double raw = n ? or_stage2_fast(n, ids, vmax_sb + (size_t)s * B, mass, plant_hours[t], rate, db) : 0.0;
+            const double sg = sigma_st ? sigma_st[(size_t)s * T + t] : 1.0;
+            total += disc[t] * sg * raw / S;
+            if (per_scen_out) per_scen_out[s] += disc[t] * sg * raw - costv;
+        }
+    }
+    *npv_out = total;
+    free(ids);
+    free(buf);
+    free(db);
+}
+
 /* ---- explicit moves (reassign / unmine / swap) ---------------------------------
  * Reassign move (b, t_new), t_old = assign[b]:
  *   t_new == t_old                 -> not a move (infeasible), as polish skips t == orig

@@ -47,6 +47,7 @@ _SIGS = {
     "or_unmine_fixpoint": (None, [_i32, _i64, _P, _P, _P, _P]),
     "or_enpv_table": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _i32, _P]),
     "or_eject": (None, [_i32, _i32, _P, _P, _P, _P, _P, _f64, _P, _P]),
+    "or_npv_relaxed": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _f64, _P, _P]),
     "or_eval_moves": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                              _P, _P, _P, _P, _i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _i32]),
 }
@@ -235,6 +236,19 @@ class Oracle:
         a = np.array(assign, dtype=np.int32, order="C")
         lib().or_precedence_repair(self.B, _p(self.pp), _p(self.pi), _p(self.order), _p(a))
         return a
+
+    def npv_relaxed(self, assign, plant_hours, rate, use_sigma=True):
+        """ScheduleEvaluator.npv_relaxed / per_scenario_npv on the single-mode fast path
+        (evaluate.py:166-183, 222-258) -> (npv, per_scenario[S])."""
+        a = np.ascontiguousarray(assign, dtype=np.int32)
+        h = np.ascontiguousarray(plant_hours, dtype=np.float64)
+        out = np.zeros(1)
+        ps = np.zeros(self.S)
+        sig = self.sigma if (use_sigma and self.sigma is not None) else None
+        lib().or_npv_relaxed(self.B, self.T, self.S, _p(a), _p(self.mass), _p(self.cost), _p(self.vmax),
+                             _p(sig) if sig is not None else None, _p(self.disc), _p(h), float(rate),
+                             _p(out), _p(ps))
+        return float(out[0]), ps
 
     def eject(self, assign, mean_grade, destroy_fraction=0.0):
         """lns_repair's over-capacity ejection (hybrid.py:213-235) -> (assign, ejected mask)."""

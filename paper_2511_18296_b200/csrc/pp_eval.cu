@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
                 const int e = s_pair[k], i = e >> 8, t = e & 0xff;
                 const int wq = i / CPW, jq = i - wq * CPW;
                 unsigned char *wb = wslices + (size_t)wq * L.total;
-                const int ab = s_cab[i], bj = s_cb[i];
+                const int ab = s_cab[i];
                 const double sp = s_csp[i];
                 const int abc = ab >= 0 ? ab : 0;
                 const double d_t = s_tab[1][t], d_ab = s_tab[1][abc];

@@ -93,6 +93,9 @@ class BlockModel:
     processing_cost_by_mode: tuple = (1.0,)
     n_modes: int = 1
     stored_values: np.ndarray | None = None  # f64[S_builtin, B, O] (blockmodel.py:141-147)
+    plant_hours: np.ndarray | None = None  # f64[T] processing hours per period (blockmodel.py:97)
+    mode_rates: tuple = ()  # throughput rate per operating mode (blockmodel.py:66)
+    n_rock_types: int = 1
     _csr: tuple | None = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -105,6 +108,9 @@ class BlockModel:
         self.coords = np.ascontiguousarray(self.coords, dtype=np.float64).reshape(B, 3)
         for name in ("alteration", "structural", "dist_intrusion", "base_grade"):
             setattr(self, name, np.ascontiguousarray(getattr(self, name), dtype=np.float64))
+        if self.plant_hours is not None:
+            self.plant_hours = np.ascontiguousarray(self.plant_hours, dtype=np.float64).reshape(T)
+        self.mode_rates = tuple(float(r) for r in self.mode_rates)
         if T < 1:
             raise ValidationError("n_periods must be >= 1")
         if self.mass.shape != (B,) or self.capacity.shape != (T,):
@@ -197,7 +203,16 @@ class BlockModel:
             processing_cost_by_mode=tuple(econ.processing_cost_by_mode),
             n_modes=len(inst.modes),
             stored_values=stored,
+            plant_hours=np.asarray(inst.plant_hours, dtype=np.float64),
+            mode_rates=tuple(float(m.rate) for m in inst.modes),
+            n_rock_types=len(inst.rock_types),
         )
+
+    @property
+    def single_mode_fast(self) -> bool:
+        """The stage-2 fast path of ScheduleEvaluator (evaluate.py:149-150): one mode, one rock
+        type, positive rate."""
+        return len(self.mode_rates) == 1 and self.n_rock_types == 1 and self.mode_rates[0] > 0
 
 
 def scenario_values(bm: BlockModel, grades: np.ndarray | None, use_stored: bool = False) -> np.ndarray:

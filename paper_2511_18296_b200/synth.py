@@ -139,6 +139,8 @@ def generate_block_model(
 
     growth = np.array([1.0 + 0.02 * t for t in range(n_periods)])
     cost = np.round(masses[:, None] * mining_cost_rate * growth[None, :], 6)
+    mean_rate = 500.0
+    hours = np.full(n_periods, np.round(0.8 * cap / mean_rate, 3), dtype=np.float64)
 
     return BlockModel(
         n_blocks=n_blocks,
@@ -159,6 +161,9 @@ def generate_block_model(
         processing_cost_by_mode=proc_cost,
         n_modes=n_modes,
         stored_values=stored,
+        plant_hours=hours,
+        mode_rates=tuple(mean_rate * (1.0 + 0.2 * o) for o in range(n_modes)),
+        n_rock_types=n_rock_types,
     )
 
 

@@ -29,6 +29,9 @@ def bm_from(store: dict, p: str) -> BlockModel:
         discount_rate=float(store[p + "discount_rate"]), coords=store[p + "coords"],
         alteration=f[:, 0], structural=f[:, 1], dist_intrusion=f[:, 2],
         base_grade=np.zeros(B),
+        plant_hours=store[p + "plant_hours"] if (p + "plant_hours") in store else None,
+        mode_rates=tuple(store[p + "mode_rates"]) if (p + "mode_rates") in store else (),
+        n_rock_types=int(store[p + "n_rock_types"]) if (p + "n_rock_types") in store else 1,
     )
 
 

@@ -28,7 +28,7 @@ sys.path.insert(0, REF)
 
 from pitplan.colgen import _enpv_adjusted  # noqa: E402
 from pitplan.blockmodel import UNMINED, Block, Economics, GeoFeatures, Instance, OperatingMode, generate_synthetic  # noqa: E402
-from pitplan.evaluate import Schedule, check_feasible, evaluate_candidates_parallel  # noqa: E402
+from pitplan.evaluate import Schedule, ScheduleEvaluator, check_feasible, evaluate_candidates_parallel  # noqa: E402
 from pitplan.hybrid import _precedence_repair_pass, greedy_initialize, lns_repair  # noqa: E402
 from pitplan.rng import substream  # noqa: E402
 from pitplan.saa import risk_metrics  # noqa: E402
@@ -59,6 +59,9 @@ def flat(inst: Instance, prefix: str) -> dict:
         f"{prefix}coords": inst.coords_array().reshape(inst.n_blocks, 3),
         f"{prefix}features": np.array([(b.features.alteration_intensity, b.features.structural_density,
                                         b.features.distance_to_intrusion) for b in inst.blocks]).reshape(-1, 3),
+        f"{prefix}plant_hours": np.asarray(inst.plant_hours, dtype=np.float64),
+        f"{prefix}mode_rates": np.array([m.rate for m in inst.modes], dtype=np.float64),
+        f"{prefix}n_rock_types": np.int64(len(inst.rock_types)),
     }
 
 
@@ -198,6 +201,14 @@ def small_cases(store):
         # while the fixpoint changed something would be the violation guard's revert (skipped)
         store[p + "mean_grade"] = scen.grades.mean(axis=0)
         store[p + "grades"] = scen.grades
+        # relaxed NPV (stage-1 costs + stage-2 greedy knapsack per (s, t), evaluate.py:166-183,
+        # 222-258) of the random schedules and of the greedy one, with and without sigma
+        ev, ev0 = ScheduleEvaluator(inst, scen, sigma), ScheduleEvaluator(inst, scen, None)
+        pop = [Schedule(r) for r in rand] + [Schedule(sched2.assignment.copy())]
+        store[p + "npv_pop"] = np.array([x.assignment for x in pop], dtype=np.int32)
+        store[p + "npv"] = np.array([ev.npv_relaxed(x) for x in pop])
+        store[p + "npv_nosig"] = np.array([ev0.npv_relaxed(x) for x in pop])
+        store[p + "npv_scen"] = np.array([ev.per_scenario_npv(x) for x in pop])
         # whole lns_repair runs (destroy + similarity-ranked insertions, hybrid.py:169-274)
         for tag, kw in (("a", dict(max_iters=50)),
                         ("b", dict(max_iters=50, destroy_fraction=0.3, net_mining_cost=True)),
@@ -339,6 +350,14 @@ def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
             outs = [lns_repair(inst, Schedule(a.astype(int)), [], scen, None, max_iters=0,
                                destroy_fraction=df).assignment.astype(np.int32) for a in ins]
             store[p + f"destroy_{tag}"] = np.array(outs)
+        # relaxed NPV of the config's schedules (evaluate.py:222-258)
+        ev = ScheduleEvaluator(inst, scen, sigma)
+        pop = [full.astype(np.int32), greedy_initialize(inst, scen, sigma).assignment.astype(np.int32)] + list(ins)
+        store[p + "npv_pop"] = np.array(pop, dtype=np.int32)
+        store[p + "npv"] = np.array([ev.npv_relaxed(Schedule(a.astype(int))) for a in pop])
+        store[p + "npv_scen"] = np.array([ev.per_scenario_npv(Schedule(a.astype(int))) for a in pop])
+        store[p + "plant_hours"] = np.asarray(inst.plant_hours, dtype=np.float64)
+        store[p + "mode_rates"] = np.array([m.rate for m in inst.modes], dtype=np.float64)
         # a whole lns_repair run at 4k blocks (40 insertion rounds after the destroy step)
         store[p + "grades"] = scen.grades
         store[p + "lns"] = lns_repair(inst, Schedule(ins[0].astype(int)), [], scen, sigma, max_iters=40,

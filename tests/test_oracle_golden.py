@@ -218,3 +218,32 @@ def _restated_helpers_check():
     pool = list(range(0, 60, 3))
     assert hybrid._scheduled_neighbor_similarity(inst, RefSchedule(a), pool, g, ref) == \
         scheduled_neighbor_similarity(a, pool, g, mine)
+
+
+@pytest.mark.parametrize("case", KD)
+def test_npv_relaxed_small(oracle_lib, case):
+    """ScheduleEvaluator.npv_relaxed / per_scenario_npv (evaluate.py:166-183, 222-258), single-mode
+    fast path, against the reference on random and greedy schedules, with and without sigma."""
+    st = load("small")
+    p = f"kd{case}_"
+    bm = bm_from(st, p)
+    assert bm.single_mode_fast
+    o = oracle_lib.Oracle(bm, st[p + "vmax"], st[p + "sigma"])
+    for k, a in enumerate(st[p + "npv_pop"]):
+        v, ps = o.npv_relaxed(a, bm.plant_hours, bm.mode_rates[0])
+        v0, _ = o.npv_relaxed(a, bm.plant_hours, bm.mode_rates[0], use_sigma=False)
+        assert v == st[p + "npv"][k] and v0 == st[p + "npv_nosig"][k]
+        assert np.array_equal(ps, st[p + "npv_scen"][k])
+
+
+def test_npv_relaxed_c1(oracle_lib):
+    st = load("c1")
+    c = config("C1")
+    bm = c["bm"]
+    assert np.array_equal(bm.plant_hours, st["C1_plant_hours"]), "synth plant hours differ from the reference"
+    assert bm.mode_rates == tuple(st["C1_mode_rates"])
+    o = oracle_lib.Oracle(bm, c["vmax"], c["sigma"])
+    for k, a in enumerate(st["C1_npv_pop"]):
+        v, ps = o.npv_relaxed(a, bm.plant_hours, bm.mode_rates[0])
+        assert v == st["C1_npv"][k], k
+        assert np.array_equal(ps, st["C1_npv_scen"][k]), k
