@@ -196,6 +196,17 @@ PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode
  * NULL) marks the ejected blocks. */
 PP_API int pp_eject(pp_ctx *ctx, int32_t *assign, int32_t n_sched, const double *mean_grade, double destroy_fraction,
              uint8_t *ejected_out, int32_t mem, void *stream);
+/* Plant data for the relaxed NPV: plant_hours[T] and the throughput rate of the single operating
+ * mode (blockmodel.py:63-97).  Only the stage-2 fast path exists on the device: one mode, one rock
+ * type, rate > 0 (evaluate.py:149-150); other instances stay on the reference's LP. */
+PP_API int pp_set_plant(pp_ctx *ctx, const double *plant_hours, double rate);
+/* ScheduleEvaluator.npv_relaxed (evaluate.py:222-234, 244-246) of P schedules assign[P][B] ->
+ * npv_out[P], and per_scenario_npv (248-258) -> per_scen_out[P][S] (may be NULL); flags
+ * PP_USE_SIGMA weights the stage-2 values by sigma[s][t] (sigma=None otherwise).  Stage 2 per
+ * (s, t) is the greedy fractional knapsack of evaluate.py:166-183, bit-exact.  A period with more
+ * than 6144 mined blocks is PP_ERR_SHAPE. */
+PP_API int pp_npv_relaxed(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, uint32_t flags, double *npv_out,
+                   double *per_scen_out, int32_t mem, void *stream);
 /* spatial[B] = geological_consistency of every block (uncertainty.py:185-191, the factor
  * pp_set_geology computed on the device), e.g. for lns_repair's realism fallback
  * (hybrid.py:238-244, 256-260). */

@@ -441,6 +441,8 @@ struct pp_ctx {
     int B = 0, T = 0, S = 0, Sp = 0, n_levels = 0, deg_max = 0;
     long long E = 0;
     bool have_instance = false, have_spatial = false, have_scen = false, have_sigma = false, have_sched = false;
+    bool have_plant = false;  // pp_set_plant (relaxed NPV)
+    double rate = 0.0;
     double mean_cap = 0.0;
     std::vector<int> level_ptr;  // host, n_levels + 1
     std::vector<int> level_of;   // host, B
@@ -468,6 +470,7 @@ struct pp_ctx {
     unsigned char *h_bounce = nullptr;  // page-locked bounce buffer for small host-mode results
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
     DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
+    DevBuf hours, npv_raw, npv_cost, npv_n, npv_flag;  // relaxed NPV (pp_npv.cu)
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
@@ -475,7 +478,8 @@ struct pp_ctx {
         return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
-                &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk};
+                &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
+                &npv_cost, &npv_n, &npv_flag};
     }
 };
 

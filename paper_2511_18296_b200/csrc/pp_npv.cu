@@ -1,0 +1,395 @@
+// pp_npv.cu -- relaxed NPV of P schedules on the device: ScheduleEvaluator.npv_relaxed and
+// per_scenario_npv (evaluate.py:222-258) on the single-mode fast path of the stage-2 problem
+// (evaluate.py:166-183), bit-exact.  Population fitness of the GA loop (hybrid.py:595-606).
+#include "pp_internal.cuh"
+#include <cub/block/block_radix_sort.cuh>
+
+// ------------------------------------------------------------------------------------
+// k_stage2: one CTA per (scenario s, period t, schedule p).
+//   1. the blocks mined in t, in block order (two vectorised passes: count, place);
+//   2. the s == 0 CTA also sums their mining costs in numpy's pairwise order (for _npv);
+//   3. density = v[s][b] / m[b]; stable descending block radix sort (cub), which is the order of
+//      np.argsort(-density, kind="stable");
+//   4. the greedy fill is a sequential f64 recurrence (hours_left, total), done by one thread
+//      over arrays prepared in parallel (d, m and m / rate in sorted order), four blocks per
+//      speculative step.
+// ------------------------------------------------------------------------------------
+#ifdef PP_EVAL_PROBE
+__device__ unsigned long long g_npv_probe[8];
+__device__ __forceinline__ unsigned long long np_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define NPVP(k) do { if (threadIdx.x == 0 && blockIdx.x == 1 && blockIdx.y == 0 && blockIdx.z == 0) g_npv_probe[k] = np_gtimer(); } while (0)
+extern "C" PP_API int pp_debug_npv_probe(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_npv_probe, sizeof(g_npv_probe)) == cudaSuccess ? 0 : 3;
+}
+#else
+#define NPVP(k) do { } while (0)
+#endif
+
+constexpr int S2_THREADS = 1024;
+constexpr int S2_IPT = 6;                        // items per thread of the block radix sort
+constexpr int S2_NMAX = S2_THREADS * S2_IPT;     // mined blocks per period handled on chip
+using S2Sort = cub::BlockRadixSort<double, S2_THREADS, S2_IPT, int>;
+
+// dynamic shared memory: [sort temp | later: density d (sorted)] [ids] [m (sorted)] [m / rate (sorted)]
+struct S2Layout {
+    __host__ __device__ static constexpr size_t a_bytes() {
+        return sizeof(typename S2Sort::TempStorage) > 8 * (size_t)S2_NMAX ? sizeof(typename S2Sort::TempStorage)
+                                                                              : 8 * (size_t)S2_NMAX;
+    }
+    __host__ __device__ static constexpr size_t ids_off() { return (a_bytes() + 15) & ~(size_t)15; }
+    __host__ __device__ static constexpr size_t m_off() { return ids_off() + 4 * (size_t)S2_NMAX; }
+    __host__ __device__ static constexpr size_t q_off() { return m_off() + 8 * (size_t)S2_NMAX; }
+    __host__ __device__ static constexpr size_t bytes() { return q_off() + 8 * (size_t)S2_NMAX; }
+};
+
+// numpy pairwise sum of a[0..n) in shared memory (pairwise.c: blocks of 8, leaves <= 128), whole
+// CTA, result on thread 0: the leaves (n <= 6144: at most 96) from the recursion on thread 0,
+// one thread per leaf with numpy's 8 accumulators, the fold in post-order on thread 0
+__device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 doubles */) {
+    __shared__ int s_ls[160], s_ll[160], s_nl;
+    if (threadIdx.x == 0) {  // pre-order traversal: leaves come out in element order
+        int stk_o[32], stk_n[32], sp = 0, nl = 0;
+        stk_o[sp] = 0;
+        stk_n[sp] = n;
+        sp++;
+        while (sp > 0) {
+            sp--;
+            const int o = stk_o[sp], ln = stk_n[sp];
+            if (ln <= 128) {
+                s_ls[nl] = o;
+                s_ll[nl] = ln;
+                nl++;
+            } else {
+                int n2 = ln / 2;
+                n2 -= n2 % 8;
+                stk_o[sp] = o + n2;  // right pushed first, popped after the left subtree
+                stk_n[sp] = ln - n2;
+                sp++;
+                stk_o[sp] = o;
+                stk_n[sp] = n2;
+                sp++;
+            }
+        }
+        s_nl = nl;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+        const int o = s_ls[l], len = s_ll[l];
+        double r;
+        if (len < 8) {
+            r = -0.0;
+            for (int i = 0; i < len; i++) r = f64_add(r, a[o + i]);
+        } else {
+            double acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) acc[j] = a[o + j];
+            const int main_ = len - (len & 7);
+            for (int i = 8; i < main_; i += 8)
+#pragma unroll
+                for (int j = 0; j < 8; j++) acc[j] = f64_add(acc[j], a[o + i + j]);
+            r = tree8(acc);
+            for (int i = main_; i < len; i++) r = f64_add(r, a[o + i]);
+        }
+        scratch[l] = r;
+    }
+    __syncthreads();
+    double res = 0.0;
+    if (threadIdx.x == 0) {
+        // fold: re-run the recursion over leaf indices (post-order)
+        int stk_n[32], stk_state[32], sp = 0, leaf = 0;
+        double val[32];
+        stk_n[0] = n;
+        stk_state[0] = 0;
+        sp = 1;
+        int vsp = 0;
+        while (sp > 0) {
+            const int ln = stk_n[sp - 1];
+            if (ln <= 128) {
+                val[vsp++] = scratch[leaf++];
+                sp--;
+                continue;
+            }
+            int n2 = ln / 2;
+            n2 -= n2 % 8;
+            if (stk_state[sp - 1] == 0) {
+                stk_state[sp - 1] = 1;
+                stk_n[sp] = n2;
+                stk_state[sp] = 0;
+                sp++;
+            } else if (stk_state[sp - 1] == 1) {
+                stk_state[sp - 1] = 2;
+                stk_n[sp] = ln - n2;
+                stk_state[sp] = 0;
+                sp++;
+            } else {
+                const double rhs = val[--vsp];
+                const double lhs = val[--vsp];
+                val[vsp++] = f64_add(lhs, rhs);
+                sp--;
+            }
+        }
+        res = f64_add(0.0, n ? val[0] : -0.0);
+    }
+    return res;
+}
+
+__global__ void __launch_bounds__(S2_THREADS, 1)
+    k_stage2(const int32_t *__restrict__ assign, int B, int T, int S, int Sp, const double *__restrict__ mass,
+             const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
+             double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
+             int32_t *__restrict__ too_big) {
+    extern __shared__ __align__(16) unsigned char s2_dyn[];
+    typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
+    double *dsort = reinterpret_cast<double *>(s2_dyn);  // after the sort
+    int32_t *ids = reinterpret_cast<int32_t *>(s2_dyn + S2Layout::ids_off());
+    double *ms = reinterpret_cast<double *>(s2_dyn + S2Layout::m_off());
+    double *qs = reinterpret_cast<double *>(s2_dyn + S2Layout::q_off());
+    __shared__ int s_wc[32];
+    __shared__ double s_scr[160];
+    const int s = blockIdx.x, t = blockIdx.y, p = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    NPVP(0);
+    const int32_t *a = assign + (size_t)p * B;
+    // 1. blocks mined in t, block order: warp w owns [w*chunk, (w+1)*chunk), 128 blocks per step
+    //    (int4 per lane when aligned)
+    const int chunk = ((B + 31) / 32 + 127) & ~127;
+    const int lo = warp * chunk, hi = min(B, lo + chunk);
+    const bool vec = (B & 3) == 0;
+    auto load4 = [&](int b0, int v[4]) {
+        const int b = b0 + 4 * lane;
+        if (vec && b + 3 < hi) {
+            const int4 x = __ldg(reinterpret_cast<const int4 *>(a + b));
+            v[0] = x.x;
+            v[1] = x.y;
+            v[2] = x.z;
+            v[3] = x.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u++) v[u] = (b + u < hi) ? __ldg(a + b + u) : -2;
+        }
+    };
+    int cnt = 0;
+    for (int b0 = lo; b0 < hi; b0 += 128) {
+        int v[4];
+        load4(b0, v);
+        cnt += (v[0] == t) + (v[1] == t) + (v[2] == t) + (v[3] == t);
+    }
+    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    if (lane == 0) s_wc[warp] = cnt;
+    __syncthreads();
+    int base = 0, n = 0;
+    for (int w = 0; w < 32; w++) {
+        base += w < warp ? s_wc[w] : 0;
+        n += s_wc[w];
+    }
+    const size_t pt = ((size_t)p * T + t);
+    if (n > S2_NMAX) {  // outside the on-chip path: flagged, the host reports it
+        if (tid == 0) {
+            *too_big = 1;
+            raw[pt * S + s] = 0.0;
+        }
+        return;
+    }
+    for (int b0 = lo; b0 < hi; b0 += 128) {
+        int v[4];
+        load4(b0, v);
+        const int c = (v[0] == t) + (v[1] == t) + (v[2] == t) + (v[3] == t);
+        int incl = c;  // lanes own consecutive groups of 4 blocks: exclusive scan of the counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int q = base + incl - c;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (v[u] == t) ids[q++] = b0 + 4 * lane + u;
+        base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncthreads();
+    NPVP(1);
+    // 2. mining-cost sum of the period (numpy pairwise, block order), once per (p, t)
+    if (s == 0) {
+        for (int k = tid; k < n; k += S2_THREADS) ms[k] = __ldg(cost + (size_t)ids[k] * T + t);
+        __syncthreads();
+        const double cs = s2_pairwise(ms, n, s_scr);
+        if (tid == 0) {
+            costsum[pt] = cs;
+            nmined[pt] = n;
+        }
+        __syncthreads();
+    }
+    if (n == 0) {
+        if (tid == 0) raw[pt * S + s] = 0.0;
+        return;
+    }
+    // 3. densities, stable descending radix sort (= np.argsort(-density, kind="stable"); the order
+    //    among densities <= 0 is irrelevant: the greedy stops at the first one)
+    double dk[S2_IPT];
+    int ik[S2_IPT];
+#pragma unroll
+    for (int u = 0; u < S2_IPT; u++) {
+        const int k = tid * S2_IPT + u;  // blocked arrangement: thread order = position order
+        if (k < n) {
+            const int b = ids[k];
+            dk[u] = f64_div(__ldg(vmax + (size_t)b * Sp + s), __ldg(mass + b));
+        } else {
+            dk[u] = -kInf;
+        }
+        ik[u] = k;
+    }
+    S2Sort(sort_tmp).SortDescending(dk, ik);
+    __syncthreads();  // the sort's temp storage becomes the sorted densities
+#pragma unroll
+    for (int u = 0; u < S2_IPT; u++) {
+        const int k = tid * S2_IPT + u;
+        if (k < n) {
+            const double m = __ldg(mass + ids[ik[u]]);
+            dsort[k] = dk[u];
+            ms[k] = m;
+            qs[k] = f64_div(m, rate);
+        }
+    }
+    __syncthreads();
+    NPVP(3);
+    // 4. the greedy fill (evaluate.py:174-182): a sequential f64 recurrence.  4 blocks per step are
+    //    taken speculatively as whole blocks (hours_left -= m / rate, total += d * m); the step is
+    //    kept when none of them hits a stop (d <= 0, hours_left <= 0) or a partial take
+    //    (hours_left * rate < m), else the exact scalar loop finishes from its start.
+    if (tid == 0) {
+        double hl = __ldg(hours + t), total = 0.0;
+        int k = 0;
+        for (; k + 4 <= n; k += 4) {  // (explicit registers: an array form compiled ~2x slower)
+            const double d0 = dsort[k], d1 = dsort[k + 1], d2 = dsort[k + 2], d3 = dsort[k + 3];
+            const double m0 = ms[k], m1 = ms[k + 1], m2 = ms[k + 2], m3 = ms[k + 3];
+            const double h1 = f64_sub(hl, qs[k]), h2 = f64_sub(h1, qs[k + 1]), h3 = f64_sub(h2, qs[k + 2]);
+            const double h4 = f64_sub(h3, qs[k + 3]);
+            const bool ok = d0 > 0 && d1 > 0 && d2 > 0 && d3 > 0 && hl > 0 && h1 > 0 && h2 > 0 && h3 > 0 &&
+                            !(f64_mul(hl, rate) < m0) && !(f64_mul(h1, rate) < m1) && !(f64_mul(h2, rate) < m2) &&
+                            !(f64_mul(h3, rate) < m3);
+            if (!ok) break;
+            total = f64_add(f64_add(f64_add(f64_add(total, f64_mul(d0, m0)), f64_mul(d1, m1)), f64_mul(d2, m2)),
+                            f64_mul(d3, m3));
+            hl = h4;
+        }
+        for (; k < n; k++) {
+            const double d = dsort[k];
+            if (d <= 0 || hl <= 0) break;
+            const double m = ms[k];
+            const double hr = f64_mul(hl, rate);
+            if (hr < m) {  // take = min(m, hours_left * rate) = hours_left * rate
+                total = f64_add(total, f64_mul(d, hr));
+                hl = f64_sub(hl, f64_div(hr, rate));
+            } else {
+                total = f64_add(total, f64_mul(d, m));
+                hl = f64_sub(hl, qs[k]);
+            }
+        }
+        raw[pt * S + s] = total;
+    }
+    NPVP(4);
+}
+
+// _npv / per_scenario_npv accumulation in the reference's order (t outer, s inner)
+__global__ void k_npv_final(int T, int S, const double *__restrict__ raw, const double *__restrict__ costsum,
+                            const int32_t *__restrict__ nmined, const double *__restrict__ disc,
+                            const double *__restrict__ sigma, double *__restrict__ npv, double *__restrict__ per_scen) {
+    const int p = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    double total = 0.0;
+    double *ps = per_scen ? per_scen + (size_t)p * S : nullptr;
+    if (ps)
+        for (int s = 0; s < S; s++) ps[s] = 0.0;
+    for (int t = 0; t < T; t++) {
+        const size_t pt = (size_t)p * T + t;
+        const double d = disc[t];
+        double cv = 0.0;
+        if (nmined[pt] > 0) {
+            const double cs = costsum[pt];
+            total = f64_sub(total, f64_mul(d, cs));
+            cv = f64_mul(d, cs);
+        }
+        for (int s = 0; s < S; s++) {
+            const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
+            const double r = raw[pt * S + s];
+            const double term = f64_mul(f64_mul(d, sg), r);
+            total = f64_add(total, f64_div(term, (double)S));
+            if (ps) ps[s] = f64_add(ps[s], f64_sub(term, cv));
+        }
+    }
+    npv[p] = total;
+}
+
+extern "C" {
+
+int pp_set_plant(pp_ctx *c, const double *plant_hours, double rate) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (!plant_hours) return fail(PP_ERR_INVALID_ARGS, "plant_hours is NULL");
+    if (!(rate > 0)) return fail(PP_ERR_INVALID_ARGS, "the stage-2 fast path needs a positive rate");
+    TRY(use_device(c));
+    TRY(c->hours.ensure(sizeof(double) * c->T));
+    CUDA_TRY(cudaMemcpy(c->hours.ptr, plant_hours, sizeof(double) * c->T, cudaMemcpyHostToDevice));
+    c->rate = rate;
+    c->have_plant = true;
+    return PP_OK;
+}
+
+int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, double *npv_out, double *per_scen_out,
+                   int32_t mem, void *stream) {
+    if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
+        return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
+    if (P < 0 || (P > 0 && (!assign || !npv_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if ((flags & PP_USE_SIGMA) && !c->have_sigma) return fail(PP_ERR_STATE, "PP_USE_SIGMA without an uploaded sigma");
+    if (P == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B, T = c->T, S = c->S;
+    const int32_t *da = assign;
+    double *dn = npv_out, *dps = per_scen_out;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_assign.ensure(sizeof(int32_t) * (size_t)P * B));
+        TRY(c->h_d1.ensure(sizeof(double) * P));
+        CUDA_TRY(cudaMemcpyAsync(c->h_assign.ptr, assign, sizeof(int32_t) * (size_t)P * B, cudaMemcpyHostToDevice, st));
+        da = c->h_assign.as<int32_t>();
+        dn = c->h_d1.as<double>();
+        if (per_scen_out) {
+            TRY(c->h_pm.ensure(sizeof(double) * (size_t)P * S));
+            dps = c->h_pm.as<double>();
+        }
+    }
+    TRY(c->npv_raw.ensure(sizeof(double) * (size_t)P * T * S));
+    TRY(c->npv_cost.ensure(sizeof(double) * (size_t)P * T));
+    TRY(c->npv_n.ensure(sizeof(int32_t) * (size_t)P * T));
+    TRY(c->npv_flag.ensure(sizeof(int32_t)));
+    CUDA_TRY(cudaMemsetAsync(c->npv_flag.ptr, 0, sizeof(int32_t), st));
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S2Layout::bytes()));
+        attr = true;
+    }
+    k_stage2<<<dim3(S, T, P), S2_THREADS, S2Layout::bytes(), st>>>(
+        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
+        c->rate, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(), c->npv_flag.as<int32_t>());
+    CUDA_TRY(cudaGetLastError());
+    k_npv_final<<<P, 32, 0, st>>>(T, S, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(),
+                                  c->disc.as<double>(), (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
+                                  dps);
+    CUDA_TRY(cudaGetLastError());
+    if (mem == PP_MEM_HOST) {
+        int32_t flag = 0;
+        CUDA_TRY(cudaMemcpyAsync(npv_out, dn, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+        if (per_scen_out)
+            CUDA_TRY(cudaMemcpyAsync(per_scen_out, dps, sizeof(double) * (size_t)P * S, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(&flag, c->npv_flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(stream_wait(st));
+        if (flag) return fail(PP_ERR_SHAPE, "a period mines more than %d blocks (device stage-2 limit)", S2_NMAX);
+    }
+    return PP_OK;
+}
+
+}  // extern "C"

@@ -315,6 +315,33 @@ class Engine:
         check(self.lib.pp_repair(self._h, ptr(a), a.shape[0], m, ptr(u), _lib.PP_MEM_HOST, None))
         return a, u
 
+    def set_plant(self, plant_hours=None, rate=None):
+        """Plant hours per period and the single mode's throughput rate (relaxed NPV); defaults
+        from the BlockModel."""
+        bm = self._need_bm()
+        h = np.ascontiguousarray(bm.plant_hours if plant_hours is None else plant_hours, dtype=np.float64)
+        r = float(bm.mode_rates[0] if rate is None else rate)
+        check(self.lib.pp_set_plant(self._h, ptr(h), r))
+        self._plant = True
+
+    def npv_relaxed(self, assign_batch, use_sigma=True, per_scenario=False):
+        """ScheduleEvaluator.npv_relaxed (and per_scenario_npv) of P schedules (evaluate.py:222-258),
+        single-mode fast path.  Returns npv[P] (and per_scenario [P][S])."""
+        bm = self._need_bm()
+        if not getattr(self, "_plant", False):
+            if not bm.single_mode_fast:
+                raise InvalidArgs("the device stage-2 path needs one mode, one rock type and a positive rate")
+            self.set_plant()
+        a = np.ascontiguousarray(np.atleast_2d(np.asarray(assign_batch)), dtype=np.int32)
+        if a.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("schedule length does not match the instance")
+        P = a.shape[0]
+        npv = np.empty(P, np.float64)
+        ps = np.empty((P, self.n_scenarios), np.float64) if per_scenario else None
+        f = _lib.PP_USE_SIGMA if (use_sigma and self.has_sigma) else 0
+        check(self.lib.pp_npv_relaxed(self._h, ptr(a), P, f, ptr(npv), ptr(ps), _lib.PP_MEM_HOST, None))
+        return (npv, ps) if per_scenario else npv
+
     def spatial(self) -> np.ndarray:
         """geological_consistency of every block (uncertainty.py:185-191), as computed on the device."""
         bm = self._need_bm()

@@ -488,3 +488,41 @@ def test_lns_repair_dropin_c1():
                             destroy_fraction=0.1)
     assert np.array_equal(out.assignment, st["C1_lns"])
     dropin.clear_cache()
+
+
+@pytest.mark.parametrize("case", range(0, 20, 3))
+def test_npv_relaxed_small(small, case):
+    """ScheduleEvaluator.npv_relaxed / per_scenario_npv on the device (evaluate.py:166-183,
+    222-258), bit-exact against the reference, population of 5 schedules in one call."""
+    p = f"kd{case}_"
+    bm = bm_from(small, p)
+    eng = Engine.from_tables(bm, tables_from(small, p))
+    pop = small[p + "npv_pop"]
+    npv, ps = eng.npv_relaxed(pop, per_scenario=True)
+    assert same(npv, small[p + "npv"])
+    assert same(ps, small[p + "npv_scen"])
+    assert same(eng.npv_relaxed(pop, use_sigma=False), small[p + "npv_nosig"])
+    eng.close()
+
+
+def test_npv_relaxed_c1(oracle_lib):
+    st = load("c1")
+    c = config("C1")
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], c["sigma"]))
+    npv, ps = eng.npv_relaxed(st["C1_npv_pop"], per_scenario=True)
+    assert same(npv, st["C1_npv"])
+    assert same(ps, st["C1_npv_scen"])
+    eng.close()
+
+
+def test_npv_relaxed_c2_against_oracle(oracle_lib):
+    c = config("C2")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    o = oracle_lib.Oracle(bm, c["vmax"], c["sigma"])
+    pop = np.stack([c["assign"], c["greedy"]])
+    npv, ps = eng.npv_relaxed(pop, per_scenario=True)
+    for k in range(2):
+        v, pr = o.npv_relaxed(pop[k], bm.plant_hours, bm.mode_rates[0])
+        assert npv[k] == v and np.array_equal(ps[k], pr), k
+    eng.close()
