@@ -4,6 +4,8 @@
     check_feasible                 pitplan/evaluate.py:82-105
     precedence_repair_pass         pitplan/hybrid.py:493-510  (`_precedence_repair_pass`)
     unmine_fixpoint                pitplan/hybrid.py:199-211  (first step of `lns_repair`)
+    ScheduleEvaluator              pitplan/evaluate.py:126-258 (npv_relaxed / per_scenario_npv /
+                                   objective on the device for the single-mode fast path)
     lns_repair                     pitplan/hybrid.py:169-274  (destroy step and every insertion
                                    evaluation on the device; candidate ranking by the
                                    reference's own neighbour-similarity helper)
@@ -293,6 +295,88 @@ def lns_repair(
     if stalled and strict:
         raise RepairStalled("no feasible insertion for remaining blocks", schedule=sched)
     return sched
+
+
+def _reference_evaluator():
+    try:
+        from pitplan.evaluate import ScheduleEvaluator as Ref
+
+        return Ref
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class _DeviceNpv:
+    """Device half of the ScheduleEvaluator drop-in: relaxed NPV and per-scenario NPV of a schedule
+    (evaluate.py:222-258) through pp_npv_relaxed when the stage-2 fast path applies (one mode, one
+    rock type, positive rate: evaluate.py:149-150)."""
+
+    def _dev_init(self, instance, scenarios, sigma):
+        self._dev_args = (instance, scenarios, sigma)
+
+    def _dev_entry(self):
+        instance, scenarios, sigma = self._dev_args
+        e = _entry(instance)
+        if not e.bm.single_mode_fast:
+            return None
+        _bind_scenarios(e, scenarios, sigma, None)
+        return e
+
+    def _dev_npv(self, schedule, per_scenario):
+        e = self._dev_entry()
+        if e is None:
+            return None
+        r = e.engine.npv_relaxed(_assignment(schedule)[None, :], use_sigma=self._dev_args[2] is not None,
+                                 per_scenario=per_scenario)
+        return (float(r[0][0]), r[1][0]) if per_scenario else float(r[0])
+
+
+def _make_evaluator_class():
+    Ref = _reference_evaluator()
+    base = (Ref, _DeviceNpv) if Ref is not None else (_DeviceNpv,)
+
+    class ScheduleEvaluator(*base):
+        """Drop-in for pitplan.evaluate.ScheduleEvaluator (evaluate.py:126-258): npv_relaxed,
+        per_scenario_npv and objective run on the device (bit-exact) on the single-mode fast path;
+        everything else (and the LP path) is the reference's own code when it is installed."""
+
+        def __init__(self, instance, scenarios, sigma=None):
+            if Ref is not None:
+                Ref.__init__(self, instance, scenarios, sigma)
+            self._dev_init(instance, scenarios, sigma)
+
+        def npv_relaxed(self, schedule):
+            v = self._dev_npv(schedule, False)
+            if v is None:
+                if Ref is None:
+                    raise InvalidArgs("only the single-mode stage-2 fast path exists without the reference")
+                return Ref.npv_relaxed(self, schedule)
+            return v
+
+        def per_scenario_npv(self, schedule):
+            r = self._dev_npv(schedule, True)
+            if r is None:
+                if Ref is None:
+                    raise InvalidArgs("only the single-mode stage-2 fast path exists without the reference")
+                return Ref.per_scenario_npv(self, schedule)
+            return r[1]
+
+        def objective(self, schedule):
+            """f(x) for a feasible schedule (evaluate.py:236-243)."""
+            report = check_feasible(self._dev_args[0], schedule)
+            if not report.feasible:
+                try:
+                    from pitplan.errors import InfeasibleSchedule
+                except Exception:  # noqa: BLE001
+                    InfeasibleSchedule = InvalidArgs  # noqa: N806
+                raise InfeasibleSchedule(
+                    f"schedule has violation {report.violation:.6g}; use the relaxed evaluator")
+            return self.npv_relaxed(schedule)
+
+    return ScheduleEvaluator
+
+
+ScheduleEvaluator = _make_evaluator_class()
 
 
 def clear_cache() -> None:

@@ -19,14 +19,17 @@ _PATCHES = {
     "pitplan.evaluate": {
         "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
         "check_feasible": _ev.check_feasible,
+        "ScheduleEvaluator": _ev.ScheduleEvaluator,
     },
     "pitplan.hybrid": {
         "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
         "check_feasible": _ev.check_feasible,
         "_precedence_repair_pass": _ev.precedence_repair_pass,
         "lns_repair": _ev.lns_repair,
+        "ScheduleEvaluator": _ev.ScheduleEvaluator,
     },
-    "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair},
+    "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair,
+                       "ScheduleEvaluator": _ev.ScheduleEvaluator},
     "pitplan.saa": {},
     "pitplan": {"check_feasible": _ev.check_feasible},
 }

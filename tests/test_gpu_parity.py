@@ -526,3 +526,19 @@ def test_npv_relaxed_c2_against_oracle(oracle_lib):
         v, pr = o.npv_relaxed(pop[k], bm.plant_hours, bm.mode_rates[0])
         assert npv[k] == v and np.array_equal(ps[k], pr), k
     eng.close()
+
+
+def test_schedule_evaluator_dropin(small):
+    """evaluate.ScheduleEvaluator (the drop-in class) on the device fast path, equal to the
+    reference's npv_relaxed / per_scenario_npv."""
+    from paper_2511_18296_b200 import evaluate as dropin
+    from paper_2511_18296_b200.model import Schedule
+
+    for case in (2, 9):
+        p = f"kd{case}_"
+        bm = bm_from(small, p)
+        ev = dropin.ScheduleEvaluator(bm, tables_from(small, p), True)
+        for k, a in enumerate(small[p + "npv_pop"]):
+            assert ev.npv_relaxed(Schedule(a)) == small[p + "npv"][k]
+            assert np.array_equal(ev.per_scenario_npv(Schedule(a)), small[p + "npv_scen"][k])
+    dropin.clear_cache()
