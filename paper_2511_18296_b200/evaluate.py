@@ -6,6 +6,8 @@
     unmine_fixpoint                pitplan/hybrid.py:199-211  (first step of `lns_repair`)
     ScheduleEvaluator              pitplan/evaluate.py:126-258 (npv_relaxed / per_scenario_npv /
                                    objective on the device for the single-mode fast path)
+    polish_schedule                pitplan/hybrid.py:326-490  (every option of a block evaluated in one
+                                   batched device call)
     lns_repair                     pitplan/hybrid.py:169-274  (destroy step and every insertion
                                    evaluation on the device; candidate ranking by the
                                    reference's own neighbour-similarity helper)
@@ -377,6 +379,185 @@ def _make_evaluator_class():
 
 
 ScheduleEvaluator = _make_evaluator_class()
+
+
+def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swaps=None):
+    """Steepest-descent polish (hybrid.py:326-490), same result as the reference.
+
+    The single-block sweep evaluates all options of a block (other period, unmine) as one batch of
+    schedules through pp_npv_relaxed (bit-exact relaxed NPV, so the `> best + 1e-9` decisions are
+    the reference's); the small-instance swap / exchange / joint-insertion phases call the device
+    evaluator per candidate, in the reference's order.  Falls back to the reference's own
+    polish_schedule when the stage-2 fast path does not apply."""
+    e = _entry(instance)
+    bm = e.bm
+    dev = isinstance(evaluator, _DeviceNpv) and evaluator._dev_entry() is not None
+    if not dev:
+        from pitplan.hybrid import polish_schedule as ref_polish
+
+        return ref_polish(instance, evaluator, schedule, max_sweeps, pair_swaps)
+    eng = e.engine
+    use_sigma = evaluator._dev_args[2] is not None
+    UN = -1
+    masses = bm.mass
+    cap = bm.capacity
+    B, T = bm.n_blocks, bm.n_periods
+    pp_, pi_, sp_, si_ = bm.csr()
+    if pair_swaps is None:
+        pair_swaps = B <= 32
+    cur = schedule.copy()
+    a = cur.assignment
+
+    def npv_of(batch):
+        return eng.npv_relaxed(np.asarray(batch), use_sigma=use_sigma)
+
+    cur_val = float(npv_of(a[None, :])[0])
+    load = np.zeros(T)
+    for t in range(T):
+        load[t] = masses[a == t].sum()
+
+    def window(b):
+        preds = pi_[pp_[b]:pp_[b + 1]]
+        if np.any(a[preds] == UN):
+            t_lo = None
+        else:
+            t_lo = int(max(a[preds].max(), 0)) if preds.size else 0
+        ms_ = a[si_[sp_[b]:sp_[b + 1]]]
+        ms_ = ms_[ms_ != UN]
+        t_hi = int(ms_.min()) if ms_.size else T - 1
+        return t_lo, t_hi
+
+    for _ in range(max_sweeps):
+        improved = False
+        for b in range(B):
+            orig = int(a[b])
+            t_lo, t_hi = window(b)
+            mined_succ_any = bool(np.any(a[si_[sp_[b]:sp_[b + 1]]] != UN))
+            options = []
+            if not mined_succ_any and orig != UN:
+                options.append(UN)
+            if t_lo is not None:
+                for t in range(t_lo, t_hi + 1):
+                    if t != orig and load[t] + masses[b] <= cap[t]:
+                        options.append(t)
+            best_t, best_val = orig, cur_val
+            if options:
+                batch = np.repeat(a[None, :], len(options), axis=0)
+                batch[np.arange(len(options)), b] = options
+                vals = npv_of(batch)
+                for t, val in zip(options, vals.tolist()):
+                    if val > best_val + 1e-9:
+                        best_t, best_val = t, val
+            a[b] = best_t
+            if best_t != orig:
+                improved = True
+                cur_val = best_val
+                if orig != UN:
+                    load[orig] -= masses[b]
+                if best_t != UN:
+                    load[best_t] += masses[b]
+
+        if pair_swaps:
+            for b1 in range(B):
+                t1 = int(a[b1])
+                if t1 == UN:
+                    continue
+                for b2 in range(b1 + 1, B):
+                    t2 = int(a[b2])
+                    if t2 == UN or t2 == t1:
+                        continue
+                    if load[t1] - masses[b1] + masses[b2] > cap[t1]:
+                        continue
+                    if load[t2] - masses[b2] + masses[b1] > cap[t2]:
+                        continue
+                    a[b1], a[b2] = t2, t1
+                    lo1, hi1 = window(b1)
+                    lo2, hi2 = window(b2)
+                    ok = lo1 is not None and lo1 <= t2 <= hi1 and lo2 is not None and lo2 <= t1 <= hi2
+                    val = float(npv_of(a[None, :])[0]) if ok else -np.inf
+                    if ok and val > cur_val + 1e-9:
+                        cur_val = val
+                        load[t1] += masses[b2] - masses[b1]
+                        load[t2] += masses[b1] - masses[b2]
+                        improved = True
+                    else:
+                        a[b1], a[b2] = t1, t2
+                    t1 = int(a[b1])
+
+            for b1 in range(B):  # 1-1 exchanges
+                t1 = int(a[b1])
+                if t1 == UN:
+                    continue
+                if np.any(a[si_[sp_[b1]:sp_[b1 + 1]]] != UN):
+                    continue
+                a[b1] = UN
+                applied = False
+                for b2 in range(B):
+                    if b2 == b1 or a[b2] != UN:
+                        continue
+                    lo2, hi2 = window(b2)
+                    if lo2 is None:
+                        continue
+                    for t2 in range(lo2, hi2 + 1):
+                        room = load[t2] - (masses[b1] if t2 == t1 else 0.0) + masses[b2]
+                        if room > cap[t2]:
+                            continue
+                        a[b2] = t2
+                        val = float(npv_of(a[None, :])[0])
+                        if val > cur_val + 1e-9:
+                            cur_val = val
+                            load[t1] -= masses[b1]
+                            load[t2] += masses[b2]
+                            improved = True
+                            applied = True
+                            break
+                        a[b2] = UN
+                    if applied:
+                        break
+                if not applied:
+                    a[b1] = t1
+
+            if B <= 12:  # joint pair insertion
+                unmined = [b for b in range(B) if a[b] == UN]
+                applied = False
+                for b1 in unmined:
+                    lo1, hi1 = window(b1)
+                    if lo1 is None:
+                        continue
+                    for t1 in range(lo1, hi1 + 1):
+                        if load[t1] + masses[b1] > cap[t1]:
+                            continue
+                        a[b1] = t1
+                        load[t1] += masses[b1]
+                        for b2 in unmined:
+                            if b2 == b1 or a[b2] != UN:
+                                continue
+                            lo2, hi2 = window(b2)
+                            if lo2 is None:
+                                continue
+                            for t2 in range(lo2, hi2 + 1):
+                                if load[t2] + masses[b2] > cap[t2]:
+                                    continue
+                                a[b2] = t2
+                                val = float(npv_of(a[None, :])[0])
+                                if val > cur_val + 1e-9:
+                                    cur_val = val
+                                    load[t2] += masses[b2]
+                                    improved = True
+                                    applied = True
+                                    break
+                                a[b2] = UN
+                            if applied:
+                                break
+                        if applied:
+                            break
+                        load[t1] -= masses[b1]
+                        a[b1] = UN
+                    if applied:
+                        break
+        if not improved:
+            break
+    return cur
 
 
 def clear_cache() -> None:

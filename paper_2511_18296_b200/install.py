@@ -27,6 +27,7 @@ _PATCHES = {
         "_precedence_repair_pass": _ev.precedence_repair_pass,
         "lns_repair": _ev.lns_repair,
         "ScheduleEvaluator": _ev.ScheduleEvaluator,
+        "polish_schedule": _ev.polish_schedule,
     },
     "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair,
                        "ScheduleEvaluator": _ev.ScheduleEvaluator},

@@ -29,7 +29,7 @@ sys.path.insert(0, REF)
 from pitplan.colgen import _enpv_adjusted  # noqa: E402
 from pitplan.blockmodel import UNMINED, Block, Economics, GeoFeatures, Instance, OperatingMode, generate_synthetic  # noqa: E402
 from pitplan.evaluate import Schedule, ScheduleEvaluator, check_feasible, evaluate_candidates_parallel  # noqa: E402
-from pitplan.hybrid import _precedence_repair_pass, greedy_initialize, lns_repair  # noqa: E402
+from pitplan.hybrid import _precedence_repair_pass, greedy_initialize, lns_repair, polish_schedule  # noqa: E402
 from pitplan.rng import substream  # noqa: E402
 from pitplan.saa import risk_metrics  # noqa: E402
 from pitplan.scenarios import builtin_scenarios, sample_lognormal  # noqa: E402
@@ -364,10 +364,36 @@ def config_case(store, name, n, dims, T, S, C, cf=1.3, scen_subset=0):
                                       destroy_fraction=0.1).assignment.astype(np.int32)
 
 
+def polish_cases(store):
+    """polish_schedule (hybrid.py:326-490) runs: 8 blocks (joint pair insertion), 27 blocks (pair
+    swaps, 1-1 exchanges), 512 blocks (single-block sweeps only)."""
+    for name, n, dims, T, S, sweeps in (("p8", 8, (2, 2, 2), 3, 3, 3), ("p27", 27, (3, 3, 3), 3, 2, 3),
+                                        ("p512", 512, (8, 8, 8), 6, 4, 2)):
+        inst = generate_synthetic(n, dims, T, 1, seed=70 + n, n_rock_types=1, capacity_factor=0.9)
+        scen = sample_lognormal(inst, S, 0.3, seed=71 + n)
+        sigma = uncertainty_factors(inst, scen.grades)
+        p = f"{name}_"
+        store.update(flat(inst, p))
+        store[p + "vmax"] = vmax_of(inst, scen)
+        store[p + "sigma"] = sigma.sigma
+        ev = ScheduleEvaluator(inst, scen, sigma)
+        starts = [greedy_initialize(inst, scen, sigma).assignment.copy()]
+        rng = np.random.default_rng(n)
+        a = starts[0].copy()
+        a[rng.random(n) < 0.3] = UNMINED
+        _precedence_repair_pass(inst, a)
+        starts.append(a)
+        store[p + "start"] = np.array(starts, dtype=np.int32)
+        store[p + "out"] = np.array([polish_schedule(inst, ev, Schedule(x.copy()), max_sweeps=sweeps).assignment
+                                     for x in starts], dtype=np.int32)
+        store[p + "sweeps"] = np.int64(sweeps)
+
+
 def main():
     store: dict = {}
     small_cases(store)
     hand_cases(store)
+    polish_cases(store)
     np.savez_compressed(os.path.join(OUT, "small.npz"), **store)
     store = {"numpy_version": np.bytes_(np.__version__)}
     config_case(store, "C1", 4000, (20, 20, 10), 10, 10, 1000, scen_subset=200)

@@ -542,3 +542,22 @@ def test_schedule_evaluator_dropin(small):
             assert ev.npv_relaxed(Schedule(a)) == small[p + "npv"][k]
             assert np.array_equal(ev.per_scenario_npv(Schedule(a)), small[p + "npv_scen"][k])
     dropin.clear_cache()
+
+
+@pytest.mark.parametrize("name", ["p8", "p27", "p512"])
+def test_polish_schedule_dropin(small, name):
+    """polish_schedule (hybrid.py:326-490) through the drop-in: options batched on the device,
+    same final schedule as the reference (joint insertion at 8 blocks, pair swaps and 1-1 exchanges
+    at 27, single-block sweeps at 512)."""
+    from paper_2511_18296_b200 import evaluate as dropin
+    from paper_2511_18296_b200.model import Schedule
+
+    p = f"{name}_"
+    bm = bm_from(small, p)
+    tables = tables_from(small, p)
+    ev = dropin.ScheduleEvaluator(bm, tables, True)
+    for k in range(small[p + "start"].shape[0]):
+        out = dropin.polish_schedule(bm, ev, Schedule(small[p + "start"][k].copy()),
+                                     max_sweeps=int(small[p + "sweeps"]))
+        assert np.array_equal(out.assignment, small[p + "out"][k]), k
+    dropin.clear_cache()
