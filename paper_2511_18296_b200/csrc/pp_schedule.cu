@@ -668,6 +668,7 @@ constexpr int PMC_MAXT = 16;
 constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;
 constexpr int PMC_MAXB = PMC_R * PMC_THREADS * 8;
 constexpr int PMC_MAXNODE = 512;  // 2^D for n <= 65536 (n = 65535: D = 9)
+constexpr int PMC_OWN = 6144;     // per-period buffer in the owning CTA (push mode; C2 periods hold ~4.2k)
 
 struct PmcSmem {
     int cnt[PMC_WARPS][PMC_MAXT];
@@ -687,6 +688,13 @@ __device__ __forceinline__ int ld_dsmem_i32(const int *p, int rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
     asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra));
     return v;
+}
+
+__device__ __forceinline__ void st_dsmem_f64(double *p, int rank, double v) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 
 // range [start, start + len) in 8-element blocks of node i at depth d of a tree over m blocks
@@ -711,6 +719,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
                  double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init,
                  int32_t *__restrict__ bad) {
     __shared__ PmcSmem h;
+    extern __shared__ __align__(16) double pmc_own[];  // [PMC_MAXQ][PMC_OWN] (push mode)
     PMCP(0, 0);
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {  // complete before the dependents' wait
         if (init.n_pairs) *init.n_pairs = 0;
@@ -788,14 +797,27 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     }
     __syncthreads();
     PMCS(2);
+    // push mode (every period fits its owner's buffer; the same decision in every CTA): each mass
+    // goes straight into the shared memory of the CTA that reduces its period; otherwise through L2
+    bool push = true;
+    for (int t = 0; t < T; t++) push &= h.n[t] <= PMC_OWN;
+    if (push) {
 #pragma unroll
-    for (int k = 0; k < K; k++)
-        if (tk[k] >= 0) {
-            const int t = tk[k];
-            compact[((size_t)p * T + t) * B + h.off[t] + h.cnt[warp][t] + pos[k]] = mk[k];
-        }
-    // the cluster barrier's release/acquire orders these global stores for every thread of the
-    // cluster (no separate sequentially consistent fence)
+        for (int k = 0; k < K; k++)
+            if (tk[k] >= 0) {
+                const int t = tk[k];
+                st_dsmem_f64(pmc_own + (t / R) * PMC_OWN + h.off[t] + h.cnt[warp][t] + pos[k], t % R, mk[k]);
+            }
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; k++)
+            if (tk[k] >= 0) {
+                const int t = tk[k];
+                compact[((size_t)p * T + t) * B + h.off[t] + h.cnt[warp][t] + pos[k]] = mk[k];
+            }
+    }
+    // the cluster barrier's release/acquire orders these stores (distributed shared memory or
+    // global) for every thread of the cluster (no separate sequentially consistent fence)
     cluster_sync_acqrel();  // every block of the schedule is in place (remote totals no longer read)
     PMCP(0, 1);
     // depth-D nodes of the (up to two) periods of this CTA
@@ -814,6 +836,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         }
     }
     const int nitems = cntg[0] + cntg[1];
+    PMCS(4);
     const int sub = tid & 7, half = (tid >> 3) & 1;  // 16 lanes per node: half c sums child leaf c
     for (int it0 = 0; it0 < nitems; it0 += PMC_THREADS / 16) {
         const int it = it0 + (tid >> 4);
@@ -835,13 +858,21 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             len = 8 * l1 + ((last && half == 1) ? rem : 0);
         }
         const bool use = act && (split || half == 0);
-        const double *a = compact + ((size_t)p * T + t) * B + o;
         // every load of the leaf in flight: 16 accumulator elements per lane + one tail element
+        // (separate shared / global paths: a pointer that may be either compiles to slow generic loads)
         const int nm = len >> 3, ntail = len & 7, e0 = len - ntail;
-        double x[16];
+        double x[16], tailv;
+        if (push) {
+            const double *a = pmc_own + g * PMC_OWN + o;
 #pragma unroll
-        for (int u = 0; u < 16; u++) x[u] = (use && u < nm) ? __ldcg(a + 8 * u + sub) : 0.0;
-        const double tailv = (use && sub < ntail) ? __ldcg(a + e0 + sub) : 0.0;
+            for (int u = 0; u < 16; u++) x[u] = (use && u < nm) ? a[8 * u + sub] : 0.0;
+            tailv = (use && sub < ntail) ? a[e0 + sub] : 0.0;
+        } else {
+            const double *a = compact + ((size_t)p * T + t) * B + o;
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = (use && u < nm) ? __ldcg(a + 8 * u + sub) : 0.0;
+            tailv = (use && sub < ntail) ? __ldcg(a + e0 + sub) : 0.0;
+        }
         double acc = x[0];
 #pragma unroll
         for (int u = 1; u < 16; u++)
@@ -858,6 +889,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         const double other = __shfl_xor_sync(FULL, res, 8);  // the sibling leaf
         if (use && sub == 0 && half == 0) h.val[g][i] = split ? f64_add(res, other) : res;
     }
+    PMCS(5);
     __syncthreads();
     PMCS(3);
     // perfect-tree fold of the 2^D node values: warp g folds period slot g
@@ -890,9 +922,16 @@ template <int K, int R>
 static int launch_pm_cluster_r(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
                                const EvalInit *init, int32_t *bad) {
     const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
+    constexpr size_t smem = sizeof(double) * PMC_MAXQ * PMC_OWN;
+    static bool smem_set = false;
+    if (!smem_set) {
+        CUDA_TRY(cudaFuncSetAttribute(k_pm_cluster<K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(R, np);
     cfg.blockDim = dim3(PMC_THREADS);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -920,9 +959,12 @@ static bool pm_use_r16(int device) {
                   cudaFuncSetAttribute(k_pm_cluster<1, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                       cudaSuccess;
         if (ok) {
+            cudaFuncSetAttribute(k_pm_cluster<4, PMC_R16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * PMC_MAXQ * PMC_OWN));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(PMC_R16);
             cfg.blockDim = dim3(PMC_THREADS);
+            cfg.dynamicSmemBytes = sizeof(double) * PMC_MAXQ * PMC_OWN;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = PMC_R16;

@@ -47,10 +47,10 @@ cl = nr >= 8
 if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
     t0 = min(pm[0, :nr, 0].min(), ev[:, 0].min())
     f = lambda x: (x - t0) / 1000
-    for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves"]):
+    for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves", "pre-leaf", "leaf-t0"]):
         v = pm[1, 16 + 16 * k:32 + 16 * k, 0]
         v = v[v > 0]
-        print(f"  pm {nm:8s} {f(v.min()):.2f}..{f(v.max()):.2f} us")
+        print(f"  pm {nm:8s} {f(v.min()):.2f}..{f(v.max()):.2f} us" + ("   per CTA: " + " ".join(f"{f(x):.1f}" for x in v) if "percta" in sys.argv else ""))
     print(f"PM cluster ({nr} CTAs): start {f(pm[0,:nr,0].min()):.2f}..{f(pm[0,:nr,0].max()):.2f}  scattered {f(pm[0,:nr,1].min()):.2f}..{f(pm[0,:nr,1].max()):.2f}  trees done {f(pm[1,:nr,1].min()):.2f}..{f(pm[1,:nr,1].max()):.2f} us")
 else:
     nch = (c["bm"].n_blocks + 511) // 512
