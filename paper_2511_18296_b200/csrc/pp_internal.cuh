@@ -180,18 +180,15 @@ struct TopK {
     }
 };
 template <>
-struct TopK<2> {  // k <= 2 (S <= 20): two registers, insertion rarely taken
+struct TopK<2> {  // k <= 2 (S <= 20): two registers, branch-free (lanes hold different moves)
     double a0, a1;
     __device__ __forceinline__ void init() { a0 = a1 = kInf; }
     __device__ __forceinline__ void push(double x) {
-        if (x < a1) {
-            if (x < a0) {
-                a1 = a0;
-                a0 = x;
-            } else {
-                a1 = x;
-            }
-        }
+        // the same selections as "if (x < a1) { if (x < a0) { a1 = a0; a0 = x; } else a1 = x; }"
+        const bool lt0 = x < a0;
+        const double lo = lt0 ? x : a0, hi = lt0 ? a0 : x;
+        a1 = (hi < a1) ? hi : a1;
+        a0 = lo;
     }
     __device__ __forceinline__ double mean(int k) const {
         double s = f64_add(-0.0, a0);
