@@ -13,6 +13,8 @@
 // matches the reference's numpy/Python scalar evaluation bit for bit.
 
 #include "pp_internal.cuh"
+#include <mutex>
+#include <vector>
 
 // ------------------------------------------------------------------------------------
 // error plumbing
@@ -39,6 +41,27 @@ int ensure_grid_scratch(pp_ctx *c, int grid) {
     return PP_OK;
 }
 
+
+// (kernel, device) -> largest dynamic shared memory opted in so far; returns 1 (and records it)
+// when cudaFuncSetAttribute is still needed for `bytes`
+int smem_attr_needed(const void *kern, int device, size_t bytes) {
+    struct Entry {
+        const void *kern;
+        int device;
+        size_t bytes;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> seen;
+    std::lock_guard<std::mutex> lock(mu);
+    for (Entry &e : seen)
+        if (e.kern == kern && e.device == device) {
+            if (e.bytes >= bytes) return 0;
+            e.bytes = bytes;
+            return 1;
+        }
+    seen.push_back(Entry{kern, device, bytes});
+    return 1;
+}
 
 int pick_kc(int k) {
     if (k <= 2) return 2;

@@ -588,6 +588,16 @@ inline int set_smem_attr(K kern, size_t bytes) {
     return PP_OK;
 }
 
+// cudaFuncSetAttribute(kern, MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
+// per device, and one process may drive several devices (evaluate.set_device)
+int smem_attr_needed(const void *kern, int device, size_t bytes);  // pp_context.cu (keyed by kernel)
+template <typename K>
+inline int ensure_max_smem(K kern, size_t bytes, int device) {
+    if (!smem_attr_needed(reinterpret_cast<const void *>(kern), device, bytes)) return PP_OK;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return PP_OK;
+}
+
 // resident CTAs of a kernel at this smem size (cached per instantiation)
 template <typename K>
 inline int resident_ctas(K kern, size_t smem, int device) {

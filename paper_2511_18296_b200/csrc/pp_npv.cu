@@ -367,11 +367,7 @@ int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, 
     TRY(c->npv_n.ensure(sizeof(int32_t) * (size_t)P * T));
     TRY(c->npv_flag.ensure(sizeof(int32_t)));
     CUDA_TRY(cudaMemsetAsync(c->npv_flag.ptr, 0, sizeof(int32_t), st));
-    static bool attr = false;
-    if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S2Layout::bytes()));
-        attr = true;
-    }
+    TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
     k_stage2<<<dim3(S, T, P), S2_THREADS, S2Layout::bytes(), st>>>(
         da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
         c->rate, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(), c->npv_flag.as<int32_t>());

@@ -923,11 +923,7 @@ static int launch_pm_cluster_r(pp_ctx *c, const int32_t *d_assign, int np, doubl
                                const EvalInit *init, int32_t *bad) {
     const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
     constexpr size_t smem = sizeof(double) * PMC_MAXQ * PMC_OWN;
-    static bool smem_set = false;
-    if (!smem_set) {
-        CUDA_TRY(cudaFuncSetAttribute(k_pm_cluster<K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = true;
-    }
+    TRY(ensure_max_smem(k_pm_cluster<K, R>, smem, c->device));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(R, np);
     cfg.blockDim = dim3(PMC_THREADS);
@@ -1021,11 +1017,7 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
     }
     if (init) TRY(init_eval_outputs(c, *init, st));
     const size_t smem = std::max(sizeof(PmTreeSmem), sizeof(int) * ((PM_THREADS / 32) * PM_MAXT + PM_MAXT));
-    static bool attr_done = false;
-    if (!attr_done) {
-        CUDA_TRY(cudaFuncSetAttribute(k_period_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_done = true;
-    }
+    TRY(ensure_max_smem(k_period_mass, smem, c->device));
     int32_t *flags = c->pm_flags.as<int32_t>();
     unsigned int *done = reinterpret_cast<unsigned int *>(flags + (size_t)pchunk * nchunk);
     for (int p0 = 0; p0 < P; p0 += pchunk) {
