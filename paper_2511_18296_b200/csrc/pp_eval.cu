@@ -760,7 +760,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         const bool scen = o.scen_delta != nullptr;
 #define PP_WARP(KC, SC)                                                     \
     {                                                                       \
-        TRY(set_smem_attr(k_eval_warp<KC, SC>, smem_w));                    \
+        TRY(set_smem_attr(k_eval_warp<KC, SC>, smem_w, c->device));         \
         TRY(launch_eval(k_eval_warp<KC, SC>, wgrid, smem_w, st, pdl, ep));  \
     }
         if (kcw == 0) PP_WARP(0, false)

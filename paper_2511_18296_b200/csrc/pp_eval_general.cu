@@ -289,7 +289,7 @@ static size_t eval_smem(int S, int Sp, int T, int G, bool stats, bool bigs) {
 template <int PER, int KC, bool BIGS, bool SCEN>
 static int launch_cand1(int ngroups, int G, size_t smem, cudaStream_t st, bool pdl, int device, const EvalParams &ep) {
     auto kern = k_eval_candidates<PER, KC, BIGS, SCEN>;
-    TRY(set_smem_attr(kern, smem));
+    TRY(set_smem_attr(kern, smem, device));
     const int gpc = (EV_THREADS / 32) * (32 / G);
     const int need = std::max(1, (ngroups + gpc - 1) / gpc);
     const int grid = std::min(need, resident_ctas(kern, smem, device));

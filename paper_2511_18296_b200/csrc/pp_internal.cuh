@@ -581,13 +581,6 @@ int check_schedule_range(pp_ctx *c, bool copied);
 int launch_general_candidates(int PER, int kc, bool scen, int C, int G, int S, int Sp, int T, bool stats,
                               cudaStream_t st, bool pdl, int device, const EvalParams &ep);
 
-template <typename K>
-inline int set_smem_attr(K kern, size_t bytes) {
-    // the 48 KB default covers static + dynamic; opt in with room for the kernels' static arrays
-    if (bytes > 32 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    return PP_OK;
-}
-
 // cudaFuncSetAttribute(kern, MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
 // per device, and one process may drive several devices (evaluate.set_device)
 int smem_attr_needed(const void *kern, int device, size_t bytes);  // pp_context.cu (keyed by kernel)
@@ -596,6 +589,13 @@ inline int ensure_max_smem(K kern, size_t bytes, int device) {
     if (!smem_attr_needed(reinterpret_cast<const void *>(kern), device, bytes)) return PP_OK;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     return PP_OK;
+}
+
+// the 48 KB default covers static + dynamic; opt in (once per kernel and device) with room for the
+// kernels' static arrays
+template <typename K>
+inline int set_smem_attr(K kern, size_t bytes, int device) {
+    return bytes > 32 * 1024 ? ensure_max_smem(kern, bytes, device) : PP_OK;
 }
 
 // resident CTAs of a kernel at this smem size (cached per instantiation)
