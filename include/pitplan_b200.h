@@ -207,6 +207,13 @@ PP_API int pp_set_plant(pp_ctx *ctx, const double *plant_hours, double rate);
  * than 6144 mined blocks is PP_ERR_SHAPE. */
 PP_API int pp_npv_relaxed(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, uint32_t flags, double *npv_out,
                    double *per_scen_out, int32_t mem, void *stream);
+/* Relaxed NPV of M one-block variants of a base schedule assign[B]: variant m moves block
+ * blocks[m] to periods[m] (-1 = unmine).  Only the two periods a variant changes are re-solved
+ * (S stage-2 problems each); the other periods reuse the base schedule's, and the accumulation is
+ * the reference's, so npv_out[m] equals pp_npv_relaxed of the modified schedule bit for bit (the
+ * exact move value polish_schedule compares, hybrid.py:369-376). */
+PP_API int pp_npv_moves(pp_ctx *ctx, const int32_t *assign, const int32_t *blocks, const int32_t *periods,
+                 int32_t n_moves, uint32_t flags, double *npv_out, int32_t mem, void *stream);
 /* spatial[B] = geological_consistency of every block (uncertainty.py:185-191, the factor
  * pp_set_geology computed on the device), e.g. for lns_repair's realism fallback
  * (hybrid.py:238-244, 256-260). */

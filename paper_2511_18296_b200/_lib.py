@@ -99,6 +99,8 @@ SIGNATURES = {
     "pp_repair": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_get_spatial": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_set_plant": (c_int32, [c_void_p, c_void_p, c_double]),
+    "pp_npv_moves": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_int32,
+                               c_void_p]),
     "pp_npv_relaxed": (c_int32, [c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_eject": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_double, c_void_p, c_int32, c_void_p]),
     "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),

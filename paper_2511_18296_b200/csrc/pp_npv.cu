@@ -3,6 +3,7 @@
 // (evaluate.py:166-183), bit-exact.  Population fitness of the GA loop (hybrid.py:595-606).
 #include "pp_internal.cuh"
 #include <cub/block/block_radix_sort.cuh>
+#include <vector>
 
 // ------------------------------------------------------------------------------------
 // k_stage2: one CTA per (scenario s, period t, schedule p).
@@ -142,7 +143,8 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     k_stage2(const int32_t *__restrict__ assign, int B, int T, int S, int Sp, const double *__restrict__ mass,
              const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
              double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
-             int32_t *__restrict__ too_big) {
+             int32_t *__restrict__ too_big, const int32_t *__restrict__ ovr_b, const int32_t *__restrict__ ovr_t,
+             const int32_t *__restrict__ slot_t) {
     extern __shared__ __align__(16) unsigned char s2_dyn[];
     typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
     double *dsort = reinterpret_cast<double *>(s2_dyn);  // after the sort
@@ -151,10 +153,16 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     double *qs = reinterpret_cast<double *>(s2_dyn + S2Layout::q_off());
     __shared__ int s_wc[32];
     __shared__ double s_scr[160];
-    const int s = blockIdx.x, t = blockIdx.y, p = blockIdx.z;
+    // whole schedules: grid (S, T, P), blockIdx.y = period.  One-block variants of a single base
+    // schedule (ovr_b != nullptr): grid (S, 2, M), variant m = base with block ovr_b[m] in period
+    // ovr_t[m], blockIdx.y = slot of the two periods it changes (slot_t[m][slot], -1 = none)
+    const int s = blockIdx.x, p = blockIdx.z;
+    const int t = ovr_b ? slot_t[2 * p + blockIdx.y] : (int)blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (t < 0) return;
     NPVP(0);
-    const int32_t *a = assign + (size_t)p * B;
+    const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
+    const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
     // 1. blocks mined in t, block order: warp w owns [w*chunk, (w+1)*chunk), 128 blocks per step
     //    (int4 per lane when aligned)
     const int chunk = ((B + 31) / 32 + 127) & ~127;
@@ -172,6 +180,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
 #pragma unroll
             for (int u = 0; u < 4; u++) v[u] = (b + u < hi) ? __ldg(a + b + u) : -2;
         }
+        if (ob >= b && ob < b + 4) v[ob - b] = ot;  // the variant's moved block
     };
     int cnt = 0;
     for (int b0 = lo; b0 < hi; b0 += 128) {
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         base += w < warp ? s_wc[w] : 0;
         n += s_wc[w];
     }
-    const size_t pt = ((size_t)p * T + t);
+    const size_t pt = ovr_b ? (size_t)2 * p + blockIdx.y : ((size_t)p * T + t);
     if (n > S2_NMAX) {  // outside the on-chip path: flagged, the host reports it
         if (tid == 0) {
             *too_big = 1;
@@ -325,6 +334,41 @@ __global__ void k_npv_final(int T, int S, const double *__restrict__ raw, const 
     npv[p] = total;
 }
 
+// npv of variant m: the reference's accumulation over (t, s), the two changed periods from the
+// variant's stage-2 results, every other period from the base schedule's
+__global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict__ braw, const double *__restrict__ bcost,
+                                  const int32_t *__restrict__ bn, const double *__restrict__ mraw,
+                                  const double *__restrict__ mcost, const int32_t *__restrict__ mn,
+                                  const int32_t *__restrict__ slot_t, const double *__restrict__ disc,
+                                  const double *__restrict__ sigma, double *__restrict__ npv) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const int t0 = slot_t[2 * m], t1 = slot_t[2 * m + 1];
+    double total = 0.0;
+    for (int t = 0; t < T; t++) {
+        const double *raw;
+        double cs;
+        int n;
+        if (t == t0 || t == t1) {
+            const int k = 2 * m + (t == t0 ? 0 : 1);
+            raw = mraw + (size_t)k * S;
+            cs = mcost[k];
+            n = mn[k];
+        } else {
+            raw = braw + (size_t)t * S;
+            cs = bcost[t];
+            n = bn[t];
+        }
+        const double d = disc[t];
+        if (n > 0) total = f64_sub(total, f64_mul(d, cs));
+        for (int s = 0; s < S; s++) {
+            const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
+            total = f64_add(total, f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S));
+        }
+    }
+    npv[m] = total;
+}
+
 extern "C" {
 
 int pp_set_plant(pp_ctx *c, const double *plant_hours, double rate) {
@@ -370,7 +414,8 @@ int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, 
     TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
     k_stage2<<<dim3(S, T, P), S2_THREADS, S2Layout::bytes(), st>>>(
         da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(), c->npv_flag.as<int32_t>());
+        c->rate, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(), c->npv_flag.as<int32_t>(),
+        nullptr, nullptr, nullptr);
     CUDA_TRY(cudaGetLastError());
     k_npv_final<<<P, 32, 0, st>>>(T, S, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(),
                                   c->disc.as<double>(), (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
@@ -381,6 +426,74 @@ int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, 
         CUDA_TRY(cudaMemcpyAsync(npv_out, dn, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
         if (per_scen_out)
             CUDA_TRY(cudaMemcpyAsync(per_scen_out, dps, sizeof(double) * (size_t)P * S, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(&flag, c->npv_flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(stream_wait(st));
+        if (flag) return fail(PP_ERR_SHAPE, "a period mines more than %d blocks (device stage-2 limit)", S2_NMAX);
+    }
+    return PP_OK;
+}
+
+int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
+                 uint32_t flags, double *npv_out, int32_t mem, void *stream) {
+    if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
+        return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
+    if (!assign || M < 0 || (M > 0 && (!blocks || !periods || !npv_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if ((flags & PP_USE_SIGMA) && !c->have_sigma) return fail(PP_ERR_STATE, "PP_USE_SIGMA without an uploaded sigma");
+    if (M == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B, T = c->T, S = c->S;
+    // which periods each variant changes (host arrays needed: the base assignment of the block)
+    std::vector<int32_t> hb(M), ht(M), ha(B);
+    const bool host = mem == PP_MEM_HOST;
+    if (host) {
+        std::copy(blocks, blocks + M, hb.begin());
+        std::copy(periods, periods + M, ht.begin());
+        std::copy(assign, assign + B, ha.begin());
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(hb.data(), blocks, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(ht.data(), periods, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(ha.data(), assign, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(stream_wait(st));
+    }
+    std::vector<int32_t> slot((size_t)2 * M);
+    for (int m = 0; m < M; m++) {
+        if (hb[m] < 0 || hb[m] >= B || ht[m] < -1 || ht[m] >= T) return fail(PP_ERR_INVALID_ARGS, "move %d out of range", m);
+        const int told = ha[hb[m]], tnew = ht[m];
+        slot[2 * m] = (told >= 0 && told < T && told != tnew) ? told : -1;
+        slot[2 * m + 1] = (tnew >= 0 && tnew != told) ? tnew : -1;
+    }
+    TRY(c->h_assign.ensure(sizeof(int32_t) * ((size_t)B + 4 * (size_t)M)));
+    int32_t *da = c->h_assign.as<int32_t>(), *db = da + B, *dt = db + M, *ds = dt + M;
+    CUDA_TRY(cudaMemcpyAsync(da, host ? assign : ha.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(db, hb.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dt, ht.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ds, slot.data(), sizeof(int32_t) * 2 * M, cudaMemcpyHostToDevice, st));
+    // base schedule: all (s, t); variants: the two changed periods
+    TRY(c->npv_raw.ensure(sizeof(double) * ((size_t)T * S + (size_t)2 * M * S)));
+    TRY(c->npv_cost.ensure(sizeof(double) * ((size_t)T + 2 * (size_t)M)));
+    TRY(c->npv_n.ensure(sizeof(int32_t) * ((size_t)T + 2 * (size_t)M)));
+    TRY(c->npv_flag.ensure(sizeof(int32_t)));
+    TRY(c->h_d1.ensure(sizeof(double) * M));
+    CUDA_TRY(cudaMemsetAsync(c->npv_flag.ptr, 0, sizeof(int32_t), st));
+    TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
+    double *braw = c->npv_raw.as<double>(), *mraw = braw + (size_t)T * S;
+    double *bcost = c->npv_cost.as<double>(), *mcost = bcost + T;
+    int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
+    k_stage2<<<dim3(S, T, 1), S2_THREADS, S2Layout::bytes(), st>>>(
+        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
+        c->rate, braw, bcost, bn, c->npv_flag.as<int32_t>(), nullptr, nullptr, nullptr);
+    k_stage2<<<dim3(S, 2, M), S2_THREADS, S2Layout::bytes(), st>>>(
+        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
+        c->rate, mraw, mcost, mn, c->npv_flag.as<int32_t>(), db, dt, ds);
+    double *dn = host ? c->h_d1.as<double>() : npv_out;
+    k_npv_moves_final<<<(M + 127) / 128, 128, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds,
+                                                        c->disc.as<double>(),
+                                                        (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
+    CUDA_TRY(cudaGetLastError());
+    if (host) {
+        int32_t flag = 0;
+        CUDA_TRY(cudaMemcpyAsync(npv_out, dn, sizeof(double) * M, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaMemcpyAsync(&flag, c->npv_flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
         if (flag) return fail(PP_ERR_SHAPE, "a period mines more than %d blocks (device stage-2 limit)", S2_NMAX);

@@ -342,6 +342,22 @@ class Engine:
         check(self.lib.pp_npv_relaxed(self._h, ptr(a), P, f, ptr(npv), ptr(ps), _lib.PP_MEM_HOST, None))
         return (npv, ps) if per_scenario else npv
 
+    def npv_moves(self, assign, blocks, periods, use_sigma=True):
+        """Relaxed NPV of the schedules assign with blocks[m] moved to periods[m] (one move each),
+        re-solving only the two periods a move changes; equal to npv_relaxed of each variant."""
+        bm = self._need_bm()
+        if not getattr(self, "_plant", False):
+            if not bm.single_mode_fast:
+                raise InvalidArgs("the device stage-2 path needs one mode, one rock type and a positive rate")
+            self.set_plant()
+        a = _i32(assign, bm.n_blocks, "assignment")
+        b = _i32(blocks)
+        t = _i32(periods, b.size, "periods")
+        out = np.empty(b.size, np.float64)
+        f = _lib.PP_USE_SIGMA if (use_sigma and self.has_sigma) else 0
+        check(self.lib.pp_npv_moves(self._h, ptr(a), ptr(b), ptr(t), b.size, f, ptr(out), _lib.PP_MEM_HOST, None))
+        return out
+
     def spatial(self) -> np.ndarray:
         """geological_consistency of every block (uncertainty.py:185-191), as computed on the device."""
         bm = self._need_bm()

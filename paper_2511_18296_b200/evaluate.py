@@ -384,9 +384,9 @@ ScheduleEvaluator = _make_evaluator_class()
 def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swaps=None):
     """Steepest-descent polish (hybrid.py:326-490), same result as the reference.
 
-    The single-block sweep evaluates all options of a block (other period, unmine) as one batch of
-    schedules through pp_npv_relaxed (bit-exact relaxed NPV, so the `> best + 1e-9` decisions are
-    the reference's); the small-instance swap / exchange / joint-insertion phases call the device
+    The single-block sweep evaluates all options of a block (other period, unmine) in one
+    pp_npv_moves call, which re-solves only the two periods each option changes (bit-exact relaxed
+    NPV, so the `> best + 1e-9` decisions are the reference's); the small-instance swap / exchange / joint-insertion phases call the device
     evaluator per candidate, in the reference's order.  Falls back to the reference's own
     polish_schedule when the stage-2 fast path does not apply."""
     e = _entry(instance)
@@ -441,10 +441,8 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
                     if t != orig and load[t] + masses[b] <= cap[t]:
                         options.append(t)
             best_t, best_val = orig, cur_val
-            if options:
-                batch = np.repeat(a[None, :], len(options), axis=0)
-                batch[np.arange(len(options)), b] = options
-                vals = npv_of(batch)
+            if options:  # every option re-solves only the two periods it changes
+                vals = eng.npv_moves(a, np.full(len(options), b), options, use_sigma=use_sigma)
                 for t, val in zip(options, vals.tolist()):
                     if val > best_val + 1e-9:
                         best_t, best_val = t, val

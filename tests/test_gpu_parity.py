@@ -561,3 +561,23 @@ def test_polish_schedule_dropin(small, name):
                                      max_sweeps=int(small[p + "sweeps"]))
         assert np.array_equal(out.assignment, small[p + "out"][k]), k
     dropin.clear_cache()
+
+
+def test_npv_moves_equal_full_recompute():
+    """pp_npv_moves (two periods re-solved per move) equals pp_npv_relaxed of each modified
+    schedule bit for bit: reassign, unmine, mine, same-period moves."""
+    c = config("C1")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    a = c["greedy"].copy()
+    rng = np.random.default_rng(12)
+    blocks = rng.integers(0, bm.n_blocks, 40).astype(np.int32)
+    periods = rng.integers(-1, bm.n_periods, 40).astype(np.int32)
+    periods[:3] = a[blocks[:3]]  # no-op moves
+    for use_sigma in (True, False):
+        got = eng.npv_moves(a, blocks, periods, use_sigma=use_sigma)
+        batch = np.repeat(a[None, :], blocks.size, axis=0)
+        batch[np.arange(blocks.size), blocks] = periods
+        ref = eng.npv_relaxed(batch, use_sigma=use_sigma)
+        assert same(got, ref)
+    eng.close()

@@ -23,3 +23,11 @@ oracle.build()
 o = oracle.Oracle(bm, c["tables"].vmax, c["tables"].sigma)
 t0 = time.perf_counter(); o.npv_relaxed(base, bm.plant_hours, bm.mode_rates[0]); t1 = time.perf_counter()
 print(f"oracle port (1 core) npv_relaxed: {1e3 * (t1 - t0):.1f} ms/schedule")
+# exact move values: one block's options, two periods re-solved per option
+blk = int(np.nonzero(base >= 0)[0][0])
+opts = np.array([t for t in range(-1, bm.n_periods) if t != base[blk]], dtype=np.int32)
+eng.npv_moves(base, np.full(opts.size, blk), opts)
+ts = []
+for _ in range(5):
+    t0 = time.perf_counter(); eng.npv_moves(base, np.full(opts.size, blk), opts); ts.append(time.perf_counter() - t0)
+print(f"device npv_moves ({opts.size} options of one block, incl. the base schedule): {1e3 * min(ts):.3f} ms")
