@@ -838,7 +838,7 @@ copy_out:
             }
             ht.mark("map check");
             if (ok) {
-                k_copy_out<<<dim3(32, co.nseg), 256, 0, st>>>(co);
+                k_copy_out<<<dim3(64, co.nseg), 256, 0, st>>>(co);
                 CUDA_TRY(cudaGetLastError());
                 ht.mark("d2h enqueue");
                 CUDA_TRY(stream_wait(st));
