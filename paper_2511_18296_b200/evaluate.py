@@ -30,7 +30,7 @@ from collections import OrderedDict
 import numpy as np
 
 from .engine import DEFAULT_PSI_WEIGHTS, Engine
-from .errors import InvalidArgs
+from .errors import InvalidArgs, ShapeMismatch
 from .model import BlockModel, CandidateMove, ScenarioTables, ViolationReport
 
 _MAX_CACHED = 4
@@ -328,8 +328,13 @@ class _DeviceNpv:
         e = self._dev_entry()
         if e is None:
             return None
-        r = e.engine.npv_relaxed(_assignment(schedule)[None, :], use_sigma=self._dev_args[2] is not None,
-                                 per_scenario=per_scenario)
+        try:
+            r = e.engine.npv_relaxed(_assignment(schedule)[None, :], use_sigma=self._dev_args[2] is not None,
+                                     per_scenario=per_scenario)
+        except ShapeMismatch:  # a period above the on-chip stage-2 size: the reference's own path
+            if _reference_evaluator() is None:
+                raise
+            return None
         return (float(r[0][0]), r[1][0]) if per_scenario else float(r[0])
 
 
