@@ -416,7 +416,12 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
     def npv_of(batch):
         return eng.npv_relaxed(np.asarray(batch), use_sigma=use_sigma)
 
-    cur_val = float(npv_of(a[None, :])[0])
+    try:
+        cur_val = float(npv_of(a[None, :])[0])
+    except ShapeMismatch:  # a period above the on-chip stage-2 size
+        from pitplan.hybrid import polish_schedule as ref_polish
+
+        return ref_polish(instance, evaluator, schedule, max_sweeps, pair_swaps)
     load = np.zeros(T)
     for t in range(T):
         load[t] = masses[a == t].sum()
