@@ -170,7 +170,10 @@ PP_API int pp_get_schedule(pp_ctx *ctx, int32_t *assign_out, double *period_mass
 /* ---- hot path ---------------------------------------------------------------------- */
 /* evaluate_candidates_parallel (evaluate.py:306-430) against the current schedule.
  * scenario: PP_SCENARIO_EXPECTED (s=None) or k in [0, S) (s=k).  Candidates may repeat;
- * results are in input order and independent of any launch geometry. */
+ * results are in input order and independent of any launch geometry.  Candidate ids outside
+ * [0, B) are PP_ERR_INVALID_ARGS in PP_MEM_HOST mode; in PP_MEM_DEVICE mode they are skipped
+ * (no move, no per-candidate output written).  `global` must be 16-byte aligned (it is updated
+ * with a 128-bit compare-and-swap). */
 PP_API int pp_eval_candidates(pp_ctx *ctx, const int32_t *cand, int32_t n_cand, int32_t scenario,
                        uint32_t flags, const pp_cand_out *out, int32_t mem, void *stream);
 /* Explicit moves against the current schedule: kind PP_MOVE_REASSIGN with (a=block,
