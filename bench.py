@@ -137,7 +137,7 @@ def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
     feasible move (sparse statistics output)."""
     C, T, S = c["C"], c["T"], c["S"]
     per_cand = (4 + 32 + 4 + 8 + 8 * deg_mean   # cand id, BlockRow, assign[b], unit_mean[b], adjacency ids+assign
-                + 8 * T + 8 * ((S + 1) & ~1)      # mining-cost row, vmax row (fp64, padded to 2)
+                + 8 * T + 8 * ((S + 3) & ~3)      # mining-cost row, vmax row (fp64, padded to 4)
                 + 13)                             # best (t, value, flag)
     per_pair = 4 + 4 + 8 + 8
     M = C * T
