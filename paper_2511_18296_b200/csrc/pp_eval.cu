@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     __shared__ double s_csp[EV_THREADS / 32 * CPW], s_cm[EV_THREADS / 32 * CPW], s_cu[EV_THREADS / 32 * CPW];
     __shared__ int s_pair[EV_THREADS / 32 * CPW * 32];
     __shared__ double s_tab[3][32];  // cap, disc, sig_row per period (cp.async at entry)
+    __shared__ unsigned s_okm[EV_THREADS / 32 * CPW];  // feasible-period masks (sparse pairs)
     constexpr int NW = EV_THREADS / 32;
     constexpr unsigned FULL = 0xffffffffu;
     const int T = p.T, S = p.S, Sp = p.Sp;
@@ -520,31 +521,19 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
     }
     EV_PROBE(5);
 
-    // ---- sparse pairs: one reservation per warp, lane t writes candidate j's period-t entry ----
-    if constexpr (STATS_T) {
-        if (stats && p.n_pairs) {
-            int pcum[CPW + 1];
-            pcum[0] = 0;
-#pragma unroll
-            for (int j = 0; j < CPW; j++) pcum[j + 1] = pcum[j] + (cw + j < p.C ? __popc(okm[j]) : 0);
-            int pbase = 0;
-            if (lane == 0 && pcum[CPW]) pbase = atomicAdd(p.n_pairs, pcum[CPW]);
-            pbase = __shfl_sync(FULL, pbase, 0);
-            const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-            for (int j = 0; j < CPW; j++)
-                if (cw + j < p.C && ((okm[j] >> lane) & 1u)) {
-                    const int q = pbase + pcum[j] + __popc(okm[j] & lt);
-                    p.pair_cand[q] = cw + j;
-                    p.pair_period[q] = lane;
-                    p.pair_exp[q] = w_ex[j * T + lane];
-                    p.pair_cvar[q] = w_cv[j * T + lane];
-                }
-        }
-    }
-    // ---- argmax: warp -> CTA (shared memory) -> the global record by one 128-bit
-    //      compare-and-swap per CTA (no last-CTA pass; initialised ahead of the launch) ----
+    // ---- CTA epilogue after one barrier: warp 0 merges the warps' best moves into the global
+    //      record (one 128-bit compare-and-swap per CTA, the record initialised ahead of the
+    //      launch); warp 1 reserves the CTA's sparse pairs with one atomic (not one per warp: the
+    //      counter is a single contended address) and lane t writes candidate i's period-t entry ----
     if (lane == 0) s_red[warp] = wbest;
+    const bool want_pairs = STATS_T && stats && p.n_pairs;
+    if (want_pairs) {
+        unsigned mine = 0u;  // lane j publishes candidate j's mask (okm is warp-uniform)
+#pragma unroll
+        for (int j = 0; j < CPW; j++)
+            if (lane == j) mine = okm[j];
+        if (lane < CPW) s_okm[warp * CPW + lane] = (cw + lane < p.C) ? mine : 0u;
+    }
     __syncthreads();
     if (warp == 0) {
         Best x = lane < NW ? s_red[lane] : Best{-kInf, INT_MAX, INT_MAX};
@@ -554,6 +543,28 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
             if (better(o, x)) x = o;
         }
         if (lane == 0 && x.b != INT_MAX) best_cas(p.global, x);
+    }
+    if (want_pairs && warp == (NW > 1 ? 1 : 0)) {
+        int total = 0;
+        for (int i = 0; i < NW * CPW; i++) total += __popc(s_okm[i]);
+        int pbase = 0;
+        if (lane == 0 && total) pbase = atomicAdd(p.n_pairs, total);
+        pbase = __shfl_sync(FULL, pbase, 0);
+        const unsigned lt = (1u << lane) - 1u;
+        int run = 0;
+        for (int i = 0; i < NW * CPW; i++) {
+            const unsigned m = s_okm[i];
+            if ((m >> lane) & 1u) {
+                const int wq = i / CPW, jq = i - wq * CPW;
+                const unsigned char *wb = wslices + (size_t)wq * L.total;
+                const int q = pbase + run + __popc(m & lt);
+                p.pair_cand[q] = blockIdx.x * NW * CPW + i;
+                p.pair_period[q] = lane;
+                p.pair_exp[q] = reinterpret_cast<const double *>(wb + L.ex)[jq * T + lane];
+                p.pair_cvar[q] = reinterpret_cast<const double *>(wb + L.cv)[jq * T + lane];
+            }
+            run += __popc(m);
+        }
     }
     EV_PROBE(6);
 }
