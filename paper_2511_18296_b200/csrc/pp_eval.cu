@@ -78,6 +78,8 @@ __device__ __forceinline__ void pair_stats(const EvalParams &p, int S, int T, co
 // period-mass kernel under programmatic dependent launch.
 // ------------------------------------------------------------------------------------
 constexpr int CPW = 4;  // candidates per warp
+constexpr int WV_THREADS = 256;  // k_eval_warp CTA: 8 warps (128 measured the same)
+constexpr int WV_MINB = 4;       // resident CTAs per SM (64 registers per thread)
 
 __device__ __forceinline__ int nth_bit(unsigned m, int k) {  // index of the k-th (0-based) set bit
     for (; k > 0; k--) m &= m - 1;
@@ -158,15 +160,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int KC, bool SCEN>
-__global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p) {
+__global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalParams p) {
     extern __shared__ __align__(16) unsigned char wv_dyn[];
-    __shared__ Best s_red[EV_THREADS / 32];
-    __shared__ int s_cab[EV_THREADS / 32 * CPW], s_cb[EV_THREADS / 32 * CPW], s_wcnt[EV_THREADS / 32];
-    __shared__ double s_csp[EV_THREADS / 32 * CPW], s_cm[EV_THREADS / 32 * CPW], s_cu[EV_THREADS / 32 * CPW];
-    __shared__ int s_pair[EV_THREADS / 32 * CPW * 32];
+    __shared__ Best s_red[WV_THREADS / 32];
+    __shared__ int s_cab[WV_THREADS / 32 * CPW], s_cb[WV_THREADS / 32 * CPW], s_wcnt[WV_THREADS / 32];
+    __shared__ double s_csp[WV_THREADS / 32 * CPW], s_cm[WV_THREADS / 32 * CPW], s_cu[WV_THREADS / 32 * CPW];
+    __shared__ int s_pair[WV_THREADS / 32 * CPW * 32];
     __shared__ double s_tab[3][32];  // cap, disc, sig_row per period (cp.async at entry)
-    __shared__ unsigned s_okm[EV_THREADS / 32 * CPW];  // feasible-period masks (sparse pairs)
-    constexpr int NW = EV_THREADS / 32;
+    __shared__ unsigned s_okm[WV_THREADS / 32 * CPW];  // feasible-period masks (sparse pairs)
+    constexpr int NW = WV_THREADS / 32;
     constexpr unsigned FULL = 0xffffffffu;
     const int T = p.T, S = p.S, Sp = p.Sp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
 #pragma unroll
     for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
     if (stats)  // sigma [S][T] for the pair statistics, staged once per CTA
-        for (int e = threadIdx.x; e < S * T; e += EV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+        for (int e = threadIdx.x; e < S * T; e += WV_THREADS) cp_async8(s_sig + e, p.sigma + e);
     if (threadIdx.x < T) {
         cp_async8(&s_tab[0][threadIdx.x], p.cap + threadIdx.x);
         cp_async8(&s_tab[1][threadIdx.x], p.disc + threadIdx.x);
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(EV_THREADS, 4) k_eval_warp(const EvalParams p)
             }
             __syncthreads();
             EV_PROBE(8);
-            for (int k = threadIdx.x; k < total; k += EV_THREADS) {
+            for (int k = threadIdx.x; k < total; k += WV_THREADS) {
                 const int e = s_pair[k], i = e >> 8, t = e & 0xff;
                 const int wq = i / CPW, jq = i - wq * CPW;
                 unsigned char *wb = wslices + (size_t)wq * L.total;
@@ -758,8 +760,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 8 ? 8 : -1;  // -1: warp per move
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
                                           kcw < 0 ? big_pow2(S) : 0);
-        const size_t smem_w = (size_t)Lw.total * (EV_THREADS / 32) + sig_bytes(S, T, stats);
-        const int per_cta = CPW * (EV_THREADS / 32);
+        const size_t smem_w = (size_t)Lw.total * (WV_THREADS / 32) + sig_bytes(S, T, stats);
+        const int per_cta = CPW * (WV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));
         if (reinterpret_cast<uintptr_t>(o.global) & 15u)
@@ -772,7 +774,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 #define PP_WARP(KC, SC)                                                     \
     {                                                                       \
         TRY(set_smem_attr(k_eval_warp<KC, SC>, smem_w, c->device));         \
-        TRY(launch_eval(k_eval_warp<KC, SC>, wgrid, smem_w, st, pdl, ep));  \
+        TRY(launch_eval_n(k_eval_warp<KC, SC>, wgrid, WV_THREADS, smem_w, st, pdl, ep));  \
     }
         if (kcw == 0) PP_WARP(0, false)
         else if (kcw == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }

@@ -557,6 +557,24 @@ inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream
     if (e != cudaSuccess) return fail(PP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return PP_OK;
 }
+template <typename... KArgs, typename... Args>
+inline int launch_eval_n(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t st, bool pdl,
+                         Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const bool no_pdl = std::getenv("PP_NO_PDL") != nullptr;  // diagnostics: serialise the launches
+    cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return PP_OK;
+}
 
 
 // ---- shared host helpers (pp_context.cu, pp_schedule.cu) ----

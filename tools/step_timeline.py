@@ -17,7 +17,7 @@ out = {"best_t": torch.empty(C, dtype=torch.int32, device=dev), "best_val": torc
        "feasible": torch.empty(C, dtype=torch.uint8, device=dev), "exp_delta": torch.empty(C, T, dtype=torch.float64, device=dev),
        "cvar": torch.empty(C, T, dtype=torch.float64, device=dev), "global": torch.empty(2, dtype=torch.float64, device=dev)}
 flush = torch.empty(256 << 18, dtype=torch.int32, device=dev)
-grid = (C + 31) // 32
+grid = (C + 31) // 32  # k_eval_warp: 32 candidates per CTA
 g = torch.cuda.CUDAGraph()
 for _ in range(3):
     eng.set_schedule_device(assign_d, stream=sp, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=sp)
