@@ -1,0 +1,7 @@
+#!/bin/bash
+# Build the microbenchmarks into tools/bin (git-ignored; they travel to the GPU box with gpurun).
+set -e
+cd "$(dirname "$0")"
+mkdir -p bin
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o bin/f64_latency f64_latency.cu
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/globaltimer_resolution globaltimer_resolution.cu
