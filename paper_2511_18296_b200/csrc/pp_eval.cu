@@ -211,28 +211,14 @@ __global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalPar
         cp_async8(&s_tab[1][threadIdx.x], p.disc + threadIdx.x);
         cp_async8(&s_tab[2][threadIdx.x], p.sig_row + threadIdx.x);
     }
-    // per-candidate scalars to shared memory (read by the pair pool and the moves)
-    if (lane < CPW) {
-        double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
-        int ab_l = -1;
-        if (bl >= 0) {
-            mass_l = __ldg(&p.rows[bl].mass);
-            spat_l = __ldg(&p.rows[bl].spatial);
-            ab_l = __ldg(p.assign + bl);
-            if (want_unit) unit_l = __ldg(p.unit_mean + bl);
-        }
-        const int i = warp * CPW + lane;
-        s_cm[i] = mass_l;
-        s_csp[i] = spat_l;
-        s_cu[i] = unit_l;
-        s_cab[i] = ab_l;
-        s_cb[i] = bl;
-    }
+    // every independent load of the warp's candidates is issued before any result is used (a
+    // store of a loaded value would hold the warp until that load returns): neighbour ids, mining
+    // costs, vmax rows, the per-candidate scalars; then the neighbours' periods
     int nb[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
-        if (net && lane < T && b[j] >= 0) cp_async8(w_cost + j * T + lane, p.cost + (size_t)b[j] * T + lane);
         nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
+        if (net && lane < T && b[j] >= 0) cp_async8(w_cost + j * T + lane, p.cost + (size_t)b[j] * T + lane);
     }
     if (need_vrow) {
 #pragma unroll
@@ -241,11 +227,27 @@ __global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalPar
                 for (int q = lane; q < (Sp >> 1); q += 32)
                     cp_async16(w_vrow + (size_t)j * Sp + 2 * q, p.vmax + (size_t)b[j] * Sp + 2 * q);
     }
+    double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
+    int ab_l = -1;
+    if (lane < CPW && bl >= 0) {
+        mass_l = __ldg(&p.rows[bl].mass);
+        spat_l = __ldg(&p.rows[bl].spatial);
+        ab_l = __ldg(p.assign + bl);
+        if (want_unit) unit_l = __ldg(p.unit_mean + bl);
+    }
     // neighbour periods -> precedence window (evaluate.py:361-372): lo = latest predecessor
     // period (an unmined predecessor forbids every period), hi = earliest mined successor
     int tn[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) tn[j] = nb[j] >= 0 ? p.assign[nb[j] & (NBR_SUCC - 1)] : 0;
+    if (lane < CPW) {  // per-candidate scalars to shared memory (the pair pool and the moves)
+        const int i = warp * CPW + lane;
+        s_cm[i] = mass_l;
+        s_csp[i] = spat_l;
+        s_cu[i] = unit_l;
+        s_cab[i] = ab_l;
+        s_cb[i] = bl;
+    }
     unsigned win[CPW];  // precedence window of candidate j as a period mask (lane t = period t)
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
