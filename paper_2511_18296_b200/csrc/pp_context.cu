@@ -36,7 +36,7 @@ int ensure_grid_scratch(pp_ctx *c, int grid) {
     TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
     if (c->counter.bytes == 0) {
         TRY(c->counter.ensure(sizeof(unsigned int) * 4));
-        CUDA_TRY(cudaMemset(c->counter.ptr, 0, c->counter.bytes));
+        CUDA_TRY(dev_zero(c, c->counter.ptr, c->counter.bytes));
     }
     return PP_OK;
 }

@@ -517,6 +517,18 @@ inline int use_device(pp_ctx *c) {
 
 inline cudaStream_t pick(pp_ctx *c, void *stream) { return stream ? (cudaStream_t)stream : c->stream; }
 
+// Setup-time upload / clear, complete on return.  Every table goes through the context stream:
+// c->stream is non-blocking, so a plain cudaMemcpy / cudaMemset (legacy default stream) is NOT
+// ordered before kernels on it, and a pageable cudaMemcpy may return before its DMA lands.
+inline cudaError_t dev_upload(pp_ctx *c, void *dst, const void *src, size_t bytes) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+    return e == cudaSuccess ? cudaStreamSynchronize(c->stream) : e;
+}
+inline cudaError_t dev_zero(pp_ctx *c, void *dst, size_t bytes) {
+    cudaError_t e = cudaMemsetAsync(dst, 0, bytes, c->stream);
+    return e == cudaSuccess ? cudaStreamSynchronize(c->stream) : e;
+}
+
 // host copy of numpy's pairwise sum (for np.mean(capacity), evaluate.py:103)
 inline double host_pairwise(const double *a, long n) {
     if (n < 8) {

@@ -377,7 +377,7 @@ int pp_set_plant(pp_ctx *c, const double *plant_hours, double rate) {
     if (!(rate > 0)) return fail(PP_ERR_INVALID_ARGS, "the stage-2 fast path needs a positive rate");
     TRY(use_device(c));
     TRY(c->hours.ensure(sizeof(double) * c->T));
-    CUDA_TRY(cudaMemcpy(c->hours.ptr, plant_hours, sizeof(double) * c->T, cudaMemcpyHostToDevice));
+    CUDA_TRY(dev_upload(c, c->hours.ptr, plant_hours, sizeof(double) * c->T));
     c->rate = rate;
     c->have_plant = true;
     return PP_OK;

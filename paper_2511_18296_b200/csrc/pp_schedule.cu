@@ -997,7 +997,7 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
     const size_t nflags = (size_t)pchunk * nchunk + 2 * (size_t)pchunk;
     if (c->pm_flags_n < nflags) {
         TRY(c->pm_flags.ensure(sizeof(int32_t) * nflags));
-        CUDA_TRY(cudaMemset(c->pm_flags.ptr, 0, sizeof(int32_t) * nflags));
+        CUDA_TRY(dev_zero(c, c->pm_flags.ptr, sizeof(int32_t) * nflags));
         c->pm_flags_n = nflags;
     }
     if (pm_cluster_path(c)) {
@@ -1052,7 +1052,7 @@ int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st) {
         if (!c->best_none.ptr) {
             TRY(c->best_none.ensure(sizeof(pp_best)));
             const pp_best none{-std::numeric_limits<double>::infinity(), -1, -1};
-            CUDA_TRY(cudaMemcpy(c->best_none.ptr, &none, sizeof(pp_best), cudaMemcpyHostToDevice));
+            CUDA_TRY(dev_upload(c, c->best_none.ptr, &none, sizeof(pp_best)));
         }
         CUDA_TRY(cudaMemcpyAsync(init.best, c->best_none.ptr, sizeof(pp_best), cudaMemcpyDeviceToDevice, st));
     }
@@ -1186,14 +1186,14 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
     TRY(c->mass.ensure(sizeof(double) * B));
     TRY(c->pm.ensure(sizeof(double) * T));
     std::vector<double> ones(T, 1.0);
-    CUDA_TRY(cudaMemcpy(c->rows.ptr, rows.data(), sizeof(BlockRow) * B, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->adj.ptr, adj.data(), sizeof(int) * adj.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->cost.ptr, cost, sizeof(double) * (size_t)B * T, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->mass.ptr, mass, sizeof(double) * B, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->cap.ptr, capacity, sizeof(double) * T, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->disc.ptr, discount, sizeof(double) * T, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->ones_t.ptr, ones.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->level_blocks.ptr, lblocks.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+    CUDA_TRY(dev_upload(c, c->rows.ptr, rows.data(), sizeof(BlockRow) * B));
+    CUDA_TRY(dev_upload(c, c->adj.ptr, adj.data(), sizeof(int) * adj.size()));
+    CUDA_TRY(dev_upload(c, c->cost.ptr, cost, sizeof(double) * (size_t)B * T));
+    CUDA_TRY(dev_upload(c, c->mass.ptr, mass, sizeof(double) * B));
+    CUDA_TRY(dev_upload(c, c->cap.ptr, capacity, sizeof(double) * T));
+    CUDA_TRY(dev_upload(c, c->disc.ptr, discount, sizeof(double) * T));
+    CUDA_TRY(dev_upload(c, c->ones_t.ptr, ones.data(), sizeof(double) * T));
+    CUDA_TRY(dev_upload(c, c->level_blocks.ptr, lblocks.data(), sizeof(int) * B));
     c->B = B;
     c->T = T;
     c->E = E;
@@ -1209,7 +1209,7 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
             for (int k = 0; k < npred[b] + nsucc[b]; k++)
                 nbr[(size_t)b * 32 + k] = adj[start[b] + k] | (k < npred[b] ? 0 : (1 << 30));
         TRY(c->nbr.ensure(sizeof(int) * nbr.size()));
-        CUDA_TRY(cudaMemcpy(c->nbr.ptr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice));
+        CUDA_TRY(dev_upload(c, c->nbr.ptr, nbr.data(), sizeof(int) * nbr.size()));
     } else {
         c->nbr.release();
     }
@@ -1236,9 +1236,9 @@ int pp_set_geology(pp_ctx *c, const double *alt, const double *strc, const doubl
     int rc = tmp.ensure(sizeof(double) * 3 * (size_t)B);
     if (rc) return rc;
     double *d = tmp.as<double>();
-    cudaError_t e = cudaMemcpy(d, alt, sizeof(double) * B, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + B, strc, sizeof(double) * B, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + 2 * (size_t)B, dist, sizeof(double) * B, cudaMemcpyHostToDevice);
+    cudaError_t e = dev_upload(c, d, alt, sizeof(double) * B);
+    if (e == cudaSuccess) e = dev_upload(c, d + B, strc, sizeof(double) * B);
+    if (e == cudaSuccess) e = dev_upload(c, d + 2 * (size_t)B, dist, sizeof(double) * B);
     if (e == cudaSuccess) {
         k_spatial<<<(B + 255) / 256, 256, 0, c->stream>>>(c->rows.as<BlockRow>(), B, d, d + B, d + 2 * (size_t)B, w1,
                                                           w2, w3, diameter);
@@ -1267,7 +1267,7 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     TRY(c->plan_dev.ensure(sizeof(int) * kPlanWords));
     DevBuf tmp;
     TRY(tmp.ensure(sizeof(double) * (size_t)S * B));
-    cudaError_t e = cudaMemcpy(tmp.ptr, vmax_sb, sizeof(double) * (size_t)S * B, cudaMemcpyHostToDevice);
+    cudaError_t e = dev_upload(c, tmp.ptr, vmax_sb, sizeof(double) * (size_t)S * B);
     if (e == cudaSuccess) {
         k_scen_tables<<<(B + 255) / 256, 256, 0, c->stream>>>(tmp.as<double>(), S, B, Sp, c->vmax.as<double>(),
                                                               c->unit_mean.as<double>());
@@ -1276,10 +1276,10 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     std::vector<double> ones((size_t)S * T, 1.0);
     int words[kPlanWords];
     plan_words(plan, words);
-    if (e == cudaSuccess) e = cudaMemcpy(c->plan_dev.ptr, words, sizeof(words), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(c->ones_st.ptr, ones.data(), sizeof(double) * ones.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = dev_upload(c, c->plan_dev.ptr, words, sizeof(words));
+    if (e == cudaSuccess) e = dev_upload(c, c->ones_st.ptr, ones.data(), sizeof(double) * ones.size());
     if (e == cudaSuccess && sigma_st) {
-        e = cudaMemcpy(c->sigma.ptr, sigma_st, sizeof(double) * (size_t)S * T, cudaMemcpyHostToDevice);
+        e = dev_upload(c, c->sigma.ptr, sigma_st, sizeof(double) * (size_t)S * T);
         if (e == cudaSuccess) {
             k_sig_mean<<<(T + 127) / 128, 128, 0, c->stream>>>(c->sigma.as<double>(), S, T, c->sig_mean.as<double>());
             e = cudaGetLastError();
@@ -1309,7 +1309,7 @@ int pp_set_schedule(pp_ctx *c, const int32_t *assign, int32_t mem, void *stream)
     if (mem == PP_MEM_HOST && pm_cluster_path(c)) {  // range-checked by k_pm_cluster on the device
         if (!c->pm_bad.ptr) {
             TRY(c->pm_bad.ensure(sizeof(int32_t) * PMC_R16));
-            CUDA_TRY(cudaMemset(c->pm_bad.ptr, 0, sizeof(int32_t) * PMC_R16));
+            CUDA_TRY(dev_zero(c, c->pm_bad.ptr, sizeof(int32_t) * PMC_R16));
             CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_bad), sizeof(int32_t) * PMC_R16,
                                    cudaHostAllocPortable | cudaHostAllocMapped));
         }

@@ -42,6 +42,17 @@ for it in range(iters):
                         _, pm = eng.get_schedule()
                         again = eng.eval_candidates(cand, s, net=net, trace=True, stats=True, scen=True)[k]
                         rep = bool(np.all((again == y) | (np.isnan(again) & np.isnan(y))))
+                        sp_ok = np.array_equal(eng.spatial(), o.spatial)
+                        eng.set_schedule(assign)
+                        again2 = eng.eval_candidates(cand, s, net=net, trace=True, stats=True, scen=True)[k]
+                        rep2 = bool(np.all((again2 == y) | (np.isnan(again2) & np.isnan(y))))
+                        e2 = Engine.from_tables(bm, ScenarioTables(vmax, sigma), assign)
+                        again3 = e2.eval_candidates(cand, s, net=net, trace=True, stats=True, scen=True)[k]
+                        e2.close()
+                        rep3 = bool(np.all((again3 == y) | (np.isnan(again3) & np.isnan(y))))
+                        rows = np.unique(idx[:, 0])
+                        print(f"   spatial ok {sp_ok}; after set_schedule correct={rep2}; fresh engine correct={rep3};"
+                              f" bad rows {rows[:20].tolist()} (of {rows.size}) blocks {cand[rows[:20]].tolist()}", flush=True)
                         print(f"it{it} T={T} S={S} s={s} net={net} {k}: {badm.sum()} bad; first {idx[:3].tolist()}"
                               f" got {x[tuple(idx[0])]!r} ref {y[tuple(idx[0])]!r}; pm ok {np.array_equal(pm, o.period_mass(assign))};"
                               f" immediate rerun correct={rep}", flush=True)
