@@ -175,6 +175,23 @@ def test_shapes_against_oracle(oracle_lib, T, S):
     eng.close()
 
 
+def test_setup_uploads_ordered_before_first_eval(oracle_lib):
+    """Fresh engines evaluated right after set_scenarios: the value table (tens of MB, pageable)
+    must have landed before the first kernel on the context's non-blocking stream reads it."""
+    from paper_2511_18296_b200 import synth
+
+    bm, vmax, sigma = _rand_instance(3, n=(40, 30, 12), T=12, S=300)
+    assign = synth.full_greedy(bm)
+    cand = np.random.default_rng(1).integers(0, bm.n_blocks, size=4096).astype(np.int32)
+    o = oracle_lib.Oracle(bm, vmax, sigma)
+    ref = o.eval_candidates(assign, cand, None)
+    for _ in range(8):
+        eng = Engine.from_tables(bm, ScenarioTables(vmax, sigma), assign)
+        got = eng.eval_candidates(cand, None)
+        eng.close()
+        _same_res(got, ref, ("best_t", "best_val", "feasible"))
+
+
 def test_explicit_moves_against_oracle(oracle_lib):
     bm, vmax, sigma = _rand_instance(5, n=(12, 10, 6), T=9, S=20, cf=0.45)
     from paper_2511_18296_b200 import synth
