@@ -81,6 +81,45 @@ constexpr int CPW = 4;  // candidates per warp
 constexpr int WV_THREADS = 256;  // k_eval_warp CTA: 8 warps (128 measured the same)
 constexpr int WV_MINB = 4;       // resident CTAs per SM (64 registers per thread)
 
+// order-preserving map of a double onto u64 (NaN after +inf, as np.sort places it)
+__device__ __forceinline__ unsigned long long f64_key(double v) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    if (v != v) return ~0ull - 1ull;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_f64(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
+}
+__device__ __forceinline__ void ce_u64(unsigned long long &a, unsigned long long &b) {
+    const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+// The k smallest of the warp's 8 x 32 keys (lane l holds elements l + 32 r), ascending, into
+// out[0..k): a per-lane sorting network, then k rounds of a warp-wide minimum over the lane
+// heads (two 32-bit redux.sync) in which the winning lane pops its head.
+__device__ __forceinline__ void warp_k_smallest(unsigned long long (&k8)[8], int k, double *out) {
+    ce_u64(k8[0], k8[1]); ce_u64(k8[2], k8[3]); ce_u64(k8[4], k8[5]); ce_u64(k8[6], k8[7]);
+    ce_u64(k8[0], k8[2]); ce_u64(k8[1], k8[3]); ce_u64(k8[4], k8[6]); ce_u64(k8[5], k8[7]);
+    ce_u64(k8[1], k8[2]); ce_u64(k8[5], k8[6]);
+    ce_u64(k8[0], k8[4]); ce_u64(k8[1], k8[5]); ce_u64(k8[2], k8[6]); ce_u64(k8[3], k8[7]);
+    ce_u64(k8[2], k8[4]); ce_u64(k8[3], k8[5]);
+    ce_u64(k8[1], k8[2]); ce_u64(k8[3], k8[4]); ce_u64(k8[5], k8[6]);
+    const int lane = threadIdx.x & 31;
+    for (int r = 0; r < k; r++) {
+        const unsigned hi = (unsigned)(k8[0] >> 32), lo = (unsigned)k8[0];
+        const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+        const unsigned who = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+        if (lane == 0) out[r] = key_f64(((unsigned long long)mhi << 32) | mlo);
+        if (lane == __ffs(who) - 1) {
+#pragma unroll
+            for (int i = 0; i < 7; i++) k8[i] = k8[i + 1];
+            k8[7] = ~0ull;
+        }
+    }
+}
+
 __device__ __forceinline__ int nth_bit(unsigned m, int k) {  // index of the k-th (0-based) set bit
     for (; k > 0; k--) m &= m - 1;
     return __ffs(m) - 1;
@@ -160,7 +199,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int KC, bool SCEN>
-__global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalParams p) {
+__global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(const EvalParams p) {
     extern __shared__ __align__(16) unsigned char wv_dyn[];
     __shared__ Best s_red[WV_THREADS / 32];
     __shared__ int s_cab[WV_THREADS / 32 * CPW], s_cb[WV_THREADS / 32 * CPW], s_wcnt[WV_THREADS / 32];
@@ -423,17 +462,21 @@ __global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalPar
                     const int t = __ffs(mm) - 1;
                     const double d_t = __ldg(p.disc + t);
                     const double dc_t = net ? f64_mul(d_t, w_cost[j * T + t]) : 0.0;
-                    for (int s_ = lane; s_ < P2; s_ += 32) {
-                        double v = kInf;  // padding sorts last
+                    unsigned long long k8[8];  // element lane + 32 r as a sort key; padding last
+#pragma unroll
+                    for (int r = 0; r < 8; r++) {
+                        const int s_ = lane + 32 * r;
+                        k8[r] = ~0ull;
                         if (s_ < S) {
                             const double x = rowb[s_];
                             const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
                             const double vo =
                                 mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
-                            v = f64_sub(vn, vo);
+                            const double v = f64_sub(vn, vo);
                             if constexpr (SCEN) p.scen_delta[((size_t)(cw + j) * S + s_) * T + t] = (float)v;
+                            vb[s_] = v;
+                            k8[r] = f64_key(v);
                         }
-                        vb[s_] = v;
                     }
                     __syncwarp();
                     // expected delta: numpy pairwise over d[0..S) (the plan's leaves, 8 lanes each)
@@ -457,21 +500,10 @@ __global__ void __launch_bounds__(WV_THREADS, WV_MINB) k_eval_warp(const EvalPar
                         }
                     }
                     __syncwarp();
-                    // CVaR10: bitonic sort ascending, then the mean of the k smallest (saa.py:157-164)
-                    for (int k2 = 2; k2 <= P2; k2 <<= 1)
-                        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
-                            for (int i = lane; i < P2; i += 32) {
-                                const int q = i ^ jj;
-                                if (q > i) {
-                                    const double a = vb[i], b2 = vb[q];
-                                    if ((a > b2) == ((i & k2) == 0)) {
-                                        vb[i] = b2;
-                                        vb[q] = a;
-                                    }
-                                }
-                            }
-                            __syncwarp();
-                        }
+                    // CVaR10: the k smallest in ascending order (np.sort, saa.py:157-164) over the
+                    // deltas just consumed by the mean, then their pairwise mean
+                    warp_k_smallest(k8, kq, vb);
+                    __syncwarp();
                     const int kn = kq >> 3;
                     double cacc = 0.0;
                     if (lane < 8 && kn > 0) {
