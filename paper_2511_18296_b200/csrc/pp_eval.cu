@@ -440,99 +440,122 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(
         }
     }
     // ---- KC < 0: statistics of the feasible moves, one warp per move (after the capacity
-    //      test: with many scenarios the statistics dominate, so only feasible moves pay) ----
+    //      test: with many scenarios the statistics dominate, so only feasible moves pay).  The
+    //      CTA's feasible moves are dealt round-robin to its warps (a warp's own four candidates
+    //      hold anywhere from 0 to 60 of them) ----
     if constexpr (KC < 0) {
         if (stats) {
+            static_assert(NW * CPW == 32, "one lane per candidate of the CTA");
+            {
+                unsigned mine = 0u;
+#pragma unroll
+                for (int j = 0; j < CPW; j++)
+                    if (lane == j) mine = okm[j];
+                if (lane < CPW) s_okm[warp * CPW + lane] = mine;
+            }
+            __syncthreads();
+            const unsigned om = s_okm[lane];  // lane i: candidate i of the CTA
+            int incl = __popc(om);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - __popc(om);
+            const int nmoves = __shfl_sync(FULL, incl, 31);
             const int P2 = big_pow2(S);
             double *vb = reinterpret_cast<double *>(wbase + L.big);
             double *lv = vb + P2;
             const int *P = p.plan;
             const int nleaf = __ldg(P + 1);
             const int kq = p.cvar_k;
-            for (int j = 0; j < CPW; j++) {
-                const int ci = warp * CPW + j;
+            for (int mv = warp; mv < nmoves; mv += NW) {
+                const int ci = __ffs(__ballot_sync(FULL, excl <= mv && mv < incl)) - 1;
+                const int t = nth_bit(__shfl_sync(FULL, om, ci), mv - __shfl_sync(FULL, excl, ci));
+                const int wq = ci / CPW, jq = ci - wq * CPW;
+                unsigned char *wb = wslices + (size_t)wq * L.total;
+                const double *crow = reinterpret_cast<const double *>(wb + L.cost) + jq * T;
+                const double *rowb = reinterpret_cast<const double *>(wb + L.vrow) + (size_t)jq * Sp;
                 const int ab = s_cab[ci];
                 const double sp = s_csp[ci];
                 const bool mined = ab >= 0;
                 const int abc = mined ? ab : 0;
-                const double d_ab = __ldg(p.disc + abc);
-                const double dc_ab = net ? f64_mul(d_ab, w_cost[j * T + abc]) : 0.0;
-                const double *rowb = w_vrow + (size_t)j * Sp;
-                for (unsigned mm = okm[j]; mm; mm &= mm - 1) {  // warp-uniform
-                    const int t = __ffs(mm) - 1;
-                    const double d_t = __ldg(p.disc + t);
-                    const double dc_t = net ? f64_mul(d_t, w_cost[j * T + t]) : 0.0;
-                    unsigned long long k8[8];  // element lane + 32 r as a sort key; padding last
+                const double d_ab = s_tab[1][abc];
+                const double dc_ab = net ? f64_mul(d_ab, crow[abc]) : 0.0;
+                const double d_t = s_tab[1][t];
+                const double dc_t = net ? f64_mul(d_t, crow[t]) : 0.0;
+                const size_t g = (size_t)blockIdx.x * NW * CPW + ci;
+                unsigned long long k8[8];  // element lane + 32 r as a sort key; padding last
 #pragma unroll
-                    for (int r = 0; r < 8; r++) {
-                        const int s_ = lane + 32 * r;
-                        k8[r] = ~0ull;
-                        if (s_ < S) {
-                            const double x = rowb[s_];
-                            const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
-                            const double vo =
-                                mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
-                            const double v = f64_sub(vn, vo);
-                            if constexpr (SCEN) p.scen_delta[((size_t)(cw + j) * S + s_) * T + t] = (float)v;
-                            vb[s_] = v;
-                            k8[r] = f64_key(v);
-                        }
+                for (int r = 0; r < 8; r++) {
+                    const int s_ = lane + 32 * r;
+                    k8[r] = ~0ull;
+                    if (s_ < S) {
+                        const double x = rowb[s_];
+                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
+                        const double vo =
+                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
+                        const double v = f64_sub(vn, vo);
+                        if constexpr (SCEN) p.scen_delta[(g * S + s_) * T + t] = (float)v;
+                        vb[s_] = v;
+                        k8[r] = f64_key(v);
                     }
-                    __syncwarp();
-                    // expected delta: numpy pairwise over d[0..S) (the plan's leaves, 8 lanes each)
-                    for (int l0 = 0; l0 < nleaf; l0 += 4) {
-                        const int l = l0 + (lane >> 3), sub = lane & 7;
-                        const bool act = l < nleaf;
-                        const int ls = act ? __ldg(P + 2 + l) : 0, len = act ? __ldg(P + 2 + kMaxLeaves + l) : 0;
-                        const int nm = len >> 3;
-                        double acc = 0.0;
-                        if (nm > 0) {
-                            acc = vb[ls + sub];
-                            for (int u = 1; u < nm; u++) acc = f64_add(acc, vb[ls + 8 * u + sub]);
-                        }
-                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
-                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
-                        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
-                        if (act && sub == 0) {
-                            double r = len >= 8 ? acc : -0.0;
-                            for (int i = len - (len & 7); i < len; i++) r = f64_add(r, vb[ls + i]);
-                            lv[l] = r;
-                        }
-                    }
-                    __syncwarp();
-                    // CVaR10: the k smallest in ascending order (np.sort, saa.py:157-164) over the
-                    // deltas just consumed by the mean, then their pairwise mean
-                    warp_k_smallest(k8, kq, vb);
-                    __syncwarp();
-                    const int kn = kq >> 3;
-                    double cacc = 0.0;
-                    if (lane < 8 && kn > 0) {
-                        cacc = vb[lane];
-                        for (int u = 1; u < kn; u++) cacc = f64_add(cacc, vb[8 * u + lane]);
-                    }
-                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 1));
-                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 2));
-                    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 4));
-                    if (lane == 0) {
-                        double r = kq >= 8 ? cacc : -0.0;
-                        for (int i = kq - (kq & 7); i < kq; i++) r = f64_add(r, vb[i]);
-                        w_cv[j * T + t] = f64_div(f64_add(0.0, r), (double)kq);
-                        double stk[8];
-                        int sp_ = 0;
-                        for (int l = 0; l < nleaf; l++) {  // numpy's recursion, post-order
-                            stk[sp_++] = lv[l];
-                            const int nadd = __ldg(P + 2 + 2 * kMaxLeaves + l);
-                            for (int a = 0; a < nadd; a++) {
-                                const double rhs = stk[--sp_];
-                                const double lhs = stk[--sp_];
-                                stk[sp_++] = f64_add(lhs, rhs);
-                            }
-                        }
-                        w_ex[j * T + t] = f64_div(f64_add(0.0, stk[0]), (double)S);
-                    }
-                    __syncwarp();
                 }
+                __syncwarp();
+                // expected delta: numpy pairwise over d[0..S) (the plan's leaves, 8 lanes each)
+                for (int l0 = 0; l0 < nleaf; l0 += 4) {
+                    const int l = l0 + (lane >> 3), sub = lane & 7;
+                    const bool act = l < nleaf;
+                    const int ls = act ? __ldg(P + 2 + l) : 0, len = act ? __ldg(P + 2 + kMaxLeaves + l) : 0;
+                    const int nm = len >> 3;
+                    double acc = 0.0;
+                    if (nm > 0) {
+                        acc = vb[ls + sub];
+                        for (int u = 1; u < nm; u++) acc = f64_add(acc, vb[ls + 8 * u + sub]);
+                    }
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
+                    acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
+                    if (act && sub == 0) {
+                        double r = len >= 8 ? acc : -0.0;
+                        for (int i = len - (len & 7); i < len; i++) r = f64_add(r, vb[ls + i]);
+                        lv[l] = r;
+                    }
+                }
+                __syncwarp();
+                // CVaR10: the k smallest in ascending order (np.sort, saa.py:157-164) over the
+                // deltas just consumed by the mean, then their pairwise mean
+                warp_k_smallest(k8, kq, vb);
+                __syncwarp();
+                const int kn = kq >> 3;
+                double cacc = 0.0;
+                if (lane < 8 && kn > 0) {
+                    cacc = vb[lane];
+                    for (int u = 1; u < kn; u++) cacc = f64_add(cacc, vb[8 * u + lane]);
+                }
+                cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 1));
+                cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 2));
+                cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 4));
+                if (lane == 0) {
+                    double r = kq >= 8 ? cacc : -0.0;
+                    for (int i = kq - (kq & 7); i < kq; i++) r = f64_add(r, vb[i]);
+                    reinterpret_cast<double *>(wb + L.cv)[jq * T + t] = f64_div(f64_add(0.0, r), (double)kq);
+                    double stk[8];
+                    int sp_ = 0;
+                    for (int l = 0; l < nleaf; l++) {  // numpy's recursion, post-order
+                        stk[sp_++] = lv[l];
+                        const int nadd = __ldg(P + 2 + 2 * kMaxLeaves + l);
+                        for (int a = 0; a < nadd; a++) {
+                            const double rhs = stk[--sp_];
+                            const double lhs = stk[--sp_];
+                            stk[sp_++] = f64_add(lhs, rhs);
+                        }
+                    }
+                    reinterpret_cast<double *>(wb + L.ex)[jq * T + t] = f64_div(f64_add(0.0, stk[0]), (double)S);
+                }
+                __syncwarp();
             }
+            __syncthreads();  // the owners' dense outputs read these statistics
         }
     }
     EV_PROBE(4);
