@@ -199,7 +199,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int KC, bool SCEN>
-__global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(const EvalParams p) {
+__global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(const EvalParams p) {
     extern __shared__ __align__(16) unsigned char wv_dyn[];
     __shared__ Best s_red[WV_THREADS / 32];
     __shared__ int s_cab[WV_THREADS / 32 * CPW], s_cb[WV_THREADS / 32 * CPW], s_wcnt[WV_THREADS / 32];
@@ -216,11 +216,13 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(
     constexpr bool STATS_T = KC != 0;  // KC > 0: pooled thread per move, top-KC in registers;
                                        // KC < 0: warp per move, bitonic sort (k > 8 or S > 128)
     const bool stats = STATS_T && (SCEN || p.exp_delta || p.cvar || p.n_pairs);
-    const bool need_vrow = stats || (!literal && p.scen >= 0);
+    // vmax rows staged per warp: the pooled statistics read every precedence-feasible move's row;
+    // the big-S statistics read only capacity-feasible moves' rows, straight from L2
+    const bool need_vrow = (stats && KC > 0) || (!literal && p.scen >= 0);
     const bool want_unit = !literal && p.scen < 0;
     const bool want_trace = p.trace_val || p.trace_feas;
     const WarpLayout L = warp_layout(T, Sp, stats, need_vrow, net, (KC < 0 && stats) ? big_pow2(S) : 0);
-    const int sigb = sig_bytes(S, T, stats);
+    const int sigb = sig_bytes(S, T, stats && KC > 0);  // big-S statistics read sigma through L1
     double *s_sig = reinterpret_cast<double *>(wv_dyn);
     unsigned char *wslices = wv_dyn + sigb;
     unsigned char *wbase = wslices + (size_t)warp * L.total;
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(
     int b[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
-    if (stats)  // sigma [S][T] for the pair statistics, staged once per CTA
+    if (stats && KC > 0)  // sigma [S][T] for the pooled pair statistics, staged once per CTA
         for (int e = threadIdx.x; e < S * T; e += WV_THREADS) cp_async8(s_sig + e, p.sigma + e);
     if (threadIdx.x < T) {
         cp_async8(&s_tab[0][threadIdx.x], p.cap + threadIdx.x);
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(
                 const int wq = ci / CPW, jq = ci - wq * CPW;
                 unsigned char *wb = wslices + (size_t)wq * L.total;
                 const double *crow = reinterpret_cast<const double *>(wb + L.cost) + jq * T;
-                const double *rowb = reinterpret_cast<const double *>(wb + L.vrow) + (size_t)jq * Sp;
+                const double *rowb = p.vmax + (size_t)s_cb[ci] * Sp;
                 const int ab = s_cab[ci];
                 const double sp = s_csp[ci];
                 const bool mined = ab >= 0;
@@ -491,10 +493,10 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 2 : WV_MINB) k_eval_warp(
                     const int s_ = lane + 32 * r;
                     k8[r] = ~0ull;
                     if (s_ < S) {
-                        const double x = rowb[s_];
-                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), s_sig[s_ * T + t]), sp), dc_t);
+                        const double x = __ldg(rowb + s_);
+                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma + s_ * T + t)), sp), dc_t);
                         const double vo =
-                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), s_sig[s_ * T + abc]), sp), dc_ab) : 0.0;
+                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma + s_ * T + abc)), sp), dc_ab) : 0.0;
                         const double v = f64_sub(vn, vo);
                         if constexpr (SCEN) p.scen_delta[(g * S + s_) * T + t] = (float)v;
                         vb[s_] = v;
@@ -813,11 +815,11 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 
     // fast path: one warp per CPW candidates (k_eval_warp)
     if (warp_path) {
-        const bool need_vrow = stats || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
         const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 8 ? 8 : -1;  // -1: warp per move
+        const bool need_vrow = (stats && kcw > 0) || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
                                           kcw < 0 ? big_pow2(S) : 0);
-        const size_t smem_w = (size_t)Lw.total * (WV_THREADS / 32) + sig_bytes(S, T, stats);
+        const size_t smem_w = (size_t)Lw.total * (WV_THREADS / 32) + sig_bytes(S, T, stats && kcw > 0);
         const int per_cta = CPW * (WV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));

@@ -6,7 +6,8 @@ lib = _lib.load(sys.argv[1]); _lib._lib = lib
 lib.pp_debug_eval_probe.argtypes = [ctypes.c_void_p]; lib.pp_debug_pm_probe.argtypes = [ctypes.c_void_p]
 from bench import build_inputs
 from paper_2511_18296_b200.engine import Engine
-c = build_inputs("C2")
+CFG = next((a for a in sys.argv[2:] if a in ("C1", "C2", "C3", "C4")), "C2")
+c = build_inputs(CFG)
 dev = torch.device("cuda", 0)
 st = torch.cuda.Stream(dev); torch.cuda.set_stream(st); sp = st.cuda_stream
 eng = Engine.from_tables(c["bm"], c["tables"], c["assign"])
@@ -62,4 +63,6 @@ else:
 names = ["start", "loads", "values", "pm-wait", "moves", "outputs", "end", "stats", "pooled"]
 for k in range(len(names)):
     print(f"eval {names[k]:9s} min {f(ev[:,k].min()):6.2f}  median {f(np.median(ev[:,k])):6.2f}  max {f(ev[:,k].max()):6.2f} us")
+d = (ev[:, 6] - ev[:, 0]) / 1000
+print("eval CTA duration us: p10 %.2f median %.2f p90 %.2f max %.2f" % tuple(np.percentile(d, [10, 50, 90, 100])))
 print(f"stamp before the step {f(stamps[0]):.2f} us, after {f(stamps[1]):.2f} us (relative to the first kernel start)")
