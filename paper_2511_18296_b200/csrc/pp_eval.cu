@@ -95,10 +95,14 @@ __device__ __forceinline__ void ce_u64(unsigned long long &a, unsigned long long
     a = lo;
     b = hi;
 }
-// The k smallest of the warp's 8 x 32 keys (lane l holds elements l + 32 r), ascending, into
-// out[0..k): a per-lane sorting network, then k rounds of a warp-wide minimum over the lane
-// heads (two 32-bit redux.sync) in which the winning lane pops its head.
-__device__ __forceinline__ void warp_k_smallest(unsigned long long (&k8)[8], int k, double *out) {
+// The k (<= 32) smallest of the warp's keys (lane l holds elements l + 32 r, r < npl <= 8; the
+// rest are padding), ascending: a per-lane sorting network, then k rounds of a warp-wide minimum
+// over the lane heads (redux.sync on the high word; the low word only on a tie) in which the
+// winning lane pops its head (its sorted tail waits in scr, 32 x npl u64 of the warp's scratch).
+// Returns the r-th smallest on lane r < k.
+__device__ __forceinline__ double warp_k_smallest(unsigned long long (&k8)[8], int k, unsigned long long *scr,
+                                                  int npl) {
+    constexpr unsigned FULL = 0xffffffffu;
     ce_u64(k8[0], k8[1]); ce_u64(k8[2], k8[3]); ce_u64(k8[4], k8[5]); ce_u64(k8[6], k8[7]);
     ce_u64(k8[0], k8[2]); ce_u64(k8[1], k8[3]); ce_u64(k8[4], k8[6]); ce_u64(k8[5], k8[7]);
     ce_u64(k8[1], k8[2]); ce_u64(k8[5], k8[6]);
@@ -106,18 +110,29 @@ __device__ __forceinline__ void warp_k_smallest(unsigned long long (&k8)[8], int
     ce_u64(k8[2], k8[4]); ce_u64(k8[3], k8[5]);
     ce_u64(k8[1], k8[2]); ce_u64(k8[3], k8[4]); ce_u64(k8[5], k8[6]);
     const int lane = threadIdx.x & 31;
-    for (int r = 0; r < k; r++) {
-        const unsigned hi = (unsigned)(k8[0] >> 32), lo = (unsigned)k8[0];
-        const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
-        const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
-        const unsigned who = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
-        if (lane == 0) out[r] = key_f64(((unsigned long long)mhi << 32) | mlo);
-        if (lane == __ffs(who) - 1) {
 #pragma unroll
-            for (int i = 0; i < 7; i++) k8[i] = k8[i + 1];
-            k8[7] = ~0ull;
+    for (int i = 2; i < 8; i++)
+        if (i < npl) scr[i * 32 + lane] = k8[i];
+    unsigned long long h0 = k8[0], h1 = k8[1], mine = ~0ull;
+    int ptr = 2;
+    for (int r = 0; r < k; r++) {
+        const unsigned hi = (unsigned)(h0 >> 32), lo = (unsigned)h0;
+        const unsigned mhi = __reduce_min_sync(FULL, hi);
+        unsigned who = __ballot_sync(FULL, hi == mhi);
+        if (__popc(who) > 1) {  // warp-uniform
+            const unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
+            who = __ballot_sync(FULL, hi == mhi && lo == mlo);
+        }
+        const int w = __ffs(who) - 1;
+        const unsigned wlo = __shfl_sync(FULL, lo, w);
+        if (lane == r) mine = ((unsigned long long)mhi << 32) | wlo;
+        if (lane == w) {
+            h0 = h1;
+            h1 = ptr < npl ? scr[ptr * 32 + lane] : ~0ull;
+            ptr++;
         }
     }
+    return key_f64(mine);
 }
 
 __device__ __forceinline__ int nth_bit(unsigned m, int k) {  // index of the k-th (0-based) set bit
@@ -504,6 +519,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                     }
                 }
                 __syncwarp();
+                if (mv == 0) EV_PROBE(9);
                 // expected delta: numpy pairwise over d[0..S) (the plan's leaves, 8 lanes each)
                 for (int l0 = 0; l0 < nleaf; l0 += 4) {
                     const int l = l0 + (lane >> 3), sub = lane & 7;
@@ -527,21 +543,22 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                 __syncwarp();
                 // CVaR10: the k smallest in ascending order (np.sort, saa.py:157-164) over the
                 // deltas just consumed by the mean, then their pairwise mean
-                warp_k_smallest(k8, kq, vb);
-                __syncwarp();
+                if (mv == 0) EV_PROBE(10);
+                const double kv = warp_k_smallest(k8, kq, reinterpret_cast<unsigned long long *>(vb), P2 >> 5);
+                if (mv == 0) EV_PROBE(11);
                 const int kn = kq >> 3;
-                double cacc = 0.0;
-                if (lane < 8 && kn > 0) {
-                    cacc = vb[lane];
-                    for (int u = 1; u < kn; u++) cacc = f64_add(cacc, vb[8 * u + lane]);
+                double cacc = (lane < 8 && kn > 0) ? kv : 0.0;  // lane l < 8: ranks l, 8 + l, ...
+                for (int u = 1; u < kn; u++) {
+                    const double x = __shfl_sync(FULL, kv, (8 * u + lane) & 31);
+                    if (lane < 8) cacc = f64_add(cacc, x);
                 }
                 cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 1));
                 cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 2));
                 cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 4));
+                double rc = kq >= 8 ? cacc : -0.0;
+                for (int i = kq - (kq & 7); i < kq; i++) rc = f64_add(rc, __shfl_sync(FULL, kv, i));
                 if (lane == 0) {
-                    double r = kq >= 8 ? cacc : -0.0;
-                    for (int i = kq - (kq & 7); i < kq; i++) r = f64_add(r, vb[i]);
-                    reinterpret_cast<double *>(wb + L.cv)[jq * T + t] = f64_div(f64_add(0.0, r), (double)kq);
+                    reinterpret_cast<double *>(wb + L.cv)[jq * T + t] = f64_div(f64_add(0.0, rc), (double)kq);
                     double stk[8];
                     int sp_ = 0;
                     for (int l = 0; l < nleaf; l++) {  // numpy's recursion, post-order

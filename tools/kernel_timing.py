@@ -3,7 +3,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, '.')
 from bench import build_inputs
 from paper_2511_18296_b200.engine import Engine
-c = build_inputs("C2")
+c = build_inputs(sys.argv[1] if len(sys.argv) > 1 else "C2")
 dev = torch.device("cuda", 0)
 st = torch.cuda.Stream(dev); torch.cuda.set_stream(st); sp = st.cuda_stream
 eng = Engine.from_tables(c["bm"], c["tables"], c["assign"])

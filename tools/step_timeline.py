@@ -66,3 +66,14 @@ for k in range(len(names)):
 d = (ev[:, 6] - ev[:, 0]) / 1000
 print("eval CTA duration us: p10 %.2f median %.2f p90 %.2f max %.2f" % tuple(np.percentile(d, [10, 50, 90, 100])))
 print(f"stamp before the step {f(stamps[0]):.2f} us, after {f(stamps[1]):.2f} us (relative to the first kernel start)")
+if "corr" in sys.argv:  # stats-phase duration per CTA against the CTA's capacity-feasible moves
+    r = eng.eval_candidates(c["cand"], None, net=True, trace=True)
+    per = np.add.reduceat(r["trace_feas"].sum(axis=1), np.arange(0, C, 32))
+    dur = (ev[:, 4] - ev[:, 3]) / 1000
+    dd = lambda a, b: np.median((ev[:, b] - ev[:, a])[ev[:, 9] > 0]) / 1000
+    print("first move of warp 0: pm-wait->computed %.2f, ->leaves %.2f, ->k-smallest %.2f us (median)" % (dd(3, 9), dd(9, 10), dd(10, 11)))
+    print("moves/CTA: mean %.1f max %d" % (per.mean(), per.max()))
+    for lo, hi in ((0, 4), (4, 8), (8, 12), (12, 16), (16, 24), (24, 33), (33, 1000)):
+        m = (per >= lo) & (per < hi)
+        if m.any():
+            print(f"  {lo:3d}-{hi:3d} moves: {m.sum():4d} CTAs, stats phase median {np.median(dur[m]):6.2f} max {dur[m].max():6.2f} us")
