@@ -314,6 +314,17 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         const int hi = (int)__reduce_min_sync(FULL, (unsigned)hc);
         win[j] = __ballot_sync(FULL, b[j] >= 0 && lane < T && lane >= lo && lane <= hi);
     }
+    if constexpr (KC < 0) {
+        if (stats) {  // warm L2 (rows of windowed candidates) and L1 (sigma) for the statistics,
+                      // which run after the period masses; this overlaps the period-mass kernel
+#pragma unroll
+            for (int j = 0; j < CPW; j++)
+                if (win[j] && lane * 16 < Sp)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.vmax + (size_t)b[j] * Sp + lane * 16));
+            for (int e = threadIdx.x * 16; e < S * T; e += WV_THREADS * 16)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.sigma_ts + e));
+        }
+    }
     cp_async_wait_all();
     __syncwarp();
     EV_PROBE(1);
@@ -471,6 +482,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                 if (lane < CPW) s_okm[warp * CPW + lane] = mine;
             }
             __syncthreads();
+            EV_PROBE(8);
             const unsigned om = s_okm[lane];  // lane i: candidate i of the CTA
             int incl = __popc(om);
 #pragma unroll
@@ -509,9 +521,9 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                     k8[r] = ~0ull;
                     if (s_ < S) {
                         const double x = __ldg(rowb + s_);
-                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma + s_ * T + t)), sp), dc_t);
+                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma_ts + t * S + s_)), sp), dc_t);
                         const double vo =
-                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma + s_ * T + abc)), sp), dc_ab) : 0.0;
+                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma_ts + abc * S + s_)), sp), dc_ab) : 0.0;
                         const double v = f64_sub(vn, vo);
                         if constexpr (SCEN) p.scen_delta[(g * S + s_) * T + t] = (float)v;
                         vb[s_] = v;
@@ -803,6 +815,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     else if (scenario < 0) ep.sig_row = c->sig_mean.as<double>();
     else ep.sig_row = c->sigma.as<double>() + (size_t)scenario * T;
     ep.sigma = (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : c->ones_st.as<double>();
+    ep.sigma_ts = (flags & PP_USE_SIGMA) ? c->sigma_ts.as<double>() : c->ones_st.as<double>();
     ep.cand = dcand;
     ep.C = C;
     ep.B = c->B;

@@ -353,6 +353,7 @@ struct EvalParams {
     const double *unit_mean; // [B]
     const double *sig_row;   // [T] (ones / scenario mean / sigma[k])
     const double *sigma;     // [S][T] (ones if no sigma)
+    const double *sigma_ts;  // [T][S]: sigma transposed (scenario-contiguous rows for lane = scenario)
     const int32_t *cand;
     int C, B, T, S, Sp, scen, cvar_k;
     unsigned flags;
@@ -452,7 +453,7 @@ struct pp_ctx {
     const int32_t *assign_ptr = nullptr;  // current schedule (own buffer or a borrowed device buffer)
     bool borrowed = false;
     bool pm_dirty = true;
-    DevBuf vmax, unit_mean, sigma, sig_mean, ones_st, plan_dev;
+    DevBuf vmax, unit_mean, sigma, sigma_ts, sig_mean, ones_st, plan_dev;
     // schedule
     DevBuf assign, pm;
     // scratch
@@ -472,7 +473,7 @@ struct pp_ctx {
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
     std::vector<DevBuf *> all() {
-        return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sig_mean,
+        return {&rows, &adj, &nbr, &cost, &cap, &disc, &level_blocks, &ones_t, &mass, &vmax, &unit_mean, &sigma, &sigma_ts, &sig_mean,
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,

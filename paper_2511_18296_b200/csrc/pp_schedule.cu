@@ -1262,6 +1262,7 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     TRY(c->vmax.ensure(sizeof(double) * (size_t)B * Sp));
     TRY(c->unit_mean.ensure(sizeof(double) * B));
     TRY(c->sigma.ensure(sizeof(double) * (size_t)S * T));
+    TRY(c->sigma_ts.ensure(sizeof(double) * (size_t)S * T));
     TRY(c->ones_st.ensure(sizeof(double) * (size_t)S * T));
     TRY(c->sig_mean.ensure(sizeof(double) * T));
     TRY(c->plan_dev.ensure(sizeof(int) * kPlanWords));
@@ -1280,6 +1281,12 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     if (e == cudaSuccess) e = dev_upload(c, c->ones_st.ptr, ones.data(), sizeof(double) * ones.size());
     if (e == cudaSuccess && sigma_st) {
         e = dev_upload(c, c->sigma.ptr, sigma_st, sizeof(double) * (size_t)S * T);
+        if (e == cudaSuccess) {
+            std::vector<double> ts((size_t)S * T);
+            for (int s_ = 0; s_ < S; s_++)
+                for (int t = 0; t < T; t++) ts[(size_t)t * S + s_] = sigma_st[(size_t)s_ * T + t];
+            e = dev_upload(c, c->sigma_ts.ptr, ts.data(), sizeof(double) * ts.size());
+        }
         if (e == cudaSuccess) {
             k_sig_mean<<<(T + 127) / 128, 128, 0, c->stream>>>(c->sigma.as<double>(), S, T, c->sig_mean.as<double>());
             e = cudaGetLastError();

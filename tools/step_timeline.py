@@ -71,7 +71,7 @@ if "corr" in sys.argv:  # stats-phase duration per CTA against the CTA's capacit
     per = np.add.reduceat(r["trace_feas"].sum(axis=1), np.arange(0, C, 32))
     dur = (ev[:, 4] - ev[:, 3]) / 1000
     dd = lambda a, b: np.median((ev[:, b] - ev[:, a])[ev[:, 9] > 0]) / 1000
-    print("first move of warp 0: pm-wait->computed %.2f, ->leaves %.2f, ->k-smallest %.2f us (median)" % (dd(3, 9), dd(9, 10), dd(10, 11)))
+    print("pm-wait->okm barrier %.2f" % dd(3, 8)); print("first move of warp 0: pm-wait->computed %.2f, ->leaves %.2f, ->k-smallest %.2f us (median)" % (dd(3, 9), dd(9, 10), dd(10, 11)))
     print("moves/CTA: mean %.1f max %d" % (per.mean(), per.max()))
     for lo, hi in ((0, 4), (4, 8), (8, 12), (12, 16), (16, 24), (24, 33), (33, 1000)):
         m = (per >= lo) & (per < hi)
