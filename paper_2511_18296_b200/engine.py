@@ -62,6 +62,9 @@ class Engine:
         self.has_sigma = False
         self._keep = []
         self._eval_cache = None
+        # last host arrays passed without a copy and their addresses (an ndarray's buffer cannot
+        # move while a reference is held, and ndarray.ctypes costs ~1.4 us per access)
+        self._sched_obj = self._sched_ptr = self._cand_obj = self._cand_ptr = None
 
     # -- lifecycle -----------------------------------------------------------------
     def close(self):
@@ -130,8 +133,14 @@ class Engine:
         if hasattr(assign, "data_ptr"):
             check(self.lib.pp_set_schedule(self._h, assign.data_ptr(), _lib.PP_MEM_DEVICE, None))
             return
+        if assign is self._sched_obj:
+            check(self.lib.pp_set_schedule(self._h, self._sched_ptr, _lib.PP_MEM_HOST, None))
+            return
         a = _i32(assign, bm.n_blocks, "assignment")  # range validated by pp_set_schedule
-        check(self.lib.pp_set_schedule(self._h, ptr(a), _lib.PP_MEM_HOST, None))
+        p = ptr(a)
+        if a is assign:
+            self._sched_obj, self._sched_ptr = a, p
+        check(self.lib.pp_set_schedule(self._h, p, _lib.PP_MEM_HOST, None))
 
     def set_schedule_device(self, assign_tensor, stream=None, borrow: bool = False):
         # borrow: read the device tensor in place (no copy) until the next set_schedule
@@ -178,8 +187,13 @@ class Engine:
         Candidate ids are range-checked by pp_eval_candidates (`validate` is kept for
         compatibility)."""
         bm = self._need_bm()
-        c = cand if (isinstance(cand, np.ndarray) and cand.dtype == np.int32 and cand.flags.c_contiguous) \
-            else _i32(cand)
+        if cand is self._cand_obj:
+            c = cand
+        else:
+            c = cand if (isinstance(cand, np.ndarray) and cand.dtype == np.int32 and cand.flags.c_contiguous) \
+                else _i32(cand)
+            if c is cand:
+                self._cand_obj, self._cand_ptr = c, c.ctypes.data
         C, T, S = c.size, bm.n_periods, self.n_scenarios
         key = None
         if out:
@@ -224,7 +238,8 @@ class Engine:
 
     def _eval_call(self, c, C, scenario, net, literal, use_sigma, argblock):
         sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
-        check(self.lib.pp_eval_candidates(self._h, c.ctypes.data, C, sc, self.flags(net, literal, use_sigma),
+        cp = self._cand_ptr if c is self._cand_obj else c.ctypes.data
+        check(self.lib.pp_eval_candidates(self._h, cp, C, sc, self.flags(net, literal, use_sigma),
                                           ctypes.byref(argblock), _lib.PP_MEM_HOST, None))
 
     @staticmethod

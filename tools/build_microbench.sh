@@ -6,3 +6,5 @@ mkdir -p bin
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o bin/f64_latency f64_latency.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/globaltimer_resolution globaltimer_resolution.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/warp_min_rounds warp_min_rounds.cu
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/zero_copy zero_copy.cu
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/sysmem_writes sysmem_writes.cu
