@@ -217,6 +217,15 @@ PP_API int pp_npv_relaxed(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, u
  * exact move value polish_schedule compares, hybrid.py:369-376). */
 PP_API int pp_npv_moves(pp_ctx *ctx, const int32_t *assign, const int32_t *blocks, const int32_t *periods,
                  int32_t n_moves, uint32_t flags, double *npv_out, int32_t mem, void *stream);
+/* The feasible-sequence greedy of column generation's pricing step (colgen.py:236-254;
+ * replaces the Python scan in colgen.price_column, colgen.py:207-293).  score[B][T] (host,
+ * row-major) is the dual-adjusted value the caller computed exactly as colgen.py:230-234 does;
+ * cap[T] = mining_capacity[t] * capacity_slack.  Writes the column's assignment (period or -1,
+ * before the capacity_slack trim of colgen.py:256-268, which stays with the caller) and the
+ * expansion count; identical to the reference's sequential scan, including its 1e-12 tolerance
+ * and node_cap cut-off.  Synchronous. */
+PP_API int pp_price_greedy(pp_ctx *ctx, const double *score, const double *cap, int64_t node_cap,
+                           int32_t *assign_out, int64_t *expansions_out);
 /* spatial[B] = geological_consistency of every block (uncertainty.py:185-191, the factor
  * pp_set_geology computed on the device), e.g. for lns_repair's realism fallback
  * (hybrid.py:238-244, 256-260). */

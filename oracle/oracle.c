@@ -459,6 +459,43 @@ void or_eject(int32_t B, int32_t T, const int32_t *succ_ptr, const int32_t *succ
     free(ej);
 }
 
+/* ---- colgen.price_column's sequence greedy (colgen.py:236-254), literally: per period, scan
+ * blocks in id order; skip blocks in the column or over the period's capacity
+ * (`masses[b] + load > cap`), skip blocks with a predecessor outside the column or at a later
+ * period; every remaining block is one expansion and becomes the pick when its score exceeds
+ * best + 1e-12 (best starts at 0.0).  The loop for a period stops when a scan picks nothing;
+ * scans start only while expansions < node_cap.  score is [B][T]. ---- */
+int64_t or_price_greedy(int32_t B, int32_t T, const int32_t *pred_ptr, const int32_t *pred_idx, const double *mass,
+                        const double *score, const double *cap, int64_t node_cap, int32_t *assign) {
+    int64_t expansions = 0;
+    for (int32_t b = 0; b < B; b++) assign[b] = UNMINED;
+    for (int32_t t = 0; t < T; t++) {
+        double load = 0.0;
+        while (expansions < node_cap) {
+            int32_t best_b = -1;
+            double best_s = 0.0;
+            for (int32_t b = 0; b < B; b++) {
+                if (assign[b] != UNMINED || mass[b] + load > cap[t]) continue;
+                int ok = 1;
+                for (int32_t k = pred_ptr[b]; k < pred_ptr[b + 1] && ok; k++) {
+                    const int32_t tp = assign[pred_idx[k]];
+                    ok = tp != UNMINED && tp <= t;
+                }
+                if (!ok) continue;
+                expansions++;
+                if (score[(size_t)b * T + t] > best_s + 1e-12) {
+                    best_b = b;
+                    best_s = score[(size_t)b * T + t];
+                }
+            }
+            if (best_b < 0) break;
+            assign[best_b] = t;
+            load += mass[best_b];
+        }
+    }
+    return expansions;
+}
+
 /* ---- relaxed NPV: ScheduleEvaluator.npv_relaxed / per_scenario_npv, single-mode fast path ----
  * stage-2 (evaluate.py:166-183): blocks of period t sorted by density = v[s,b,0] / m[b] with
  * np.argsort(-density, kind="stable") (ties keep block order); greedy: while density > 0 and

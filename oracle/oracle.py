@@ -47,6 +47,7 @@ _SIGS = {
     "or_unmine_fixpoint": (None, [_i32, _i64, _P, _P, _P, _P]),
     "or_enpv_table": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _i32, _P]),
     "or_eject": (None, [_i32, _i32, _P, _P, _P, _P, _P, _f64, _P, _P]),
+    "or_price_greedy": (ctypes.c_int64, [_i32, _i32, _P, _P, _P, _P, _P, ctypes.c_int64, _P]),
     "or_npv_relaxed": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _f64, _P, _P]),
     "or_eval_moves": (None, [_i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                              _P, _P, _P, _P, _i32, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _i32]),
@@ -258,6 +259,15 @@ class Oracle:
         lib().or_eject(self.B, self.T, _p(self.sp), _p(self.si), _p(self.mass), _p(self.cap), _p(g),
                        float(destroy_fraction), _p(a), _p(e))
         return a, e
+
+    def price_greedy(self, score, cap, node_cap):
+        """colgen.price_column's sequence greedy (colgen.py:236-254) -> (assign int32, expansions)."""
+        sc = np.ascontiguousarray(score, dtype=np.float64)
+        cp = np.ascontiguousarray(cap, dtype=np.float64)
+        a = np.empty(self.B, np.int32)
+        ex = lib().or_price_greedy(self.B, self.T, _p(self.pp), _p(self.pi), _p(self.mass), _p(sc), _p(cp),
+                                   int(node_cap), _p(a))
+        return a, int(ex)
 
     def unmine_fixpoint(self, assign):
         a = np.array(assign, dtype=np.int32, order="C")

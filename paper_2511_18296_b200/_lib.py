@@ -106,6 +106,7 @@ SIGNATURES = {
     "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_enpv_table": (c_int32, [c_void_p, c_uint32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_get_levels": (c_int32, [c_void_p, ctypes.POINTER(c_int32), c_void_p]),
+    "pp_price_greedy": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -469,6 +469,7 @@ struct pp_ctx {
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
     DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
     DevBuf hours, npv_raw, npv_cost, npv_n, npv_flag;  // relaxed NPV (pp_npv.cu)
+    DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
@@ -477,7 +478,7 @@ struct pp_ctx {
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
-                &npv_cost, &npv_n, &npv_flag};
+                &npv_cost, &npv_n, &npv_flag, &pr_score, &pr_cap, &pr_assign, &pr_elig};
     }
 };
 

@@ -373,6 +373,21 @@ class Engine:
         check(self.lib.pp_npv_moves(self._h, ptr(a), ptr(b), ptr(t), b.size, f, ptr(out), _lib.PP_MEM_HOST, None))
         return out
 
+    def price_greedy(self, score, cap, node_cap: int):
+        """colgen.price_column's sequence greedy (colgen.py:236-254) on the device: score[B][T]
+        f64, cap[T] = mining_capacity * capacity_slack; returns (assign int32[B], expansions)."""
+        bm = self._need_bm()
+        sc = np.ascontiguousarray(score, dtype=np.float64)
+        if sc.shape != (bm.n_blocks, bm.n_periods):
+            raise ShapeMismatch(f"score has shape {sc.shape}, expected {(bm.n_blocks, bm.n_periods)}")
+        cp = np.ascontiguousarray(cap, dtype=np.float64)
+        if cp.size != bm.n_periods:
+            raise ShapeMismatch(f"cap has {cp.size} entries, expected {bm.n_periods}")
+        a = np.empty(bm.n_blocks, np.int32)
+        ex = ctypes.c_int64(0)
+        check(self.lib.pp_price_greedy(self._h, ptr(sc), ptr(cp), int(node_cap), ptr(a), ctypes.addressof(ex)))
+        return a, int(ex.value)
+
     def spatial(self) -> np.ndarray:
         """geological_consistency of every block (uncertainty.py:185-191), as computed on the device."""
         bm = self._need_bm()

@@ -11,6 +11,7 @@
     lns_repair                     pitplan/hybrid.py:169-274  (destroy step and every insertion
                                    evaluation on the device; candidate ranking by the
                                    reference's own neighbour-similarity helper)
+    price_column                   pitplan/colgen.py:207-293  (the sequence greedy on the device)
 
 Same signatures, argument meaning, return types and error behaviour as the
 reference; the work runs in the sm_100a kernels of csrc/pitplan_b200.cu through the
@@ -566,6 +567,61 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         if not improved:
             break
     return cur
+
+
+def price_column(instance, duals, scenarios, sigma, equipment, seed, evaluator=None, node_cap: int = 5000,
+                 capacity_slack: float = 1.0, noise: float = 0.0):
+    """colgen.price_column (colgen.py:207-293): the dual-adjusted score matrix and its noise are
+    formed exactly as the reference does (its own `_enpv_adjusted` and `substream`), the
+    feasible-sequence greedy (colgen.py:236-254, one Python scan of every block per pick) runs
+    in `pp_price_greedy`, and the capacity-slack trim and the column's value / reduced cost
+    follow the reference line by line. Needs `pitplan` (the column type is the reference's)."""
+    from pitplan import colgen as _cg  # the reference module (its helpers are not rebound)
+
+    rng = _cg.substream(seed[0], *seed[1:]) if isinstance(seed, tuple) else _cg.substream(seed, "price")
+    enpv = _cg._enpv_adjusted(instance, scenarios, sigma)
+    masses = instance.masses()
+    n_t = instance.n_periods
+    score = enpv - duals.block[:, None] - np.outer(masses, duals.capacity)
+    if noise > 0:
+        scale = max(float(np.abs(score).max()), 1e-9)
+        score = score + rng.normal(0.0, noise * scale, size=score.shape)
+    cap = np.array([instance.mining_capacity[t] * capacity_slack for t in range(n_t)], dtype=np.float64)
+    a32, _ = _entry(instance).engine.price_greedy(score, cap, node_cap)
+    UN = _cg.UNMINED
+    assign = a32.astype(int)
+    in_col = assign != UN
+
+    # trim back to the hard capacity if the slack let the sequence overfill (colgen.py:256-268)
+    if capacity_slack > 1.0:
+        for t in range(n_t):
+            load = float(masses[assign == t].sum())
+            if load <= instance.mining_capacity[t]:
+                continue
+            for b in reversed(instance.topological_order()):
+                if assign[b] != t:
+                    continue
+                if all(assign[c] == UN for c in instance.successors(b)):
+                    assign[b] = UN
+                    in_col[b] = False
+                    load -= masses[b]
+                if load <= instance.mining_capacity[t]:
+                    break
+
+    if not in_col.any():
+        return None, float("inf")
+    mass_t = np.array([float(masses[assign == t].sum()) for t in range(n_t)])
+    column = _cg.SequenceColumn(id=-1, equipment=equipment, assignment=assign, mass_per_period=mass_t, value=0.0)
+    if evaluator is not None:
+        column.value = evaluator.npv_relaxed(column.schedule())
+    else:
+        mined = assign != UN
+        column.value = float(enpv[mined, assign[mined]].sum())
+    charge = float(duals.block[assign != UN].sum())
+    charge += float(duals.capacity @ mass_t)
+    charge += float(duals.convexity[equipment])
+    column.reduced_cost = column.value - charge
+    return column, column.reduced_cost
 
 
 def clear_cache() -> None:

@@ -30,7 +30,7 @@ _PATCHES = {
         "polish_schedule": _ev.polish_schedule,
     },
     "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair,
-                       "ScheduleEvaluator": _ev.ScheduleEvaluator},
+                       "ScheduleEvaluator": _ev.ScheduleEvaluator, "price_column": _ev.price_column},
     "pitplan.saa": {},
     "pitplan": {"check_feasible": _ev.check_feasible},
 }

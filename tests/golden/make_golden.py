@@ -389,7 +389,52 @@ def polish_cases(store):
         store[p + "sweeps"] = np.int64(sweeps)
 
 
+def price_cases(store):
+    """colgen.price_column (colgen.py:207-293) runs: the score matrix is formed exactly as
+    colgen.py:227-234 does (the reference's own _enpv_adjusted and substream), and the expected
+    sequence is the reference's returned column (capacity_slack 1.0: no trim)."""
+    from pitplan.colgen import DualPrices, price_column
+
+    cases = (("q8", 8, (2, 2, 2), 3, 2, 0.0, 5000, "zero"), ("q27", 27, (3, 3, 3), 3, 3, 0.4, 5000, "zero"),
+             ("q512", 512, (8, 8, 8), 6, 4, 0.0, 10 ** 7, "rand"), ("q512n", 512, (8, 8, 8), 6, 4, 0.3, 700, "rand"),
+             ("qC1", 4000, (20, 20, 10), 10, 5, 0.0, 5000, "rand"), ("qC1big", 4000, (20, 20, 10), 10, 5, 0.2, 10 ** 7,
+                                                                     "rand"))
+    for name, n, dims, T, S, noise, node_cap, dk in cases:
+        inst = generate_synthetic(n, dims, T, 1, seed=90 + n, n_rock_types=1, capacity_factor=0.6)
+        scen = sample_lognormal(inst, S, 0.3, seed=91 + n)
+        sigma = uncertainty_factors(inst, scen.grades)
+        rng = np.random.default_rng(n + T)
+        if dk == "zero":
+            duals = DualPrices(block=np.zeros(n), capacity=np.zeros(T), convexity=np.zeros(1))
+        else:
+            enpv0 = _enpv_adjusted(inst, scen, sigma)
+            duals = DualPrices(block=np.abs(rng.normal(0, 0.3, n)) * np.abs(enpv0).mean(),
+                               capacity=np.abs(rng.normal(0, 0.5, T)) * np.abs(enpv0).mean() / inst.masses().mean(),
+                               convexity=np.zeros(1))
+        seed = (5, "price", n)
+        col, rc = price_column(inst, duals, scen, sigma, 0, seed, node_cap=node_cap, noise=noise)
+        # the score the greedy sees (colgen.py:226-234, same calls in the same order)
+        srng = substream(seed[0], *seed[1:])
+        enpv = _enpv_adjusted(inst, scen, sigma)
+        score = enpv - duals.block[:, None] - np.outer(inst.masses(), duals.capacity)
+        if noise > 0:
+            scale = max(float(np.abs(score).max()), 1e-9)
+            score = score + srng.normal(0.0, noise * scale, size=score.shape)
+        p = f"{name}_"
+        store.update(flat(inst, p))
+        store[p + "score"] = score
+        store[p + "cap"] = np.array([inst.mining_capacity[t] * 1.0 for t in range(T)], dtype=np.float64)
+        store[p + "node_cap"] = np.int64(node_cap)
+        store[p + "assign"] = (np.full(n, UNMINED) if col is None else col.assignment).astype(np.int32)
+        store[p + "rc"] = np.float64(rc)
+
+
 def main():
+    if sys.argv[1:] == ["price"]:  # regenerate only the pricing fixture
+        store: dict = {"numpy_version": np.bytes_(np.__version__)}
+        price_cases(store)
+        np.savez_compressed(os.path.join(OUT, "price.npz"), **store)
+        return
     store: dict = {}
     small_cases(store)
     hand_cases(store)

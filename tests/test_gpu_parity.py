@@ -598,3 +598,43 @@ def test_npv_moves_equal_full_recompute():
         ref = eng.npv_relaxed(batch, use_sigma=use_sigma)
         assert same(got, ref)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ("q8", "q27", "q512", "q512n", "qC1", "qC1big"))
+def test_price_greedy_matches_reference(oracle_lib, name):
+    """pp_price_greedy against the reference's price_column sequences (colgen.py:236-254)."""
+    st = load("price")
+    p = f"{name}_"
+    bm = bm_from(st, p)
+    eng = Engine.from_tables(bm, None)
+    a, ex = eng.price_greedy(st[p + "score"], st[p + "cap"], int(st[p + "node_cap"]))
+    eng.close()
+    assert np.array_equal(a, st[p + "assign"])
+    _, ex_ref = oracle_lib.Oracle(bm).price_greedy(st[p + "score"], st[p + "cap"], int(st[p + "node_cap"]))
+    assert ex == ex_ref
+
+
+def test_price_greedy_near_ties_against_oracle(oracle_lib):
+    """Scores with exact ties, ties within the reference's 1e-12 tolerance and tiny magnitudes
+    (where the tolerance is not absorbed by rounding) take the sequential replay."""
+    bm, _, _ = _rand_instance(21, n=(10, 10, 8), T=5, S=2, cf=0.4)
+    B, T = bm.n_blocks, bm.n_periods
+    rng = np.random.default_rng(4)
+    o = oracle_lib.Oracle(bm)
+    eng = Engine.from_tables(bm, None)
+    cap = np.asarray(bm.capacity, dtype=np.float64)
+    for kind in range(4):
+        if kind == 0:  # few distinct values: exact ties everywhere
+            score = rng.integers(-2, 6, size=(B, T)).astype(np.float64)
+        elif kind == 1:  # near-ties below the tolerance
+            score = 1e-9 + rng.integers(0, 4, size=(B, T)) * 4e-13
+        elif kind == 2:  # around the 1e-12 threshold itself
+            score = rng.choice([0.0, 5e-13, 1e-12, 1.0000000001e-12, 2e-12, 3e-12], size=(B, T))
+        else:  # distinct values, large node_cap
+            score = rng.normal(0.0, 1.0, size=(B, T))
+        for node_cap in (50, 10 ** 7):
+            a, ex = eng.price_greedy(score, cap, node_cap)
+            ar, exr = o.price_greedy(score, cap, node_cap)
+            assert np.array_equal(a, ar), (kind, node_cap)
+            assert ex == exr, (kind, node_cap)
+    eng.close()

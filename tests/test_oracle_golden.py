@@ -247,3 +247,17 @@ def test_npv_relaxed_c1(oracle_lib):
         v, ps = o.npv_relaxed(a, bm.plant_hours, bm.mode_rates[0])
         assert v == st["C1_npv"][k], k
         assert np.array_equal(ps, st["C1_npv_scen"][k]), k
+
+
+PRICE_CASES = ("q8", "q27", "q512", "q512n", "qC1", "qC1big")
+
+
+@pytest.mark.parametrize("name", PRICE_CASES)
+def test_price_greedy_matches_reference(oracle_lib, name):
+    """colgen.price_column's sequence greedy (colgen.py:236-254) against the reference's column."""
+    st = load("price")
+    p = f"{name}_"
+    o = oracle_lib.Oracle(bm_from(st, p))
+    a, ex = o.price_greedy(st[p + "score"], st[p + "cap"], int(st[p + "node_cap"]))
+    assert np.array_equal(a, st[p + "assign"])
+    assert ex >= int(np.count_nonzero(a >= 0))
