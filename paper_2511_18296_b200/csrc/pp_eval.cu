@@ -60,7 +60,8 @@ __device__ __forceinline__ void pair_stats(const EvalParams &p, int S, int T, co
 }
 
 // ------------------------------------------------------------------------------------
-// k_eval_warp: the fast path of pp_eval_candidates (T <= 32, S <= 128, degree <= 32).
+// k_eval_warp: the fast path of pp_eval_candidates (T <= 32, degree <= 32; S <= 256 when
+// statistics are requested).
 // Every warp owns CPW consecutive candidates end to end; warps never wait for one another
 // until the final CTA argmax, so the SM overlaps one warp's load latency with another's
 // arithmetic.  Lane t is period t for the capacity / value / argmax of a candidate
@@ -71,8 +72,10 @@ __device__ __forceinline__ void pair_stats(const EvalParams &p, int S, int T, co
 //   wait      griddepcontrol.wait (the period-mass kernel), lane t loads pm[t]
 //   moves     capacity (373-378), value (379-384), lowest-t argmax (387-388) per candidate:
 //             ballot of the feasible periods, butterfly argmax, trace row written by lane t
-//   stats     per feasible (candidate, period) pair: 8-lane sub-groups (CVaR k <= 2) or one
-//             lane per pair: expected delta (numpy pairwise mean) and CVaR10
+//   stats     KC > 0 (CVaR k <= 8): every precedence-feasible pair, one thread per pair pooled
+//             across the CTA, before the wait; KC < 0 (k > 8): every capacity-feasible pair,
+//             one warp per pair dealt across the CTA's warps, after it (section 4.1 of DESIGN.md):
+//             expected delta (numpy pairwise mean) and CVaR10
 //   argmax    warp -> CTA -> deterministic grid argmax (last CTA)
 // Everything before the wait is independent of the period masses and overlaps the
 // period-mass kernel under programmatic dependent launch.
