@@ -146,6 +146,19 @@ def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
             "per_launch": per_cand * C + per_pair * n_pairs, "survey_uncached": survey}
 
 
+def workload_config(args, c) -> dict:
+    """The `config` object of both arms (identical, so the driver compares like with like)."""
+    C, T, S = c["C"], c["T"], c["S"]
+    return {
+        "workload": ("C2: 50k-block model (50x50x20), 15 periods, 20 lognormal scenarios with sigma, "
+                     "16,667 candidate blocks x 15 periods = 250,005 moves per GPU per step, "
+                     "net mining cost, per-move expected delta + CVaR10, argmax")
+        if args.config == "C2" else args.config,
+        "blocks": c["bm"].n_blocks, "periods": T, "scenarios": S, "candidates": C, "moves_per_batch": C * T,
+        "l2": "256 MiB flush write between timed GPU steps",
+    }
+
+
 def cpu_reference(c, seconds: float = 3.0, nthreads: int | None = None, max_batches: int | None = None):
     """Time the oracle port on the same batch (period mass + evaluation + scenario stats)."""
     from oracle import oracle
@@ -201,9 +214,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "ms_per_250k_batch": t * 1e3 * (M / (n_c * c["T"])), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: 50k-block model, 15 periods, 20 scenarios, 16,667 candidates x 15 periods"
-                   if args.config == "C2" else args.config, "blocks": c["bm"].n_blocks, "periods": c["T"],
-                   "scenarios": S, "moves_per_batch": M, "net_mining_cost": True},
+        "config": workload_config(args, c),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -383,7 +394,11 @@ def run_gpu(args):
     if rank == 0:
         hbm, peak_kind = _peaks()
         ab = algorithmic_bytes(c, deg_mean, int(out["n_pairs"].item()))
+        # roofline numerator: the compulsory bytes of one launch (each candidate's rows once for
+        # all its periods). SURVEY §8(d)'s per-move figure counts every (b, t) move
+        # as re-reading its rows; it is reported beside it and exceeds the HBM peak at C3/C4
         achieved = ab["per_launch"] / (k_ms * 1e-3) / 1e9
+        achieved_survey = ab["survey_uncached"] / (k_ms * 1e-3) / 1e9
         value = world * M * S / (t_max * 1e-3)
 
         cpu = None
@@ -408,15 +423,8 @@ def run_gpu(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {
-                "workload": ("C2: 50k-block model (50x50x20), 15 periods, 20 lognormal scenarios with sigma, "
-                             "16,667 candidate blocks x 15 periods = 250,005 moves per GPU per step, "
-                             "net mining cost, per-move expected delta + CVaR10, argmax")
-                if args.config == "C2" else args.config,
-                "blocks": bm.n_blocks, "periods": T, "scenarios": S, "candidates": C, "moves_per_batch": M,
-                "l2": "256 MiB flush write between timed steps",
-                "cuda_graph": graph is not None,
-            },
+            "config": workload_config(args, c),
+            "cuda_graph": graph is not None,
             "roofline": {
                 "bound": "hbm",
                 "achieved": achieved,
@@ -427,8 +435,11 @@ def run_gpu(args):
                 "kernel": "k_eval_warp",
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": ab["per_launch"],
+                "algorithmic_basis": "compulsory: per candidate 4+32+4+8+8*deg+8*T+8*Sp+13 B, per feasible pair 24 B",
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "survey_uncached_bytes_per_launch": ab["survey_uncached"],
+                "survey_uncached_achieved": achieved_survey,
+                "survey_uncached_frac": achieved_survey / hbm,
             },
             "e2e": {"value": world * M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_t * 1e3,
