@@ -56,7 +56,7 @@ def _cache() -> OrderedDict:
 
 
 class _Entry:
-    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params", "rook")
+    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params", "rook", "rook_pad")
 
     def __init__(self, instance, bm, engine):
         self.instance = instance  # strong ref: keeps id(instance) from being reused
@@ -66,6 +66,7 @@ class _Entry:
         self.scen_refs = None
         self.params = None
         self.rook = None
+        self.rook_pad = None
 
 
 def _device() -> int:
@@ -252,7 +253,7 @@ def lns_repair(
     The reference's helpers are restated in model.py (rook_neighbor_map,
     scheduled_neighbor_similarity), so pitplan is not required."""
     from .errors import RepairStalled
-    from .model import rook_neighbor_map, scheduled_neighbor_similarity
+    from .model import neighbor_similarity_array, rook_neighbor_map, rook_padded, scheduled_neighbor_similarity
 
     e = _entry(instance)
     _bind_scenarios(e, scenarios, sigma, params)
@@ -270,12 +271,22 @@ def lns_repair(
     spatial = e.engine.spatial()
     rook = e.rook if e.rook is not None else rook_neighbor_map(e.bm)
     e.rook = rook
+    pad = e.rook_pad
+    if pad is None:
+        pad = e.rook_pad = rook_padded(rook, e.bm.n_blocks)
+    in_pool = np.zeros(e.bm.n_blocks, dtype=bool)
+    in_pool[list(pool)] = True
     iters = 0
     stalled = False
     while pool and iters < max_iters:
-        sims = scheduled_neighbor_similarity(sched.assignment, pool, mean_grade, rook)
-        ranked = sorted(pool, key=lambda b: (-sims[b], b))
-        cand = ranked[:candidate_width]
+        if pad is not None:  # vectorised ranking, identical order (model.neighbor_similarity_array)
+            ids = np.flatnonzero(in_pool)
+            sims = neighbor_similarity_array(sched.assignment, ids, mean_grade, pad)
+            cand = ids[np.lexsort((ids, -sims))[:candidate_width]].tolist()
+        else:
+            sims = scheduled_neighbor_similarity(sched.assignment, pool, mean_grade, rook)
+            ranked = sorted(pool, key=lambda b: (-sims[b], b))
+            cand = ranked[:candidate_width]
         moves, best = evaluate_candidates_parallel(
             instance, sched, cand, scenarios, None, sigma,
             net_mining_cost=net_mining_cost, params=params,
@@ -290,6 +301,7 @@ def lns_repair(
             chosen = feasible[0]
         sched.assignment[chosen.block] = chosen.period
         pool.discard(chosen.block)
+        in_pool[chosen.block] = False
         iters += 1
 
     after = check_feasible(instance, sched)

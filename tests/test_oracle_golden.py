@@ -261,3 +261,27 @@ def test_price_greedy_matches_reference(oracle_lib, name):
     a, ex = o.price_greedy(st[p + "score"], st[p + "cap"], int(st[p + "node_cap"]))
     assert np.array_equal(a, st[p + "assign"])
     assert ex >= int(np.count_nonzero(a >= 0))
+
+
+def test_vectorised_neighbor_similarity_matches_scalar():
+    """model.neighbor_similarity_array (the lns_repair ranking, vectorised) against the
+    reference-shaped scalar restatement, including -inf rows and -0.0 means."""
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.model import (neighbor_similarity_array, rook_neighbor_map, rook_padded,
+                                             scheduled_neighbor_similarity)
+
+    bm = synth.generate_block_model(6 * 5 * 4, (6, 5, 4), 5, 1, seed=3, n_rock_types=1)
+    rook = rook_neighbor_map(bm)
+    pad = rook_padded(rook, bm.n_blocks)
+    assert pad is not None
+    rng = np.random.default_rng(0)
+    for it in range(50):
+        assign = rng.integers(-1, 5, size=bm.n_blocks)
+        g = rng.normal(1.0, 0.3, bm.n_blocks) if it % 3 else np.round(rng.normal(1.0, 0.3, bm.n_blocks), 1)
+        blocks = np.flatnonzero(rng.random(bm.n_blocks) < 0.5)
+        ref = scheduled_neighbor_similarity(assign, blocks.tolist(), g, rook)
+        got = neighbor_similarity_array(assign, blocks, g, pad)
+        for b, v in zip(blocks.tolist(), got.tolist()):
+            assert v == ref[b] and np.signbit(v) == np.signbit(ref[b]), (it, b)
+        order = blocks[np.lexsort((blocks, -got))].tolist()
+        assert order == sorted(blocks.tolist(), key=lambda b: (-ref[b], b))
