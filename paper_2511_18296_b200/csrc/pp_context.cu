@@ -126,6 +126,7 @@ int pp_ctx_destroy(pp_ctx *c) {
     for (DevBuf *b : c->all()) b->release();
     if (c->h_bad) cudaFreeHost(c->h_bad);
     if (c->h_bounce) cudaFreeHost(c->h_bounce);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return PP_OK;

@@ -466,6 +466,13 @@ struct pp_ctx {
     DevBuf pm_bad;
     int32_t *h_bad = nullptr;  // page-locked mirror [8]
     unsigned char *h_bounce = nullptr;  // page-locked bounce buffer for small host-mode results
+    unsigned char *h_stage = nullptr;   // page-locked staging for packed host-mode uploads/results
+    // pp_npv_moves: the base schedule's stage-2 results stay in npv_raw/_cost/_n between calls;
+    // reused while the tables (npv_gen), the buffers and the base assignment are unchanged
+    uint64_t npv_gen = 0, npvm_gen = ~0ull;
+    std::vector<int32_t> npvm_base;
+    const void *npvm_ptrs[3] = {nullptr, nullptr, nullptr};
+    size_t h_stage_bytes = 0;
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
     DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
     DevBuf hours, npv_raw, npv_cost, npv_n, npv_flag;  // relaxed NPV (pp_npv.cu)
@@ -510,6 +517,20 @@ inline cudaError_t stream_wait(cudaStream_t st) {
     while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
     }
     return e;
+}
+
+// page-locked staging of at least `bytes` (grown on demand, kept for the context's lifetime)
+inline int host_stage(pp_ctx *c, size_t bytes, unsigned char **out) {
+    if (c->h_stage_bytes < bytes) {
+        if (c->h_stage) CUDA_TRY(cudaFreeHost(c->h_stage));
+        c->h_stage = nullptr;
+        c->h_stage_bytes = 0;
+        const size_t n = std::max<size_t>(bytes, 4096);
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&c->h_stage), n, cudaHostAllocPortable));
+        c->h_stage_bytes = n;
+    }
+    *out = c->h_stage;
+    return PP_OK;
 }
 
 inline int use_device(pp_ctx *c) {

@@ -1217,6 +1217,7 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
     c->level_of = level;
     c->mean_cap = (0.0 + host_pairwise(capacity, T)) / (double)T;
     c->have_instance = true;
+    c->npv_gen++;
     c->assign_ptr = c->assign.as<int32_t>();
     c->borrowed = false;
     c->pm_dirty = true;
@@ -1301,6 +1302,7 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     c->cvar_k = std::max(1, (int)std::ceil(0.1 * S));
     c->have_sigma = sigma_st != nullptr;
     c->have_scen = true;
+    c->npv_gen++;
     return PP_OK;
 }
 

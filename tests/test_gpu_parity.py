@@ -600,6 +600,37 @@ def test_npv_moves_equal_full_recompute():
     eng.close()
 
 
+def test_npv_moves_base_cache_invalidation():
+    """pp_npv_moves keeps the base schedule's stage-2 results between calls: a sequence of calls
+    alternating bases, interleaved pp_npv_relaxed batches (which reuse the buffers) and a new
+    plant table must each equal a full recompute."""
+    c = config("C1")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    rng = np.random.default_rng(5)
+    bases = [c["greedy"].copy(), c["assign"].copy()]
+
+    def check(a, m=12):
+        blocks = rng.integers(0, bm.n_blocks, m).astype(np.int32)
+        periods = rng.integers(-1, bm.n_periods, m).astype(np.int32)
+        got = eng.npv_moves(a, blocks, periods)
+        batch = np.repeat(a[None, :], m, axis=0)
+        batch[np.arange(m), blocks] = periods
+        assert same(got, eng.npv_relaxed(batch))
+
+    for k in (0, 0, 1, 0, 1, 1):
+        check(bases[k])
+        check(bases[k], m=3)  # same base, fewer moves: a cache hit
+    a = bases[0].copy()
+    a[np.flatnonzero(a >= 0)[:5]] = -1  # the same array object, new contents
+    check(a)
+    check(bases[0])
+    hours = np.asarray(bm.plant_hours, dtype=np.float64) * 0.5
+    eng.set_plant(hours)
+    check(bases[0])
+    eng.close()
+
+
 @pytest.mark.parametrize("name", ("q8", "q27", "q512", "q512n", "qC1", "qC1big"))
 def test_price_greedy_matches_reference(oracle_lib, name):
     """pp_price_greedy against the reference's price_column sequences (colgen.py:236-254)."""
