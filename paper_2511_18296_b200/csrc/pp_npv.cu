@@ -282,40 +282,70 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     }
     __syncthreads();
     NPVP(3);
-    // 4. the greedy fill (evaluate.py:174-182): a sequential f64 recurrence.  4 blocks per step are
-    //    taken speculatively as whole blocks (hours_left -= m / rate, total += d * m); the step is
-    //    kept when none of them hits a stop (d <= 0, hours_left <= 0) or a partial take
-    //    (hours_left * rate < m), else the exact scalar loop finishes from its start.
-    if (tid == 0) {
+    // 4. the greedy fill (evaluate.py:174-182): a sequential f64 recurrence.  Warp 0 takes 32
+    //    blocks per step speculatively as whole blocks: every lane runs the two chains
+    //    hours_left -= m / rate and total += d * m over the step's 32 blocks (values broadcast by
+    //    shuffles, the same adds in the same order) and lane j keeps the values before block j;
+    //    then each lane tests its block for a stop (d <= 0, hours_left <= 0) or a partial take
+    //    (hours_left * rate < m).  At the first flagged block the exact scalar loop takes over from
+    //    that block's hours_left and total.
+    __shared__ int s_kpos;
+    __shared__ double s_q32[32], s_dm32[32];
+    if (tid == 0) s_kpos = n;
+    __syncthreads();
+    for (int k = tid; k < n; k += S2_THREADS)
+        if (dsort[k] <= 0) atomicMin(&s_kpos, k);  // first d <= 0 (the scalar loop's stop)
+    __syncthreads();
+    if (warp == 0) {
+        const int kpos = s_kpos;
         double hl = __ldg(hours + t), total = 0.0;
-        int k = 0;
-        for (; k + 4 <= n; k += 4) {  // (explicit registers: an array form compiled ~2x slower)
-            const double d0 = dsort[k], d1 = dsort[k + 1], d2 = dsort[k + 2], d3 = dsort[k + 3];
-            const double m0 = ms[k], m1 = ms[k + 1], m2 = ms[k + 2], m3 = ms[k + 3];
-            const double h1 = f64_sub(hl, qs[k]), h2 = f64_sub(h1, qs[k + 1]), h3 = f64_sub(h2, qs[k + 2]);
-            const double h4 = f64_sub(h3, qs[k + 3]);
-            const bool ok = d0 > 0 && d1 > 0 && d2 > 0 && d3 > 0 && hl > 0 && h1 > 0 && h2 > 0 && h3 > 0 &&
-                            !(f64_mul(hl, rate) < m0) && !(f64_mul(h1, rate) < m1) && !(f64_mul(h2, rate) < m2) &&
-                            !(f64_mul(h3, rate) < m3);
-            if (!ok) break;
-            total = f64_add(f64_add(f64_add(f64_add(total, f64_mul(d0, m0)), f64_mul(d1, m1)), f64_mul(d2, m2)),
-                            f64_mul(d3, m3));
-            hl = h4;
-        }
-        for (; k < n; k++) {
-            const double d = dsort[k];
-            if (d <= 0 || hl <= 0) break;
-            const double m = ms[k];
-            const double hr = f64_mul(hl, rate);
-            if (hr < m) {  // take = min(m, hours_left * rate) = hours_left * rate
-                total = f64_add(total, f64_mul(d, hr));
-                hl = f64_sub(hl, f64_div(hr, rate));
-            } else {
-                total = f64_add(total, f64_mul(d, m));
-                hl = f64_sub(hl, qs[k]);
+        int k = n;
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int kk = k0 + lane;
+            const bool in = kk < n;
+            const double m = in ? ms[kk] : 0.0;
+            s_q32[lane] = in ? qs[kk] : 0.0;  // broadcast reads below: independent of the chains,
+            s_dm32[lane] = in ? f64_mul(dsort[kk], m) : 0.0;  // so they issue ahead of them
+            __syncwarp();
+            double h = hl, tt = total, h_mine = 0.0, t_mine = 0.0;
+#pragma unroll 8
+            for (int j = 0; j < 32; j++) {
+                if (lane == j) {
+                    h_mine = h;
+                    t_mine = tt;
+                }
+                h = f64_sub(h, s_q32[j]);
+                tt = f64_add(tt, s_dm32[j]);
             }
+            __syncwarp();
+            const bool stop = !in || kk >= kpos || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
+            const unsigned sm = __ballot_sync(0xffffffffu, stop);
+            if (sm) {
+                const int jf = __ffs(sm) - 1;
+                k = k0 + jf;
+                hl = __shfl_sync(0xffffffffu, h_mine, jf);
+                total = __shfl_sync(0xffffffffu, t_mine, jf);
+                break;
+            }
+            hl = h;
+            total = tt;
         }
-        raw[pt * S + s] = total;
+        if (lane == 0) {
+            for (; k < n; k++) {
+                const double d = dsort[k];
+                if (d <= 0 || hl <= 0) break;
+                const double mk = ms[k];
+                const double hr = f64_mul(hl, rate);
+                if (hr < mk) {  // take = min(m, hours_left * rate) = hours_left * rate
+                    total = f64_add(total, f64_mul(d, hr));
+                    hl = f64_sub(hl, f64_div(hr, rate));
+                } else {
+                    total = f64_add(total, f64_mul(d, mk));
+                    hl = f64_sub(hl, qs[k]);
+                }
+            }
+            raw[pt * S + s] = total;
+        }
     }
     NPVP(4);
 }
