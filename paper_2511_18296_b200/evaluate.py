@@ -25,6 +25,7 @@ a switch).  When `pitplan` is importable the reference's own `CandidateMove` and
 from __future__ import annotations
 
 import csv
+import os
 import threading
 from collections import OrderedDict
 
@@ -35,6 +36,8 @@ from .errors import InvalidArgs, ShapeMismatch
 from .model import BlockModel, CandidateMove, ScenarioTables, ViolationReport
 
 _MAX_CACHED = 4
+_POLISH_CHUNK = int(os.environ.get('PP_POLISH_CHUNK', '64'))  # first speculative chunk (blocks)
+_POLISH_CHUNK_MAX = 128
 _tls = threading.local()  # one engine cache per host thread (contexts are not thread-safe)
 
 
@@ -450,33 +453,56 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         t_hi = int(ms_.min()) if ms_.size else T - 1
         return t_lo, t_hi
 
+    def options_of(b):
+        orig = int(a[b])
+        t_lo, t_hi = window(b)
+        mined_succ_any = bool(np.any(a[si_[sp_[b]:sp_[b + 1]]] != UN))
+        options = []
+        if not mined_succ_any and orig != UN:
+            options.append(UN)
+        if t_lo is not None:
+            for t in range(t_lo, t_hi + 1):
+                if t != orig and load[t] + masses[b] <= cap[t]:
+                    options.append(t)
+        return options
+
     for _ in range(max_sweeps):
         improved = False
-        for b in range(B):
-            orig = int(a[b])
-            t_lo, t_hi = window(b)
-            mined_succ_any = bool(np.any(a[si_[sp_[b]:sp_[b + 1]]] != UN))
-            options = []
-            if not mined_succ_any and orig != UN:
-                options.append(UN)
-            if t_lo is not None:
-                for t in range(t_lo, t_hi + 1):
-                    if t != orig and load[t] + masses[b] <= cap[t]:
-                        options.append(t)
-            best_t, best_val = orig, cur_val
-            if options:  # every option re-solves only the two periods it changes
-                vals = eng.npv_moves(a, np.full(len(options), b), options, use_sigma=use_sigma)
-                for t, val in zip(options, vals.tolist()):
+        # Speculative chunks: the options of the next `k` blocks are built and valued against
+        # the current schedule in one pp_npv_moves call.  The blocks are then decided in the
+        # reference's order; a block's options and values depend only on (a, load, cur_val),
+        # which change only when a move is accepted, so the first acceptance ends the chunk and
+        # the next chunk starts at the following block: the decisions are the sequential ones.
+        b0 = 0
+        k = _POLISH_CHUNK
+        while b0 < B:
+            blocks = range(b0, min(B, b0 + k))
+            opts = [options_of(b) for b in blocks]
+            nb = np.fromiter((b for b, o in zip(blocks, opts) for _ in o), np.int64)
+            nt = [t for o in opts for t in o]
+            vals = eng.npv_moves(a, nb, nt, use_sigma=use_sigma).tolist() if nt else []
+            pos = 0
+            nxt = blocks.stop
+            for b, options in zip(blocks, opts):
+                orig = int(a[b])
+                best_t, best_val = orig, cur_val
+                for t, val in zip(options, vals[pos:pos + len(options)]):
                     if val > best_val + 1e-9:
                         best_t, best_val = t, val
-            a[b] = best_t
-            if best_t != orig:
-                improved = True
-                cur_val = best_val
-                if orig != UN:
-                    load[orig] -= masses[b]
-                if best_t != UN:
-                    load[best_t] += masses[b]
+                pos += len(options)
+                if best_t != orig:
+                    a[b] = best_t
+                    improved = True
+                    cur_val = best_val
+                    if orig != UN:
+                        load[orig] -= masses[b]
+                    if best_t != UN:
+                        load[best_t] += masses[b]
+                    nxt = b + 1
+                    break
+            # shrink the chunk while moves are being accepted, grow it while they are not
+            k = max(1, k // 2) if nxt < blocks.stop else min(_POLISH_CHUNK_MAX, k * 2)
+            b0 = nxt
 
         if pair_swaps:
             for b1 in range(B):
