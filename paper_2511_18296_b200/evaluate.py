@@ -453,18 +453,36 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         t_hi = int(ms_.min()) if ms_.size else T - 1
         return t_lo, t_hi
 
-    def options_of(b):
-        orig = int(a[b])
-        t_lo, t_hi = window(b)
-        mined_succ_any = bool(np.any(a[si_[sp_[b]:sp_[b + 1]]] != UN))
-        options = []
-        if not mined_succ_any and orig != UN:
-            options.append(UN)
-        if t_lo is not None:
-            for t in range(t_lo, t_hi + 1):
-                if t != orig and load[t] + masses[b] <= cap[t]:
-                    options.append(t)
-        return options
+    tgrid = np.arange(T)
+
+    def options_chunk(b0, b1):
+        """The options of blocks b0..b1-1 against the current (a, load), vectorised: the
+        reference's window (hybrid.py:348-355) and option list (357-385) per block, UNMINED
+        first, then the periods in ascending order.  CSR rows of consecutive blocks are
+        contiguous, so each chunk's neighbour periods are one gather."""
+        n = b1 - b0
+        orig = a[b0:b1]
+        pa = a[pi_[pp_[b0]:pp_[b1]]]
+        pc = np.diff(pp_[b0:b1 + 1])
+        po = pp_[b0:b1] - pp_[b0]
+        sa = a[si_[sp_[b0]:sp_[b1]]]
+        sc = np.diff(sp_[b0:b1 + 1])
+        so = sp_[b0:b1] - sp_[b0]
+        # reduceat over [po[i], po[i+1]) with one neutral sentinel appended, so an empty last
+        # row reads the sentinel and no row is truncated; empty rows are masked by their counts
+        pun = (np.add.reduceat(np.append(pa == UN, False), po) > 0) & (pc > 0)
+        pmax = np.where(pc > 0, np.maximum.reduceat(np.append(pa, UN), po), 0)
+        sm = sa != UN
+        smined = (np.add.reduceat(np.append(sm, False), so) > 0) & (sc > 0)
+        smin = np.minimum.reduceat(np.append(np.where(sm, sa, T), T), so)
+        thi = np.where(smined, smin, T - 1)
+        ok = ((~pun)[:, None] & (tgrid[None, :] >= pmax[:, None]) & (tgrid[None, :] <= thi[:, None])
+              & (tgrid[None, :] != orig[:, None])
+              & (load[None, :] + masses[b0:b1, None] <= cap[None, :]))
+        un = (~smined) & (orig != UN)
+        opt = np.concatenate([un[:, None], ok], axis=1)  # column 0 = UNMINED
+        rows, cols = np.nonzero(opt)
+        return rows, cols - 1, np.bincount(rows, minlength=n)
 
     for _ in range(max_sweeps):
         improved = False
@@ -476,20 +494,21 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         b0 = 0
         k = _POLISH_CHUNK
         while b0 < B:
-            blocks = range(b0, min(B, b0 + k))
-            opts = [options_of(b) for b in blocks]
-            nb = np.fromiter((b for b, o in zip(blocks, opts) for _ in o), np.int64)
-            nt = [t for o in opts for t in o]
-            vals = eng.npv_moves(a, nb, nt, use_sigma=use_sigma).tolist() if nt else []
+            b1 = min(B, b0 + k)
+            rows, nt, cnt = options_chunk(b0, b1)
+            vals = eng.npv_moves(a, rows + b0, nt, use_sigma=use_sigma).tolist() if nt.size else []
+            nt = nt.tolist()
             pos = 0
-            nxt = blocks.stop
-            for b, options in zip(blocks, opts):
+            nxt = b1
+            for i in np.nonzero(cnt)[0].tolist():
+                b = b0 + i
                 orig = int(a[b])
                 best_t, best_val = orig, cur_val
-                for t, val in zip(options, vals[pos:pos + len(options)]):
+                c = int(cnt[i])
+                for t, val in zip(nt[pos:pos + c], vals[pos:pos + c]):
                     if val > best_val + 1e-9:
                         best_t, best_val = t, val
-                pos += len(options)
+                pos += c
                 if best_t != orig:
                     a[b] = best_t
                     improved = True
@@ -501,7 +520,7 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
                     nxt = b + 1
                     break
             # shrink the chunk while moves are being accepted, grow it while they are not
-            k = max(1, k // 2) if nxt < blocks.stop else min(_POLISH_CHUNK_MAX, k * 2)
+            k = max(1, k // 2) if nxt < b1 else min(_POLISH_CHUNK_MAX, k * 2)
             b0 = nxt
 
         if pair_swaps:

@@ -15,25 +15,39 @@ import importlib
 
 from . import evaluate as _ev
 
-_PATCHES = {
-    "pitplan.evaluate": {
-        "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
-        "check_feasible": _ev.check_feasible,
-        "ScheduleEvaluator": _ev.ScheduleEvaluator,
-    },
-    "pitplan.hybrid": {
-        "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
-        "check_feasible": _ev.check_feasible,
-        "_precedence_repair_pass": _ev.precedence_repair_pass,
-        "lns_repair": _ev.lns_repair,
-        "ScheduleEvaluator": _ev.ScheduleEvaluator,
-        "polish_schedule": _ev.polish_schedule,
-    },
-    "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair,
-                       "ScheduleEvaluator": _ev.ScheduleEvaluator, "price_column": _ev.price_column},
-    "pitplan.saa": {},
-    "pitplan": {"check_feasible": _ev.check_feasible},
-}
+
+def _evaluator_class():
+    """The ScheduleEvaluator drop-in, subclassing the reference's own class: rebuilt here when
+    this package was imported before `pitplan` became importable (the class built at import
+    then lacks the reference's attributes, e.g. `values`, hybrid.py:673)."""
+    Ref = _ev._reference_evaluator()
+    if Ref is not None and not issubclass(_ev.ScheduleEvaluator, Ref):
+        _ev.ScheduleEvaluator = _ev._make_evaluator_class()
+    return _ev.ScheduleEvaluator
+
+
+def _patches():
+    E = _evaluator_class()
+    return {
+        "pitplan.evaluate": {
+            "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
+            "check_feasible": _ev.check_feasible,
+            "ScheduleEvaluator": E,
+        },
+        "pitplan.hybrid": {
+            "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
+            "check_feasible": _ev.check_feasible,
+            "_precedence_repair_pass": _ev.precedence_repair_pass,
+            "lns_repair": _ev.lns_repair,
+            "ScheduleEvaluator": E,
+            "polish_schedule": _ev.polish_schedule,
+        },
+        "pitplan.colgen": {"check_feasible": _ev.check_feasible, "lns_repair": _ev.lns_repair,
+                           "ScheduleEvaluator": E, "price_column": _ev.price_column},
+        "pitplan.saa": {},
+        "pitplan": {"check_feasible": _ev.check_feasible},
+    }
+
 
 _saved: list[tuple[object, str, object]] = []
 
@@ -41,7 +55,7 @@ _saved: list[tuple[object, str, object]] = []
 def install() -> list[str]:
     """Rebind the reference entry points; returns the patched 'module.name' list."""
     done = []
-    for modname, names in _PATCHES.items():
+    for modname, names in _patches().items():
         try:
             mod = importlib.import_module(modname)
         except ImportError:

@@ -79,3 +79,33 @@ def test_header_abi_version_and_struct_layouts_match_ctypes():
         want = [f.rstrip("_") for f in _struct_fields(cname)]
         got = [f[0].rstrip("_") for f in py._fields_]
         assert want == got, (cname, want, got)
+
+
+def test_install_rebinds_reference_names_on_cpu():
+    """install.py rebinds every reference entry point (hybrid.py:22-28 binds by value) and
+    uninstall restores them; the ScheduleEvaluator drop-in subclasses the reference's class even
+    when this package was imported before the reference became importable.  No compute runs."""
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pitplan")):
+        pytest.skip("baseline/_ref (pip install of the reference) absent")
+    from paper_2511_18296_b200 import evaluate as ev
+    from paper_2511_18296_b200.install import install, uninstall
+
+    if ref not in sys.path:
+        sys.path.append(ref)
+    import pitplan.evaluate as PE
+    import pitplan.hybrid as PH
+
+    orig = (PH.evaluate_candidates_parallel, PH.polish_schedule, PE.ScheduleEvaluator)
+    done = install()
+    try:
+        assert PH.evaluate_candidates_parallel is ev.evaluate_candidates_parallel
+        assert PH.polish_schedule is ev.polish_schedule
+        assert issubclass(PH.ScheduleEvaluator, orig[2]) and PH.ScheduleEvaluator is not orig[2]
+        assert "pitplan.hybrid.lns_repair" in done and "pitplan.colgen.price_column" in done
+    finally:
+        uninstall()
+    assert (PH.evaluate_candidates_parallel, PH.polish_schedule, PE.ScheduleEvaluator) == orig
