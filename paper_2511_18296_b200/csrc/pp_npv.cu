@@ -3,6 +3,7 @@
 // (evaluate.py:166-183), bit-exact.  Population fitness of the GA loop (hybrid.py:595-606).
 #include "pp_internal.cuh"
 #include <cub/block/block_radix_sort.cuh>
+#include <unordered_map>
 #include <vector>
 
 // ------------------------------------------------------------------------------------
@@ -385,7 +386,8 @@ __global__ void k_npv_final(int T, int S, const double *__restrict__ raw, const 
 __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict__ braw, const double *__restrict__ bcost,
                                   const int32_t *__restrict__ bn, const double *__restrict__ mraw,
                                   const double *__restrict__ mcost, const int32_t *__restrict__ mn,
-                                  const int32_t *__restrict__ slot_t, const double *__restrict__ disc,
+                                  const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
+                                  const double *__restrict__ disc,
                                   const double *__restrict__ sigma, double *__restrict__ npv,
                                   const int32_t *__restrict__ flag_in, int32_t *__restrict__ flag_out) {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -398,7 +400,7 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
         double cs;
         int n;
         if (t == t0 || t == t1) {
-            const int k = 2 * m + (t == t0 ? 0 : 1);
+            const int k = slot_src[2 * m + (t == t0 ? 0 : 1)];  // deduplicated re-solve
             raw = mraw + (size_t)k * S;
             cs = mcost[k];
             n = mn[k];
@@ -506,18 +508,35 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
         CUDA_TRY(cudaMemcpyAsync(ha.data(), assign, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
     }
-    std::vector<int32_t> slot((size_t)2 * M);
+    // slot[2m] = the period the move leaves, slot[2m+1] = the period it enters (-1 = none).
+    // The re-solve of the left period (block removed) depends only on the block, so the moves of
+    // one block share it: run[] = the periods actually re-solved (-1 for a duplicate), src[] = the
+    // slot whose results a move reads.
+    std::vector<int32_t> slot((size_t)2 * M), run((size_t)2 * M), src((size_t)2 * M);
+    std::unordered_map<int32_t, int32_t> left_of;
     for (int m = 0; m < M; m++) {
         if (hb[m] < 0 || hb[m] >= B || ht[m] < -1 || ht[m] >= T) return fail(PP_ERR_INVALID_ARGS, "move %d out of range", m);
         const int told = ha[hb[m]], tnew = ht[m];
         slot[2 * m] = (told >= 0 && told < T && told != tnew) ? told : -1;
         slot[2 * m + 1] = (tnew >= 0 && tnew != told) ? tnew : -1;
+        run[2 * m] = slot[2 * m];
+        run[2 * m + 1] = slot[2 * m + 1];
+        src[2 * m] = 2 * m;
+        src[2 * m + 1] = 2 * m + 1;
+        if (slot[2 * m] >= 0) {
+            auto it = left_of.emplace(hb[m], 2 * m);
+            if (!it.second) {
+                src[2 * m] = it.first->second;
+                run[2 * m] = -1;
+            }
+        }
     }
-    // one packed upload (assign | blocks | periods | slots | stage-2 flag = 0) and one packed
-    // result copy (values | flag): each separate small copy costs a PCIe round trip
-    const size_t nin = (size_t)B + 4 * (size_t)M + 1;
+    // one packed upload (assign | blocks | periods | slots | runs | sources | stage-2 flag = 0)
+    // and one packed result copy (values | flag): each separate small copy costs a PCIe round trip
+    const size_t nin = (size_t)B + 8 * (size_t)M + 1;
     TRY(c->h_assign.ensure(sizeof(int32_t) * nin));
-    int32_t *da = c->h_assign.as<int32_t>(), *db = da + B, *dt = db + M, *ds = dt + M, *dflag = ds + 2 * M;
+    int32_t *da = c->h_assign.as<int32_t>(), *db = da + B, *dt = db + M, *ds = dt + M, *dr = ds + 2 * M,
+            *dsrc = dr + 2 * M, *dflag = dsrc + 2 * M;
     TRY(c->npv_raw.ensure(sizeof(double) * ((size_t)T * S + (size_t)2 * M * S)));
     TRY(c->npv_cost.ensure(sizeof(double) * ((size_t)T + 2 * (size_t)M)));
     TRY(c->npv_n.ensure(sizeof(int32_t) * ((size_t)T + 2 * (size_t)M)));
@@ -532,6 +551,8 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
         std::copy(hb.begin(), hb.end(), pk + B);
         std::copy(ht.begin(), ht.end(), pk + B + M);
         std::copy(slot.begin(), slot.end(), pk + B + 2 * M);
+        std::copy(run.begin(), run.end(), pk + B + 4 * M);
+        std::copy(src.begin(), src.end(), pk + B + 6 * M);
         pk[nin - 1] = 0;
         CUDA_TRY(cudaMemcpyAsync(da, pk, sizeof(int32_t) * nin, cudaMemcpyHostToDevice, st));
     }
@@ -547,10 +568,10 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
             c->hours.as<double>(), c->rate, braw, bcost, bn, dflag, nullptr, nullptr, nullptr);
     k_stage2<<<dim3(S, 2, M), S2_THREADS, S2Layout::bytes(), st>>>(
         da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, mraw, mcost, mn, dflag, db, dt, ds);
+        c->rate, mraw, mcost, mn, dflag, db, dt, dr);
     double *dn = host ? c->h_d1.as<double>() : npv_out;
     int32_t *flag_out = host ? reinterpret_cast<int32_t *>(c->h_d1.as<double>() + M) : nullptr;
-    k_npv_moves_final<<<(M + 127) / 128, 128, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds,
+    k_npv_moves_final<<<(M + 127) / 128, 128, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
                                                         c->disc.as<double>(),
                                                         (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
                                                         dflag, flag_out);
