@@ -669,3 +669,21 @@ def test_price_greedy_near_ties_against_oracle(oracle_lib):
             assert np.array_equal(a, ar), (kind, node_cap)
             assert ex == exr, (kind, node_cap)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_configs_against_oracle(oracle_lib, name):
+    """C3 (S = 200, the many-scenario statistics kernel, capacity binding) and C4 (200k
+    blocks, 1M moves) at their full bench sizes: every per-candidate output, the dense
+    statistics, the sparse pairs and the selected move against the oracle; the selected move
+    is invariant under a permutation of the candidates (test_evaluate.py:231-236)."""
+    c = config(name)
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], c["sigma"]), c["assign"])
+    o = oracle_lib.Oracle(c["bm"], c["vmax"], c["sigma"])
+    ref = o.eval_candidates(c["assign"], c["cand"], None, net=True, trace=True, stats=True, nthreads=8)
+    got = eng.eval_candidates(c["cand"], None, net=True, trace=True, stats=True)
+    _same_res(got, ref, ("best_t", "best_val", "feasible", "trace_val", "trace_feas", "exp_delta", "cvar"))
+    _pairs_match_dense(eng.eval_candidates(c["cand"], None, net=True, pairs=True)["pairs"], ref)
+    perm = np.random.default_rng(7).permutation(c["cand"].size)
+    assert eng.eval_candidates(c["cand"][perm].copy(), None, net=True)["best"] == got["best"]
+    eng.close()
