@@ -206,8 +206,8 @@ PP_API int pp_set_plant(pp_ctx *ctx, const double *plant_hours, double rate);
 /* ScheduleEvaluator.npv_relaxed (evaluate.py:222-234, 244-246) of P schedules assign[P][B] ->
  * npv_out[P], and per_scenario_npv (248-258) -> per_scen_out[P][S] (may be NULL); flags
  * PP_USE_SIGMA weights the stage-2 values by sigma[s][t] (sigma=None otherwise).  Stage 2 per
- * (s, t) is the greedy fractional knapsack of evaluate.py:166-183, bit-exact.  A period with more
- * than 6144 mined blocks is PP_ERR_SHAPE. */
+ * (s, t) is the greedy fractional knapsack of evaluate.py:166-183, bit-exact, for any period size
+ * (periods of more than 6144 mined blocks are sorted in global scratch by a second kernel). */
 PP_API int pp_npv_relaxed(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, uint32_t flags, double *npv_out,
                    double *per_scen_out, int32_t mem, void *stream);
 /* Relaxed NPV of M one-block variants of a base schedule assign[B]: variant m moves block

@@ -412,11 +412,13 @@ struct MoveParams {
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;
+    uint64_t gen = 0;  // bumped on every (re)allocation: caches keyed on a buffer compare this, not ptr
     int ensure(size_t need) {
         if (need <= bytes) return PP_OK;
         if (ptr) cudaFree(ptr);
         ptr = nullptr;
         bytes = 0;
+        gen++;
         size_t n = std::max<size_t>(need, 256);
         CUDA_TRY(cudaMalloc(&ptr, n));
         bytes = n;
@@ -471,11 +473,12 @@ struct pp_ctx {
     // reused while the tables (npv_gen), the buffers and the base assignment are unchanged
     uint64_t npv_gen = 0, npvm_gen = ~0ull;
     std::vector<int32_t> npvm_base;
-    const void *npvm_ptrs[3] = {nullptr, nullptr, nullptr};
+    uint64_t npvm_bufgen[3] = {0, 0, 0};  // DevBuf::gen of npv_raw / npv_cost / npv_n when cached
     size_t h_stage_bytes = 0;
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)
     DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
-    DevBuf hours, npv_raw, npv_cost, npv_n, npv_flag;  // relaxed NPV (pp_npv.cu)
+    DevBuf hours, npv_raw, npv_cost, npv_n;  // relaxed NPV (pp_npv.cu)
+    DevBuf s2_items, s2_scratch;  // large-period stage-2: work list [S*T*P | S*2*M] and per-CTA scratch
     DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
@@ -485,7 +488,7 @@ struct pp_ctx {
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
-                &npv_cost, &npv_n, &npv_flag, &pr_score, &pr_cap, &pr_assign, &pr_elig};
+                &npv_cost, &npv_n, &s2_items, &s2_scratch, &pr_score, &pr_cap, &pr_assign, &pr_elig};
     }
 };
 

@@ -7,7 +7,8 @@
 #include <vector>
 
 // ------------------------------------------------------------------------------------
-// k_stage2: one CTA per (scenario s, period t, schedule p).
+// k_stage2: one CTA per (scenario s, period t, schedule p); periods of more than S2_NMAX mined
+// blocks go to k_stage2_big (global-memory runs + merge), so every period size runs on the device.
 //   1. the blocks mined in t, in block order (two vectorised passes: count, place);
 //   2. the s == 0 CTA also sums their mining costs in numpy's pairwise order (for _npv);
 //   3. density = v[s][b] / m[b]; stable descending block radix sort (cub), which is the order of
@@ -49,12 +50,13 @@ struct S2Layout {
     __host__ __device__ static constexpr size_t bytes() { return q_off() + 8 * (size_t)S2_NMAX; }
 };
 
-// numpy pairwise sum of a[0..n) in shared memory (pairwise.c: blocks of 8, leaves <= 128), whole
-// CTA, result on thread 0: the leaves (n <= 6144: at most 96) from the recursion on thread 0,
-// one thread per leaf with numpy's 8 accumulators, the fold in post-order on thread 0
-__device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 doubles */) {
-    __shared__ int s_ls[160], s_ll[160], s_nl;
-    if (threadIdx.x == 0) {  // pre-order traversal: leaves come out in element order
+// numpy pairwise sum of a[0..n) (pairwise.c: blocks of 8, leaves <= 128), whole CTA, result on
+// thread 0: the leaves from the recursion on thread 0 (pre-order, i.e. element order) into
+// ls/ll (capacity >= n/64 + 2), one thread per leaf with numpy's 8 accumulators into leafval[],
+// the fold in post-order on thread 0.  `a`, ls, ll and leafval may live in shared or global memory.
+__device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *leafval) {
+    __shared__ int s_nl;
+    if (threadIdx.x == 0) {
         int stk_o[32], stk_n[32], sp = 0, nl = 0;
         stk_o[sp] = 0;
         stk_n[sp] = n;
@@ -63,8 +65,8 @@ __device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 
             sp--;
             const int o = stk_o[sp], ln = stk_n[sp];
             if (ln <= 128) {
-                s_ls[nl] = o;
-                s_ll[nl] = ln;
+                ls[nl] = o;
+                ll[nl] = ln;
                 nl++;
             } else {
                 int n2 = ln / 2;
@@ -82,7 +84,7 @@ __device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 
     __syncthreads();
     const int nl = s_nl;
     for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-        const int o = s_ls[l], len = s_ll[l];
+        const int o = ls[l], len = ll[l];
         double r;
         if (len < 8) {
             r = -0.0;
@@ -98,7 +100,7 @@ __device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 
             r = tree8(acc);
             for (int i = main_; i < len; i++) r = f64_add(r, a[o + i]);
         }
-        scratch[l] = r;
+        leafval[l] = r;
     }
     __syncthreads();
     double res = 0.0;
@@ -113,7 +115,7 @@ __device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 
         while (sp > 0) {
             const int ln = stk_n[sp - 1];
             if (ln <= 128) {
-                val[vsp++] = scratch[leaf++];
+                val[vsp++] = leafval[leaf++];
                 sp--;
                 continue;
             }
@@ -141,32 +143,12 @@ __device__ double s2_pairwise(const double *a, int n, double *scratch /* >= 160 
     return res;
 }
 
-__global__ void __launch_bounds__(S2_THREADS, 1)
-    k_stage2(const int32_t *__restrict__ assign, int B, int T, int S, int Sp, const double *__restrict__ mass,
-             const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
-             double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
-             int32_t *__restrict__ too_big, const int32_t *__restrict__ ovr_b, const int32_t *__restrict__ ovr_t,
-             const int32_t *__restrict__ slot_t) {
-    extern __shared__ __align__(16) unsigned char s2_dyn[];
-    typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
-    double *dsort = reinterpret_cast<double *>(s2_dyn);  // after the sort
-    int32_t *ids = reinterpret_cast<int32_t *>(s2_dyn + S2Layout::ids_off());
-    double *ms = reinterpret_cast<double *>(s2_dyn + S2Layout::m_off());
-    double *qs = reinterpret_cast<double *>(s2_dyn + S2Layout::q_off());
+// The blocks of schedule `a` (block ob moved to period ot when ob >= 0) mined in period t, in
+// block order: warp w owns [w*chunk, (w+1)*chunk), 128 blocks per step (int4 per lane when
+// aligned).  Returns n on every thread; writes ids[0..n) only when n <= nmax.  1024 threads.
+__device__ int s2_compact(const int32_t *__restrict__ a, int B, int t, int ob, int ot, int32_t *ids, int nmax) {
     __shared__ int s_wc[32];
-    __shared__ double s_scr[160];
-    // whole schedules: grid (S, T, P), blockIdx.y = period.  One-block variants of a single base
-    // schedule (ovr_b != nullptr): grid (S, 2, M), variant m = base with block ovr_b[m] in period
-    // ovr_t[m], blockIdx.y = slot of the two periods it changes (slot_t[m][slot], -1 = none)
-    const int s = blockIdx.x, p = blockIdx.z;
-    const int t = ovr_b ? slot_t[2 * p + blockIdx.y] : (int)blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (t < 0) return;
-    NPVP(0);
-    const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
-    const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
-    // 1. blocks mined in t, block order: warp w owns [w*chunk, (w+1)*chunk), 128 blocks per step
-    //    (int4 per lane when aligned)
     const int chunk = ((B + 31) / 32 + 127) & ~127;
     const int lo = warp * chunk, hi = min(B, lo + chunk);
     const bool vec = (B & 3) == 0;
@@ -198,14 +180,8 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         base += w < warp ? s_wc[w] : 0;
         n += s_wc[w];
     }
-    const size_t pt = ovr_b ? (size_t)2 * p + blockIdx.y : ((size_t)p * T + t);
-    if (n > S2_NMAX) {  // outside the on-chip path: flagged, the host reports it
-        if (tid == 0) {
-            *too_big = 1;
-            raw[pt * S + s] = 0.0;
-        }
-        return;
-    }
+    __syncthreads();  // s_wc is reused by the next call
+    if (n > nmax) return n;
     for (int b0 = lo; b0 < hi; b0 += 128) {
         int v[4];
         load4(b0, v);
@@ -222,13 +198,115 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
             if (v[u] == t) ids[q++] = b0 + 4 * lane + u;
         base += __shfl_sync(0xffffffffu, incl, 31);
     }
+    return n;
+}
+
+// The greedy fill of evaluate.py:174-182 over n blocks in density order (d(k) > 0 for k < kpos,
+// m(k) the mass, q(k) = m(k) / rate): a sequential f64 recurrence (hours_left, total).  Warp 0
+// takes 32 blocks per step speculatively as whole blocks: every lane runs the two chains
+// hours_left -= m / rate and total += d * m over the step's 32 blocks (values broadcast through
+// shared memory, the same adds in the same order) and lane j keeps the values before block j;
+// then each lane tests its block for a stop (k >= kpos, hours_left <= 0) or a partial take
+// (hours_left * rate < m).  At the first flagged block the exact scalar loop takes over from
+// that block's hours_left and total.  Call from warp 0 only; the result is on lane 0.
+template <class DF, class MF, class QF>
+__device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF dof, MF mof, QF qof) {
+    __shared__ double s_q32[32], s_dm32[32];
+    const int lane = threadIdx.x & 31;
+    double hl = hours0, total = 0.0;
+    int k = n;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int kk = k0 + lane;
+        const bool in = kk < n;
+        const double m = in ? mof(kk) : 0.0;
+        s_q32[lane] = in ? qof(kk) : 0.0;  // broadcast reads below: independent of the chains,
+        s_dm32[lane] = in ? f64_mul(dof(kk), m) : 0.0;  // so they issue ahead of them
+        __syncwarp();
+        double h = hl, tt = total, h_mine = 0.0, t_mine = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < 32; j++) {
+            if (lane == j) {
+                h_mine = h;
+                t_mine = tt;
+            }
+            h = f64_sub(h, s_q32[j]);
+            tt = f64_add(tt, s_dm32[j]);
+        }
+        __syncwarp();
+        const bool stop = !in || kk >= kpos || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
+        const unsigned sm = __ballot_sync(0xffffffffu, stop);
+        if (sm) {
+            const int jf = __ffs(sm) - 1;
+            k = k0 + jf;
+            hl = __shfl_sync(0xffffffffu, h_mine, jf);
+            total = __shfl_sync(0xffffffffu, t_mine, jf);
+            break;
+        }
+        hl = h;
+        total = tt;
+    }
+    if (lane == 0) {
+        for (; k < n; k++) {
+            if (k >= kpos || hl <= 0) break;
+            const double d = dof(k);
+            const double mk = mof(k);
+            const double hr = f64_mul(hl, rate);
+            if (hr < mk) {  // take = min(m, hours_left * rate) = hours_left * rate
+                total = f64_add(total, f64_mul(d, hr));
+                hl = f64_sub(hl, f64_div(hr, rate));
+            } else {
+                total = f64_add(total, f64_mul(d, mk));
+                hl = f64_sub(hl, qof(k));
+            }
+        }
+    }
+    return total;
+}
+
+// Work item of the large-period path: (scenario, grid y, grid z) of a k_stage2 CTA whose period
+// has more than S2_NMAX mined blocks.
+struct S2Item {
+    int s, y, z, n;
+};
+
+__global__ void __launch_bounds__(S2_THREADS, 1)
+    k_stage2(const int32_t *__restrict__ assign, int B, int T, int S, int Sp, const double *__restrict__ mass,
+             const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
+             double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
+             S2Item *__restrict__ big_items, int32_t *__restrict__ big_count, const int32_t *__restrict__ ovr_b,
+             const int32_t *__restrict__ ovr_t, const int32_t *__restrict__ slot_t) {
+    extern __shared__ __align__(16) unsigned char s2_dyn[];
+    typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
+    double *dsort = reinterpret_cast<double *>(s2_dyn);  // after the sort
+    int32_t *ids = reinterpret_cast<int32_t *>(s2_dyn + S2Layout::ids_off());
+    double *ms = reinterpret_cast<double *>(s2_dyn + S2Layout::m_off());
+    double *qs = reinterpret_cast<double *>(s2_dyn + S2Layout::q_off());
+    __shared__ int s_ls[160], s_ll[160];
+    __shared__ double s_scr[160];
+    // whole schedules: grid (S, T, P), blockIdx.y = period.  One-block variants of a single base
+    // schedule (ovr_b != nullptr): grid (S, 2, M), variant m = base with block ovr_b[m] in period
+    // ovr_t[m], blockIdx.y = slot of the two periods it changes (slot_t[m][slot], -1 = none)
+    const int s = blockIdx.x, p = blockIdx.z;
+    const int t = ovr_b ? slot_t[2 * p + blockIdx.y] : (int)blockIdx.y;
+    const int tid = threadIdx.x;
+    if (t < 0) return;
+    NPVP(0);
+    const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
+    const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
+    // 1. blocks mined in t, block order
+    const int n = s2_compact(a, B, t, ob, ot, ids, S2_NMAX);
+    const size_t pt = ovr_b ? (size_t)2 * p + blockIdx.y : ((size_t)p * T + t);
+    if (n > S2_NMAX) {  // larger than the on-chip buffers: handed to k_stage2_big
+        if (tid == 0) big_items[atomicAdd(big_count, 1)] = S2Item{s, (int)blockIdx.y, p, n};
+        return;
+    }
     __syncthreads();
     NPVP(1);
     // 2. mining-cost sum of the period (numpy pairwise, block order), once per (p, t)
     if (s == 0) {
         for (int k = tid; k < n; k += S2_THREADS) ms[k] = __ldg(cost + (size_t)ids[k] * T + t);
         __syncthreads();
-        const double cs = s2_pairwise(ms, n, s_scr);
+        const double cs = s2_pairwise(ms, n, s_ls, s_ll, s_scr);
         if (tid == 0) {
             costsum[pt] = cs;
             nmined[pt] = n;
@@ -283,72 +361,220 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     }
     __syncthreads();
     NPVP(3);
-    // 4. the greedy fill (evaluate.py:174-182): a sequential f64 recurrence.  Warp 0 takes 32
-    //    blocks per step speculatively as whole blocks: every lane runs the two chains
-    //    hours_left -= m / rate and total += d * m over the step's 32 blocks (values broadcast by
-    //    shuffles, the same adds in the same order) and lane j keeps the values before block j;
-    //    then each lane tests its block for a stop (d <= 0, hours_left <= 0) or a partial take
-    //    (hours_left * rate < m).  At the first flagged block the exact scalar loop takes over from
-    //    that block's hours_left and total.
+    // 4. the greedy fill (evaluate.py:174-182)
     __shared__ int s_kpos;
-    __shared__ double s_q32[32], s_dm32[32];
     if (tid == 0) s_kpos = n;
     __syncthreads();
     for (int k = tid; k < n; k += S2_THREADS)
         if (dsort[k] <= 0) atomicMin(&s_kpos, k);  // first d <= 0 (the scalar loop's stop)
     __syncthreads();
-    if (warp == 0) {
-        const int kpos = s_kpos;
-        double hl = __ldg(hours + t), total = 0.0;
-        int k = n;
-        for (int k0 = 0; k0 < n; k0 += 32) {
-            const int kk = k0 + lane;
-            const bool in = kk < n;
-            const double m = in ? ms[kk] : 0.0;
-            s_q32[lane] = in ? qs[kk] : 0.0;  // broadcast reads below: independent of the chains,
-            s_dm32[lane] = in ? f64_mul(dsort[kk], m) : 0.0;  // so they issue ahead of them
-            __syncwarp();
-            double h = hl, tt = total, h_mine = 0.0, t_mine = 0.0;
-#pragma unroll 8
-            for (int j = 0; j < 32; j++) {
-                if (lane == j) {
-                    h_mine = h;
-                    t_mine = tt;
-                }
-                h = f64_sub(h, s_q32[j]);
-                tt = f64_add(tt, s_dm32[j]);
-            }
-            __syncwarp();
-            const bool stop = !in || kk >= kpos || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
-            const unsigned sm = __ballot_sync(0xffffffffu, stop);
-            if (sm) {
-                const int jf = __ffs(sm) - 1;
-                k = k0 + jf;
-                hl = __shfl_sync(0xffffffffu, h_mine, jf);
-                total = __shfl_sync(0xffffffffu, t_mine, jf);
-                break;
-            }
-            hl = h;
-            total = tt;
-        }
-        if (lane == 0) {
-            for (; k < n; k++) {
-                const double d = dsort[k];
-                if (d <= 0 || hl <= 0) break;
-                const double mk = ms[k];
-                const double hr = f64_mul(hl, rate);
-                if (hr < mk) {  // take = min(m, hours_left * rate) = hours_left * rate
-                    total = f64_add(total, f64_mul(d, hr));
-                    hl = f64_sub(hl, f64_div(hr, rate));
-                } else {
-                    total = f64_add(total, f64_mul(d, mk));
-                    hl = f64_sub(hl, qs[k]);
-                }
-            }
-            raw[pt * S + s] = total;
-        }
+    if (tid < 32) {
+        const double total = s2_greedy_warp(
+            n, s_kpos, __ldg(hours + t), rate, [&](int k) { return dsort[k]; }, [&](int k) { return ms[k]; },
+            [&](int k) { return qs[k]; });
+        if (tid == 0) raw[pt * S + s] = total;
     }
     NPVP(4);
+}
+
+// strict total order of the large-period sort: density descending, then block ascending -- the
+// order of np.argsort(-density, kind="stable") over blocks listed in block order
+__device__ __forceinline__ bool s2_before(double da, int ba, double db, int bb) {
+    return da > db || (da == db && ba < bb);
+}
+
+// Per-CTA global scratch of the large-period path (n <= B): ids | keys A | keys B | blocks A | blocks B
+__host__ __device__ inline size_t s2_big_stride(int B) { return (size_t)B * 28 + 64; }
+
+// k_stage2_big: the (s, t, schedule) problems whose period mines more than S2_NMAX blocks, one
+// persistent CTA per SM looping over the work list k_stage2 filled.  Same steps and arithmetic as
+// k_stage2 with the arrays in L2-resident global scratch:
+//   1. compaction of the period's blocks into ids[] (block order);
+//   2. s == 0: mining-cost sum, numpy pairwise order, over ids[];
+//   3. (density, block) of every block with density > 0 (the greedy stops at the first d <= 0, so
+//      the others never matter), in block order;
+//   4. sort: runs of S2_NMAX sorted on chip by the block radix sort (stable: ties keep block
+//      order), then pairwise merge-path rounds over the strict (density desc, block asc) order;
+//   5. the greedy fill over the sorted prefix (s2_greedy_warp).
+__global__ void __launch_bounds__(S2_THREADS, 1)
+    k_stage2_big(const int32_t *__restrict__ assign, int B, int T, int S, int Sp, const double *__restrict__ mass,
+                 const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
+                 double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
+                 const S2Item *__restrict__ items, const int32_t *__restrict__ count, unsigned char *__restrict__ scratch,
+                 const int32_t *__restrict__ ovr_b, const int32_t *__restrict__ ovr_t,
+                 const int32_t *__restrict__ slot_t) {
+    extern __shared__ __align__(16) unsigned char s2_dyn[];
+    typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
+    __shared__ int s_np;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned char *base = scratch + (size_t)blockIdx.x * s2_big_stride(B);
+    int32_t *ids = reinterpret_cast<int32_t *>(base);
+    double *ka = reinterpret_cast<double *>(base + (((size_t)B * 4 + 15) & ~(size_t)15));
+    double *kb = ka + B;
+    int32_t *ba = reinterpret_cast<int32_t *>(kb + B);
+    int32_t *bb = ba + B;
+    const int nitems = *count;
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const S2Item it = items[w];
+        const int s = it.s, p = it.z;
+        const int t = ovr_b ? slot_t[2 * p + it.y] : it.y;
+        const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
+        const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
+        const size_t pt = ovr_b ? (size_t)2 * p + it.y : ((size_t)p * T + t);
+        __syncthreads();  // the previous item's readers of the scratch are done
+        // 1.
+        const int n = s2_compact(a, B, t, ob, ot, ids, B);
+        __syncthreads();
+        // 2.
+        if (s == 0) {
+            for (int k = tid; k < n; k += S2_THREADS) kb[k] = __ldg(cost + (size_t)ids[k] * T + t);
+            __syncthreads();
+            // leaves: at most n/64 + 2 of them, in ba / bb; leaf values in ka
+            const double cs = s2_pairwise(kb, n, ba, bb, ka);
+            if (tid == 0) {
+                costsum[pt] = cs;
+                nmined[pt] = n;
+            }
+            __syncthreads();
+        }
+        // 3. positive densities in block order: per 1024-tile, a ballot scan
+        if (tid == 0) s_np = 0;
+        __syncthreads();
+        for (int k0 = 0; k0 < n; k0 += S2_THREADS) {
+            const int k = k0 + tid;
+            double d = 0.0;
+            int b = -1;
+            if (k < n) {
+                b = ids[k];
+                d = f64_div(__ldg(vmax + (size_t)b * Sp + s), __ldg(mass + b));
+            }
+            const bool keep = k < n && d > 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            __shared__ int s_wcnt[32];
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int off = s_np;
+            for (int x = 0; x < warp; x++) off += s_wcnt[x];
+            if (keep) {
+                const int q = off + __popc(bal & ((1u << lane) - 1u));
+                ka[q] = d;
+                ba[q] = b;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int tot = 0;
+                for (int x = 0; x < 32; x++) tot += s_wcnt[x];
+                s_np += tot;
+            }
+            __syncthreads();
+        }
+        const int np_ = s_np;
+        // 4a. runs of S2_NMAX sorted on chip (blocked arrangement in block order: stable)
+        for (int r0 = 0; r0 < np_; r0 += S2_NMAX) {
+            const int rn = min(S2_NMAX, np_ - r0);
+            double dk[S2_IPT];
+            int ik[S2_IPT];
+#pragma unroll
+            for (int u = 0; u < S2_IPT; u++) {
+                const int k = tid * S2_IPT + u;
+                dk[u] = k < rn ? ka[r0 + k] : -kInf;
+                ik[u] = k < rn ? ba[r0 + k] : INT_MAX;
+            }
+            __syncthreads();
+            S2Sort(sort_tmp).SortDescending(dk, ik);
+#pragma unroll
+            for (int u = 0; u < S2_IPT; u++) {
+                const int k = tid * S2_IPT + u;
+                if (k < rn) {
+                    ka[r0 + k] = dk[u];
+                    ba[r0 + k] = ik[u];
+                }
+            }
+            __syncthreads();
+        }
+        // 4b. merge rounds, ping-pong between (ka, ba) and (kb, bb)
+        double *srck = ka, *dstk = kb;
+        int32_t *srcb = ba, *dstb = bb;
+        for (int wdt = S2_NMAX; wdt < np_; wdt *= 2) {
+            for (int m0 = 0; m0 < np_; m0 += 2 * wdt) {
+                const int mid = min(m0 + wdt, np_), end = min(m0 + 2 * wdt, np_);
+                const int la = mid - m0, lb = end - mid, L = la + lb;
+                const double *Ak = srck + m0, *Bk = srck + mid;
+                const int32_t *Ab = srcb + m0, *Bb = srcb + mid;
+                const int per = (L + S2_THREADS - 1) / S2_THREADS;
+                const int d0 = min(tid * per, L), d1 = min(d0 + per, L);
+                if (d0 < d1) {
+                    int lo = max(0, d0 - lb), hi = min(d0, la);  // merge path: A elements among the first d0
+                    while (lo < hi) {
+                        const int md = (lo + hi) >> 1;
+                        if (s2_before(Ak[md], Ab[md], Bk[d0 - 1 - md], Bb[d0 - 1 - md]))
+                            lo = md + 1;
+                        else
+                            hi = md;
+                    }
+                    int ia = lo, ib = d0 - lo;
+                    for (int k = d0; k < d1; k++) {
+                        const bool takeA = ib >= lb || (ia < la && s2_before(Ak[ia], Ab[ia], Bk[ib], Bb[ib]));
+                        if (takeA) {
+                            dstk[m0 + k] = Ak[ia];
+                            dstb[m0 + k] = Ab[ia];
+                            ia++;
+                        } else {
+                            dstk[m0 + k] = Bk[ib];
+                            dstb[m0 + k] = Bb[ib];
+                            ib++;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            double *tk = srck;
+            srck = dstk;
+            dstk = tk;
+            int32_t *tb = srcb;
+            srcb = dstb;
+            dstb = tb;
+        }
+        // 5. the greedy fill over the positive prefix
+        if (tid < 32) {
+            const double *dk_ = srck;
+            const int32_t *bk_ = srcb;
+            const double total = s2_greedy_warp(
+                np_, np_, __ldg(hours + t), rate, [&](int k) { return dk_[k]; },
+                [&](int k) { return __ldg(mass + bk_[k]); }, [&](int k) { return f64_div(__ldg(mass + bk_[k]), rate); });
+            if (tid == 0) raw[pt * S + s] = total;
+        }
+    }
+}
+
+// Launches the stage-2 problems of grid (S, gy, gz): k_stage2 for every period that fits on chip,
+// then k_stage2_big for the rest (only when some period can exceed S2_NMAX, i.e. B > S2_NMAX).
+static int run_stage2(pp_ctx *c, cudaStream_t st, const int32_t *da, int gy, int gz, double *raw, double *costsum,
+                      int32_t *nmined, const int32_t *ovr_b, const int32_t *ovr_t, const int32_t *slot_t) {
+    const int B = c->B, T = c->T, S = c->S;
+    const bool big = B > S2_NMAX;
+    TRY(c->s2_items.ensure(sizeof(S2Item) * (size_t)S * gy * gz + 16));
+    int32_t *count = reinterpret_cast<int32_t *>(c->s2_items.as<unsigned char>() + sizeof(S2Item) * (size_t)S * gy * gz);
+    S2Item *items = c->s2_items.as<S2Item>();
+    if (big) CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+    TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
+    k_stage2<<<dim3(S, gy, gz), S2_THREADS, S2Layout::bytes(), st>>>(
+        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
+        c->rate, raw, costsum, nmined, items, count, ovr_b, ovr_t, slot_t);
+    CUDA_TRY(cudaGetLastError());
+    if (!big) return PP_OK;
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || sms < 1) sms = 148;
+    // one CTA per SM, scratch budget 1 GiB
+    const size_t stride = s2_big_stride(B);
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)sms, ((size_t)1 << 30) / stride));
+    TRY(c->s2_scratch.ensure(stride * grid));
+    TRY(ensure_max_smem(k_stage2_big, S2Layout::bytes(), c->device));
+    k_stage2_big<<<grid, S2_THREADS, S2Layout::bytes(), st>>>(
+        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
+        c->rate, raw, costsum, nmined, items, count, c->s2_scratch.as<unsigned char>(), ovr_b, ovr_t, slot_t);
+    CUDA_TRY(cudaGetLastError());
+    return PP_OK;
 }
 
 // _npv / per_scenario_npv accumulation in the reference's order (t outer, s inner)
@@ -388,10 +614,8 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
                                   const double *__restrict__ mcost, const int32_t *__restrict__ mn,
                                   const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                                   const double *__restrict__ disc,
-                                  const double *__restrict__ sigma, double *__restrict__ npv,
-                                  const int32_t *__restrict__ flag_in, int32_t *__restrict__ flag_out) {
+                                  const double *__restrict__ sigma, double *__restrict__ npv) {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m == 0 && flag_out) *flag_out = *flag_in;  // travels back with the values in one copy
     if (m >= M) return;
     const int t0 = slot_t[2 * m], t1 = slot_t[2 * m + 1];
     double total = 0.0;
@@ -461,26 +685,17 @@ int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, 
     c->npv_gen++;  // overwrites pp_npv_moves' cached base results
     TRY(c->npv_cost.ensure(sizeof(double) * (size_t)P * T));
     TRY(c->npv_n.ensure(sizeof(int32_t) * (size_t)P * T));
-    TRY(c->npv_flag.ensure(sizeof(int32_t)));
-    CUDA_TRY(cudaMemsetAsync(c->npv_flag.ptr, 0, sizeof(int32_t), st));
-    TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
-    k_stage2<<<dim3(S, T, P), S2_THREADS, S2Layout::bytes(), st>>>(
-        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(), c->npv_flag.as<int32_t>(),
-        nullptr, nullptr, nullptr);
-    CUDA_TRY(cudaGetLastError());
+    TRY(run_stage2(c, st, da, T, P, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(),
+                   nullptr, nullptr, nullptr));
     k_npv_final<<<P, 32, 0, st>>>(T, S, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(),
                                   c->disc.as<double>(), (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
                                   dps);
     CUDA_TRY(cudaGetLastError());
     if (mem == PP_MEM_HOST) {
-        int32_t flag = 0;
         CUDA_TRY(cudaMemcpyAsync(npv_out, dn, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
         if (per_scen_out)
             CUDA_TRY(cudaMemcpyAsync(per_scen_out, dps, sizeof(double) * (size_t)P * S, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(&flag, c->npv_flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
-        if (flag) return fail(PP_ERR_SHAPE, "a period mines more than %d blocks (device stage-2 limit)", S2_NMAX);
     }
     return PP_OK;
 }
@@ -531,17 +746,17 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
             }
         }
     }
-    // one packed upload (assign | blocks | periods | slots | runs | sources | stage-2 flag = 0)
-    // and one packed result copy (values | flag): each separate small copy costs a PCIe round trip
-    const size_t nin = (size_t)B + 8 * (size_t)M + 1;
+    // one packed upload (assign | blocks | periods | slots | runs | sources) and one result copy:
+    // each separate small copy costs a PCIe round trip
+    const size_t nin = (size_t)B + 8 * (size_t)M;
     TRY(c->h_assign.ensure(sizeof(int32_t) * nin));
     int32_t *da = c->h_assign.as<int32_t>(), *db = da + B, *dt = db + M, *ds = dt + M, *dr = ds + 2 * M,
-            *dsrc = dr + 2 * M, *dflag = dsrc + 2 * M;
+            *dsrc = dr + 2 * M;
     TRY(c->npv_raw.ensure(sizeof(double) * ((size_t)T * S + (size_t)2 * M * S)));
     TRY(c->npv_cost.ensure(sizeof(double) * ((size_t)T + 2 * (size_t)M)));
     TRY(c->npv_n.ensure(sizeof(int32_t) * ((size_t)T + 2 * (size_t)M)));
     TRY(c->h_d1.ensure(sizeof(double) * ((size_t)M + 1)));
-    const size_t out_bytes = sizeof(double) * ((size_t)M + 1);
+    const size_t out_bytes = sizeof(double) * (size_t)M;
     unsigned char *stage = nullptr;
     TRY(host_stage(c, std::max(sizeof(int32_t) * nin, out_bytes), &stage));
     std::vector<int32_t> pkv(host ? 0 : nin);  // device mode returns before the copy completes:
@@ -553,46 +768,36 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
         std::copy(slot.begin(), slot.end(), pk + B + 2 * M);
         std::copy(run.begin(), run.end(), pk + B + 4 * M);
         std::copy(src.begin(), src.end(), pk + B + 6 * M);
-        pk[nin - 1] = 0;
         CUDA_TRY(cudaMemcpyAsync(da, pk, sizeof(int32_t) * nin, cudaMemcpyHostToDevice, st));
     }
-    TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
     double *braw = c->npv_raw.as<double>(), *mraw = braw + (size_t)T * S;
     double *bcost = c->npv_cost.as<double>(), *mcost = bcost + T;
     int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
-    const bool base_hit = host && c->npvm_gen == c->npv_gen && c->npvm_ptrs[0] == braw && c->npvm_ptrs[1] == bcost &&
-                          c->npvm_ptrs[2] == bn && c->npvm_base == ha;
-    if (!base_hit)
-        k_stage2<<<dim3(S, T, 1), S2_THREADS, S2Layout::bytes(), st>>>(
-            da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(),
-            c->hours.as<double>(), c->rate, braw, bcost, bn, dflag, nullptr, nullptr, nullptr);
-    k_stage2<<<dim3(S, 2, M), S2_THREADS, S2Layout::bytes(), st>>>(
-        da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, mraw, mcost, mn, dflag, db, dt, dr);
+    // the base schedule's results are reused while the tables (npv_gen), the three buffers (their
+    // allocation generation: a re-allocation may return the same address) and the base are unchanged
+    const bool base_hit = host && c->npvm_gen == c->npv_gen && c->npvm_bufgen[0] == c->npv_raw.gen &&
+                          c->npvm_bufgen[1] == c->npv_cost.gen && c->npvm_bufgen[2] == c->npv_n.gen &&
+                          c->npvm_base == ha;
+    if (!base_hit) TRY(run_stage2(c, st, da, T, 1, braw, bcost, bn, nullptr, nullptr, nullptr));
+    TRY(run_stage2(c, st, da, 2, M, mraw, mcost, mn, db, dt, dr));
     double *dn = host ? c->h_d1.as<double>() : npv_out;
-    int32_t *flag_out = host ? reinterpret_cast<int32_t *>(c->h_d1.as<double>() + M) : nullptr;
     k_npv_moves_final<<<(M + 127) / 128, 128, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
                                                         c->disc.as<double>(),
-                                                        (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
-                                                        dflag, flag_out);
+                                                        (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
     CUDA_TRY(cudaGetLastError());
     if (host) {
         CUDA_TRY(cudaMemcpyAsync(stage, dn, out_bytes, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
         std::memcpy(npv_out, stage, sizeof(double) * M);
-        int32_t flag = 0;
-        std::memcpy(&flag, stage + sizeof(double) * M, sizeof(int32_t));
-        if (flag) {
-            c->npvm_gen = ~0ull;
-            return fail(PP_ERR_SHAPE, "a period mines more than %d blocks (device stage-2 limit)", S2_NMAX);
-        }
         if (!base_hit) {  // the base results just computed are complete and valid
             c->npvm_gen = c->npv_gen;
-            c->npvm_ptrs[0] = braw;
-            c->npvm_ptrs[1] = bcost;
-            c->npvm_ptrs[2] = bn;
+            c->npvm_bufgen[0] = c->npv_raw.gen;
+            c->npvm_bufgen[1] = c->npv_cost.gen;
+            c->npvm_bufgen[2] = c->npv_n.gen;
             c->npvm_base = ha;
         }
+    } else {
+        c->npvm_gen = ~0ull;  // device mode: the base results may be read before they are complete
     }
     return PP_OK;
 }

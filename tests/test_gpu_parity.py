@@ -687,3 +687,64 @@ def test_full_size_configs_against_oracle(oracle_lib, name):
     perm = np.random.default_rng(7).permutation(c["cand"].size)
     assert eng.eval_candidates(c["cand"][perm].copy(), None, net=True)["best"] == got["best"]
     eng.close()
+
+
+def _big_period_population(c):
+    """Schedules whose periods hold far more than the 6,144 blocks of k_stage2's on-chip buffers:
+    the C2 schedule folded into 4 periods (~12.5k blocks each), everything in one period (n = B),
+    and a ragged mix (one period of ~25k beside small ones) -- the large-period path
+    (k_stage2_big: on-chip runs + merge rounds in global scratch) next to the on-chip one."""
+    a = c["assign"].astype(np.int64)
+    T = c["bm"].n_periods
+    fold = np.where(a >= 0, a // 4, -1)
+    one = np.zeros_like(a)
+    rag = a.copy()
+    rag[(a >= 0) & (a < 6)] = 2
+    rag[np.arange(a.size) % 97 == 0] = -1
+    assert fold.max() < T
+    return np.stack([fold, one, rag, a])
+
+
+def test_npv_relaxed_large_periods_against_oracle(oracle_lib):
+    """Stage 2 (evaluate.py:166-183) of periods mining 12k-50k blocks runs on the device and equals
+    the oracle bit for bit, with and without sigma, per scenario included."""
+    c = config("C2")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    o = oracle_lib.Oracle(bm, c["vmax"], c["sigma"])
+    pop = _big_period_population(c)
+    for use_sigma in (True, False):
+        npv, ps = eng.npv_relaxed(pop, per_scenario=True, use_sigma=use_sigma)
+        for k in range(pop.shape[0]):
+            v, pr = o.npv_relaxed(pop[k], bm.plant_hours, bm.mode_rates[0], use_sigma=use_sigma)
+            assert npv[k] == v and same(ps[k], pr), (k, use_sigma)
+    eng.close()
+
+
+def test_npv_moves_large_periods_equal_full_recompute():
+    """pp_npv_moves re-solving periods of ~12.5k blocks (the large-period path with the variant's
+    moved block) equals pp_npv_relaxed of each modified schedule."""
+    c = config("C2")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    a = _big_period_population(c)[0].astype(np.int32)
+    rng = np.random.default_rng(3)
+    blocks = rng.integers(0, bm.n_blocks, 24).astype(np.int32)
+    periods = rng.integers(-1, 4, 24).astype(np.int32)
+    got = eng.npv_moves(a, blocks, periods)
+    batch = np.repeat(a[None, :], blocks.size, axis=0)
+    batch[np.arange(blocks.size), blocks] = periods
+    assert same(got, eng.npv_relaxed(batch))
+    eng.close()
+
+
+def test_npv_relaxed_c4_against_oracle(oracle_lib):
+    """C4 (200k blocks, 20 periods of ~10k blocks, S = 50): every period is above the on-chip size."""
+    c = config("C4")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]))
+    o = oracle_lib.Oracle(bm, c["vmax"], c["sigma"])
+    npv, ps = eng.npv_relaxed(c["assign"][None, :], per_scenario=True)
+    v, pr = o.npv_relaxed(c["assign"], bm.plant_hours, bm.mode_rates[0])
+    assert npv[0] == v and same(ps[0], pr)
+    eng.close()
