@@ -15,8 +15,15 @@ One step = one evaluator batch of the headline configuration C2 (SURVEY.md §8(d
 `value` is device-timed (CUDA events, inputs resident in HBM, L2 flushed by a 256 MiB
 write between timed steps); `e2e` is the same batch through the C ABI with host
 buffers (pinned), host<->device copies inside the timed region.
-`--impl reference` times the CPU restatement of the reference (oracle/, the reference
-itself is pure Python and cannot run on the GPU box) on all host cores.
+`--impl reference` times the CPU restatement of the reference path (oracle/oracle.c, OpenMP,
+all host cores; the reference is pure Python, so there is no compiled oracle/_ref) and, beside
+it, the reference itself -- pitplan's own evaluate_candidates_parallel from its pip install
+under baseline/_ref, worker_count 1 and os.cpu_count(), best of 3.
+
+Roofline: `achieved` = SURVEY §8(d)'s algorithmic bytes of one batch
+(M·(80 + 8·d̄) + 8·M·S, f64 values) / the k_eval_warp launch time measured with CUDA events
+around a graph holding only that launch; the compulsory bytes (each candidate's rows once) and
+ncu's measured DRAM bytes of the same config are reported beside it.
 """
 
 from __future__ import annotations
@@ -115,20 +122,82 @@ def build_inputs(config: str, rank: int = 0):
     return c
 
 
-def _ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum of one k_eval_warp launch from the committed
-    `ncu --set full` capture (profiles/r01_ncu_full.json), or None."""
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full.json")
-    try:
-        m = json.load(open(f))["k_eval_warp"]
-    except (OSError, KeyError, ValueError):
-        return None
+def _ncu_traffic(config: str):
+    """(dram__bytes_read.sum + dram__bytes_write.sum of one k_eval_warp launch, source file) from the
+    committed `ncu --set full` capture of the same --config (profiles/r02_ncu_<config>.json, or the
+    round-1 C2 capture for C2), or (None, None)."""
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    cands = [f"r02_ncu_{config.lower()}.json"] + (["r01_ncu_full.json"] if config == "C2" else [])
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        v, u = m[k]
-        tot += float(v) * scale.get(u, 1)
+    for name in cands:
+        try:
+            m = json.load(open(os.path.join(prof, name)))["k_eval_warp"]
+        except (OSError, KeyError, ValueError):
+            continue
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = m[k]
+            tot += float(v) * scale.get(u, 1)
+        return tot, f"profiles/{name}"
+    return None, None
+
+
+def precedence_feasible_moves(c) -> int:
+    """Moves whose precedence window admits the period (evaluate.py:361-372): the moves that reach
+    the per-scenario statistics (scen_evals_performed = this x S)."""
+    bm, a, cand, T = c["bm"], c["assign"], c["cand"], c["T"]
+    pp_, pi_, sp_, si_ = bm.csr()
+    tot = 0
+    for b in cand.tolist():
+        pa = a[pi_[pp_[b]:pp_[b + 1]]]
+        if pa.size and np.any(pa < 0):
+            continue
+        lo = int(pa.max()) if pa.size else 0
+        sa = a[si_[sp_[b]:sp_[b + 1]]]
+        sa = sa[sa >= 0]
+        hi = int(sa.min()) if sa.size else T - 1
+        tot += max(0, min(hi, T - 1) - max(lo, 0) + 1)
     return tot
+
+
+def python_reference_timing(config: str, cand: np.ndarray, assign: np.ndarray, repeats: int = 3) -> dict | None:
+    """The reference itself: pitplan.evaluate.evaluate_candidates_parallel from its pip install under
+    baseline/_ref, on inputs built by the reference's own generators (identical to synth's, digests
+    checked in tests), worker_count 1 and os.cpu_count(), best of `repeats`."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pitplan")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    from pitplan.blockmodel import generate_synthetic
+    from pitplan.evaluate import Schedule, evaluate_candidates_parallel
+    from pitplan.scenarios import sample_lognormal
+    from pitplan.uncertainty import uncertainty_factors
+
+    from paper_2511_18296_b200 import synth
+
+    spec = {"C1": (4000, (20, 20, 10), 10, 10, 1.3), "C2": (50000, (50, 50, 20), 15, 20, 1.3),
+            "C3": (50000, (50, 50, 20), 15, 200, 0.3), "C4": (200000, (100, 100, 20), 20, 50, 1.3)}[config]
+    n, dims, T, S, cf = spec
+    t0 = time.perf_counter()
+    inst = generate_synthetic(n, dims, T, 1, seed=1, n_rock_types=1, capacity_factor=cf)
+    scen = sample_lognormal(inst, S, 0.3, seed=2)
+    sigma = uncertainty_factors(inst, scen.grades)
+    build_s = time.perf_counter() - t0
+    sched = Schedule(np.asarray(assign, dtype=np.int64).copy())
+    cl = [int(b) for b in cand]
+    out = {"kind": "reference", "impl": "pitplan.evaluate.evaluate_candidates_parallel (baseline/_ref)",
+           "inputs_build_s": build_s, "moves": len(cl) * T, "scenarios": S}
+    for w in sorted({1, os.cpu_count() or 1}):
+        ts = []
+        for _ in range(repeats):
+            t1 = time.perf_counter()
+            evaluate_candidates_parallel(inst, sched, cl, scen, None, sigma, worker_count=w, net_mining_cost=True)
+            ts.append(time.perf_counter() - t1)
+        best = min(ts)
+        out[f"W{w}"] = {"s_per_batch": best, "value": len(cl) * T * S / best, "unit": UNIT, "cores": w,
+                        "moves_per_s": len(cl) * T / best}
+    return out
 
 
 def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
@@ -217,6 +286,8 @@ def run_reference(args):
         "config": workload_config(args, c),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline_reference": None if args.no_python_ref else python_reference_timing(args.config, c["cand"],
+                                                                                        c["assign"]),
     }
     print(json.dumps(line))
     return 0
@@ -326,19 +397,35 @@ def run_gpu(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
 
-    # dominant kernel alone: k_eval_warp timed with events on its stream, L2 flushed,
-    # period masses refreshed beforehand so the call launches only the evaluation kernel
-    kms = []
-    for i in range(min(args.steps, 200)):
+    # dominant kernel alone: k_eval_warp in its own CUDA graph (period masses refreshed beforehand,
+    # so the captured call launches only the evaluation kernel and its output-init copy), timed
+    # with events on its stream, L2 flushed between replays
+    eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
+    eng.period_mass_device(pm_copy, stream=sptr)
+    torch.cuda.synchronize()
+    kgraph = None
+    if not args.no_graph:
+        try:
+            kg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(kg):
+                eng.eval_candidates_device(cand_d, out, None, net=True, stream=torch.cuda.current_stream().cuda_stream)
+            kg.replay()
+            torch.cuda.synchronize()
+            kgraph = kg
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] kernel graph capture failed, eager launch: {exc}", file=sys.stderr)
+    nk = min(args.steps, 200)
+    for i in range(nk):
         flush.fill_(i)
-        eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
-        eng.period_mass_device(pm_copy, stream=sptr)
         kstarts[i].record(stream)
-        eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
+        if kgraph is not None:
+            kgraph.replay()
+        else:
+            eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
         kends[i].record(stream)
     torch.cuda.synchronize()
-    kms = [s.elapsed_time(e) for s, e in zip(kstarts[:min(args.steps, 200)], kends[:min(args.steps, 200)])]
-    k_ms = float(np.mean(kms))
+    kms = [s.elapsed_time(e) for s, e in zip(kstarts[:nk], kends[:nk])]
+    k_ms = float(np.median(kms))
 
     # e2e through the C ABI with host (pinned) buffers on every rank: H2D schedule + candidates,
     # both kernels, D2H of the best moves and the sparse statistics; for N > 1 also the 16-byte
@@ -394,20 +481,28 @@ def run_gpu(args):
     if rank == 0:
         hbm, peak_kind = _peaks()
         ab = algorithmic_bytes(c, deg_mean, int(out["n_pairs"].item()))
-        # roofline numerator: the compulsory bytes of one launch (each candidate's rows once for
-        # all its periods). SURVEY §8(d)'s per-move figure counts every (b, t) move
-        # as re-reading its rows; it is reported beside it and exceeds the HBM peak at C3/C4
-        achieved = ab["per_launch"] / (k_ms * 1e-3) / 1e9
-        achieved_survey = ab["survey_uncached"] / (k_ms * 1e-3) / 1e9
+        # roofline numerator (the contract's): SURVEY §8(d)'s algorithmic bytes of the batch, which
+        # count every (b, t) move as reading its rows and its scenario row; the kernel reads each
+        # candidate's rows once for all its periods, so the compulsory bytes and ncu's DRAM bytes
+        # are reported beside it
+        ks = k_ms * 1e-3
+        achieved = ab["survey_uncached"] / ks / 1e9
+        achieved_comp = ab["per_launch"] / ks / 1e9
+        traffic, traffic_src = (args.ncu_traffic, "--ncu-traffic") if args.ncu_traffic is not None \
+            else _ncu_traffic(args.config)
         value = world * M * S / (t_max * 1e-3)
+        n_prec = precedence_feasible_moves(c)
 
         cpu = None
+        pyref = None
         if world == 1 and not args.no_cpu_baseline:
             ts, nth = cpu_reference(c, seconds=args.cpu_seconds)
             t_cpu = float(np.median(ts))
             cpu = {"value": M * S / t_cpu, "unit": UNIT, "cores": nth, "kind": "port",
                    "sample": f"{len(ts)} full batches ({M} moves x {S} scenarios each, incl. period masses), "
                              f"oracle/oracle.c with OpenMP, median"}
+            if not args.no_python_ref:
+                pyref = python_reference_timing(args.config, c["cand"], c["assign"])
         launches_per_step = 2 + (1 if world > 1 else 0)  # k_pm_cluster + k_eval_warp [+ k_reduce_best]
         result = {
             "metric": METRIC,
@@ -431,16 +526,25 @@ def run_gpu(args):
                 "peak": hbm,
                 "unit": "GB/s",
                 "frac": achieved / hbm,
-                "traffic": args.ncu_traffic if args.ncu_traffic is not None else _ncu_traffic(),
+                "traffic": traffic,
+                "traffic_source": traffic_src,
                 "kernel": "k_eval_warp",
                 "kernel_ms": k_ms,
-                "algorithmic_bytes_per_launch": ab["per_launch"],
-                "algorithmic_basis": "compulsory: per candidate 4+32+4+8+8*deg+8*T+8*Sp+13 B, per feasible pair 24 B",
+                "kernel_timing": "median CUDA-event time of a graph holding only the k_eval_warp launch, L2 flushed",
+                "algorithmic_bytes_per_launch": ab["survey_uncached"],
+                "algorithmic_basis": "SURVEY §8(d): M*(80 + 8*deg) + 8*M*S (f64 scenario values), M = moves per batch",
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                "survey_uncached_bytes_per_launch": ab["survey_uncached"],
-                "survey_uncached_achieved": achieved_survey,
-                "survey_uncached_frac": achieved_survey / hbm,
+                "compulsory_bytes_per_launch": ab["per_launch"],
+                "compulsory_basis": "per candidate 4+32+4+8+8*deg+8*T+8*Sp+13 B, per feasible pair 24 B",
+                "compulsory_achieved": achieved_comp,
+                "compulsory_frac": achieved_comp / hbm,
+                "dram_achieved": (traffic / ks / 1e9) if traffic else None,
+                "dram_frac": (traffic / ks / 1e9 / hbm) if traffic else None,
             },
+            "moves_per_step": M,
+            "scen_evals_nominal_per_step": M * S,
+            "precedence_feasible_moves_per_step": n_prec,
+            "scen_evals_performed_per_step": n_prec * S,
             "e2e": {"value": world * M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_t * 1e3,
                     "api": "Engine.set_schedule + Engine.eval_candidates (pp_set_schedule/pp_eval_candidates, "
@@ -449,6 +553,7 @@ def run_gpu(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
+            "cpu_baseline_reference": pyref,
             "best_move": {"block": r["best"][0], "period": r["best"][1], "value": r["best"][2]},
         }
         print(json.dumps(result))
@@ -469,6 +574,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    ap.add_argument("--no-python-ref", action="store_true", help="skip timing pitplan itself (baseline/_ref)")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram bytes per k_eval_warp launch from the committed ncu capture")
     args = ap.parse_args()

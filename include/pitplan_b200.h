@@ -210,6 +210,12 @@ PP_API int pp_set_plant(pp_ctx *ctx, const double *plant_hours, double rate);
  * (periods of more than 6144 mined blocks are sorted in global scratch by a second kernel). */
 PP_API int pp_npv_relaxed(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, uint32_t flags, double *npv_out,
                    double *per_scen_out, int32_t mem, void *stream);
+/* The stage-2 optimum itself (ScheduleEvaluator.stage2_raw / _solve_stage2, evaluate.py:153-183, sigma = 1)
+ * of every (schedule p, period t, scenario s): raw_out[P][T][S], and optionally the period's summed
+ * undiscounted mining cost cost_out[P][T] (numpy pairwise over its blocks in block order; 0.0 for an
+ * empty period).  In PP_MEM_DEVICE mode cost_out of an empty period is unspecified. */
+PP_API int pp_stage2(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, double *raw_out, double *cost_out,
+                     int32_t mem, void *stream);
 /* Relaxed NPV of M one-block variants of a base schedule assign[B]: variant m moves block
  * blocks[m] to periods[m] (-1 = unmine).  Only the two periods a variant changes are re-solved
  * (S stage-2 problems each); the other periods reuse the base schedule's, and the accumulation is

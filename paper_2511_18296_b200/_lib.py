@@ -7,6 +7,7 @@ entry point raises `ExtensionMissing`.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import threading
@@ -102,12 +103,51 @@ SIGNATURES = {
     "pp_npv_moves": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_int32,
                                c_void_p]),
     "pp_npv_relaxed": (c_int32, [c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p, c_int32, c_void_p]),
+    "pp_stage2": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_eject": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_double, c_void_p, c_int32, c_void_p]),
     "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_enpv_table": (c_int32, [c_void_p, c_uint32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_get_levels": (c_int32, [c_void_p, ctypes.POINTER(c_int32), c_void_p]),
     "pp_price_greedy": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
 }
+
+# entry points that launch device work: every call through the default handle is counted, so
+# tests and the bench can show the drop-ins ran on the device (and how often)
+COMPUTE_ENTRY_POINTS = frozenset({
+    "pp_set_schedule", "pp_apply_moves", "pp_eval_candidates", "pp_eval_moves", "pp_check_feasible",
+    "pp_repair", "pp_eject", "pp_npv_relaxed", "pp_stage2", "pp_npv_moves", "pp_price_greedy", "pp_reduce_best",
+    "pp_enpv_table", "pp_get_spatial",
+})
+CALLS: collections.Counter = collections.Counter()
+
+
+class _CountingLib:
+    """The ctypes handle with a per-entry-point call counter (CALLS) on the compute entry points."""
+
+    def __init__(self, handle):
+        self._handle = handle
+
+    def __getattr__(self, name):
+        fn = getattr(self._handle, name)
+        if name in COMPUTE_ENTRY_POINTS:
+            def counted(*args, _fn=fn, _name=name):
+                CALLS[_name] += 1
+                return _fn(*args)
+
+            counted.restype, counted.argtypes = fn.restype, fn.argtypes
+            fn = counted
+        self.__dict__[name] = fn
+        return fn
+
+
+def device_calls() -> dict:
+    """Calls of each compute entry point since the last reset (all threads, all contexts)."""
+    return dict(CALLS)
+
+
+def reset_device_calls() -> None:
+    CALLS.clear()
+
 
 _lock = threading.Lock()
 _lib = None
@@ -136,7 +176,8 @@ def load(path: str | None = None):
         if handle.pp_abi_version() != ABI_VERSION:
             raise ExtensionMissing(f"{p} has ABI {handle.pp_abi_version()}, expected {ABI_VERSION}; rebuild it")
         if path is None:
-            _lib = handle
+            _lib = _CountingLib(handle)
+            return _lib
         return handle
 
 

@@ -700,6 +700,46 @@ int pp_npv_relaxed(pp_ctx *c, const int32_t *assign, int32_t P, uint32_t flags, 
     return PP_OK;
 }
 
+int pp_stage2(pp_ctx *c, const int32_t *assign, int32_t P, double *raw_out, double *cost_out, int32_t mem,
+              void *stream) {
+    if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
+        return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
+    if (P < 0 || (P > 0 && (!assign || !raw_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    if (P == 0) return PP_OK;
+    TRY(use_device(c));
+    cudaStream_t st = pick(c, stream);
+    const int B = c->B, T = c->T, S = c->S;
+    const int32_t *da = assign;
+    if (mem == PP_MEM_HOST) {
+        TRY(c->h_assign.ensure(sizeof(int32_t) * (size_t)P * B));
+        CUDA_TRY(cudaMemcpyAsync(c->h_assign.ptr, assign, sizeof(int32_t) * (size_t)P * B, cudaMemcpyHostToDevice, st));
+        da = c->h_assign.as<int32_t>();
+    }
+    TRY(c->npv_raw.ensure(sizeof(double) * (size_t)P * T * S));
+    c->npv_gen++;  // overwrites pp_npv_moves' cached base results
+    TRY(c->npv_cost.ensure(sizeof(double) * (size_t)P * T));
+    TRY(c->npv_n.ensure(sizeof(int32_t) * (size_t)P * T));
+    TRY(run_stage2(c, st, da, T, P, c->npv_raw.as<double>(), c->npv_cost.as<double>(), c->npv_n.as<int32_t>(),
+                   nullptr, nullptr, nullptr));
+    // periods with no mined block have no costsum written: zero them in the copy (cost 0.0)
+    const cudaMemcpyKind k = mem == PP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CUDA_TRY(cudaMemcpyAsync(raw_out, c->npv_raw.ptr, sizeof(double) * (size_t)P * T * S, k, st));
+    if (cost_out) {
+        if (mem == PP_MEM_HOST) {
+            std::vector<double> cs((size_t)P * T);
+            std::vector<int32_t> nm((size_t)P * T);
+            CUDA_TRY(cudaMemcpyAsync(cs.data(), c->npv_cost.ptr, sizeof(double) * cs.size(), k, st));
+            CUDA_TRY(cudaMemcpyAsync(nm.data(), c->npv_n.ptr, sizeof(int32_t) * nm.size(), k, st));
+            CUDA_TRY(stream_wait(st));
+            for (size_t i = 0; i < cs.size(); i++) cost_out[i] = nm[i] > 0 ? cs[i] : 0.0;
+            return PP_OK;
+        }
+        CUDA_TRY(cudaMemcpyAsync(cost_out, c->npv_cost.ptr, sizeof(double) * (size_t)P * T, k, st));
+    }
+    if (mem == PP_MEM_HOST) CUDA_TRY(stream_wait(st));
+    return PP_OK;
+}
+
 int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
                  uint32_t flags, double *npv_out, int32_t mem, void *stream) {
     if (!c || !c->have_instance || !c->have_scen || !c->have_plant)

@@ -120,6 +120,13 @@ class Engine:
         check(self.lib.pp_set_scenarios(self._h, vmax.shape[0], ptr(vmax), ptr(sig)))
         self.n_scenarios = int(vmax.shape[0])
         self.has_sigma = sig is not None
+        self._tables = tables
+
+    def scenario_table(self) -> np.ndarray:
+        """vmax[S][B] of the bound scenario set (scenario_mode_values, single mode)."""
+        if getattr(self, "_tables", None) is None:
+            raise InvalidArgs("set_scenarios first")
+        return self._tables.vmax
 
     def _need_bm(self) -> BlockModel:
         if self.bm is None:
@@ -356,6 +363,23 @@ class Engine:
         f = _lib.PP_USE_SIGMA if (use_sigma and self.has_sigma) else 0
         check(self.lib.pp_npv_relaxed(self._h, ptr(a), P, f, ptr(npv), ptr(ps), _lib.PP_MEM_HOST, None))
         return (npv, ps) if per_scenario else npv
+
+    def stage2(self, assign_batch):
+        """Stage-2 optima raw[P][T][S] (sigma = 1) and period mining-cost sums cost[P][T] of P schedules
+        (ScheduleEvaluator.stage2_raw, evaluate.py:153-183)."""
+        bm = self._need_bm()
+        if not getattr(self, "_plant", False):
+            if not bm.single_mode_fast:
+                raise InvalidArgs("the device stage-2 path needs one mode, one rock type and a positive rate")
+            self.set_plant()
+        a = np.ascontiguousarray(np.atleast_2d(np.asarray(assign_batch)), dtype=np.int32)
+        if a.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("schedule length does not match the instance")
+        P = a.shape[0]
+        raw = np.empty((P, bm.n_periods, self.n_scenarios), np.float64)
+        cost = np.empty((P, bm.n_periods), np.float64)
+        check(self.lib.pp_stage2(self._h, ptr(a), P, ptr(raw), ptr(cost), _lib.PP_MEM_HOST, None))
+        return raw, cost
 
     def npv_moves(self, assign, blocks, periods, use_sigma=True):
         """Relaxed NPV of the schedules assign with blocks[m] moved to periods[m] (one move each),

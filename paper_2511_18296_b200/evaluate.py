@@ -14,17 +14,25 @@
     price_column                   pitplan/colgen.py:207-293  (the sequence greedy on the device)
 
 Same signatures, argument meaning, return types and error behaviour as the
-reference; the work runs in the sm_100a kernels of csrc/pitplan_b200.cu through the
-C ABI.  Objects are duck-typed: a `pitplan` Instance / ScenarioSet /
-UncertaintyFactors / Schedule, or this package's own `BlockModel` with a
-`ScenarioTables` (then `scenarios` carries both vmax and sigma and `sigma` is only
-a switch).  When `pitplan` is importable the reference's own `CandidateMove` and
-`ViolationReport` classes are returned.
+reference; the work runs in the sm_100a kernels of csrc/ through the C ABI, and no
+function here executes reference code: `pitplan` is imported only for its record types
+(CandidateMove, ViolationReport, SequenceColumn) and exception classes.  Objects are
+duck-typed: a `pitplan` Instance / ScenarioSet / UncertaintyFactors / Schedule, or this
+package's own `BlockModel` with a `ScenarioTables` (then `scenarios` carries both vmax
+and sigma and `sigma` is only a switch).
+
+One explicit exception, counted in REFERENCE_CALLS and logged: the multi-mode / multi-rock
+stage-2 LP (evaluate.py:185-220) is out of scope, so for such an instance the
+installed `ScheduleEvaluator` factory returns the reference's own evaluator class and
+`polish_schedule` runs the reference's own function (captured by install() before it
+rebinds the name).  Single-mode instances never reach the reference.
 """
 
 from __future__ import annotations
 
+import collections
 import csv
+import logging
 import os
 import threading
 from collections import OrderedDict
@@ -39,6 +47,43 @@ _MAX_CACHED = 4
 _POLISH_CHUNK = int(os.environ.get('PP_POLISH_CHUNK', '64'))  # first speculative chunk (blocks)
 _POLISH_CHUNK_MAX = 128
 _tls = threading.local()  # one engine cache per host thread (contexts are not thread-safe)
+_log = logging.getLogger(__name__)
+
+# Calls routed to the reference's own code (only the out-of-scope multi-mode LP path).
+REFERENCE_CALLS: collections.Counter = collections.Counter()
+
+
+def path_counters() -> dict:
+    """{"device": calls per C-ABI compute entry point, "reference": calls handed to reference code}."""
+    from . import _lib
+
+    return {"device": _lib.device_calls(), "reference": dict(REFERENCE_CALLS)}
+
+
+def reset_path_counters() -> None:
+    from . import _lib
+
+    _lib.reset_device_calls()
+    REFERENCE_CALLS.clear()
+
+
+def _reference_fn(module: str, name: str):
+    """The reference's own function `module.name` as it was before install() rebound it."""
+    from . import install as _inst
+
+    fn = _inst.original(module, name)
+    if fn is None:
+        import importlib
+
+        fn = getattr(importlib.import_module(module), name)
+    return fn
+
+
+def _to_reference(what: str) -> None:
+    REFERENCE_CALLS[what] += 1
+    if REFERENCE_CALLS[what] == 1:
+        _log.warning("%s: multi-mode / multi-rock stage-2 LP instance -- the reference's own code runs "
+                     "(out of scope for the device engine)", what)
 
 
 def _types():
@@ -124,6 +169,24 @@ def _bind_scenarios(e: _Entry, scenarios, sigma, params):
     e.scen_refs = (scenarios, sigma)
 
 
+def _bind_sigma_only(e: _Entry, sigma, params):
+    """literal_kernel_value=True with scenarios=None: unit = mass * 100 needs no value table, but the
+    sigma row does (evaluate.py:348-353): bind sigma[S][T] with an all-zero value table."""
+    weights = _psi_weights(params)
+    if e.params != weights:
+        e.engine.set_geology(weights)
+        e.params = weights
+    if sigma is None:
+        return
+    key = (None, id(sigma))
+    if e.scen_key == key and e.scen_refs is not None and e.scen_refs[1] is sigma:
+        return
+    sig = np.asarray(getattr(sigma, "sigma", sigma), dtype=np.float64)
+    e.engine.set_scenarios(ScenarioTables(vmax=np.zeros((sig.shape[0], e.bm.n_blocks)), sigma=sig))
+    e.scen_key = key
+    e.scen_refs = (None, sigma)
+
+
 def _assignment(schedule) -> np.ndarray:
     return np.asarray(getattr(schedule, "assignment", schedule))
 
@@ -152,13 +215,20 @@ def evaluate_candidates_parallel(
     cand = np.fromiter((int(b) for b in candidates), dtype=np.int64)
     e = _entry(instance)
     B = e.bm.n_blocks
-    if cand.size and (cand.min() < -B or cand.max() >= B):
-        raise InvalidArgs("candidate block id out of range")
-    cand = np.where(cand < 0, cand + B, cand)  # Python negative indexing, as assign[b] would
-    _bind_scenarios(e, None if literal_kernel_value and scenarios is None else scenarios, sigma, params)
+    if cand.size and (cand.min() < 0 or cand.max() >= B):
+        # the reference would index assign[b] Python-style for -B <= b < 0 and report the negative
+        # id; the engine takes block ids in [0, B) only (documented difference)
+        raise InvalidArgs("candidate block id out of range [0, n_blocks)")
+    if literal_kernel_value and scenarios is None:
+        _bind_sigma_only(e, sigma, params)
+    else:
+        _bind_scenarios(e, scenarios, sigma, params)
     eng = e.engine
-    if s is not None and not (0 <= int(s) < max(eng.n_scenarios, 1)):
-        raise InvalidArgs(f"scenario index {s} out of range")
+    if s is not None:
+        n_s = max(eng.n_scenarios, 1)
+        if not (-n_s <= int(s) < n_s):
+            raise InvalidArgs(f"scenario index {s} out of range")
+        s = int(s) % n_s  # v[s] / sigma[s] with Python indexing (evaluate.py:302, 353)
     eng.set_schedule(_assignment(schedule))
     res = eng.eval_candidates(
         cand, None if s is None else int(s), net=net_mining_cost, literal=literal_kernel_value,
@@ -315,91 +385,132 @@ def lns_repair(
     return sched
 
 
-def _reference_evaluator():
-    try:
-        from pitplan.evaluate import ScheduleEvaluator as Ref
+class _Stage2Count:
+    """Stands in for the reference's `_stage2_cache` dict (evaluate.py:147), whose only outside use
+    is `len()` in the run's timing.json (runstore.py:453): the number of stage-2 problems the
+    device solved for this evaluator (no cache: re-solves are counted again)."""
 
-        return Ref
-    except Exception:  # noqa: BLE001
-        return None
+    __slots__ = ("n",)
+
+    def __init__(self):
+        self.n = 0
+
+    def __len__(self):
+        return self.n
 
 
-class _DeviceNpv:
-    """Device half of the ScheduleEvaluator drop-in: relaxed NPV and per-scenario NPV of a schedule
-    (evaluate.py:222-258) through pp_npv_relaxed when the stage-2 fast path applies (one mode, one
-    rock type, positive rate: evaluate.py:149-150)."""
+class ScheduleEvaluator:
+    """Drop-in for pitplan.evaluate.ScheduleEvaluator (evaluate.py:126-258): npv_relaxed,
+    per_scenario_npv and objective on the device (k_stage2 / k_stage2_big + k_npv_final),
+    bit-exact, for instances on the stage-2 fast path (one mode, one rock type, positive rate,
+    evaluate.py:149-150).  The multi-mode LP instances are refused here (InvalidArgs); the
+    installed factory `evaluator_for` gives them the reference's own class.
 
-    def _dev_init(self, instance, scenarios, sigma):
-        self._dev_args = (instance, scenarios, sigma)
+    The attributes callers read (`values`, `masses`, `costs`, `discount` -- hybrid.py:673-678,
+    saa.py:60-65 -- and len(`_stage2_cache`), runstore.py:453) are provided; `values` is built on
+    first use, not at construction."""
 
-    def _dev_entry(self):
-        instance, scenarios, sigma = self._dev_args
+    def __init__(self, instance, scenarios, sigma=None):
+        n_b = getattr(scenarios, "n_blocks", None)
+        if n_b is None and getattr(scenarios, "vmax", None) is not None:
+            n_b = np.asarray(scenarios.vmax).shape[1]
         e = _entry(instance)
+        if n_b is not None and int(n_b) != e.bm.n_blocks:
+            raise InvalidArgs("scenario set does not match instance block count")
         if not e.bm.single_mode_fast:
-            return None
-        _bind_scenarios(e, scenarios, sigma, None)
+            raise InvalidArgs("the device evaluator covers the single-mode stage-2 fast path only "
+                              "(evaluate.py:149-150); use the reference evaluator for the LP path")
+        self.instance = instance
+        self.scenarios = scenarios
+        self.sigma = sigma
+        self._values = None
+        self._stage2_cache = _Stage2Count()
+
+    # -- the reference's attributes ------------------------------------------------------
+    @property
+    def masses(self) -> np.ndarray:
+        return _entry(self.instance).bm.mass
+
+    @property
+    def costs(self) -> np.ndarray:
+        return _entry(self.instance).bm.cost
+
+    @property
+    def discount(self) -> np.ndarray:
+        return _entry(self.instance).bm.discount()
+
+    @property
+    def values(self) -> np.ndarray:
+        """v[s][b][o] (scenario_mode_values, evaluate.py:108-124); single mode: o = 0."""
+        if self._values is None:
+            e = self._entry()
+            self._values = e.engine.scenario_table()[:, :, None]
+        return self._values
+
+    def sigma_st(self, s: int, t: int) -> float:
+        return 1.0 if self.sigma is None else float(np.asarray(getattr(self.sigma, "sigma", self.sigma))[s, t])
+
+    def stage2_raw(self, s: int, t: int, blocks) -> float:
+        """Unadjusted optimal processing value of the mined set (evaluate.py:153-164, sigma = 1),
+        solved on the device (pp_stage2)."""
+        blocks = tuple(int(b) for b in blocks)
+        if not blocks:
+            return 0.0
+        e = self._entry()
+        a = np.full(e.bm.n_blocks, -1, dtype=np.int32)
+        a[list(blocks)] = t
+        raw, _ = e.engine.stage2(a[None, :])
+        self._stage2_cache.n += e.engine.n_scenarios
+        return float(raw[0, t, s])
+
+    _solve_stage2 = stage2_raw
+
+    # -- device --------------------------------------------------------------------------
+    def _entry(self) -> _Entry:
+        e = _entry(self.instance)
+        _bind_scenarios(e, self.scenarios, self.sigma, None)
         return e
 
-    def _dev_npv(self, schedule, per_scenario):
-        e = self._dev_entry()
-        if e is None:
-            return None
-        try:
-            r = e.engine.npv_relaxed(_assignment(schedule)[None, :], use_sigma=self._dev_args[2] is not None,
-                                     per_scenario=per_scenario)
-        except ShapeMismatch:  # a period above the on-chip stage-2 size: the reference's own path
-            if _reference_evaluator() is None:
-                raise
-            return None
-        return (float(r[0][0]), r[1][0]) if per_scenario else float(r[0])
+    def _npv(self, schedules, per_scenario):
+        e = self._entry()
+        a = _assignment(schedules)
+        r = e.engine.npv_relaxed(a if a.ndim == 2 else a[None, :], use_sigma=self.sigma is not None,
+                                 per_scenario=per_scenario)
+        self._stage2_cache.n += e.engine.n_scenarios * e.bm.n_periods * (a.shape[0] if a.ndim == 2 else 1)
+        return r
+
+    def npv_relaxed(self, schedule) -> float:
+        """Stage-1 + stage-2 value evaluated as-is, violations ignored (evaluate.py:244-246)."""
+        return float(self._npv(schedule, False)[0])
+
+    def npv_relaxed_batch(self, assignments) -> np.ndarray:
+        """npv_relaxed of a population [P][B] in one device call."""
+        return self._npv(np.atleast_2d(np.asarray(assignments)), False)
+
+    def per_scenario_npv(self, schedule) -> np.ndarray:
+        """evaluate.py:248-258."""
+        return self._npv(schedule, True)[1][0]
+
+    def objective(self, schedule) -> float:
+        """f(x) for a feasible schedule (evaluate.py:236-243)."""
+        report = check_feasible(self.instance, schedule)
+        if not report.feasible:
+            try:
+                from pitplan.errors import InfeasibleSchedule
+            except Exception:  # noqa: BLE001
+                InfeasibleSchedule = InvalidArgs  # noqa: N806
+            raise InfeasibleSchedule(
+                f"schedule has violation {report.violation:.6g}; use the relaxed evaluator")
+        return self.npv_relaxed(schedule)
 
 
-def _make_evaluator_class():
-    Ref = _reference_evaluator()
-    base = (Ref, _DeviceNpv) if Ref is not None else (_DeviceNpv,)
-
-    class ScheduleEvaluator(*base):
-        """Drop-in for pitplan.evaluate.ScheduleEvaluator (evaluate.py:126-258): npv_relaxed,
-        per_scenario_npv and objective run on the device (bit-exact) on the single-mode fast path;
-        everything else (and the LP path) is the reference's own code when it is installed."""
-
-        def __init__(self, instance, scenarios, sigma=None):
-            if Ref is not None:
-                Ref.__init__(self, instance, scenarios, sigma)
-            self._dev_init(instance, scenarios, sigma)
-
-        def npv_relaxed(self, schedule):
-            v = self._dev_npv(schedule, False)
-            if v is None:
-                if Ref is None:
-                    raise InvalidArgs("only the single-mode stage-2 fast path exists without the reference")
-                return Ref.npv_relaxed(self, schedule)
-            return v
-
-        def per_scenario_npv(self, schedule):
-            r = self._dev_npv(schedule, True)
-            if r is None:
-                if Ref is None:
-                    raise InvalidArgs("only the single-mode stage-2 fast path exists without the reference")
-                return Ref.per_scenario_npv(self, schedule)
-            return r[1]
-
-        def objective(self, schedule):
-            """f(x) for a feasible schedule (evaluate.py:236-243)."""
-            report = check_feasible(self._dev_args[0], schedule)
-            if not report.feasible:
-                try:
-                    from pitplan.errors import InfeasibleSchedule
-                except Exception:  # noqa: BLE001
-                    InfeasibleSchedule = InvalidArgs  # noqa: N806
-                raise InfeasibleSchedule(
-                    f"schedule has violation {report.violation:.6g}; use the relaxed evaluator")
-            return self.npv_relaxed(schedule)
-
-    return ScheduleEvaluator
-
-
-ScheduleEvaluator = _make_evaluator_class()
+def evaluator_for(instance, scenarios, sigma=None):
+    """What install() binds as `ScheduleEvaluator`: the device evaluator for fast-path instances;
+    for a multi-mode LP instance (out of scope) the reference's own class, counted and logged."""
+    if _entry(instance).bm.single_mode_fast:
+        return ScheduleEvaluator(instance, scenarios, sigma)
+    _to_reference("ScheduleEvaluator")
+    return _reference_fn("pitplan.evaluate", "ScheduleEvaluator")(instance, scenarios, sigma)
 
 
 def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swaps=None):
@@ -407,18 +518,20 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
 
     The single-block sweep evaluates all options of a block (other period, unmine) in one
     pp_npv_moves call, which re-solves only the two periods each option changes (bit-exact relaxed
-    NPV, so the `> best + 1e-9` decisions are the reference's); the small-instance swap / exchange / joint-insertion phases call the device
-    evaluator per candidate, in the reference's order.  Falls back to the reference's own
-    polish_schedule when the stage-2 fast path does not apply."""
+    NPV, so the `> best + 1e-9` decisions are the reference's); the small-instance swap / exchange /
+    joint-insertion phases call the device evaluator per candidate, in the reference's order.
+    Any evaluator object is accepted (its instance, scenarios and sigma are what count); a
+    multi-mode LP instance -- out of scope -- runs the reference's own polish_schedule (counted,
+    logged)."""
     e = _entry(instance)
     bm = e.bm
-    dev = isinstance(evaluator, _DeviceNpv) and evaluator._dev_entry() is not None
-    if not dev:
-        from pitplan.hybrid import polish_schedule as ref_polish
-
-        return ref_polish(instance, evaluator, schedule, max_sweeps, pair_swaps)
+    if not bm.single_mode_fast:
+        _to_reference("polish_schedule")
+        return _reference_fn("pitplan.hybrid", "polish_schedule")(instance, evaluator, schedule, max_sweeps,
+                                                                  pair_swaps)
+    _bind_scenarios(e, evaluator.scenarios, evaluator.sigma, None)
     eng = e.engine
-    use_sigma = evaluator._dev_args[2] is not None
+    use_sigma = evaluator.sigma is not None
     UN = -1
     masses = bm.mass
     cap = bm.capacity
@@ -432,12 +545,7 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
     def npv_of(batch):
         return eng.npv_relaxed(np.asarray(batch), use_sigma=use_sigma)
 
-    try:
-        cur_val = float(npv_of(a[None, :])[0])
-    except ShapeMismatch:  # a period above the on-chip stage-2 size
-        from pitplan.hybrid import polish_schedule as ref_polish
-
-        return ref_polish(instance, evaluator, schedule, max_sweeps, pair_swaps)
+    cur_val = float(npv_of(a[None, :])[0])
     load = np.zeros(T)
     for t in range(T):
         load[t] = masses[a == t].sum()
@@ -628,47 +736,62 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
 
 def price_column(instance, duals, scenarios, sigma, equipment, seed, evaluator=None, node_cap: int = 5000,
                  capacity_slack: float = 1.0, noise: float = 0.0):
-    """colgen.price_column (colgen.py:207-293): the dual-adjusted score matrix and its noise are
-    formed exactly as the reference does (its own `_enpv_adjusted` and `substream`), the
-    feasible-sequence greedy (colgen.py:236-254, one Python scan of every block per pick) runs
-    in `pp_price_greedy`, and the capacity-slack trim and the column's value / reduced cost
-    follow the reference line by line. Needs `pitplan` (the column type is the reference's)."""
-    from pitplan import colgen as _cg  # the reference module (its helpers are not rebound)
+    """colgen.price_column (colgen.py:207-293), same signature and column.
 
-    rng = _cg.substream(seed[0], *seed[1:]) if isinstance(seed, tuple) else _cg.substream(seed, "price")
-    enpv = _cg._enpv_adjusted(instance, scenarios, sigma)
-    masses = instance.masses()
-    n_t = instance.n_periods
+    * the risk-adjusted ENPV table `_enpv_adjusted` (colgen.py:187-204) is `pp_enpv_table` of the
+      column's scenario set (k_enpv_table, bit-identical);
+    * the noise stream is `substream(seed, ...)` (rng.py:23-32, restated in synth.substream; the
+      normal draws are numpy's own Generator, as in the reference);
+    * the feasible-sequence greedy (colgen.py:236-254, one scan of every block per pick) runs in
+      `pp_price_greedy`;
+    * the capacity-slack trim (colgen.py:256-268) walks this package's topological order
+      (synth.topological_order, blockmodel.py:228-245) and the column's value / reduced cost
+      follow colgen.py:270-293.
+    The returned column is the reference's `SequenceColumn` type when pitplan is importable."""
+    from .model import UNMINED as UN
+    from .synth import substream, topological_order
+
+    e = _entry(instance)
+    bm = e.bm
+    rng = substream(seed[0], *seed[1:]) if isinstance(seed, tuple) else substream(seed, "price")
+    _bind_scenarios(e, scenarios, sigma, None)
+    enpv = e.engine.enpv_table(use_sigma=sigma is not None, factored=False)
+    masses = bm.mass
+    n_t = bm.n_periods
     score = enpv - duals.block[:, None] - np.outer(masses, duals.capacity)
     if noise > 0:
         scale = max(float(np.abs(score).max()), 1e-9)
         score = score + rng.normal(0.0, noise * scale, size=score.shape)
-    cap = np.array([instance.mining_capacity[t] * capacity_slack for t in range(n_t)], dtype=np.float64)
-    a32, _ = _entry(instance).engine.price_greedy(score, cap, node_cap)
-    UN = _cg.UNMINED
+    cap_t = bm.capacity
+    cap = np.array([cap_t[t] * capacity_slack for t in range(n_t)], dtype=np.float64)
+    a32, _ = e.engine.price_greedy(score, cap, node_cap)
     assign = a32.astype(int)
     in_col = assign != UN
 
     # trim back to the hard capacity if the slack let the sequence overfill (colgen.py:256-268)
     if capacity_slack > 1.0:
+        pp_, pi_, sp_, si_ = bm.csr()
+        topo = None
         for t in range(n_t):
             load = float(masses[assign == t].sum())
-            if load <= instance.mining_capacity[t]:
+            if load <= cap_t[t]:
                 continue
-            for b in reversed(instance.topological_order()):
+            if topo is None:
+                topo = topological_order(bm)
+            for b in topo[::-1].tolist():
                 if assign[b] != t:
                     continue
-                if all(assign[c] == UN for c in instance.successors(b)):
+                if np.all(assign[si_[sp_[b]:sp_[b + 1]]] == UN):
                     assign[b] = UN
                     in_col[b] = False
                     load -= masses[b]
-                if load <= instance.mining_capacity[t]:
+                if load <= cap_t[t]:
                     break
 
     if not in_col.any():
         return None, float("inf")
     mass_t = np.array([float(masses[assign == t].sum()) for t in range(n_t)])
-    column = _cg.SequenceColumn(id=-1, equipment=equipment, assignment=assign, mass_per_period=mass_t, value=0.0)
+    column = _sequence_column(equipment, assign, mass_t)
     if evaluator is not None:
         column.value = evaluator.npv_relaxed(column.schedule())
     else:
@@ -679,6 +802,15 @@ def price_column(instance, duals, scenarios, sigma, equipment, seed, evaluator=N
     charge += float(duals.convexity[equipment])
     column.reduced_cost = column.value - charge
     return column, column.reduced_cost
+
+
+def _sequence_column(equipment, assign, mass_t):
+    """A colgen.SequenceColumn (colgen.py:60-80) -- the reference's record type when importable."""
+    try:
+        from pitplan.colgen import SequenceColumn
+    except Exception:  # noqa: BLE001
+        from .model import SequenceColumn
+    return SequenceColumn(id=-1, equipment=equipment, assignment=assign, mass_per_period=mass_t, value=0.0)
 
 
 def clear_cache() -> None:

@@ -16,18 +16,8 @@ import importlib
 from . import evaluate as _ev
 
 
-def _evaluator_class():
-    """The ScheduleEvaluator drop-in, subclassing the reference's own class: rebuilt here when
-    this package was imported before `pitplan` became importable (the class built at import
-    then lacks the reference's attributes, e.g. `values`, hybrid.py:673)."""
-    Ref = _ev._reference_evaluator()
-    if Ref is not None and not issubclass(_ev.ScheduleEvaluator, Ref):
-        _ev.ScheduleEvaluator = _ev._make_evaluator_class()
-    return _ev.ScheduleEvaluator
-
-
 def _patches():
-    E = _evaluator_class()
+    E = _ev.evaluator_for  # device evaluator; the reference class for out-of-scope LP instances
     return {
         "pitplan.evaluate": {
             "evaluate_candidates_parallel": _ev.evaluate_candidates_parallel,
@@ -50,6 +40,12 @@ def _patches():
 
 
 _saved: list[tuple[object, str, object]] = []
+_originals: dict[tuple[str, str], object] = {}
+
+
+def original(module: str, name: str):
+    """The reference's own `module.name` as it was before the first install(), or None."""
+    return _originals.get((module, name))
 
 
 def install() -> list[str]:
@@ -62,7 +58,9 @@ def install() -> list[str]:
             continue
         for name, fn in names.items():
             if hasattr(mod, name):
-                _saved.append((mod, name, getattr(mod, name)))
+                cur = getattr(mod, name)
+                _saved.append((mod, name, cur))
+                _originals.setdefault((modname, name), cur)
                 setattr(mod, name, fn)
                 done.append(f"{modname}.{name}")
     return done

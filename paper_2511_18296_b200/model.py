@@ -265,6 +265,24 @@ class ScenarioTables:
         return cls(vmax=vmax, sigma=sig, grades=getattr(scenarios, "grades", None))
 
 
+@dataclass
+class SequenceColumn:
+    """A column of the Dantzig-Wolfe master (colgen.py:71-95), used when pitplan is absent."""
+
+    id: int
+    equipment: int
+    assignment: np.ndarray
+    mass_per_period: np.ndarray
+    value: float
+    reduced_cost: float = float("nan")
+    birth: int = 0
+    last_used: int = 0
+    quality: float = 0.0
+
+    def schedule(self) -> "Schedule":
+        return Schedule(self.assignment.copy())
+
+
 def cvar_k(n_scenarios: int) -> int:
     """ceil(0.1 n) lowest samples enter CVaR10 (saa.py:157)."""
     import math

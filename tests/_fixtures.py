@@ -79,10 +79,16 @@ def config(name: str):
 
 
 def same(a, b) -> bool:
-    """Bit-level equality for float arrays (NaN == NaN, -inf == -inf; -0.0 == 0.0)."""
+    """Bit-level equality of float arrays: identical bit patterns (so -0.0 != +0.0), any NaN equal
+    to any NaN; plain equality for integer arrays."""
     a, b = np.asarray(a), np.asarray(b)
     if a.shape != b.shape:
         return False
+    if a.dtype != b.dtype and a.dtype.kind == b.dtype.kind == "f":  # widen exactly (f32 -> f64)
+        wide = a.dtype if a.dtype.itemsize >= b.dtype.itemsize else b.dtype
+        a, b = a.astype(wide), b.astype(wide)
     if a.dtype.kind == "f":
-        return bool(np.all((a == b) | (np.isnan(a) & np.isnan(b))))
+        ui = {2: np.uint16, 4: np.uint32, 8: np.uint64}[a.dtype.itemsize]
+        bits = np.ascontiguousarray(a).view(ui) == np.ascontiguousarray(b).view(ui)
+        return bool(np.all(bits | (np.isnan(a) & np.isnan(b))))
     return bool(np.array_equal(a, b))

@@ -429,13 +429,104 @@ def price_cases(store):
         store[p + "rc"] = np.float64(rc)
 
 
+def stats_cases(store):
+    """Per-scenario statistics with CVaR10 over k > 1 scenarios, from the reference kernel itself
+    (run once per scenario with s=k) and saa.risk_metrics: a C2 subset (S = 20, k = 2) and a C3
+    subset (S = 200, k = 20: the many-scenario warp-selection path).  Inputs are rebuilt by the
+    package's synth module and checked against the digests stored here."""
+    for name, cf, S, n_sub in (("C2", 1.3, 20, 300), ("C3", 0.3, 200, 60)):
+        inst = generate_synthetic(50000, (50, 50, 20), 15, 1, seed=1, n_rock_types=1, capacity_factor=cf)
+        scen = sample_lognormal(inst, S, 0.3, seed=2)
+        sigma = uncertainty_factors(inst, scen.grades)
+        cand = substream(3, "cand").integers(0, 50000, size=16667).astype(np.int32)
+        p = f"{name}_"
+        f = flat(inst, "")
+        store[p + "digest_instance"] = np.bytes_(digest(f["edges"].astype(np.int32), f["mass"], f["cost"],
+                                                        f["capacity"], f["coords"], f["features"]))
+        store[p + "digest_vmax"] = np.bytes_(digest(vmax_of(inst, scen)))
+        store[p + "sigma"] = sigma.sigma
+        full = full_greedy(inst)
+        store[p + "digest_assign"] = np.bytes_(digest(full.astype(np.int32)))
+        # the subset: candidates with at least one precedence-feasible period, so the statistics
+        # are exercised (a random draw is mostly unplaceable in a fully mined schedule)
+        sub = cand[:n_sub].tolist()
+        store[p + "sub"] = np.array(sub, dtype=np.int32)
+        sd, ex, cv = scenario_stats(inst, Schedule(full), sub, scen, sigma, net=True)
+        store[p + "sub_scen_delta"], store[p + "sub_exp"], store[p + "sub_cvar"] = sd, ex, cv
+        print(name, "feasible moves in subset:", int(np.isfinite(ex).sum()), file=sys.stderr)
+
+
+class _RecordingEvaluator:
+    """Wraps a reference ScheduleEvaluator for polish_schedule: returns the base value for the
+    unmodified schedule and -inf for every option, so no move is ever accepted and one sweep
+    visits every block's option list against the same schedule; records each option as the
+    difference between the evaluated assignment and the base (hybrid.py:357-403)."""
+
+    def __init__(self, base):
+        self.base = np.asarray(base).copy()
+        self.reassign, self.swap, self.other = [], [], []
+
+    def npv_relaxed(self, sched):
+        a = np.asarray(sched.assignment)
+        d = np.nonzero(a != self.base)[0]
+        if d.size == 0:
+            return 0.0
+        if d.size == 1:
+            self.reassign.append((int(d[0]), int(a[d[0]])))
+        elif (d.size == 2 and a[d[0]] == self.base[d[1]] and a[d[1]] == self.base[d[0]]
+              and self.base[d[0]] != UNMINED and self.base[d[1]] != UNMINED):  # not a 1-1 exchange
+            self.swap.append((int(d[0]), int(d[1])))
+        else:
+            self.other.append(tuple(int(x) for x in d))
+        return -np.inf
+
+
+def move_cases(store):
+    """The reference's own move generation of polish_schedule (hybrid.py:348-403): for a fixed
+    schedule, every reassign / unmine option (window + capacity) and every feasible pair swap it
+    evaluates, recorded through _RecordingEvaluator.  Pins pp_eval_moves' feasibility rules."""
+    for name, n, dims, T, S, cf in (("m27", 27, (3, 3, 3), 3, 2, 0.9), ("m32", 32, (4, 4, 2), 4, 3, 0.7),
+                                    ("m512", 512, (8, 8, 8), 6, 4, 0.9), ("mC1", 4000, (20, 20, 10), 10, 10, 1.3)):
+        inst = generate_synthetic(n, dims, T, 1, seed=170 + n, n_rock_types=1, capacity_factor=cf)
+        scen = sample_lognormal(inst, S, 0.3, seed=171 + n)
+        sigma = uncertainty_factors(inst, scen.grades)
+        p = f"{name}_"
+        store.update(flat(inst, p))
+        store[p + "vmax"] = vmax_of(inst, scen)
+        store[p + "sigma"] = sigma.sigma
+        scheds = [greedy_initialize(inst, scen, sigma).assignment.copy(), full_greedy(inst)]
+        rng = np.random.default_rng(n + 1)
+        a = scheds[1].copy()
+        a[rng.random(n) < 0.25] = UNMINED
+        _precedence_repair_pass(inst, a)
+        scheds.append(a)
+        for k, base in enumerate(scheds):
+            rec = _RecordingEvaluator(base)
+            polish_schedule(inst, rec, Schedule(base.copy()), max_sweeps=1, pair_swaps=n <= 32)
+            q = f"{p}{k}_"
+            store[q + "assign"] = base.astype(np.int32)
+            store[q + "reassign"] = np.array(rec.reassign, dtype=np.int32).reshape(-1, 2)
+            store[q + "swap"] = np.array(rec.swap, dtype=np.int32).reshape(-1, 2)
+            print(name, k, len(rec.reassign), len(rec.swap), len(rec.other), file=sys.stderr)
+
+
 def main():
+    if sys.argv[1:] == ["stats"]:  # the k > 1 statistics fixture only
+        store: dict = {"numpy_version": np.bytes_(np.__version__)}
+        stats_cases(store)
+        np.savez_compressed(os.path.join(OUT, "stats.npz"), **store)
+        return
+    if sys.argv[1:] == ["moves"]:  # the polish move-generation fixture only
+        store = {"numpy_version": np.bytes_(np.__version__)}
+        move_cases(store)
+        np.savez_compressed(os.path.join(OUT, "moves.npz"), **store)
+        return
     if sys.argv[1:] == ["price"]:  # regenerate only the pricing fixture
         store: dict = {"numpy_version": np.bytes_(np.__version__)}
         price_cases(store)
         np.savez_compressed(os.path.join(OUT, "price.npz"), **store)
         return
-    store: dict = {}
+    store = {}
     small_cases(store)
     hand_cases(store)
     polish_cases(store)

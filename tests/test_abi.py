@@ -83,8 +83,9 @@ def test_header_abi_version_and_struct_layouts_match_ctypes():
 
 def test_install_rebinds_reference_names_on_cpu():
     """install.py rebinds every reference entry point (hybrid.py:22-28 binds by value) and
-    uninstall restores them; the ScheduleEvaluator drop-in subclasses the reference's class even
-    when this package was imported before the reference became importable.  No compute runs."""
+    uninstall restores them; `ScheduleEvaluator` becomes the evaluator factory and the
+    reference's own objects stay reachable through install.original (the LP-instance path and
+    polish_schedule's: no self-recursion after install).  No compute runs."""
     import os
     import sys
 
@@ -104,8 +105,13 @@ def test_install_rebinds_reference_names_on_cpu():
     try:
         assert PH.evaluate_candidates_parallel is ev.evaluate_candidates_parallel
         assert PH.polish_schedule is ev.polish_schedule
-        assert issubclass(PH.ScheduleEvaluator, orig[2]) and PH.ScheduleEvaluator is not orig[2]
+        assert PH.ScheduleEvaluator is ev.evaluator_for and PE.ScheduleEvaluator is ev.evaluator_for
         assert "pitplan.hybrid.lns_repair" in done and "pitplan.colgen.price_column" in done
+        from paper_2511_18296_b200.install import original
+
+        assert original("pitplan.hybrid", "polish_schedule") is orig[1]
+        assert ev._reference_fn("pitplan.hybrid", "polish_schedule") is orig[1]
+        assert original("pitplan.evaluate", "ScheduleEvaluator") is orig[2]
     finally:
         uninstall()
     assert (PH.evaluate_candidates_parallel, PH.polish_schedule, PE.ScheduleEvaluator) == orig

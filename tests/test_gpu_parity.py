@@ -748,3 +748,56 @@ def test_npv_relaxed_c4_against_oracle(oracle_lib):
     v, pr = o.npv_relaxed(c["assign"], bm.plant_hours, bm.mode_rates[0])
     assert npv[0] == v and same(ps[0], pr)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ["m27", "m32", "m512", "mC1"])
+def test_explicit_moves_match_reference_polish_options(name):
+    """pp_eval_moves' feasibility against the reference's own move generation: the reassign /
+    unmine options and the pair swaps polish_schedule evaluates for a fixed schedule
+    (hybrid.py:348-403, recorded by tests/golden/make_golden.py move_cases) are exactly the
+    moves the engine reports feasible."""
+    st = load("moves")
+    p = f"{name}_"
+    bm = bm_from(st, p)
+    eng = Engine.from_tables(bm, tables_from(st, p))
+    B, T = bm.n_blocks, bm.n_periods
+    for k in range(3):
+        q = f"{p}{k}_"
+        eng.set_schedule(st[q + "assign"])
+        bb = np.repeat(np.arange(B), T + 1).astype(np.int32)
+        tt = np.tile(np.arange(-1, T), B).astype(np.int32)
+        r = eng.eval_moves(bb, tt, "reassign", net=True)
+        f = r["feasible"] == 1
+        assert set(zip(bb[f].tolist(), tt[f].tolist())) == set(map(tuple, st[q + "reassign"].tolist())), k
+        assert np.all(np.isfinite(r["delta"][f])) and np.all(r["delta"][~f] == -np.inf)
+        if B <= 32:
+            i, j = np.triu_indices(B, 1)
+            r = eng.eval_moves(i.astype(np.int32), j.astype(np.int32), "swap", net=True)
+            f = r["feasible"] == 1
+            assert set(zip(i[f].tolist(), j[f].tolist())) == set(map(tuple, st[q + "swap"].tolist())), k
+    eng.close()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_scenario_stats_cvar_k_gt_1_match_reference(name):
+    """Expected delta and CVaR10 over k > 1 scenarios (C2: S = 20, k = 2; C3: S = 200, k = 20, the
+    warp-per-move selection path) and the per-scenario deltas, against the reference kernel run
+    once per scenario plus saa.risk_metrics (tests/golden/make_golden.py stats_cases)."""
+    from tests._fixtures import digest, instance_digest
+
+    st = load("stats")
+    c = config(name)
+    assert instance_digest(c["bm"]) == st[f"{name}_digest_instance"].item().decode()
+    assert digest(c["vmax"]) == st[f"{name}_digest_vmax"].item().decode()
+    assert digest(c["assign"].astype(np.int32)) == st[f"{name}_digest_assign"].item().decode()
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], st[f"{name}_sigma"]), c["assign"])
+    sub = st[f"{name}_sub"]
+    got = eng.eval_candidates(sub, None, net=True, stats=True, scen=True)
+    assert same(got["exp_delta"], st[f"{name}_sub_exp"])
+    assert same(got["cvar"], st[f"{name}_sub_cvar"])
+    assert same(got["scen_delta"], st[f"{name}_sub_scen_delta"])
+    pr = eng.eval_candidates(sub, None, net=True, pairs=True)["pairs"]
+    ex = st[f"{name}_sub_exp"]
+    assert pr["cand"].size == int(np.isfinite(ex).sum())
+    assert same(pr["exp"], ex[pr["cand"], pr["period"]]) and same(pr["cvar"], st[f"{name}_sub_cvar"][pr["cand"], pr["period"]])
+    eng.close()
