@@ -141,6 +141,30 @@ struct TopK {
 #pragma unroll
         for (int j = 0; j < KC; j++) a[j] = kInf;
     }
+    // merge with the list of lane (lane ^ m): both lanes end with the KC smallest of the union,
+    // ascending (values are only compared and moved, never combined)
+    __device__ __forceinline__ void merge_xor(int m) {
+        double o[KC];
+#pragma unroll
+        for (int j = 0; j < KC; j++) o[j] = __shfl_xor_sync(0xffffffffu, a[j], m);
+        double r[KC];
+        int ia = 0, ib = 0;
+#pragma unroll
+        for (int j = 0; j < KC; j++) {
+            double x = a[0], y = o[0];
+#pragma unroll
+            for (int u = 0; u < KC; u++) {
+                if (u == ia) x = a[u];
+                if (u == ib) y = o[u];
+            }
+            const bool ta = !(y < x);
+            r[j] = ta ? x : y;
+            ia += ta ? 1 : 0;
+            ib += ta ? 0 : 1;
+        }
+#pragma unroll
+        for (int j = 0; j < KC; j++) a[j] = r[j];
+    }
     __device__ __forceinline__ void push(double x) {
         if (x < a[KC - 1]) {
             if constexpr (KC <= 8) {
@@ -183,6 +207,15 @@ template <>
 struct TopK<2> {  // k <= 2 (S <= 20): two registers, branch-free (lanes hold different moves)
     double a0, a1;
     __device__ __forceinline__ void init() { a0 = a1 = kInf; }
+    __device__ __forceinline__ void merge_xor(int m) {
+        const double b0 = __shfl_xor_sync(0xffffffffu, a0, m), b1 = __shfl_xor_sync(0xffffffffu, a1, m);
+        // two smallest of {a0 <= a1} u {b0 <= b1}, ascending
+        const bool ta = !(b0 < a0);
+        const double lo = ta ? a0 : b0;
+        const double n1 = ta ? a1 : a0, n2 = ta ? b0 : b1;  // the candidates for second place
+        a0 = lo;
+        a1 = (n2 < n1) ? n2 : n1;
+    }
     __device__ __forceinline__ void push(double x) {
         // the same selections as "if (x < a1) { if (x < a0) { a1 = a0; a0 = x; } else a1 = x; }"
         const bool lt0 = x < a0;
@@ -200,6 +233,7 @@ struct TopK<2> {  // k <= 2 (S <= 20): two registers, branch-free (lanes hold di
 template <>
 struct TopK<0> {
     __device__ __forceinline__ void init() {}
+    __device__ __forceinline__ void merge_xor(int) {}
     __device__ __forceinline__ void push(double) {}
     __device__ __forceinline__ double mean(int) const { return 0.0; }
 };

@@ -1045,24 +1045,37 @@ int check_schedule_range(pp_ctx *c, bool copied) {
     return PP_OK;
 }
 
-int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st) {
-    if (init.n_pairs) CUDA_TRY(cudaMemsetAsync(init.n_pairs, 0, sizeof(int32_t), st));
-    if (init.bad_cand) CUDA_TRY(cudaMemsetAsync(init.bad_cand, 0, sizeof(int32_t), st));
-    if (init.best) {
-        if (!c->best_none.ptr) {
-            TRY(c->best_none.ensure(sizeof(pp_best)));
-            const pp_best none{-std::numeric_limits<double>::infinity(), -1, -1};
-            CUDA_TRY(dev_upload(c, c->best_none.ptr, &none, sizeof(pp_best)));
-        }
-        CUDA_TRY(cudaMemcpyAsync(init.best, c->best_none.ptr, sizeof(pp_best), cudaMemcpyDeviceToDevice, st));
+// the per-launch output state of an evaluation when no period-mass kernel precedes it: one tiny
+// kernel (graph-capturable, no host staging) instead of memsets and a copy
+__global__ void k_init_eval(int32_t *n_pairs, int32_t *bad_cand, pp_best *best) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (threadIdx.x != 0) return;
+    if (n_pairs) *n_pairs = 0;
+    if (bad_cand) *bad_cand = 0;
+    if (best) {
+        best->value = -kInf;
+        best->block = -1;
+        best->period = -1;
     }
+}
+
+int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st) {
+    (void)c;
+    if (!init.n_pairs && !init.bad_cand && !init.best) return PP_OK;
+    k_init_eval<<<1, 32, 0, st>>>(init.n_pairs, init.bad_cand, init.best);
+    CUDA_TRY(cudaGetLastError());
     return PP_OK;
 }
 
 int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init) {
     *launched = false;
     if (!c->pm_dirty) {
-        if (init) TRY(init_eval_outputs(c, *init, st));
+        if (init) {
+            TRY(init_eval_outputs(c, *init, st));
+            // the evaluation may start under PDL: it touches the initialised state only after its
+            // griddepcontrol.wait -- except the host-mode bad-candidate flag (set before the wait)
+            *launched = !init->bad_cand && (init->n_pairs || init->best);
+        }
         return PP_OK;
     }
     TRY(run_period_mass(c, c->assign_ptr, 1, c->pm.as<double>(), st, init));
