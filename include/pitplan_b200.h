@@ -247,6 +247,18 @@ PP_API int pp_reduce_best(pp_ctx *ctx, const pp_best *records, int32_t n, pp_bes
  *               saa.py:65-69); sig = ones unless PP_USE_SIGMA. */
 PP_API int pp_enpv_table(pp_ctx *ctx, uint32_t flags, int32_t factored, double *out, int32_t mem,
                          void *stream);
+/* ---- host-native GA helpers (no device work, no context) -------------------------------- */
+/* HybridSearch._mutate (hybrid.py:692-714) on assign[n_blocks] (int64, in place) over blocks[n_sel],
+ * drawing from a numpy Generator(PCG64) stream supplied as raw 64-bit outputs raw[n_raw] plus the
+ * bit generator's uint32 buffer (*has_u32, *uinteger; updated).  *consumed receives the number of raw
+ * outputs used, so the caller can leave its Generator exactly where the reference's loop would.
+ * CSR adjacency pred_ptr/pred_idx, succ_ptr/succ_idx as BlockModel.csr().  PP_ERR_SHAPE (assign
+ * untouched) when raw runs out: retry with a longer block. */
+PP_API int pp_host_mutate(int64_t *assign, int32_t n_blocks, const int64_t *blocks, int64_t n_sel,
+                          const int32_t *pred_ptr, const int32_t *pred_idx, const int32_t *succ_ptr,
+                          const int32_t *succ_idx, int32_t n_periods, double rate, const uint64_t *raw,
+                          int64_t n_raw, int32_t *has_u32, uint32_t *uinteger, int64_t *consumed);
+
 /* Topological level of every block (longest predecessor chain), host output. */
 PP_API int pp_get_levels(pp_ctx *ctx, int32_t *n_levels, int32_t *level_of_block);
 

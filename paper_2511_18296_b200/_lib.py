@@ -109,6 +109,8 @@ SIGNATURES = {
     "pp_enpv_table": (c_int32, [c_void_p, c_uint32, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_get_levels": (c_int32, [c_void_p, ctypes.POINTER(c_int32), c_void_p]),
     "pp_price_greedy": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "pp_host_mutate": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_int32, c_double, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
 }
 
 # entry points that launch device work: every call through the default handle is counted, so

@@ -14,6 +14,7 @@ from __future__ import annotations
 import importlib
 
 from . import evaluate as _ev
+from . import hybrid_batch as _hb
 
 
 def _patches():
@@ -36,6 +37,8 @@ def _patches():
                            "ScheduleEvaluator": E, "price_column": _ev.price_column},
         "pitplan.saa": {},
         "pitplan": {"check_feasible": _ev.check_feasible},
+        # the GA generation of the unchanged HybridSearch class: batched fitness, native mutation
+        "pitplan.hybrid:HybridSearch": {"_member": _hb.member, "_measure": _hb.measure, "_mutate": _hb.mutate},
     }
 
 
@@ -48,21 +51,38 @@ def original(module: str, name: str):
     return _originals.get((module, name))
 
 
+def original_attr(target: str, name: str):
+    """The reference's own attribute `name` of `module:Class` / `module.Class` before install()."""
+    key = target.replace(":", ".") if ":" in target else target
+    fn = _originals.get((key, name)) or _originals.get((target, name))
+    if fn is None:  # never installed: the class's current attribute is the reference's
+        mod, _, cls = (target.replace(":", ".")).rpartition(".")
+        fn = getattr(getattr(importlib.import_module(mod), cls), name)
+    return fn
+
+
+def _resolve(target: str):
+    if ":" in target:
+        mod, cls = target.split(":", 1)
+        return getattr(importlib.import_module(mod), cls)
+    return importlib.import_module(target)
+
+
 def install() -> list[str]:
     """Rebind the reference entry points; returns the patched 'module.name' list."""
     done = []
     for modname, names in _patches().items():
         try:
-            mod = importlib.import_module(modname)
-        except ImportError:
+            mod = _resolve(modname)
+        except (ImportError, AttributeError):
             continue
         for name, fn in names.items():
             if hasattr(mod, name):
                 cur = getattr(mod, name)
                 _saved.append((mod, name, cur))
-                _originals.setdefault((modname, name), cur)
+                _originals.setdefault((modname.replace(":", "."), name), cur)
                 setattr(mod, name, fn)
-                done.append(f"{modname}.{name}")
+                done.append(f"{modname.replace(':', '.')}.{name}")
     return done
 
 
