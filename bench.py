@@ -111,13 +111,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_inputs(config: str, rank: int = 0):
+STRONG = ("C4",)  # C4: one 1M-move list split over the GPUs; the others: C candidates per GPU
+
+
+def build_inputs(config: str, rank: int = 0, world: int = 1):
+    """The config's inputs plus this rank's shard of ONE global candidate list:
+    weak scaling (C1-C3) draws world x C candidates from the config's stream and gives rank r the
+    contiguous range [r C, (r+1) C) -- at world = 1 exactly the config's list; strong scaling (C4)
+    splits the config's list into contiguous balanced shards."""
     from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.distributed import shard_bounds
     from paper_2511_18296_b200.model import ScenarioTables, scenario_values
 
     c = synth.build_config(config)
-    if rank:
-        c["cand"] = synth.candidate_blocks(c["bm"].n_blocks, c["C"], seed=3 + rank)
+    if config in STRONG:
+        c["cand_global"] = c["cand"]
+    else:
+        c["cand_global"] = c["cand"] if world == 1 else synth.candidate_blocks(c["bm"].n_blocks, c["C"] * world)
+    lo, hi = shard_bounds(c["cand_global"].size, world, rank)
+    c["cand"] = np.ascontiguousarray(c["cand_global"][lo:hi])
+    c["C"] = int(c["cand"].size)
     c["tables"] = ScenarioTables(scenario_values(c["bm"], c["grades"]), c["sigma"])
     return c
 
@@ -218,12 +231,18 @@ def algorithmic_bytes(c, deg_mean: float, n_pairs: int) -> dict:
 def workload_config(args, c) -> dict:
     """The `config` object of both arms (identical, so the driver compares like with like)."""
     C, T, S = c["C"], c["T"], c["S"]
+    G = int(c["cand_global"].size)
     return {
         "workload": ("C2: 50k-block model (50x50x20), 15 periods, 20 lognormal scenarios with sigma, "
                      "16,667 candidate blocks x 15 periods = 250,005 moves per GPU per step, "
                      "net mining cost, per-move expected delta + CVaR10, argmax")
         if args.config == "C2" else args.config,
-        "blocks": c["bm"].n_blocks, "periods": T, "scenarios": S, "candidates": C, "moves_per_batch": C * T,
+        "blocks": c["bm"].n_blocks, "periods": T, "scenarios": S,
+        "candidates_global": G, "moves_global_per_step": G * T,
+        "candidates_per_gpu": C, "moves_per_gpu_per_step": C * T,
+        "sharding": ("one global candidate list, contiguous per-GPU ranges; "
+                     + ("strong scaling (fixed 1M-move list)" if args.config in STRONG
+                        else "weak scaling (C candidates per GPU)")),
         "l2": "256 MiB flush write between timed GPU steps",
     }
 
@@ -251,7 +270,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    c = build_inputs(args.config)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    c = build_inputs(args.config, 0, world)
+    cfg = workload_config(args, c)
+    c["cand"] = np.ascontiguousarray(c["cand_global"])  # the whole job's list, on the host cores
+    c["C"] = int(c["cand"].size)
     M, S = c["C"] * c["T"], c["S"]
     from oracle import oracle
 
@@ -282,8 +305,8 @@ def run_reference(args):
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "ms_per_250k_batch": t * 1e3 * (M / (n_c * c["T"])), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, c),
+        "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "cpu_baseline_reference": None if args.no_python_ref else python_reference_timing(args.config, c["cand"],
@@ -299,17 +322,42 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PP_BENCH_DIST") == "gloo" and torch.cuda.device_count() <= local:
+        local = 0  # the one-GPU functional check: every rank on device 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink/NVSwitch; PP_BENCH_DIST=gloo is a functional multi-rank check on one GPU
+        # (host-staged exchange, not a measurement)
+        backend = os.environ.get("PP_BENCH_DIST", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def all_gather_dev(dst, src):
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(dst, src)
+        else:
+            parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, src.cpu())
+            dst.copy_(torch.cat(parts))
+
+    def all_reduce_max(t):
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        return h
     from paper_2511_18296_b200.engine import Engine, PinnedPool
 
-    c = build_inputs(args.config, rank)
+    c = build_inputs(args.config, rank, world)
     bm, T, S, C = c["bm"], c["T"], c["S"], c["C"]
     M = C * T
+    M_global = c["cand_global"].size * T
     dev = torch.device("cuda", local)
     eng = Engine.from_tables(bm, c["tables"], c["assign"], device=local)
     deg_mean = 2.0 * bm.n_edges / bm.n_blocks
@@ -345,7 +393,7 @@ def run_gpu(args):
         eng.set_schedule_device(assign_d, stream=sptr, borrow=True)
         eng.eval_candidates_device(cand_d, out, None, net=True, stream=sptr)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out["global"])
+            all_gather_dev(gathered, out["global"])
             eng.reduce_best_device(gathered, final, stream=sptr)
 
     for _ in range(max(args.warmup, 3)):
@@ -394,8 +442,7 @@ def run_gpu(args):
     t_max = t_local
     if dist is not None:
         tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+        t_max = float(all_reduce_max(tt).item())
 
     # dominant kernel alone: k_eval_warp in its own CUDA graph (period masses refreshed beforehand,
     # so the captured call launches only the evaluation kernel and its output-init copy), timed
@@ -451,11 +498,11 @@ def run_gpu(args):
         eng.set_schedule(h_assign)
         r = eng.eval_candidates(h_cand, None, net=True, pairs=True, out=h_out, validate=False)
         if world > 1:
-            bv, bb, bt = r["best"] if r["best"] is not None else (-np.inf, -1, -1)
+            bb, bt, bv = r["best"] if r["best"] is not None else (-1, -1, -np.inf)  # (block, period, value)
             h_best[0] = bv
             h_best.view(np.int32)[2:4] = (bb, bt)
             d_best.copy_(h_best_t, non_blocking=True)
-            dist.all_gather_into_tensor(gathered, d_best)
+            all_gather_dev(gathered, d_best)
             eng.reduce_best_device(gathered, final, stream=sptr)
             h_best_t.copy_(final)  # synchronising D2H of the global best
         t1 = time.perf_counter()
@@ -464,8 +511,7 @@ def run_gpu(args):
     e2e_t = float(np.median(e2e))
     if dist is not None:
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
+        e2e_t = float(all_reduce_max(tt).item())
     h2d = h_assign.nbytes + h_cand.nbytes
     npairs = int(h_out["n_pairs"][0])
     d2h = (h_out["best_t"].nbytes + h_out["best_val"].nbytes + h_out["feasible"].nbytes + 16 + 4
@@ -475,6 +521,14 @@ def run_gpu(args):
     g = out["global"].cpu().numpy()
     gi = g.view(np.int32)
     assert (int(gi[2]), int(gi[3]), float(g[0])) == r["best"], "device/host paths disagree"
+    argmax_check = None
+    if world > 1:  # the all-gathered argmax of the shards == one GPU evaluating the whole global list
+        glob = (int(h_best.view(np.int32)[2]), int(h_best.view(np.int32)[3]), float(h_best[0]))
+        if rank == 0:
+            eng.set_schedule(c["assign"])
+            whole = eng.eval_candidates(np.ascontiguousarray(c["cand_global"], dtype=np.int32), None, net=True)["best"]
+            argmax_check = {"sharded": list(glob), "whole_list_on_rank0": list(whole), "equal": whole == glob}
+            assert whole == glob, ("sharded argmax differs from the whole-list evaluation", glob, whole)
     pool.close()
 
     result = None
@@ -490,7 +544,7 @@ def run_gpu(args):
         achieved_comp = ab["per_launch"] / ks / 1e9
         traffic, traffic_src = (args.ncu_traffic, "--ncu-traffic") if args.ncu_traffic is not None \
             else _ncu_traffic(args.config)
-        value = world * M * S / (t_max * 1e-3)
+        value = M_global * S / (t_max * 1e-3)
         n_prec = precedence_feasible_moves(c)
 
         cpu = None
@@ -514,11 +568,12 @@ def run_gpu(args):
             "ms_per_step": t_max,
             "ms_per_250k_batch": t_max * (250000.0 / M),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if args.config in STRONG else "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
             "config": workload_config(args, c),
+            "argmax_check": argmax_check,
             "cuda_graph": graph is not None,
             "roofline": {
                 "bound": "hbm",
@@ -545,7 +600,7 @@ def run_gpu(args):
             "scen_evals_nominal_per_step": M * S,
             "precedence_feasible_moves_per_step": n_prec,
             "scen_evals_performed_per_step": n_prec * S,
-            "e2e": {"value": world * M * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": M_global * S / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_t * 1e3,
                     "api": "Engine.set_schedule + Engine.eval_candidates (pp_set_schedule/pp_eval_candidates, "
                            "PP_MEM_HOST, pinned)" + (" + NCCL all-gather/reduce of the per-rank best" if world > 1 else ""),

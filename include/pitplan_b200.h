@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 2
+#define PP_ABI_VERSION 3
 
 /* status codes (mapped to pitplan.errors classes by the Python shim) */
 #define PP_OK 0
@@ -104,6 +104,11 @@ typedef struct pp_cand_out {
     double *pair_exp;     /* [<= C*T] */
     double *pair_cvar;    /* [<= C*T] */
     int32_t *n_pairs;     /* [1] */
+    /* Second selection key (may be NULL): the feasible candidate first in lns_repair's realism
+     * fallback order -- geological consistency spatial[b] descending, then block ascending
+     * (hybrid.py:256-263) -- as {value = spatial[b], block, period = its best period}; block = -1
+     * when no candidate is feasible.  16-byte aligned. */
+    pp_best *realism;
 } pp_cand_out;
 
 /* Outputs of pp_eval_moves; NULL members are not computed / written.

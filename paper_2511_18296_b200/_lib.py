@@ -17,7 +17,7 @@ from .errors import ExtensionMissing, raise_for_status
 LIB_NAME = "libpitplan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-ABI_VERSION = 2  # include/pitplan_b200.h PP_ABI_VERSION
+ABI_VERSION = 3  # include/pitplan_b200.h PP_ABI_VERSION
 PP_MEM_HOST = 0
 PP_MEM_DEVICE = 1
 PP_MEM_DEVICE_BORROW = 2
@@ -58,6 +58,7 @@ class PPCandOut(ctypes.Structure):
         ("pair_exp", c_void_p),
         ("pair_cvar", c_void_p),
         ("n_pairs", c_void_p),
+        ("realism", c_void_p),
     ]
 
 

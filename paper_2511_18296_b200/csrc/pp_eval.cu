@@ -679,6 +679,26 @@ extern "C" PP_API int pp_debug_eval_probe(unsigned long long *out) {
 
 
 // ------------------------------------------------------------------------------------
+// k_realism: lns_repair's realism-fallback choice (hybrid.py:256-263) on the device -- among
+// the feasible candidates (best period >= 0), the first by geological consistency descending,
+// then block ascending: the evaluate.py:404-409 total order with value = spatial[b], so the same
+// deterministic grid argmax (per-CTA partials, last CTA reduces) gives it.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_realism(const int32_t *__restrict__ cand, int C, int B,
+                                                 const int32_t *__restrict__ best_t, const BlockRow *__restrict__ rows,
+                                                 pp_best *partial, unsigned int *counter, pp_best *out) {
+    __shared__ Best s_red[8];
+    Best mine{-kInf, INT_MAX, INT_MAX};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
+        const int b = __ldg(cand + i), t = best_t[i];
+        if (b < 0 || b >= B || t < 0) continue;
+        const Best o{__ldg(&rows[b].spatial), b, t};
+        if (better(o, mine)) mine = o;
+    }
+    grid_argmax(mine, s_red, partial, counter, out);
+}
+
+// ------------------------------------------------------------------------------------
 // Host-mode copy-out: when every output array is page-locked (device-mapped under UVA), one
 // launch writes all of them straight into host memory with 16-byte stores, reading the sparse
 // pair count on the device -- instead of one cudaMemcpyAsync per array (each ~4 us of CPU) and
@@ -777,11 +797,12 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         TRY(c->h_o1.ensure(sizeof(int32_t) * Cs));
         TRY(c->h_o2.ensure(sizeof(double) * Cs));
         TRY(c->h_o3.ensure(Cs));
-        TRY(c->h_glob.ensure(sizeof(pp_best)));
+        TRY(c->h_glob.ensure(2 * sizeof(pp_best)));
         o.best_t = c->h_o1.as<int32_t>();
         o.best_val = c->h_o2.as<double>();
         o.feasible = c->h_o3.as<uint8_t>();
         o.global = c->h_glob.as<pp_best>();
+        if (out->realism) o.realism = c->h_glob.as<pp_best>() + 1;
         if (out->trace_val) { TRY(c->h_o4.ensure(sizeof(double) * CT)); o.trace_val = c->h_o4.as<double>(); }
         if (out->trace_feas) { TRY(c->h_o5.ensure(CT)); o.trace_feas = c->h_o5.as<uint8_t>(); }
         if (out->exp_delta) { TRY(c->h_o6.ensure(sizeof(double) * CT)); o.exp_delta = c->h_o6.as<double>(); }
@@ -883,6 +904,15 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
                                       ep));
     }
 copy_out:
+    if (o.realism) {  // second key over the per-candidate results just written (stream-ordered)
+        if (reinterpret_cast<uintptr_t>(o.realism) & 15u)
+            return fail(PP_ERR_INVALID_ARGS, "realism (pp_best) must be 16-byte aligned");
+        const int rgrid = std::max(1, std::min((C + 255) / 256, 148 * 4));
+        TRY(ensure_grid_scratch(c, rgrid));
+        k_realism<<<rgrid, 256, 0, st>>>(dcand, C, c->B, o.best_t, c->rows.as<BlockRow>(), c->partial.as<pp_best>(),
+                                         c->counter.as<unsigned int>() + 1, o.realism);
+        CUDA_TRY(cudaGetLastError());
+    }
     ht.mark("launch");
 
     if (mem == PP_MEM_HOST) {
@@ -920,6 +950,7 @@ copy_out:
                                             (unsigned long long)bytes, per_pair};
             };
             add(o.global, out->global, sizeof(pp_best), 0);
+            if (o.realism) add(o.realism, out->realism, sizeof(pp_best), 0);
             if (C > 0) {
                 add(o.best_t, out->best_t, sizeof(int32_t) * Cs, 0);
                 add(o.best_val, out->best_val, sizeof(double) * Cs, 0);
@@ -956,6 +987,7 @@ copy_out:
             }
         }
         CUDA_TRY(cudaMemcpyAsync(out->global, o.global, sizeof(pp_best), cudaMemcpyDeviceToHost, st));
+        if (o.realism) CUDA_TRY(cudaMemcpyAsync(out->realism, o.realism, sizeof(pp_best), cudaMemcpyDeviceToHost, st));
         if (C > 0) {
             CUDA_TRY(cudaMemcpyAsync(out->best_t, o.best_t, sizeof(int32_t) * Cs, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaMemcpyAsync(out->best_val, o.best_val, sizeof(double) * Cs, cudaMemcpyDeviceToHost, st));

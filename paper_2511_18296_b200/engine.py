@@ -184,13 +184,16 @@ class Engine:
 
     def eval_candidates(self, cand, scenario=None, *, net=False, literal=False, use_sigma=True,
                         trace=False, stats=False, scen=False, pairs=False, out: dict | None = None,
-                        validate: bool = True) -> dict:
+                        validate: bool = True, realism: bool = False) -> dict:
         """Host-buffer evaluation; returns numpy arrays (and `best` as a tuple or None).
         `out` may supply preallocated (e.g. pinned) host arrays for any output; page-locked
         arrays (PinnedPool) are written in place by one copy-out launch, and a repeated call
         with the same `out` arrays reuses the argument block (no per-call marshalling).
         pairs=True returns the statistics of the feasible moves only, as
         res["pairs"] = {"cand", "period", "exp", "cvar"} (unordered; capacity C*T).
+        realism=True adds res["realism"]: lns_repair's fallback choice (hybrid.py:256-263), the
+        feasible candidate with the highest geological consistency, lowest block on ties, as
+        (block, period, spatial) or None.
         Candidate ids are range-checked by pp_eval_candidates (`validate` is kept for
         compatibility)."""
         bm = self._need_bm()
@@ -204,7 +207,7 @@ class Engine:
         C, T, S = c.size, bm.n_periods, self.n_scenarios
         key = None
         if out:
-            key = (C, trace, stats, scen, pairs) + tuple(id(v) for v in out.values())
+            key = (C, trace, stats, scen, pairs, realism) + tuple(id(v) for v in out.values())
             hit = self._eval_cache
             if hit is not None and hit[0] == key:
                 _, _keep, res, pr, g, argblock = hit
@@ -232,12 +235,14 @@ class Engine:
                   "exp": out["pair_exp"] if "pair_exp" in out else np.empty(cap, np.float64),
                   "cvar": out["pair_cvar"] if "pair_cvar" in out else np.empty(cap, np.float64),
                   "n": out["n_pairs"] if "n_pairs" in out else np.zeros(1, np.int32)}
-        g = PPBest()
+        g = (PPBest * 2)()  # [0] global best, [1] realism key
         argblock = PPCandOut(
             ptr(res["best_t"]), ptr(res["best_val"]), ptr(res["feasible"]),
             ptr(res.get("trace_val")), ptr(res.get("trace_feas")), ptr(res.get("exp_delta")),
             ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g),
             *((ptr(pr["cand"]), ptr(pr["period"]), ptr(pr["exp"]), ptr(pr["cvar"]), ptr(pr["n"])) if pr else ()))
+        if realism:
+            argblock.realism = ctypes.addressof(g) + ctypes.sizeof(PPBest)
         if key is not None:  # the arrays are kept alive by the cache entry, so their ids stay valid
             self._eval_cache = (key, tuple(out.values()), res, pr, g, argblock)
         self._eval_call(c, C, scenario, net, literal, use_sigma, argblock)
@@ -250,9 +255,12 @@ class Engine:
                                           ctypes.byref(argblock), _lib.PP_MEM_HOST, None))
 
     @staticmethod
-    def _eval_result(res, pr, g):
+    def _eval_result(res, pr, gg):
         res = dict(res)
+        g = gg[0]
         res["best"] = None if g.block < 0 else (int(g.block), int(g.period), float(g.value))
+        r = gg[1]
+        res["realism"] = None if r.block < 0 else (int(r.block), int(r.period), float(r.value))
         if pr is not None:
             n = int(pr["n"][0])
             res["pairs"] = {k: pr[k][:n] for k in ("cand", "period", "exp", "cvar")}
@@ -269,7 +277,7 @@ class Engine:
             ptr(out.get("trace_val")), ptr(out.get("trace_feas")), ptr(out.get("exp_delta")),
             ptr(out.get("cvar")), ptr(out.get("scen_delta")), ptr(out["global"]),
             ptr(out.get("pair_cand")), ptr(out.get("pair_period")), ptr(out.get("pair_exp")),
-            ptr(out.get("pair_cvar")), ptr(out.get("n_pairs")))
+            ptr(out.get("pair_cvar")), ptr(out.get("n_pairs")), ptr(out.get("realism")))
         sc = _lib.PP_SCENARIO_EXPECTED if scenario is None else int(scenario)
         check(self.lib.pp_eval_candidates(self._h, ptr(cand), int(cand.numel()), sc,
                                           self.flags(net, literal, use_sigma), ctypes.byref(o),

@@ -321,8 +321,9 @@ def lns_repair(
     Destroy (hybrid.py:199-235): the unmine fixpoint and the over-capacity ejection run on the
     device (pp_repair + pp_eject, bit-exact period masses).  Repair (238-263): the geological
     consistency of every block comes from the device (pp_get_spatial) instead of 50k Python
-    calls; each insertion round evaluates its candidates with the device kernel; the ranking
-    by scheduled-neighbour similarity and the realism fallback are the reference's own code.
+    calls; each insertion round evaluates its candidates with the device kernel, which also
+    selects both keys -- the best move and the realism fallback's (k_realism); the ranking by
+    scheduled-neighbour similarity is vectorised on the host.
     The reference's helpers are restated in model.py (rook_neighbor_map,
     scheduled_neighbor_similarity), so pitplan is not required."""
     from .errors import RepairStalled
@@ -360,21 +361,21 @@ def lns_repair(
             sims = scheduled_neighbor_similarity(sched.assignment, pool, mean_grade, rook)
             ranked = sorted(pool, key=lambda b: (-sims[b], b))
             cand = ranked[:candidate_width]
-        moves, best = evaluate_candidates_parallel(
-            instance, sched, cand, scenarios, None, sigma,
-            net_mining_cost=net_mining_cost, params=params,
-        )
-        if best is None or (only_positive and best.improvement <= 0.0):
+        e.engine.set_schedule(sched.assignment)
+        res = e.engine.eval_candidates(np.asarray(cand, dtype=np.int32), None, net=net_mining_cost,
+                                       use_sigma=sigma is not None, realism=True)
+        best = res["best"]  # (block, period, improvement) in evaluate.py:404-421 order
+        if best is None or (only_positive and best[2] <= 0.0):
             stalled = best is None
             break
         chosen = best
-        if spatial[best.block] < realism_threshold:
-            feasible = [m for m in moves if m.feasible]
-            feasible.sort(key=lambda m: (-spatial[m.block], m.block))
-            chosen = feasible[0]
-        sched.assignment[chosen.block] = chosen.period
-        pool.discard(chosen.block)
-        in_pool[chosen.block] = False
+        if spatial[best[0]] < realism_threshold:
+            # the realism fallback (hybrid.py:256-263): the feasible candidate of highest
+            # geological consistency, lowest block on ties -- selected on the device
+            chosen = res["realism"]
+        sched.assignment[chosen[0]] = chosen[1]
+        pool.discard(chosen[0])
+        in_pool[chosen[0]] = False
         iters += 1
 
     after = check_feasible(instance, sched)

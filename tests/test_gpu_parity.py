@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2511_18296_b200.engine import Engine
-from paper_2511_18296_b200.model import ScenarioTables
+from paper_2511_18296_b200.model import BlockModel, ScenarioTables
 from tests._fixtures import bm_from, config, load, same, tables_from
 
 pytestmark = pytest.mark.gpu
@@ -800,4 +800,56 @@ def test_scenario_stats_cvar_k_gt_1_match_reference(name):
     ex = st[f"{name}_sub_exp"]
     assert pr["cand"].size == int(np.isfinite(ex).sum())
     assert same(pr["exp"], ex[pr["cand"], pr["period"]]) and same(pr["cvar"], st[f"{name}_sub_cvar"][pr["cand"], pr["period"]])
+    eng.close()
+
+
+def _realism_ref(cand, best_t, spatial):
+    """lns_repair's realism fallback (hybrid.py:256-263): feasible moves sorted by
+    (-spatial[b], b), first one."""
+    feas = [(int(b), int(t)) for b, t in zip(cand, best_t) if t >= 0]
+    if not feas:
+        return None
+    b, t = sorted(feas, key=lambda m: (-spatial[m[0]], m[0]))[0]
+    return (b, t, float(spatial[b]))
+
+
+def test_realism_key_on_device(oracle_lib):
+    """The second selection key (k_realism) equals the reference's sort of the feasible moves, with
+    duplicated candidates, ties in geological consistency (a constant-feature instance), host and
+    device buffers, both evaluation kernels (T <= 32 and T = 40)."""
+    c = config("C1")
+    rng = np.random.default_rng(9)
+    eng = Engine.from_tables(c["bm"], ScenarioTables(c["vmax"], c["sigma"]), c["greedy"])
+    sp = eng.spatial()
+    for k in range(6):
+        cand = rng.integers(0, c["bm"].n_blocks, size=int(rng.integers(1, 3000))).astype(np.int32)
+        cand = np.concatenate([cand, cand[: cand.size // 3]])
+        r = eng.eval_candidates(cand, None, net=bool(k % 2), realism=True)
+        assert r["realism"] == _realism_ref(cand, r["best_t"], sp), k
+    eng.close()
+    # ties: every block has the same features, hence the same consistency -> lowest block wins
+    bm = c["bm"]
+    flat = BlockModel(n_blocks=bm.n_blocks, n_periods=bm.n_periods, edges_i=bm.edges_i, edges_j=bm.edges_j,
+                      mass=bm.mass, cost=bm.cost, capacity=bm.capacity, discount_rate=bm.discount_rate,
+                      coords=bm.coords, alteration=np.full(bm.n_blocks, 0.5), structural=np.full(bm.n_blocks, 0.5),
+                      dist_intrusion=np.ones(bm.n_blocks), base_grade=np.zeros(bm.n_blocks))
+    eng = Engine.from_tables(flat, ScenarioTables(c["vmax"], c["sigma"]), c["greedy"])
+    sp = eng.spatial()
+    assert np.all(sp == sp[0])
+    cand = rng.permutation(bm.n_blocks)[:1500].astype(np.int32)
+    r = eng.eval_candidates(cand, None, realism=True)
+    assert r["realism"] == _realism_ref(cand, r["best_t"], sp)
+    eng.close()
+    # T = 40: the general evaluation kernel
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.model import scenario_values
+
+    bm40 = synth.generate_block_model(2000, (20, 10, 10), 40, 1, seed=4, n_rock_types=1)
+    g = synth.sample_lognormal(bm40, 7, 0.3, seed=5)
+    eng = Engine.from_tables(bm40, ScenarioTables(scenario_values(bm40, g), synth.uncertainty_sigma(bm40, g)),
+                             synth.full_greedy(bm40))
+    sp = eng.spatial()
+    cand = rng.integers(0, 2000, size=900).astype(np.int32)
+    r = eng.eval_candidates(cand, None, realism=True)
+    assert r["realism"] == _realism_ref(cand, r["best_t"], sp)
     eng.close()
