@@ -154,6 +154,18 @@ PP_API int pp_set_geology(pp_ctx *ctx, const double *alteration, const double *s
 PP_API int pp_set_scenarios(pp_ctx *ctx, int32_t n_scenarios, const double *vmax_sb,
                      const double *sigma_st);
 
+/* Device-side ingestion of a scenario set: the value table is built on the
+ * device from grades[S][B] as scenario_mode_values does (evaluate.py:116-124),
+ *   v[s][b][o] = ((grade * mass) * price) * recovery[o % n_recovery] - mass * proc_cost[o % n_proc_cost],
+ * vmax = max over the n_modes modes -- bit-identical to the host computation -- so a freshly sampled
+ * set (the DW loop refreshes one per iteration, colgen.py:477-478) crosses PCIe once as grades
+ * and never materialises on the host.  sigma_st as pp_set_scenarios. */
+PP_API int pp_set_scenarios_grades(pp_ctx *ctx, int32_t n_scenarios, const double *grades_sb, int32_t n_modes,
+                                   double price, const double *recovery, int32_t n_recovery, const double *proc_cost,
+                                   int32_t n_proc_cost, const double *sigma_st);
+/* The bound value table back in the reference layout vmax[S][B] (host output). */
+PP_API int pp_get_scenario_values(pp_ctx *ctx, double *vmax_sb_out);
+
 /* ---- schedule -------------------------------------------------------------------- */
 /* Install assign[B] as the current schedule (copied, or borrowed in place with
  * PP_MEM_DEVICE_BORROW until the next call).  period_mass[t] = masses[assign == t].sum()

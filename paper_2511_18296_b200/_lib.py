@@ -89,6 +89,9 @@ SIGNATURES = {
     "pp_set_geology": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                                  c_double]),
     "pp_set_scenarios": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    "pp_set_scenarios_grades": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_double, c_void_p, c_int32, c_void_p,
+                                          c_int32, c_void_p]),
+    "pp_get_scenario_values": (c_int32, [c_void_p, c_void_p]),
     "pp_set_schedule": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_apply_moves": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     "pp_get_schedule": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),

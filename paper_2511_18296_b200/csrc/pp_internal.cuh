@@ -513,6 +513,8 @@ struct pp_ctx {
     DevBuf ej_count, ej_key, ej_blk;    // ejection lists [T][B] (pp_eject)
     DevBuf hours, npv_raw, npv_cost, npv_n;  // relaxed NPV (pp_npv.cu)
     DevBuf s2_items, s2_scratch;  // large-period stage-2: work list [S*T*P | S*2*M] and per-CTA scratch
+    DevBuf s2_rec;                // pp_npv_moves: the base schedule's per-(s, t) greedy structure
+    DevBuf s2_assign;             // pp_npv_moves: the device copy of the cached base schedule
     DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
@@ -522,7 +524,7 @@ struct pp_ctx {
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
-                &npv_cost, &npv_n, &s2_items, &s2_scratch, &pr_score, &pr_cap, &pr_assign, &pr_elig};
+                &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig};
     }
 };
 

@@ -54,7 +54,8 @@ struct S2Layout {
 // thread 0: the leaves from the recursion on thread 0 (pre-order, i.e. element order) into
 // ls/ll (capacity >= n/64 + 2), one thread per leaf with numpy's 8 accumulators into leafval[],
 // the fold in post-order on thread 0.  `a`, ls, ll and leafval may live in shared or global memory.
-__device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *leafval) {
+template <class GF>
+__device__ double s2_pairwise_f(GF a, int n, int *ls, int *ll, double *leafval) {
     __shared__ int s_nl;
     if (threadIdx.x == 0) {
         int stk_o[32], stk_n[32], sp = 0, nl = 0;
@@ -83,24 +84,28 @@ __device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *
     }
     __syncthreads();
     const int nl = s_nl;
-    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-        const int o = ls[l], len = ll[l];
-        double r;
-        if (len < 8) {
-            r = -0.0;
-            for (int i = 0; i < len; i++) r = f64_add(r, a[o + i]);
-        } else {
-            double acc[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++) acc[j] = a[o + j];
-            const int main_ = len - (len & 7);
-            for (int i = 8; i < main_; i += 8)
-#pragma unroll
-                for (int j = 0; j < 8; j++) acc[j] = f64_add(acc[j], a[o + i + j]);
-            r = tree8(acc);
-            for (int i = main_; i < len; i++) r = f64_add(r, a[o + i]);
+    // leaf sums, eight lanes per leaf: lane j is numpy's accumulator j over the leaf's blocks of 8
+    // (reads of consecutive elements by consecutive lanes), the xor butterfly over the eight lanes
+    // is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the remainder is added in order by the group's lane 0
+    const int grp = threadIdx.x >> 3, jl = threadIdx.x & 7, ngrp = blockDim.x >> 3;
+    for (int l0 = 0; l0 < nl; l0 += ngrp) {
+        const int l = l0 + grp;
+        const bool act = l < nl;
+        const int o = act ? ls[l] : 0, len = act ? ll[l] : 0;
+        const int main_ = len >= 8 ? len - (len & 7) : 0;
+        double acc = 0.0;
+        if (main_) {
+            acc = a(o + jl);
+            for (int i = 8; i < main_; i += 8) acc = f64_add(acc, a(o + i + jl));
         }
-        leafval[l] = r;
+        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+        if (act && jl == 0) {
+            double r = main_ ? acc : -0.0;
+            for (int i = main_; i < len; i++) r = f64_add(r, a(o + i));
+            leafval[l] = r;
+        }
     }
     __syncthreads();
     double res = 0.0;
@@ -141,6 +146,10 @@ __device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *
         res = f64_add(0.0, n ? val[0] : -0.0);
     }
     return res;
+}
+
+__device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *leafval) {
+    return s2_pairwise_f([&](int k) { return a[k]; }, n, ls, ll, leafval);
 }
 
 // The blocks of schedule `a` (block ob moved to period ot when ob >= 0) mined in period t, in
@@ -209,8 +218,12 @@ __device__ int s2_compact(const int32_t *__restrict__ a, int B, int t, int ob, i
 // then each lane tests its block for a stop (k >= kpos, hours_left <= 0) or a partial take
 // (hours_left * rate < m).  At the first flagged block the exact scalar loop takes over from
 // that block's hours_left and total.  Call from warp 0 only; the result is on lane 0.
+// With rec_h / rec_t (may be null) the state before every processed position k -- (hours_left,
+// total) -- is recorded for k = 0..K, K the position where the loop stopped (K = n when it ran
+// through), and K goes to *rec_k: the prefix an incremental variant restarts from (k_s2_chain).
 template <class DF, class MF, class QF>
-__device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF dof, MF mof, QF qof) {
+__device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF dof, MF mof, QF qof,
+                                 double *rec_h = nullptr, double *rec_t = nullptr, int32_t *rec_k = nullptr) {
     __shared__ double s_q32[32], s_dm32[32];
     const int lane = threadIdx.x & 31;
     double hl = hours0, total = 0.0;
@@ -235,6 +248,10 @@ __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF
         __syncwarp();
         const bool stop = !in || kk >= kpos || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
         const unsigned sm = __ballot_sync(0xffffffffu, stop);
+        if (rec_h && in && (!sm || lane <= __ffs(sm) - 1)) {
+            rec_h[kk] = h_mine;
+            rec_t[kk] = t_mine;
+        }
         if (sm) {
             const int jf = __ffs(sm) - 1;
             k = k0 + jf;
@@ -247,6 +264,10 @@ __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF
     }
     if (lane == 0) {
         for (; k < n; k++) {
+            if (rec_h) {
+                rec_h[k] = hl;
+                rec_t[k] = total;
+            }
             if (k >= kpos || hl <= 0) break;
             const double d = dof(k);
             const double mk = mof(k);
@@ -259,9 +280,32 @@ __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF
                 hl = f64_sub(hl, qof(k));
             }
         }
+        if (rec_h) {
+            if (k >= n) {
+                rec_h[n] = hl;
+                rec_t[n] = total;
+            }
+            *rec_k = k < n ? k : n;
+        }
     }
     return total;
 }
+
+// Per-(scenario, period) structure of one base schedule, kept on the device between pp_npv_moves
+// calls so a one-block variant is valued incrementally (k_s2_chain) instead of re-sorting:
+//   D/M/BID [S][T][L]  the period's blocks with density > 0 in greedy order (density desc, block
+//                      asc), their masses and ids; npos[S][T] of them
+//   H/TT    [S][T][L]  (hours_left, total) before position k, k = 0..K[S][T] (K = where the loop
+//                      stopped; npos when it ran through)
+//   pos     [S][B]     position of block b in its period's list, -1 if its density is <= 0
+//   IDS     [T][L]     the period's mined blocks in block order; nper[T] of them
+//   CS      [T][L]     their mining costs cost[b][t] in that order (the variants' cost sums)
+// L = B + 1.  All pointers null = not recorded.
+struct S2Struct {
+    double *D, *M, *H, *TT, *CS;
+    int32_t *BID, *npos, *K, *pos, *IDS, *nper;
+    int L;
+};
 
 // Work item of the large-period path: (scenario, grid y, grid z) of a k_stage2 CTA whose period
 // has more than S2_NMAX mined blocks.
@@ -274,7 +318,8 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
              const double *__restrict__ cost, const double *__restrict__ vmax, const double *__restrict__ hours,
              double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
              S2Item *__restrict__ big_items, int32_t *__restrict__ big_count, const int32_t *__restrict__ ovr_b,
-             const int32_t *__restrict__ ovr_t, const int32_t *__restrict__ slot_t) {
+             const int32_t *__restrict__ ovr_t, const int32_t *__restrict__ slot_t, const int32_t *__restrict__ tsel,
+             const S2Struct rec) {
     extern __shared__ __align__(16) unsigned char s2_dyn[];
     typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
     double *dsort = reinterpret_cast<double *>(s2_dyn);  // after the sort
@@ -287,10 +332,12 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     // schedule (ovr_b != nullptr): grid (S, 2, M), variant m = base with block ovr_b[m] in period
     // ovr_t[m], blockIdx.y = slot of the two periods it changes (slot_t[m][slot], -1 = none)
     const int s = blockIdx.x, p = blockIdx.z;
-    const int t = ovr_b ? slot_t[2 * p + blockIdx.y] : (int)blockIdx.y;
+    const int t = ovr_b ? slot_t[2 * p + blockIdx.y] : (tsel ? tsel[blockIdx.y] : (int)blockIdx.y);
     const int tid = threadIdx.x;
     if (t < 0) return;
     NPVP(0);
+    const bool record = rec.D != nullptr;  // whole single schedule (ovr_b == nullptr, P == 1)
+    const size_t rst = ((size_t)s * T + t) * rec.L;
     const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
     const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
     // 1. blocks mined in t, block order
@@ -304,17 +351,32 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     NPVP(1);
     // 2. mining-cost sum of the period (numpy pairwise, block order), once per (p, t)
     if (s == 0) {
-        for (int k = tid; k < n; k += S2_THREADS) ms[k] = __ldg(cost + (size_t)ids[k] * T + t);
+        for (int k = tid; k < n; k += S2_THREADS) {
+            ms[k] = __ldg(cost + (size_t)ids[k] * T + t);
+            if (record) {
+                rec.IDS[(size_t)t * rec.L + k] = ids[k];
+                rec.CS[(size_t)t * rec.L + k] = ms[k];
+            }
+        }
         __syncthreads();
         const double cs = s2_pairwise(ms, n, s_ls, s_ll, s_scr);
         if (tid == 0) {
             costsum[pt] = cs;
             nmined[pt] = n;
+            if (record) rec.nper[t] = n;
         }
         __syncthreads();
     }
     if (n == 0) {
-        if (tid == 0) raw[pt * S + s] = 0.0;
+        if (tid == 0) {
+            raw[pt * S + s] = 0.0;
+            if (record) {
+                rec.npos[(size_t)s * T + t] = 0;
+                rec.K[(size_t)s * T + t] = 0;
+                rec.H[rst] = __ldg(hours + t);
+                rec.TT[rst] = 0.0;
+            }
+        }
         return;
     }
     // 3. densities, stable descending radix sort (= np.argsort(-density, kind="stable"); the order
@@ -327,10 +389,17 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         S2Sort1(*reinterpret_cast<typename S2Sort1::TempStorage *>(s2_dyn)).SortDescending(d1, i1);
         __syncthreads();  // the sort's temp storage becomes the sorted densities
         if (tid < n) {
-            const double m = __ldg(mass + ids[i1[0]]);
+            const int bb = ids[i1[0]];
+            const double m = __ldg(mass + bb);
             dsort[tid] = d1[0];
             ms[tid] = m;
             qs[tid] = f64_div(m, rate);
+            if (record) {
+                rec.D[rst + tid] = d1[0];
+                rec.M[rst + tid] = m;
+                rec.BID[rst + tid] = bb;
+                rec.pos[(size_t)s * B + bb] = d1[0] > 0 ? tid : -1;
+            }
         }
     } else {
         double dk[S2_IPT];
@@ -352,10 +421,17 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         for (int u = 0; u < S2_IPT; u++) {
             const int k = tid * S2_IPT + u;
             if (k < n) {
-                const double m = __ldg(mass + ids[ik[u]]);
+                const int bb = ids[ik[u]];
+                const double m = __ldg(mass + bb);
                 dsort[k] = dk[u];
                 ms[k] = m;
                 qs[k] = f64_div(m, rate);
+                if (record) {
+                    rec.D[rst + k] = dk[u];
+                    rec.M[rst + k] = m;
+                    rec.BID[rst + k] = bb;
+                    rec.pos[(size_t)s * B + bb] = dk[u] > 0 ? k : -1;
+                }
             }
         }
     }
@@ -369,10 +445,15 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         if (dsort[k] <= 0) atomicMin(&s_kpos, k);  // first d <= 0 (the scalar loop's stop)
     __syncthreads();
     if (tid < 32) {
+        const int kpos = s_kpos;
         const double total = s2_greedy_warp(
-            n, s_kpos, __ldg(hours + t), rate, [&](int k) { return dsort[k]; }, [&](int k) { return ms[k]; },
-            [&](int k) { return qs[k]; });
-        if (tid == 0) raw[pt * S + s] = total;
+            kpos, kpos, __ldg(hours + t), rate, [&](int k) { return dsort[k]; }, [&](int k) { return ms[k]; },
+            [&](int k) { return qs[k]; }, record ? rec.H + rst : nullptr, record ? rec.TT + rst : nullptr,
+            record ? rec.K + (size_t)s * T + t : nullptr);
+        if (tid == 0) {
+            raw[pt * S + s] = total;
+            if (record) rec.npos[(size_t)s * T + t] = kpos;
+        }
     }
     NPVP(4);
 }
@@ -402,7 +483,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
                  double rate, double *__restrict__ raw, double *__restrict__ costsum, int32_t *__restrict__ nmined,
                  const S2Item *__restrict__ items, const int32_t *__restrict__ count, unsigned char *__restrict__ scratch,
                  const int32_t *__restrict__ ovr_b, const int32_t *__restrict__ ovr_t,
-                 const int32_t *__restrict__ slot_t) {
+                 const int32_t *__restrict__ slot_t, const int32_t *__restrict__ tsel, const S2Struct rec) {
     extern __shared__ __align__(16) unsigned char s2_dyn[];
     typename S2Sort::TempStorage &sort_tmp = *reinterpret_cast<typename S2Sort::TempStorage *>(s2_dyn);
     __shared__ int s_np;
@@ -417,7 +498,9 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
         const S2Item it = items[w];
         const int s = it.s, p = it.z;
-        const int t = ovr_b ? slot_t[2 * p + it.y] : it.y;
+        const int t = ovr_b ? slot_t[2 * p + it.y] : (tsel ? tsel[it.y] : it.y);
+        const bool record = rec.D != nullptr;
+        const size_t rst = ((size_t)s * T + t) * rec.L;
         const int32_t *a = ovr_b ? assign : assign + (size_t)p * B;
         const int ob = ovr_b ? ovr_b[p] : -1, ot = ovr_b ? ovr_t[p] : -1;
         const size_t pt = ovr_b ? (size_t)2 * p + it.y : ((size_t)p * T + t);
@@ -426,14 +509,23 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
         const int n = s2_compact(a, B, t, ob, ot, ids, B);
         __syncthreads();
         // 2.
+        if (record)  // every block of the period leaves its scenario-s position unset ...
+            for (int k = tid; k < n; k += S2_THREADS) rec.pos[(size_t)s * B + ids[k]] = -1;
         if (s == 0) {
-            for (int k = tid; k < n; k += S2_THREADS) kb[k] = __ldg(cost + (size_t)ids[k] * T + t);
+            for (int k = tid; k < n; k += S2_THREADS) {
+                kb[k] = __ldg(cost + (size_t)ids[k] * T + t);
+                if (record) {
+                    rec.IDS[(size_t)t * rec.L + k] = ids[k];
+                    rec.CS[(size_t)t * rec.L + k] = kb[k];
+                }
+            }
             __syncthreads();
             // leaves: at most n/64 + 2 of them, in ba / bb; leaf values in ka
             const double cs = s2_pairwise(kb, n, ba, bb, ka);
             if (tid == 0) {
                 costsum[pt] = cs;
                 nmined[pt] = n;
+                if (record) rec.nper[t] = n;
             }
             __syncthreads();
         }
@@ -535,14 +627,29 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
             srcb = dstb;
             dstb = tb;
         }
+        if (record) {  // ... and the positives get their place in the greedy order (after the -1s above)
+            __syncthreads();
+            for (int k = tid; k < np_; k += S2_THREADS) {
+                const int bb = srcb[k];
+                rec.D[rst + k] = srck[k];
+                rec.M[rst + k] = __ldg(mass + bb);
+                rec.BID[rst + k] = bb;
+                rec.pos[(size_t)s * B + bb] = k;
+            }
+        }
         // 5. the greedy fill over the positive prefix
         if (tid < 32) {
             const double *dk_ = srck;
             const int32_t *bk_ = srcb;
             const double total = s2_greedy_warp(
                 np_, np_, __ldg(hours + t), rate, [&](int k) { return dk_[k]; },
-                [&](int k) { return __ldg(mass + bk_[k]); }, [&](int k) { return f64_div(__ldg(mass + bk_[k]), rate); });
-            if (tid == 0) raw[pt * S + s] = total;
+                [&](int k) { return __ldg(mass + bk_[k]); }, [&](int k) { return f64_div(__ldg(mass + bk_[k]), rate); },
+                record ? rec.H + rst : nullptr, record ? rec.TT + rst : nullptr,
+                record ? rec.K + (size_t)s * T + t : nullptr);
+            if (tid == 0) {
+                raw[pt * S + s] = total;
+                if (record) rec.npos[(size_t)s * T + t] = np_;
+            }
         }
     }
 }
@@ -550,9 +657,12 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
 // Launches the stage-2 problems of grid (S, gy, gz): k_stage2 for every period that fits on chip,
 // then k_stage2_big for the rest (only when some period can exceed S2_NMAX, i.e. B > S2_NMAX).
 static int run_stage2(pp_ctx *c, cudaStream_t st, const int32_t *da, int gy, int gz, double *raw, double *costsum,
-                      int32_t *nmined, const int32_t *ovr_b, const int32_t *ovr_t, const int32_t *slot_t) {
+                      int32_t *nmined, const int32_t *ovr_b, const int32_t *ovr_t, const int32_t *slot_t,
+                      const int32_t *tsel = nullptr, const S2Struct *rec = nullptr, bool may_be_big = true) {
+    const S2Struct none{};
+    const S2Struct &rc = rec ? *rec : none;
     const int B = c->B, T = c->T, S = c->S;
-    const bool big = B > S2_NMAX;
+    const bool big = B > S2_NMAX && may_be_big;
     TRY(c->s2_items.ensure(sizeof(S2Item) * (size_t)S * gy * gz + 16));
     int32_t *count = reinterpret_cast<int32_t *>(c->s2_items.as<unsigned char>() + sizeof(S2Item) * (size_t)S * gy * gz);
     S2Item *items = c->s2_items.as<S2Item>();
@@ -560,7 +670,7 @@ static int run_stage2(pp_ctx *c, cudaStream_t st, const int32_t *da, int gy, int
     TRY(ensure_max_smem(k_stage2, S2Layout::bytes(), c->device));
     k_stage2<<<dim3(S, gy, gz), S2_THREADS, S2Layout::bytes(), st>>>(
         da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, raw, costsum, nmined, items, count, ovr_b, ovr_t, slot_t);
+        c->rate, raw, costsum, nmined, items, count, ovr_b, ovr_t, slot_t, tsel, rc);
     CUDA_TRY(cudaGetLastError());
     if (!big) return PP_OK;
     int sms = 148;
@@ -572,9 +682,175 @@ static int run_stage2(pp_ctx *c, cudaStream_t st, const int32_t *da, int gy, int
     TRY(ensure_max_smem(k_stage2_big, S2Layout::bytes(), c->device));
     k_stage2_big<<<grid, S2_THREADS, S2Layout::bytes(), st>>>(
         da, B, T, S, c->Sp, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(), c->hours.as<double>(),
-        c->rate, raw, costsum, nmined, items, count, c->s2_scratch.as<unsigned char>(), ovr_b, ovr_t, slot_t);
+        c->rate, raw, costsum, nmined, items, count, c->s2_scratch.as<unsigned char>(), ovr_b, ovr_t, slot_t, tsel,
+        rc);
     CUDA_TRY(cudaGetLastError());
     return PP_OK;
+}
+
+
+// ------------------------------------------------------------------------------------
+// Incremental one-block variants (pp_npv_moves).  A variant moves block b from period t_old to
+// t_new; only those two periods' stage-2 problems change.  With the base schedule's greedy
+// order and its recorded prefix states (S2Struct) each re-solve is exact without a sort:
+//   leave t_old: b sits at position j of the (s, t_old) order (pos[s][b]; absent if its density
+//                is <= 0, then nothing changes); restart the recurrence from the state before j
+//                and continue with positions j+1, j+2, ...
+//   enter t_new: its position j is the binary search of (density, b) in the (s, t_new) order;
+//                restart from the state before j with b, then positions j, j+1, ...
+// A position beyond the base's stop K leaves the result unchanged.  The recurrence is the
+// scalar loop of evaluate.py:174-182 verbatim, so the values equal a full re-solve bit for bit.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int T, int S, int Sp, int M,
+                                                  const int32_t *__restrict__ blocks, const int32_t *__restrict__ slot_t,
+                                                  const int32_t *__restrict__ run, const double *__restrict__ vmax,
+                                                  const double *__restrict__ mass, double rate,
+                                                  const double *__restrict__ braw, double *__restrict__ mraw) {
+    // one warp per (slot, scenario): lanes load 32 consecutive elements of the modified order at a
+    // time (coalesced, one batch ahead), every lane runs the speculative whole-take recurrence over
+    // them (the adds of the scalar loop, in its order), and the first element where the scalar loop
+    // would stop or take partially hands over to the exact scalar tail -- as s2_greedy_warp.  (A
+    // thread per chain measured 2.8x slower: each chain walks its own list, so the loads of a thread
+    // are serialised by latency; the warp's coalesced batches are not.)
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const long long unit = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (unit >= 2ll * M * S) return;
+    const int s = (int)(unit % S), si = (int)(unit / S);
+    const int t = slot_t[si];
+    if (t < 0 || run[si] < 0) return;
+    const int b = blocks[si >> 1];
+    const size_t st_ = (size_t)s * T + t, base = st_ * rec.L;
+    const int np = rec.npos[st_], K = rec.K[st_];
+    const double *D = rec.D + base, *Mm = rec.M + base;
+    const bool ins = si & 1;
+    double dnew = 0.0, mnew = 0.0;
+    int j;
+    if (!ins) {
+        j = rec.pos[(size_t)s * B + b];
+    } else {
+        mnew = __ldg(mass + b);
+        dnew = f64_div(__ldg(vmax + (size_t)b * Sp + s), mnew);
+        j = -1;
+        if (dnew > 0) {  // first position that does not precede (dnew, b) in the greedy order
+            const int32_t *BI = rec.BID + base;
+            int lo = 0, hi = np;
+            while (lo < hi) {
+                const int md = (lo + hi) >> 1;
+                const double dm = D[md];
+                if (dm > dnew || (dm == dnew && BI[md] < b))
+                    lo = md + 1;
+                else
+                    hi = md;
+            }
+            j = lo;
+        }
+    }
+    if (j < 0 || j > K) {  // the variant's order agrees with the base's up to its stop
+        if (lane == 0) mraw[(size_t)si * S + s] = braw[(size_t)t * S + s];
+        return;
+    }
+    // the modified order: element e = the inserted block (e = 0) then positions j, j+1, ... , or
+    // positions j+1, j+2, ... after a removal
+    const int E = ins ? np - j + 1 : np - j - 1;
+    auto elem = [&](int e, double &d, double &m) {
+        if (ins && e == 0) {
+            d = dnew;
+            m = mnew;
+        } else {
+            const int k = ins ? j + e - 1 : j + 1 + e;
+            d = D[k];
+            m = Mm[k];
+        }
+    };
+    double hl = rec.H[base + j], tot = rec.TT[base + j];
+    int e = E;
+    double dnx = 0.0, mnx = 0.0;  // the next batch's element, loaded one batch ahead
+    if (lane < E) elem(lane, dnx, mnx);
+    for (int e0 = 0; e0 < E; e0 += 32) {
+        const int ee = e0 + lane;
+        const bool in = ee < E;
+        const double d = dnx, m = mnx;
+        if (ee + 32 < E) elem(ee + 32, dnx, mnx);
+        const double q = in ? f64_div(m, rate) : 0.0;
+        const double dm = in ? f64_mul(d, m) : 0.0;
+        double h = hl, tt = tot, h_mine = 0.0, t_mine = 0.0;
+#pragma unroll 8
+        for (int jj = 0; jj < 32; jj++) {
+            if (lane == jj) {
+                h_mine = h;
+                t_mine = tt;
+            }
+            h = f64_sub(h, __shfl_sync(FULL, q, jj));
+            tt = f64_add(tt, __shfl_sync(FULL, dm, jj));
+        }
+        const bool stop = !in || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
+        const unsigned sm = __ballot_sync(FULL, stop);
+        if (sm) {
+            const int jf = __ffs(sm) - 1;
+            e = e0 + jf;
+            hl = __shfl_sync(FULL, h_mine, jf);
+            tot = __shfl_sync(FULL, t_mine, jf);
+            break;
+        }
+        hl = h;
+        tot = tt;
+    }
+    if (lane == 0) {
+        for (; e < E; e++) {  // the scalar loop of evaluate.py:174-182
+            if (hl <= 0) break;
+            double d, m;
+            elem(e, d, m);
+            const double hr = f64_mul(hl, rate);
+            if (hr < m) {  // take = hours_left * rate
+                tot = f64_add(tot, f64_mul(d, hr));
+                hl = f64_sub(hl, f64_div(hr, rate));
+            } else {
+                tot = f64_add(tot, f64_mul(d, m));
+                hl = f64_sub(hl, f64_div(m, rate));
+            }
+        }
+        mraw[(size_t)si * S + s] = tot;
+    }
+}
+
+// The variant period's mining-cost sum (numpy pairwise over its blocks in block order, the base
+// list with b removed / inserted) and block count, one CTA per re-solved slot (persistent).
+__global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, int M, const int32_t *__restrict__ blocks,
+                                                    const int32_t *__restrict__ slot_t, const int32_t *__restrict__ run,
+                                                    const double *__restrict__ cost, double *__restrict__ mcost,
+                                                    int32_t *__restrict__ mn, int cap) {
+    // the pairwise plan's leaves (<= n/64 + 2) live in shared memory: cap of each array
+    extern __shared__ __align__(16) unsigned char vc_dyn[];
+    double *lv = reinterpret_cast<double *>(vc_dyn);
+    int *ls = reinterpret_cast<int *>(lv + cap);
+    int *ll = ls + cap;
+    for (int si = blockIdx.x; si < 2 * M; si += gridDim.x) {
+        const int t = slot_t[si];
+        if (t < 0 || run[si] < 0) continue;
+        const int b = blocks[si >> 1];
+        const int32_t *ids = rec.IDS + (size_t)t * rec.L;
+        const double *csl = rec.CS + (size_t)t * rec.L;
+        const double cb = __ldg(cost + (size_t)b * T + t);
+        const int n0 = rec.nper[t];
+        int lo = 0, hi = n0;  // block-order position of b
+        while (lo < hi) {
+            const int md = (lo + hi) >> 1;
+            if (ids[md] < b) lo = md + 1;
+            else hi = md;
+        }
+        const int r = lo;
+        const bool ins = si & 1;
+        const int n = ins ? n0 + 1 : n0 - 1;
+        const double cs = s2_pairwise_f(
+            [&](int k) { return ins ? (k < r ? csl[k] : (k == r ? cb : csl[k - 1])) : csl[k < r ? k : k + 1]; },
+            n, ls, ll, lv);
+        if (threadIdx.x == 0) {
+            mcost[si] = cs;
+            mn[si] = n;
+        }
+        __syncthreads();
+    }
 }
 
 // _npv / per_scenario_npv accumulation in the reference's order (t outer, s inner)
@@ -608,14 +884,18 @@ __global__ void k_npv_final(int T, int S, const double *__restrict__ raw, const 
 }
 
 // npv of variant m: the reference's accumulation over (t, s), the two changed periods from the
-// variant's stage-2 results, every other period from the base schedule's
+// variant's stage-2 results, every other period from the base schedule's.  One warp per variant:
+// lane s forms the scenario terms (d * sigma * raw) / S in parallel (the divisions dominate), lane 0
+// adds them in the reference's (t, s) order.
 __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict__ braw, const double *__restrict__ bcost,
                                   const int32_t *__restrict__ bn, const double *__restrict__ mraw,
                                   const double *__restrict__ mcost, const int32_t *__restrict__ mn,
                                   const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                                   const double *__restrict__ disc,
                                   const double *__restrict__ sigma, double *__restrict__ npv) {
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int m = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (m >= M) return;
     const int t0 = slot_t[2 * m], t1 = slot_t[2 * m + 1];
     double total = 0.0;
@@ -635,12 +915,18 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
         }
         const double d = disc[t];
         if (n > 0) total = f64_sub(total, f64_mul(d, cs));
-        for (int s = 0; s < S; s++) {
-            const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
-            total = f64_add(total, f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S));
+        for (int s0 = 0; s0 < S; s0 += 32) {
+            const int s = s0 + lane;
+            double q = 0.0;
+            if (s < S) {
+                const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
+                q = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
+            }
+            const int cnt = min(32, S - s0);
+            for (int u = 0; u < cnt; u++) total = f64_add(total, __shfl_sync(FULL, q, u));
         }
     }
-    npv[m] = total;
+    if (lane == 0) npv[m] = total;
 }
 
 extern "C" {
@@ -740,6 +1026,40 @@ int pp_stage2(pp_ctx *c, const int32_t *assign, int32_t P, double *raw_out, doub
     return PP_OK;
 }
 
+__global__ void k_scatter_assign(int32_t *__restrict__ assign, const int32_t *__restrict__ blk,
+                                 const int32_t *__restrict__ per, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) assign[blk[i]] = per[i];  // distinct blocks (a diff)
+}
+
+// carve the base structure (S2Struct) out of c->s2_rec for the current (S, T, B)
+static int s2_struct(pp_ctx *c, S2Struct *r) {
+    const size_t S = c->S, T = c->T, B = c->B, L = B + 1;
+    const size_t nd = S * T * L;
+    const size_t bytes = 4 * nd * sizeof(double) + T * L * sizeof(double) + nd * sizeof(int32_t) + 2 * S * T * sizeof(int32_t) +
+                         S * B * sizeof(int32_t) + T * L * sizeof(int32_t) + T * sizeof(int32_t) + 256;
+    TRY(c->s2_rec.ensure(bytes));
+    unsigned char *p = c->s2_rec.as<unsigned char>();
+    auto take = [&](size_t n) {
+        unsigned char *q = p;
+        p += (n + 15) & ~(size_t)15;
+        return q;
+    };
+    r->D = reinterpret_cast<double *>(take(nd * 8));
+    r->M = reinterpret_cast<double *>(take(nd * 8));
+    r->H = reinterpret_cast<double *>(take(nd * 8));
+    r->TT = reinterpret_cast<double *>(take(nd * 8));
+    r->CS = reinterpret_cast<double *>(take(T * L * 8));
+    r->BID = reinterpret_cast<int32_t *>(take(nd * 4));
+    r->npos = reinterpret_cast<int32_t *>(take(S * T * 4));
+    r->K = reinterpret_cast<int32_t *>(take(S * T * 4));
+    r->pos = reinterpret_cast<int32_t *>(take(S * B * 4));
+    r->IDS = reinterpret_cast<int32_t *>(take(T * L * 4));
+    r->nper = reinterpret_cast<int32_t *>(take(T * 4));
+    r->L = (int)L;
+    return PP_OK;
+}
+
 int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
                  uint32_t flags, double *npv_out, int32_t mem, void *stream) {
     if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
@@ -751,17 +1071,19 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
     cudaStream_t st = pick(c, stream);
     const int B = c->B, T = c->T, S = c->S;
     // which periods each variant changes (host arrays needed: the base assignment of the block)
-    std::vector<int32_t> hb(M), ht(M), ha(B);
+    std::vector<int32_t> hb(M), ht(M), hdev;
     const bool host = mem == PP_MEM_HOST;
+    const int32_t *ha = assign;
     if (host) {
         std::copy(blocks, blocks + M, hb.begin());
         std::copy(periods, periods + M, ht.begin());
-        std::copy(assign, assign + B, ha.begin());
     } else {
+        hdev.resize(B);
         CUDA_TRY(cudaMemcpyAsync(hb.data(), blocks, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaMemcpyAsync(ht.data(), periods, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(ha.data(), assign, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(hdev.data(), assign, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
+        ha = hdev.data();
     }
     // slot[2m] = the period the move leaves, slot[2m+1] = the period it enters (-1 = none).
     // The re-solve of the left period (block removed) depends only on the block, so the moves of
@@ -786,58 +1108,125 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
             }
         }
     }
-    // one packed upload (assign | blocks | periods | slots | runs | sources) and one result copy:
-    // each separate small copy costs a PCIe round trip
-    const size_t nin = (size_t)B + 8 * (size_t)M;
-    TRY(c->h_assign.ensure(sizeof(int32_t) * nin));
-    int32_t *da = c->h_assign.as<int32_t>(), *db = da + B, *dt = db + M, *ds = dt + M, *dr = ds + 2 * M,
-            *dsrc = dr + 2 * M;
-    TRY(c->npv_raw.ensure(sizeof(double) * ((size_t)T * S + (size_t)2 * M * S)));
-    TRY(c->npv_cost.ensure(sizeof(double) * ((size_t)T + 2 * (size_t)M)));
-    TRY(c->npv_n.ensure(sizeof(int32_t) * ((size_t)T + 2 * (size_t)M)));
+    // the base schedule's structure: reused when the tables (npv_gen), the result buffers (their
+    // allocation generation: a re-allocation may return the same address) and the structure are
+    // intact; then only the periods whose block sets changed since the cached base are re-solved
+    int Mcap = 1024;
+    while (Mcap < M) Mcap <<= 1;
+    TRY(c->npv_raw.ensure(sizeof(double) * ((size_t)T * S + (size_t)2 * Mcap * S)));
+    TRY(c->npv_cost.ensure(sizeof(double) * ((size_t)T + 2 * (size_t)Mcap)));
+    TRY(c->npv_n.ensure(sizeof(int32_t) * ((size_t)T + 2 * (size_t)Mcap)));
+    const uint64_t recgen = c->s2_rec.gen;
+    S2Struct rec;
+    TRY(s2_struct(c, &rec));
+    const bool intact = c->npvm_gen == c->npv_gen && c->npvm_bufgen[0] == c->npv_raw.gen &&
+                        c->npvm_bufgen[1] == c->npv_cost.gen && c->npvm_bufgen[2] == c->npv_n.gen &&
+                        c->s2_rec.gen == recgen && c->npvm_base.size() == (size_t)B;
+    // one pass over the base: range check, the blocks that changed since the cached base (their old
+    // and new periods are the ones to re-solve) and the period sizes (whether the large-period
+    // kernel can be needed at all)
+    std::vector<int32_t> dirty, chg_b, chg_t, cnt(T, 0);
+    {
+        std::vector<char> mark(T, 0);
+        const int32_t *old = intact ? c->npvm_base.data() : nullptr;
+        for (int b = 0; b < B; b++) {
+            const int32_t n = ha[b];
+            if (n < -1 || n >= T) return fail(PP_ERR_INVALID_ARGS, "assign[%d] = %d out of range", b, n);
+            if (n >= 0) cnt[n]++;
+            if (old && old[b] != n) {
+                if (old[b] >= 0) mark[old[b]] = 1;
+                if (n >= 0) mark[n] = 1;
+                chg_b.push_back(b);
+                chg_t.push_back(n);
+            }
+        }
+        for (int t = 0; t < T; t++)
+            if (mark[t]) dirty.push_back(t);
+    }
+    const bool full = !intact || (int)dirty.size() * 2 > T || chg_b.size() * 8 > (size_t)B;
+    const bool may_be_big = *std::max_element(cnt.begin(), cnt.end()) > S2_NMAX;
+    // the device keeps its own copy of the base assignment: a full upload when the structure is
+    // rebuilt, else only the changed entries (scattered by k_scatter_assign)
+    TRY(c->s2_assign.ensure(sizeof(int32_t) * (size_t)B));
+    int32_t *dbase = c->s2_assign.as<int32_t>();
+    const size_t nchg = full ? 0 : chg_b.size();
+    // one packed upload (blocks | periods | slots | runs | sources | re-solved periods | changed
+    // blocks | their periods) and one result copy: each separate small copy costs a PCIe round trip
+    const size_t nin = 8 * (size_t)M + T + 2 * nchg;
+    TRY(c->h_assign.ensure(sizeof(int32_t) * std::max<size_t>(nin, 1)));
+    int32_t *db = c->h_assign.as<int32_t>(), *dt = db + M, *ds = dt + M, *dr = ds + 2 * M,
+            *dsrc = dr + 2 * M, *dtsel = dsrc + 2 * M, *dcb = dtsel + T, *dct = dcb + nchg;
     TRY(c->h_d1.ensure(sizeof(double) * ((size_t)M + 1)));
     const size_t out_bytes = sizeof(double) * (size_t)M;
     unsigned char *stage = nullptr;
-    TRY(host_stage(c, std::max(sizeof(int32_t) * nin, out_bytes), &stage));
-    std::vector<int32_t> pkv(host ? 0 : nin);  // device mode returns before the copy completes:
-    {                                          // pack in pageable memory (staged synchronously)
-        int32_t *pk = host ? reinterpret_cast<int32_t *>(stage) : pkv.data();
-        std::copy(ha.begin(), ha.end(), pk);
-        std::copy(hb.begin(), hb.end(), pk + B);
-        std::copy(ht.begin(), ht.end(), pk + B + M);
-        std::copy(slot.begin(), slot.end(), pk + B + 2 * M);
-        std::copy(run.begin(), run.end(), pk + B + 4 * M);
-        std::copy(src.begin(), src.end(), pk + B + 6 * M);
-        CUDA_TRY(cudaMemcpyAsync(da, pk, sizeof(int32_t) * nin, cudaMemcpyHostToDevice, st));
+    TRY(host_stage(c, std::max(sizeof(int32_t) * std::max(nin, (size_t)B), out_bytes), &stage));
+    std::vector<int32_t> pkv(host ? 0 : std::max(nin, (size_t)B));  // device mode returns before the
+    int32_t *pk = host ? reinterpret_cast<int32_t *>(stage) : pkv.data();  // copy completes: pageable
+    if (full) {
+        if (host) {
+            CUDA_TRY(cudaMemcpyAsync(dbase, assign, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(dbase, assign, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+        }
     }
+    std::copy(hb.begin(), hb.end(), pk);
+    std::copy(ht.begin(), ht.end(), pk + M);
+    std::copy(slot.begin(), slot.end(), pk + 2 * M);
+    std::copy(run.begin(), run.end(), pk + 4 * M);
+    std::copy(src.begin(), src.end(), pk + 6 * M);
+    std::copy(dirty.begin(), dirty.end(), pk + 8 * M);
+    if (nchg) {
+        std::copy(chg_b.begin(), chg_b.end(), pk + 8 * M + T);
+        std::copy(chg_t.begin(), chg_t.end(), pk + 8 * M + T + nchg);
+    }
+    CUDA_TRY(cudaMemcpyAsync(db, pk, sizeof(int32_t) * nin, cudaMemcpyHostToDevice, st));
+    if (nchg) {
+        k_scatter_assign<<<(unsigned)((nchg + 255) / 256), 256, 0, st>>>(dbase, dcb, dct, (int)nchg);
+        CUDA_TRY(cudaGetLastError());
+    }
+    const int32_t *da = dbase;
     double *braw = c->npv_raw.as<double>(), *mraw = braw + (size_t)T * S;
     double *bcost = c->npv_cost.as<double>(), *mcost = bcost + T;
     int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
-    // the base schedule's results are reused while the tables (npv_gen), the three buffers (their
-    // allocation generation: a re-allocation may return the same address) and the base are unchanged
-    const bool base_hit = host && c->npvm_gen == c->npv_gen && c->npvm_bufgen[0] == c->npv_raw.gen &&
-                          c->npvm_bufgen[1] == c->npv_cost.gen && c->npvm_bufgen[2] == c->npv_n.gen &&
-                          c->npvm_base == ha;
-    if (!base_hit) TRY(run_stage2(c, st, da, T, 1, braw, bcost, bn, nullptr, nullptr, nullptr));
-    TRY(run_stage2(c, st, da, 2, M, mraw, mcost, mn, db, dt, dr));
+    if (full)
+        TRY(run_stage2(c, st, da, T, 1, braw, bcost, bn, nullptr, nullptr, nullptr, nullptr, &rec, may_be_big));
+    else if (!dirty.empty())
+        TRY(run_stage2(c, st, da, (int)dirty.size(), 1, braw, bcost, bn, nullptr, nullptr, nullptr, dtsel, &rec,
+                       may_be_big));
+    {
+        const long long nthr = 2ll * M * S * 32;  // a warp per (slot, scenario)
+        k_s2_chain<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(rec, B, T, S, c->Sp, M, db, ds, dr,
+                                                                  c->vmax.as<double>(), c->mass.as<double>(), c->rate,
+                                                                  braw, mraw);
+        CUDA_TRY(cudaGetLastError());
+        const int cap = B / 64 + 16;
+        const size_t smem = (size_t)16 * cap;
+        int sms = 148;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || sms < 1) sms = 148;
+        const int grid = std::max(1, std::min(2 * M, 4 * sms));
+        TRY(set_smem_attr(k_s2_varcost, smem, c->device));
+        k_s2_varcost<<<grid, 256, smem, st>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap);
+        CUDA_TRY(cudaGetLastError());
+    }
     double *dn = host ? c->h_d1.as<double>() : npv_out;
-    k_npv_moves_final<<<(M + 127) / 128, 128, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
+    k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
                                                         c->disc.as<double>(),
                                                         (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
     CUDA_TRY(cudaGetLastError());
+    // the structure now describes `ha` (complete once the stream reaches this point)
+    c->npvm_gen = c->npv_gen;
+    c->npvm_bufgen[0] = c->npv_raw.gen;
+    c->npvm_bufgen[1] = c->npv_cost.gen;
+    c->npvm_bufgen[2] = c->npv_n.gen;
+    if (full) {
+        c->npvm_base.assign(ha, ha + B);
+    } else {
+        for (size_t k = 0; k < chg_b.size(); k++) c->npvm_base[chg_b[k]] = chg_t[k];
+    }
     if (host) {
         CUDA_TRY(cudaMemcpyAsync(stage, dn, out_bytes, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(stream_wait(st));
         std::memcpy(npv_out, stage, sizeof(double) * M);
-        if (!base_hit) {  // the base results just computed are complete and valid
-            c->npvm_gen = c->npv_gen;
-            c->npvm_bufgen[0] = c->npv_raw.gen;
-            c->npvm_bufgen[1] = c->npv_cost.gen;
-            c->npvm_bufgen[2] = c->npv_n.gen;
-            c->npvm_base = ha;
-        }
-    } else {
-        c->npvm_gen = ~0ull;  // device mode: the base results may be read before they are complete
     }
     return PP_OK;
 }

@@ -586,6 +586,41 @@ __global__ void k_scen_tables(const double *__restrict__ vsb, int S, int B, int 
     unit_mean[b] = f64_div(acc, (double)S);
 }
 
+// Scenario values straight from grades[S][B] (scenario_mode_values, evaluate.py:116-124):
+//   v[s][b][o] = ((grade * mass) * price) * recovery[o % nrec] - mass * proc_cost[o % ncost]
+// (numpy's left-to-right evaluation), vmax = max over modes, written block-major [B][Sp] with the
+// sequential scenario mean unit_mean[b] (evaluate.py:302).  One thread per block; the grade reads
+// g[s][b] are coalesced across the warp for every s.
+__global__ void k_scen_from_grades(const double *__restrict__ g, int S, int B, int Sp, const double *__restrict__ mass,
+                                   double price, const double *__restrict__ rec, int nrec,
+                                   const double *__restrict__ pcost, int ncost, int nmodes,
+                                   double *__restrict__ vbs, double *__restrict__ unit_mean) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double m = __ldg(mass + b);
+    double acc = 0.0;
+    for (int s = 0; s < S; s++) {
+        const double gm = f64_mul(f64_mul(__ldg(g + (size_t)s * B + b), m), price);
+        double v = 0.0;
+        for (int o = 0; o < nmodes; o++) {
+            const double vo = f64_sub(f64_mul(gm, __ldg(rec + o % nrec)), f64_mul(m, __ldg(pcost + o % ncost)));
+            v = (o == 0 || vo > v || vo != vo) ? vo : v;  // np.max over the mode axis (NaN propagates)
+        }
+        vbs[(size_t)b * Sp + s] = v;
+        acc = f64_add(acc, v);
+    }
+    for (int s = S; s < Sp; s++) vbs[(size_t)b * Sp + s] = 0.0;
+    unit_mean[b] = f64_div(acc, (double)S);
+}
+
+// block-major vmax [B][Sp] back to the reference layout [S][B]
+__global__ void k_scen_to_sb(const double *__restrict__ vbs, int S, int B, int Sp, double *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)S * B) return;
+    const int s = (int)(i / B), b = (int)(i % B);
+    out[i] = vbs[(size_t)b * Sp + s];
+}
+
 // sigma.mean(axis=0) sequentially over s (evaluate.py:351)
 __global__ void k_sig_mean(const double *sigma, int S, int T, double *out) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1265,9 +1300,12 @@ int pp_set_geology(pp_ctx *c, const double *alt, const double *strc, const doubl
     return PP_OK;
 }
 
-int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *sigma_st) {
-    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
-    if (S < 1 || !vmax_sb) return fail(PP_ERR_INVALID_ARGS, "need n_scenarios >= 1 and a value table");
+}  // extern "C"
+
+// common part of pp_set_scenarios / pp_set_scenarios_grades: `fill` writes c->vmax [B][Sp] and
+// c->unit_mean on c->stream from host data
+template <class Fill>
+static int set_scenarios_common(pp_ctx *c, int32_t S, const double *sigma_st, Fill fill) {
     TRY(use_device(c));
     PwPlan plan;
     TRY(make_plan(S, &plan));
@@ -1280,14 +1318,7 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     TRY(c->ones_st.ensure(sizeof(double) * (size_t)S * T));
     TRY(c->sig_mean.ensure(sizeof(double) * T));
     TRY(c->plan_dev.ensure(sizeof(int) * kPlanWords));
-    DevBuf tmp;
-    TRY(tmp.ensure(sizeof(double) * (size_t)S * B));
-    cudaError_t e = dev_upload(c, tmp.ptr, vmax_sb, sizeof(double) * (size_t)S * B);
-    if (e == cudaSuccess) {
-        k_scen_tables<<<(B + 255) / 256, 256, 0, c->stream>>>(tmp.as<double>(), S, B, Sp, c->vmax.as<double>(),
-                                                              c->unit_mean.as<double>());
-        e = cudaGetLastError();
-    }
+    cudaError_t e = fill(Sp);
     std::vector<double> ones((size_t)S * T, 1.0);
     int words[kPlanWords];
     plan_words(plan, words);
@@ -1307,7 +1338,6 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
         }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    tmp.release();
     if (e != cudaSuccess) return fail(PP_ERR_CUDA, "pp_set_scenarios: %s", cudaGetErrorString(e));
     c->S = S;
     c->Sp = Sp;
@@ -1316,6 +1346,75 @@ int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *
     c->have_sigma = sigma_st != nullptr;
     c->have_scen = true;
     c->npv_gen++;
+    return PP_OK;
+}
+
+extern "C" {
+
+int pp_set_scenarios(pp_ctx *c, int32_t S, const double *vmax_sb, const double *sigma_st) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (S < 1 || !vmax_sb) return fail(PP_ERR_INVALID_ARGS, "need n_scenarios >= 1 and a value table");
+    const int B = c->B;
+    DevBuf tmp;
+    TRY(tmp.ensure(sizeof(double) * (size_t)S * B));
+    const int rc = set_scenarios_common(c, S, sigma_st, [&](int Sp) {
+        cudaError_t e = dev_upload(c, tmp.ptr, vmax_sb, sizeof(double) * (size_t)S * B);
+        if (e == cudaSuccess) {
+            k_scen_tables<<<(B + 255) / 256, 256, 0, c->stream>>>(tmp.as<double>(), S, B, Sp, c->vmax.as<double>(),
+                                                                  c->unit_mean.as<double>());
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        return e;
+    });
+    tmp.release();
+    return rc;
+}
+
+int pp_set_scenarios_grades(pp_ctx *c, int32_t S, const double *grades_sb, int32_t n_modes, double price,
+                            const double *recovery, int32_t n_recovery, const double *proc_cost, int32_t n_proc_cost,
+                            const double *sigma_st) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (S < 1 || !grades_sb) return fail(PP_ERR_INVALID_ARGS, "need n_scenarios >= 1 and a grade matrix");
+    if (n_modes < 1 || !recovery || n_recovery < 1 || !proc_cost || n_proc_cost < 1)
+        return fail(PP_ERR_INVALID_ARGS, "need at least one operating mode with recovery and processing cost");
+    const int B = c->B;
+    DevBuf tmp, par;
+    TRY(tmp.ensure(sizeof(double) * (size_t)S * B));
+    TRY(par.ensure(sizeof(double) * (size_t)(n_recovery + n_proc_cost)));
+    const int rc = set_scenarios_common(c, S, sigma_st, [&](int Sp) {
+        cudaError_t e = dev_upload(c, tmp.ptr, grades_sb, sizeof(double) * (size_t)S * B);
+        if (e == cudaSuccess) e = dev_upload(c, par.ptr, recovery, sizeof(double) * n_recovery);
+        if (e == cudaSuccess)
+            e = dev_upload(c, par.as<double>() + n_recovery, proc_cost, sizeof(double) * n_proc_cost);
+        if (e == cudaSuccess) {
+            k_scen_from_grades<<<(B + 127) / 128, 128, 0, c->stream>>>(
+                tmp.as<double>(), S, B, Sp, c->mass.as<double>(), price, par.as<double>(), n_recovery,
+                par.as<double>() + n_recovery, n_proc_cost, n_modes, c->vmax.as<double>(), c->unit_mean.as<double>());
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        return e;
+    });
+    tmp.release();
+    par.release();
+    return rc;
+}
+
+int pp_get_scenario_values(pp_ctx *c, double *vmax_sb_out) {
+    if (!c || !c->have_scen) return fail(PP_ERR_STATE, "pp_set_scenarios first");
+    if (!vmax_sb_out) return fail(PP_ERR_INVALID_ARGS, "vmax_sb_out is NULL");
+    TRY(use_device(c));
+    const size_t n = (size_t)c->S * c->B;
+    DevBuf tmp;
+    TRY(tmp.ensure(sizeof(double) * n));
+    k_scen_to_sb<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->vmax.as<double>(), c->S, c->B, c->Sp,
+                                                                    tmp.as<double>());
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(vmax_sb_out, tmp.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    tmp.release();
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "pp_get_scenario_values: %s", cudaGetErrorString(e));
     return PP_OK;
 }
 

@@ -108,24 +108,41 @@ class Engine:
                                       ptr(bm.dist_intrusion), w1, w2, w3, diam))
 
     def set_scenarios(self, tables: ScenarioTables):
+        """Bind a scenario set: a host value table vmax[S][B], or -- vmax None -- grades[S][B] from
+        which the device builds it (pp_set_scenarios_grades)."""
         bm = self._need_bm()
-        vmax = np.ascontiguousarray(tables.vmax, dtype=np.float64)
-        if vmax.ndim != 2 or vmax.shape[1] != bm.n_blocks:
-            raise ShapeMismatch("scenario value table does not match the instance")
+        S = tables.n_scenarios
         sig = None
         if tables.sigma is not None:
             sig = np.ascontiguousarray(tables.sigma, dtype=np.float64)
-            if sig.shape != (vmax.shape[0], bm.n_periods):
+            if sig.shape != (S, bm.n_periods):
                 raise ShapeMismatch("sigma must be [S][T]")
-        check(self.lib.pp_set_scenarios(self._h, vmax.shape[0], ptr(vmax), ptr(sig)))
-        self.n_scenarios = int(vmax.shape[0])
+        if tables.vmax is not None:
+            vmax = np.ascontiguousarray(tables.vmax, dtype=np.float64)
+            if vmax.ndim != 2 or vmax.shape[1] != bm.n_blocks:
+                raise ShapeMismatch("scenario value table does not match the instance")
+            check(self.lib.pp_set_scenarios(self._h, S, ptr(vmax), ptr(sig)))
+        else:
+            g = np.ascontiguousarray(tables.grades, dtype=np.float64)
+            if g.ndim != 2 or g.shape[1] != bm.n_blocks:
+                raise ShapeMismatch("scenario grades do not match the instance")
+            rec = np.ascontiguousarray(bm.recovery_by_mode, dtype=np.float64)
+            pc = np.ascontiguousarray(bm.processing_cost_by_mode, dtype=np.float64)
+            check(self.lib.pp_set_scenarios_grades(self._h, S, ptr(g), int(bm.n_modes), float(bm.price), ptr(rec),
+                                                   rec.size, ptr(pc), pc.size, ptr(sig)))
+        self.n_scenarios = int(S)
         self.has_sigma = sig is not None
         self._tables = tables
 
     def scenario_table(self) -> np.ndarray:
-        """vmax[S][B] of the bound scenario set (scenario_mode_values, single mode)."""
+        """vmax[S][B] of the bound scenario set (scenario_mode_values reduced over modes); read back
+        from the device when the set was ingested from grades."""
         if getattr(self, "_tables", None) is None:
             raise InvalidArgs("set_scenarios first")
+        if self._tables.vmax is None:
+            out = np.empty((self.n_scenarios, self._need_bm().n_blocks), np.float64)
+            check(self.lib.pp_get_scenario_values(self._h, ptr(out)))
+            self._tables.vmax = out
         return self._tables.vmax
 
     def _need_bm(self) -> BlockModel:

@@ -602,10 +602,11 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         # the next chunk starts at the following block: the decisions are the sequential ones.
         b0 = 0
         k = _POLISH_CHUNK
+        a32 = a.astype(np.int32)  # the int32 copy pp_npv_moves reads, kept in step with `a`
         while b0 < B:
             b1 = min(B, b0 + k)
             rows, nt, cnt = options_chunk(b0, b1)
-            vals = eng.npv_moves(a, rows + b0, nt, use_sigma=use_sigma).tolist() if nt.size else []
+            vals = eng.npv_moves(a32, rows + b0, nt, use_sigma=use_sigma).tolist() if nt.size else []
             nt = nt.tolist()
             pos = 0
             nxt = b1
@@ -620,6 +621,7 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
                 pos += c
                 if best_t != orig:
                     a[b] = best_t
+                    a32[b] = best_t
                     improved = True
                     cur_val = best_val
                     if orig != UN:

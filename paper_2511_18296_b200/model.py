@@ -239,30 +239,44 @@ def scenario_values(bm: BlockModel, grades: np.ndarray | None, use_stored: bool 
 
 @dataclass
 class ScenarioTables:
-    """Per-scenario-set tables: vmax[S][B] (reference layout) and sigma[S][T] or None."""
+    """Per-scenario-set tables: vmax[S][B] (reference layout) and sigma[S][T] or None.
 
-    vmax: np.ndarray
+    vmax may be None when grades[S][B] is given: the engine then builds the value table on the
+    device (pp_set_scenarios_grades, scenario_mode_values evaluate.py:116-124) and the host copy is
+    fetched back only if someone asks for it (Engine.scenario_table)."""
+
+    vmax: np.ndarray | None
     sigma: np.ndarray | None
     grades: np.ndarray | None = None  # [S][B], optional (lns_repair's mean grade, hybrid.py:214)
 
     def __post_init__(self):
-        self.vmax = np.ascontiguousarray(self.vmax, dtype=np.float64)
+        if self.vmax is None and self.grades is None:
+            raise InvalidArgs("a scenario table needs vmax or grades")
+        if self.vmax is not None:
+            self.vmax = np.ascontiguousarray(self.vmax, dtype=np.float64)
         if self.sigma is not None:
             self.sigma = np.ascontiguousarray(self.sigma, dtype=np.float64)
-            if self.sigma.shape[0] != self.vmax.shape[0]:
+            if self.sigma.shape[0] != self.n_scenarios:
                 raise ShapeMismatch("sigma scenario count differs from the value table")
 
     @property
     def n_scenarios(self) -> int:
-        return int(self.vmax.shape[0])
+        return int((self.vmax if self.vmax is not None else np.asarray(self.grades)).shape[0])
 
     @classmethod
     def from_reference(cls, bm: BlockModel, scenarios, sigma) -> "ScenarioTables":
-        """From a `pitplan.scenarios.ScenarioSet` and `UncertaintyFactors | None`."""
+        """From a `pitplan.scenarios.ScenarioSet` and `UncertaintyFactors | None`: the stored
+        per-mode values (use_stored_values) are reduced on the host; sampled grades go to the
+        device as they are."""
         use_stored = bool(getattr(scenarios, "meta", {}).get("use_stored_values"))
-        vmax = scenario_values(bm, None if use_stored else scenarios.grades, use_stored)
         sig = None if sigma is None else np.asarray(sigma.sigma, dtype=np.float64)
-        return cls(vmax=vmax, sigma=sig, grades=getattr(scenarios, "grades", None))
+        grades = getattr(scenarios, "grades", None)
+        if use_stored:
+            return cls(vmax=scenario_values(bm, None, True), sigma=sig, grades=grades)
+        g = np.ascontiguousarray(grades, dtype=np.float64)
+        if g.ndim != 2 or g.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("scenario set does not match instance block count")
+        return cls(vmax=None, sigma=sig, grades=g)
 
 
 @dataclass

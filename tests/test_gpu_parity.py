@@ -853,3 +853,63 @@ def test_realism_key_on_device(oracle_lib):
     r = eng.eval_candidates(cand, None, realism=True)
     assert r["realism"] == _realism_ref(cand, r["best_t"], sp)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_npv_moves_incremental_base_sequence(name):
+    """pp_npv_moves keeps the base schedule's per-(scenario, period) greedy structure and, when the
+    base changes by a few blocks (as in polish_schedule), re-solves only the changed periods: a
+    sequence of drifting bases with reassign / unmine / mine variants -- including empty periods,
+    blocks of non-positive density and large batches -- equals pp_npv_relaxed of every variant."""
+    c = config(name)
+    bm = c["bm"]
+    vmax = c["vmax"].copy()
+    vmax[:, ::13] = -np.abs(vmax[:, ::13])  # non-positive densities in every scenario
+    eng = Engine.from_tables(bm, ScenarioTables(vmax, c["sigma"]))
+    rng = np.random.default_rng(21)
+    a = c["greedy"].copy().astype(np.int32)
+    a[a == 3] = -1  # an empty period
+    B, T = bm.n_blocks, bm.n_periods
+    for step in range(8):
+        m = int(rng.choice([3, 40, 700]))
+        blocks = rng.integers(0, B, m).astype(np.int32)
+        periods = rng.integers(-1, T, m).astype(np.int32)
+        got = eng.npv_moves(a, blocks, periods)
+        batch = np.repeat(a[None, :], m, axis=0)
+        batch[np.arange(m), blocks] = periods
+        ref = np.concatenate([eng.npv_relaxed(batch[i:i + 256]) for i in range(0, m, 256)])
+        assert same(got, ref), (name, step)
+        # drift the base like accepted polish moves: one to three blocks per step, sometimes many
+        k = 1 + step % 3 if step != 5 else B // 3
+        idx = rng.integers(0, B, k)
+        a[idx] = rng.integers(-1, T, k)
+    eng.close()
+
+
+@pytest.mark.parametrize("name,modes", [("C1", 1), ("C1", 3), ("C2", 1)])
+def test_device_ingestion_from_grades(name, modes):
+    """pp_set_scenarios_grades builds the value table on the device from grades[S][B]
+    (scenario_mode_values, evaluate.py:116-124, max over modes) bit-identical to the host table, and
+    an engine fed grades evaluates exactly like one fed the host table."""
+    import dataclasses
+
+    from paper_2511_18296_b200.model import scenario_values
+
+    c = config(name)
+    bm = c["bm"]
+    if modes > 1:
+        bm = dataclasses.replace(bm, n_modes=modes, recovery_by_mode=(0.85, 0.9, 0.7),
+                                 processing_cost_by_mode=(1.0, 1.6, 0.4))
+    host = scenario_values(bm, c["grades"])
+    e_dev = Engine.from_tables(bm, ScenarioTables(None, c["sigma"], grades=c["grades"]), c["assign"])
+    assert same(e_dev.scenario_table(), host)
+    e_host = Engine.from_tables(bm, ScenarioTables(host, c["sigma"]), c["assign"])
+    for kw in (dict(net=True, stats=True), dict(net=False, trace=True)):
+        a = e_dev.eval_candidates(c["cand"], None, **kw)
+        b = e_host.eval_candidates(c["cand"], None, **kw)
+        assert a["best"] == b["best"]
+        for k in ("best_t", "best_val", "exp_delta", "cvar", "trace_val"):
+            if k in a:
+                assert same(a[k], b[k]), k
+    e_dev.close()
+    e_host.close()
