@@ -84,60 +84,6 @@ constexpr int CPW = 4;  // candidates per warp
 constexpr int WV_THREADS = 256;  // k_eval_warp CTA: 8 warps (128 measured the same)
 constexpr int WV_MINB = 4;       // resident CTAs per SM (64 registers per thread)
 
-// order-preserving map of a double onto u64 (NaN after +inf, as np.sort places it)
-__device__ __forceinline__ unsigned long long f64_key(double v) {
-    const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-    if (v != v) return ~0ull - 1ull;
-    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double key_f64(unsigned long long k) {
-    return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
-}
-__device__ __forceinline__ void ce_u64(unsigned long long &a, unsigned long long &b) {
-    const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
-    a = lo;
-    b = hi;
-}
-// The k (<= 32) smallest of the warp's keys (lane l holds elements l + 32 r, r < npl <= 8; the
-// rest are padding), ascending: a per-lane sorting network, then k rounds of a warp-wide minimum
-// over the lane heads (redux.sync on the high word; the low word only on a tie) in which the
-// winning lane pops its head (its sorted tail waits in scr, 32 x npl u64 of the warp's scratch).
-// Returns the r-th smallest on lane r < k.
-__device__ __forceinline__ double warp_k_smallest(unsigned long long (&k8)[8], int k, unsigned long long *scr,
-                                                  int npl) {
-    constexpr unsigned FULL = 0xffffffffu;
-    ce_u64(k8[0], k8[1]); ce_u64(k8[2], k8[3]); ce_u64(k8[4], k8[5]); ce_u64(k8[6], k8[7]);
-    ce_u64(k8[0], k8[2]); ce_u64(k8[1], k8[3]); ce_u64(k8[4], k8[6]); ce_u64(k8[5], k8[7]);
-    ce_u64(k8[1], k8[2]); ce_u64(k8[5], k8[6]);
-    ce_u64(k8[0], k8[4]); ce_u64(k8[1], k8[5]); ce_u64(k8[2], k8[6]); ce_u64(k8[3], k8[7]);
-    ce_u64(k8[2], k8[4]); ce_u64(k8[3], k8[5]);
-    ce_u64(k8[1], k8[2]); ce_u64(k8[3], k8[4]); ce_u64(k8[5], k8[6]);
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int i = 2; i < 8; i++)
-        if (i < npl) scr[i * 32 + lane] = k8[i];
-    unsigned long long h0 = k8[0], h1 = k8[1], mine = ~0ull;
-    int ptr = 2;
-    for (int r = 0; r < k; r++) {
-        const unsigned hi = (unsigned)(h0 >> 32), lo = (unsigned)h0;
-        const unsigned mhi = __reduce_min_sync(FULL, hi);
-        unsigned who = __ballot_sync(FULL, hi == mhi);
-        if (__popc(who) > 1) {  // warp-uniform
-            const unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
-            who = __ballot_sync(FULL, hi == mhi && lo == mlo);
-        }
-        const int w = __ffs(who) - 1;
-        const unsigned wlo = __shfl_sync(FULL, lo, w);
-        if (lane == r) mine = ((unsigned long long)mhi << 32) | wlo;
-        if (lane == w) {
-            h0 = h1;
-            h1 = ptr < npl ? scr[ptr * 32 + lane] : ~0ull;
-            ptr++;
-        }
-    }
-    return key_f64(mine);
-}
-
 __device__ __forceinline__ int nth_bit(unsigned m, int k) {  // index of the k-th (0-based) set bit
     for (; k > 0; k--) m &= m - 1;
     return __ffs(m) - 1;

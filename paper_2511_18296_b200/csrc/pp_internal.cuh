@@ -238,6 +238,135 @@ struct TopK<0> {
     __device__ __forceinline__ double mean(int) const { return 0.0; }
 };
 
+// order-preserving map of a double onto u64 (NaN after +inf, as np.sort places it)
+__device__ __forceinline__ unsigned long long f64_key(double v) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    if (v != v) return ~0ull - 1ull;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_f64(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
+}
+__device__ __forceinline__ void ce_u64(unsigned long long &a, unsigned long long &b) {
+    const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+// The k (<= 32) smallest of the warp's keys (lane l holds elements l + 32 r, r < npl <= 8; the
+// rest are padding), ascending: a per-lane sorting network, then k rounds of a warp-wide minimum
+// over the lane heads (redux.sync on the high word; the low word only on a tie) in which the
+// winning lane pops its head (its sorted tail waits in scr, 32 x npl u64 of the warp's scratch).
+// Returns the r-th smallest on lane r < k.
+__device__ __forceinline__ double warp_k_smallest(unsigned long long (&k8)[8], int k, unsigned long long *scr,
+                                                  int npl) {
+    constexpr unsigned FULL = 0xffffffffu;
+    ce_u64(k8[0], k8[1]); ce_u64(k8[2], k8[3]); ce_u64(k8[4], k8[5]); ce_u64(k8[6], k8[7]);
+    ce_u64(k8[0], k8[2]); ce_u64(k8[1], k8[3]); ce_u64(k8[4], k8[6]); ce_u64(k8[5], k8[7]);
+    ce_u64(k8[1], k8[2]); ce_u64(k8[5], k8[6]);
+    ce_u64(k8[0], k8[4]); ce_u64(k8[1], k8[5]); ce_u64(k8[2], k8[6]); ce_u64(k8[3], k8[7]);
+    ce_u64(k8[2], k8[4]); ce_u64(k8[3], k8[5]);
+    ce_u64(k8[1], k8[2]); ce_u64(k8[3], k8[4]); ce_u64(k8[5], k8[6]);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 2; i < 8; i++)
+        if (i < npl) scr[i * 32 + lane] = k8[i];
+    unsigned long long h0 = k8[0], h1 = k8[1], mine = ~0ull;
+    int ptr = 2;
+    for (int r = 0; r < k; r++) {
+        const unsigned hi = (unsigned)(h0 >> 32), lo = (unsigned)h0;
+        const unsigned mhi = __reduce_min_sync(FULL, hi);
+        unsigned who = __ballot_sync(FULL, hi == mhi);
+        if (__popc(who) > 1) {  // warp-uniform
+            const unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
+            who = __ballot_sync(FULL, hi == mhi && lo == mlo);
+        }
+        const int w = __ffs(who) - 1;
+        const unsigned wlo = __shfl_sync(FULL, lo, w);
+        if (lane == r) mine = ((unsigned long long)mhi << 32) | wlo;
+        if (lane == w) {
+            h0 = h1;
+            h1 = ptr < npl ? scr[ptr * 32 + lane] : ~0ull;
+            ptr++;
+        }
+    }
+    return key_f64(mine);
+}
+
+
+// numpy pairwise mean over a warp's scratch vb[0..S) with the scenario plan P (<= kMaxLeaves leaves
+// of <= 128 elements): eight lanes per leaf (accumulator j = lane & 7, xor butterfly = numpy's
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), the leaf's tail in order, then lane 0 folds the leaves in
+// the recursion's post-order.  lv: >= kMaxLeaves doubles of warp scratch.  Result on lane 0.
+__device__ __forceinline__ double warp_pairwise_mean(const double *vb, const int *P, double *lv) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int nleaf = __ldg(P + 1);
+    for (int l0 = 0; l0 < nleaf; l0 += 4) {
+        const int l = l0 + (lane >> 3), sub = lane & 7;
+        const bool act = l < nleaf;
+        const int ls = act ? __ldg(P + 2 + l) : 0, len = act ? __ldg(P + 2 + kMaxLeaves + l) : 0;
+        const int nm = len >> 3;
+        double acc = 0.0;
+        if (nm > 0) {
+            acc = vb[ls + sub];
+            for (int u = 1; u < nm; u++) acc = f64_add(acc, vb[ls + 8 * u + sub]);
+        }
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
+        acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
+        if (act && sub == 0) {
+            double r = len >= 8 ? acc : -0.0;
+            for (int i = len - (len & 7); i < len; i++) r = f64_add(r, vb[ls + i]);
+            lv[l] = r;
+        }
+    }
+    __syncwarp();
+    double res = 0.0;
+    if (lane == 0) {
+        double stk[8];
+        int sp_ = 0;
+        for (int l = 0; l < nleaf; l++) {  // numpy's recursion, post-order
+            stk[sp_++] = lv[l];
+            const int nadd = __ldg(P + 2 + 2 * kMaxLeaves + l);
+            for (int a = 0; a < nadd; a++) {
+                const double rhs = stk[--sp_];
+                const double lhs = stk[--sp_];
+                stk[sp_++] = f64_add(lhs, rhs);
+            }
+        }
+        res = f64_div(f64_add(0.0, stk[0]), (double)__ldg(P));
+    }
+    return res;
+}
+
+// CVaR10 (saa.py:157-164) of a warp's values vb[0..S) (S <= 32 * npl, npl <= 8): the mean of the
+// kq <= 32 smallest in ascending order, numpy pairwise (8 accumulators, butterfly, tail).  `scr`:
+// 32 * npl u64 of warp scratch (may alias nothing the caller still needs).  Result on every lane.
+__device__ __forceinline__ double warp_cvar(const double *vb, int S, int kq, unsigned long long *scr, int npl) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    unsigned long long k8[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const int s_ = lane + 32 * r;
+        k8[r] = (r < npl && s_ < S) ? f64_key(vb[s_]) : ~0ull;
+    }
+    __syncwarp();
+    const double kv = warp_k_smallest(k8, kq, scr, npl);
+    const int kn = kq >> 3;
+    double cacc = (lane < 8 && kn > 0) ? kv : 0.0;  // lane l < 8: ranks l, 8 + l, ...
+    for (int u = 1; u < kn; u++) {
+        const double x = __shfl_sync(FULL, kv, (8 * u + lane) & 31);
+        if (lane < 8) cacc = f64_add(cacc, x);
+    }
+    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 1));
+    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 2));
+    cacc = f64_add(cacc, __shfl_xor_sync(FULL, cacc, 4));
+    double rc = kq >= 8 ? cacc : -0.0;
+    for (int i = kq - (kq & 7); i < kq; i++) rc = f64_add(rc, __shfl_sync(FULL, kv, i));
+    return f64_div(f64_add(0.0, rc), (double)kq);
+}
+
 // selection order of evaluate.py:404-409: value desc, then block asc, then period asc
 struct Best {
     double v;

@@ -913,3 +913,32 @@ def test_device_ingestion_from_grades(name, modes):
                 assert same(a[k], b[k]), k
     e_dev.close()
     e_host.close()
+
+
+@pytest.mark.parametrize("T,S", [(3, 1), (9, 7), (15, 20), (6, 64), (12, 129), (5, 256), (7, 300)])
+def test_explicit_moves_shapes_against_oracle(oracle_lib, T, S):
+    """k_moves_warp (a warp per move, 128-bit scenario-row loads; S <= 256) and its fallback
+    k_eval_moves (S = 300) against the oracle: reassign / unmine and swaps, both flags, s = None and
+    s = k, statistics and per-scenario deltas; the selected move (lowest index on ties)."""
+    bm, vmax, sigma = _rand_instance(11 + T, n=(10, 8, 5), T=T, S=S, cf=0.5)
+    from paper_2511_18296_b200 import synth
+
+    rng = np.random.default_rng(T * 100 + S)
+    assign = synth.full_greedy(bm)
+    eng = Engine.from_tables(bm, ScenarioTables(vmax, sigma), assign)
+    o = oracle_lib.Oracle(bm, vmax, sigma)
+    M = 3000
+    b = rng.integers(0, bm.n_blocks, M).astype(np.int32)
+    t = rng.integers(-1, bm.n_periods, M).astype(np.int32)
+    keys = ("feasible", "delta", "exp_delta", "cvar", "scen_delta")
+    for net, s in ((False, None), (True, S - 1)):
+        got = eng.eval_moves(b, t, "reassign", s, net=net, stats=True, scen=True)
+        ref = o.eval_moves(assign, b, t, "reassign", s, net=net, stats=True, scen=True)
+        _same_res(got, ref, keys)
+        assert got["best"] == ref["best"]
+    b2 = rng.integers(0, bm.n_blocks, M).astype(np.int32)
+    got = eng.eval_moves(b, b2, "swap", None, net=True, stats=True, scen=True)
+    ref = o.eval_moves(assign, b, b2, "swap", None, net=True, stats=True, scen=True)
+    _same_res(got, ref, keys)
+    assert got["best"] == ref["best"]
+    eng.close()
