@@ -619,6 +619,109 @@ def run_gpu(args):
     return 0
 
 
+def run_moves(args):
+    """Explicit moves (north_star (1)): M reassign (b, t_new) pairs or M swaps
+    (b1, b2) per step at the config's scale, evaluated by k_moves_warp (a warp per move) with the
+    per-scenario statistics; one GPU.  Device-timed (graph: period masses + the moves kernel, L2
+    flushed), e2e through Engine.eval_moves with host buffers, and the oracle port on all host
+    cores for the same moves."""
+    import torch
+
+    from oracle import oracle
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.engine import Engine
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    c = build_inputs(args.config)
+    bm, T, S = c["bm"], c["T"], c["S"]
+    M = args.moves
+    rng = synth.substream(3, "moves", args.workload)
+    a = rng.integers(0, bm.n_blocks, M).astype(np.int32)
+    b = (rng.integers(-1, T, M) if args.workload == "reassign" else rng.integers(0, bm.n_blocks, M)).astype(np.int32)
+    eng = Engine.from_tables(bm, c["tables"], c["assign"])
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assign_d = torch.from_numpy(c["assign"].astype(np.int32)).to(dev)
+    a_d, b_d = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    out = {"feasible": torch.empty(M, dtype=torch.uint8, device=dev),
+           "delta": torch.empty(M, dtype=torch.float64, device=dev),
+           "exp_delta": torch.empty(M, dtype=torch.float64, device=dev),
+           "cvar": torch.empty(M, dtype=torch.float64, device=dev),
+           "global": torch.empty(2, dtype=torch.float64, device=dev)}
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def step(sp):
+        eng.set_schedule_device(assign_d, stream=sp, borrow=True)
+        eng.eval_moves_device(a_d, b_d, out, args.workload, None, net=True, stream=sp)
+
+    for _ in range(max(args.warmup, 3)):
+        step(stream.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step(torch.cuda.current_stream().cuda_stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(0) as clocks:
+        for i in range(args.steps):
+            flush.fill_(i)
+            ev[i][0].record(stream)
+            g.replay()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    t_ms = float(np.mean([x.elapsed_time(y) for x, y in ev]))
+    # e2e: host arrays through the C ABI (upload schedule + moves, kernels, download of all outputs)
+    e2e = []
+    res = None
+    for i in range(args.warmup + min(args.steps, 100)):
+        flush.fill_(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.set_schedule(c["assign"])
+        res = eng.eval_moves(a, b, args.workload, None, net=True, stats=True)
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
+    e2e_t = float(np.median(e2e))
+    ref = None
+    if not args.no_cpu_baseline:
+        oracle.build()
+        o = oracle.Oracle(bm, c["tables"].vmax, c["tables"].sigma)
+        n_cpu = min(M, 50000)
+        t0 = time.perf_counter()
+        r = o.eval_moves(c["assign"], a[:n_cpu], b[:n_cpu], args.workload, None, net=True, stats=True)
+        t_cpu = time.perf_counter() - t0
+        ref = {"value": n_cpu * S / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{n_cpu} of {M} moves x {S} scenarios, oracle/oracle.c eval_moves, one core"}
+        assert np.array_equal(r["feasible"], res["feasible"][:n_cpu]) and np.array_equal(
+            r["delta"], res["delta"][:n_cpu]), "oracle parity on the bench moves"
+    deg = 2.0 * bm.n_edges / bm.n_blocks
+    nblk = 1 if args.workload == "reassign" else 2
+    survey = M * nblk * (80 + 8 * deg) + 8 * M * nblk * S
+    hbm, peak_kind = _peaks()
+    print(json.dumps({
+        "metric": METRIC, "workload": f"explicit {args.workload} moves", "value": M * S / (t_ms * 1e-3),
+        "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {M} explicit {args.workload} moves x {S} scenarios per step, "
+                               "net mining cost, per-move delta + expected delta + CVaR10, argmax",
+                   "blocks": bm.n_blocks, "periods": T, "scenarios": S, "moves_per_step": M,
+                   "l2": "256 MiB flush write between timed GPU steps"},
+        "feasible_moves": int(res["feasible"].sum()),
+        "roofline": {"bound": "hbm", "achieved": survey / (t_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": survey / (t_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                     "algorithmic_basis": "SURVEY §8(d) per move and block: 80 + 8*deg + 8*S (f64 values); "
+                                          "step time (period masses + moves kernel)",
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+        "e2e": {"value": M * S / e2e_t, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
+                "h2d_bytes_per_step": int(c["assign"].size * 4 + 8 * M),
+                "d2h_bytes_per_step": int(M * (1 + 8 + 8 + 8) + 16),
+                "api": "Engine.set_schedule + Engine.eval_moves (PP_MEM_HOST)"},
+        "gpu_launches": 2 * args.steps, "clocks": clocks.summary(), "cpu_baseline": ref,
+        "best_move": res["best"]}))
+    eng.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -632,9 +735,15 @@ def main():
     ap.add_argument("--no-python-ref", action="store_true", help="skip timing pitplan itself (baseline/_ref)")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram bytes per k_eval_warp launch from the committed ncu capture")
+    ap.add_argument("--workload", default="candidates", choices=["candidates", "reassign", "swap"],
+                    help="candidates: the headline evaluate_candidates_parallel batch; reassign / swap: "
+                         "explicit moves (one GPU, a separate line)")
+    ap.add_argument("--moves", type=int, default=250000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload != "candidates":
+        return run_moves(args)
     return run_gpu(args)
 
 

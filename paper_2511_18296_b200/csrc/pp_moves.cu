@@ -163,23 +163,24 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_moves(const MoveParams p) {
 }
 
 // ------------------------------------------------------------------------------------
-// k_moves_warp: explicit moves, one warp per move (north_star (1)).
-//   feasibility  lane k = neighbour slot k of the padded 128-byte neighbour row: the window of
-//                hybrid.py:348-355 by redux.sync max / min (a swap sees its partner at its new
-//                period), capacity of the destination periods (hybrid.py:370, 396-399)
-//   value        the kernel value delta (the parity key, evaluate.py:379-382 at both periods)
-//   statistics   lanes own scenarios two at a time: the scenario-major value rows are read with
-//                128-bit loads (double2), sigma[S][T] and the T-tables sit in shared memory; the
-//                per-scenario deltas go to the warp's slice, their numpy pairwise mean (8 lanes
-//                per leaf) and CVaR10 (warp k-smallest) follow
-//   argmax       warp -> CTA -> grid (move index order on ties)
-// For S <= 256 (CVaR k <= 25) and blocks of <= 32 neighbours; k_eval_moves covers the rest.
+// k_moves_warp: explicit moves (north_star (1)), persistent warps.
+//   feasibility  a lane per move, 32 moves per warp step (coalesced move ids): the window of
+//                hybrid.py:348-355 over the block's adjacency (a swap sees its partner at its new
+//                period), capacity of the destination periods (hybrid.py:370, 396-399), and the
+//                kernel-value delta (the parity key, evaluate.py:379-382 at both periods)
+//   statistics   then a warp per FEASIBLE move (the step's ballot, in lane order): lanes own
+//                scenarios two at a time, the scenario-major value rows read with 128-bit loads
+//                (double2), sigma[S][T] and the T-tables in shared memory; the per-scenario deltas go
+//                to the warp's slice, their numpy pairwise mean (8 lanes per leaf) and CVaR10 (warp
+//                k-smallest) follow.  Infeasible moves (most of a random batch) cost one lane.
+//   argmax       lane -> warp -> CTA -> grid (move index order on ties), one atomic per CTA
+// For S <= 256 (CVaR k <= 25); k_eval_moves covers larger scenario sets.
 // ------------------------------------------------------------------------------------
 constexpr int MW_THREADS = 256;
 constexpr int MW_NW = MW_THREADS / 32;
 
 template <bool STATS>
-__global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p, const int32_t *__restrict__ nbr) {
+__global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
     extern __shared__ __align__(16) unsigned char mw_dyn[];
     __shared__ Best s_red[MW_NW];
     __shared__ double s_tab[3][32];  // disc, cap, sig_row
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p, c
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int T = p.T, S = p.S, Sp = p.Sp;
     const int P2 = S <= 32 ? 32 : S <= 64 ? 64 : S <= 128 ? 128 : 256;
-    double *s_sig = reinterpret_cast<double *>(mw_dyn);                          // [S][T]
+    double *s_sig = reinterpret_cast<double *>(mw_dyn);                                   // [S][T]
     double *vb = s_sig + (size_t)(STATS ? S * T : 0) + (size_t)warp * (P2 + kMaxLeaves);  // warp slice
     double *lv = vb + P2;
     if (threadIdx.x < T) {
@@ -198,138 +199,132 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p, c
     if (STATS)
         for (int e = threadIdx.x; e < S * T; e += MW_THREADS) s_sig[e] = __ldg(p.sigma + e);
     __syncthreads();
-    const int i = blockIdx.x * MW_NW + warp;
-    bool ok = false;
-    double dl = -kInf;
-    int b1 = -1, b2 = -1, t1 = -1, t2 = -1;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the period masses (pm) may be in flight
-    if (i < p.M) {
-        const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
-        if (p.kind == PP_MOVE_REASSIGN) {
-            if (x >= 0 && x < p.B && y >= -1 && y < p.T) {
-                b1 = x;
-                t1 = p.assign[b1];
-                t2 = y;
-                const int nb = __ldg(nbr + (size_t)b1 * 32 + lane);
-                const bool has = nb >= 0, succ = has && (nb & (1 << 30));
-                const int tn = has ? p.assign[nb & ((1 << 30) - 1)] : 0;
-                if (t2 == t1) {
-                    ok = false;
-                } else if (t2 < 0) {  // unmine: allowed iff no mined successor
-                    ok = !__any_sync(FULL, succ && tn >= 0);
-                } else {
-                    const bool bad = (has && !succ && (tn < 0 || tn > t2)) || (succ && tn >= 0 && tn < t2);
-                    ok = !__any_sync(FULL, bad);
-                    if (ok) {
-                        const double load = f64_add(__ldcg(p.pm + t2), __ldg(&p.rows[b1].mass));
-                        if (load > s_tab[1][t2]) ok = false;
-                    }
-                }
-            }
-        } else if (x >= 0 && x < p.B && y >= 0 && y < p.B && x != y) {
-            b1 = x;
-            b2 = y;
-            t1 = p.assign[b1];
-            t2 = p.assign[b2];
-            if (t1 >= 0 && t2 >= 0 && t1 != t2) {
-                const double m1 = __ldg(&p.rows[b1].mass), m2 = __ldg(&p.rows[b2].mass);
-                const double l1 = f64_add(f64_sub(__ldcg(p.pm + t1), m1), m2);
-                const double l2 = f64_add(f64_sub(__ldcg(p.pm + t2), m2), m1);
-                if (!(l1 > s_tab[1][t1]) && !(l2 > s_tab[1][t2])) {
-                    // windows after the swap: b1 at t2 sees b2 at t1 and vice versa (hybrid.py:400-403)
-                    bool bad = false;
-#pragma unroll
-                    for (int side = 0; side < 2; side++) {
-                        // bb moves to tt; its partner ob moves to ot (the swap's other period)
-                        const int bb = side ? b2 : b1, ob = side ? b1 : b2, ot = side ? t2 : t1;
-                        const int tt = side ? t1 : t2;
-                        const int nb = __ldg(nbr + (size_t)bb * 32 + lane);
-                        const bool has = nb >= 0, succ = has && (nb & (1 << 30));
-                        const int id = nb & ((1 << 30) - 1);
-                        const int tn = has ? (id == ob ? ot : p.assign[id]) : 0;
-                        bad |= (has && !succ && (tn < 0 || tn > tt)) || (succ && tn >= 0 && tn < tt);
-                    }
-                    ok = !__any_sync(FULL, bad);
-                }
-            }
-        }
-        if (ok && lane == 0) {  // the kernel-value delta (parity key)
-            const BlockRow r1 = p.rows[b1];
+    const bool net = p.flags & PP_NET_MINING_COST;
+    Best mine{-kInf, INT_MAX, INT_MAX};
+    for (int base = (blockIdx.x * MW_NW + warp) * 32; base < p.M; base += gridDim.x * MW_NW * 32) {
+        const int i = base + lane;
+        bool ok = false;
+        double dl = -kInf;
+        int b1 = 0, b2 = -1, t1 = -1, t2 = -1;
+        if (i < p.M) {
+            const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
             if (p.kind == PP_MOVE_REASSIGN) {
-                const double vn = (t2 >= 0) ? kernel_value(p, r1, b1, t2) : 0.0;
-                const double vo = (t1 >= 0) ? kernel_value(p, r1, b1, t1) : 0.0;
-                dl = f64_sub(vn, vo);
-            } else {
-                const BlockRow r2 = p.rows[b2];
-                const double v12 = kernel_value(p, r1, b1, t2), v11 = kernel_value(p, r1, b1, t1);
-                const double v21 = kernel_value(p, r2, b2, t1), v22 = kernel_value(p, r2, b2, t2);
-                dl = f64_add(f64_sub(v12, v11), f64_sub(v21, v22));
-            }
-            p.feas[i] = 1;
-            p.delta[i] = dl;
-        } else if (lane == 0) {
-            p.feas[i] = 0;
-            p.delta[i] = -kInf;
-        }
-        if (STATS) {
-            if (ok) {
-                // per-scenario deltas: lane l owns scenarios 2l, 2l+1 (+64 r); one 128-bit load per
-                // row and lane
-                const bool net = p.flags & PP_NET_MINING_COST;
-                auto sval = [&](double x_, int t, int s, double sp, double dc) {
-                    return f64_sub(f64_mul(f64_mul(f64_mul(x_, s_tab[0][t]), s_sig[s * T + t]), sp), dc);
-                };
-                const double sp1 = __ldg(&p.rows[b1].spatial);
-                const double sp2 = b2 >= 0 ? __ldg(&p.rows[b2].spatial) : 0.0;
-                const double c11 = (net && t1 >= 0) ? f64_mul(s_tab[0][t1], __ldg(p.cost + (size_t)b1 * T + t1)) : 0.0;
-                const double c12 = (net && t2 >= 0) ? f64_mul(s_tab[0][t2], __ldg(p.cost + (size_t)b1 * T + t2)) : 0.0;
-                const double c21 = (net && b2 >= 0) ? f64_mul(s_tab[0][t1], __ldg(p.cost + (size_t)b2 * T + t1)) : 0.0;
-                const double c22 = (net && b2 >= 0) ? f64_mul(s_tab[0][t2], __ldg(p.cost + (size_t)b2 * T + t2)) : 0.0;
-                for (int s0 = 2 * lane; s0 < S; s0 += 64) {
-                    const double2 w1 = __ldg(reinterpret_cast<const double2 *>(p.vmax + (size_t)b1 * Sp + s0));
-                    double2 w2 = make_double2(0.0, 0.0);
-                    if (p.kind == PP_MOVE_SWAP) w2 = __ldg(reinterpret_cast<const double2 *>(p.vmax + (size_t)b2 * Sp + s0));
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const int s_ = s0 + h;
-                        if (s_ >= S) break;
-                        const double x1 = h ? w1.y : w1.x;
-                        double ds;
-                        if (p.kind == PP_MOVE_REASSIGN) {
-                            ds = (t2 >= 0) ? sval(x1, t2, s_, sp1, c12) : 0.0;
-                            if (t1 >= 0) ds = f64_sub(ds, sval(x1, t1, s_, sp1, c11));
-                        } else {
-                            const double x2 = h ? w2.y : w2.x;
-                            ds = f64_add(f64_sub(sval(x1, t2, s_, sp1, c12), sval(x1, t1, s_, sp1, c11)),
-                                         f64_sub(sval(x2, t1, s_, sp2, c21), sval(x2, t2, s_, sp2, c22)));
+                if (x >= 0 && x < p.B && y >= -1 && y < p.T) {
+                    b1 = x;
+                    const BlockRow r1 = p.rows[b1];
+                    t1 = p.assign[b1];
+                    t2 = y;
+                    const int npred = r1.cnt & 0xffff, nnb = npred + (r1.cnt >> 16);
+                    if (t2 == t1) {
+                        ok = false;
+                    } else if (t2 < 0) {  // unmine: allowed iff no mined successor
+                        ok = true;
+                        for (int k = npred; k < nnb; k++)
+                            if (p.assign[__ldg(p.adj + r1.adj + k)] >= 0) ok = false;
+                    } else {
+                        ok = true;
+                        for (int k = 0; k < nnb; k++) {
+                            const int tn = p.assign[__ldg(p.adj + r1.adj + k)];
+                            if (k < npred) {
+                                if (tn < 0 || tn > t2) ok = false;
+                            } else if (tn >= 0 && tn < t2) {
+                                ok = false;
+                            }
                         }
-                        vb[s_] = ds;
-                        if (p.scen_delta) p.scen_delta[(size_t)i * S + s_] = (float)ds;
+                        if (ok && f64_add(__ldcg(p.pm + t2), r1.mass) > s_tab[1][t2]) ok = false;
+                    }
+                    if (ok) {
+                        const double vn = (t2 >= 0) ? kernel_value(p, r1, b1, t2) : 0.0;
+                        const double vo = (t1 >= 0) ? kernel_value(p, r1, b1, t1) : 0.0;
+                        dl = f64_sub(vn, vo);
                     }
                 }
-                __syncwarp();
-                const double ex = warp_pairwise_mean(vb, p.plan, lv);
-                // the k-smallest scratch reuses the slice (after the mean has read it)
-                const double cv = warp_cvar(vb, S, p.cvar_k, reinterpret_cast<unsigned long long *>(vb), P2 >> 5);
-                if (lane == 0) {
-                    if (p.exp_delta) p.exp_delta[i] = ex;
-                    if (p.cvar) p.cvar[i] = cv;
+            } else if (x >= 0 && x < p.B && y >= 0 && y < p.B && x != y) {
+                b1 = x;
+                b2 = y;
+                const BlockRow r1 = p.rows[b1], r2 = p.rows[b2];
+                t1 = p.assign[b1];
+                t2 = p.assign[b2];
+                if (t1 >= 0 && t2 >= 0 && t1 != t2) {
+                    const double l1 = f64_add(f64_sub(__ldcg(p.pm + t1), r1.mass), r2.mass);
+                    const double l2 = f64_add(f64_sub(__ldcg(p.pm + t2), r2.mass), r1.mass);
+                    if (!(l1 > s_tab[1][t1]) && !(l2 > s_tab[1][t2])) {
+                        int lo1, hi1, lo2, hi2;  // windows after the swap (hybrid.py:400-403)
+                        move_window(p, r1, b2, t1, lo1, hi1);
+                        move_window(p, r2, b1, t2, lo2, hi2);
+                        ok = lo1 != -2 && lo1 <= t2 && t2 <= hi1 && lo2 != -2 && lo2 <= t1 && t1 <= hi2;
+                    }
                 }
-            } else {
-                if (lane == 0) {
-                    if (p.exp_delta) p.exp_delta[i] = -kInf;
-                    if (p.cvar) p.cvar[i] = -kInf;
+                if (ok) {
+                    const double v12 = kernel_value(p, r1, b1, t2), v11 = kernel_value(p, r1, b1, t1);
+                    const double v21 = kernel_value(p, r2, b2, t1), v22 = kernel_value(p, r2, b2, t2);
+                    dl = f64_add(f64_sub(v12, v11), f64_sub(v21, v22));
                 }
-                if (p.scen_delta)
-                    for (int s_ = lane; s_ < S; s_ += 32) p.scen_delta[(size_t)i * S + s_] = -__int_as_float(0x7f800000);
             }
+            p.feas[i] = ok ? 1 : 0;
+            p.delta[i] = dl;
+            if (ok) {
+                const Best cb{dl, i, -1};
+                if (better(cb, mine)) mine = cb;
+            } else if (STATS) {
+                if (p.exp_delta) p.exp_delta[i] = -kInf;
+                if (p.cvar) p.cvar[i] = -kInf;
+                if (p.scen_delta)
+                    for (int s_ = 0; s_ < S; s_++) p.scen_delta[(size_t)i * S + s_] = -__int_as_float(0x7f800000);
+            }
+        }
+        if (!STATS) continue;
+        // statistics of this step's feasible moves, the warp on one move at a time
+        for (unsigned fm = __ballot_sync(FULL, ok); fm; fm &= fm - 1) {
+            const int src = __ffs(fm) - 1;
+            const int mi = base + src;
+            const int c1 = __shfl_sync(FULL, b1, src), c2 = __shfl_sync(FULL, b2, src);
+            const int u1 = __shfl_sync(FULL, t1, src), u2 = __shfl_sync(FULL, t2, src);
+            auto sval = [&](double x_, int t, int s_, double sp, double dc) {
+                return f64_sub(f64_mul(f64_mul(f64_mul(x_, s_tab[0][t]), s_sig[s_ * T + t]), sp), dc);
+            };
+            const double sp1 = __ldg(&p.rows[c1].spatial);
+            const double sp2 = c2 >= 0 ? __ldg(&p.rows[c2].spatial) : 0.0;
+            const double k11 = (net && u1 >= 0) ? f64_mul(s_tab[0][u1], __ldg(p.cost + (size_t)c1 * T + u1)) : 0.0;
+            const double k12 = (net && u2 >= 0) ? f64_mul(s_tab[0][u2], __ldg(p.cost + (size_t)c1 * T + u2)) : 0.0;
+            const double k21 = (net && c2 >= 0) ? f64_mul(s_tab[0][u1], __ldg(p.cost + (size_t)c2 * T + u1)) : 0.0;
+            const double k22 = (net && c2 >= 0) ? f64_mul(s_tab[0][u2], __ldg(p.cost + (size_t)c2 * T + u2)) : 0.0;
+            for (int s0 = 2 * lane; s0 < S; s0 += 64) {  // lane: scenarios s0, s0 + 1 (one 128-bit load per row)
+                const double2 w1 = __ldg(reinterpret_cast<const double2 *>(p.vmax + (size_t)c1 * Sp + s0));
+                double2 w2 = make_double2(0.0, 0.0);
+                if (p.kind == PP_MOVE_SWAP) w2 = __ldg(reinterpret_cast<const double2 *>(p.vmax + (size_t)c2 * Sp + s0));
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int s_ = s0 + h;
+                    if (s_ >= S) break;
+                    const double x1 = h ? w1.y : w1.x;
+                    double ds;
+                    if (p.kind == PP_MOVE_REASSIGN) {
+                        ds = (u2 >= 0) ? sval(x1, u2, s_, sp1, k12) : 0.0;
+                        if (u1 >= 0) ds = f64_sub(ds, sval(x1, u1, s_, sp1, k11));
+                    } else {
+                        const double x2 = h ? w2.y : w2.x;
+                        ds = f64_add(f64_sub(sval(x1, u2, s_, sp1, k12), sval(x1, u1, s_, sp1, k11)),
+                                     f64_sub(sval(x2, u1, s_, sp2, k21), sval(x2, u2, s_, sp2, k22)));
+                    }
+                    vb[s_] = ds;
+                    if (p.scen_delta) p.scen_delta[(size_t)mi * S + s_] = (float)ds;
+                }
+            }
+            __syncwarp();
+            const double ex = warp_pairwise_mean(vb, p.plan, lv);
+            // the k-smallest scratch reuses the slice (after the mean has read it)
+            const double cv = warp_cvar(vb, S, p.cvar_k, reinterpret_cast<unsigned long long *>(vb), P2 >> 5);
+            if (lane == 0) {
+                if (p.exp_delta) p.exp_delta[mi] = ex;
+                if (p.cvar) p.cvar[mi] = cv;
+            }
+            __syncwarp();
         }
     }
-    Best mine{-kInf, INT_MAX, INT_MAX};
-    if (lane == 0 && ok) mine = Best{dl, i, -1};
     grid_argmax(mine, s_red, p.partial, p.counter, p.global);
 }
-
 
 extern "C" {
 
@@ -408,21 +403,24 @@ int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, i
     mp.global = o.global;
     bool pdl;
     TRY(refresh_pm(c, st, &pdl));
-    // one warp per move: blocks of <= 32 neighbours (the padded table exists), S <= 256, k <= 25
-    const bool warp_path = c->nbr.ptr && (!stats || (S <= 256 && c->cvar_k <= 32));
+    // persistent warps, statistics a warp per feasible move: S <= 256, k <= 25
+    static const bool force_thread = std::getenv("PP_MOVES_THREAD") != nullptr;  // diagnostics: A/B the kernels
+    const bool warp_path = !force_thread && (!stats || (S <= 256 && c->cvar_k <= 32));
     if (warp_path) {
         const int P2 = S <= 32 ? 32 : S <= 64 ? 64 : S <= 128 ? 128 : 256;
         const size_t smem = sizeof(double) * ((stats ? (size_t)S * T : 0) + (size_t)MW_NW * (P2 + kMaxLeaves));
-        const int wgrid = std::max(1, (M + MW_NW - 1) / MW_NW);
+        int sms = 148;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || sms < 1) sms = 148;
+        const int wgrid = std::max(1, std::min((M + 32 * MW_NW - 1) / (32 * MW_NW), 8 * sms));
         TRY(ensure_grid_scratch(c, wgrid));  // may re-allocate: take the pointers after it
         mp.partial = c->partial.as<pp_best>();
         mp.counter = c->counter.as<unsigned int>();
         if (stats) {
             TRY(set_smem_attr(k_moves_warp<true>, smem, c->device));
-            TRY(launch_eval_n(k_moves_warp<true>, wgrid, MW_THREADS, smem, st, pdl, mp, c->nbr.as<int32_t>()));
+            TRY(launch_eval_n(k_moves_warp<true>, wgrid, MW_THREADS, smem, st, pdl, mp));
         } else {
             TRY(set_smem_attr(k_moves_warp<false>, smem, c->device));
-            TRY(launch_eval_n(k_moves_warp<false>, wgrid, MW_THREADS, smem, st, pdl, mp, c->nbr.as<int32_t>()));
+            TRY(launch_eval_n(k_moves_warp<false>, wgrid, MW_THREADS, smem, st, pdl, mp));
         }
     } else switch (kc) {
         case 0: TRY(launch_eval(k_eval_moves<0>, grid, 0, st, pdl, mp)); break;
