@@ -240,6 +240,15 @@ PP_API int pp_stage2(pp_ctx *ctx, const int32_t *assign, int32_t n_sched, double
  * exact move value polish_schedule compares, hybrid.py:369-376). */
 PP_API int pp_npv_moves(pp_ctx *ctx, const int32_t *assign, const int32_t *blocks, const int32_t *periods,
                  int32_t n_moves, uint32_t flags, double *npv_out, int32_t mem, void *stream);
+/* One single-block sweep of polish_schedule (hybrid.py:357-385) natively: for each block in order
+ * its options -- unmine (no mined successor), every other period of its precedence window
+ * (hybrid.py:348-355) that fits load[t] + m <= cap[t] -- valued by the incremental exact relaxed NPV
+ * (pp_npv_moves) in speculative chunks of blocks, the best option strictly above *cur_val + 1e-9
+ * accepted in the reference's order.  assign[B] (host, int32), load[T] (host, the caller's running
+ * period loads) and *cur_val are updated in place; *improved_out = 1 if any block moved; *calls_out
+ * (may be NULL) = device evaluations.  Results identical to the reference's sweep. */
+PP_API int pp_polish_sweep(pp_ctx *ctx, int32_t *assign, double *load, double *cur_val, uint32_t flags,
+                           int32_t chunk0, int32_t chunk_max, int32_t *improved_out, int64_t *calls_out);
 /* The feasible-sequence greedy of column generation's pricing step (colgen.py:236-254;
  * replaces the Python scan in colgen.price_column, colgen.py:207-293).  score[B][T] (host,
  * row-major) is the dual-adjusted value the caller computed exactly as colgen.py:230-234 does;

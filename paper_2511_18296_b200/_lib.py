@@ -108,6 +108,8 @@ SIGNATURES = {
                                c_void_p]),
     "pp_npv_relaxed": (c_int32, [c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_stage2": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
+    "pp_polish_sweep": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_int32, c_int32, c_void_p,
+                                  c_void_p]),
     "pp_eject": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_double, c_void_p, c_int32, c_void_p]),
     "pp_reduce_best": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
     "pp_enpv_table": (c_int32, [c_void_p, c_uint32, c_int32, c_void_p, c_int32, c_void_p]),
@@ -121,7 +123,7 @@ SIGNATURES = {
 # tests and the bench can show the drop-ins ran on the device (and how often)
 COMPUTE_ENTRY_POINTS = frozenset({
     "pp_set_schedule", "pp_apply_moves", "pp_eval_candidates", "pp_eval_moves", "pp_check_feasible",
-    "pp_repair", "pp_eject", "pp_npv_relaxed", "pp_stage2", "pp_npv_moves", "pp_price_greedy", "pp_reduce_best",
+    "pp_repair", "pp_eject", "pp_npv_relaxed", "pp_stage2", "pp_npv_moves", "pp_polish_sweep", "pp_price_greedy", "pp_reduce_best",
     "pp_enpv_table", "pp_get_spatial",
 })
 CALLS: collections.Counter = collections.Counter()

@@ -609,6 +609,10 @@ struct pp_ctx {
     double mean_cap = 0.0;
     std::vector<int> level_ptr;  // host, n_levels + 1
     std::vector<int> level_of;   // host, B
+    // host copies of the instance for host-side drivers (pp_polish_sweep): adjacency (predecessors
+    // then successors per block), masses, capacities
+    std::vector<int> h_start, h_npred, h_adj;
+    std::vector<double> h_mass, h_cap;
     PwPlan plan{};
     int cvar_k = 1;
     // static tables

@@ -1060,8 +1060,10 @@ static int s2_struct(pp_ctx *c, S2Struct *r) {
     return PP_OK;
 }
 
-int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
-                 uint32_t flags, double *npv_out, int32_t mem, void *stream) {
+}  // extern "C"
+
+static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
+                          uint32_t flags, double *npv_out, int32_t mem, void *stream) {
     if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
         return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
     if (!assign || M < 0 || (M > 0 && (!blocks || !periods || !npv_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
@@ -1228,6 +1230,116 @@ int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const 
         CUDA_TRY(stream_wait(st));
         std::memcpy(npv_out, stage, sizeof(double) * M);
     }
+    return PP_OK;
+}
+
+
+extern "C" {
+
+int pp_npv_moves(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
+                 uint32_t flags, double *npv_out, int32_t mem, void *stream) {
+    return npv_moves_impl(c, assign, blocks, periods, M, flags, npv_out, mem, stream);
+}
+
+// The single-block sweep of polish_schedule (hybrid.py:357-385) as a native driver over speculative
+// chunks of blocks: the options of blocks [b0, b1) -- unmine first when no successor is mined, then
+// every period of the precedence window (hybrid.py:348-355) other than the current one whose
+// capacity admits the block (load[t] + m <= cap[t]) -- valued against the current schedule in one
+// incremental pp_npv_moves evaluation; the blocks are then decided in order with the reference's
+// rule (the best option strictly above cur + 1e-9), and the first acceptance ends the chunk, so
+// every decision is the sequential one.  The chunk halves after an early acceptance and doubles
+// otherwise (1 .. chunk_max blocks).
+int pp_polish_sweep(pp_ctx *c, int32_t *assign, double *load, double *cur_val, uint32_t flags, int32_t chunk0,
+                    int32_t chunk_max, int32_t *improved_out, int64_t *calls_out) {
+    if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
+        return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
+    if (!assign || !load || !cur_val || !improved_out) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
+    const int B = c->B, T = c->T;
+    const int UN = -1;
+    const std::vector<int> &st = c->h_start, &np = c->h_npred, &adj = c->h_adj;
+    const std::vector<double> &mass = c->h_mass, &cap = c->h_cap;
+    int k = std::max(1, chunk0);
+    const int kmax = std::max(1, chunk_max);
+    std::vector<int32_t> ob, ot;   // the chunk's options (block, period)
+    std::vector<int32_t> first;    // per chunk block: index of its first option, then one past the last
+    std::vector<double> vals;
+    int improved = 0;
+    int64_t calls = 0;
+    double cv = *cur_val;
+    int b0 = 0;
+    while (b0 < B) {
+        const int b1 = std::min(B, b0 + k);
+        ob.clear();
+        ot.clear();
+        first.assign((size_t)(b1 - b0) + 1, 0);
+        for (int b = b0; b < b1; b++) {
+            first[b - b0] = (int)ob.size();
+            const int orig = assign[b];
+            bool pred_un = false;
+            int t_lo = 0;
+            for (int q = st[b]; q < st[b] + np[b]; q++) {
+                const int tp = assign[adj[q]];
+                if (tp == UN) {
+                    pred_un = true;
+                    break;
+                }
+                t_lo = std::max(t_lo, tp);
+            }
+            bool succ_mined = false;
+            int t_hi = T - 1;
+            for (int q = st[b] + np[b]; q < st[b + 1]; q++) {
+                const int tc = assign[adj[q]];
+                if (tc != UN) {
+                    t_hi = succ_mined ? std::min(t_hi, tc) : tc;
+                    succ_mined = true;
+                }
+            }
+            if (!succ_mined && orig != UN) {
+                ob.push_back(b);
+                ot.push_back(UN);
+            }
+            if (!pred_un)
+                for (int t = t_lo; t <= t_hi; t++)
+                    if (t != orig && load[t] + mass[b] <= cap[t]) {
+                        ob.push_back(b);
+                        ot.push_back(t);
+                    }
+        }
+        first[b1 - b0] = (int)ob.size();
+        int nxt = b1;
+        if (!ob.empty()) {
+            vals.resize(ob.size());
+            TRY(npv_moves_impl(c, assign, ob.data(), ot.data(), (int32_t)ob.size(), flags, vals.data(), PP_MEM_HOST,
+                               nullptr));
+            calls++;
+            for (int b = b0; b < b1; b++) {
+                const int lo = first[b - b0], hi = first[b - b0 + 1];
+                if (lo == hi) continue;
+                const int orig = assign[b];
+                int best_t = orig;
+                double best_val = cv;
+                for (int q = lo; q < hi; q++)
+                    if (vals[q] > best_val + 1e-9) {
+                        best_t = ot[q];
+                        best_val = vals[q];
+                    }
+                if (best_t != orig) {
+                    assign[b] = best_t;
+                    improved = 1;
+                    cv = best_val;
+                    if (orig != UN) load[orig] -= mass[b];
+                    if (best_t != UN) load[best_t] += mass[b];
+                    nxt = b + 1;
+                    break;
+                }
+            }
+        }
+        k = nxt < b1 ? std::max(1, k / 2) : std::min(kmax, k * 2);
+        b0 = nxt;
+    }
+    *cur_val = cv;
+    *improved_out = improved;
+    if (calls_out) *calls_out = calls;
     return PP_OK;
 }
 

@@ -1214,6 +1214,11 @@ int pp_set_instance(pp_ctx *c, int32_t B, int32_t T, int64_t E, const int32_t *e
         std::vector<int> fill(lptr.begin(), lptr.end() - 1);
         for (int b = 0; b < B; b++) lblocks[fill[level[b]]++] = b;
     }
+    c->h_start = start;
+    c->h_npred = npred;
+    c->h_adj = adj;
+    c->h_mass.assign(mass, mass + B);
+    c->h_cap.assign(capacity, capacity + T);
     std::vector<BlockRow> rows(B);
     for (int b = 0; b < B; b++) {
         rows[b].mass = mass[b];

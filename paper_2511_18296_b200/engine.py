@@ -422,6 +422,25 @@ class Engine:
         check(self.lib.pp_npv_moves(self._h, ptr(a), ptr(b), ptr(t), b.size, f, ptr(out), _lib.PP_MEM_HOST, None))
         return out
 
+    def polish_sweep(self, assign32: np.ndarray, load: np.ndarray, cur_val: float, use_sigma=True,
+                     chunk0: int = 64, chunk_max: int = 128):
+        """One single-block sweep of polish_schedule (hybrid.py:357-385) in the C++ driver; assign32
+        (int32) and load (f64[T]) are updated in place.  Returns (cur_val, improved, device calls)."""
+        bm = self._need_bm()
+        if not getattr(self, "_plant", False):
+            self.set_plant()
+        if assign32.dtype != np.int32 or not assign32.flags.c_contiguous or assign32.size != bm.n_blocks:
+            raise ShapeMismatch("assign32 must be a contiguous int32 [B] array")
+        if load.dtype != np.float64 or not load.flags.c_contiguous or load.size != bm.n_periods:
+            raise ShapeMismatch("load must be a contiguous float64 [T] array")
+        cv = ctypes.c_double(cur_val)
+        imp = ctypes.c_int32(0)
+        calls = ctypes.c_int64(0)
+        f = _lib.PP_USE_SIGMA if (use_sigma and self.has_sigma) else 0
+        check(self.lib.pp_polish_sweep(self._h, ptr(assign32), ptr(load), ctypes.byref(cv), f, int(chunk0),
+                                       int(chunk_max), ctypes.byref(imp), ctypes.byref(calls)))
+        return float(cv.value), bool(imp.value), int(calls.value)
+
     def price_greedy(self, score, cap, node_cap: int):
         """colgen.price_column's sequence greedy (colgen.py:236-254) on the device: score[B][T]
         f64, cap[T] = mining_capacity * capacity_slack; returns (assign int32[B], expansions)."""

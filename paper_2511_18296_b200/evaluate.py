@@ -562,77 +562,16 @@ def polish_schedule(instance, evaluator, schedule, max_sweeps: int = 5, pair_swa
         t_hi = int(ms_.min()) if ms_.size else T - 1
         return t_lo, t_hi
 
-    tgrid = np.arange(T)
-
-    def options_chunk(b0, b1):
-        """The options of blocks b0..b1-1 against the current (a, load), vectorised: the
-        reference's window (hybrid.py:348-355) and option list (357-385) per block, UNMINED
-        first, then the periods in ascending order.  CSR rows of consecutive blocks are
-        contiguous, so each chunk's neighbour periods are one gather."""
-        n = b1 - b0
-        orig = a[b0:b1]
-        pa = a[pi_[pp_[b0]:pp_[b1]]]
-        pc = np.diff(pp_[b0:b1 + 1])
-        po = pp_[b0:b1] - pp_[b0]
-        sa = a[si_[sp_[b0]:sp_[b1]]]
-        sc = np.diff(sp_[b0:b1 + 1])
-        so = sp_[b0:b1] - sp_[b0]
-        # reduceat over [po[i], po[i+1]) with one neutral sentinel appended, so an empty last
-        # row reads the sentinel and no row is truncated; empty rows are masked by their counts
-        pun = (np.add.reduceat(np.append(pa == UN, False), po) > 0) & (pc > 0)
-        pmax = np.where(pc > 0, np.maximum.reduceat(np.append(pa, UN), po), 0)
-        sm = sa != UN
-        smined = (np.add.reduceat(np.append(sm, False), so) > 0) & (sc > 0)
-        smin = np.minimum.reduceat(np.append(np.where(sm, sa, T), T), so)
-        thi = np.where(smined, smin, T - 1)
-        ok = ((~pun)[:, None] & (tgrid[None, :] >= pmax[:, None]) & (tgrid[None, :] <= thi[:, None])
-              & (tgrid[None, :] != orig[:, None])
-              & (load[None, :] + masses[b0:b1, None] <= cap[None, :]))
-        un = (~smined) & (orig != UN)
-        opt = np.concatenate([un[:, None], ok], axis=1)  # column 0 = UNMINED
-        rows, cols = np.nonzero(opt)
-        return rows, cols - 1, np.bincount(rows, minlength=n)
-
     for _ in range(max_sweeps):
-        improved = False
-        # Speculative chunks: the options of the next `k` blocks are built and valued against
-        # the current schedule in one pp_npv_moves call.  The blocks are then decided in the
-        # reference's order; a block's options and values depend only on (a, load, cur_val),
-        # which change only when a move is accepted, so the first acceptance ends the chunk and
-        # the next chunk starts at the following block: the decisions are the sequential ones.
-        b0 = 0
-        k = _POLISH_CHUNK
-        a32 = a.astype(np.int32)  # the int32 copy pp_npv_moves reads, kept in step with `a`
-        while b0 < B:
-            b1 = min(B, b0 + k)
-            rows, nt, cnt = options_chunk(b0, b1)
-            vals = eng.npv_moves(a32, rows + b0, nt, use_sigma=use_sigma).tolist() if nt.size else []
-            nt = nt.tolist()
-            pos = 0
-            nxt = b1
-            for i in np.nonzero(cnt)[0].tolist():
-                b = b0 + i
-                orig = int(a[b])
-                best_t, best_val = orig, cur_val
-                c = int(cnt[i])
-                for t, val in zip(nt[pos:pos + c], vals[pos:pos + c]):
-                    if val > best_val + 1e-9:
-                        best_t, best_val = t, val
-                pos += c
-                if best_t != orig:
-                    a[b] = best_t
-                    a32[b] = best_t
-                    improved = True
-                    cur_val = best_val
-                    if orig != UN:
-                        load[orig] -= masses[b]
-                    if best_t != UN:
-                        load[best_t] += masses[b]
-                    nxt = b + 1
-                    break
-            # shrink the chunk while moves are being accepted, grow it while they are not
-            k = max(1, k // 2) if nxt < b1 else min(_POLISH_CHUNK_MAX, k * 2)
-            b0 = nxt
+        # The single-block sweep (hybrid.py:357-385) runs in the native driver: speculative chunks of
+        # blocks whose options are valued against the current schedule in one incremental
+        # pp_npv_moves evaluation, then decided in the reference's order; the first acceptance ends
+        # a chunk (a block's options and values depend only on (a, load, cur_val), which change only
+        # when a move is accepted), so the decisions are the sequential ones.
+        a32 = a.astype(np.int32)
+        cur_val, improved, _ = eng.polish_sweep(a32, load, cur_val, use_sigma=use_sigma, chunk0=_POLISH_CHUNK,
+                                                chunk_max=_POLISH_CHUNK_MAX)
+        a[...] = a32
 
         if pair_swaps:
             for b1 in range(B):
