@@ -158,8 +158,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 #define EV_PROBE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_ev_probe[blockIdx.x][k] = gtimer(); } while (0)
+// per warp: lane 0 of every warp stamps phase k
+__device__ unsigned long long g_wp_probe[1024][8][12];
+#define WP_PROBE(k) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) g_wp_probe[blockIdx.x][threadIdx.x >> 5][k] = gtimer(); } while (0)
+extern "C" PP_API int pp_debug_warp_probe(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_wp_probe, sizeof(g_wp_probe)) == cudaSuccess ? 0 : 3;
+}
 #else
 #define EV_PROBE(k) do { } while (0)
+#define WP_PROBE(k) do { } while (0)
 #endif
 
 template <int KC, bool SCEN>
@@ -196,6 +203,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     double *w_cv = reinterpret_cast<double *>(wbase + L.cv);
     const int cw = (blockIdx.x * NW + warp) * CPW;
     EV_PROBE(0);
+    WP_PROBE(0);
 
     // ---- loads: ids, then every row of the warp's candidates in one round trip ----
     int bl = -1;
@@ -277,6 +285,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     cp_async_wait_all();
     __syncwarp();
     EV_PROBE(1);
+    WP_PROBE(1);
 
     // ---- statistics of the precedence-feasible (candidate, period) pairs, before the
     //      period masses are known (overlaps the period-mass kernel); capacity only
@@ -307,6 +316,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
             }
             __syncthreads();
             EV_PROBE(8);
+            WP_PROBE(2);
             for (int k = threadIdx.x; k < total; k += WV_THREADS) {
                 const int e = s_pair[k], i = e >> 8, t = e & 0xff;
                 const int wq = i / CPW, jq = i - wq * CPW;
@@ -333,18 +343,19 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                                      reinterpret_cast<double *>(wb + L.ex) + jq * T + t,
                                      reinterpret_cast<double *>(wb + L.cv) + jq * T + t, sd);
             }
+            WP_PROBE(3);
             __syncthreads();
         }
     }
     EV_PROBE(7);
+    WP_PROBE(4);
 
 
-    // ---- moves, pm-independent half: value of every window period (evaluate.py:379-384) and
-    //      its rank in the reference's selection order (value desc, then period asc: the
-    //      strict '>' scan of 387-388 keeps the first maximum; -inf / NaN never selected) ----
+    // ---- moves, pm-independent half: the value of every window period (evaluate.py:379-384),
+    //      kept in the lane's registers for the selection after the wait ----
     if (!(KC > 0 && stats)) __syncthreads();  // s_tab (the pooled path passed a CTA barrier already)
     double *w_val = reinterpret_cast<double *>(wbase + L.val);
-    unsigned key[CPW];
+    double vj[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
         const int ci = warp * CPW + j;
@@ -352,37 +363,34 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         double v = -kInf;
         if (KC > 0 && stats) {
             if (in) v = w_val[j * 32 + lane];  // computed with the statistics of the move
-        } else {
-            if (in) {
-                const double disc_t = s_tab[1][lane];
-                double unit;
-                if (literal) unit = f64_mul(s_cm[ci], 100.0);
-                else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
-                else unit = s_cu[ci];
-                v = f64_mul(f64_mul(f64_mul(unit, disc_t), s_tab[2][lane]), s_csp[ci]);
-                if (net) v = f64_sub(v, f64_mul(disc_t, w_cost[j * T + lane]));
-            }
-            w_val[j * 32 + lane] = v;
+        } else if (in) {
+            const double disc_t = s_tab[1][lane];
+            double unit;
+            if (literal) unit = f64_mul(s_cm[ci], 100.0);
+            else if (p.scen >= 0) unit = w_vrow[(size_t)j * Sp + p.scen];
+            else unit = s_cu[ci];
+            v = f64_mul(f64_mul(f64_mul(unit, disc_t), s_tab[2][lane]), s_csp[ci]);
+            if (net) v = f64_sub(v, f64_mul(disc_t, w_cost[j * T + lane]));
         }
-        const bool valid = in && v > -kInf;
-        const unsigned vm = __ballot_sync(FULL, valid);
-        __syncwarp();
-        int rank = 0;
-        for (unsigned mm = vm; mm; mm &= mm - 1) {
-            const int u = __ffs(mm) - 1;
-            const double vu = w_val[j * 32 + u];
-            rank += (vu > v || (vu == v && u < lane)) ? 1 : 0;
-        }
-        key[j] = valid ? (unsigned)((rank << 5) | lane) : 0xffffffffu;
+        vj[j] = v;
     }
     EV_PROBE(2);
+    WP_PROBE(5);
 
-    // ---- moves, pm half: capacity (evaluate.py:373-378) and the selection ----
+    // ---- moves, pm half: capacity (evaluate.py:373-378) and the selection: the reference's strict
+    //      '>' scan over t (387-388) keeps the first maximum, i.e. the maximum of (value, -t); as an
+    //      order-preserving 64-bit key (-0.0 folded onto +0.0, which compare equal) that is two
+    //      warp maxima (high then low word) and the lowest lane holding it.  -inf / NaN never
+    //      selected ----
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const double pm_t = lane < T ? __ldcg(p.pm + lane) : 0.0;
     EV_PROBE(3);
+    WP_PROBE(6);
     Best wbest{-kInf, INT_MAX, INT_MAX};
     unsigned okm[CPW];
+    bool okl[CPW];
+    unsigned hi[CPW], lo[CPW], mhi[CPW], mlo[CPW];
+    // the four candidates' steps interleaved: capacity and keys, then each warp reduction for all four
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
         const int ci = warp * CPW + j;
@@ -395,20 +403,34 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
             if (ab == lane) load = f64_sub(load, mass);
             ok = !(load > s_tab[0][lane]);
         }
-        okm[j] = __ballot_sync(FULL, ok);
-        const unsigned kmin = __reduce_min_sync(FULL, ok ? key[j] : 0xffffffffu);
-        const int bt = kmin == 0xffffffffu ? INT_MAX : (int)(kmin & 31u);
-        const double bv = bt != INT_MAX ? w_val[j * 32 + bt] : -kInf;
+        okl[j] = ok;
+        const bool sel = ok && vj[j] > -kInf;
+        const unsigned long long kk = sel ? f64_key(vj[j] == 0.0 ? 0.0 : vj[j]) : 0ull;
+        hi[j] = (unsigned)(kk >> 32);
+        lo[j] = (unsigned)kk;
+    }
+#pragma unroll
+    for (int j = 0; j < CPW; j++) {
+        okm[j] = __ballot_sync(FULL, okl[j]);
+        mhi[j] = __reduce_max_sync(FULL, hi[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < CPW; j++) mlo[j] = __reduce_max_sync(FULL, (hi[j] == mhi[j] && hi[j]) ? lo[j] : 0u);
+#pragma unroll
+    for (int j = 0; j < CPW; j++) {
+        const unsigned win_t = __ballot_sync(FULL, hi[j] && hi[j] == mhi[j] && lo[j] == mlo[j]);
+        const int bt = win_t ? __ffs(win_t) - 1 : INT_MAX;
+        const double bv = __shfl_sync(FULL, vj[j], win_t ? bt : 0);
         const int g = cw + j;
         if (g < p.C) {
             if (lane == 0 && b[j] >= 0) {
                 p.best_t[g] = bt != INT_MAX ? bt : -1;
-                p.best_val[g] = bv;
+                p.best_val[g] = bt != INT_MAX ? bv : -kInf;
                 p.feas[g] = bt != INT_MAX ? 1 : 0;
             }
             if (want_trace && lane < T) {
-                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = ok ? w_val[j * 32 + lane] : -kInf;
-                if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = ok ? 1 : 0;
+                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = okl[j] ? vj[j] : -kInf;
+                if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = okl[j] ? 1 : 0;
             }
         }
         if (b[j] >= 0 && bt != INT_MAX) {
@@ -539,6 +561,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         }
     }
     EV_PROBE(4);
+    WP_PROBE(7);
 
     // ---- per-(candidate, period) statistics outputs (capacity-feasible pairs only) ----
     if constexpr (STATS_T) {
@@ -559,6 +582,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         }
     }
     EV_PROBE(5);
+    WP_PROBE(8);
 
     // ---- CTA epilogue after one barrier: warp 0 merges the warps' best moves into the global
     //      record (one 128-bit compare-and-swap per CTA, the record initialised ahead of the
@@ -584,28 +608,35 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         if (lane == 0 && x.b != INT_MAX) best_cas(p.global, x);
     }
     if (want_pairs && warp == (NW > 1 ? 1 : 0)) {
-        int total = 0;
-        for (int i = 0; i < NW * CPW; i++) total += __popc(s_okm[i]);
+        // lane i: candidate i of the CTA (NW * CPW == 32): its pairs go to a contiguous range after
+        // the exclusive scan of the counts; one atomic reserves the CTA's range
+        static_assert(NW * CPW == 32, "one lane per candidate of the CTA");
+        const unsigned m = s_okm[lane];
+        const int cnt = __popc(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
         int pbase = 0;
         if (lane == 0 && total) pbase = atomicAdd(p.n_pairs, total);
         pbase = __shfl_sync(FULL, pbase, 0);
-        const unsigned lt = (1u << lane) - 1u;
-        int run = 0;
-        for (int i = 0; i < NW * CPW; i++) {
-            const unsigned m = s_okm[i];
-            if ((m >> lane) & 1u) {
-                const int wq = i / CPW, jq = i - wq * CPW;
-                const unsigned char *wb = wslices + (size_t)wq * L.total;
-                const int q = pbase + run + __popc(m & lt);
-                p.pair_cand[q] = blockIdx.x * NW * CPW + i;
-                p.pair_period[q] = lane;
-                p.pair_exp[q] = reinterpret_cast<const double *>(wb + L.ex)[jq * T + lane];
-                p.pair_cvar[q] = reinterpret_cast<const double *>(wb + L.cv)[jq * T + lane];
-            }
-            run += __popc(m);
+        const int wq = lane / CPW, jq = lane - wq * CPW;
+        const double *wex = reinterpret_cast<const double *>(wslices + (size_t)wq * L.total + L.ex) + jq * T;
+        const double *wcv = reinterpret_cast<const double *>(wslices + (size_t)wq * L.total + L.cv) + jq * T;
+        int q = pbase + incl - cnt;
+        for (unsigned mm = m; mm; mm &= mm - 1, q++) {
+            const int t = __ffs(mm) - 1;
+            p.pair_cand[q] = blockIdx.x * NW * CPW + lane;
+            p.pair_period[q] = t;
+            p.pair_exp[q] = wex[t];
+            p.pair_cvar[q] = wcv[t];
         }
     }
     EV_PROBE(6);
+    WP_PROBE(9);
 }
 
 #ifdef PP_EVAL_PROBE
