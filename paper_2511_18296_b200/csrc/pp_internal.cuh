@@ -640,6 +640,7 @@ struct pp_ctx {
     // reused while the tables (npv_gen), the buffers and the base assignment are unchanged
     uint64_t npv_gen = 0, npvm_gen = ~0ull;
     std::vector<int32_t> npvm_base;
+    std::vector<int32_t> npvm_cnt;  // mined blocks per period of npvm_base
     uint64_t npvm_bufgen[3] = {0, 0, 0};  // DevBuf::gen of npv_raw / npv_cost / npv_n when cached
     size_t h_stage_bytes = 0;
     DevBuf bad_cand;                    // int32: out-of-range candidate id seen (host-mode check)

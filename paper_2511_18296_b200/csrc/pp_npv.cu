@@ -94,9 +94,14 @@ __device__ double s2_pairwise_f(GF a, int n, int *ls, int *ll, double *leafval) 
         const int o = act ? ls[l] : 0, len = act ? ll[l] : 0;
         const int main_ = len >= 8 ? len - (len & 7) : 0;
         double acc = 0.0;
-        if (main_) {
-            acc = a(o + jl);
-            for (int i = 8; i < main_; i += 8) acc = f64_add(acc, a(o + i + jl));
+        if (main_) {  // all (<= 16) loads of the accumulator issued before its sequential adds
+            double x[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = (8 * u < main_) ? a(o + 8 * u + jl) : 0.0;
+            acc = x[0];
+#pragma unroll
+            for (int u = 1; u < 16; u++)
+                if (8 * u < main_) acc = f64_add(acc, x[u]);
         }
         acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
         acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
@@ -223,12 +228,15 @@ __device__ int s2_compact(const int32_t *__restrict__ a, int B, int t, int ob, i
 // through), and K goes to *rec_k: the prefix an incremental variant restarts from (k_s2_chain).
 template <class DF, class MF, class QF>
 __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF dof, MF mof, QF qof,
-                                 double *rec_h = nullptr, double *rec_t = nullptr, int32_t *rec_k = nullptr) {
+                                 double *rec_h = nullptr, double *rec_t = nullptr, int32_t *rec_k = nullptr,
+                                 int k_begin = 0, double total0 = 0.0) {
+    // k_begin / total0: resume at position k_begin with state (hours0, total0) -- the recorded
+    // state there (an incremental base update, k_s2_apply_one)
     __shared__ double s_q32[32], s_dm32[32];
     const int lane = threadIdx.x & 31;
-    double hl = hours0, total = 0.0;
+    double hl = hours0, total = total0;
     int k = n;
-    for (int k0 = 0; k0 < n; k0 += 32) {
+    for (int k0 = k_begin; k0 < n; k0 += 32) {
         const int kk = k0 + lane;
         const bool in = kk < n;
         const double m = in ? mof(kk) : 0.0;
@@ -765,6 +773,8 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
     };
     double hl = rec.H[base + j], tot = rec.TT[base + j];
     int e = E;
+    __shared__ double s_qd[8][64];
+    double *wq_ = s_qd[threadIdx.x >> 5], *wdm = wq_ + 32;
     double dnx = 0.0, mnx = 0.0;  // the next batch's element, loaded one batch ahead
     if (lane < E) elem(lane, dnx, mnx);
     for (int e0 = 0; e0 < E; e0 += 32) {
@@ -772,8 +782,10 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
         const bool in = ee < E;
         const double d = dnx, m = mnx;
         if (ee + 32 < E) elem(ee + 32, dnx, mnx);
-        const double q = in ? f64_div(m, rate) : 0.0;
-        const double dm = in ? f64_mul(d, m) : 0.0;
+        // the batch's terms through shared memory (broadcast reads, off the add chains)
+        wq_[lane] = in ? f64_div(m, rate) : 0.0;
+        wdm[lane] = in ? f64_mul(d, m) : 0.0;
+        __syncwarp();
         double h = hl, tt = tot, h_mine = 0.0, t_mine = 0.0;
 #pragma unroll 8
         for (int jj = 0; jj < 32; jj++) {
@@ -781,9 +793,10 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
                 h_mine = h;
                 t_mine = tt;
             }
-            h = f64_sub(h, __shfl_sync(FULL, q, jj));
-            tt = f64_add(tt, __shfl_sync(FULL, dm, jj));
+            h = f64_sub(h, wq_[jj]);
+            tt = f64_add(tt, wdm[jj]);
         }
+        __syncwarp();
         const bool stop = !in || !(h_mine > 0) || f64_mul(h_mine, rate) < m;
         const unsigned sm = __ballot_sync(FULL, stop);
         if (sm) {
@@ -885,8 +898,8 @@ __global__ void k_npv_final(int T, int S, const double *__restrict__ raw, const 
 
 // npv of variant m: the reference's accumulation over (t, s), the two changed periods from the
 // variant's stage-2 results, every other period from the base schedule's.  One warp per variant:
-// lane s forms the scenario terms (d * sigma * raw) / S in parallel (the divisions dominate), lane 0
-// adds them in the reference's (t, s) order.
+// lane s forms the scenario terms (d * sigma * raw) / S in parallel (the divisions dominate) into
+// shared memory, lane 0 adds them in the reference's (t, s) order.
 __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict__ braw, const double *__restrict__ bcost,
                                   const int32_t *__restrict__ bn, const double *__restrict__ mraw,
                                   const double *__restrict__ mcost, const int32_t *__restrict__ mn,
@@ -898,6 +911,8 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
     const int m = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (m >= M) return;
     const int t0 = slot_t[2 * m], t1 = slot_t[2 * m + 1];
+    __shared__ double s_q[8][32];
+    double *wq = s_q[(threadIdx.x >> 5) & 7];
     double total = 0.0;
     for (int t = 0; t < T; t++) {
         const double *raw;
@@ -917,13 +932,15 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
         if (n > 0) total = f64_sub(total, f64_mul(d, cs));
         for (int s0 = 0; s0 < S; s0 += 32) {
             const int s = s0 + lane;
-            double q = 0.0;
             if (s < S) {
                 const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
-                q = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
+                wq[lane] = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
             }
+            __syncwarp();
             const int cnt = min(32, S - s0);
-            for (int u = 0; u < cnt; u++) total = f64_add(total, __shfl_sync(FULL, q, u));
+            if (lane == 0)  // the adds in the reference's order; the terms are broadcast reads
+                for (int u = 0; u < cnt; u++) total = f64_add(total, wq[u]);
+            __syncwarp();
         }
     }
     if (lane == 0) npv[m] = total;
@@ -1032,6 +1049,181 @@ __global__ void k_scatter_assign(int32_t *__restrict__ assign, const int32_t *__
     if (i < n) assign[blk[i]] = per[i];  // distinct blocks (a diff)
 }
 
+
+// ------------------------------------------------------------------------------------
+// Incremental base update when the base schedule changed by ONE block b: t_old -> t_new (the
+// polish pattern: every accepted move ends a call).  Instead of re-solving the two periods from
+// scratch (compaction, sort, greedy), the recorded structure is spliced: grid (S, 2), y = 0 takes b
+// out of (s, t_old), y = 1 puts it into (s, t_new) at its binary-searched place; the arrays after
+// the place shift by one in 1024-element chunks (ascending for a removal, descending for an
+// insertion, so no chunk overwrites what a later one reads), the positions of the shifted blocks
+// are renumbered, and the greedy resumes from the recorded state at the place (the prefix before it
+// is unchanged) with recording.  The s == 0 CTAs splice the block-ordered id and cost lists the same
+// way and recompute the period's mining-cost sum (numpy pairwise).  Identical to a rebuild.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(S2_THREADS, 1)
+    k_s2_apply_one(const S2Struct rec, int B, int T, int S, int Sp, int b, int t_old, int t_new,
+                   const double *__restrict__ mass, const double *__restrict__ cost, const double *__restrict__ vmax,
+                   const double *__restrict__ hours, double rate, double *__restrict__ raw,
+                   double *__restrict__ costsum, int32_t *__restrict__ nmined) {
+    __shared__ int s_j, s_ls[256], s_ll[256];
+    __shared__ double s_lv[256];
+    const int s = blockIdx.x;
+    const bool ins = blockIdx.y == 1;
+    const int t = ins ? t_new : t_old;
+    if (t < 0) return;
+    const int tid = threadIdx.x;
+    const size_t st_ = (size_t)s * T + t, base = st_ * rec.L;
+    double *D = rec.D + base, *M_ = rec.M + base, *H = rec.H + base, *TT = rec.TT + base;
+    int32_t *BI = rec.BID + base;
+    const int np = rec.npos[st_];
+    const double mb = __ldg(mass + b);
+    const double db = f64_div(__ldg(vmax + (size_t)b * Sp + s), mb);
+    // 1. the place of b in the greedy order
+    if (tid == 0) {
+        int j;
+        if (!ins) {
+            j = rec.pos[(size_t)s * B + b];  // -1: not in the list (density <= 0)
+        } else if (!(db > 0)) {
+            j = -1;
+            rec.pos[(size_t)s * B + b] = -1;
+        } else {
+            int lo = 0, hi = np;
+            while (lo < hi) {
+                const int md = (lo + hi) >> 1;
+                if (D[md] > db || (D[md] == db && BI[md] < b)) lo = md + 1;
+                else hi = md;
+            }
+            j = lo;
+        }
+        s_j = j;
+    }
+    __syncthreads();
+    const int j = s_j;
+    const int K = rec.K[st_];
+    if (j >= 0) {
+        // 2. splice the order (D, M, BID) and renumber the shifted blocks' positions
+        if (!ins) {
+            for (int k0 = j; k0 < np - 1; k0 += S2_THREADS) {
+                const int k = k0 + tid;
+                double dd = 0.0, mm = 0.0;
+                int bb = 0;
+                if (k < np - 1) {
+                    dd = D[k + 1];
+                    mm = M_[k + 1];
+                    bb = BI[k + 1];
+                }
+                __syncthreads();
+                if (k < np - 1) {
+                    D[k] = dd;
+                    M_[k] = mm;
+                    BI[k] = bb;
+                    rec.pos[(size_t)s * B + bb] = k;
+                }
+                __syncthreads();
+            }
+        } else {
+            for (int k1 = np; k1 > j; k1 -= S2_THREADS) {
+                const int k = k1 - 1 - tid;  // old position, moves to k + 1
+                double dd = 0.0, mm = 0.0;
+                int bb = 0;
+                if (k >= j) {
+                    dd = D[k];
+                    mm = M_[k];
+                    bb = BI[k];
+                }
+                __syncthreads();
+                if (k >= j) {
+                    D[k + 1] = dd;
+                    M_[k + 1] = mm;
+                    BI[k + 1] = bb;
+                    rec.pos[(size_t)s * B + bb] = k + 1;
+                }
+                __syncthreads();
+            }
+            if (tid == 0) {
+                D[j] = db;
+                M_[j] = mb;
+                BI[j] = b;
+                rec.pos[(size_t)s * B + b] = j;
+            }
+        }
+        __syncthreads();
+        const int npn = ins ? np + 1 : np - 1;
+        // 3. the greedy from the place on, from the recorded state there (unchanged prefix); a place
+        //    beyond the stop changes nothing the greedy reaches
+        if (j <= K && tid < 32) {
+            const double total = s2_greedy_warp(
+                npn, npn, H[j], rate, [&](int k) { return D[k]; }, [&](int k) { return M_[k]; },
+                [&](int k) { return f64_div(M_[k], rate); }, H, TT, rec.K + st_, j, TT[j]);
+            if (tid == 0) raw[(size_t)t * S + s] = total;
+        }
+        if (tid == 0) rec.npos[st_] = npn;
+    }
+    // 4. s == 0: the block-ordered ids and costs, the period's cost sum and size
+    if (s != 0) return;
+    __syncthreads();
+    int32_t *ids = rec.IDS + (size_t)t * rec.L;
+    double *csl = rec.CS + (size_t)t * rec.L;
+    const int n0 = rec.nper[t];
+    if (tid == 0) {
+        int lo = 0, hi = n0;
+        while (lo < hi) {
+            const int md = (lo + hi) >> 1;
+            if (ids[md] < b) lo = md + 1;
+            else hi = md;
+        }
+        s_j = lo;
+    }
+    __syncthreads();
+    const int r = s_j;
+    if (!ins) {
+        for (int k0 = r; k0 < n0 - 1; k0 += S2_THREADS) {
+            const int k = k0 + tid;
+            int bb = 0;
+            double cc = 0.0;
+            if (k < n0 - 1) {
+                bb = ids[k + 1];
+                cc = csl[k + 1];
+            }
+            __syncthreads();
+            if (k < n0 - 1) {
+                ids[k] = bb;
+                csl[k] = cc;
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int k1 = n0; k1 > r; k1 -= S2_THREADS) {
+            const int k = k1 - 1 - tid;
+            int bb = 0;
+            double cc = 0.0;
+            if (k >= r) {
+                bb = ids[k];
+                cc = csl[k];
+            }
+            __syncthreads();
+            if (k >= r) {
+                ids[k + 1] = bb;
+                csl[k + 1] = cc;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            ids[r] = b;
+            csl[r] = __ldg(cost + (size_t)b * T + t);
+        }
+    }
+    __syncthreads();
+    const int n1 = ins ? n0 + 1 : n0 - 1;
+    const double cs = s2_pairwise(csl, n1, s_ls, s_ll, s_lv);  // n1 < 16000: <= 252 leaves
+    if (tid == 0) {
+        rec.nper[t] = n1;
+        costsum[t] = cs;
+        nmined[t] = n1;
+    }
+}
+
 // carve the base structure (S2Struct) out of c->s2_rec for the current (S, T, B)
 static int s2_struct(pp_ctx *c, S2Struct *r) {
     const size_t S = c->S, T = c->T, B = c->B, L = B + 1;
@@ -1069,6 +1261,7 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     if (!assign || M < 0 || (M > 0 && (!blocks || !periods || !npv_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
     if ((flags & PP_USE_SIGMA) && !c->have_sigma) return fail(PP_ERR_STATE, "PP_USE_SIGMA without an uploaded sigma");
     if (M == 0) return PP_OK;
+    HostTrace ht_("pp_npv_moves");
     TRY(use_device(c));
     cudaStream_t st = pick(c, stream);
     const int B = c->B, T = c->T, S = c->S;
@@ -1124,28 +1317,55 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     const bool intact = c->npvm_gen == c->npv_gen && c->npvm_bufgen[0] == c->npv_raw.gen &&
                         c->npvm_bufgen[1] == c->npv_cost.gen && c->npvm_bufgen[2] == c->npv_n.gen &&
                         c->s2_rec.gen == recgen && c->npvm_base.size() == (size_t)B;
-    // one pass over the base: range check, the blocks that changed since the cached base (their old
-    // and new periods are the ones to re-solve) and the period sizes (whether the large-period
-    // kernel can be needed at all)
-    std::vector<int32_t> dirty, chg_b, chg_t, cnt(T, 0);
-    {
+    // the blocks that changed since the cached base (their old and new periods are the ones to
+    // re-solve): equal 64-block runs are skipped with memcmp, so a base that drifted by a few blocks
+    // costs a few microseconds; period sizes (whether the large-period kernel can be needed) are kept
+    // in step with the diff, and the range check covers every entry the device has not seen
+    std::vector<int32_t> dirty, chg_b, chg_t;
+    std::vector<int32_t> &cnt = c->npvm_cnt;
+    bool full = !intact;
+    if (!full) {
         std::vector<char> mark(T, 0);
-        const int32_t *old = intact ? c->npvm_base.data() : nullptr;
-        for (int b = 0; b < B; b++) {
-            const int32_t n = ha[b];
-            if (n < -1 || n >= T) return fail(PP_ERR_INVALID_ARGS, "assign[%d] = %d out of range", b, n);
-            if (n >= 0) cnt[n]++;
-            if (old && old[b] != n) {
-                if (old[b] >= 0) mark[old[b]] = 1;
+        const int32_t *old = c->npvm_base.data();
+        for (int b0 = 0; b0 < B; b0 += 64) {
+            const int nb = std::min(64, B - b0);
+            if (std::memcmp(old + b0, ha + b0, sizeof(int32_t) * nb) == 0) continue;
+            for (int b = b0; b < b0 + nb; b++) {
+                const int32_t o = old[b], n = ha[b];
+                if (o == n) continue;
+                if (n < -1 || n >= T) return fail(PP_ERR_INVALID_ARGS, "assign[%d] = %d out of range", b, n);
+                if (o >= 0) mark[o] = 1;
                 if (n >= 0) mark[n] = 1;
                 chg_b.push_back(b);
                 chg_t.push_back(n);
             }
+            if (chg_b.size() * 8 > (size_t)B) break;  // a new schedule rather than a drift
         }
         for (int t = 0; t < T; t++)
             if (mark[t]) dirty.push_back(t);
+        full = (int)dirty.size() * 2 > T || chg_b.size() * 8 > (size_t)B;
     }
-    const bool full = !intact || (int)dirty.size() * 2 > T || chg_b.size() * 8 > (size_t)B;
+    if (full) {
+        cnt.assign(T, 0);
+        int32_t lo = 0, hi = -1;  // branch-free range check (vectorises), then the period sizes
+        for (int b = 0; b < B; b++) {
+            lo = std::min(lo, ha[b]);
+            hi = std::max(hi, ha[b]);
+        }
+        if (lo < -1 || hi >= T) return fail(PP_ERR_INVALID_ARGS, "assign holds a period outside [-1, %d)", T);
+        for (int b = 0; b < B; b++)
+            if (ha[b] >= 0) cnt[ha[b]]++;
+        chg_b.clear();
+        chg_t.clear();
+        dirty.clear();
+    } else {
+        const int32_t *old = c->npvm_base.data();
+        for (size_t k = 0; k < chg_b.size(); k++) {
+            if (old[chg_b[k]] >= 0) cnt[old[chg_b[k]]]--;
+            if (chg_t[k] >= 0) cnt[chg_t[k]]++;
+        }
+    }
+    ht_.mark("diff");
     const bool may_be_big = *std::max_element(cnt.begin(), cnt.end()) > S2_NMAX;
     // the device keeps its own copy of the base assignment: a full upload when the structure is
     // rebuilt, else only the changed entries (scattered by k_scatter_assign)
@@ -1187,12 +1407,20 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         CUDA_TRY(cudaGetLastError());
     }
     const int32_t *da = dbase;
+    ht_.mark("upload");
     double *braw = c->npv_raw.as<double>(), *mraw = braw + (size_t)T * S;
     double *bcost = c->npv_cost.as<double>(), *mcost = bcost + T;
     int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
-    if (full)
+    if (full) {
         TRY(run_stage2(c, st, da, T, 1, braw, bcost, bn, nullptr, nullptr, nullptr, nullptr, &rec, may_be_big));
-    else if (!dirty.empty())
+    } else if (chg_b.size() == 1 && c->npvm_cnt[dirty[0]] < 16000 &&
+               (dirty.size() < 2 || c->npvm_cnt[dirty[1]] < 16000)) {  // one block moved: splice
+        const int bb = chg_b[0], to = c->npvm_base[bb], tn = chg_t[0];
+        k_s2_apply_one<<<dim3(S, 2), S2_THREADS, 0, st>>>(rec, B, T, S, c->Sp, bb, to, tn, c->mass.as<double>(),
+                                                          c->cost.as<double>(), c->vmax.as<double>(),
+                                                          c->hours.as<double>(), c->rate, braw, bcost, bn);
+        CUDA_TRY(cudaGetLastError());
+    } else if (!dirty.empty())
         TRY(run_stage2(c, st, da, (int)dirty.size(), 1, braw, bcost, bn, nullptr, nullptr, nullptr, dtsel, &rec,
                        may_be_big));
     {
@@ -1210,6 +1438,7 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         k_s2_varcost<<<grid, 256, smem, st>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap);
         CUDA_TRY(cudaGetLastError());
     }
+    ht_.mark("launch");
     double *dn = host ? c->h_d1.as<double>() : npv_out;
     k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
                                                         c->disc.as<double>(),
@@ -1227,7 +1456,9 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     }
     if (host) {
         CUDA_TRY(cudaMemcpyAsync(stage, dn, out_bytes, cudaMemcpyDeviceToHost, st));
+        ht_.mark("final+d2h");
         CUDA_TRY(stream_wait(st));
+        ht_.mark("sync");
         std::memcpy(npv_out, stage, sizeof(double) * M);
     }
     return PP_OK;
