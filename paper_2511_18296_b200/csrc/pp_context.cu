@@ -32,6 +32,40 @@ int fail(int code, const char *fmt, ...) {
 }
 
 
+// Registry of the page-locked buffers pp_host_alloc handed out (host range -> device mapping), so
+// the host-mode copy-out resolves its destinations without a driver query per array and call.
+namespace {
+struct PinnedRange {
+    uintptr_t lo, hi, dev;
+};
+std::mutex g_pinned_mu;
+std::vector<PinnedRange> g_pinned;
+}  // namespace
+
+void pinned_register(void *host, size_t bytes, void *dev) {
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    g_pinned.push_back({reinterpret_cast<uintptr_t>(host), reinterpret_cast<uintptr_t>(host) + bytes,
+                        reinterpret_cast<uintptr_t>(dev)});
+}
+
+void pinned_unregister(void *host) {
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    const uintptr_t h = reinterpret_cast<uintptr_t>(host);
+    for (size_t i = 0; i < g_pinned.size(); i++)
+        if (g_pinned[i].lo == h) {
+            g_pinned.erase(g_pinned.begin() + (long)i);
+            return;
+        }
+}
+
+void *pinned_lookup(const void *host) {
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    const uintptr_t h = reinterpret_cast<uintptr_t>(host);
+    for (const PinnedRange &r : g_pinned)
+        if (h >= r.lo && h < r.hi) return reinterpret_cast<void *>(r.dev + (h - r.lo));
+    return nullptr;
+}
+
 int ensure_grid_scratch(pp_ctx *c, int grid) {
     TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
     if (c->counter.bytes == 0) {
@@ -147,12 +181,19 @@ int pp_synchronize(pp_ctx *c, void *stream) {
 
 int pp_host_alloc(size_t bytes, void **ptr) {
     if (!ptr) return fail(PP_ERR_INVALID_ARGS, "ptr is NULL");
-    CUDA_TRY(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable | cudaHostAllocMapped));
+    const size_t n = std::max<size_t>(bytes, 1);
+    CUDA_TRY(cudaHostAlloc(ptr, n, cudaHostAllocPortable | cudaHostAllocMapped));
+    void *dev = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&dev, *ptr, 0));
+    pinned_register(*ptr, n, dev);
     return PP_OK;
 }
 
 int pp_host_free(void *ptr) {
-    if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+    if (ptr) {
+        pinned_unregister(ptr);
+        CUDA_TRY(cudaFreeHost(ptr));
+    }
     return PP_OK;
 }
 

@@ -714,6 +714,7 @@ __global__ void __launch_bounds__(256) k_copy_out(const CopyOut co) {
 // device pointer of a page-locked host buffer, or nullptr (pageable / unknown)
 static void *mapped_host(const void *p) {
     if (!p) return nullptr;
+    if (void *d = pinned_lookup(p)) return d;  // one of pp_host_alloc's buffers: no driver query
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();

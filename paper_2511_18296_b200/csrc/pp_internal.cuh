@@ -786,6 +786,10 @@ inline int launch_eval_n(void (*kern)(KArgs...), int grid, int threads, size_t s
 
 
 // ---- shared host helpers (pp_context.cu, pp_schedule.cu) ----
+// page-locked buffers from pp_host_alloc: host range -> device mapping (nullptr if not one of them)
+void pinned_register(void *host, size_t bytes, void *dev);
+void pinned_unregister(void *host);
+void *pinned_lookup(const void *host);
 int ensure_grid_scratch(pp_ctx *c, int grid);
 int check_ready(pp_ctx *c, uint32_t flags, int scenario);
 int pick_kc(int k);
