@@ -680,30 +680,37 @@ __global__ void k_apply_moves(int32_t *assign, int B, int T, const int32_t *bloc
 // period masses of P schedules (device pointers) into pm_out[P][T]: P1 (chunks) then
 // P2 (trees), P2 launched as a programmatic dependent of P1
 // ---------------------------------------------------------------------------------------------
-// Cluster fast path (B <= 65536, T <= 16): one 8-CTA cluster per schedule, 1024 threads per CTA.
-//  1. Warp w of CTA r owns the contiguous blocks [(32 r + w) * 32K, +32K).  Lane t keeps the
-//     warp's running count of period t; a block's rank inside its period is that count plus
-//     the lower lanes of the same ballot (no shared-memory round trips).  Per-warp counts are
-//     scanned over the warps; the CTA totals are exchanged through distributed shared memory
-//     (8 x T integers), which fixes every block's position in its period's numpy order.
-//  2. The masses are scattered to compact[p][t][pos] (L2), then a cluster barrier.
-//  3. CTA r reduces periods r and r + 8.  numpy's recursion (pairwise.c: blocks of 8, leaves of
+// Cluster fast path (T <= 32, B <= 245,760): one cluster of R = 16 CTAs per schedule (8 when the
+// GPU cannot place a 16-CTA cluster), 1024 threads per CTA.
+//  1. Warp w of CTA r owns the contiguous blocks [(32 r + w) * 32K, +32K), K blocks per lane.  A
+//     block's rank inside its (warp, period) group is the running count of that period plus the
+//     lower lanes of the same match_any group.  Per-warp counts are scanned over the warps; the
+//     CTA totals are exchanged through distributed shared memory (R x T integers), which fixes
+//     every block's position in its period's numpy order.  Up to K = 8 the periods and masses
+//     stay in registers between ranking and scatter; above that (C4: 200k blocks, K = 13) a first
+//     pass only counts and the scatter pass re-reads the blocks (L2) and ranks them again.
+//  2. Push mode (every period fits its slot): each mass goes straight into the shared memory of
+//     the CTA that reduces its period (period t -> CTA t % R, slot t / R); otherwise into
+//     compact[p][t][pos] in global memory.  A cluster barrier orders the stores.
+//  3. CTA r reduces periods r, r + R, ...  numpy's recursion (pairwise.c: blocks of 8, leaves of
 //     <= 128 elements) splits m = n/8 blocks floor|ceil, so the rightmost node is the largest at
 //     every depth and every leaf sits at depth D or D + 1, D = (first depth whose rightmost node
 //     is a leaf) - 1.  Sixteen lanes per depth-D node walk its root path to find its range and
-//     sum its one or two leaves (one L2 round trip); the 2^D node values fold as a perfect tree.
-// Distributed shared memory carries only the counts: its bandwidth (~20 B/clk/SM) is far below
-// L2's, so the masses go through L2.
+//     sum its one or two leaves; the 2^D node values fold as a perfect tree.
 // ---------------------------------------------------------------------------------------------
 constexpr int PMC_R = 8;    // portable cluster size (fallback)
 constexpr int PMC_R16 = 16;  // non-portable: used when the GPU can place a 16-CTA cluster
 constexpr int PMC_THREADS = 1024;
 constexpr int PMC_WARPS = PMC_THREADS / 32;
-constexpr int PMC_MAXT = 16;
-constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;
-constexpr int PMC_MAXB = PMC_R * PMC_THREADS * 8;
-constexpr int PMC_MAXNODE = 512;  // 2^D for n <= 65536 (n = 65535: D = 9)
-constexpr int PMC_OWN = 6144;     // per-period buffer in the owning CTA (push mode; C2 periods hold ~4.2k)
+constexpr int PMC_MAXT = 32;
+constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;  // periods per CTA
+constexpr int PMC_MAXNODE = 1024;  // 2^D <= n / 240: periods of up to 245,760 blocks
+constexpr int PMC_MAXN = 245760;
+constexpr int PMC_FOLD = 512;      // node values one warp folds (16 per lane)
+constexpr int PMC_KREG = 8;        // blocks per lane kept in registers
+constexpr int PMC_GRP = 8;         // loads in flight per lane in the two-pass mode
+constexpr size_t PMC_SMEM_MAX = 227 * 1024;
+static_assert(PMC_MAXNODE <= 2 * PMC_FOLD, "one pre-fold level");
 
 struct PmcSmem {
     int cnt[PMC_WARPS][PMC_MAXT];
@@ -748,13 +755,14 @@ __device__ __forceinline__ void pw_node(int m, int d, int i, int &start, int &le
     len = l;
 }
 
+// K > 0: K blocks per lane in registers; K == 0: kk blocks per lane, count pass + scatter pass
 template <int K, int R>  // R CTAs per schedule, one cluster (launch attribute)
 __global__ void __launch_bounds__(PMC_THREADS, 1)
-    k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T,
-                 double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init,
+    k_pm_cluster(const int32_t *__restrict__ assign, const double *__restrict__ mass, int B, int T, int kk,
+                 int own_cap, double *__restrict__ compact, double *__restrict__ pm_out, EvalInit init,
                  int32_t *__restrict__ bad) {
     __shared__ PmcSmem h;
-    extern __shared__ __align__(16) double pmc_own[];  // [PMC_MAXQ][PMC_OWN] (push mode)
+    extern __shared__ __align__(16) double pmc_own[];  // [ceil(T / R)][own_cap] (push mode)
     PMCP(0, 0);
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {  // complete before the dependents' wait
         if (init.n_pairs) *init.n_pairs = 0;
@@ -763,41 +771,64 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     }
     asm volatile("griddepcontrol.launch_dependents;");
     constexpr unsigned FULL = 0xffffffffu;
+    constexpr int KR = K > 0 ? K : 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = blockIdx.x, p = blockIdx.y;
     const int32_t *as = assign + (size_t)p * B;
-    const int base = (r * PMC_WARPS + warp) * (32 * K);
-    int tk[K];
-    double mk[K];
+    const int KB = K > 0 ? K : kk;
+    const int base = (r * PMC_WARPS + warp) * (32 * KB);
+    const unsigned lt = (1u << lane) - 1u;
+    int tk[KR];
+    double mk[KR];
+    int pos[KR];
     int badl = 0;
+    if constexpr (K > 0) {
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        const int b = base + k * 32 + lane;
-        int t = -1;
-        double m = 0.0;
-        if (b < B) {
-            t = __ldg(as + b);
-            m = __ldg(mass + b);
+        for (int k = 0; k < K; k++) {
+            const int b = base + k * 32 + lane;
+            int t = -1;
+            double m = 0.0;
+            if (b < B) {
+                t = __ldg(as + b);
+                m = __ldg(mass + b);
+            }
+            tk[k] = ((unsigned)t < (unsigned)T) ? t : -1;
+            badl |= (t < -1) | (t >= T);
+            mk[k] = m;
         }
-        tk[k] = ((unsigned)t < (unsigned)T) ? t : -1;
-        badl |= (t < -1) | (t >= T);
-        mk[k] = m;
     }
     PMCS(0);
-    // ranks inside (warp, period): match_any groups, running counts in shared memory
     for (int i = tid; i < PMC_WARPS * PMC_MAXT; i += PMC_THREADS) (&h.cnt[0][0])[i] = 0;
     __syncthreads();
-    const unsigned lt = (1u << lane) - 1u;
-    int pos[K];
+    if constexpr (K > 0) {  // ranks inside (warp, period): match_any groups, running counts in shared memory
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        const unsigned mt = __match_any_sync(FULL, tk[k]);
-        const int lr = __popc(mt & lt);
-        const int b0 = tk[k] >= 0 ? h.cnt[warp][tk[k]] : 0;
-        pos[k] = b0 + lr;
-        __syncwarp();
-        if (tk[k] >= 0 && lr == 0) h.cnt[warp][tk[k]] = b0 + __popc(mt);
-        __syncwarp();
+        for (int k = 0; k < K; k++) {
+            const unsigned mt = __match_any_sync(FULL, tk[k]);
+            const int lr = __popc(mt & lt);
+            const int b0 = tk[k] >= 0 ? h.cnt[warp][tk[k]] : 0;
+            pos[k] = b0 + lr;
+            __syncwarp();
+            if (tk[k] >= 0 && lr == 0) h.cnt[warp][tk[k]] = b0 + __popc(mt);
+            __syncwarp();
+        }
+    } else {  // count pass: PMC_GRP loads in flight per lane
+        for (int k0 = 0; k0 < kk; k0 += PMC_GRP) {
+            int tq[PMC_GRP];
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int b = base + (k0 + u) * 32 + lane;
+                tq[u] = (k0 + u < kk && b < B) ? __ldg(as + b) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int t = tq[u];
+                badl |= (t < -1) | (t >= T);
+                const int tv = ((unsigned)t < (unsigned)T) ? t : -1;
+                const unsigned mt = __match_any_sync(FULL, tv);
+                if (tv >= 0 && __popc(mt & lt) == 0) h.cnt[warp][tv] += __popc(mt);
+                __syncwarp();
+            }
+        }
     }
     const int anybad = __syncthreads_or(badl);  // (also the barrier after the ranks)
     if (bad && threadIdx.x == 0 && blockIdx.y == 0) bad[blockIdx.x] = anybad;  // every CTA writes its flag
@@ -832,32 +863,55 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     }
     __syncthreads();
     PMCS(2);
-    // push mode (every period fits its owner's buffer; the same decision in every CTA): each mass
-    // goes straight into the shared memory of the CTA that reduces its period; otherwise through L2
+    // push mode (every period fits its slot; the same decision in every CTA): each mass goes
+    // straight into the shared memory of the CTA that reduces its period; otherwise through L2
     bool push = true;
-    for (int t = 0; t < T; t++) push &= h.n[t] <= PMC_OWN;
-    if (push) {
+    for (int t = 0; t < T; t++) push &= h.n[t] <= own_cap;
+    if constexpr (K > 0) {
 #pragma unroll
         for (int k = 0; k < K; k++)
             if (tk[k] >= 0) {
-                const int t = tk[k];
-                st_dsmem_f64(pmc_own + (t / R) * PMC_OWN + h.off[t] + h.cnt[warp][t] + pos[k], t % R, mk[k]);
+                const int t = tk[k], at = h.off[t] + h.cnt[warp][t] + pos[k];
+                if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mk[k]);
+                else compact[((size_t)p * T + t) * B + at] = mk[k];
             }
-    } else {
+    } else {  // scatter pass: re-read, rank again (same groups), h.cnt[warp][t] is the running position
+        for (int k0 = 0; k0 < kk; k0 += PMC_GRP) {
+            int tq[PMC_GRP];
+            double mq[PMC_GRP];
 #pragma unroll
-        for (int k = 0; k < K; k++)
-            if (tk[k] >= 0) {
-                const int t = tk[k];
-                compact[((size_t)p * T + t) * B + h.off[t] + h.cnt[warp][t] + pos[k]] = mk[k];
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int b = base + (k0 + u) * 32 + lane;
+                const bool in = k0 + u < kk && b < B;
+                const int t = in ? __ldg(as + b) : -1;
+                tq[u] = ((unsigned)t < (unsigned)T) ? t : -1;
+                mq[u] = in ? __ldg(mass + b) : 0.0;
             }
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int t = tq[u];
+                const unsigned mt = __match_any_sync(FULL, t);
+                const int lr = __popc(mt & lt);
+                const int w0 = t >= 0 ? h.cnt[warp][t] : 0;
+                __syncwarp();
+                if (t >= 0) {
+                    const int at = h.off[t] + w0 + lr;
+                    if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mq[u]);
+                    else compact[((size_t)p * T + t) * B + at] = mq[u];
+                    if (lr == 0) h.cnt[warp][t] = w0 + __popc(mt);
+                }
+                __syncwarp();
+            }
+        }
     }
     // the cluster barrier's release/acquire orders these stores (distributed shared memory or
     // global) for every thread of the cluster (no separate sequentially consistent fence)
     cluster_sync_acqrel();  // every block of the schedule is in place (remote totals no longer read)
     PMCP(0, 1);
-    // depth-D nodes of the (up to two) periods of this CTA
+    // depth-D nodes of this CTA's periods r, r + R, ...
     const int q = max(0, (T - r + R - 1) / R);
     int Dg[PMC_MAXQ], cntg[PMC_MAXQ];
+    int nitems = 0;
 #pragma unroll
     for (int g = 0; g < PMC_MAXQ; g++) {
         Dg[g] = 0;
@@ -869,17 +923,28 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             Dg[g] = max(d - 1, 0);
             cntg[g] = 1 << Dg[g];
         }
+        nitems += cntg[g];
     }
-    const int nitems = cntg[0] + cntg[1];
     PMCS(4);
     const int sub = tid & 7, half = (tid >> 3) & 1;  // 16 lanes per node: half c sums child leaf c
     for (int it0 = 0; it0 < nitems; it0 += PMC_THREADS / 16) {
         const int it = it0 + (tid >> 4);
         const bool act = it < nitems;
-        const int g = (it >= cntg[0]) ? 1 : 0;
-        const int i = act ? it - (g ? cntg[0] : 0) : 0;
+        int g = 0, i = act ? it : 0, D = Dg[0];  // (unrolled selects: no local-memory indexing)
+        bool fnd = false;
+#pragma unroll
+        for (int u = 0; u < PMC_MAXQ; u++)
+            if (!fnd) {
+                if (i < cntg[u] || u == PMC_MAXQ - 1) {
+                    g = u;
+                    D = Dg[u];
+                    fnd = true;
+                } else {
+                    i -= cntg[u];
+                }
+            }
         const int t = r + R * g;
-        const int n = act ? h.n[t] : 0, m = n >> 3, rem = n & 7, D = g ? Dg[1] : Dg[0];
+        const int n = act ? h.n[t] : 0, m = n >> 3, rem = n & 7;
         int s0, l0;
         pw_node(m, D, i, s0, l0);
         const bool last = i == (1 << D) - 1;
@@ -898,7 +963,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         const int nm = len >> 3, ntail = len & 7, e0 = len - ntail;
         double x[16], tailv;
         if (push) {
-            const double *a = pmc_own + g * PMC_OWN + o;
+            const double *a = pmc_own + g * own_cap + o;
 #pragma unroll
             for (int u = 0; u < 16; u++) x[u] = (use && u < nm) ? a[8 * u + sub] : 0.0;
             tailv = (use && sub < ntail) ? a[e0 + sub] : 0.0;
@@ -926,10 +991,35 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     }
     PMCS(5);
     __syncthreads();
+    // periods above ~123k blocks have more than PMC_FOLD depth-D nodes: fold one level first
+    // (pairs (2i, 2i + 1) are the perfect tree's lowest level)
+    {
+        double y[PMC_MAXQ];
+#pragma unroll
+        for (int g = 0; g < PMC_MAXQ; g++)
+            y[g] = (cntg[g] > PMC_FOLD && tid < cntg[g] / 2) ? f64_add(h.val[g][2 * tid], h.val[g][2 * tid + 1]) : 0.0;
+        bool any = false;
+#pragma unroll
+        for (int g = 0; g < PMC_MAXQ; g++) any |= cntg[g] > PMC_FOLD;
+        if (any) {  // uniform over the CTA
+            __syncthreads();
+#pragma unroll
+            for (int g = 0; g < PMC_MAXQ; g++)
+                if (cntg[g] > PMC_FOLD && tid < cntg[g] / 2) h.val[g][tid] = y[g];
+            __syncthreads();
+#pragma unroll
+            for (int g = 0; g < PMC_MAXQ; g++)
+                if (cntg[g] > PMC_FOLD) cntg[g] >>= 1;
+        }
+    }
     PMCS(3);
-    // perfect-tree fold of the 2^D node values: warp g folds period slot g
+    // perfect-tree fold of the node values: warp g folds period slot g
     if (warp < q) {
-        const int g = warp, cnt = g ? cntg[1] : cntg[0];
+        int cnt = cntg[0];
+#pragma unroll
+        for (int g = 1; g < PMC_MAXQ; g++)
+            if (warp == g) cnt = cntg[g];
+        const int g = warp;
         const int per = cnt > 32 ? cnt >> 5 : 1;  // consecutive values per lane (<= 16)
         double v = 0.0;
         if (lane * per < cnt) {
@@ -953,11 +1043,24 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     PMCP(1, 1);
 }
 
+// dynamic shared memory of the push-mode slots: ceil(T / R) slots of own_cap doubles, each sized
+// for twice the mean period (periods beyond it take the global path), within the 227 KB opt-in
+static void pm_cluster_slots(int B, int T, int R, int *own_cap, size_t *smem) {
+    const int q = (T + R - 1) / R;
+    const size_t avail = PMC_SMEM_MAX - sizeof(PmcSmem) - 1024;
+    const size_t want = std::max<size_t>(6144, 2 * (((size_t)B + T - 1) / T));
+    const size_t cap = std::min(avail / (8 * (size_t)q), want);
+    *own_cap = (int)cap;
+    *smem = 8 * (size_t)q * cap;
+}
+
 template <int K, int R>
 static int launch_pm_cluster_r(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
-                               const EvalInit *init, int32_t *bad) {
+                               const EvalInit *init, int32_t *bad, int kk) {
     const EvalInit in = init ? *init : EvalInit{nullptr, nullptr, nullptr};
-    constexpr size_t smem = sizeof(double) * PMC_MAXQ * PMC_OWN;
+    int own_cap;
+    size_t smem;
+    pm_cluster_slots(c->B, c->T, R, &own_cap, &smem);
     TRY(ensure_max_smem(k_pm_cluster<K, R>, smem, c->device));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(R, np);
@@ -972,30 +1075,30 @@ static int launch_pm_cluster_r(pp_ctx *c, const int32_t *d_assign, int np, doubl
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k_pm_cluster<K, R>, d_assign, (const double *)c->mass.as<double>(),
-                                             c->B, c->T, c->compact.as<double>(), d_pm, in, bad);
+                                             c->B, c->T, kk, own_cap, c->compact.as<double>(), d_pm, in, bad);
     if (e != cudaSuccess) return fail(PP_ERR_CUDA, "k_pm_cluster launch: %s", cudaGetErrorString(e));
     return PP_OK;
 }
 
 // 16-CTA clusters halve each CTA's share of the blocks (the kernel is latency-bound on 8 SMs);
 // they need the non-portable opt-in and a GPC with 16 free SMs, probed once per device
+template <int K>
+static bool pm_r16_attr() {
+    return cudaFuncSetAttribute(k_pm_cluster<K, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+           cudaSuccess;
+}
 static bool pm_use_r16(int device) {
     static int cached[64];  // 0 unknown, 1 yes, 2 no
     if (device < 0 || device >= 64) return false;
     if (!cached[device]) {
-        bool ok = cudaFuncSetAttribute(k_pm_cluster<4, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                      cudaSuccess &&
-                  cudaFuncSetAttribute(k_pm_cluster<2, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                      cudaSuccess &&
-                  cudaFuncSetAttribute(k_pm_cluster<1, PMC_R16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                      cudaSuccess;
+        bool ok = pm_r16_attr<0>() && pm_r16_attr<1>() && pm_r16_attr<2>() && pm_r16_attr<4>() && pm_r16_attr<8>();
         if (ok) {
-            cudaFuncSetAttribute(k_pm_cluster<4, PMC_R16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * PMC_MAXQ * PMC_OWN));
+            const size_t smem = PMC_SMEM_MAX - sizeof(PmcSmem) - 1024;  // the largest launch
+            cudaFuncSetAttribute(k_pm_cluster<0, PMC_R16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(PMC_R16);
             cfg.blockDim = dim3(PMC_THREADS);
-            cfg.dynamicSmemBytes = sizeof(double) * PMC_MAXQ * PMC_OWN;
+            cfg.dynamicSmemBytes = smem;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = PMC_R16;
@@ -1004,7 +1107,7 @@ static bool pm_use_r16(int device) {
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int n = 0;
-            ok = cudaOccupancyMaxActiveClusters(&n, k_pm_cluster<4, PMC_R16>, &cfg) == cudaSuccess && n >= 1;
+            ok = cudaOccupancyMaxActiveClusters(&n, k_pm_cluster<0, PMC_R16>, &cfg) == cudaSuccess && n >= 1;
         }
         cudaGetLastError();
         cached[device] = ok ? 1 : 2;
@@ -1012,13 +1115,15 @@ static bool pm_use_r16(int device) {
     return cached[device] == 1;
 }
 
-template <int K>
+template <int R>
 static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double *d_pm, cudaStream_t st,
                              const EvalInit *init, int32_t *bad) {
-    // same K per thread with twice the CTAs covers twice the blocks: use K/2 at 16 CTAs
-    if (K > 1 && pm_use_r16(c->device))
-        return launch_pm_cluster_r<(K > 1 ? K / 2 : 1), PMC_R16>(c, d_assign, np, d_pm, st, init, bad);
-    return launch_pm_cluster_r<K, PMC_R>(c, d_assign, np, d_pm, st, init, bad);
+    const int per_lane = (c->B + R * PMC_THREADS - 1) / (R * PMC_THREADS);  // blocks per lane
+    if (per_lane <= 1) return launch_pm_cluster_r<1, R>(c, d_assign, np, d_pm, st, init, bad, 1);
+    if (per_lane <= 2) return launch_pm_cluster_r<2, R>(c, d_assign, np, d_pm, st, init, bad, 2);
+    if (per_lane <= 4) return launch_pm_cluster_r<4, R>(c, d_assign, np, d_pm, st, init, bad, 4);
+    if (per_lane <= PMC_KREG) return launch_pm_cluster_r<8, R>(c, d_assign, np, d_pm, st, init, bad, 8);
+    return launch_pm_cluster_r<0, R>(c, d_assign, np, d_pm, st, init, bad, per_lane);
 }
 
 int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cudaStream_t st, const EvalInit *init) {
@@ -1036,17 +1141,15 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
         c->pm_flags_n = nflags;
     }
     if (pm_cluster_path(c)) {
-        const int K = B <= PMC_MAXB / 8 ? 1 : B <= PMC_MAXB / 4 ? 2 : B <= PMC_MAXB / 2 ? 4 : 8;
+        const bool r16 = pm_use_r16(c->device);
         for (int p0 = 0; p0 < P; p0 += pchunk) {
             const int np = std::min(pchunk, P - p0);
             const int32_t *a = d_assign + (size_t)p0 * B;
             double *o = d_pm + (size_t)p0 * T;
             const EvalInit *z = p0 == 0 ? init : nullptr;
             int32_t *bad = (P == 1 && d_assign == c->assign_ptr && c->bad_pending) ? c->pm_bad.as<int32_t>() : nullptr;
-            if (K == 1) TRY(launch_pm_cluster<1>(c, a, np, o, st, z, bad));
-            else if (K == 2) TRY(launch_pm_cluster<2>(c, a, np, o, st, z, bad));
-            else if (K == 4) TRY(launch_pm_cluster<4>(c, a, np, o, st, z, bad));
-            else TRY(launch_pm_cluster<8>(c, a, np, o, st, z, bad));
+            if (r16) TRY(launch_pm_cluster<PMC_R16>(c, a, np, o, st, z, bad));
+            else TRY(launch_pm_cluster<PMC_R>(c, a, np, o, st, z, bad));
         }
         return PP_OK;
     }
@@ -1066,7 +1169,10 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
 }
 
 // recompute the current schedule's period masses if the schedule changed
-bool pm_cluster_path(const pp_ctx *c) { return c->T <= PMC_MAXT && c->B <= PMC_MAXB; }
+bool pm_cluster_path(const pp_ctx *c) {
+    static const bool off = getenv("PP_PM_NOCLUSTER") != nullptr;  // A/B timing of the chunk + tree kernel
+    return c->T <= PMC_MAXT && c->B <= PMC_MAXN && !off;
+}
 
 int check_schedule_range(pp_ctx *c, bool copied) {
     if (!c->bad_pending || c->pm_dirty) return PP_OK;  // not range-checked yet

@@ -361,11 +361,15 @@ def _flat_bm(B, T, seed):
 
 
 @pytest.mark.parametrize("B,T", [(1, 1), (100, 3), (8192, 15), (8193, 16), (16385, 9), (50000, 15),
-                                 (65536, 8), (65536, 16), (65537, 15), (70000, 17), (5000, 40)])
+                                 (65536, 8), (65536, 16), (65537, 15), (70000, 17), (5000, 40),
+                                 (131072, 20), (131073, 20), (200000, 20), (200000, 1), (245760, 32),
+                                 (100000, 33), (245761, 15)])
 def test_period_mass_paths(oracle_lib, B, T):
-    """numpy-pairwise period masses on both device paths (the 8-CTA cluster path for
-    B <= 65536 and T <= 16, the look-back path otherwise): uniform, skewed (one period
-    holding almost every block, the deepest pairwise tree), all unmined, ragged tails."""
+    """numpy-pairwise period masses on both device paths (the cluster path for B <= 245,760 and
+    T <= 32 -- registers up to 8 blocks per lane, the count + scatter passes above; slots in
+    shared memory or the global spill; the one-level pre-fold for periods above ~123k blocks --
+    and the look-back path otherwise): uniform, skewed (one period holding almost every block,
+    the deepest pairwise tree), all unmined, ragged tails."""
     bm = _flat_bm(B, T, B + T)
     rng = np.random.default_rng(B * 7 + T)
     pop = [rng.integers(-1, T, B), np.where(rng.random(B) < 0.97, T - 1, rng.integers(-1, T, B)),
