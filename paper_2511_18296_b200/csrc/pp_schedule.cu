@@ -704,7 +704,8 @@ constexpr int PMC_THREADS = 1024;
 constexpr int PMC_WARPS = PMC_THREADS / 32;
 constexpr int PMC_MAXT = 32;
 constexpr int PMC_MAXQ = (PMC_MAXT + PMC_R - 1) / PMC_R;  // periods per CTA
-constexpr int PMC_MAXNODE = 1024;  // 2^D <= n / 240: periods of up to 245,760 blocks
+constexpr int PMC_MAXNODE = 1024;  // 2^D <= n / 240: periods of up to 245,760 blocks (global mode)
+constexpr int PMC_PUSHNODE = 128;  // push mode: n <= own_cap < 30,720
 constexpr int PMC_MAXN = 245760;
 constexpr int PMC_FOLD = 512;      // node values one warp folds (16 per lane)
 constexpr int PMC_KREG = 8;        // blocks per lane kept in registers
@@ -717,8 +718,11 @@ struct PmcSmem {
     int tot[PMC_MAXT];  // this CTA's count per period (read by the cluster)
     int off[PMC_MAXT];  // this CTA's first position per period
     int n[PMC_MAXT];
-    double val[PMC_MAXQ][PMC_MAXNODE];
+    double val[PMC_MAXQ][PMC_PUSHNODE];  // node values in push mode (global mode: the slot area)
 };
+
+// the lanes of the warp holding the same period (six ballots over the bits measured slower)
+__device__ __forceinline__ unsigned match_period(int t) { return __match_any_sync(0xffffffffu, t); }
 
 __device__ __forceinline__ void cluster_sync_acqrel() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -771,18 +775,22 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     }
     asm volatile("griddepcontrol.launch_dependents;");
     constexpr unsigned FULL = 0xffffffffu;
-    constexpr int KR = K > 0 ? K : 1;
+    constexpr bool REG = K > 0 && K <= PMC_KREG;  // periods, masses and ranks in registers
+    constexpr bool PACK = K > PMC_KREG;            // ranks packed 2 per register, blocks re-read
+    constexpr int KR = REG ? K : 1;
+    static_assert(K <= 2 * PMC_GRP, "packed ranks cover two load groups");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = blockIdx.x, p = blockIdx.y;
     const int32_t *as = assign + (size_t)p * B;
-    const int KB = K > 0 ? K : kk;
+    const int KB = REG ? K : kk;
     const int base = (r * PMC_WARPS + warp) * (32 * KB);
     const unsigned lt = (1u << lane) - 1u;
     int tk[KR];
     double mk[KR];
     int pos[KR];
     int badl = 0;
-    if constexpr (K > 0) {
+    unsigned pk[PMC_GRP] = {};  // PACK: rank of block k in bits 16 (k & 1) of pk[k >> 1]
+    if constexpr (REG) {
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const int b = base + k * 32 + lane;
@@ -800,16 +808,40 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     PMCS(0);
     for (int i = tid; i < PMC_WARPS * PMC_MAXT; i += PMC_THREADS) (&h.cnt[0][0])[i] = 0;
     __syncthreads();
-    if constexpr (K > 0) {  // ranks inside (warp, period): match_any groups, running counts in shared memory
+    if constexpr (REG) {  // ranks inside (warp, period): match_any groups, running counts in shared memory
 #pragma unroll
         for (int k = 0; k < K; k++) {
-            const unsigned mt = __match_any_sync(FULL, tk[k]);
+            const unsigned mt = match_period(tk[k]);
             const int lr = __popc(mt & lt);
             const int b0 = tk[k] >= 0 ? h.cnt[warp][tk[k]] : 0;
             pos[k] = b0 + lr;
             __syncwarp();
             if (tk[k] >= 0 && lr == 0) h.cnt[warp][tk[k]] = b0 + __popc(mt);
             __syncwarp();
+        }
+    } else if constexpr (PACK) {  // the same ranks, PMC_GRP loads in flight per lane, kept packed
+#pragma unroll
+        for (int k0 = 0; k0 < 2 * PMC_GRP; k0 += PMC_GRP) {
+            if (k0 >= kk) break;
+            int tq[PMC_GRP];
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int b = base + (k0 + u) * 32 + lane;
+                tq[u] = (k0 + u < kk && b < B) ? __ldg(as + b) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int t = tq[u];
+                badl |= (t < -1) | (t >= T);
+                const int tv = ((unsigned)t < (unsigned)T) ? t : -1;
+                const unsigned mt = match_period(tv);
+                const int lr = __popc(mt & lt);
+                const int b0 = tv >= 0 ? h.cnt[warp][tv] : 0;
+                __syncwarp();
+                if (tv >= 0 && lr == 0) h.cnt[warp][tv] = b0 + __popc(mt);
+                __syncwarp();
+                pk[(k0 + u) >> 1] |= (unsigned)(b0 + lr) << (16 * ((k0 + u) & 1));
+            }
         }
     } else {  // count pass: PMC_GRP loads in flight per lane
         for (int k0 = 0; k0 < kk; k0 += PMC_GRP) {
@@ -824,7 +856,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
                 const int t = tq[u];
                 badl |= (t < -1) | (t >= T);
                 const int tv = ((unsigned)t < (unsigned)T) ? t : -1;
-                const unsigned mt = __match_any_sync(FULL, tv);
+                const unsigned mt = match_period(tv);
                 if (tv >= 0 && __popc(mt & lt) == 0) h.cnt[warp][tv] += __popc(mt);
                 __syncwarp();
             }
@@ -867,7 +899,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
     // straight into the shared memory of the CTA that reduces its period; otherwise through L2
     bool push = true;
     for (int t = 0; t < T; t++) push &= h.n[t] <= own_cap;
-    if constexpr (K > 0) {
+    if constexpr (REG) {
 #pragma unroll
         for (int k = 0; k < K; k++)
             if (tk[k] >= 0) {
@@ -875,6 +907,30 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
                 if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mk[k]);
                 else compact[((size_t)p * T + t) * B + at] = mk[k];
             }
+    } else if constexpr (PACK) {  // scatter pass: re-read the blocks (L2), ranks from the first pass
+#pragma unroll
+        for (int k0 = 0; k0 < 2 * PMC_GRP; k0 += PMC_GRP) {
+            if (k0 >= kk) break;
+            int tq[PMC_GRP];
+            double mq[PMC_GRP];
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int b = base + (k0 + u) * 32 + lane;
+                const bool in = k0 + u < kk && b < B;
+                const int t = in ? __ldg(as + b) : -1;
+                tq[u] = ((unsigned)t < (unsigned)T) ? t : -1;
+                mq[u] = in ? __ldg(mass + b) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < PMC_GRP; u++) {
+                const int t = tq[u];
+                if (t >= 0) {
+                    const int at = h.off[t] + h.cnt[warp][t] + (int)((pk[(k0 + u) >> 1] >> (16 * ((k0 + u) & 1))) & 0xffffu);
+                    if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mq[u]);
+                    else compact[((size_t)p * T + t) * B + at] = mq[u];
+                }
+            }
+        }
     } else {  // scatter pass: re-read, rank again (same groups), h.cnt[warp][t] is the running position
         for (int k0 = 0; k0 < kk; k0 += PMC_GRP) {
             int tq[PMC_GRP];
@@ -890,7 +946,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
 #pragma unroll
             for (int u = 0; u < PMC_GRP; u++) {
                 const int t = tq[u];
-                const unsigned mt = __match_any_sync(FULL, t);
+                const unsigned mt = match_period(t);
                 const int lr = __popc(mt & lt);
                 const int w0 = t >= 0 ? h.cnt[warp][t] : 0;
                 __syncwarp();
@@ -917,18 +973,24 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         Dg[g] = 0;
         cntg[g] = 0;
         if (g < q) {
+            // d = first depth whose rightmost node is a leaf: 8 ceil(m / 2^d) + rem <= 128, i.e.
+            // 2^d >= ceil(m / thr) with thr = 16 when rem = 0, else 15
             const int n = h.n[r + R * g], m = n >> 3, rem = n & 7;
-            int d = 0;
-            while (8 * ((m + (1 << d) - 1) >> d) + rem > 128) d++;
+            const int thr = rem ? 15 : 16, qd = (m + thr - 1) / thr;
+            const int d = qd <= 1 ? 0 : 32 - __clz(qd - 1);
             Dg[g] = max(d - 1, 0);
             cntg[g] = 1 << Dg[g];
         }
         nitems += cntg[g];
     }
+    // node values: push mode in h.val; global mode in the (then unused) slot area, own_cap apart
+    double *const nodes = push ? &h.val[0][0] : pmc_own;
+    const int nstride = push ? PMC_PUSHNODE : own_cap;
     PMCS(4);
     const int sub = tid & 7, half = (tid >> 3) & 1;  // 16 lanes per node: half c sums child leaf c
     for (int it0 = 0; it0 < nitems; it0 += PMC_THREADS / 16) {
         const int it = it0 + (tid >> 4);
+        if (it0 + 2 * warp >= nitems) continue;  // warp-uniform: this warp's two nodes are past the end
         const bool act = it < nitems;
         int g = 0, i = act ? it : 0, D = Dg[0];  // (unrolled selects: no local-memory indexing)
         bool fnd = false;
@@ -945,19 +1007,21 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             }
         const int t = r + R * g;
         const int n = act ? h.n[t] : 0, m = n >> 3, rem = n & 7;
-        int s0, l0;
-        pw_node(m, D, i, s0, l0);
+        // half c walks to child 2i + c at depth D + 1; the node is the union of the two halves
+        int s1, l1;
+        pw_node(m, D + 1, 2 * i + half, s1, l1);
+        const int s_sib = __shfl_xor_sync(FULL, s1, 8), l_sib = __shfl_xor_sync(FULL, l1, 8);
+        const int s0 = half ? s_sib : s1, l0 = l1 + l_sib;
         const bool last = i == (1 << D) - 1;
         const int L = 8 * l0 + (last ? rem : 0);
         const bool split = L > 128;  // a node of depth D is one leaf or two
         int o = 8 * s0, len = L;
         if (split) {
-            int s1, l1;
-            pw_node(m, D + 1, 2 * i + half, s1, l1);
             o = 8 * s1;
             len = 8 * l1 + ((last && half == 1) ? rem : 0);
         }
         const bool use = act && (split || half == 0);
+        if (it0 == 0) PMCS(6);
         // every load of the leaf in flight: 16 accumulator elements per lane + one tail element
         // (separate shared / global paths: a pointer that may be either compiles to slow generic loads)
         const int nm = len >> 3, ntail = len & 7, e0 = len - ntail;
@@ -977,6 +1041,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
 #pragma unroll
         for (int u = 1; u < 16; u++)
             if (u < nm) acc = f64_add(acc, x[u]);
+        if (it0 == 0) PMCS(7);
         acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 1));
         acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 2));
         acc = f64_add(acc, __shfl_xor_sync(FULL, acc, 4));
@@ -986,8 +1051,9 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             const double y = __shfl_sync(FULL, tailv, lbase + e);
             if (e < ntail) res = f64_add(res, y);
         }
+        if (it0 == 0) PMCS(8);
         const double other = __shfl_xor_sync(FULL, res, 8);  // the sibling leaf
-        if (use && sub == 0 && half == 0) h.val[g][i] = split ? f64_add(res, other) : res;
+        if (use && sub == 0 && half == 0) nodes[g * nstride + i] = split ? f64_add(res, other) : res;
     }
     PMCS(5);
     __syncthreads();
@@ -997,7 +1063,9 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         double y[PMC_MAXQ];
 #pragma unroll
         for (int g = 0; g < PMC_MAXQ; g++)
-            y[g] = (cntg[g] > PMC_FOLD && tid < cntg[g] / 2) ? f64_add(h.val[g][2 * tid], h.val[g][2 * tid + 1]) : 0.0;
+            y[g] = (cntg[g] > PMC_FOLD && tid < cntg[g] / 2)
+                       ? f64_add(nodes[g * nstride + 2 * tid], nodes[g * nstride + 2 * tid + 1])
+                       : 0.0;
         bool any = false;
 #pragma unroll
         for (int g = 0; g < PMC_MAXQ; g++) any |= cntg[g] > PMC_FOLD;
@@ -1005,7 +1073,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
             __syncthreads();
 #pragma unroll
             for (int g = 0; g < PMC_MAXQ; g++)
-                if (cntg[g] > PMC_FOLD && tid < cntg[g] / 2) h.val[g][tid] = y[g];
+                if (cntg[g] > PMC_FOLD && tid < cntg[g] / 2) nodes[g * nstride + tid] = y[g];
             __syncthreads();
 #pragma unroll
             for (int g = 0; g < PMC_MAXQ; g++)
@@ -1025,7 +1093,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         if (lane * per < cnt) {
             double x[16];
 #pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = (u < per) ? h.val[g][lane * per + u] : 0.0;
+            for (int u = 0; u < 16; u++) x[u] = (u < per) ? nodes[g * nstride + lane * per + u] : 0.0;
 #pragma unroll
             for (int w = 1; w < 16; w <<= 1)
 #pragma unroll
@@ -1048,7 +1116,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
 static void pm_cluster_slots(int B, int T, int R, int *own_cap, size_t *smem) {
     const int q = (T + R - 1) / R;
     const size_t avail = PMC_SMEM_MAX - sizeof(PmcSmem) - 1024;
-    const size_t want = std::max<size_t>(6144, 2 * (((size_t)B + T - 1) / T));
+    const size_t want = std::min<size_t>(30720, std::max<size_t>(6144, 2 * (((size_t)B + T - 1) / T)));  // PMC_PUSHNODE
     const size_t cap = std::min(avail / (8 * (size_t)q), want);
     *own_cap = (int)cap;
     *smem = 8 * (size_t)q * cap;
@@ -1091,7 +1159,7 @@ static bool pm_use_r16(int device) {
     static int cached[64];  // 0 unknown, 1 yes, 2 no
     if (device < 0 || device >= 64) return false;
     if (!cached[device]) {
-        bool ok = pm_r16_attr<0>() && pm_r16_attr<1>() && pm_r16_attr<2>() && pm_r16_attr<4>() && pm_r16_attr<8>();
+        bool ok = pm_r16_attr<0>() && pm_r16_attr<2 * PMC_GRP>() && pm_r16_attr<1>() && pm_r16_attr<2>() && pm_r16_attr<4>() && pm_r16_attr<8>();
         if (ok) {
             const size_t smem = PMC_SMEM_MAX - sizeof(PmcSmem) - 1024;  // the largest launch
             cudaFuncSetAttribute(k_pm_cluster<0, PMC_R16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1123,6 +1191,7 @@ static int launch_pm_cluster(pp_ctx *c, const int32_t *d_assign, int np, double 
     if (per_lane <= 2) return launch_pm_cluster_r<2, R>(c, d_assign, np, d_pm, st, init, bad, 2);
     if (per_lane <= 4) return launch_pm_cluster_r<4, R>(c, d_assign, np, d_pm, st, init, bad, 4);
     if (per_lane <= PMC_KREG) return launch_pm_cluster_r<8, R>(c, d_assign, np, d_pm, st, init, bad, 8);
+    if (per_lane <= 2 * PMC_GRP) return launch_pm_cluster_r<2 * PMC_GRP, R>(c, d_assign, np, d_pm, st, init, bad, per_lane);
     return launch_pm_cluster_r<0, R>(c, d_assign, np, d_pm, st, init, bad, per_lane);
 }
 

@@ -17,19 +17,25 @@ cand_d = torch.from_numpy(c["cand"]).to(dev)
 out = {"best_t": torch.empty(C, dtype=torch.int32, device=dev), "best_val": torch.empty(C, dtype=torch.float64, device=dev),
        "feasible": torch.empty(C, dtype=torch.uint8, device=dev), "exp_delta": torch.empty(C, T, dtype=torch.float64, device=dev),
        "cvar": torch.empty(C, T, dtype=torch.float64, device=dev), "global": torch.empty(2, dtype=torch.float64, device=dev)}
+pm_out = torch.empty(T, dtype=torch.float64, device=dev)
 flush = torch.empty(256 << 18, dtype=torch.int32, device=dev)
 grid = (C + 31) // 32  # k_eval_warp: 32 candidates per CTA
 g = torch.cuda.CUDAGraph()
 for _ in range(3):
     eng.set_schedule_device(assign_d, stream=sp, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=sp)
+    eng.period_mass_device(pm_out, stream=sp)
 st.synchronize()
 with torch.cuda.graph(g):
     cs = torch.cuda.current_stream().cuda_stream
-    eng.set_schedule_device(assign_d, stream=cs, borrow=True); eng.eval_candidates_device(cand_d, out, None, net=True, stream=cs)
+    eng.set_schedule_device(assign_d, stream=cs, borrow=True)
+    if "pmonly" in sys.argv:  # the period-mass kernel alone (no concurrent evaluation CTAs)
+        eng.period_mass_device(pm_out, stream=cs)
+    else:
+        eng.eval_candidates_device(cand_d, out, None, net=True, stream=cs)
 lib.pp_debug_stamp.argtypes = [ctypes.c_void_p, ctypes.c_int]; lib.pp_debug_stamps.argtypes = [ctypes.c_void_p]
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 for rep in range(4):
-    flush.fill_(rep)
+    if "noflush" not in sys.argv: flush.fill_(rep)
     lib.pp_debug_stamp(sp, 0)
     if "noevents" not in sys.argv: e0.record(st)
     if "eager" in sys.argv:
@@ -42,13 +48,15 @@ for rep in range(4):
 stamps = np.zeros(8, np.uint64); lib.pp_debug_stamps(stamps.ctypes.data); stamps = stamps.astype(np.int64)
 print(f"event elapsed {e0.elapsed_time(e1) * 1000 if 'noevents' not in sys.argv else 0:.2f} us; stamp-to-stamp {(stamps[1] - stamps[0]) / 1000:.2f} us")
 ev = np.zeros((4096, 12), np.uint64); lib.pp_debug_eval_probe(ev.ctypes.data); ev = ev[:grid].astype(np.int64)
+if "pmonly" in sys.argv:
+    ev[:] = ev.max()
 pm = np.zeros((2, 512, 2), np.uint64); lib.pp_debug_pm_probe(pm.ctypes.data); pm = pm.astype(np.int64)
 nr = int((pm[0, :16, 0] > 0).sum())
 cl = nr >= 8
 if cl:  # cluster path: 8 CTAs, [0][r] = (start, scatter done), [1][r][1] = trees done
     t0 = min(pm[0, :nr, 0].min(), ev[:, 0].min())
     f = lambda x: (x - t0) / 1000
-    for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves", "pre-leaf", "leaf-t0"]):
+    for k, nm in enumerate(["loaded", "ranked+bar", "offsets", "leaves", "pre-leaf", "leaf-t0", "leaf-addr", "leaf-sum", "leaf-tail"]):
         v = pm[1, 16 + 16 * k:32 + 16 * k, 0]
         v = v[v > 0]
         print(f"  pm {nm:8s} {f(v.min()):.2f}..{f(v.max()):.2f} us" + ("   per CTA: " + " ".join(f"{f(x):.1f}" for x in v) if "percta" in sys.argv else ""))
