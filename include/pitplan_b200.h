@@ -132,6 +132,11 @@ PP_API int pp_ctx_stream(pp_ctx *ctx, void **stream);          /* the context's 
 PP_API int pp_synchronize(pp_ctx *ctx, void *stream);
 PP_API int pp_host_alloc(size_t bytes, void **ptr);             /* pinned host memory */
 PP_API int pp_host_free(void *ptr);
+/* Diagnostic (no reference counterpart): in the checked build (libpitplan_b200_checked.so,
+ * -DPP_CHECKED) verifies the 512-byte guard zones around every live device buffer and returns the
+ * number of overwritten guards found so far (also checked at every free / re-allocation);
+ * PP_ERR_STATE in the release build. */
+PP_API int pp_debug_check_guards(int64_t *n_bad);
 
 /* ---- static tables (host pointers) ------------------------------------------------
  * Instance: precedence edge list in reference order (blockmodel.py:94, 180-184),

@@ -16,6 +16,10 @@ from .errors import ExtensionMissing, raise_for_status
 
 LIB_NAME = "libpitplan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PP_LIB: load another build of the same ABI instead (the checked build for the guard-zone run:
+# PP_LIB=paper_2511_18296_b200/libpitplan_b200_checked.so)
+if os.environ.get("PP_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["PP_LIB"])
 
 ABI_VERSION = 3  # include/pitplan_b200.h PP_ABI_VERSION
 PP_MEM_HOST = 0
@@ -84,6 +88,7 @@ SIGNATURES = {
     "pp_synchronize": (c_int32, [c_void_p, c_void_p]),
     "pp_host_alloc": (c_int32, [c_size_t, ctypes.POINTER(c_void_p)]),
     "pp_host_free": (c_int32, [c_void_p]),
+    "pp_debug_check_guards": (c_int32, [ctypes.POINTER(c_int64)]),
     "pp_set_instance": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p]),
     "pp_set_geology": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,

@@ -66,6 +66,51 @@ void *pinned_lookup(const void *host) {
     return nullptr;
 }
 
+#ifdef PP_CHECKED
+// guard-zone registry of the live device buffers (checked builds only)
+namespace {
+std::mutex g_guard_mu;
+std::vector<DevBuf *> g_guard_bufs;
+long long g_guard_bad = 0;  // corrupted guards found so far (at free / re-allocation / explicit checks)
+}  // namespace
+
+void guard_register(DevBuf *b) {
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    g_guard_bufs.push_back(b);
+}
+
+void guard_unregister(DevBuf *b) {
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    for (size_t i = 0; i < g_guard_bufs.size(); i++)
+        if (g_guard_bufs[i] == b) {
+            g_guard_bufs.erase(g_guard_bufs.begin() + (long)i);
+            return;
+        }
+}
+
+bool guard_intact(const DevBuf *b) {
+    if (!b->base) return true;
+    std::vector<unsigned char> h(2 * PP_GUARD);
+    if (cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(h.data(), b->base, PP_GUARD, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(h.data() + PP_GUARD, static_cast<const unsigned char *>(b->ptr) + b->bytes, PP_GUARD,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+        return true;  // a sticky CUDA error is reported by the call that hit it
+    size_t first = SIZE_MAX, nbad = 0;
+    for (size_t i = 0; i < h.size(); i++)
+        if (h[i] != 0xA5) {
+            nbad++;
+            if (first == SIZE_MAX) first = i;
+        }
+    if (!nbad) return true;
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    g_guard_bad++;
+    fprintf(stderr, "[pp checked] guard of a %zu-byte buffer overwritten: %zu bytes, first at %s%zd\n", b->bytes, nbad,
+            first < PP_GUARD ? "payload-" : "payload end+", first < PP_GUARD ? (ssize_t)(PP_GUARD - first) : (ssize_t)(first - PP_GUARD));
+    return false;
+}
+#endif
+
 int ensure_grid_scratch(pp_ctx *c, int grid) {
     TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
     if (c->counter.bytes == 0) {
@@ -119,6 +164,24 @@ int check_ready(pp_ctx *c, uint32_t flags, int scenario) {
 extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+int pp_debug_check_guards(int64_t *n_bad) {
+#ifdef PP_CHECKED
+    if (!n_bad) return fail(PP_ERR_INVALID_ARGS, "n_bad is NULL");
+    std::vector<DevBuf *> bufs;
+    {
+        std::lock_guard<std::mutex> lock(g_guard_mu);
+        bufs = g_guard_bufs;
+    }
+    for (DevBuf *b : bufs) guard_intact(b);
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    *n_bad = g_guard_bad;
+    return PP_OK;
+#else
+    (void)n_bad;
+    return fail(PP_ERR_STATE, "not a checked build (build_checked(): libpitplan_b200_checked.so)");
+#endif
+}
 
 const char *pp_last_error(void) { return g_last_error.c_str(); }
 

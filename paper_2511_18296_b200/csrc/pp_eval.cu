@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                 const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
                 for (int j = 0; j < CPW; j++)
-                    if ((win[j] >> lane) & 1u) s_pair[base + cum[j] + __popc(win[j] & lt)] = ((warp * CPW + j) << 8) | lane;
+                    if ((win[j] >> lane) & 1u) {
+                        PP_DCHECK(base + cum[j] + __popc(win[j] & lt) < NW * CPW * 32);
+                        s_pair[base + cum[j] + __popc(win[j] & lt)] = ((warp * CPW + j) << 8) | lane;
+                    }
             }
             __syncthreads();
             EV_PROBE(8);
@@ -629,6 +632,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
         int q = pbase + incl - cnt;
         for (unsigned mm = m; mm; mm &= mm - 1, q++) {
             const int t = __ffs(mm) - 1;
+            PP_DCHECK(q < p.C * p.T && t < p.T);
             p.pair_cand[q] = blockIdx.x * NW * CPW + lane;
             p.pair_period[q] = t;
             p.pair_exp[q] = wex[t];

@@ -572,23 +572,71 @@ struct MoveParams {
 // ------------------------------------------------------------------------------------
 // host side: context
 // ------------------------------------------------------------------------------------
+// Checked builds (-DPP_CHECKED, __graft_entry__.build_checked(): libpitplan_b200_checked.so) stand
+// in for compute-sanitizer memcheck, which this GPU pool does not offer: every device buffer gets
+// 512-byte guard zones on both sides (pattern 0xA5) whose bytes are verified when the buffer is
+// freed or re-allocated and by pp_debug_check_guards; fresh payloads are filled with 0xFF (NaN /
+// -1) so reads of never-written memory surface as parity failures; PP_DCHECK traps on a failed
+// device-side index check.
+#ifdef PP_CHECKED
+constexpr size_t PP_GUARD = 512;
+struct DevBuf;
+void guard_register(DevBuf *b);
+void guard_unregister(DevBuf *b);
+bool guard_intact(const DevBuf *b);  // false: the guard bytes were overwritten (reported once)
+#define PP_DCHECK(c)                                                                                      \
+    do {                                                                                                  \
+        if (!(c)) {                                                                                       \
+            printf("PP_DCHECK failed %s:%d: %s (block %d,%d thread %d)\n", __FILE__, __LINE__, #c,           \
+                   (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                     \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define PP_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;
     uint64_t gen = 0;  // bumped on every (re)allocation: caches keyed on a buffer compare this, not ptr
+#ifdef PP_CHECKED
+    void *base = nullptr;  // allocation start: [guard][payload: bytes][guard]
+    DevBuf() { guard_register(this); }
+    ~DevBuf() { guard_unregister(this); }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+#endif
     int ensure(size_t need) {
         if (need <= bytes) return PP_OK;
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        bytes = 0;
+        release();
         gen++;
         size_t n = std::max<size_t>(need, 256);
+#ifdef PP_CHECKED
+        CUDA_TRY(cudaMalloc(&base, n + 2 * PP_GUARD));
+        ptr = static_cast<unsigned char *>(base) + PP_GUARD;
+        CUDA_TRY(cudaMemset(base, 0xA5, PP_GUARD));
+        CUDA_TRY(cudaMemset(static_cast<unsigned char *>(ptr) + n, 0xA5, PP_GUARD));
+        CUDA_TRY(cudaMemset(ptr, 0xFF, n));
+        CUDA_TRY(cudaDeviceSynchronize());
+#else
         CUDA_TRY(cudaMalloc(&ptr, n));
+#endif
         bytes = n;
         return PP_OK;
     }
     void release() {
+#ifdef PP_CHECKED
+        if (base) {
+            guard_intact(this);
+            cudaFree(base);
+        }
+        base = nullptr;
+#else
         if (ptr) cudaFree(ptr);
+#endif
         ptr = nullptr;
         bytes = 0;
     }

@@ -274,9 +274,8 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
                     for (int s_ = 0; s_ < S; s_++) p.scen_delta[(size_t)i * S + s_] = -__int_as_float(0x7f800000);
             }
         }
-        if (!STATS) continue;
         // statistics of this step's feasible moves, the warp on one move at a time
-        for (unsigned fm = __ballot_sync(FULL, ok); fm; fm &= fm - 1) {
+        for (unsigned fm = STATS ? __ballot_sync(FULL, ok) : 0u; fm; fm &= fm - 1) {
             const int src = __ffs(fm) - 1;
             const int mi = base + src;
             const int c1 = __shfl_sync(FULL, b1, src), c2 = __shfl_sync(FULL, b2, src);

@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
                             hi = md;
                     }
                     int ia = lo, ib = d0 - lo;
+                    PP_DCHECK(ia >= 0 && ia <= la && ib >= 0 && ib <= lb && m0 + d1 <= np_ && np_ <= B);
                     for (int k = d0; k < d1; k++) {
                         const bool takeA = ib >= lb || (ia < la && s2_before(Ak[ia], Ab[ia], Bk[ib], Bb[ib]));
                         if (takeA) {
@@ -730,12 +731,14 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
     const int b = blocks[si >> 1];
     const size_t st_ = (size_t)s * T + t, base = st_ * rec.L;
     const int np = rec.npos[st_], K = rec.K[st_];
+    PP_DCHECK(np >= 0 && np < rec.L && K >= 0 && K <= np);
     const double *D = rec.D + base, *Mm = rec.M + base;
     const bool ins = si & 1;
     double dnew = 0.0, mnew = 0.0;
     int j;
     if (!ins) {
         j = rec.pos[(size_t)s * B + b];
+        PP_DCHECK(j < 0 || (j < np && rec.BID[base + j] == b));  // pos[] points at b's place
     } else {
         mnew = __ldg(mass + b);
         dnew = f64_div(__ldg(vmax + (size_t)b * Sp + s), mnew);
@@ -767,6 +770,7 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
             m = mnew;
         } else {
             const int k = ins ? j + e - 1 : j + 1 + e;
+            PP_DCHECK(k >= 0 && k < np);
             d = D[k];
             m = Mm[k];
         }
@@ -846,6 +850,7 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         const double *csl = rec.CS + (size_t)t * rec.L;
         const double cb = __ldg(cost + (size_t)b * T + t);
         const int n0 = rec.nper[t];
+        PP_DCHECK(n0 >= 0 && n0 < rec.L && (n0 + 1) / 64 + 2 <= cap);
         int lo = 0, hi = n0;  // block-order position of b
         while (lo < hi) {
             const int md = (lo + hi) >> 1;
@@ -854,6 +859,7 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         }
         const int r = lo;
         const bool ins = si & 1;
+        PP_DCHECK(ins || (r < n0 && ids[r] == b));  // a removed block is in its period's list
         const int n = ins ? n0 + 1 : n0 - 1;
         const double cs = s2_pairwise_f(
             [&](int k) { return ins ? (k < r ? csl[k] : (k == r ? cb : csl[k - 1])) : csl[k < r ? k : k + 1]; },
@@ -906,7 +912,6 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
                                   const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                                   const double *__restrict__ disc,
                                   const double *__restrict__ sigma, double *__restrict__ npv) {
-    constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int m = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (m >= M) return;
@@ -1077,6 +1082,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     double *D = rec.D + base, *M_ = rec.M + base, *H = rec.H + base, *TT = rec.TT + base;
     int32_t *BI = rec.BID + base;
     const int np = rec.npos[st_];
+    PP_DCHECK(np >= 0 && np + 1 < rec.L);
     const double mb = __ldg(mass + b);
     const double db = f64_div(__ldg(vmax + (size_t)b * Sp + s), mb);
     // 1. the place of b in the greedy order
@@ -1096,11 +1102,13 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
             }
             j = lo;
         }
+        PP_DCHECK(ins || j < 0 || (j < np && BI[j] == b));
         s_j = j;
     }
     __syncthreads();
     const int j = s_j;
     const int K = rec.K[st_];
+    PP_DCHECK(K >= 0 && K <= np);
     if (j >= 0) {
         // 2. splice the order (D, M, BID) and renumber the shifted blocks' positions
         if (!ins) {
@@ -1177,6 +1185,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     }
     __syncthreads();
     const int r = s_j;
+    PP_DCHECK(n0 >= 0 && n0 + 1 < 16000 && (ins || (r < n0 && ids[r] == b)));
     if (!ins) {
         for (int k0 = r; k0 < n0 - 1; k0 += S2_THREADS) {
             const int k = k0 + tid;

@@ -904,6 +904,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         for (int k = 0; k < K; k++)
             if (tk[k] >= 0) {
                 const int t = tk[k], at = h.off[t] + h.cnt[warp][t] + pos[k];
+                PP_DCHECK(at >= 0 && at < h.n[t] && (!push || at < own_cap));
                 if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mk[k]);
                 else compact[((size_t)p * T + t) * B + at] = mk[k];
             }
@@ -926,6 +927,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
                 const int t = tq[u];
                 if (t >= 0) {
                     const int at = h.off[t] + h.cnt[warp][t] + (int)((pk[(k0 + u) >> 1] >> (16 * ((k0 + u) & 1))) & 0xffffu);
+                    PP_DCHECK(at >= 0 && at < h.n[t] && (!push || at < own_cap));
                     if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mq[u]);
                     else compact[((size_t)p * T + t) * B + at] = mq[u];
                 }
@@ -952,6 +954,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
                 __syncwarp();
                 if (t >= 0) {
                     const int at = h.off[t] + w0 + lr;
+                    PP_DCHECK(at >= 0 && at < h.n[t] && (!push || at < own_cap));
                     if (push) st_dsmem_f64(pmc_own + (t / R) * own_cap + at, t % R, mq[u]);
                     else compact[((size_t)p * T + t) * B + at] = mq[u];
                     if (lr == 0) h.cnt[warp][t] = w0 + __popc(mt);
@@ -1053,6 +1056,7 @@ __global__ void __launch_bounds__(PMC_THREADS, 1)
         }
         if (it0 == 0) PMCS(8);
         const double other = __shfl_xor_sync(FULL, res, 8);  // the sibling leaf
+        PP_DCHECK(!use || (i < nstride && o + len <= n && (!push || o + len <= own_cap)));
         if (use && sub == 0 && half == 0) nodes[g * nstride + i] = split ? f64_add(res, other) : res;
     }
     PMCS(5);
