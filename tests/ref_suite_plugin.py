@@ -23,3 +23,18 @@ def pytest_unconfigure(config):
     if out:
         with open(out, "w") as fh:
             json.dump({"patched": getattr(config, "_pp_patched", []), **ev.path_counters()}, fh, indent=1)
+
+
+def pytest_runtest_teardown(item):
+    """With the checked library (PP_LIB=...checked.so): a guard-zone sweep after every test."""
+    if "checked" not in os.environ.get("PP_LIB", ""):
+        return
+    import ctypes
+
+    from paper_2511_18296_b200 import _lib
+
+    if _lib._lib is None:
+        return
+    n = ctypes.c_int64(0)
+    assert _lib._lib.pp_debug_check_guards(ctypes.byref(n)) == 0, _lib._lib.pp_last_error()
+    assert n.value == 0, f"{n.value} device buffer guard zone(s) overwritten (see stderr)"
