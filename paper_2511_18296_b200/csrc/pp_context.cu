@@ -165,6 +165,16 @@ extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
 
+#ifdef PP_CHECKED
+// negative control of the checked build (not in the header): one byte written just past the end
+// of the context's period-mass buffer, as an out-of-bounds kernel store would
+PP_API int pp_debug_corrupt_guard(pp_ctx *c) {
+    if (!c || !c->pm.ptr) return fail(PP_ERR_STATE, "no period-mass buffer yet");
+    CUDA_TRY(cudaMemset(static_cast<unsigned char *>(c->pm.ptr) + c->pm.bytes, 0, 1));
+    return PP_OK;
+}
+#endif
+
 int pp_debug_check_guards(int64_t *n_bad) {
 #ifdef PP_CHECKED
     if (!n_bad) return fail(PP_ERR_INVALID_ARGS, "n_bad is NULL");
