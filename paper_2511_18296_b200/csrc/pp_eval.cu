@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     //      warp maxima (high then low word) and the lowest lane holding it.  -inf / NaN never
     //      selected ----
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const double pm_t = lane < T ? __ldcg(p.pm + lane) : 0.0;
+    // a plain (L1-cached) load: one L2 request per SM instead of one per warp on the same line --
+    // all ~4,000 warps pass the wait together (griddepcontrol.wait makes the writes visible; no
+    // load of pm precedes it)
+    const double pm_t = lane < T ? p.pm[lane] : 0.0;
     EV_PROBE(3);
     WP_PROBE(6);
     Best wbest{-kInf, INT_MAX, INT_MAX};
