@@ -111,6 +111,17 @@ bool guard_intact(const DevBuf *b) {
 }
 #endif
 
+void *mapped_host(const void *p) {
+    if (!p) return nullptr;
+    if (void *d = pinned_lookup(p)) return d;  // one of pp_host_alloc's buffers: no driver query
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+}
+
 int ensure_grid_scratch(pp_ctx *c, int grid) {
     TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
     if (c->counter.bytes == 0) {

@@ -719,17 +719,6 @@ __global__ void __launch_bounds__(256) k_copy_out(const CopyOut co) {
 }
 
 // device pointer of a page-locked host buffer, or nullptr (pageable / unknown)
-static void *mapped_host(const void *p) {
-    if (!p) return nullptr;
-    if (void *d = pinned_lookup(p)) return d;  // one of pp_host_alloc's buffers: no driver query
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
-}
-
 extern "C" {
 
 int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenario, uint32_t flags,
@@ -862,12 +851,14 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         const int per_cta = CPW * (WV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));
+        ht.mark("eval setup");
         if (reinterpret_cast<uintptr_t>(o.global) & 15u)
             return fail(PP_ERR_INVALID_ARGS, "global (pp_best) must be 16-byte aligned");
         bool pdl;
         ep.bad_cand = mem == PP_MEM_HOST ? c->bad_cand.as<int32_t>() : nullptr;
         const EvalInit init{o.n_pairs, o.global, ep.bad_cand};
         TRY(refresh_pm(c, st, &pdl, &init));  // initialises n_pairs and the best record ahead of the evaluation
+        ht.mark("pm launch");
         const bool scen = o.scen_delta != nullptr;
 #define PP_WARP(KC, SC)                                                     \
     {                                                                       \

@@ -715,14 +715,18 @@ struct HostTrace {
     const char *name;
     bool on;
     std::chrono::steady_clock::time_point t0, t;
-    explicit HostTrace(const char *n) : name(n), on(std::getenv("PP_TRACE_HOST") != nullptr) {
+    static bool enabled() {
+        static const bool on_ = std::getenv("PP_TRACE_HOST") != nullptr;
+        return on_;
+    }
+    explicit HostTrace(const char *n) : name(n), on(enabled()) {
         if (on) t0 = t = std::chrono::steady_clock::now();
     }
-    void mark(const char *what) {
+    void mark(const char *what) {  // (the print is not charged to the next phase)
         if (!on) return;
         const auto n = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[%s] %-12s %7.1f us\n", name, what, std::chrono::duration<double, std::micro>(n - t).count());
-        t = n;
+        t = std::chrono::steady_clock::now();
     }
     ~HostTrace() {
         if (on)
@@ -853,6 +857,7 @@ int run_period_mass(pp_ctx *c, const int32_t *d_assign, int P, double *d_pm, cud
 int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init = nullptr);
 int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st);
 bool pm_cluster_path(const pp_ctx *c);
+void *mapped_host(const void *p);  // device alias of page-locked host memory, or nullptr
 // after the stream was synchronised: PP_ERR_INVALID_ARGS if the pending host schedule had
 // period indices out of range (h_bad already copied when `copied`)
 int check_schedule_range(pp_ctx *c, bool copied);
