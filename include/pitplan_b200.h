@@ -221,6 +221,25 @@ PP_API int pp_repair(pp_ctx *ctx, int32_t *assign, int32_t n_sched, int32_t mode
  * NULL) marks the ejected blocks. */
 PP_API int pp_eject(pp_ctx *ctx, int32_t *assign, int32_t n_sched, const double *mean_grade, double destroy_fraction,
              uint8_t *ejected_out, int32_t mem, void *stream);
+/* lns_repair's rook neighbour map (hybrid.py:159-166, the order of uncertainty.rook_weights) as a
+ * CSR: rook_ptr[B+1], rook_idx[rook_ptr[B]]; at most 7 neighbours per block (PP_ERR_SHAPE
+ * otherwise: numpy's mean of 8+ values is a pairwise sum, the device ranking does the sequential
+ * one).  Instance data, set once. */
+PP_API int pp_set_rook(pp_ctx *ctx, const int32_t *rook_ptr, const int32_t *rook_idx);
+/* lns_repair's insertion loop (hybrid.py:238-266) on the device: one CUDA-graph launch whose
+ * conditional WHILE node runs up to max_iters rounds of -- rank the pool by scheduled-neighbour
+ * similarity (hybrid.py:142-156) and take the first candidate_width (<= 64) blocks in
+ * (similarity desc, block asc) order; evaluate them as evaluate_candidates_parallel with the
+ * expected scenario value (flags: PP_NET_MINING_COST, PP_USE_SIGMA); stop when there is no move
+ * (*stalled = 1) or, with only_positive, when the best improvement is <= 0; apply the best move,
+ * or the realism fallback's choice when the best block's geological consistency is below
+ * realism_threshold; drop the block from the pool -- with no host round trip between rounds.
+ * assign[B] (host, in/out): the schedule after the destroy step; pool[B] (host u8, in/out): the
+ * unassigned blocks; mean_grade[B] = scenarios.grades.mean(axis=0).  Needs pp_set_geology
+ * (consistency), pp_set_scenarios and pp_set_rook.  Returns when assign and pool hold the result. */
+PP_API int pp_lns_insert(pp_ctx *ctx, int32_t *assign, uint8_t *pool, const double *mean_grade, int32_t max_iters,
+                         int32_t candidate_width, double realism_threshold, int32_t only_positive, uint32_t flags,
+                         int32_t *iters, int32_t *stalled);
 /* Plant data for the relaxed NPV: plant_hours[T] and the throughput rate of the single operating
  * mode (blockmodel.py:63-97).  Only the stage-2 fast path exists on the device: one mode, one rock
  * type, rate > 0 (evaluate.py:149-150); other instances stay on the reference's LP. */

@@ -698,6 +698,10 @@ struct pp_ctx {
     DevBuf s2_rec;                // pp_npv_moves: the base schedule's per-(s, t) greedy structure
     DevBuf s2_assign;             // pp_npv_moves: the device copy of the cached base schedule
     DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
+    // device-resident lns insertion loop (pp_lns.cu): rook CSR (pp_set_rook), mean grades, the pool
+    // (unordered list + positions), ranking keys, control block, per-round candidates and results
+    DevBuf lns_rptr, lns_ridx, lns_mg, lns_pool, lns_pos, lns_keys, lns_ctl, lns_out;
+    bool have_rook = false;
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;
@@ -706,7 +710,8 @@ struct pp_ctx {
                 &ones_st, &plan_dev, &assign, &pm, &cnt, &compact, &pm_batch, &predcnt, &partial, &counter, &pm_flags, &h_cand, &h_a,
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
-                &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig};
+                &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig,
+                &pm_bad, &lns_rptr, &lns_ridx, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
     }
 };
 

@@ -485,6 +485,31 @@ class Engine:
         a, e = self.eject(a, mean_grade, destroy_fraction)
         return a, (u | e)
 
+    def set_rook(self, rook_ptr, rook_idx):
+        """lns_repair's rook neighbour map as a CSR (at most 7 neighbours per block), once per instance."""
+        bm = self._need_bm()
+        rp = np.ascontiguousarray(rook_ptr, dtype=np.int32)
+        ri = np.ascontiguousarray(rook_idx, dtype=np.int32)
+        if rp.size != bm.n_blocks + 1:
+            raise ShapeMismatch("rook_ptr must have n_blocks + 1 entries")
+        check(self.lib.pp_set_rook(self._h, ptr(rp), ptr(ri) if ri.size else None))
+
+    def lns_insert(self, assign, pool, mean_grade, *, max_iters, candidate_width=16, realism_threshold=0.5,
+                   only_positive=False, net=False, use_sigma=True):
+        """lns_repair's insertion loop (hybrid.py:238-266) as one device-resident CUDA graph
+        (pp_lns_insert).  Returns (assign int32 [B], pool uint8 [B], iterations, stalled)."""
+        bm = self._need_bm()
+        a = np.array(assign, dtype=np.int32, order="C")
+        pl = np.array(pool, dtype=np.uint8, order="C")
+        g = np.ascontiguousarray(mean_grade, dtype=np.float64)
+        if a.size != bm.n_blocks or pl.size != bm.n_blocks or g.size != bm.n_blocks:
+            raise ShapeMismatch("assign / pool / mean_grade length does not match the instance")
+        it, stl = ctypes.c_int32(0), ctypes.c_int32(0)
+        check(self.lib.pp_lns_insert(self._h, ptr(a), ptr(pl), ptr(g), int(max_iters), int(candidate_width),
+                                     float(realism_threshold), int(bool(only_positive)),
+                                     self.flags(net, False, use_sigma), ctypes.byref(it), ctypes.byref(stl)))
+        return a, pl, int(it.value), bool(stl.value)
+
     def reduce_best_device(self, records, out, stream=None):
         """Ordered argmax over n 16-byte pp_best records (device tensors)."""
         n = records.numel() * records.element_size() // 16

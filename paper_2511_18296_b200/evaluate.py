@@ -104,7 +104,7 @@ def _cache() -> OrderedDict:
 
 
 class _Entry:
-    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params", "rook", "rook_pad")
+    __slots__ = ("instance", "bm", "engine", "scen_key", "scen_refs", "params", "rook", "rook_pad", "rook_on_device")
 
     def __init__(self, instance, bm, engine):
         self.instance = instance  # strong ref: keeps id(instance) from being reused
@@ -115,6 +115,7 @@ class _Entry:
         self.params = None
         self.rook = None
         self.rook_pad = None
+        self.rook_on_device = False
 
 
 def _device() -> int:
@@ -300,6 +301,17 @@ def unmine_fixpoint(instance, assign: np.ndarray):
     return np.nonzero(u[0])[0]
 
 
+_LNS_GRAPH_WMAX = 64  # pp_lns_insert's candidate_width limit
+
+
+def _rook_csr(pad: np.ndarray):
+    """model.rook_padded's [B][L] table (-1 padding, reference order) as a CSR."""
+    valid = pad >= 0
+    ptr_ = np.zeros(pad.shape[0] + 1, dtype=np.int32)
+    np.cumsum(valid.sum(axis=1), out=ptr_[1:])
+    return ptr_, pad[valid].astype(np.int32)
+
+
 def lns_repair(
     instance,
     schedule,
@@ -352,6 +364,18 @@ def lns_repair(
     in_pool[list(pool)] = True
     iters = 0
     stalled = False
+    if pad is not None and 1 <= candidate_width <= _LNS_GRAPH_WMAX and pool and max_iters > 0:
+        # the whole insertion loop as one device-resident CUDA graph (pp_lns_insert): ranking,
+        # evaluation, both selection keys, the decision and the update on the device per round
+        if not e.rook_on_device:
+            e.engine.set_rook(*_rook_csr(pad))
+            e.rook_on_device = True
+        a, in_pool, iters, stalled = e.engine.lns_insert(
+            sched.assignment, in_pool, mean_grade, max_iters=max_iters, candidate_width=candidate_width,
+            realism_threshold=realism_threshold, only_positive=only_positive, net=net_mining_cost,
+            use_sigma=sigma is not None)
+        sched.assignment[...] = a
+        pool = set()  # (consumed)
     while pool and iters < max_iters:
         if pad is not None:  # vectorised ranking, identical order (model.neighbor_similarity_array)
             ids = np.flatnonzero(in_pool)
