@@ -279,17 +279,39 @@ int pp_lns_insert(pp_ctx *c, int32_t *assign, uint8_t *pool, const double *mean_
     // the round, captured into the loop body
     if (cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return done(fail(PP_ERR_CUDA, "capture: %s", cudaGetErrorString(cudaGetLastError())));
+    // the ranking (one CTA) runs beside the period masses (one cluster): both read only the round's
+    // schedule; the evaluation joins them
     const int32_t *dassign = c->assign_ptr;
-    k_lns_rank<<<1, LNS_THREADS, 0, st>>>(dctl, dpool, dassign, c->lns_mg.as<double>(), c->lns_rptr.as<int32_t>(),
-                                          c->lns_ridx.as<int32_t>(), c->lns_keys.as<unsigned long long>(), dcand, W);
-    c->pm_dirty = true;  // every round recomputes the period masses of the round's schedule
-    rc = pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st);
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
+        rc = fail(PP_ERR_CUDA, "lns: stream / events");
+    if (rc == PP_OK && (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess))
+        rc = fail(PP_ERR_CUDA, "lns: fork");
+    if (rc == PP_OK) {
+        k_lns_rank<<<1, LNS_THREADS, 0, side>>>(dctl, dpool, dassign, c->lns_mg.as<double>(), c->lns_rptr.as<int32_t>(),
+                                                c->lns_ridx.as<int32_t>(), c->lns_keys.as<unsigned long long>(), dcand, W);
+        if (cudaGetLastError() != cudaSuccess || cudaEventRecord(join, side) != cudaSuccess)
+            rc = fail(PP_ERR_CUDA, "lns: k_lns_rank");
+    }
+    if (rc == PP_OK) {
+        bool launched;
+        c->pm_dirty = true;  // every round recomputes the period masses of the round's schedule
+        rc = refresh_pm(c, st, &launched, nullptr);
+    }
+    if (rc == PP_OK && cudaStreamWaitEvent(st, join, 0) != cudaSuccess) rc = fail(PP_ERR_CUDA, "lns: join");
+    if (rc == PP_OK) rc = pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st);
     if (rc == PP_OK) {
         k_lns_apply<<<1, 32, 0, st>>>(dctl, rec, c->rows.as<BlockRow>(), c->assign.as<int32_t>(), dpool, dpos, hc);
         if (cudaGetLastError() != cudaSuccess) rc = fail(PP_ERR_CUDA, "k_lns_apply launch");
     }
     cudaGraph_t cap = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(st, &cap);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
     if (rc != PP_OK) return done(rc);
     if (ec != cudaSuccess) return done(fail(PP_ERR_CUDA, "end capture: %s", cudaGetErrorString(ec)));
     if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess)

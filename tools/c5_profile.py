@@ -24,3 +24,4 @@ H.hybrid_optimize(inst, scen, sigma, cfg)
 pr.disable()
 print(f"total {time.perf_counter() - t0:.2f} s")
 pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("cumtime").print_stats("lns_repair|lns_insert|polish_schedule|_measure|_member")
