@@ -122,6 +122,16 @@ void *mapped_host(const void *p) {
     return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
 }
 
+int ensure_side_stream(pp_ctx *c) {
+    if (c->side) return PP_OK;
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0) c->n_sms = sms;
+    return PP_OK;
+}
+
 int ensure_grid_scratch(pp_ctx *c, int grid) {
     TRY(c->partial.ensure(sizeof(pp_best) * (size_t)std::max(grid, 1)));
     if (c->counter.bytes == 0) {
@@ -245,6 +255,12 @@ int pp_ctx_destroy(pp_ctx *c) {
     if (c->h_bad) cudaFreeHost(c->h_bad);
     if (c->h_bounce) cudaFreeHost(c->h_bounce);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return PP_OK;

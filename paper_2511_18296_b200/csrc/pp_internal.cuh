@@ -649,6 +649,9 @@ struct DevBuf {
 struct pp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;                        // second stream (ensure_side_stream)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;   // fork / join between stream and side
+    int n_sms = 148;
     int B = 0, T = 0, S = 0, Sp = 0, n_levels = 0, deg_max = 0;
     long long E = 0;
     bool have_instance = false, have_spatial = false, have_scen = false, have_sigma = false, have_sched = false;
@@ -863,6 +866,7 @@ int refresh_pm(pp_ctx *c, cudaStream_t st, bool *launched, const EvalInit *init 
 int init_eval_outputs(pp_ctx *c, const EvalInit &init, cudaStream_t st);
 bool pm_cluster_path(const pp_ctx *c);
 void *mapped_host(const void *p);  // device alias of page-locked host memory, or nullptr
+int ensure_side_stream(pp_ctx *c);  // c->side + fork/join events, created on first use
 // after the stream was synchronised: PP_ERR_INVALID_ARGS if the pending host schedule had
 // period indices out of range (h_bad already copied when `copied`)
 int check_schedule_range(pp_ctx *c, bool copied);

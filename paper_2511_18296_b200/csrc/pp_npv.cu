@@ -951,6 +951,52 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
     if (lane == 0) npv[m] = total;
 }
 
+// The same accumulation with every term of the variant formed up front: the warp's lanes form
+// all T*S terms (their loads and divisions independent of one another, so in flight together)
+// into the warp's shared slice, then lane 0 adds them in the reference's (t, s) order -- one
+// dependent add chain instead of T rounds of load latency.  For T*S <= NPVF_MAX.
+constexpr int NPVF_MAX = 480;
+constexpr int NPVF_WARPS = 4;
+__global__ void __launch_bounds__(32 * NPVF_WARPS)
+    k_npv_moves_final_staged(int T, int S, int M, const double *__restrict__ braw, const double *__restrict__ bcost,
+                             const int32_t *__restrict__ bn, const double *__restrict__ mraw,
+                             const double *__restrict__ mcost, const int32_t *__restrict__ mn,
+                             const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
+                             const double *__restrict__ disc, const double *__restrict__ sigma,
+                             double *__restrict__ npv) {
+    __shared__ double s_term[NPVF_WARPS][NPVF_MAX];
+    __shared__ double s_cost[NPVF_WARPS][32];  // d * cs per period, or +inf: no mined block (skip)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int m = (int)blockIdx.x * NPVF_WARPS + w;
+    if (m >= M) return;
+    const int t0 = slot_t[2 * m], t1 = slot_t[2 * m + 1];
+    const int k0 = slot_src[2 * m], k1 = slot_src[2 * m + 1];
+    double *tw = s_term[w];
+    for (int i = lane; i < T * S; i += 32) {
+        const int t = i / S, s = i - t * S;
+        const double *raw = t == t0 ? mraw + (size_t)k0 * S : t == t1 ? mraw + (size_t)k1 * S : braw + (size_t)t * S;
+        const double d = disc[t];
+        const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
+        tw[i] = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
+    }
+    if (lane < T) {
+        const int t = lane;
+        const double cs = t == t0 ? mcost[k0] : t == t1 ? mcost[k1] : bcost[t];
+        const int n = t == t0 ? mn[k0] : t == t1 ? mn[k1] : bn[t];
+        s_cost[w][t] = n > 0 ? f64_mul(disc[t], cs) : kInf;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double total = 0.0;
+        for (int t = 0; t < T; t++) {
+            const double dc = s_cost[w][t];
+            if (dc != kInf) total = f64_sub(total, dc);
+            for (int s = 0; s < S; s++) total = f64_add(total, tw[t * S + s]);
+        }
+        npv[m] = total;
+    }
+}
+
 extern "C" {
 
 int pp_set_plant(pp_ctx *c, const double *plant_hours, double rate) {
@@ -1433,25 +1479,35 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         TRY(run_stage2(c, st, da, (int)dirty.size(), 1, braw, bcost, bn, nullptr, nullptr, nullptr, dtsel, &rec,
                        may_be_big));
     {
+        // the cost sums (k_s2_varcost) and the stage-2 chains (k_s2_chain) read disjoint parts of
+        // the base structure: the cost sums run on the side stream, joined before the accumulation
+        TRY(ensure_side_stream(c));
+        CUDA_TRY(cudaEventRecord(c->ev_fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        const int cap = B / 64 + 16;
+        const size_t smem = (size_t)16 * cap;
+        const int grid = std::max(1, std::min(2 * M, 4 * c->n_sms));
+        TRY(set_smem_attr(k_s2_varcost, smem, c->device));
+        k_s2_varcost<<<grid, 256, smem, c->side>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
         const long long nthr = 2ll * M * S * 32;  // a warp per (slot, scenario)
         k_s2_chain<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(rec, B, T, S, c->Sp, M, db, ds, dr,
                                                                   c->vmax.as<double>(), c->mass.as<double>(), c->rate,
                                                                   braw, mraw);
         CUDA_TRY(cudaGetLastError());
-        const int cap = B / 64 + 16;
-        const size_t smem = (size_t)16 * cap;
-        int sms = 148;
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || sms < 1) sms = 148;
-        const int grid = std::max(1, std::min(2 * M, 4 * sms));
-        TRY(set_smem_attr(k_s2_varcost, smem, c->device));
-        k_s2_varcost<<<grid, 256, smem, st>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap);
-        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamWaitEvent(st, c->ev_join, 0));
     }
     ht_.mark("launch");
     double *dn = host ? c->h_d1.as<double>() : npv_out;
-    k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
-                                                        c->disc.as<double>(),
-                                                        (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
+    if (T * S <= NPVF_MAX && T <= 32)
+        k_npv_moves_final_staged<<<(M + NPVF_WARPS - 1) / NPVF_WARPS, 32 * NPVF_WARPS, 0, st>>>(
+            T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc, c->disc.as<double>(),
+            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
+    else
+        k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
+                                                            c->disc.as<double>(),
+                                                            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
     CUDA_TRY(cudaGetLastError());
     // the structure now describes `ha` (complete once the stream reaches this point)
     c->npvm_gen = c->npv_gen;
