@@ -700,6 +700,9 @@ struct pp_ctx {
     DevBuf s2_items, s2_scratch;  // large-period stage-2: work list [S*T*P | S*2*M] and per-CTA scratch
     DevBuf s2_rec;                // pp_npv_moves: the base schedule's per-(s, t) greedy structure
     DevBuf s2_assign;             // pp_npv_moves: the device copy of the cached base schedule
+    DevBuf npvm_flags;            // pp_npv_moves: progress flags of the concurrent one-block update
+    uint64_t npvm_flags_gen = 0;
+    uint32_t npvm_epoch = 0;
     DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
     // device-resident lns insertion loop (pp_lns.cu): rook CSR (pp_set_rook), mean grades, the pool
     // (unordered list + positions), ranking keys, control block, per-round candidates and results
@@ -714,7 +717,7 @@ struct pp_ctx {
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
                 &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig,
-                &pm_bad, &lns_rptr, &lns_ridx, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
+                &pm_bad, &npvm_flags, &lns_rptr, &lns_ridx, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
     }
 };
 

@@ -28,8 +28,46 @@ __device__ __forceinline__ unsigned long long np_gtimer() {
 extern "C" PP_API int pp_debug_npv_probe(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_npv_probe, sizeof(g_npv_probe)) == cudaSuccess ? 0 : 3;
 }
+// kernel spans of one pp_npv_moves call: [id][0] earliest CTA start, [id][1] latest warp end
+__device__ unsigned long long g_kspan[8][2];
+#define KSPAN_BEGIN(id) do { if (threadIdx.x == 0) atomicMin(&g_kspan[id][0], np_gtimer()); } while (0)
+#define KSPAN_END(id) do { if ((threadIdx.x & 31) == 0) atomicMax(&g_kspan[id][1], np_gtimer()); } while (0)
+// per-call log of the spans (probe builds): npv_moves_impl appends one row per host-mode call
+static std::vector<unsigned long long> g_kspan_log;
+static void kspan_reset() {
+    unsigned long long h[8][2];
+    for (int i = 0; i < 8; i++) {
+        h[i][0] = ~0ull;
+        h[i][1] = 0ull;
+    }
+    cudaMemcpyToSymbol(g_kspan, h, sizeof(h));
+}
+static void kspan_append() {
+    unsigned long long h[16];
+    if (cudaMemcpyFromSymbol(h, g_kspan, sizeof(h)) == cudaSuccess) g_kspan_log.insert(g_kspan_log.end(), h, h + 16);
+}
+extern "C" PP_API int pp_debug_kspan_log(unsigned long long *out, int64_t max_rows, int64_t *rows) {
+    const int64_t n = (int64_t)g_kspan_log.size() / 16;
+    *rows = n;
+    if (out) std::memcpy(out, g_kspan_log.data(), sizeof(unsigned long long) * 16 * (size_t)std::min(n, max_rows));
+    g_kspan_log.clear();
+    return 0;
+}
+extern "C" PP_API int pp_debug_kspan(unsigned long long *out, int reset) {
+    if (reset) {
+        unsigned long long h[8][2];
+        for (int i = 0; i < 8; i++) {
+            h[i][0] = ~0ull;
+            h[i][1] = 0ull;
+        }
+        return cudaMemcpyToSymbol(g_kspan, h, sizeof(h)) == cudaSuccess ? 0 : 3;
+    }
+    return cudaMemcpyFromSymbol(out, g_kspan, sizeof(g_kspan)) == cudaSuccess ? 0 : 3;
+}
 #else
 #define NPVP(k) do { } while (0)
+#define KSPAN_BEGIN(id) do { } while (0)
+#define KSPAN_END(id) do { } while (0)
 #endif
 
 constexpr int S2_THREADS = 1024;
@@ -226,10 +264,36 @@ __device__ int s2_compact(const int32_t *__restrict__ a, int B, int t, int ob, i
 // With rec_h / rec_t (may be null) the state before every processed position k -- (hours_left,
 // total) -- is recorded for k = 0..K, K the position where the loop stopped (K = n when it ran
 // through), and K goes to *rec_k: the prefix an incremental variant restarts from (k_s2_chain).
+// Progress flags of the one-block base update (k_s2_apply_one) that the variants' kernels of the
+// same call read while it still runs (programmatic dependent launch: all its CTAs are resident
+// before theirs start, so the waits cannot deadlock).  A flag is (call epoch << 32) | x:
+// x = valid + 2 once the splice is in place and the recorded states H/TT[k] are final for
+// k < valid; x = S2_DONE when the period's structure, stop K and stage-2 value are final.
+constexpr unsigned S2_DONE = 0xffffffffu;
+__device__ __forceinline__ unsigned long long s2_flag_load(const unsigned long long *f) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+    return v;
+}
+__device__ __forceinline__ void s2_flag_publish(unsigned long long *f, unsigned long long v) {
+    __threadfence();  // the caller's (and, through the preceding barrier, its group's) writes first
+    atomicExch(f, v);
+}
+__device__ __forceinline__ unsigned long long s2_flag_wait(const unsigned long long *f, unsigned long long need) {
+    unsigned long long v;
+    long long spins = 0;
+    while ((v = s2_flag_load(f)) < need) {  // bounded: a lost update traps instead of hanging the GPU
+        __nanosleep(100);
+        if (++spins > (1ll << 26)) __trap();
+    }
+    return v;
+}
+
 template <class DF, class MF, class QF>
 __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF dof, MF mof, QF qof,
                                  double *rec_h = nullptr, double *rec_t = nullptr, int32_t *rec_k = nullptr,
-                                 int k_begin = 0, double total0 = 0.0) {
+                                 int k_begin = 0, double total0 = 0.0, unsigned long long *prog = nullptr,
+                                 unsigned long long eh = 0) {
     // k_begin / total0: resume at position k_begin with state (hours0, total0) -- the recorded
     // state there (an incremental base update, k_s2_apply_one)
     __shared__ double s_q32[32], s_dm32[32];
@@ -259,6 +323,11 @@ __device__ double s2_greedy_warp(int n, int kpos, double hours0, double rate, DF
         if (rec_h && in && (!sm || lane <= __ffs(sm) - 1)) {
             rec_h[kk] = h_mine;
             rec_t[kk] = t_mine;
+        }
+        if (prog && !sm && (((k0 - k_begin) >> 5) & 7) == 7) {  // every 8 batches: states < k0 + 32 final
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicExch(prog, eh | (unsigned long long)(k0 + 32 + 2));
         }
         if (sm) {
             const int jf = __ffs(sm) - 1;
@@ -714,7 +783,11 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
                                                   const int32_t *__restrict__ blocks, const int32_t *__restrict__ slot_t,
                                                   const int32_t *__restrict__ run, const double *__restrict__ vmax,
                                                   const double *__restrict__ mass, double rate,
-                                                  const double *__restrict__ braw, double *__restrict__ mraw) {
+                                                  const double *__restrict__ braw, double *__restrict__ mraw,
+                                                  const unsigned long long *__restrict__ prog, unsigned long long eh,
+                                                  int pend0, int pend1) {
+    // pend0 / pend1: the periods k_s2_apply_one is updating concurrently (-1: none); a variant in
+    // one of them waits for the splice, then for the recorded state at its place (or the end)
     // one warp per (slot, scenario): lanes load 32 consecutive elements of the modified order at a
     // time (coalesced, one batch ahead), every lane runs the speculative whole-take recurrence over
     // them (the adds of the scalar loop, in its order), and the first element where the scalar loop
@@ -722,6 +795,7 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
     // thread per chain measured 2.8x slower: each chain walks its own list, so the loads of a thread
     // are serialised by latency; the warp's coalesced batches are not.)
     constexpr unsigned FULL = 0xffffffffu;
+    KSPAN_BEGIN(2);
     const int lane = threadIdx.x & 31;
     const long long unit = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (unit >= 2ll * M * S) return;
@@ -730,14 +804,18 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
     if (t < 0 || run[si] < 0) return;
     const int b = blocks[si >> 1];
     const size_t st_ = (size_t)s * T + t, base = st_ * rec.L;
-    const int np = rec.npos[st_], K = rec.K[st_];
-    PP_DCHECK(np >= 0 && np < rec.L && K >= 0 && K <= np);
+    const int y = t == pend0 ? 0 : (t == pend1 ? 1 : -1);
+    const unsigned long long *pf = y >= 0 ? prog + (size_t)y * S + s : nullptr;
+    if (pf) s2_flag_wait(pf, eh | 2ull);  // the spliced order, npos and positions
+    const int np = __ldcg(rec.npos + st_);
+    int K = __ldcg(rec.K + st_);
+    PP_DCHECK(np >= 0 && np < rec.L);
     const double *D = rec.D + base, *Mm = rec.M + base;
     const bool ins = si & 1;
     double dnew = 0.0, mnew = 0.0;
     int j;
     if (!ins) {
-        j = rec.pos[(size_t)s * B + b];
+        j = __ldcg(rec.pos + (size_t)s * B + b);
         PP_DCHECK(j < 0 || (j < np && rec.BID[base + j] == b));  // pos[] points at b's place
     } else {
         mnew = __ldg(mass + b);
@@ -748,8 +826,8 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
             int lo = 0, hi = np;
             while (lo < hi) {
                 const int md = (lo + hi) >> 1;
-                const double dm = D[md];
-                if (dm > dnew || (dm == dnew && BI[md] < b))
+                const double dm = __ldcg(D + md);
+                if (dm > dnew || (dm == dnew && __ldcg(BI + md) < b))
                     lo = md + 1;
                 else
                     hi = md;
@@ -757,8 +835,15 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
             j = lo;
         }
     }
+    if (pf) {  // the state at j recorded (the update's walk passed j), or the update done; a variant
+               // that leaves the order unchanged (j < 0) reads the updated base value: done
+        const unsigned long long v = s2_flag_wait(pf, j >= 0 ? (eh | (unsigned long long)(j + 3)) : (eh | S2_DONE));
+        K = (unsigned)v == S2_DONE ? __ldcg(rec.K + st_) : INT_MAX;  // not done: j is before the stop
+    }
+    PP_DCHECK(K >= 0 && (K == INT_MAX || K <= np));
     if (j < 0 || j > K) {  // the variant's order agrees with the base's up to its stop
-        if (lane == 0) mraw[(size_t)si * S + s] = braw[(size_t)t * S + s];
+        if (lane == 0) mraw[(size_t)si * S + s] = __ldcg(braw + (size_t)t * S + s);
+        KSPAN_END(2);
         return;
     }
     // the modified order: element e = the inserted block (e = 0) then positions j, j+1, ... , or
@@ -771,11 +856,11 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
         } else {
             const int k = ins ? j + e - 1 : j + 1 + e;
             PP_DCHECK(k >= 0 && k < np);
-            d = D[k];
-            m = Mm[k];
+            d = __ldcg(D + k);
+            m = __ldcg(Mm + k);
         }
     };
-    double hl = rec.H[base + j], tot = rec.TT[base + j];
+    double hl = __ldcg(rec.H + base + j), tot = __ldcg(rec.TT + base + j);
     int e = E;
     __shared__ double s_qd[8][64];
     double *wq_ = s_qd[threadIdx.x >> 5], *wdm = wq_ + 32;
@@ -829,6 +914,7 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
         }
         mraw[(size_t)si * S + s] = tot;
     }
+    KSPAN_END(2);
 }
 
 // The variant period's mining-cost sum (numpy pairwise over its blocks in block order, the base
@@ -836,7 +922,11 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
 __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, int M, const int32_t *__restrict__ blocks,
                                                     const int32_t *__restrict__ slot_t, const int32_t *__restrict__ run,
                                                     const double *__restrict__ cost, double *__restrict__ mcost,
-                                                    int32_t *__restrict__ mn, int cap) {
+                                                    int32_t *__restrict__ mn, int cap,
+                                                    const unsigned long long *__restrict__ cflag, unsigned long long eh,
+                                                    int pend0, int pend1) {
+    asm volatile("griddepcontrol.launch_dependents;");  // the chains may start (they wait on their own flags)
+    KSPAN_BEGIN(1);
     // the pairwise plan's leaves (<= n/64 + 2) live in shared memory: cap of each array
     extern __shared__ __align__(16) unsigned char vc_dyn[];
     double *lv = reinterpret_cast<double *>(vc_dyn);
@@ -846,15 +936,20 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         const int t = slot_t[si];
         if (t < 0 || run[si] < 0) continue;
         const int b = blocks[si >> 1];
+        const int y = t == pend0 ? 0 : (t == pend1 ? 1 : -1);
+        if (y >= 0) {  // the concurrent base update splices this period's list first
+            if (threadIdx.x == 0) s2_flag_wait(cflag + y, eh | 1ull);
+            __syncthreads();
+        }
         const int32_t *ids = rec.IDS + (size_t)t * rec.L;
         const double *csl = rec.CS + (size_t)t * rec.L;
         const double cb = __ldg(cost + (size_t)b * T + t);
-        const int n0 = rec.nper[t];
+        const int n0 = __ldcg(rec.nper + t);
         PP_DCHECK(n0 >= 0 && n0 < rec.L && (n0 + 1) / 64 + 2 <= cap);
         int lo = 0, hi = n0;  // block-order position of b
         while (lo < hi) {
             const int md = (lo + hi) >> 1;
-            if (ids[md] < b) lo = md + 1;
+            if (__ldcg(ids + md) < b) lo = md + 1;
             else hi = md;
         }
         const int r = lo;
@@ -862,7 +957,9 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         PP_DCHECK(ins || (r < n0 && ids[r] == b));  // a removed block is in its period's list
         const int n = ins ? n0 + 1 : n0 - 1;
         const double cs = s2_pairwise_f(
-            [&](int k) { return ins ? (k < r ? csl[k] : (k == r ? cb : csl[k - 1])) : csl[k < r ? k : k + 1]; },
+            [&](int k) {
+                return ins ? (k < r ? __ldcg(csl + k) : (k == r ? cb : __ldcg(csl + k - 1))) : __ldcg(csl + (k < r ? k : k + 1));
+            },
             n, ls, ll, lv);
         if (threadIdx.x == 0) {
             mcost[si] = cs;
@@ -870,6 +967,7 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         }
         __syncthreads();
     }
+    KSPAN_END(1);
 }
 
 // _npv / per_scenario_npv accumulation in the reference's order (t outer, s inner)
@@ -911,7 +1009,13 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
                                   const double *__restrict__ mcost, const int32_t *__restrict__ mn,
                                   const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                                   const double *__restrict__ disc,
-                                  const double *__restrict__ sigma, double *__restrict__ npv) {
+                                  const double *__restrict__ sigma, double *__restrict__ npv,
+                                  const unsigned long long *__restrict__ pflags, unsigned long long eh) {
+    if (eh) {  // a one-block base update may still be finishing: every flag done first
+        for (int i = threadIdx.x; i < 2 * S + 2; i += blockDim.x)
+            s2_flag_wait(pflags + i, i < 2 * S ? (eh | S2_DONE) : (eh | 1ull));
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const int m = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (m >= M) return;
@@ -930,8 +1034,8 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
             n = mn[k];
         } else {
             raw = braw + (size_t)t * S;
-            cs = bcost[t];
-            n = bn[t];
+            cs = __ldcg(bcost + t);
+            n = __ldcg(bn + t);
         }
         const double d = disc[t];
         if (n > 0) total = f64_sub(total, f64_mul(d, cs));
@@ -939,7 +1043,7 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
             const int s = s0 + lane;
             if (s < S) {
                 const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
-                wq[lane] = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
+                wq[lane] = f64_div(f64_mul(f64_mul(d, sg), __ldcg(raw + s)), (double)S);
             }
             __syncwarp();
             const int cnt = min(32, S - s0);
@@ -963,7 +1067,16 @@ __global__ void __launch_bounds__(32 * NPVF_WARPS)
                              const double *__restrict__ mcost, const int32_t *__restrict__ mn,
                              const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                              const double *__restrict__ disc, const double *__restrict__ sigma,
-                             double *__restrict__ npv) {
+                             double *__restrict__ npv, const unsigned long long *__restrict__ pflags,
+                             unsigned long long eh) {
+    // eh != 0: a one-block base update may still be finishing (its dependents need not wait for
+    // it): every base value is read after all its periods' flags say done
+    KSPAN_BEGIN(3);
+    if (eh) {
+        for (int i = threadIdx.x; i < 2 * S + 2; i += blockDim.x)
+            s2_flag_wait(pflags + i, i < 2 * S ? (eh | S2_DONE) : (eh | 1ull));
+        __syncthreads();
+    }
     __shared__ double s_term[NPVF_WARPS][NPVF_MAX];
     __shared__ double s_cost[NPVF_WARPS][32];  // d * cs per period, or +inf: no mined block (skip)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -977,12 +1090,12 @@ __global__ void __launch_bounds__(32 * NPVF_WARPS)
         const double *raw = t == t0 ? mraw + (size_t)k0 * S : t == t1 ? mraw + (size_t)k1 * S : braw + (size_t)t * S;
         const double d = disc[t];
         const double sg = sigma ? sigma[(size_t)s * T + t] : 1.0;
-        tw[i] = f64_div(f64_mul(f64_mul(d, sg), raw[s]), (double)S);
+        tw[i] = f64_div(f64_mul(f64_mul(d, sg), __ldcg(raw + s)), (double)S);
     }
     if (lane < T) {
         const int t = lane;
-        const double cs = t == t0 ? mcost[k0] : t == t1 ? mcost[k1] : bcost[t];
-        const int n = t == t0 ? mn[k0] : t == t1 ? mn[k1] : bn[t];
+        const double cs = t == t0 ? mcost[k0] : t == t1 ? mcost[k1] : __ldcg(bcost + t);
+        const int n = t == t0 ? mn[k0] : t == t1 ? mn[k1] : __ldcg(bn + t);
         s_cost[w][t] = n > 0 ? f64_mul(disc[t], cs) : kInf;
     }
     __syncwarp();
@@ -994,6 +1107,7 @@ __global__ void __launch_bounds__(32 * NPVF_WARPS)
             for (int s = 0; s < S; s++) total = f64_add(total, tw[t * S + s]);
         }
         npv[m] = total;
+        KSPAN_END(3);
     }
 }
 
@@ -1109,20 +1223,108 @@ __global__ void k_scatter_assign(int32_t *__restrict__ assign, const int32_t *__
 // the place shift by one in 1024-element chunks (ascending for a removal, descending for an
 // insertion, so no chunk overwrites what a later one reads), the positions of the shifted blocks
 // are renumbered, and the greedy resumes from the recorded state at the place (the prefix before it
-// is unchanged) with recording.  The s == 0 CTAs splice the block-ordered id and cost lists the same
-// way and recompute the period's mining-cost sum (numpy pairwise).  Identical to a rebuild.
+// is unchanged) with recording.  One extra CTA per period (blockIdx.x == S) splices the
+// block-ordered id and cost lists the same way and recomputes the period's mining-cost sum (numpy
+// pairwise) beside the greedy CTAs.  Identical to a rebuild.  The call's variant kernels run
+// concurrently as programmatic dependents and wait only on the progress flags they need.
 // ------------------------------------------------------------------------------------
+__device__ void s2_apply_cost(const S2Struct &rec, int T, int b, int t, bool ins, const double *__restrict__ cost,
+                              double *__restrict__ costsum, int32_t *__restrict__ nmined,
+                              unsigned long long *__restrict__ cflag, unsigned long long eh) {
+    __shared__ int s_j, s_ls[256], s_ll[256];
+    __shared__ double s_lv[256];
+    const int tid = threadIdx.x;
+    int32_t *ids = rec.IDS + (size_t)t * rec.L;
+    double *csl = rec.CS + (size_t)t * rec.L;
+    const int n0 = rec.nper[t];
+    if (tid == 0) {
+        int lo = 0, hi = n0;
+        while (lo < hi) {
+            const int md = (lo + hi) >> 1;
+            if (ids[md] < b) lo = md + 1;
+            else hi = md;
+        }
+        s_j = lo;
+    }
+    __syncthreads();
+    const int r = s_j;
+    PP_DCHECK(n0 >= 0 && n0 + 1 < 16000 && (ins || (r < n0 && ids[r] == b)));
+    if (!ins) {
+        for (int k0 = r; k0 < n0 - 1; k0 += S2_THREADS) {
+            const int k = k0 + tid;
+            int bb = 0;
+            double cc = 0.0;
+            if (k < n0 - 1) {
+                bb = ids[k + 1];
+                cc = csl[k + 1];
+            }
+            __syncthreads();
+            if (k < n0 - 1) {
+                ids[k] = bb;
+                csl[k] = cc;
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int k1 = n0; k1 > r; k1 -= S2_THREADS) {
+            const int k = k1 - 1 - tid;
+            int bb = 0;
+            double cc = 0.0;
+            if (k >= r) {
+                bb = ids[k];
+                cc = csl[k];
+            }
+            __syncthreads();
+            if (k >= r) {
+                ids[k + 1] = bb;
+                csl[k + 1] = cc;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            ids[r] = b;
+            csl[r] = __ldg(cost + (size_t)b * T + t);
+        }
+    }
+    __syncthreads();
+    const int n1 = ins ? n0 + 1 : n0 - 1;
+    const double cs = s2_pairwise(csl, n1, s_ls, s_ll, s_lv);  // n1 < 16000: <= 252 leaves
+    if (tid == 0) {
+        rec.nper[t] = n1;
+        costsum[t] = cs;
+        nmined[t] = n1;
+        s2_flag_publish(cflag + blockIdx.y, eh | 1ull);  // the block-ordered list is spliced
+    }
+}
+
 __global__ void __launch_bounds__(S2_THREADS, 1)
     k_s2_apply_one(const S2Struct rec, int B, int T, int S, int Sp, int b, int t_old, int t_new,
                    const double *__restrict__ mass, const double *__restrict__ cost, const double *__restrict__ vmax,
                    const double *__restrict__ hours, double rate, double *__restrict__ raw,
-                   double *__restrict__ costsum, int32_t *__restrict__ nmined) {
-    __shared__ int s_j, s_ls[256], s_ll[256];
-    __shared__ double s_lv[256];
+                   double *__restrict__ costsum, int32_t *__restrict__ nmined, unsigned long long *__restrict__ prog,
+                   unsigned long long *__restrict__ cflag, unsigned long long eh) {
+    // prog[y][s] / cflag[y] (y = blockIdx.y): progress of this update for the variants' kernels of
+    // the same call, which run concurrently (programmatic dependents, launched once every CTA here
+    // has started)
+    asm volatile("griddepcontrol.launch_dependents;");
+    KSPAN_BEGIN(0);
+    __shared__ int s_j;
     const int s = blockIdx.x;
     const bool ins = blockIdx.y == 1;
     const int t = ins ? t_new : t_old;
-    if (t < 0) return;
+    if (s == S) {  // the cost CTA
+        if (t < 0) {
+            if (threadIdx.x == 0) s2_flag_publish(cflag + blockIdx.y, eh | 1ull);
+        } else {
+            s2_apply_cost(rec, T, b, t, ins, cost, costsum, nmined, cflag, eh);
+        }
+        return;
+    }
+    unsigned long long *pf = prog + (size_t)blockIdx.y * S + s;
+    if (t < 0) {  // no such period (the block was / becomes unmined): nothing to update
+        if (threadIdx.x == 0) s2_flag_publish(pf, eh | S2_DONE);
+        return;
+    }
     const int tid = threadIdx.x;
     const size_t st_ = (size_t)s * T + t, base = st_ * rec.L;
     double *D = rec.D + base, *M_ = rec.M + base, *H = rec.H + base, *TT = rec.TT + base;
@@ -1202,80 +1404,23 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
                 rec.pos[(size_t)s * B + b] = j;
             }
         }
-        __syncthreads();
         const int npn = ins ? np + 1 : np - 1;
+        if (tid == 0) rec.npos[st_] = npn;
+        __syncthreads();
+        if (tid == 0) s2_flag_publish(pf, eh | (unsigned long long)(j + 3));  // spliced; states <= j final
         // 3. the greedy from the place on, from the recorded state there (unchanged prefix); a place
         //    beyond the stop changes nothing the greedy reaches
         if (j <= K && tid < 32) {
             const double total = s2_greedy_warp(
                 npn, npn, H[j], rate, [&](int k) { return D[k]; }, [&](int k) { return M_[k]; },
-                [&](int k) { return f64_div(M_[k], rate); }, H, TT, rec.K + st_, j, TT[j]);
+                [&](int k) { return f64_div(M_[k], rate); }, H, TT, rec.K + st_, j, TT[j], pf, eh);
             if (tid == 0) raw[(size_t)t * S + s] = total;
         }
-        if (tid == 0) rec.npos[st_] = npn;
     }
-    // 4. s == 0: the block-ordered ids and costs, the period's cost sum and size
-    if (s != 0) return;
-    __syncthreads();
-    int32_t *ids = rec.IDS + (size_t)t * rec.L;
-    double *csl = rec.CS + (size_t)t * rec.L;
-    const int n0 = rec.nper[t];
-    if (tid == 0) {
-        int lo = 0, hi = n0;
-        while (lo < hi) {
-            const int md = (lo + hi) >> 1;
-            if (ids[md] < b) lo = md + 1;
-            else hi = md;
-        }
-        s_j = lo;
-    }
-    __syncthreads();
-    const int r = s_j;
-    PP_DCHECK(n0 >= 0 && n0 + 1 < 16000 && (ins || (r < n0 && ids[r] == b)));
-    if (!ins) {
-        for (int k0 = r; k0 < n0 - 1; k0 += S2_THREADS) {
-            const int k = k0 + tid;
-            int bb = 0;
-            double cc = 0.0;
-            if (k < n0 - 1) {
-                bb = ids[k + 1];
-                cc = csl[k + 1];
-            }
-            __syncthreads();
-            if (k < n0 - 1) {
-                ids[k] = bb;
-                csl[k] = cc;
-            }
-            __syncthreads();
-        }
-    } else {
-        for (int k1 = n0; k1 > r; k1 -= S2_THREADS) {
-            const int k = k1 - 1 - tid;
-            int bb = 0;
-            double cc = 0.0;
-            if (k >= r) {
-                bb = ids[k];
-                cc = csl[k];
-            }
-            __syncthreads();
-            if (k >= r) {
-                ids[k + 1] = bb;
-                csl[k + 1] = cc;
-            }
-            __syncthreads();
-        }
-        if (tid == 0) {
-            ids[r] = b;
-            csl[r] = __ldg(cost + (size_t)b * T + t);
-        }
-    }
-    __syncthreads();
-    const int n1 = ins ? n0 + 1 : n0 - 1;
-    const double cs = s2_pairwise(csl, n1, s_ls, s_ll, s_lv);  // n1 < 16000: <= 252 leaves
-    if (tid == 0) {
-        rec.nper[t] = n1;
-        costsum[t] = cs;
-        nmined[t] = n1;
+    if (tid < 32) {  // the period's structure, stop and value are final
+        __syncwarp();
+        if (tid == 0) s2_flag_publish(pf, eh | S2_DONE);
+        KSPAN_END(0);
     }
 }
 
@@ -1463,6 +1608,13 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     }
     const int32_t *da = dbase;
     ht_.mark("upload");
+#ifdef PP_EVAL_PROBE
+    if (host) kspan_reset();
+#endif
+    // a one-block base update (k_s2_apply_one) runs concurrently with this call's variant kernels,
+    // which wait on its progress flags for the two periods it updates (pend0 / pend1)
+    int pend0 = -1, pend1 = -1;
+    unsigned long long pend_eh = 0;
     double *braw = c->npv_raw.as<double>(), *mraw = braw + (size_t)T * S;
     double *bcost = c->npv_cost.as<double>(), *mcost = bcost + T;
     int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
@@ -1471,43 +1623,69 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     } else if (chg_b.size() == 1 && c->npvm_cnt[dirty[0]] < 16000 &&
                (dirty.size() < 2 || c->npvm_cnt[dirty[1]] < 16000)) {  // one block moved: splice
         const int bb = chg_b[0], to = c->npvm_base[bb], tn = chg_t[0];
-        k_s2_apply_one<<<dim3(S, 2), S2_THREADS, 0, st>>>(rec, B, T, S, c->Sp, bb, to, tn, c->mass.as<double>(),
-                                                          c->cost.as<double>(), c->vmax.as<double>(),
-                                                          c->hours.as<double>(), c->rate, braw, bcost, bn);
+        TRY(c->npvm_flags.ensure(sizeof(unsigned long long) * (2 * (size_t)S + 2)));
+        if (c->npvm_flags.gen != c->npvm_flags_gen) {  // fresh buffer: epoch 0 everywhere
+            CUDA_TRY(cudaMemsetAsync(c->npvm_flags.ptr, 0, sizeof(unsigned long long) * (2 * (size_t)S + 2), st));
+            c->npvm_flags_gen = c->npvm_flags.gen;
+            c->npvm_epoch = 0;
+        }
+        pend_eh = (unsigned long long)(++c->npvm_epoch) << 32;
+        pend0 = to;
+        pend1 = tn;
+        k_s2_apply_one<<<dim3(S + 1, 2), S2_THREADS, 0, st>>>(
+            rec, B, T, S, c->Sp, bb, to, tn, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(),
+            c->hours.as<double>(), c->rate, braw, bcost, bn, c->npvm_flags.as<unsigned long long>(),
+            c->npvm_flags.as<unsigned long long>() + 2 * S, pend_eh);
         CUDA_TRY(cudaGetLastError());
     } else if (!dirty.empty())
         TRY(run_stage2(c, st, da, (int)dirty.size(), 1, braw, bcost, bn, nullptr, nullptr, nullptr, dtsel, &rec,
                        may_be_big));
     {
-        // the cost sums (k_s2_varcost) and the stage-2 chains (k_s2_chain) read disjoint parts of
-        // the base structure: the cost sums run on the side stream, joined before the accumulation
-        TRY(ensure_side_stream(c));
-        CUDA_TRY(cudaEventRecord(c->ev_fork, st));
-        CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        // the cost sums (k_s2_varcost) and the stage-2 chains (k_s2_chain) read disjoint parts of the
+        // base structure.  After a one-block update both are programmatic dependents of it on the
+        // stream (varcost first, the chains once every varcost CTA has started), overlapping it
+        // through its flags; otherwise the cost sums run on the side stream beside the chains
         const int cap = B / 64 + 16;
         const size_t smem = (size_t)16 * cap;
+        TRY(ensure_side_stream(c));
         const int grid = std::max(1, std::min(2 * M, 4 * c->n_sms));
         TRY(set_smem_attr(k_s2_varcost, smem, c->device));
-        k_s2_varcost<<<grid, 256, smem, c->side>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap);
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+        const unsigned long long *pflags = c->npvm_flags.as<unsigned long long>();
         const long long nthr = 2ll * M * S * 32;  // a warp per (slot, scenario)
-        k_s2_chain<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(rec, B, T, S, c->Sp, M, db, ds, dr,
-                                                                  c->vmax.as<double>(), c->mass.as<double>(), c->rate,
-                                                                  braw, mraw);
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaStreamWaitEvent(st, c->ev_join, 0));
+        const int cgrid = (int)((nthr + 255) / 256);
+        if (pend_eh) {
+            TRY(launch_eval_n(k_s2_varcost, grid, 256, smem, st, true, rec, T, M, (const int32_t *)db, (const int32_t *)ds,
+                              (const int32_t *)dr, (const double *)c->cost.as<double>(), mcost, mn, cap,
+                              pflags + 2 * S, pend_eh, pend0, pend1));
+            TRY(launch_eval_n(k_s2_chain, cgrid, 256, 0, st, true, rec, B, T, S, c->Sp, M, (const int32_t *)db,
+                              (const int32_t *)ds, (const int32_t *)dr, (const double *)c->vmax.as<double>(),
+                              (const double *)c->mass.as<double>(), c->rate, (const double *)braw, mraw, pflags,
+                              pend_eh, pend0, pend1));
+        } else {
+            CUDA_TRY(cudaEventRecord(c->ev_fork, st));
+            CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+            k_s2_varcost<<<grid, 256, smem, c->side>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap,
+                                                       pflags, 0ull, -1, -1);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+            k_s2_chain<<<cgrid, 256, 0, st>>>(rec, B, T, S, c->Sp, M, db, ds, dr, c->vmax.as<double>(),
+                                              c->mass.as<double>(), c->rate, braw, mraw, pflags, 0ull, -1, -1);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaStreamWaitEvent(st, c->ev_join, 0));
+        }
     }
     ht_.mark("launch");
     double *dn = host ? c->h_d1.as<double>() : npv_out;
     if (T * S <= NPVF_MAX && T <= 32)
         k_npv_moves_final_staged<<<(M + NPVF_WARPS - 1) / NPVF_WARPS, 32 * NPVF_WARPS, 0, st>>>(
             T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc, c->disc.as<double>(),
-            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
+            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn, c->npvm_flags.as<unsigned long long>(),
+            pend_eh);
     else
         k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
                                                             c->disc.as<double>(),
-                                                            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn);
+                                                            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
+                                                            c->npvm_flags.as<unsigned long long>(), pend_eh);
     CUDA_TRY(cudaGetLastError());
     // the structure now describes `ha` (complete once the stream reaches this point)
     c->npvm_gen = c->npv_gen;
@@ -1524,6 +1702,9 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         ht_.mark("final+d2h");
         CUDA_TRY(stream_wait(st));
         ht_.mark("sync");
+#ifdef PP_EVAL_PROBE
+        kspan_append();
+#endif
         std::memcpy(npv_out, stage, sizeof(double) * M);
     }
     return PP_OK;
