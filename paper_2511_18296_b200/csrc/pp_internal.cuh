@@ -703,6 +703,7 @@ struct pp_ctx {
     DevBuf npvm_flags;            // pp_npv_moves: progress flags of the concurrent one-block update
     uint64_t npvm_flags_gen = 0;
     uint32_t npvm_epoch = 0;
+    unsigned long long npvm_vc = 0;  // cost-sum CTAs launched as dependents of an update (cumulative)
     DevBuf pr_score, pr_cap, pr_assign, pr_elig;       // pricing greedy (pp_price.cu)
     // device-resident lns insertion loop (pp_lns.cu): rook CSR (pp_set_rook), mean grades, the pool
     // (unordered list + positions), ranking keys, control block, per-round candidates and results

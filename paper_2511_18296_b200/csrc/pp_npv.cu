@@ -795,6 +795,7 @@ __global__ void __launch_bounds__(256) k_s2_chain(const S2Struct rec, int B, int
     // thread per chain measured 2.8x slower: each chain walks its own list, so the loads of a thread
     // are serialised by latency; the warp's coalesced batches are not.)
     constexpr unsigned FULL = 0xffffffffu;
+    asm volatile("griddepcontrol.launch_dependents;");  // the accumulation may start (it waits for us)
     KSPAN_BEGIN(2);
     const int lane = threadIdx.x & 31;
     const long long unit = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
                                                     const double *__restrict__ cost, double *__restrict__ mcost,
                                                     int32_t *__restrict__ mn, int cap,
                                                     const unsigned long long *__restrict__ cflag, unsigned long long eh,
-                                                    int pend0, int pend1) {
+                                                    int pend0, int pend1, unsigned long long *__restrict__ vc_done) {
     asm volatile("griddepcontrol.launch_dependents;");  // the chains may start (they wait on their own flags)
     KSPAN_BEGIN(1);
     // the pairwise plan's leaves (<= n/64 + 2) live in shared memory: cap of each array
@@ -968,6 +969,10 @@ __global__ void __launch_bounds__(256) k_s2_varcost(const S2Struct rec, int T, i
         __syncthreads();
     }
     KSPAN_END(1);
+    if (vc_done && threadIdx.x == 0) {  // this CTA's cost sums are written (the accumulation counts them)
+        __threadfence();
+        atomicAdd(vc_done, 1ull);
+    }
 }
 
 // _npv / per_scenario_npv accumulation in the reference's order (t outer, s inner)
@@ -1010,10 +1015,13 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
                                   const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                                   const double *__restrict__ disc,
                                   const double *__restrict__ sigma, double *__restrict__ npv,
-                                  const unsigned long long *__restrict__ pflags, unsigned long long eh) {
-    if (eh) {  // a one-block base update may still be finishing: every flag done first
+                                  const unsigned long long *__restrict__ pflags, unsigned long long eh,
+                                  unsigned long long vc_need) {
+    if (eh) {  // as k_npv_moves_final_staged
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int i = threadIdx.x; i < 2 * S + 2; i += blockDim.x)
             s2_flag_wait(pflags + i, i < 2 * S ? (eh | S2_DONE) : (eh | 1ull));
+        if (threadIdx.x == 0) s2_flag_wait(pflags + 2 * S + 2, vc_need);
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -1030,8 +1038,8 @@ __global__ void k_npv_moves_final(int T, int S, int M, const double *__restrict_
         if (t == t0 || t == t1) {
             const int k = slot_src[2 * m + (t == t0 ? 0 : 1)];  // deduplicated re-solve
             raw = mraw + (size_t)k * S;
-            cs = mcost[k];
-            n = mn[k];
+            cs = __ldcg(mcost + k);
+            n = __ldcg(mn + k);
         } else {
             raw = braw + (size_t)t * S;
             cs = __ldcg(bcost + t);
@@ -1068,13 +1076,16 @@ __global__ void __launch_bounds__(32 * NPVF_WARPS)
                              const int32_t *__restrict__ slot_t, const int32_t *__restrict__ slot_src,
                              const double *__restrict__ disc, const double *__restrict__ sigma,
                              double *__restrict__ npv, const unsigned long long *__restrict__ pflags,
-                             unsigned long long eh) {
-    // eh != 0: a one-block base update may still be finishing (its dependents need not wait for
-    // it): every base value is read after all its periods' flags say done
+                             unsigned long long eh, unsigned long long vc_need) {
+    // eh != 0: launched as a programmatic dependent of the chains, while the one-block base update
+    // and the cost sums may still be finishing: the chains' results after griddepcontrol.wait,
+    // the base values after every period's flag says done, the cost sums after all their CTAs
     KSPAN_BEGIN(3);
     if (eh) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int i = threadIdx.x; i < 2 * S + 2; i += blockDim.x)
             s2_flag_wait(pflags + i, i < 2 * S ? (eh | S2_DONE) : (eh | 1ull));
+        if (threadIdx.x == 0) s2_flag_wait(pflags + 2 * S + 2, vc_need);
         __syncthreads();
     }
     __shared__ double s_term[NPVF_WARPS][NPVF_MAX];
@@ -1094,8 +1105,8 @@ __global__ void __launch_bounds__(32 * NPVF_WARPS)
     }
     if (lane < T) {
         const int t = lane;
-        const double cs = t == t0 ? mcost[k0] : t == t1 ? mcost[k1] : __ldcg(bcost + t);
-        const int n = t == t0 ? mn[k0] : t == t1 ? mn[k1] : __ldcg(bn + t);
+        const double cs = t == t0 ? __ldcg(mcost + k0) : t == t1 ? __ldcg(mcost + k1) : __ldcg(bcost + t);
+        const int n = t == t0 ? __ldcg(mn + k0) : t == t1 ? __ldcg(mn + k1) : __ldcg(bn + t);
         s_cost[w][t] = n > 0 ? f64_mul(disc[t], cs) : kInf;
     }
     __syncwarp();
@@ -1302,7 +1313,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
                    const double *__restrict__ mass, const double *__restrict__ cost, const double *__restrict__ vmax,
                    const double *__restrict__ hours, double rate, double *__restrict__ raw,
                    double *__restrict__ costsum, int32_t *__restrict__ nmined, unsigned long long *__restrict__ prog,
-                   unsigned long long *__restrict__ cflag, unsigned long long eh) {
+                   unsigned long long *__restrict__ cflag, unsigned long long eh, int32_t *__restrict__ dbase) {
     // prog[y][s] / cflag[y] (y = blockIdx.y): progress of this update for the variants' kernels of
     // the same call, which run concurrently (programmatic dependents, launched once every CTA here
     // has started)
@@ -1312,6 +1323,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1)
     const int s = blockIdx.x;
     const bool ins = blockIdx.y == 1;
     const int t = ins ? t_new : t_old;
+    if (s == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbase[b] = t_new;  // the device copy of the base
     if (s == S) {  // the cost CTA
         if (t < 0) {
             if (threadIdx.x == 0) s2_flag_publish(cflag + blockIdx.y, eh | 1ull);
@@ -1454,8 +1466,11 @@ static int s2_struct(pp_ctx *c, S2Struct *r) {
 
 }  // extern "C"
 
+// hint (may be null): the only blocks that can differ from the cached base (pp_polish_sweep knows
+// them: the block it accepted since its previous evaluation), instead of the memcmp diff
 static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *blocks, const int32_t *periods, int32_t M,
-                          uint32_t flags, double *npv_out, int32_t mem, void *stream) {
+                          uint32_t flags, double *npv_out, int32_t mem, void *stream,
+                          const std::vector<int32_t> *hint = nullptr) {
     if (!c || !c->have_instance || !c->have_scen || !c->have_plant)
         return fail(PP_ERR_STATE, "pp_set_instance, pp_set_scenarios and pp_set_plant first");
     if (!assign || M < 0 || (M > 0 && (!blocks || !periods || !npv_out))) return fail(PP_ERR_INVALID_ARGS, "bad arguments");
@@ -1524,7 +1539,21 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     std::vector<int32_t> dirty, chg_b, chg_t;
     std::vector<int32_t> &cnt = c->npvm_cnt;
     bool full = !intact;
-    if (!full) {
+    if (!full && hint) {
+        std::vector<char> mark(T, 0);
+        const int32_t *old = c->npvm_base.data();
+        for (const int32_t b : *hint) {
+            const int32_t o = old[b], n = ha[b];
+            if (o == n) continue;
+            if (n < -1 || n >= T) return fail(PP_ERR_INVALID_ARGS, "assign[%d] = %d out of range", b, n);
+            if (o >= 0) mark[o] = 1;
+            if (n >= 0) mark[n] = 1;
+            chg_b.push_back(b);
+            chg_t.push_back(n);
+        }
+        for (int t = 0; t < T; t++)
+            if (mark[t]) dirty.push_back(t);
+    } else if (!full) {
         std::vector<char> mark(T, 0);
         const int32_t *old = c->npvm_base.data();
         for (int b0 = 0; b0 < B; b0 += 64) {
@@ -1602,7 +1631,10 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         std::copy(chg_t.begin(), chg_t.end(), pk + 8 * M + T + nchg);
     }
     CUDA_TRY(cudaMemcpyAsync(db, pk, sizeof(int32_t) * nin, cudaMemcpyHostToDevice, st));
-    if (nchg) {
+    // one moved block: the update kernel splices it (and writes its entry of the device base)
+    const bool splice = !full && chg_b.size() == 1 && c->npvm_cnt[dirty[0]] < 16000 &&
+                        (dirty.size() < 2 || c->npvm_cnt[dirty[1]] < 16000);
+    if (nchg && !splice) {
         k_scatter_assign<<<(unsigned)((nchg + 255) / 256), 256, 0, st>>>(dbase, dcb, dct, (int)nchg);
         CUDA_TRY(cudaGetLastError());
     }
@@ -1620,14 +1652,14 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     int32_t *bn = c->npv_n.as<int32_t>(), *mn = bn + T;
     if (full) {
         TRY(run_stage2(c, st, da, T, 1, braw, bcost, bn, nullptr, nullptr, nullptr, nullptr, &rec, may_be_big));
-    } else if (chg_b.size() == 1 && c->npvm_cnt[dirty[0]] < 16000 &&
-               (dirty.size() < 2 || c->npvm_cnt[dirty[1]] < 16000)) {  // one block moved: splice
+    } else if (splice) {  // one block moved: splice
         const int bb = chg_b[0], to = c->npvm_base[bb], tn = chg_t[0];
-        TRY(c->npvm_flags.ensure(sizeof(unsigned long long) * (2 * (size_t)S + 2)));
-        if (c->npvm_flags.gen != c->npvm_flags_gen) {  // fresh buffer: epoch 0 everywhere
-            CUDA_TRY(cudaMemsetAsync(c->npvm_flags.ptr, 0, sizeof(unsigned long long) * (2 * (size_t)S + 2), st));
+        TRY(c->npvm_flags.ensure(sizeof(unsigned long long) * (2 * (size_t)S + 3)));
+        if (c->npvm_flags.gen != c->npvm_flags_gen) {  // fresh buffer: epoch 0 everywhere, no CTA counted
+            CUDA_TRY(cudaMemsetAsync(c->npvm_flags.ptr, 0, sizeof(unsigned long long) * (2 * (size_t)S + 3), st));
             c->npvm_flags_gen = c->npvm_flags.gen;
             c->npvm_epoch = 0;
+            c->npvm_vc = 0;
         }
         pend_eh = (unsigned long long)(++c->npvm_epoch) << 32;
         pend0 = to;
@@ -1635,7 +1667,7 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         k_s2_apply_one<<<dim3(S + 1, 2), S2_THREADS, 0, st>>>(
             rec, B, T, S, c->Sp, bb, to, tn, c->mass.as<double>(), c->cost.as<double>(), c->vmax.as<double>(),
             c->hours.as<double>(), c->rate, braw, bcost, bn, c->npvm_flags.as<unsigned long long>(),
-            c->npvm_flags.as<unsigned long long>() + 2 * S, pend_eh);
+            c->npvm_flags.as<unsigned long long>() + 2 * S, pend_eh, dbase);
         CUDA_TRY(cudaGetLastError());
     } else if (!dirty.empty())
         TRY(run_stage2(c, st, da, (int)dirty.size(), 1, braw, bcost, bn, nullptr, nullptr, nullptr, dtsel, &rec,
@@ -1654,9 +1686,10 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
         const long long nthr = 2ll * M * S * 32;  // a warp per (slot, scenario)
         const int cgrid = (int)((nthr + 255) / 256);
         if (pend_eh) {
+            c->npvm_vc += (unsigned long long)grid;  // the accumulation waits for this many finished CTAs
             TRY(launch_eval_n(k_s2_varcost, grid, 256, smem, st, true, rec, T, M, (const int32_t *)db, (const int32_t *)ds,
                               (const int32_t *)dr, (const double *)c->cost.as<double>(), mcost, mn, cap,
-                              pflags + 2 * S, pend_eh, pend0, pend1));
+                              pflags + 2 * S, pend_eh, pend0, pend1, c->npvm_flags.as<unsigned long long>() + 2 * S + 2));
             TRY(launch_eval_n(k_s2_chain, cgrid, 256, 0, st, true, rec, B, T, S, c->Sp, M, (const int32_t *)db,
                               (const int32_t *)ds, (const int32_t *)dr, (const double *)c->vmax.as<double>(),
                               (const double *)c->mass.as<double>(), c->rate, (const double *)braw, mraw, pflags,
@@ -1665,7 +1698,7 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
             CUDA_TRY(cudaEventRecord(c->ev_fork, st));
             CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
             k_s2_varcost<<<grid, 256, smem, c->side>>>(rec, T, M, db, ds, dr, c->cost.as<double>(), mcost, mn, cap,
-                                                       pflags, 0ull, -1, -1);
+                                                       pflags, 0ull, -1, -1, nullptr);
             CUDA_TRY(cudaGetLastError());
             CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
             k_s2_chain<<<cgrid, 256, 0, st>>>(rec, B, T, S, c->Sp, M, db, ds, dr, c->vmax.as<double>(),
@@ -1676,17 +1709,22 @@ static int npv_moves_impl(pp_ctx *c, const int32_t *assign, const int32_t *block
     }
     ht_.mark("launch");
     double *dn = host ? c->h_d1.as<double>() : npv_out;
-    if (T * S <= NPVF_MAX && T <= 32)
-        k_npv_moves_final_staged<<<(M + NPVF_WARPS - 1) / NPVF_WARPS, 32 * NPVF_WARPS, 0, st>>>(
-            T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc, c->disc.as<double>(),
-            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn, c->npvm_flags.as<unsigned long long>(),
-            pend_eh);
-    else
-        k_npv_moves_final<<<(M + 7) / 8, 256, 0, st>>>(T, S, M, braw, bcost, bn, mraw, mcost, mn, ds, dsrc,
-                                                            c->disc.as<double>(),
-                                                            (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr, dn,
-                                                            c->npvm_flags.as<unsigned long long>(), pend_eh);
-    CUDA_TRY(cudaGetLastError());
+    {
+        const double *sg = (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : nullptr;
+        const unsigned long long *pf = c->npvm_flags.as<unsigned long long>();
+        const bool pdl = pend_eh != 0;  // a programmatic dependent of the chains (see the kernels)
+        if (T * S <= NPVF_MAX && T <= 32)
+            TRY(launch_eval_n(k_npv_moves_final_staged, (M + NPVF_WARPS - 1) / NPVF_WARPS, 32 * NPVF_WARPS, 0, st, pdl,
+                              T, S, M, (const double *)braw, (const double *)bcost, (const int32_t *)bn,
+                              (const double *)mraw, (const double *)mcost, (const int32_t *)mn, (const int32_t *)ds,
+                              (const int32_t *)dsrc, (const double *)c->disc.as<double>(), sg, dn, pf, pend_eh,
+                              c->npvm_vc));
+        else
+            TRY(launch_eval_n(k_npv_moves_final, (M + 7) / 8, 256, 0, st, pdl, T, S, M, (const double *)braw,
+                              (const double *)bcost, (const int32_t *)bn, (const double *)mraw, (const double *)mcost,
+                              (const int32_t *)mn, (const int32_t *)ds, (const int32_t *)dsrc,
+                              (const double *)c->disc.as<double>(), sg, dn, pf, pend_eh, c->npvm_vc));
+    }
     // the structure now describes `ha` (complete once the stream reaches this point)
     c->npvm_gen = c->npv_gen;
     c->npvm_bufgen[0] = c->npv_raw.gen;
@@ -1740,6 +1778,7 @@ int pp_polish_sweep(pp_ctx *c, int32_t *assign, double *load, double *cur_val, u
     std::vector<int32_t> ob, ot;   // the chunk's options (block, period)
     std::vector<int32_t> first;    // per chunk block: index of its first option, then one past the last
     std::vector<double> vals;
+    std::vector<int32_t> moved;  // blocks accepted since the previous evaluation (its diff)
     int improved = 0;
     int64_t calls = 0;
     double cv = *cur_val;
@@ -1787,7 +1826,8 @@ int pp_polish_sweep(pp_ctx *c, int32_t *assign, double *load, double *cur_val, u
         if (!ob.empty()) {
             vals.resize(ob.size());
             TRY(npv_moves_impl(c, assign, ob.data(), ot.data(), (int32_t)ob.size(), flags, vals.data(), PP_MEM_HOST,
-                               nullptr));
+                               nullptr, calls ? &moved : nullptr));
+            moved.clear();
             calls++;
             for (int b = b0; b < b1; b++) {
                 const int lo = first[b - b0], hi = first[b - b0 + 1];
@@ -1801,6 +1841,7 @@ int pp_polish_sweep(pp_ctx *c, int32_t *assign, double *load, double *cur_val, u
                         best_val = vals[q];
                     }
                 if (best_t != orig) {
+                    moved.push_back(b);  // the next evaluation's base differs from this one's in b only
                     assign[b] = best_t;
                     improved = 1;
                     cv = best_val;
