@@ -255,6 +255,8 @@ int pp_ctx_destroy(pp_ctx *c) {
     if (c->h_bad) cudaFreeHost(c->h_bad);
     if (c->h_bounce) cudaFreeHost(c->h_bounce);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->lns_exec) cudaGraphExecDestroy(c->lns_exec);
+    if (c->lns_graph) cudaGraphDestroy(c->lns_graph);
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);

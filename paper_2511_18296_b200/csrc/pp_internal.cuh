@@ -709,6 +709,9 @@ struct pp_ctx {
     // (unordered list + positions), ranking keys, control block, per-round candidates and results
     DevBuf lns_rptr, lns_ridx, lns_mg, lns_pool, lns_pos, lns_keys, lns_ctl, lns_out;
     bool have_rook = false;
+    cudaGraph_t lns_graph = nullptr;      // the cached insertion-loop graph (pp_lns_insert)
+    cudaGraphExec_t lns_exec = nullptr;
+    uint64_t lns_key[3] = {0, 0, 0};      // width, flags, sum of the buffers' allocation generations
     bool bad_pending = false;
     DevBuf h_cand, h_a, h_b, h_o1, h_o2, h_o3, h_o4, h_o5, h_o6, h_o7, h_o8, h_glob, h_assign, h_i64, h_d1, h_d2,
         h_pm, h_p;

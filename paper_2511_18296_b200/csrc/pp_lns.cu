@@ -153,6 +153,78 @@ __global__ void k_lns_apply(LnsCtl *__restrict__ ctl, const pp_best *__restrict_
     cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
+// The graph: k_lns_begin (the initial condition) -> WHILE { the round }, the round captured
+// into the loop body (c->lns_graph / c->lns_exec)
+static int lns_build_graph(pp_ctx *c, cudaStream_t st, int W, uint32_t flags, LnsCtl *dctl, int32_t *dpool,
+                           int32_t *dpos, int32_t *dcand, pp_best *rec, const pp_cand_out &o) {
+    cudaGraph_t g = nullptr;
+    auto bail = [&](int r) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+    };
+    CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hc;
+    if (cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+        return bail(fail(PP_ERR_CUDA, "cudaGraphConditionalHandleCreate: %s", cudaGetErrorString(cudaGetLastError())));
+    cudaGraphNode_t begin;
+    {
+        cudaKernelNodeParams kp = {};
+        void *args[] = {&dctl, &hc};
+        kp.func = reinterpret_cast<void *>(k_lns_begin);
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        if (cudaGraphAddKernelNode(&begin, g, nullptr, 0, &kp) != cudaSuccess)
+            return bail(fail(PP_ERR_CUDA, "graph: k_lns_begin node: %s", cudaGetErrorString(cudaGetLastError())));
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hc;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    if (cudaGraphAddNode(&loop, g, &begin, 1, &cp) != cudaSuccess)
+        return bail(fail(PP_ERR_CUDA, "graph: WHILE node: %s", cudaGetErrorString(cudaGetLastError())));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    // the round, captured into the loop body
+    if (cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return bail(fail(PP_ERR_CUDA, "capture: %s", cudaGetErrorString(cudaGetLastError())));
+    // the ranking (one CTA) runs beside the period masses (one cluster): both read only the round's
+    // schedule; the evaluation joins them
+    int rc = PP_OK;
+    rc = ensure_side_stream(c);
+    if (rc == PP_OK && (cudaEventRecord(c->ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev_fork, 0) != cudaSuccess))
+        rc = fail(PP_ERR_CUDA, "lns: fork");
+    if (rc == PP_OK) {
+        k_lns_rank<<<1, LNS_THREADS, 0, c->side>>>(dctl, dpool, c->assign_ptr, c->lns_mg.as<double>(),
+                                                   c->lns_rptr.as<int32_t>(), c->lns_ridx.as<int32_t>(),
+                                                   c->lns_keys.as<unsigned long long>(), dcand, W);
+        if (cudaGetLastError() != cudaSuccess || cudaEventRecord(c->ev_join, c->side) != cudaSuccess)
+            rc = fail(PP_ERR_CUDA, "lns: k_lns_rank");
+    }
+    if (rc == PP_OK) {
+        bool launched;
+        c->pm_dirty = true;  // every round recomputes the period masses of the round's schedule
+        rc = refresh_pm(c, st, &launched, nullptr);
+    }
+    if (rc == PP_OK && cudaStreamWaitEvent(st, c->ev_join, 0) != cudaSuccess) rc = fail(PP_ERR_CUDA, "lns: join");
+    if (rc == PP_OK) rc = pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st);
+    if (rc == PP_OK) {
+        k_lns_apply<<<1, 32, 0, st>>>(dctl, rec, c->rows.as<BlockRow>(), c->assign.as<int32_t>(), dpool, dpos, hc);
+        if (cudaGetLastError() != cudaSuccess) rc = fail(PP_ERR_CUDA, "k_lns_apply launch");
+    }
+    cudaGraph_t cap = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &cap);
+    if (rc != PP_OK) return bail(rc);
+    if (ec != cudaSuccess) return bail(fail(PP_ERR_CUDA, "end capture: %s", cudaGetErrorString(ec)));
+    cudaGraphExec_t ex = nullptr;
+    if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess)
+        return bail(fail(PP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(cudaGetLastError())));
+    c->lns_graph = g;
+    c->lns_exec = ex;
+    return PP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -191,6 +263,7 @@ int pp_lns_insert(pp_ctx *c, int32_t *assign, uint8_t *pool, const double *mean_
         return fail(PP_ERR_SHAPE, "candidate_width %d outside [1, %d]", candidate_width, LNS_WMAX);
     if (max_iters < 0) return fail(PP_ERR_INVALID_ARGS, "max_iters < 0");
     flags &= (PP_NET_MINING_COST | PP_USE_SIGMA);
+    HostTrace ht("pp_lns_insert");
     TRY(use_device(c));
     cudaStream_t st = c->stream;
     const int B = c->B, W = candidate_width;
@@ -239,94 +312,42 @@ int pp_lns_insert(pp_ctx *c, int32_t *assign, uint8_t *pool, const double *mean_
     o.feasible = fe;
     o.global = rec;
     o.realism = rec + 1;
-    // one uncaptured evaluation first: every scratch buffer and kernel attribute the round needs is
-    // in place before capture (no allocation or attribute call may happen inside it)
-    TRY(pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st));
-
-    cudaGraph_t g = nullptr, body = nullptr;
-    cudaGraphExec_t ex = nullptr;
-    int rc = PP_OK;
-    auto done = [&](int r) {
-        if (ex) cudaGraphExecDestroy(ex);
-        if (g) cudaGraphDestroy(g);
-        c->pm_dirty = true;  // the schedule changed on the device
-        return r;
-    };
-    CUDA_TRY(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle hc;
-    if (cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
-        return done(fail(PP_ERR_CUDA, "cudaGraphConditionalHandleCreate: %s", cudaGetErrorString(cudaGetLastError())));
-    cudaGraphNode_t begin;
-    {
-        cudaKernelNodeParams kp = {};
-        void *args[] = {&dctl, &hc};
-        kp.func = reinterpret_cast<void *>(k_lns_begin);
-        kp.gridDim = dim3(1);
-        kp.blockDim = dim3(1);
-        kp.kernelParams = args;
-        if (cudaGraphAddKernelNode(&begin, g, nullptr, 0, &kp) != cudaSuccess)
-            return done(fail(PP_ERR_CUDA, "graph: k_lns_begin node: %s", cudaGetErrorString(cudaGetLastError())));
+    // the executable graph is kept in the context and reused while its shape (width, flags) and
+    // every device buffer it references (no re-allocation since: the sum of the buffers'
+    // allocation generations) are unchanged; a call then costs the uploads, one launch, the copies
+    uint64_t gensum = 0;
+    for (DevBuf *d : c->all()) gensum += d->gen;
+    const uint64_t key[3] = {(uint64_t)W, (uint64_t)flags, gensum};
+    if (!c->lns_exec || memcmp(key, c->lns_key, sizeof(key)) != 0) {
+        if (c->lns_exec) cudaGraphExecDestroy(c->lns_exec);
+        if (c->lns_graph) cudaGraphDestroy(c->lns_graph);
+        c->lns_exec = nullptr;
+        c->lns_graph = nullptr;
+        // one uncaptured evaluation first: every scratch buffer and kernel attribute the round needs
+        // is in place before capture (no allocation or attribute call may happen inside it)
+        TRY(pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st));
+        gensum = 0;  // (that evaluation may have grown a buffer)
+        for (DevBuf *d : c->all()) gensum += d->gen;
+        const uint64_t key2[3] = {(uint64_t)W, (uint64_t)flags, gensum};
+        TRY(lns_build_graph(c, st, W, flags, dctl, dpool, dpos, dcand, rec, o));
+        memcpy(c->lns_key, key2, sizeof(key2));
+        ht.mark("build");
     }
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = hc;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t loop;
-    if (cudaGraphAddNode(&loop, g, &begin, 1, &cp) != cudaSuccess)
-        return done(fail(PP_ERR_CUDA, "graph: WHILE node: %s", cudaGetErrorString(cudaGetLastError())));
-    body = cp.conditional.phGraph_out[0];
-    // the round, captured into the loop body
-    if (cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
-        return done(fail(PP_ERR_CUDA, "capture: %s", cudaGetErrorString(cudaGetLastError())));
-    // the ranking (one CTA) runs beside the period masses (one cluster): both read only the round's
-    // schedule; the evaluation joins them
-    const int32_t *dassign = c->assign_ptr;
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
-        rc = fail(PP_ERR_CUDA, "lns: stream / events");
-    if (rc == PP_OK && (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess))
-        rc = fail(PP_ERR_CUDA, "lns: fork");
-    if (rc == PP_OK) {
-        k_lns_rank<<<1, LNS_THREADS, 0, side>>>(dctl, dpool, dassign, c->lns_mg.as<double>(), c->lns_rptr.as<int32_t>(),
-                                                c->lns_ridx.as<int32_t>(), c->lns_keys.as<unsigned long long>(), dcand, W);
-        if (cudaGetLastError() != cudaSuccess || cudaEventRecord(join, side) != cudaSuccess)
-            rc = fail(PP_ERR_CUDA, "lns: k_lns_rank");
+    if (cudaGraphLaunch(c->lns_exec, st) != cudaSuccess) {
+        c->pm_dirty = true;
+        return fail(PP_ERR_CUDA, "graph launch: %s", cudaGetErrorString(cudaGetLastError()));
     }
-    if (rc == PP_OK) {
-        bool launched;
-        c->pm_dirty = true;  // every round recomputes the period masses of the round's schedule
-        rc = refresh_pm(c, st, &launched, nullptr);
-    }
-    if (rc == PP_OK && cudaStreamWaitEvent(st, join, 0) != cudaSuccess) rc = fail(PP_ERR_CUDA, "lns: join");
-    if (rc == PP_OK) rc = pp_eval_candidates(c, dcand, W, PP_SCENARIO_EXPECTED, flags, &o, PP_MEM_DEVICE, st);
-    if (rc == PP_OK) {
-        k_lns_apply<<<1, 32, 0, st>>>(dctl, rec, c->rows.as<BlockRow>(), c->assign.as<int32_t>(), dpool, dpos, hc);
-        if (cudaGetLastError() != cudaSuccess) rc = fail(PP_ERR_CUDA, "k_lns_apply launch");
-    }
-    cudaGraph_t cap = nullptr;
-    const cudaError_t ec = cudaStreamEndCapture(st, &cap);
-    if (fork) cudaEventDestroy(fork);
-    if (join) cudaEventDestroy(join);
-    if (side) cudaStreamDestroy(side);
-    if (rc != PP_OK) return done(rc);
-    if (ec != cudaSuccess) return done(fail(PP_ERR_CUDA, "end capture: %s", cudaGetErrorString(ec)));
-    if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess)
-        return done(fail(PP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(cudaGetLastError())));
-    if (cudaGraphLaunch(ex, st) != cudaSuccess)
-        return done(fail(PP_ERR_CUDA, "graph launch: %s", cudaGetErrorString(cudaGetLastError())));
+    c->pm_dirty = true;  // the schedule changes on the device
     CUDA_TRY(cudaMemcpyAsync(assign, c->assign.ptr, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(pos.data(), dpos, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(&h, dctl, sizeof(LnsCtl), cudaMemcpyDeviceToHost, st));
     const cudaError_t es = cudaStreamSynchronize(st);
-    if (es != cudaSuccess) return done(fail(PP_ERR_CUDA, "lns graph: %s", cudaGetErrorString(es)));
+    if (es != cudaSuccess) return fail(PP_ERR_CUDA, "lns graph: %s", cudaGetErrorString(es));
+    ht.mark("run+d2h");
     for (int b = 0; b < B; b++) pool[b] = pos[b] >= 0 ? 1 : 0;
     *iters_out = h.iters;
     *stalled_out = h.stalled;
-    return done(PP_OK);
+    return PP_OK;
 }
 
 }  // extern "C"
