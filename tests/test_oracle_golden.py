@@ -285,3 +285,19 @@ def test_vectorised_neighbor_similarity_matches_scalar():
             assert v == ref[b] and np.signbit(v) == np.signbit(ref[b]), (it, b)
         order = blocks[np.lexsort((blocks, -got))].tolist()
         assert order == sorted(blocks.tolist(), key=lambda b: (-ref[b], b))
+
+
+def test_rook_csr_matches_the_neighbour_map():
+    """evaluate._rook_csr (what pp_set_rook receives) holds every block's rook neighbours in the
+    reference order (hybrid.py:159-166), and the list lengths stay within the device ranking's 7."""
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.evaluate import _rook_csr
+    from paper_2511_18296_b200.model import rook_neighbor_map, rook_padded
+
+    bm = synth.generate_block_model(7 * 6 * 5, (7, 6, 5), 5, 1, seed=4, n_rock_types=1)
+    rook = rook_neighbor_map(bm)
+    ptr, idx = _rook_csr(rook_padded(rook, bm.n_blocks))
+    assert ptr.dtype == np.int32 and idx.dtype == np.int32 and ptr[0] == 0 and ptr.size == bm.n_blocks + 1
+    assert int(np.max(np.diff(ptr))) <= 7
+    for b in range(bm.n_blocks):
+        assert idx[ptr[b]:ptr[b + 1]].tolist() == rook.get(b, [])
