@@ -33,7 +33,7 @@ __global__ void walk(const double *D, const double *M, int n, double rate, doubl
             q1 = in1 ? f64_div(m2, rate) : 0.0;
             dm1 = in1 ? f64_mul(d2, m2) : 0.0;
             if (kk + 64 < n) { m2 = M[kk + 64]; d2 = D[kk + 64]; }
-        } else if (V == 3 || V == 5 || V == 6 || V == 7) {  // this batch's inputs were loaded one batch ahead
+        } else if (V == 3 || V >= 5) {  // this batch's inputs were loaded one batch ahead
             m = in ? m_nx : 0.0;
             q = in ? f64_div(m, rate) : 0.0;
             dm = in ? f64_mul(d_nx, m) : 0.0;
@@ -85,6 +85,64 @@ __global__ void walk(const double *D, const double *M, int n, double rate, doubl
             // the batch's end state: lane 31's state minus its own element
             h = __shfl_sync(0xffffffffu, f64_sub(h, q), 31);
             tt = __shfl_sync(0xffffffffu, f64_add(tt, dm), 31);
+            __syncwarp();
+        } else if (V == 9) {  // as V3, the next group's terms loaded while this group's steps run
+            s_q[lane] = q;
+            s_dm[lane] = dm;
+            __syncwarp();
+            double qa[8], da[8], qb[8], db[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) { qa[u] = s_q[u]; da[u] = s_dm[u]; }
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+                if (g < 3) {
+#pragma unroll
+                    for (int u = 0; u < 8; u++) { qb[u] = s_q[(g + 1) * 8 + u]; db[u] = s_dm[(g + 1) * 8 + u]; }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    if (lane == g * 8 + u) { h_mine = h; t_mine = tt; }
+                    h = f64_sub(h, qa[u]);
+                    tt = f64_add(tt, da[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) { qa[u] = qb[u]; da[u] = db[u]; }
+            }
+            __syncwarp();
+        } else if (V == 10) {  // as V3 with groups of 16
+            s_q[lane] = q;
+            s_dm[lane] = dm;
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 2; g++) {
+                double qa[16], da[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) { qa[u] = s_q[g * 16 + u]; da[u] = s_dm[g * 16 + u]; }
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    if (lane == g * 16 + u) { h_mine = h; t_mine = tt; }
+                    h = f64_sub(h, qa[u]);
+                    tt = f64_add(tt, da[u]);
+                }
+            }
+            __syncwarp();
+        } else if (V == 11) {  // timing floor only (not the algorithm): V3 without the state captures
+            s_q[lane] = q;
+            s_dm[lane] = dm;
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+                double qa[8], da[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) { qa[u] = s_q[g * 8 + u]; da[u] = s_dm[g * 8 + u]; }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    h = f64_sub(h, qa[u]);
+                    tt = f64_add(tt, da[u]);
+                }
+            }
+            h_mine = h;
+            t_mine = tt;
             __syncwarp();
         } else if (V == 5) {  // as V3, the states stored per step (one broadcast store) instead of selects
             s_q[lane] = q;
@@ -140,6 +198,56 @@ __global__ void walk(const double *D, const double *M, int n, double rate, doubl
     if (lane == 0) { out[0] = tot + hl; cyc[0] = t1 - t0; }
 }
 
+// V12: 64 elements per batch (lane l holds elements l and 32 + l), inputs one batch ahead
+__global__ void walk64(const double *D, const double *M, int n, double rate, double h0, double *out, long long *cyc) {
+    __shared__ double s_q[64], s_dm[64];
+    const int lane = threadIdx.x & 31;
+    double hl = h0, tot = 0.0;
+    long long t0 = clock64();
+    double ma = lane < n ? M[lane] : 0.0, da_ = lane < n ? D[lane] : 0.0;
+    double mb = lane + 32 < n ? M[lane + 32] : 0.0, db_ = lane + 32 < n ? D[lane + 32] : 0.0;
+    for (int k0 = 0; k0 < n; k0 += 64) {
+        const int ka = k0 + lane, kb = k0 + 32 + lane;
+        const bool ina = ka < n, inb = kb < n;
+        const double m0 = ina ? ma : 0.0, m1 = inb ? mb : 0.0;
+        s_q[lane] = ina ? f64_div(m0, rate) : 0.0;
+        s_dm[lane] = ina ? f64_mul(da_, m0) : 0.0;
+        s_q[32 + lane] = inb ? f64_div(m1, rate) : 0.0;
+        s_dm[32 + lane] = inb ? f64_mul(db_, m1) : 0.0;
+        if (ka + 64 < n) { ma = M[ka + 64]; da_ = D[ka + 64]; }
+        if (kb + 64 < n) { mb = M[kb + 64]; db_ = D[kb + 64]; }
+        __syncwarp();
+        double h = hl, tt = tot, ha = 0.0, ta = 0.0, hb = 0.0, tb = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; g++) {
+            double qa[8], dd[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) { qa[u] = s_q[g * 8 + u]; dd[u] = s_dm[g * 8 + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int j = g * 8 + u;
+                if (j < 32) { if (lane == j) { ha = h; ta = tt; } }
+                else { if (lane == j - 32) { hb = h; tb = tt; } }
+                h = f64_sub(h, qa[u]);
+                tt = f64_add(tt, dd[u]);
+            }
+        }
+        __syncwarp();
+        const bool sa = !ina || !(ha > 0) || f64_mul(ha, rate) < m0;
+        const bool sb = !inb || !(hb > 0) || f64_mul(hb, rate) < m1;
+        const unsigned ba = __ballot_sync(0xffffffffu, sa), bb = __ballot_sync(0xffffffffu, sb);
+        if (ba | bb) {
+            if (ba) { const int jf = __ffs(ba) - 1; hl = __shfl_sync(0xffffffffu, ha, jf); tot = __shfl_sync(0xffffffffu, ta, jf); }
+            else { const int jf = __ffs(bb) - 1; hl = __shfl_sync(0xffffffffu, hb, jf); tot = __shfl_sync(0xffffffffu, tb, jf); }
+            break;
+        }
+        hl = h;
+        tot = tt;
+    }
+    long long t1 = clock64();
+    if (lane == 0) { out[0] = tot + hl; cyc[0] = t1 - t0; }
+}
+
 int main() {
     const int n = 4096;
     double *D, *M, *o; long long *c;
@@ -167,6 +275,16 @@ int main() {
         printf("V7 = V3, lanes stop at their element: same result %d\n", (int)(o[0] == r7));
         walk<7><<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
         printf("V7 = V3, lanes stop at their element: %.1f cycles/element\n", c[0] / (double)n);
+        walk<9><<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
+        printf("V9 = V3, next group loaded during this group: %.1f cycles/element\n", c[0] / (double)n);
+        walk<10><<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
+        printf("V10 = V3 with groups of 16: %.1f cycles/element\n", c[0] / (double)n);
+        walk<11><<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
+        printf("V11 (floor, no captures): %.1f cycles/element\n", c[0] / (double)n);
+        walk<3><<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
+        const double r3 = o[0];
+        walk64<<<1, 32>>>(D, M, n, rate, h0, o, c); cudaDeviceSynchronize();
+        printf("V12 64 elements per batch: %.1f cycles/element (same result %d)\n", c[0] / (double)n, (int)(o[0] == r3));
     }
 }
 
