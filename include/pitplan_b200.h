@@ -168,6 +168,20 @@ PP_API int pp_set_scenarios(pp_ctx *ctx, int32_t n_scenarios, const double *vmax
 PP_API int pp_set_scenarios_grades(pp_ctx *ctx, int32_t n_scenarios, const double *grades_sb, int32_t n_modes,
                                    double price, const double *recovery, int32_t n_recovery, const double *proc_cost,
                                    int32_t n_proc_cost, const double *sigma_st);
+/* VAE scenario source on the device (vae.py:91-93, 284-292; the decoder of nn.py:42-53): the
+ * decoder's n_layers dense layers with widths[0] = latent dim ... widths[n_layers] = B, params =
+ * for each layer W[out][in] (row-major, as Dense.W) then b[out], and the normalisation norm_mean[B],
+ * norm_std[B].  The decode agrees with numpy's (BLAS) to rounding, not bit for bit. */
+PP_API int pp_set_vae_decoder(pp_ctx *ctx, int32_t n_layers, const int32_t *widths, const double *params,
+                              const double *norm_mean, const double *norm_std);
+/* grades[S][B] = max(decoder(z) * norm_std + norm_mean, 0) for prior samples z[S][latent]. */
+PP_API int pp_vae_decode(pp_ctx *ctx, int32_t n_scenarios, const double *z, double *grades_out, int32_t mem,
+                         void *stream);
+/* Decode z[S][latent] and bind the grades as the scenario set (the value table built on the device
+ * as pp_set_scenarios_grades; the grades never visit the host). */
+PP_API int pp_set_scenarios_vae(pp_ctx *ctx, int32_t n_scenarios, const double *z, int32_t n_modes, double price,
+                                const double *recovery, int32_t n_recovery, const double *proc_cost,
+                                int32_t n_proc_cost, const double *sigma_st);
 /* The bound value table back in the reference layout vmax[S][B] (host output). */
 PP_API int pp_get_scenario_values(pp_ctx *ctx, double *vmax_sb_out);
 

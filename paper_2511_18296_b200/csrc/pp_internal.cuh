@@ -709,6 +709,9 @@ struct pp_ctx {
     // (unordered list + positions), ranking keys, control block, per-round candidates and results
     DevBuf lns_rptr, lns_ridx, lns_mg, lns_pool, lns_pos, lns_keys, lns_ctl, lns_out;
     bool have_rook = false;
+    // VAE decoder (pp_vae.cu): layer widths, packed W/b per layer, norm_mean | norm_std, scratch
+    std::vector<int32_t> vae_widths;
+    DevBuf vae_params, vae_norm, vae_h, vae_io;
     cudaGraph_t lns_graph = nullptr;      // the cached insertion-loop graph (pp_lns_insert)
     cudaGraphExec_t lns_exec = nullptr;
     uint64_t lns_key[3] = {0, 0, 0};      // width, flags, sum of the buffers' allocation generations
@@ -721,7 +724,7 @@ struct pp_ctx {
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
                 &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig,
-                &pm_bad, &npvm_flags, &lns_rptr, &lns_ridx, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
+                &pm_bad, &npvm_flags, &vae_params, &vae_norm, &vae_h, &vae_io, &lns_rptr, &lns_ridx, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
     }
 };
 

@@ -1585,6 +1585,38 @@ int pp_set_scenarios_grades(pp_ctx *c, int32_t S, const double *grades_sb, int32
     return rc;
 }
 
+}  // extern "C"
+
+// grades[S][B] already on the device (the VAE decode, pp_vae.cu) bound as the scenario set: the value
+// table built by k_scen_from_grades exactly as pp_set_scenarios_grades does for host grades
+int set_scenarios_from_device_grades(pp_ctx *c, int32_t S, const double *dgrades, int32_t n_modes, double price,
+                                     const double *recovery, int32_t n_recovery, const double *proc_cost,
+                                     int32_t n_proc_cost, const double *sigma_st) {
+    if (!c || !c->have_instance) return fail(PP_ERR_STATE, "pp_set_instance first");
+    if (S < 1 || !dgrades) return fail(PP_ERR_INVALID_ARGS, "need n_scenarios >= 1 and a grade matrix");
+    if (n_modes < 1 || !recovery || n_recovery < 1 || !proc_cost || n_proc_cost < 1)
+        return fail(PP_ERR_INVALID_ARGS, "need at least one operating mode with recovery and processing cost");
+    const int B = c->B;
+    DevBuf par;
+    TRY(par.ensure(sizeof(double) * (size_t)(n_recovery + n_proc_cost)));
+    const int rc = set_scenarios_common(c, S, sigma_st, [&](int Sp) {
+        cudaError_t e = dev_upload(c, par.ptr, recovery, sizeof(double) * n_recovery);
+        if (e == cudaSuccess) e = dev_upload(c, par.as<double>() + n_recovery, proc_cost, sizeof(double) * n_proc_cost);
+        if (e == cudaSuccess) {
+            k_scen_from_grades<<<(B + 127) / 128, 128, 0, c->stream>>>(
+                dgrades, S, B, Sp, c->mass.as<double>(), price, par.as<double>(), n_recovery,
+                par.as<double>() + n_recovery, n_proc_cost, n_modes, c->vmax.as<double>(), c->unit_mean.as<double>());
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        return e;
+    });
+    par.release();
+    return rc;
+}
+
+extern "C" {
+
 int pp_get_scenario_values(pp_ctx *c, double *vmax_sb_out) {
     if (!c || !c->have_scen) return fail(PP_ERR_STATE, "pp_set_scenarios first");
     if (!vmax_sb_out) return fail(PP_ERR_INVALID_ARGS, "vmax_sb_out is NULL");

@@ -134,10 +134,57 @@ class Engine:
         self.has_sigma = sig is not None
         self._tables = tables
 
+    def set_vae_decoder(self, decoder):
+        """Upload a model.VaeDecoder (the VAE's decoder MLP and normalisation)."""
+        bm = self._need_bm()
+        widths = np.array(decoder.widths, dtype=np.int32)
+        if widths[-1] != bm.n_blocks:
+            raise ShapeMismatch("the decoder's output width differs from the instance's block count")
+        params = decoder.packed()
+        nm = np.ascontiguousarray(decoder.norm_mean, dtype=np.float64)
+        ns = np.ascontiguousarray(decoder.norm_std, dtype=np.float64)
+        check(self.lib.pp_set_vae_decoder(self._h, int(widths.size - 1), ptr(widths), ptr(params), ptr(nm), ptr(ns)))
+        self._vae_latent = int(widths[0])
+
+    def vae_decode(self, z) -> np.ndarray:
+        """grades[S][B] = max(decoder(z) * norm_std + norm_mean, 0) on the device (vae.py:284-292)."""
+        bm = self._need_bm()
+        zz = np.ascontiguousarray(np.atleast_2d(z), dtype=np.float64)
+        if zz.shape[1] != getattr(self, "_vae_latent", -1):
+            raise ShapeMismatch("z must be [S][latent_dim] of the bound decoder")
+        out = np.empty((zz.shape[0], bm.n_blocks), np.float64)
+        check(self.lib.pp_vae_decode(self._h, zz.shape[0], ptr(zz), ptr(out), _lib.PP_MEM_HOST, None))
+        return out
+
+    def set_scenarios_vae(self, z, sigma=None):
+        """Decode prior samples z[S][latent] on the device and bind the grades as the scenario set
+        (the value table built there too; nothing returns to the host)."""
+        bm = self._need_bm()
+        zz = np.ascontiguousarray(np.atleast_2d(z), dtype=np.float64)
+        if zz.shape[1] != getattr(self, "_vae_latent", -1):
+            raise ShapeMismatch("z must be [S][latent_dim] of the bound decoder")
+        S = zz.shape[0]
+        sig = None
+        if sigma is not None:
+            sig = np.ascontiguousarray(sigma, dtype=np.float64)
+            if sig.shape != (S, bm.n_periods):
+                raise ShapeMismatch("sigma must be [S][T]")
+        rec = np.ascontiguousarray(bm.recovery_by_mode, dtype=np.float64)
+        pc = np.ascontiguousarray(bm.processing_cost_by_mode, dtype=np.float64)
+        check(self.lib.pp_set_scenarios_vae(self._h, S, ptr(zz), int(bm.n_modes), float(bm.price), ptr(rec), rec.size,
+                                            ptr(pc), pc.size, ptr(sig)))
+        self.n_scenarios = int(S)
+        self.has_sigma = sig is not None
+        self._tables = None
+
     def scenario_table(self) -> np.ndarray:
         """vmax[S][B] of the bound scenario set (scenario_mode_values reduced over modes); read back
         from the device when the set was ingested from grades."""
         if getattr(self, "_tables", None) is None:
+            if getattr(self, "n_scenarios", 0):  # a set decoded on the device (set_scenarios_vae)
+                out = np.empty((self.n_scenarios, self._need_bm().n_blocks), np.float64)
+                check(self.lib.pp_get_scenario_values(self._h, ptr(out)))
+                return out
             raise InvalidArgs("set_scenarios first")
         if self._tables.vmax is None:
             out = np.empty((self.n_scenarios, self._need_bm().n_blocks), np.float64)

@@ -357,3 +357,63 @@ def scheduled_neighbor_similarity(assign: np.ndarray, blocks, mean_grade: np.nda
         vals = [abs(mean_grade[b] - mean_grade[j]) for j in rook.get(b, ()) if assign[j] != UNMINED]
         sims[b] = -float(np.mean(vals)) if vals else -np.inf
     return sims
+
+
+@dataclass
+class VaeDecoder:
+    """The decoder half of the reference's VAE (vae.py:61-93; nn.py:20-53): dense layers
+    (W[out][in], b[out]) with relu between them and a linear last layer, then
+    y * norm_std + norm_mean, clamped at zero by the prior decode (vae.py:284-292).  The engine
+    runs it on the device (pp_set_vae_decoder / pp_vae_decode / pp_set_scenarios_vae)."""
+
+    layers: list  # [(W, b)], W[out][in]
+    norm_mean: np.ndarray  # [B]
+    norm_std: np.ndarray  # [B]
+
+    @property
+    def widths(self) -> list:
+        return [int(self.layers[0][0].shape[1])] + [int(W.shape[0]) for W, _ in self.layers]
+
+    @property
+    def latent_dim(self) -> int:
+        return self.widths[0]
+
+    def packed(self) -> np.ndarray:
+        """W then b of every layer, concatenated (the C-ABI layout)."""
+        return np.concatenate([np.concatenate([np.ascontiguousarray(W, dtype=np.float64).ravel(),
+                                               np.ascontiguousarray(b, dtype=np.float64).ravel()])
+                               for W, b in self.layers])
+
+    def decode_host(self, z: np.ndarray) -> np.ndarray:
+        """numpy restatement (row by row, as vae.py:288-291): test infrastructure for the device
+        decode, which agrees with it to rounding."""
+        rows = []
+        for zi in np.atleast_2d(np.asarray(z, dtype=np.float64)):
+            h = zi[None, :]
+            for k, (W, b) in enumerate(self.layers):
+                h = h @ W.T + b
+                if k < len(self.layers) - 1:
+                    h = np.maximum(h, 0.0)
+            rows.append((h * self.norm_std + self.norm_mean)[0])
+        return np.maximum(np.array(rows), 0.0)
+
+    @classmethod
+    def from_reference(cls, model) -> "VaeDecoder":
+        """From a trained `pitplan.vae.VaeModel`."""
+        return cls([(np.asarray(l.W, dtype=np.float64), np.asarray(l.b, dtype=np.float64)) for l in model.decoder.layers],
+                   np.asarray(model.norm_mean, dtype=np.float64), np.asarray(model.norm_std, dtype=np.float64))
+
+    @classmethod
+    def random_init(cls, n_blocks: int, norm_mean: np.ndarray, norm_std: np.ndarray, latent_dim: int = 16,
+                    widths: tuple = (64, 128, 256), seed: int = 0) -> "VaeDecoder":
+        """The reference architecture (VaeConfig defaults, vae.py:32-44) with freshly initialised
+        weights (Mlp.init's he / xavier scales, nn.py:24-27, 37-42): a synthetic scenario source of
+        the right shape when no trained model is at hand."""
+        rng = np.random.default_rng(seed)
+        sizes = [latent_dim, *widths, n_blocks]
+        layers = []
+        for k in range(len(sizes) - 1):
+            n_in, n_out = sizes[k], sizes[k + 1]
+            std = np.sqrt(2.0 / n_in) if k < len(sizes) - 2 else np.sqrt(1.0 / n_in)
+            layers.append((rng.standard_normal((n_out, n_in)) * std, np.zeros(n_out)))
+        return cls(layers, np.asarray(norm_mean, dtype=np.float64), np.asarray(norm_std, dtype=np.float64))

@@ -11,6 +11,7 @@ Every array below is produced by calling the reference's own functions:
   _precedence_repair_pass       hybrid.py:493-510
   lns_repair (max_iters=0)      hybrid.py:199-211 unmine fixpoint
   risk_metrics                  saa.py:150-166 (CVaR10 of per-scenario deltas)
+  vae_generate                  vae.py:306-321 (python make_golden.py vae -> vae.npz)
 """
 
 from __future__ import annotations
@@ -510,7 +511,39 @@ def move_cases(store):
             print(name, k, len(rec.reassign), len(rec.swap), len(rec.other), file=sys.stderr)
 
 
+def vae_cases(store: dict) -> None:
+    """vae_generate (vae.py:306-321) from a VAE trained by the reference on a small instance
+    (train_on_instance, vae.py:295-303, a few epochs): the decoder's layers and normalisation, the
+    prior samples z of each scenario (the substream of vae.py:288-290) and the decoded grades."""
+    from pitplan.vae import VaeConfig, train_on_instance, vae_generate
+
+    for name, n, dims, T, n_s, widths in (("v1", 240, (8, 6, 5), 6, 12, (16, 32, 48)),
+                                           ("v2", 900, (15, 12, 5), 8, 40, (64, 128, 256))):
+        inst = generate_synthetic(n, dims, T, 1, seed=5, n_rock_types=1)
+        cfg = VaeConfig(latent_dim=8 if name == "v1" else 16, encoder_widths=tuple(reversed(widths)),
+                        decoder_widths=widths, epochs=3, batch_size=16, seed=3)
+        model = train_on_instance(inst, cfg, n_fields=64)
+        out = vae_generate(model, n_s, seed=11)
+        p = name + "_"
+        store.update(flat(inst, p))
+        store[p + "widths"] = np.array([cfg.latent_dim, *widths, n], dtype=np.int32)
+        for k, layer in enumerate(model.decoder.layers):
+            store[p + f"W{k}"] = layer.W
+            store[p + f"b{k}"] = layer.b
+        store[p + "norm_mean"] = model.norm_mean
+        store[p + "norm_std"] = model.norm_std
+        store[p + "z"] = np.stack([substream(11, "vae-gen", i).standard_normal((1, cfg.latent_dim))[0]
+                                   for i in range(n_s)])
+        store[p + "grades"] = out.grades
+        print(name, n, n_s, file=sys.stderr)
+
+
 def main():
+    if sys.argv[1:] == ["vae"]:  # the VAE decode fixture only
+        store: dict = {"numpy_version": np.bytes_(np.__version__)}
+        vae_cases(store)
+        np.savez_compressed(os.path.join(OUT, "vae.npz"), **store)
+        return
     if sys.argv[1:] == ["stats"]:  # the k > 1 statistics fixture only
         store: dict = {"numpy_version": np.bytes_(np.__version__)}
         stats_cases(store)
