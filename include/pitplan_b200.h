@@ -182,6 +182,14 @@ PP_API int pp_vae_decode(pp_ctx *ctx, int32_t n_scenarios, const double *z, doub
 PP_API int pp_set_scenarios_vae(pp_ctx *ctx, int32_t n_scenarios, const double *z, int32_t n_modes, double price,
                                 const double *recovery, int32_t n_recovery, const double *proc_cost,
                                 int32_t n_proc_cost, const double *sigma_st);
+/* uncertainty_factors (uncertainty.py:276-321) on the device for grades[S][B]: sigma[S][T] =
+ * clip(f_spatial[s] * phi[t] * psi, 1e-6, 2), f_spatial = 1 - Moran's I + local CV (1 + local CV
+ * for a zero-variance field), Moran's I over the rook pairs of pp_set_rook.  phi[T] =
+ * exp(-kappa t) and psi (psi_geological) come from the host.  moran_out[S] (NaN when degenerate)
+ * and local_out[S] may be NULL.  Agrees with the reference to rounding: its Moran denominator is a
+ * BLAS dot product, here a numpy-order pairwise sum. */
+PP_API int pp_uncertainty_sigma(pp_ctx *ctx, int32_t n_scenarios, const double *grades, const double *phi, double psi,
+                                double *sigma_out, double *moran_out, double *local_out, int32_t mem, void *stream);
 /* The bound value table back in the reference layout vmax[S][B] (host output). */
 PP_API int pp_get_scenario_values(pp_ctx *ctx, double *vmax_sb_out);
 

@@ -118,6 +118,8 @@ SIGNATURES = {
     "pp_eject": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_double, c_void_p, c_int32, c_void_p]),
     "pp_set_rook": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "pp_set_vae_decoder": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pp_uncertainty_sigma": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p,
+                                       c_int32, c_void_p]),
     "pp_vae_decode": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "pp_set_scenarios_vae": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_double, c_void_p, c_int32, c_void_p,
                                        c_int32, c_void_p]),
@@ -136,7 +138,7 @@ SIGNATURES = {
 COMPUTE_ENTRY_POINTS = frozenset({
     "pp_set_schedule", "pp_apply_moves", "pp_eval_candidates", "pp_eval_moves", "pp_check_feasible",
     "pp_repair", "pp_eject", "pp_npv_relaxed", "pp_stage2", "pp_npv_moves", "pp_polish_sweep", "pp_price_greedy", "pp_reduce_best",
-    "pp_enpv_table", "pp_get_spatial", "pp_lns_insert", "pp_vae_decode", "pp_set_scenarios_vae",
+    "pp_enpv_table", "pp_get_spatial", "pp_lns_insert", "pp_vae_decode", "pp_set_scenarios_vae", "pp_uncertainty_sigma",
 })
 CALLS: collections.Counter = collections.Counter()
 

@@ -247,8 +247,16 @@ int pp_set_rook(pp_ctx *c, const int32_t *rook_ptr, const int32_t *rook_idx) {
     TRY(use_device(c));
     TRY(c->lns_rptr.ensure(sizeof(int32_t) * (size_t)(B + 1)));
     TRY(c->lns_ridx.ensure(sizeof(int32_t) * (size_t)std::max(E, 1)));
+    TRY(c->lns_rpi.ensure(sizeof(int32_t) * (size_t)std::max(E, 1)));
     CUDA_TRY(cudaMemcpy(c->lns_rptr.ptr, rook_ptr, sizeof(int32_t) * (size_t)(B + 1), cudaMemcpyHostToDevice));
-    if (E > 0) CUDA_TRY(cudaMemcpy(c->lns_ridx.ptr, rook_idx, sizeof(int32_t) * (size_t)E, cudaMemcpyHostToDevice));
+    if (E > 0) {
+        std::vector<int32_t> pi((size_t)E);  // the pair's first block (rook_weights' i_idx)
+        for (int b = 0; b < B; b++)
+            for (int q = rook_ptr[b]; q < rook_ptr[b + 1]; q++) pi[q] = b;
+        CUDA_TRY(cudaMemcpy(c->lns_ridx.ptr, rook_idx, sizeof(int32_t) * (size_t)E, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(c->lns_rpi.ptr, pi.data(), sizeof(int32_t) * (size_t)E, cudaMemcpyHostToDevice));
+    }
+    c->rook_pairs = E;
     c->have_rook = true;
     return PP_OK;
 }

@@ -88,112 +88,6 @@ struct S2Layout {
     __host__ __device__ static constexpr size_t bytes() { return q_off() + 8 * (size_t)S2_NMAX; }
 };
 
-// numpy pairwise sum of a[0..n) (pairwise.c: blocks of 8, leaves <= 128), whole CTA, result on
-// thread 0: the leaves from the recursion on thread 0 (pre-order, i.e. element order) into
-// ls/ll (capacity >= n/64 + 2), one thread per leaf with numpy's 8 accumulators into leafval[],
-// the fold in post-order on thread 0.  `a`, ls, ll and leafval may live in shared or global memory.
-template <class GF>
-__device__ double s2_pairwise_f(GF a, int n, int *ls, int *ll, double *leafval) {
-    __shared__ int s_nl;
-    if (threadIdx.x == 0) {
-        int stk_o[32], stk_n[32], sp = 0, nl = 0;
-        stk_o[sp] = 0;
-        stk_n[sp] = n;
-        sp++;
-        while (sp > 0) {
-            sp--;
-            const int o = stk_o[sp], ln = stk_n[sp];
-            if (ln <= 128) {
-                ls[nl] = o;
-                ll[nl] = ln;
-                nl++;
-            } else {
-                int n2 = ln / 2;
-                n2 -= n2 % 8;
-                stk_o[sp] = o + n2;  // right pushed first, popped after the left subtree
-                stk_n[sp] = ln - n2;
-                sp++;
-                stk_o[sp] = o;
-                stk_n[sp] = n2;
-                sp++;
-            }
-        }
-        s_nl = nl;
-    }
-    __syncthreads();
-    const int nl = s_nl;
-    // leaf sums, eight lanes per leaf: lane j is numpy's accumulator j over the leaf's blocks of 8
-    // (reads of consecutive elements by consecutive lanes), the xor butterfly over the eight lanes
-    // is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the remainder is added in order by the group's lane 0
-    const int grp = threadIdx.x >> 3, jl = threadIdx.x & 7, ngrp = blockDim.x >> 3;
-    for (int l0 = 0; l0 < nl; l0 += ngrp) {
-        const int l = l0 + grp;
-        const bool act = l < nl;
-        const int o = act ? ls[l] : 0, len = act ? ll[l] : 0;
-        const int main_ = len >= 8 ? len - (len & 7) : 0;
-        double acc = 0.0;
-        if (main_) {  // all (<= 16) loads of the accumulator issued before its sequential adds
-            double x[16];
-#pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = (8 * u < main_) ? a(o + 8 * u + jl) : 0.0;
-            acc = x[0];
-#pragma unroll
-            for (int u = 1; u < 16; u++)
-                if (8 * u < main_) acc = f64_add(acc, x[u]);
-        }
-        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
-        acc = f64_add(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
-        if (act && jl == 0) {
-            double r = main_ ? acc : -0.0;
-            for (int i = main_; i < len; i++) r = f64_add(r, a(o + i));
-            leafval[l] = r;
-        }
-    }
-    __syncthreads();
-    double res = 0.0;
-    if (threadIdx.x == 0) {
-        // fold: re-run the recursion over leaf indices (post-order)
-        int stk_n[32], stk_state[32], sp = 0, leaf = 0;
-        double val[32];
-        stk_n[0] = n;
-        stk_state[0] = 0;
-        sp = 1;
-        int vsp = 0;
-        while (sp > 0) {
-            const int ln = stk_n[sp - 1];
-            if (ln <= 128) {
-                val[vsp++] = leafval[leaf++];
-                sp--;
-                continue;
-            }
-            int n2 = ln / 2;
-            n2 -= n2 % 8;
-            if (stk_state[sp - 1] == 0) {
-                stk_state[sp - 1] = 1;
-                stk_n[sp] = n2;
-                stk_state[sp] = 0;
-                sp++;
-            } else if (stk_state[sp - 1] == 1) {
-                stk_state[sp - 1] = 2;
-                stk_n[sp] = ln - n2;
-                stk_state[sp] = 0;
-                sp++;
-            } else {
-                const double rhs = val[--vsp];
-                const double lhs = val[--vsp];
-                val[vsp++] = f64_add(lhs, rhs);
-                sp--;
-            }
-        }
-        res = f64_add(0.0, n ? val[0] : -0.0);
-    }
-    return res;
-}
-
-__device__ double s2_pairwise(const double *a, int n, int *ls, int *ll, double *leafval) {
-    return s2_pairwise_f([&](int k) { return a[k]; }, n, ls, ll, leafval);
-}
 
 // The blocks of schedule `a` (block ob moved to period ot when ob >= 0) mined in period t, in
 // block order: warp w owns [w*chunk, (w+1)*chunk), 128 blocks per step (int4 per lane when

@@ -541,6 +541,43 @@ class Engine:
             raise ShapeMismatch("rook_ptr must have n_blocks + 1 entries")
         check(self.lib.pp_set_rook(self._h, ptr(rp), ptr(ri) if ri.size else None))
 
+    def ensure_rook(self):
+        """Upload the instance's rook neighbour map (rook_weights order) once."""
+        if getattr(self, "_rook_set", False):
+            return
+        from .evaluate import _rook_csr
+        from .model import rook_neighbor_map, rook_padded
+
+        bm = self._need_bm()
+        pad = rook_padded(rook_neighbor_map(bm), bm.n_blocks)
+        if pad is None:
+            raise ShapeMismatch("a block has 8 or more rook neighbours")
+        self.set_rook(*_rook_csr(pad))
+        self._rook_set = True
+
+    def uncertainty_sigma(self, grades, kappa=0.1, psi_weights=(0.4, 0.35, 0.25), psi_min=0.5):
+        """uncertainty_factors (uncertainty.py:276-321) on the device: (sigma[S][T], moran[S],
+        local[S]); agrees with the reference to rounding (its Moran denominator is a BLAS dot)."""
+        bm = self._need_bm()
+        self.ensure_rook()
+        g = np.ascontiguousarray(np.atleast_2d(grades), dtype=np.float64)
+        if g.shape[1] != bm.n_blocks:
+            raise ShapeMismatch("grades must be [S][n_blocks]")
+        # psi_geological (uncertainty.py:173-182) and phi (uncertainty.py:292) on the host, as the reference
+        diam = bm.diameter()
+        w1, w2, w3 = psi_weights
+        dn = np.clip(bm.dist_intrusion / diam, 0.0, 1.0) if diam > 0 else np.zeros_like(bm.dist_intrusion)
+        raw = float(np.mean(w1 * bm.alteration + w2 * bm.structural + w3 * dn))
+        psi = psi_min + (1.0 - psi_min) * min(max(raw, 0.0), 1.0)
+        phi = np.exp(-kappa * np.arange(bm.n_periods))
+        S = g.shape[0]
+        sig = np.empty((S, bm.n_periods), np.float64)
+        mo = np.empty(S, np.float64)
+        lo = np.empty(S, np.float64)
+        check(self.lib.pp_uncertainty_sigma(self._h, S, ptr(g), ptr(phi), float(psi), ptr(sig), ptr(mo), ptr(lo),
+                                            _lib.PP_MEM_HOST, None))
+        return sig, mo, lo
+
     def lns_insert(self, assign, pool, mean_grade, *, max_iters, candidate_width=16, realism_threshold=0.5,
                    only_positive=False, net=False, use_sigma=True):
         """lns_repair's insertion loop (hybrid.py:238-266) as one device-resident CUDA graph

@@ -98,3 +98,34 @@ def test_vae_decode_large_random_decoder_against_numpy():
     ref = dec.decode_host(z)
     assert _close(g, ref), float(np.max(np.abs(g - ref) / np.maximum(np.abs(ref), 1.0)))
     eng.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_device_uncertainty_sigma_matches_reference(cfg):
+    """uncertainty_factors' sigma[S][T] on the device (pp_uncertainty_sigma) against the
+    reference's (C1: the golden fixture's, computed by pitplan) and the host restatement (C2), to
+    rounding: the reference's Moran denominator is a BLAS dot product."""
+    from paper_2511_18296_b200 import synth
+    from paper_2511_18296_b200.engine import Engine
+    from tests._fixtures import config
+
+    if cfg == "C1":
+        st = load("c1")
+        c = config("C1")
+        bm, grades, ref = c["bm"], st["C1_grades"], c["sigma"]
+    else:
+        c = synth.build_config("C2")
+        bm, grades = c["bm"], c["grades"]
+        ref = synth.uncertainty_sigma(bm, grades)
+    eng = Engine.from_tables(bm, None)
+    sig, moran, local = eng.uncertainty_sigma(grades)
+    assert sig.shape == ref.shape
+    assert _close(sig, ref), float(np.max(np.abs(sig - ref) / np.maximum(np.abs(ref), 1.0)))
+    # a zero-variance field: Moran's I is undefined, f_spatial = 1 + local CV
+    flat = np.full((1, bm.n_blocks), 1.5)
+    s1, m1, l1 = eng.uncertainty_sigma(flat)
+    assert np.isnan(m1[0]) and l1[0] == 0.0
+    phi = np.exp(-0.1 * np.arange(bm.n_periods))
+    assert np.array_equal(s1[0], np.clip((1.0 * phi) * s1[0, 0], 1e-6, 2.0))  # s1[0, 0] = psi (phi[0] = 1)
+    eng.close()
