@@ -2,7 +2,8 @@
 // walks n elements (q = m / rate, dm = d * m), cycles per element for loop variants.  V3 (inputs
 // one batch ahead, the batch's terms read eight at a time into registers) is what pp_npv.cu uses
 // (s2_batch_steps).  A chain per lane (32 chains per warp, q precomputed, 4-deep register ring)
-// measured ~190 cycles per element per chain: its uncoalesced loads are not hidden.
+// measured ~190 cycles per element per chain: its uncoalesced loads are not hidden; software
+// pipelining across batches (the next chain while the previous stop test resolves) ~27.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o tools/bin/walk_bench tools/walk_bench.cu
 #include <cstdio>
 #include <cstdint>
