@@ -320,6 +320,9 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
             __syncthreads();
             EV_PROBE(8);
             WP_PROBE(2);
+#ifdef PP_EVAL_PROBE
+            const long long c_st0 = clock64();
+#endif
             for (int k = threadIdx.x; k < total; k += WV_THREADS) {
                 const int e = s_pair[k], i = e >> 8, t = e & 0xff;
                 const int wq = i / CPW, jq = i - wq * CPW;
@@ -347,6 +350,9 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                                      reinterpret_cast<double *>(wb + L.cv) + jq * T + t, sd);
             }
             WP_PROBE(3);
+#ifdef PP_EVAL_PROBE
+            if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) g_wp_probe[blockIdx.x][threadIdx.x >> 5][10] = clock64() - c_st0;
+#endif
             __syncthreads();
         }
     }

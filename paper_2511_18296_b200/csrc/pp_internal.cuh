@@ -143,10 +143,10 @@ struct TopK {
     }
     // merge with the list of lane (lane ^ m): both lanes end with the KC smallest of the union,
     // ascending (values are only compared and moved, never combined)
-    __device__ __forceinline__ void merge_xor(int m) {
+    __device__ __forceinline__ void merge_xor(int m, unsigned mask = 0xffffffffu) {
         double o[KC];
 #pragma unroll
-        for (int j = 0; j < KC; j++) o[j] = __shfl_xor_sync(0xffffffffu, a[j], m);
+        for (int j = 0; j < KC; j++) o[j] = __shfl_xor_sync(mask, a[j], m);
         double r[KC];
         int ia = 0, ib = 0;
 #pragma unroll
@@ -189,6 +189,12 @@ struct TopK {
 #pragma unroll
             for (int j = 0; j < KC; j++)
                 if (j < k) s = f64_add(s, a[j]);
+        } else if constexpr (KC <= 8) {  // k == 8 == KC: one block of eight; constant indices only,
+                                          // so a[] stays in registers
+            double r[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = a[j < KC ? j : 0];
+            s = tree8(r);
         } else {
             double r[8];
 #pragma unroll
@@ -207,8 +213,8 @@ template <>
 struct TopK<2> {  // k <= 2 (S <= 20): two registers, branch-free (lanes hold different moves)
     double a0, a1;
     __device__ __forceinline__ void init() { a0 = a1 = kInf; }
-    __device__ __forceinline__ void merge_xor(int m) {
-        const double b0 = __shfl_xor_sync(0xffffffffu, a0, m), b1 = __shfl_xor_sync(0xffffffffu, a1, m);
+    __device__ __forceinline__ void merge_xor(int m, unsigned mask = 0xffffffffu) {
+        const double b0 = __shfl_xor_sync(mask, a0, m), b1 = __shfl_xor_sync(mask, a1, m);
         // two smallest of {a0 <= a1} u {b0 <= b1}, ascending
         const bool ta = !(b0 < a0);
         const double lo = ta ? a0 : b0;
@@ -233,7 +239,7 @@ struct TopK<2> {  // k <= 2 (S <= 20): two registers, branch-free (lanes hold di
 template <>
 struct TopK<0> {
     __device__ __forceinline__ void init() {}
-    __device__ __forceinline__ void merge_xor(int) {}
+    __device__ __forceinline__ void merge_xor(int, unsigned = 0xffffffffu) {}
     __device__ __forceinline__ void push(double) {}
     __device__ __forceinline__ double mean(int) const { return 0.0; }
 };

@@ -49,3 +49,8 @@ print("phase durations per warp (median / p90 us):")
 for k in range(1, len(names)):
     d = (w[:, :, k] - w[:, :, k - 1]).ravel() / 1000.0
     print(f"  {names[k - 1]:10s} -> {names[k]:10s} {np.median(d):6.2f} / {np.percentile(d, 90):6.2f}")
+
+cyc = w[:, :, 10].ravel()
+cyc = cyc[(cyc > 0) & (cyc < 10**9)]
+if cyc.size:
+    print("statistics loop, SM cycles per warp: median %d p90 %d max %d" % (np.median(cyc), np.percentile(cyc, 90), cyc.max()))
