@@ -166,12 +166,17 @@ struct TopK {
         for (int j = 0; j < KC; j++) a[j] = r[j];
     }
     __device__ __forceinline__ void push(double x) {
-        if (x < a[KC - 1]) {
-            if constexpr (KC <= 8) {
+        if constexpr (KC <= 8) {
+            // branch-free (x >= a[KC-1], or NaN, leaves every entry as it was): straight-line code lets
+            // the next scenario's value be formed while this push runs
+            bool lt[KC];  // every comparison against the old list first: selects only, no branches
 #pragma unroll
-                for (int j = KC - 1; j > 0; j--) a[j] = (x < a[j - 1]) ? a[j - 1] : ((x < a[j]) ? x : a[j]);
-                a[0] = (x < a[0]) ? x : a[0];
-            } else {  // insertion sort step in local memory
+            for (int j = 0; j < KC; j++) lt[j] = x < a[j];
+#pragma unroll
+            for (int j = KC - 1; j > 0; j--) a[j] = lt[j - 1] ? a[j - 1] : (lt[j] ? x : a[j]);
+            a[0] = lt[0] ? x : a[0];
+        } else if (x < a[KC - 1]) {
+            {  // insertion sort step in local memory
                 int j = KC - 1;
                 while (j > 0 && x < a[j - 1]) {
                     a[j] = a[j - 1];
