@@ -498,15 +498,24 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
                 const double dc_t = net ? f64_mul(d_t, crow[t]) : 0.0;
                 const size_t g = (size_t)blockIdx.x * NW * CPW + ci;
                 unsigned long long k8[8];  // element lane + 32 r as a sort key; padding last
+                // every load of the move's scenario rows first (one round trip, not eight), then the values
+                double xr[8], gt[8], ga[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const int s_ = lane + 32 * r;
+                    const bool in = s_ < S;
+                    xr[r] = in ? __ldg(rowb + s_) : 0.0;
+                    gt[r] = in ? __ldg(p.sigma_ts + t * S + s_) : 0.0;
+                    ga[r] = (in && mined) ? __ldg(p.sigma_ts + abc * S + s_) : 0.0;
+                }
 #pragma unroll
                 for (int r = 0; r < 8; r++) {
                     const int s_ = lane + 32 * r;
                     k8[r] = ~0ull;
                     if (s_ < S) {
-                        const double x = __ldg(rowb + s_);
-                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), __ldg(p.sigma_ts + t * S + s_)), sp), dc_t);
-                        const double vo =
-                            mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), __ldg(p.sigma_ts + abc * S + s_)), sp), dc_ab) : 0.0;
+                        const double x = xr[r];
+                        const double vn = f64_sub(f64_mul(f64_mul(f64_mul(x, d_t), gt[r]), sp), dc_t);
+                        const double vo = mined ? f64_sub(f64_mul(f64_mul(f64_mul(x, d_ab), ga[r]), sp), dc_ab) : 0.0;
                         const double v = f64_sub(vn, vo);
                         if constexpr (SCEN) p.scen_delta[(g * S + s_) * T + t] = (float)v;
                         vb[s_] = v;
