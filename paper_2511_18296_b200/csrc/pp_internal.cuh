@@ -556,6 +556,7 @@ constexpr int EV_THREADS = 256;
 struct MoveParams {
     const BlockRow *rows;
     const int32_t *adj;
+    const int32_t *nbr;  // padded neighbour rows [B][32] (successors tagged 1 << 30), or null
     const int32_t *assign;
     const double *pm;
     const double *cap;

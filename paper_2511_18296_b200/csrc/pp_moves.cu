@@ -44,6 +44,50 @@ __device__ __forceinline__ void move_window(const MoveParams &p, const BlockRow 
     hi = h;
 }
 
+// The precedence windows of the warp's 32 moves, the warp together (the padded neighbour rows: lane k
+// = neighbour k, coalesced), eight moves per round with every row load and then every period load
+// issued before use -- two memory round trips per eight moves instead of a dependent chain of
+// loads per neighbour in each lane.  Move m of the warp asks for block bw (lane m's value; -1:
+// none), with block sub (if it is a neighbour) seen at period subt; lane m gets lo = the latest
+// predecessor period (-2: an unmined predecessor) and hi = the earliest mined successor period
+// (INT_MAX: none) -- the quantities of move_window / hybrid.py:348-355.
+constexpr int MV_NBR_W = 32, MV_NBR_SUCC = 1 << 30;
+__device__ __forceinline__ void warp_windows(const MoveParams &p, int bw, int sub, int subt, int &lo_out, int &hi_out) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    lo_out = 0;
+    hi_out = INT_MAX;
+#pragma unroll 1
+    for (int m0 = 0; m0 < 32; m0 += 8) {
+        int nb[8], bb[8], sb[8], st[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            bb[u] = __shfl_sync(FULL, bw, m0 + u);
+            sb[u] = __shfl_sync(FULL, sub, m0 + u);
+            st[u] = __shfl_sync(FULL, subt, m0 + u);
+            nb[u] = bb[u] >= 0 ? __ldg(p.nbr + (size_t)bb[u] * MV_NBR_W + lane) : -1;
+        }
+        int tn[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int b = nb[u] >= 0 ? (nb[u] & (MV_NBR_SUCC - 1)) : 0;
+            tn[u] = nb[u] >= 0 ? (b == sb[u] ? st[u] : p.assign[b]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const bool pred = nb[u] >= 0 && !(nb[u] & MV_NBR_SUCC), succ = nb[u] >= 0 && (nb[u] & MV_NBR_SUCC);
+            const unsigned lc = pred ? (tn[u] < 0 ? 0x7fffffffu : (unsigned)tn[u]) : 0u;
+            const unsigned hc = (succ && tn[u] >= 0) ? (unsigned)tn[u] : 0x7fffffffu;
+            const int lo = (int)__reduce_max_sync(FULL, lc);
+            const int hi = (int)__reduce_min_sync(FULL, hc);
+            if (lane == m0 + u) {
+                lo_out = lo == 0x7fffffff ? -2 : lo;
+                hi_out = hi;
+            }
+        }
+    }
+}
+
 template <int KC>
 __global__ void __launch_bounds__(EV_THREADS) k_eval_moves(const MoveParams p) {
     __shared__ Best s_red[EV_THREADS / 32];
@@ -207,6 +251,26 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
         bool ok = false;
         double dl = -kInf;
         int b1 = 0, b2 = -1, t1 = -1, t2 = -1;
+        // the warp's windows together (warp-uniform: every lane reaches these shuffles)
+        int wlo = 0, whi = INT_MAX, wlo2 = 0, whi2 = INT_MAX;
+        if (p.nbr) {
+            int bw = -1, sub = -1, subt = 0, bw2 = -1, sub2 = -1, subt2 = 0;
+            if (i < p.M) {
+                const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
+                if (p.kind == PP_MOVE_REASSIGN) {
+                    if (x >= 0 && x < p.B && y >= -1 && y < p.T) bw = x;
+                } else if (x >= 0 && x < p.B && y >= 0 && y < p.B && x != y) {
+                    bw = x;  // b1's window with b2 at b1's period, and the other way round
+                    sub = y;
+                    subt = p.assign[x];
+                    bw2 = y;
+                    sub2 = x;
+                    subt2 = p.assign[y];
+                }
+            }
+            warp_windows(p, bw, sub, subt, wlo, whi);
+            if (p.kind == PP_MOVE_SWAP) warp_windows(p, bw2, sub2, subt2, wlo2, whi2);
+        }
         if (i < p.M) {
             const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
             if (p.kind == PP_MOVE_REASSIGN) {
@@ -218,6 +282,9 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
                     const int npred = r1.cnt & 0xffff, nnb = npred + (r1.cnt >> 16);
                     if (t2 == t1) {
                         ok = false;
+                    } else if (p.nbr) {  // from the warp's windows
+                        ok = t2 < 0 ? whi == INT_MAX : (wlo != -2 && wlo <= t2 && t2 <= whi);
+                        if (ok && t2 >= 0 && f64_add(__ldcg(p.pm + t2), r1.mass) > s_tab[1][t2]) ok = false;
                     } else if (t2 < 0) {  // unmine: allowed iff no mined successor
                         ok = true;
                         for (int k = npred; k < nnb; k++)
@@ -251,8 +318,15 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
                     const double l2 = f64_add(f64_sub(__ldcg(p.pm + t2), r2.mass), r1.mass);
                     if (!(l1 > s_tab[1][t1]) && !(l2 > s_tab[1][t2])) {
                         int lo1, hi1, lo2, hi2;  // windows after the swap (hybrid.py:400-403)
-                        move_window(p, r1, b2, t1, lo1, hi1);
-                        move_window(p, r2, b1, t2, lo2, hi2);
+                        if (p.nbr) {
+                            lo1 = wlo;
+                            hi1 = whi == INT_MAX ? p.T - 1 : whi;
+                            lo2 = wlo2;
+                            hi2 = whi2 == INT_MAX ? p.T - 1 : whi2;
+                        } else {
+                            move_window(p, r1, b2, t1, lo1, hi1);
+                            move_window(p, r2, b1, t2, lo2, hi2);
+                        }
                         ok = lo1 != -2 && lo1 <= t2 && t2 <= hi1 && lo2 != -2 && lo2 <= t1 && t1 <= hi2;
                     }
                 }
@@ -369,6 +443,7 @@ int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, i
     memset(&mp, 0, sizeof(mp));
     mp.rows = c->rows.as<BlockRow>();
     mp.adj = c->adj.as<int32_t>();
+    mp.nbr = c->nbr.as<int32_t>();  // (null when a block has more than 32 neighbours)
     mp.assign = c->assign_ptr;
     mp.pm = c->pm.as<double>();
     mp.cap = c->cap.as<double>();
