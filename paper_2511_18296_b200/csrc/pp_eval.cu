@@ -609,6 +609,9 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     //      record (one 128-bit compare-and-swap per CTA, the record initialised ahead of the
     //      launch); warp 1 reserves the CTA's sparse pairs with one atomic (not one per warp: the
     //      counter is a single contended address) and lane t writes candidate i's period-t entry ----
+    // the copy-out launch (PDL) may be staged once every CTA of the grid has reached this point, so
+    // its CTAs never take a slot an evaluation CTA still needs
+    asm volatile("griddepcontrol.launch_dependents;");
     if (lane == 0) s_red[warp] = wbest;
     const bool want_pairs = STATS_T && stats && p.n_pairs;
     if (want_pairs) {
@@ -717,6 +720,7 @@ struct CopyOut {
 };
 
 __global__ void __launch_bounds__(256) k_copy_out(const CopyOut co) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched under PDL behind the evaluation
     const CopySeg &sg = co.seg[blockIdx.y];
     const unsigned long long bytes =
         sg.per_pair > 0 ? (unsigned long long)max(0, __ldcg(co.n_pairs)) * sg.per_pair : sg.bytes;
@@ -965,8 +969,9 @@ copy_out:
             }
             ht.mark("map check");
             if (ok) {
-                k_copy_out<<<dim3(64, co.nseg), 256, 0, st>>>(co);
-                CUDA_TRY(cudaGetLastError());
+                // PDL: the launch is staged while the evaluation's CTAs finish (they trigger at
+                // their epilogue); griddepcontrol.wait above still orders every read after them
+                TRY(launch_eval_n(k_copy_out, dim3(64, co.nseg), 256, 0, st, true, co));
                 ht.mark("d2h enqueue");
                 CUDA_TRY(stream_wait(st));
                 ht.mark("sync");

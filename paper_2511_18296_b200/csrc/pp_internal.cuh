@@ -957,10 +957,10 @@ inline int launch_eval(void (*kern)(KArgs...), int grid, size_t smem, cudaStream
     return PP_OK;
 }
 template <typename... KArgs, typename... Args>
-inline int launch_eval_n(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t st, bool pdl,
+inline int launch_eval_n(void (*kern)(KArgs...), dim3 grid, int threads, size_t smem, cudaStream_t st, bool pdl,
                          Args... args) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
