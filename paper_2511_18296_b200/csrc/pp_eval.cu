@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     const bool need_vrow = (stats && KC > 0) || (!literal && p.scen >= 0);
     const bool want_unit = !literal && p.scen < 0;
     const bool want_trace = p.trace_val || p.trace_feas;
-    const WarpLayout L = warp_layout(T, Sp, stats, need_vrow, net, (KC < 0 && stats) ? big_pow2(S) : 0);
+    // the layout the host sized the launch with (warp_layout, passed in: not recomputed per thread)
+    const WarpLayout L{p.wl[0], p.wl[1], p.wl[2], p.wl[3], p.wl[4], p.wl[5], p.wl[6]};
     const int sigb = sig_bytes(S, T, stats && KC > 0);  // big-S statistics read sigma through L1
     double *s_sig = reinterpret_cast<double *>(wv_dyn);
     unsigned char *wslices = wv_dyn + sigb;
@@ -228,17 +229,43 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     // store of a loaded value would hold the warp until that load returns): neighbour ids, mining
     // costs, vmax rows, the per-candidate scalars; then the neighbours' periods
     int nb[CPW];
+    // the rows per candidate (one round each) or as one flat list over the lanes (two rounds at C2
+    // instead of four); measured per instantiation: flat is faster at C2 (KC 2: step 19.45 ->
+    // 19.2 us) and C3 (KC < 0), slower at C4 (KC 8, S = 50: kernel 59.4 -> 63.5 us, more spills)
+    constexpr bool FLAT_ROWS = KC != 8;
 #pragma unroll
-    for (int j = 0; j < CPW; j++) {
-        nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
-        if (net && lane < T && b[j] >= 0) cp_async8(w_cost + j * T + lane, p.cost + (size_t)b[j] * T + lane);
-    }
-    if (need_vrow) {
+    for (int j = 0; j < CPW; j++) nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
+    if constexpr (!FLAT_ROWS) {
 #pragma unroll
         for (int j = 0; j < CPW; j++)
-            if (b[j] >= 0)
-                for (int q = lane; q < (Sp >> 1); q += 32)
-                    cp_async16(w_vrow + (size_t)j * Sp + 2 * q, p.vmax + (size_t)b[j] * Sp + 2 * q);
+            if (net && lane < T && b[j] >= 0) cp_async8(w_cost + j * T + lane, p.cost + (size_t)b[j] * T + lane);
+        if (need_vrow) {
+#pragma unroll
+            for (int j = 0; j < CPW; j++)
+                if (b[j] >= 0)
+                    for (int q = lane; q < (Sp >> 1); q += 32)
+                        cp_async16(w_vrow + (size_t)j * Sp + 2 * q, p.vmax + (size_t)b[j] * Sp + 2 * q);
+        }
+    } else {
+        static_assert(CPW == 4, "three thresholds below");
+        if (net) {  // element e of the flat list: candidate j = e / T, period e - j T
+            const int n = CPW * T;
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                const int j = (e >= T) + (e >= 2 * T) + (e >= 3 * T);
+                const int bj = __shfl_sync(FULL, bl, j);
+                if (e < n && bj >= 0) cp_async8(w_cost + e, p.cost + (size_t)bj * T + (e - j * T));
+            }
+        }
+        if (need_vrow) {  // 16-byte chunk e: candidate j = e / h, chunk e - j h
+            const int h = Sp >> 1, n = CPW * h;
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                const int j = (e >= h) + (e >= 2 * h) + (e >= 3 * h);
+                const int bj = __shfl_sync(FULL, bl, j);
+                if (e < n && bj >= 0) cp_async16(w_vrow + 2 * e, p.vmax + (size_t)bj * Sp + 2 * (e - j * h));
+            }
+        }
     }
     double mass_l = 0.0, spat_l = 0.0, unit_l = 0.0;
     int ab_l = -1;
@@ -428,27 +455,37 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     }
 #pragma unroll
     for (int j = 0; j < CPW; j++) mlo[j] = __reduce_max_sync(FULL, (hi[j] == mhi[j] && hi[j]) ? lo[j] : 0u);
+    int my_bt = INT_MAX;  // lane j < CPW: candidate j's selected period and value
+    double my_bv = -kInf;
 #pragma unroll
     for (int j = 0; j < CPW; j++) {
         const unsigned win_t = __ballot_sync(FULL, hi[j] && hi[j] == mhi[j] && lo[j] == mlo[j]);
         const int bt = win_t ? __ffs(win_t) - 1 : INT_MAX;
         const double bv = __shfl_sync(FULL, vj[j], win_t ? bt : 0);
+        if (lane == j) {
+            my_bt = bt;
+            my_bv = bv;
+        }
         const int g = cw + j;
-        if (g < p.C) {
-            if (lane == 0 && b[j] >= 0) {
-                p.best_t[g] = bt != INT_MAX ? bt : -1;
-                p.best_val[g] = bt != INT_MAX ? bv : -kInf;
-                p.feas[g] = bt != INT_MAX ? 1 : 0;
-            }
-            if (want_trace && lane < T) {
-                if (p.trace_val) p.trace_val[(size_t)g * T + lane] = okl[j] ? vj[j] : -kInf;
-                if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = okl[j] ? 1 : 0;
-            }
+        if (want_trace && g < p.C && lane < T) {
+            if (p.trace_val) p.trace_val[(size_t)g * T + lane] = okl[j] ? vj[j] : -kInf;
+            if (p.trace_feas) p.trace_feas[(size_t)g * T + lane] = okl[j] ? 1 : 0;
         }
-        if (b[j] >= 0 && bt != INT_MAX) {
-            const Best cb{bv, b[j], bt};
-            if (better(cb, wbest)) wbest = cb;
-        }
+    }
+    // per-candidate outputs by lane j (one store each, not four rounds of lane 0), and the
+    // warp's best move over lanes 0..CPW-1 (bl = lane j's candidate id, -1 past the end)
+    if (lane < CPW && bl >= 0) {
+        const int g = cw + lane;
+        const bool f = my_bt != INT_MAX;
+        p.best_t[g] = f ? my_bt : -1;
+        p.best_val[g] = f ? my_bv : -kInf;
+        p.feas[g] = f ? 1 : 0;
+        if (f) wbest = Best{my_bv, bl, my_bt};
+    }
+#pragma unroll
+    for (int off = 1; off < CPW; off <<= 1) {
+        const Best o = shfl_best(wbest, off);
+        if (better(o, wbest)) wbest = o;
     }
     // ---- KC < 0: statistics of the feasible moves, one warp per move (after the capacity
     //      test: with many scenarios the statistics dominate, so only feasible moves pay).  The
@@ -867,6 +904,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
                                           kcw < 0 ? big_pow2(S) : 0);
         const size_t smem_w = (size_t)Lw.total * (WV_THREADS / 32) + sig_bytes(S, T, stats && kcw > 0);
+        const int wl[7] = {Lw.vrow, Lw.cost, Lw.val, Lw.ex, Lw.cv, Lw.big, Lw.total};
+        memcpy(ep.wl, wl, sizeof(wl));
         const int per_cta = CPW * (WV_THREADS / 32);
         const int wgrid = std::max(1, (C + per_cta - 1) / per_cta);
         TRY(ensure_grid_scratch(c, wgrid));

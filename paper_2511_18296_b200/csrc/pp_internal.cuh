@@ -528,6 +528,7 @@ struct EvalParams {
     const double *sig_row;   // [T] (ones / scenario mean / sigma[k])
     const double *sigma;     // [S][T] (ones if no sigma)
     const double *sigma_ts;  // [T][S]: sigma transposed (scenario-contiguous rows for lane = scenario)
+    int wl[7];               // k_eval_warp: the per-warp shared-memory layout (host-computed)
     const int32_t *cand;
     int C, B, T, S, Sp, scen, cvar_k;
     unsigned flags;
