@@ -218,8 +218,11 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     int b[CPW];
 #pragma unroll
     for (int j = 0; j < CPW; j++) b[j] = __shfl_sync(FULL, bl, j);
-    if (stats && KC > 0)  // sigma [S][T] for the pooled pair statistics, staged once per CTA
-        for (int e = threadIdx.x; e < S * T; e += WV_THREADS) cp_async8(s_sig + e, p.sigma + e);
+    if (stats && KC > 0) {  // sigma [S][T] for the pooled pair statistics, staged once per CTA
+        const int n = S * T;    // 16-byte copies (the table and the slot are 16-byte aligned)
+        for (int e = threadIdx.x; e < (n >> 1); e += WV_THREADS) cp_async16(s_sig + 2 * e, p.sigma + 2 * e);
+        if ((n & 1) && threadIdx.x == 0) cp_async8(s_sig + n - 1, p.sigma + n - 1);
+    }
     if (threadIdx.x < T) {
         cp_async8(&s_tab[0][threadIdx.x], p.cap + threadIdx.x);
         cp_async8(&s_tab[1][threadIdx.x], p.disc + threadIdx.x);
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
 
     // ---- per-(candidate, period) statistics outputs (capacity-feasible pairs only) ----
     if constexpr (STATS_T) {
-        if (stats) {
+        if (stats && (SCEN || p.exp_delta || p.cvar)) {  // (sparse pairs only: nothing dense to write)
 #pragma unroll
             for (int j = 0; j < CPW; j++) {
                 const int g = cw + j;
