@@ -558,6 +558,7 @@ struct MoveParams {
     const BlockRow *rows;
     const int32_t *adj;
     const int32_t *nbr;  // padded neighbour rows [B][32] (successors tagged 1 << 30), or null
+    const int2 *bwin;    // reassign moves: every block's precedence window {lo, hi} (k_block_windows), or null
     const int32_t *assign;
     const double *pm;
     const double *cap;
@@ -804,6 +805,7 @@ struct pp_ctx {
     // host-mode schedules on the cluster path are range-checked on the device by k_pm_cluster
     // (one flag per CTA) and reported by the next host-mode call that synchronises
     DevBuf pm_bad;
+    DevBuf mv_win;  // pp_eval_moves: per-block precedence windows of the current schedule
     int32_t *h_bad = nullptr;  // page-locked mirror [8]
     unsigned char *h_bounce = nullptr;  // page-locked bounce buffer for small host-mode results
     unsigned char *h_stage = nullptr;   // page-locked staging for packed host-mode uploads/results
@@ -846,7 +848,7 @@ struct pp_ctx {
                 &h_b, &h_o1, &h_o2, &h_o3, &h_o4, &h_o5, &h_o6, &h_o7, &h_o8, &h_glob, &h_assign, &h_i64, &h_d1,
                 &h_d2, &h_pm, &h_p, &best_none, &bad_cand, &ej_count, &ej_key, &ej_blk, &hours, &npv_raw,
                 &npv_cost, &npv_n, &s2_items, &s2_scratch, &s2_rec, &s2_assign, &pr_score, &pr_cap, &pr_assign, &pr_elig,
-                &pm_bad, &npvm_flags, &vae_params, &vae_norm, &vae_h, &vae_io, &lns_rptr, &lns_ridx, &lns_rpi, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
+                &pm_bad, &mv_win, &npvm_flags, &vae_params, &vae_norm, &vae_h, &vae_io, &lns_rptr, &lns_ridx, &lns_rpi, &lns_mg, &lns_pool, &lns_pos, &lns_keys, &lns_ctl, &lns_out};
     }
 };
 

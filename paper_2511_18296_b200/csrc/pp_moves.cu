@@ -88,6 +88,22 @@ __device__ __forceinline__ void warp_windows(const MoveParams &p, int bw, int su
     }
 }
 
+// Every block's precedence window under the current schedule, a warp per 32 blocks (warp_windows):
+// reassign batches hold several moves per block (250k moves over 50k blocks at C2), so one window
+// per block replaces one per move.  Launched behind the period masses under PDL; it completes only
+// after them, so the moves kernel's griddepcontrol.wait covers both.
+__global__ void __launch_bounds__(256) k_block_windows(const MoveParams p, int2 *__restrict__ win) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int lane = threadIdx.x & 31;
+    for (int base = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32; base < p.B; base += gridDim.x * 256) {
+        const int b = base + lane;
+        int lo, hi;
+        warp_windows(p, b < p.B ? b : -1, -1, 0, lo, hi);
+        if (b < p.B) win[b] = make_int2(lo, hi);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <int KC>
 __global__ void __launch_bounds__(EV_THREADS) k_eval_moves(const MoveParams p) {
     __shared__ Best s_red[EV_THREADS / 32];
@@ -253,7 +269,16 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
         int b1 = 0, b2 = -1, t1 = -1, t2 = -1;
         // the warp's windows together (warp-uniform: every lane reaches these shuffles)
         int wlo = 0, whi = INT_MAX, wlo2 = 0, whi2 = INT_MAX;
-        if (p.nbr) {
+        if (p.bwin) {  // reassign: the block's window, computed once per block
+            if (i < p.M) {
+                const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
+                if (x >= 0 && x < p.B && y >= -1 && y < p.T) {
+                    const int2 w = __ldcg(p.bwin + x);
+                    wlo = w.x;
+                    whi = w.y;
+                }
+            }
+        } else if (p.nbr) {
             int bw = -1, sub = -1, subt = 0, bw2 = -1, sub2 = -1, subt2 = 0;
             if (i < p.M) {
                 const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
                     const int npred = r1.cnt & 0xffff, nnb = npred + (r1.cnt >> 16);
                     if (t2 == t1) {
                         ok = false;
-                    } else if (p.nbr) {  // from the warp's windows
+                    } else if (p.nbr || p.bwin) {  // from the warp's windows / the block windows
                         ok = t2 < 0 ? whi == INT_MAX : (wlo != -2 && wlo <= t2 && t2 <= whi);
                         if (ok && t2 >= 0 && f64_add(__ldcg(p.pm + t2), r1.mass) > s_tab[1][t2]) ok = false;
                     } else if (t2 < 0) {  // unmine: allowed iff no mined successor
@@ -489,6 +514,15 @@ int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, i
         TRY(ensure_grid_scratch(c, wgrid));  // may re-allocate: take the pointers after it
         mp.partial = c->partial.as<pp_best>();
         mp.counter = c->counter.as<unsigned int>();
+        // reassign batches with several moves per block: the windows once per block first
+        static const bool no_bwin = std::getenv("PP_NO_BLOCK_WINDOWS") != nullptr;  // diagnostics
+        if (kind == PP_MOVE_REASSIGN && mp.nbr && !no_bwin && (long long)M >= 2ll * c->B) {
+            TRY(c->mv_win.ensure(sizeof(int2) * (size_t)c->B));
+            const int bgrid = std::max(1, std::min((c->B + 255) / 256, 8 * sms));
+            TRY(launch_eval_n(k_block_windows, bgrid, 256, 0, st, pdl, mp, c->mv_win.as<int2>()));
+            mp.bwin = c->mv_win.as<int2>();
+            pdl = true;  // the moves kernel behind the windows (which complete after the masses)
+        }
         if (stats) {
             TRY(set_smem_attr(k_moves_warp<true>, smem, c->device));
             TRY(launch_eval_n(k_moves_warp<true>, wgrid, MW_THREADS, smem, st, pdl, mp));

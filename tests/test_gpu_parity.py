@@ -209,6 +209,10 @@ def test_explicit_moves_against_oracle(oracle_lib):
             got = eng.eval_moves(b, t, "reassign", s, net=net, stats=True, scen=True)
             ref = o.eval_moves(assign, b, t, "reassign", s, net=net, stats=True, scen=True)
             _same_res(got, ref, keys)
+    # M = 5000 >= 2 B takes the per-block windows (k_block_windows); M = 500 the per-move ones
+    got = eng.eval_moves(b[:500].copy(), t[:500].copy(), "reassign", None, net=True, stats=True, scen=True)
+    ref = o.eval_moves(assign, b[:500].copy(), t[:500].copy(), "reassign", None, net=True, stats=True, scen=True)
+    _same_res(got, ref, keys)
     b2 = rng.integers(0, bm.n_blocks, M).astype(np.int32)
     got = eng.eval_moves(b, b2, "swap", None, net=True, stats=True, scen=True)
     ref = o.eval_moves(assign, b, b2, "swap", None, net=True, stats=True, scen=True)
