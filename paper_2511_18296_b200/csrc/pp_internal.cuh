@@ -558,7 +558,7 @@ struct MoveParams {
     const BlockRow *rows;
     const int32_t *adj;
     const int32_t *nbr;  // padded neighbour rows [B][32] (successors tagged 1 << 30), or null
-    const int2 *bwin;    // reassign moves: every block's precedence window {lo, hi} (k_block_windows), or null
+    const int2 *bwin;    // every block's precedence window, 3 x int2 per block (k_block_windows), or null
     const int32_t *assign;
     const double *pm;
     const double *cap;

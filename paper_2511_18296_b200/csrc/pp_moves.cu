@@ -88,20 +88,100 @@ __device__ __forceinline__ void warp_windows(const MoveParams &p, int bw, int su
     }
 }
 
-// Every block's precedence window under the current schedule, a warp per 32 blocks (warp_windows):
-// reassign batches hold several moves per block (250k moves over 50k blocks at C2), so one window
-// per block replaces one per move.  Launched behind the period masses under PDL; it completes only
-// after them, so the moves kernel's griddepcontrol.wait covers both.
+// Every block's precedence window under the current schedule, a warp per 32 blocks: batches hold
+// several moves per block (250k moves over 50k blocks at C2), so one window per block replaces one
+// (or, for swaps, two) per move.  Per block, three int2: {lo, hi} raw (lo = the latest predecessor
+// period, 0x7fffffff when a predecessor is unmined; hi = the earliest mined successor period,
+// 0x7fffffff when none), {lob, hib} = a neighbour block attaining each, {lo2, hi2} = the same
+// extremes without that one neighbour -- so a swap can re-form the window with its partner seen at
+// another period.  Launched behind the period masses under PDL; it completes only after them, so
+// the moves kernel's griddepcontrol.wait covers both.
+constexpr int BW_NONE = 0x7fffffff;
 __global__ void __launch_bounds__(256) k_block_windows(const MoveParams p, int2 *__restrict__ win) {
     asm volatile("griddepcontrol.launch_dependents;");
+    constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     for (int base = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32; base < p.B; base += gridDim.x * 256) {
+        int2 w0 = make_int2(0, BW_NONE), w1 = make_int2(-1, -1), w2 = make_int2(0, BW_NONE);
+#pragma unroll 1
+        for (int m0 = 0; m0 < 32; m0 += 8) {
+            int nb[8], tn[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int b = base + m0 + u;
+                nb[u] = b < p.B ? __ldg(p.nbr + (size_t)b * MV_NBR_W + lane) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) tn[u] = nb[u] >= 0 ? p.assign[nb[u] & (MV_NBR_SUCC - 1)] : 0;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const bool pred = nb[u] >= 0 && !(nb[u] & MV_NBR_SUCC), succ = nb[u] >= 0 && (nb[u] & MV_NBR_SUCC);
+                const int blk = nb[u] & (MV_NBR_SUCC - 1);
+                const unsigned lc = pred ? (tn[u] < 0 ? (unsigned)BW_NONE : (unsigned)tn[u]) : 0u;
+                const unsigned hc = (succ && tn[u] >= 0) ? (unsigned)tn[u] : (unsigned)BW_NONE;
+                const unsigned lo = __reduce_max_sync(FULL, lc), hi = __reduce_min_sync(FULL, hc);
+                const unsigned ml = __ballot_sync(FULL, pred && lc == lo);
+                const unsigned mh = __ballot_sync(FULL, succ && tn[u] >= 0 && hc == hi);
+                const int ll = ml ? __ffs(ml) - 1 : -1, lh = mh ? __ffs(mh) - 1 : -1;
+                const int lob = __shfl_sync(FULL, blk, ll < 0 ? 0 : ll), hib = __shfl_sync(FULL, blk, lh < 0 ? 0 : lh);
+                const unsigned lo2 = __reduce_max_sync(FULL, lane == ll ? 0u : lc);
+                const unsigned hi2 = __reduce_min_sync(FULL, lane == lh ? (unsigned)BW_NONE : hc);
+                if (lane == m0 + u) {
+                    w0 = make_int2((int)lo, (int)hi);
+                    w1 = make_int2(ll < 0 ? -1 : lob, lh < 0 ? -1 : hib);
+                    w2 = make_int2((int)lo2, (int)hi2);
+                }
+            }
+        }
         const int b = base + lane;
-        int lo, hi;
-        warp_windows(p, b < p.B ? b : -1, -1, 0, lo, hi);
-        if (b < p.B) win[b] = make_int2(lo, hi);
+        if (b < p.B) {
+            win[3 * (size_t)b] = w0;
+            win[3 * (size_t)b + 1] = w1;
+            win[3 * (size_t)b + 2] = w2;
+        }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Swaps: where block sub sits in bw's neighbour row (lane m asks for its own pair): 1 = a
+// predecessor of bw, 2 = a successor, 0 = neither; eight rows per round, one memory round trip
+__device__ __forceinline__ int warp_relation(const MoveParams &p, int bw, int sub) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    int rel = 0;
+#pragma unroll 1
+    for (int m0 = 0; m0 < 32; m0 += 8) {
+        int nb[8], sb[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int bb = __shfl_sync(FULL, bw, m0 + u);
+            sb[u] = __shfl_sync(FULL, sub, m0 + u);
+            nb[u] = bb >= 0 ? __ldg(p.nbr + (size_t)bb * MV_NBR_W + lane) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const bool hit = nb[u] >= 0 && (nb[u] & (MV_NBR_SUCC - 1)) == sb[u];
+            const unsigned m = __ballot_sync(FULL, hit), ms = __ballot_sync(FULL, hit && (nb[u] & MV_NBR_SUCC));
+            if (lane == m0 + u) rel = ms ? 2 : (m ? 1 : 0);
+        }
+    }
+    return rel;
+}
+// block b's window (k_block_windows) with neighbour o (relation rel: 1 pred, 2 succ) seen at period
+// to, in warp_windows' convention (lo -2 when a predecessor is unmined, hi INT_MAX when none)
+__device__ __forceinline__ void window_with(const int2 *win, int b, int o, int rel, int to, int &lo, int &hi) {
+    const int2 w0 = __ldcg(win + 3 * (size_t)b), w1 = __ldcg(win + 3 * (size_t)b + 1),
+               w2 = __ldcg(win + 3 * (size_t)b + 2);
+    int l = w0.x, h = w0.y;
+    if (rel == 1) {
+        const int lw = o == w1.x ? w2.x : w0.x;
+        l = lw == BW_NONE ? BW_NONE : max(lw, to);
+    } else if (rel == 2) {
+        const int hw = o == w1.y ? w2.y : w0.y;
+        h = min(hw, to);
+    }
+    lo = l == BW_NONE ? -2 : l;
+    hi = h;  // BW_NONE == INT_MAX
 }
 
 template <int KC>
@@ -269,13 +349,22 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
         int b1 = 0, b2 = -1, t1 = -1, t2 = -1;
         // the warp's windows together (warp-uniform: every lane reaches these shuffles)
         int wlo = 0, whi = INT_MAX, wlo2 = 0, whi2 = INT_MAX;
-        if (p.bwin) {  // reassign: the block's window, computed once per block
+        if (p.bwin) {  // the blocks' windows, computed once per block
+            int bw = -1, sub = -1;
             if (i < p.M) {
                 const int x = __ldg(p.ma + i), y = __ldg(p.mb + i);
-                if (x >= 0 && x < p.B && y >= -1 && y < p.T) {
-                    const int2 w = __ldcg(p.bwin + x);
-                    wlo = w.x;
-                    whi = w.y;
+                if (p.kind == PP_MOVE_REASSIGN) {
+                    if (x >= 0 && x < p.B && y >= -1 && y < p.T) window_with(p.bwin, x, -1, 0, 0, wlo, whi);
+                } else if (x >= 0 && x < p.B && y >= 0 && y < p.B && x != y) {
+                    bw = x;
+                    sub = y;
+                }
+            }
+            if (p.kind == PP_MOVE_SWAP) {  // b1's window with b2 at b1's period, and the other way round
+                const int rel = warp_relation(p, bw, sub);
+                if (bw >= 0) {
+                    window_with(p.bwin, bw, sub, rel, p.assign[bw], wlo, whi);
+                    window_with(p.bwin, sub, bw, rel == 1 ? 2 : rel == 2 ? 1 : 0, p.assign[sub], wlo2, whi2);
                 }
             }
         } else if (p.nbr) {
@@ -343,7 +432,7 @@ __global__ void __launch_bounds__(MW_THREADS) k_moves_warp(const MoveParams p) {
                     const double l2 = f64_add(f64_sub(__ldcg(p.pm + t2), r2.mass), r1.mass);
                     if (!(l1 > s_tab[1][t1]) && !(l2 > s_tab[1][t2])) {
                         int lo1, hi1, lo2, hi2;  // windows after the swap (hybrid.py:400-403)
-                        if (p.nbr) {
+                        if (p.nbr || p.bwin) {
                             lo1 = wlo;
                             hi1 = whi == INT_MAX ? p.T - 1 : whi;
                             lo2 = wlo2;
@@ -514,10 +603,10 @@ int pp_eval_moves(pp_ctx *c, int32_t kind, const int32_t *a, const int32_t *b, i
         TRY(ensure_grid_scratch(c, wgrid));  // may re-allocate: take the pointers after it
         mp.partial = c->partial.as<pp_best>();
         mp.counter = c->counter.as<unsigned int>();
-        // reassign batches with several moves per block: the windows once per block first
+        // batches with several moves per block: the windows once per block first
         static const bool no_bwin = std::getenv("PP_NO_BLOCK_WINDOWS") != nullptr;  // diagnostics
-        if (kind == PP_MOVE_REASSIGN && mp.nbr && !no_bwin && (long long)M >= 2ll * c->B) {
-            TRY(c->mv_win.ensure(sizeof(int2) * (size_t)c->B));
+        if (mp.nbr && !no_bwin && (long long)M >= 2ll * c->B) {
+            TRY(c->mv_win.ensure(3 * sizeof(int2) * (size_t)c->B));
             const int bgrid = std::max(1, std::min((c->B + 255) / 256, 8 * sms));
             TRY(launch_eval_n(k_block_windows, bgrid, 256, 0, st, pdl, mp, c->mv_win.as<int2>()));
             mp.bwin = c->mv_win.as<int2>();

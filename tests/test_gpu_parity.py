@@ -218,6 +218,20 @@ def test_explicit_moves_against_oracle(oracle_lib):
     ref = o.eval_moves(assign, b, b2, "swap", None, net=True, stats=True, scen=True)
     _same_res(got, ref, keys)
     assert got["feasible"].sum() > 0
+    # swaps between neighbours (the partner seen at the other's period): every block with each of
+    # its neighbours, through the per-block windows (M >= 2 B) and the per-move ones (M < 2 B)
+    pp_, pi_, sp_, si_ = bm.csr()
+    pa, pb = [], []
+    for x in range(bm.n_blocks):
+        for y in list(pi_[pp_[x]:pp_[x + 1]]) + list(si_[sp_[x]:sp_[x + 1]]):
+            pa.append(x)
+            pb.append(int(y))
+    pa, pb = np.asarray(pa, np.int32), np.asarray(pb, np.int32)
+    assert pa.size >= 2 * bm.n_blocks
+    for lo_, hi_ in ((0, pa.size), (0, 400)):
+        got = eng.eval_moves(pa[lo_:hi_].copy(), pb[lo_:hi_].copy(), "swap", None, net=True, stats=True)
+        ref = o.eval_moves(assign, pa[lo_:hi_].copy(), pb[lo_:hi_].copy(), "swap", None, net=True, stats=True)
+        _same_res(got, ref, ("feasible", "delta", "exp_delta", "cvar"))
     eng.close()
 
 
