@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
     int nb[CPW];
     // the rows per candidate (one round each) or as one flat list over the lanes (two rounds at C2
     // instead of four); measured per instantiation: flat is faster at C2 (KC 2: step 19.45 ->
-    // 19.2 us) and C3 (KC < 0), slower at C4 (KC 8, S = 50: kernel 59.4 -> 63.5 us, more spills)
-    constexpr bool FLAT_ROWS = KC != 8;
+    // 19.2 us) and C3 (KC < 0), slower at C4 (KC 8 then, S = 50: kernel 59.4 -> 63.5 us, more spills)
+    constexpr bool FLAT_ROWS = KC == 2 || KC < 0;
 #pragma unroll
     for (int j = 0; j < CPW; j++) nb[j] = b[j] >= 0 ? __ldg(p.nbr + (size_t)b[j] * NBR_W + lane) : -1;
     if constexpr (!FLAT_ROWS) {
@@ -902,7 +902,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 
     // fast path: one warp per CPW candidates (k_eval_warp)
     if (warp_path) {
-        const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 8 ? 8 : -1;  // -1: warp per move
+        // the k-smallest list sized to k (each push compares and moves every slot); -1: warp per move
+        const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 4 ? 4 : c->cvar_k <= 6 ? 6 : c->cvar_k <= 8 ? 8 : -1;
         const bool need_vrow = (stats && kcw > 0) || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
                                           kcw < 0 ? big_pow2(S) : 0);
@@ -928,6 +929,8 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     }
         if (kcw == 0) PP_WARP(0, false)
         else if (kcw == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }
+        else if (kcw == 4) { if (scen) PP_WARP(4, true) else PP_WARP(4, false) }
+        else if (kcw == 6) { if (scen) PP_WARP(6, true) else PP_WARP(6, false) }
         else if (kcw == 8) { if (scen) PP_WARP(8, true) else PP_WARP(8, false) }
         else { if (scen) PP_WARP(-1, true) else PP_WARP(-1, false) }
 #undef PP_WARP
