@@ -903,7 +903,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     // fast path: one warp per CPW candidates (k_eval_warp)
     if (warp_path) {
         // the k-smallest list sized to k (each push compares and moves every slot); -1: warp per move
-        const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 4 ? 4 : c->cvar_k <= 6 ? 6 : c->cvar_k <= 8 ? 8 : -1;
+        const int kcw = !stats ? 0 : c->cvar_k <= 2 ? 2 : c->cvar_k <= 8 ? c->cvar_k : -1;
         const bool need_vrow = (stats && kcw > 0) || (!(flags & PP_LITERAL_VALUE) && scenario >= 0);
         const WarpLayout Lw = warp_layout(T, c->Sp, stats, need_vrow, (flags & PP_NET_MINING_COST) != 0,
                                           kcw < 0 ? big_pow2(S) : 0);
@@ -929,8 +929,11 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     }
         if (kcw == 0) PP_WARP(0, false)
         else if (kcw == 2) { if (scen) PP_WARP(2, true) else PP_WARP(2, false) }
+        else if (kcw == 3) { if (scen) PP_WARP(3, true) else PP_WARP(3, false) }
         else if (kcw == 4) { if (scen) PP_WARP(4, true) else PP_WARP(4, false) }
+        else if (kcw == 5) { if (scen) PP_WARP(5, true) else PP_WARP(5, false) }
         else if (kcw == 6) { if (scen) PP_WARP(6, true) else PP_WARP(6, false) }
+        else if (kcw == 7) { if (scen) PP_WARP(7, true) else PP_WARP(7, false) }
         else if (kcw == 8) { if (scen) PP_WARP(8, true) else PP_WARP(8, false) }
         else { if (scen) PP_WARP(-1, true) else PP_WARP(-1, false) }
 #undef PP_WARP

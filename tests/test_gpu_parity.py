@@ -148,8 +148,8 @@ def _rand_instance(seed, n=(6, 5, 4), T=7, S=9, cf=0.5):
     return bm, scenario_values(bm, grades), sigma
 
 
-@pytest.mark.parametrize("T,S", [(1, 1), (3, 7), (7, 9), (9, 20), (12, 35), (20, 55), (16, 64), (17, 129),
-                                 (32, 200), (33, 40), (40, 300), (5, 1000)])
+@pytest.mark.parametrize("T,S", [(1, 1), (3, 7), (7, 9), (9, 20), (8, 25), (12, 35), (10, 45), (20, 55), (16, 64),
+                                 (17, 129), (32, 200), (33, 40), (40, 300), (5, 1000)])
 def test_shapes_against_oracle(oracle_lib, T, S):
     """Group widths 4..32, the multi-slot path (T > 32), single- and multi-leaf pairwise
     plans (S up to 1000), CVaR sample counts 1..100."""
