@@ -170,15 +170,17 @@ __device__ __forceinline__ int warp_relation(const MoveParams &p, int bw, int su
 // block b's window (k_block_windows) with neighbour o (relation rel: 1 pred, 2 succ) seen at period
 // to, in warp_windows' convention (lo -2 when a predecessor is unmined, hi INT_MAX when none)
 __device__ __forceinline__ void window_with(const int2 *win, int b, int o, int rel, int to, int &lo, int &hi) {
-    const int2 w0 = __ldcg(win + 3 * (size_t)b), w1 = __ldcg(win + 3 * (size_t)b + 1),
-               w2 = __ldcg(win + 3 * (size_t)b + 2);
+    const int2 w0 = __ldcg(win + 3 * (size_t)b);
     int l = w0.x, h = w0.y;
-    if (rel == 1) {
-        const int lw = o == w1.x ? w2.x : w0.x;
-        l = lw == BW_NONE ? BW_NONE : max(lw, to);
-    } else if (rel == 2) {
-        const int hw = o == w1.y ? w2.y : w0.y;
-        h = min(hw, to);
+    if (rel != 0) {  // (only then the attaining neighbours and the runners-up)
+        const int2 w1 = __ldcg(win + 3 * (size_t)b + 1), w2 = __ldcg(win + 3 * (size_t)b + 2);
+        if (rel == 1) {
+            const int lw = o == w1.x ? w2.x : w0.x;
+            l = lw == BW_NONE ? BW_NONE : max(lw, to);
+        } else {
+            const int hw = o == w1.y ? w2.y : w0.y;
+            h = min(hw, to);
+        }
     }
     lo = l == BW_NONE ? -2 : l;
     hi = h;  // BW_NONE == INT_MAX
