@@ -11,8 +11,8 @@ python bench.py > gpurun_out/r02_bench_c2.json 2> gpurun_out/bench_c2.err; tail 
 python bench.py --impl reference > gpurun_out/r02_bench_reference_c2.json 2> gpurun_out/bench_ref.err
 python bench.py --config C3 --steps 200 --warmup 10 --no-python-ref > gpurun_out/r02_bench_c3.json 2> gpurun_out/bench_c3.err
 python bench.py --config C4 --steps 200 --warmup 10 --no-python-ref > gpurun_out/r02_bench_c4.json 2> gpurun_out/bench_c4.err
-python bench.py --workload reassign --steps 100 --warmup 5 > gpurun_out/r02_bench_moves_reassign.json 2> gpurun_out/bench_mr.err
-python bench.py --workload swap --steps 100 --warmup 5 > gpurun_out/r02_bench_moves_swap.json 2> gpurun_out/bench_ms.err
+python bench.py --workload reassign --steps 5000 --warmup 10 > gpurun_out/r02_bench_moves_reassign.json 2> gpurun_out/bench_mr.err
+python bench.py --workload swap --steps 5000 --warmup 10 > gpurun_out/r02_bench_moves_swap.json 2> gpurun_out/bench_ms.err
 for C in C2 C3 C4; do
   ncu --set full --clock-control none --import-source on -k regex:k_eval_warp -s 5 -c 1 -f -o gpurun_out/r02_eval_$C python bench.py --config $C --steps 20 --warmup 5 --no-cpu-baseline --no-python-ref > /dev/null 2>&1
   ncu --set full --clock-control none -k regex:"k_pm_cluster|k_period_mass" -s 5 -c 1 -f -o gpurun_out/r02_pm_$C python bench.py --config $C --steps 20 --warmup 5 --no-cpu-baseline --no-python-ref > /dev/null 2>&1
