@@ -271,7 +271,7 @@ class Engine:
         C, T, S = c.size, bm.n_periods, self.n_scenarios
         key = None
         if out:
-            key = (C, trace, stats, scen, pairs, realism) + tuple(id(v) for v in out.values())
+            key = (C, trace, stats, scen, pairs, realism) + tuple(map(id, out.values()))
             hit = self._eval_cache
             if hit is not None and hit[0] == key:
                 _, _keep, res, pr, g, argblock = hit
