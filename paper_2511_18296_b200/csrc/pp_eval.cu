@@ -208,8 +208,19 @@ __global__ void __launch_bounds__(WV_THREADS, KC < 0 ? 4 : WV_MINB) k_eval_warp(
 
     // ---- loads: ids, then every row of the warp's candidates in one round trip ----
     int bl = -1;
-    if (lane < CPW && cw + lane < p.C) {
+    if (p.cand_host) {  // ids in page-locked host memory (no copy-in): one 128-byte PCIe read per CTA
+        __shared__ int s_cid[NW * CPW];
+        static_assert(NW * CPW == 32, "one lane per candidate of the CTA");
+        if (warp == 0) {
+            const int g = blockIdx.x * NW * CPW + lane;
+            s_cid[lane] = g < p.C ? p.cand[g] : -1;
+        }
+        __syncthreads();
+        if (lane < CPW && cw + lane < p.C) bl = s_cid[warp * CPW + lane];
+    } else if (lane < CPW && cw + lane < p.C) {
         bl = __ldg(p.cand + cw + lane);
+    }
+    if (lane < CPW && cw + lane < p.C) {
         if (bl < 0 || bl >= p.B) {
             if (p.bad_cand) *p.bad_cand = 1;  // reported by the host-mode call
             bl = -1;
@@ -812,6 +823,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
 
     pp_cand_out o = *out;
     const int32_t *dcand = cand;
+    bool cand_host = false;  // dcand: the device mapping of page-locked host ids (k_eval_warp only)
     const bool warp_path = T <= 32 && (!stats || S <= 256) && c->nbr.ptr;
     if (mem == PP_MEM_HOST) {
         if (!warp_path) {  // the warp kernel range-checks the ids itself (reported after the sync)
@@ -850,8 +862,17 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
             o.pair_period = reinterpret_cast<int32_t *>(q + 2 * sizeof(double) * CT + sizeof(int32_t) * CT);
             o.n_pairs = reinterpret_cast<int32_t *>(q + (2 * sizeof(double) + 2 * sizeof(int32_t)) * CT);
         }
-        if (C > 0) CUDA_TRY(cudaMemcpyAsync(c->h_cand.ptr, cand, sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
-        dcand = c->h_cand.as<int32_t>();
+        // page-locked ids on the warp path: read in place by k_eval_warp (one PCIe read per CTA)
+        // instead of a DMA copy-in ahead of the kernels
+        static const bool no_zc = std::getenv("PP_NO_ZEROCOPY_CAND") != nullptr;  // diagnostics
+        const void *mc = (C > 0 && warp_path && !out->realism && !no_zc) ? mapped_host(cand) : nullptr;
+        if (mc) {
+            dcand = static_cast<const int32_t *>(mc);
+            cand_host = true;
+        } else {
+            if (C > 0) CUDA_TRY(cudaMemcpyAsync(c->h_cand.ptr, cand, sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
+            dcand = c->h_cand.as<int32_t>();
+        }
         ht.mark("h2d");
     }
 
@@ -874,6 +895,7 @@ int pp_eval_candidates(pp_ctx *c, const int32_t *cand, int32_t C, int32_t scenar
     ep.sigma = (flags & PP_USE_SIGMA) ? c->sigma.as<double>() : c->ones_st.as<double>();
     ep.sigma_ts = (flags & PP_USE_SIGMA) ? c->sigma_ts.as<double>() : c->ones_st.as<double>();
     ep.cand = dcand;
+    ep.cand_host = cand_host ? 1 : 0;
     ep.C = C;
     ep.B = c->B;
     ep.T = T;

@@ -530,6 +530,7 @@ struct EvalParams {
     const double *sigma_ts;  // [T][S]: sigma transposed (scenario-contiguous rows for lane = scenario)
     int wl[7];               // k_eval_warp: the per-warp shared-memory layout (host-computed)
     const int32_t *cand;
+    int cand_host;           // cand is page-locked host memory (read once per CTA, k_eval_warp)
     int C, B, T, S, Sp, scen, cvar_k;
     unsigned flags;
     const int *plan;

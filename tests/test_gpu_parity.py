@@ -730,11 +730,14 @@ def test_pinned_copy_out_matches_pageable(name):
            "cvar": pool.empty((C, T), np.float64), "pair_cand": pool.empty(C * T, np.int32),
            "pair_period": pool.empty(C * T, np.int32), "pair_exp": pool.empty(C * T, np.float64),
            "pair_cvar": pool.empty(C * T, np.float64), "n_pairs": pool.empty(1, np.int32)}
+    hc = pool.empty(C, np.int32)  # page-locked ids: read in place by k_eval_warp (no copy-in)
+    hc[:] = c["cand"]
     try:
         for rep in range(3):
             for v in out.values():
                 v.view(np.uint8)[...] = 0xA5  # stale bytes must be overwritten
-            got = eng.eval_candidates(c["cand"], None, net=True, trace=True, stats=True, pairs=True, out=out)
+            got = eng.eval_candidates(hc if rep else c["cand"], None, net=True, trace=True, stats=True, pairs=True,
+                                      out=out)
             _same_res(got, ref, ("best_t", "best_val", "feasible", "trace_val", "trace_feas", "exp_delta", "cvar"))
             assert got["best"] == ref["best"], rep
             n = ref["pairs"]["cand"].size
@@ -743,6 +746,11 @@ def test_pinned_copy_out_matches_pageable(name):
             kb = np.lexsort((got["pairs"]["period"], got["pairs"]["cand"]))
             for k in ("cand", "period", "exp", "cvar"):
                 assert same(got["pairs"][k][kb], ref["pairs"][k][ka]), (rep, k)
+        hc[C // 2] = c["bm"].n_blocks  # an out-of-range id in the page-locked list is still reported
+        with pytest.raises(Exception, match="out of range"):
+            eng.eval_candidates(hc, None, net=True, pairs=True, out=out)
+        hc[C // 2] = c["cand"][C // 2]
+        assert eng.eval_candidates(hc, None, net=True, trace=True, stats=True, pairs=True, out=out)["best"] == ref["best"]
     finally:
         eng.close()
         pool.close()
