@@ -716,15 +716,22 @@ def run_moves(args):
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     t_ms = float(np.mean([x.elapsed_time(y) for x, y in ev]))
-    # e2e: host arrays through the C ABI (upload schedule + moves, kernels, download of all outputs)
+    # e2e: page-locked host arrays through the C ABI (upload schedule + moves, kernels, download
+    # of all outputs into page-locked arrays)
+    from paper_2511_18296_b200.engine import PinnedPool
+    pool = PinnedPool()
+    ha, hb, hs = pool.empty(M, np.int32), pool.empty(M, np.int32), pool.empty(bm.n_blocks, np.int32)
+    ha[:], hb[:], hs[:] = a, b, c["assign"]
+    hout = {"feasible": pool.empty(M, np.uint8), "delta": pool.empty(M, np.float64),
+            "exp_delta": pool.empty(M, np.float64), "cvar": pool.empty(M, np.float64)}
     e2e = []
     res = None
     for i in range(args.warmup + min(args.steps, 100)):
         flush.fill_(i)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        eng.set_schedule(c["assign"])
-        res = eng.eval_moves(a, b, args.workload, None, net=True, stats=True)
+        eng.set_schedule(hs)
+        res = eng.eval_moves(ha, hb, args.workload, None, net=True, stats=True, out=hout)
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
     e2e_t = float(np.median(e2e))
@@ -761,10 +768,12 @@ def run_moves(args):
         "e2e": {"value": M * S / e2e_t, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
                 "h2d_bytes_per_step": int(c["assign"].size * 4 + 8 * M),
                 "d2h_bytes_per_step": int(M * (1 + 8 + 8 + 8) + 16),
-                "api": "Engine.set_schedule + Engine.eval_moves (PP_MEM_HOST)"},
-        "gpu_launches": 2 * args.steps, "clocks": clocks.summary(), "cpu_baseline": ref,
-        "best_move": res["best"]}))
+                "api": "Engine.set_schedule + Engine.eval_moves (PP_MEM_HOST, pinned)"},
+        # period masses + (k_block_windows when the batch holds >= 2 moves per block) + k_moves_warp
+        "gpu_launches": (3 if M >= 2 * bm.n_blocks else 2) * args.steps, "clocks": clocks.summary(),
+        "cpu_baseline": ref, "best_move": res["best"]}))
     eng.close()
+    pool.close()
     return 0
 
 

@@ -348,18 +348,30 @@ class Engine:
                                           _lib.PP_MEM_DEVICE, stream))
 
     def eval_moves(self, a, b, kind="reassign", scenario=None, *, net=False, literal=False,
-                   use_sigma=True, stats=False, scen=False) -> dict:
+                   use_sigma=True, stats=False, scen=False, out: dict | None = None) -> dict:
+        """Host-buffer evaluation of explicit moves; `out` may supply preallocated (e.g. pinned,
+        PinnedPool) output arrays, written in place."""
         bm = self._need_bm()
         av = _i32(a)
         bv = _i32(b, av.size, "move arrays")
         M, S = av.size, self.n_scenarios
         k = _lib.PP_MOVE_SWAP if kind == "swap" else _lib.PP_MOVE_REASSIGN
-        res = {"feasible": np.empty(M, np.uint8), "delta": np.empty(M, np.float64)}
+        out = out or {}
+
+        def buf(name, shape, dt):
+            v = out.get(name)
+            if v is None:
+                return np.empty(shape, dt)
+            if v.dtype != np.dtype(dt) or v.size != int(np.prod(shape)) or not v.flags.c_contiguous:
+                raise ShapeMismatch(f"out[{name!r}] must be a contiguous {np.dtype(dt)} array of {shape}")
+            return v
+
+        res = {"feasible": buf("feasible", M, np.uint8), "delta": buf("delta", M, np.float64)}
         if stats:
-            res["exp_delta"] = np.empty(M, np.float64)
-            res["cvar"] = np.empty(M, np.float64)
+            res["exp_delta"] = buf("exp_delta", M, np.float64)
+            res["cvar"] = buf("cvar", M, np.float64)
         if scen:
-            res["scen_delta"] = np.empty((M, S), np.float32)
+            res["scen_delta"] = buf("scen_delta", (M, S), np.float32)
         g = PPBest()
         out = PPMoveOut(ptr(res["feasible"]), ptr(res["delta"]), ptr(res.get("exp_delta")),
                         ptr(res.get("cvar")), ptr(res.get("scen_delta")), ctypes.addressof(g))
