@@ -756,6 +756,39 @@ def test_pinned_copy_out_matches_pageable(name):
         pool.close()
 
 
+def test_eval_moves_into_pinned_outputs(oracle_lib):
+    """Engine.eval_moves(out=...): page-locked move arrays and outputs, written in place, equal the
+    oracle; a wrong-typed output array is rejected."""
+    from paper_2511_18296_b200.engine import PinnedPool
+    from paper_2511_18296_b200.errors import ShapeMismatch
+    bm, vmax, sigma = _rand_instance(9, n=(12, 10, 6), T=9, S=20, cf=0.45)
+    from paper_2511_18296_b200 import synth
+
+    rng = np.random.default_rng(5)
+    assign = synth.full_greedy(bm)
+    eng = Engine.from_tables(bm, ScenarioTables(vmax, sigma), assign)
+    o = oracle_lib.Oracle(bm, vmax, sigma)
+    pool = PinnedPool()
+    try:
+        M = 4000
+        for kind in ("reassign", "swap"):
+            a = pool.empty(M, np.int32)
+            b = pool.empty(M, np.int32)
+            a[:] = rng.integers(0, bm.n_blocks, M)
+            b[:] = rng.integers(-1, bm.n_periods, M) if kind == "reassign" else rng.integers(0, bm.n_blocks, M)
+            out = {"feasible": pool.empty(M, np.uint8), "delta": pool.empty(M, np.float64),
+                   "exp_delta": pool.empty(M, np.float64), "cvar": pool.empty(M, np.float64)}
+            got = eng.eval_moves(a, b, kind, None, net=True, stats=True, out=out)
+            assert got["delta"] is out["delta"]
+            ref = o.eval_moves(assign, np.array(a), np.array(b), kind, None, net=True, stats=True)
+            _same_res(got, ref, ("feasible", "delta", "exp_delta", "cvar"))
+        with pytest.raises(ShapeMismatch):
+            eng.eval_moves(a, b, "swap", None, net=True, stats=True, out={"delta": np.empty(M, np.float32)})
+    finally:
+        eng.close()
+        pool.close()
+
+
 def _big_period_population(c):
     """Schedules whose periods hold far more than the 6,144 blocks of k_stage2's on-chip buffers:
     the C2 schedule folded into 4 periods (~12.5k blocks each), everything in one period (n = B),
