@@ -13,6 +13,7 @@
 // matches the reference's numpy/Python scalar evaluation bit for bit.
 
 #include "pp_internal.cuh"
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -40,15 +41,20 @@ struct PinnedRange {
 };
 std::mutex g_pinned_mu;
 std::vector<PinnedRange> g_pinned;
+std::atomic<uint64_t> g_pinned_gen{0};  // bumped on every (un)registration: cached mappings compare it
 }  // namespace
 
+uint64_t pinned_generation() { return g_pinned_gen.load(std::memory_order_relaxed); }
+
 void pinned_register(void *host, size_t bytes, void *dev) {
+    g_pinned_gen.fetch_add(1, std::memory_order_relaxed);
     std::lock_guard<std::mutex> lock(g_pinned_mu);
     g_pinned.push_back({reinterpret_cast<uintptr_t>(host), reinterpret_cast<uintptr_t>(host) + bytes,
                         reinterpret_cast<uintptr_t>(dev)});
 }
 
 void pinned_unregister(void *host) {
+    g_pinned_gen.fetch_add(1, std::memory_order_relaxed);
     std::lock_guard<std::mutex> lock(g_pinned_mu);
     const uintptr_t h = reinterpret_cast<uintptr_t>(host);
     for (size_t i = 0; i < g_pinned.size(); i++)
@@ -257,6 +263,8 @@ int pp_ctx_destroy(pp_ctx *c) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->lns_exec) cudaGraphExecDestroy(c->lns_exec);
     if (c->lns_graph) cudaGraphDestroy(c->lns_graph);
+    if (c->ev_exec) cudaGraphExecDestroy(c->ev_exec);
+    if (c->ev_graph) cudaGraphDestroy(c->ev_graph);
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);

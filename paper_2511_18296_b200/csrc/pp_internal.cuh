@@ -837,6 +837,27 @@ struct pp_ctx {
     // VAE decoder (pp_vae.cu): layer widths, packed W/b per layer, norm_mean | norm_std, scratch
     std::vector<int32_t> vae_widths;
     DevBuf vae_params, vae_norm, vae_h, vae_io;
+    // host-mode pp_eval_candidates repeated with identical arguments (page-locked ids and outputs):
+    // its launches (period masses or output init, evaluation, copy-out) replayed as one graph
+    struct EvalGraphKey {
+        const void *cand;
+        int32_t C, scenario;
+        uint32_t flags;
+        int32_t pm_dirty, bad_pending, cvar_k, S, T, B, Sp;
+        pp_cand_out out;
+        const void *assign_ptr;
+        uint64_t gensum, pinned_gen;
+    };
+    struct EvalBounce {
+        void *user;  // nullptr: the call's own bad-candidate flag
+        size_t off, bytes;
+    };
+    EvalGraphKey ev_key{}, ev_seen{};
+    bool ev_have_seen = false, ev_bad_copy = false;
+    cudaGraph_t ev_graph = nullptr;
+    cudaGraphExec_t ev_exec = nullptr;
+    EvalBounce ev_bounce[4]{};
+    int ev_nb = 0;
     cudaGraph_t lns_graph = nullptr;      // the cached insertion-loop graph (pp_lns_insert)
     cudaGraphExec_t lns_exec = nullptr;
     uint64_t lns_key[3] = {0, 0, 0};      // width, flags, sum of the buffers' allocation generations
@@ -985,6 +1006,7 @@ inline int launch_eval_n(void (*kern)(KArgs...), dim3 grid, int threads, size_t 
 void pinned_register(void *host, size_t bytes, void *dev);
 void pinned_unregister(void *host);
 void *pinned_lookup(const void *host);
+uint64_t pinned_generation();  // changes whenever a pp_host_alloc buffer is registered or freed
 int ensure_grid_scratch(pp_ctx *c, int grid);
 int check_ready(pp_ctx *c, uint32_t flags, int scenario);
 int pick_kc(int k);
