@@ -756,6 +756,49 @@ def test_pinned_copy_out_matches_pageable(name):
         pool.close()
 
 
+def test_repeated_host_calls_replay_graph_with_fresh_inputs():
+    """A host-mode call repeated with the same page-locked arrays replays one cached graph: the
+    schedule and the ids are re-read on every replay (two schedules alternating in one page-locked
+    buffer, the ids changed in place), and freeing / re-allocating page-locked buffers invalidates
+    the cached device mappings (the registry generation is part of the key)."""
+    from paper_2511_18296_b200.engine import PinnedPool
+    c = config("C1")
+    bm = c["bm"]
+    eng = Engine.from_tables(bm, ScenarioTables(c["vmax"], c["sigma"]), c["assign"])
+    C, T = c["cand"].size, c["T"]
+    a0 = c["assign"].astype(np.int32)
+    a1 = a0.copy()
+    a1[(a1 >= 0) & (np.arange(a1.size) % 7 == 0)] = -1  # some blocks unmined: other windows, masses
+    rng = np.random.default_rng(11)
+    ids = [c["cand"].copy(), rng.permutation(c["cand"]).astype(np.int32)]
+    refs = {}
+    for ia, a in enumerate((a0, a1)):
+        for ic, cd in enumerate(ids):
+            eng.set_schedule(a)
+            refs[ia, ic] = eng.eval_candidates(cd, None, net=True, stats=True, pairs=True)
+    for round_ in range(2):
+        pool = PinnedPool()
+        hs = pool.empty(bm.n_blocks, np.int32)
+        hc = pool.empty(C, np.int32)
+        out = {"best_t": pool.empty(C, np.int32), "best_val": pool.empty(C, np.float64),
+               "feasible": pool.empty(C, np.uint8), "exp_delta": pool.empty((C, T), np.float64),
+               "cvar": pool.empty((C, T), np.float64), "pair_cand": pool.empty(C * T, np.int32),
+               "pair_period": pool.empty(C * T, np.int32), "pair_exp": pool.empty(C * T, np.float64),
+               "pair_cvar": pool.empty(C * T, np.float64), "n_pairs": pool.empty(1, np.int32)}
+        for step in range(8):
+            ia, ic = step % 2, (step // 2) % 2
+            hs[:] = (a0, a1)[ia]
+            hc[:] = ids[ic]
+            eng.set_schedule(hs)
+            got = eng.eval_candidates(hc, None, net=True, stats=True, pairs=True, out=out)
+            ref = refs[ia, ic]
+            _same_res(got, ref, ("best_t", "best_val", "feasible", "exp_delta", "cvar"))
+            n = ref["pairs"]["cand"].size
+            assert got["pairs"]["cand"].size == n, (round_, step)
+        pool.close()  # the next round's buffers may reuse these addresses
+    eng.close()
+
+
 def test_eval_moves_into_pinned_outputs(oracle_lib):
     """Engine.eval_moves(out=...): page-locked move arrays and outputs, written in place, equal the
     oracle; a wrong-typed output array is rejected."""
