@@ -99,6 +99,9 @@ class Engine:
             ptr(np.ascontiguousarray(bm.cost)), ptr(bm.capacity), ptr(disc)))
         self.bm = bm
         self.n_scenarios = 0
+        # a new instance (possibly another block count): forget the cached host arrays
+        self._sched_obj = self._sched_ptr = self._cand_obj = self._cand_ptr = None
+        self._eval_cache = None
 
     def set_geology(self, psi_weights=DEFAULT_PSI_WEIGHTS, diameter: float | None = None):
         bm = self._need_bm()
@@ -200,12 +203,12 @@ class Engine:
     # -- schedule --------------------------------------------------------------------
     def set_schedule(self, assign):
         """Host numpy array or a device int32 torch tensor."""
+        if assign is not None and assign is self._sched_obj:  # the array of the previous call
+            check(self.lib.pp_set_schedule(self._h, self._sched_ptr, _lib.PP_MEM_HOST, None))
+            return
         bm = self._need_bm()
         if hasattr(assign, "data_ptr"):
             check(self.lib.pp_set_schedule(self._h, assign.data_ptr(), _lib.PP_MEM_DEVICE, None))
-            return
-        if assign is self._sched_obj:
-            check(self.lib.pp_set_schedule(self._h, self._sched_ptr, _lib.PP_MEM_HOST, None))
             return
         a = _i32(assign, bm.n_blocks, "assignment")  # range validated by pp_set_schedule
         p = ptr(a)
